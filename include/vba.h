@@ -1,0 +1,172 @@
+/*
+ * vba.h — C ABI of the B200-native dense visual-inertial bundle adjustment.
+ *
+ * Drop-in boundary for the reference's VI-BA path
+ * (/root/reference/pkg/src/vislam/solver.py).  The reference has no native
+ * FFI — it is pure Python/numpy — so each entry point below replaces one
+ * reference *function*; a maintainer binds them with ctypes.
+ *
+ *   vba_solve            <- solve_vi_ba        solver.py:344-411
+ *   vba_energy           <- total_energy       solver.py:118-131
+ *   vba_linearize        <- _linearize         solver.py:173-251
+ *   vba_export_normal_eq <- (_linearize's dense outputs H_pp,H_pd,H_dd,g_p,g_d)
+ *   vba_solve_step       <- _solve_step        solver.py:254-308
+ *   vba_apply_step       <- _snapshot + _apply_step  solver.py:311-341
+ *   vba_restore          <- _restore           solver.py:318-323
+ *   vba_trial            <- one LM trial (solve, apply, energy) solver.py:370-383
+ *   vba_accept           <- accepted step bookkeeping       solver.py:383-393
+ *
+ * Conventions: plain pointers and sizes only; every pointer in vba_problem is
+ * a DEVICE pointer owned by the caller except the h_* topology arrays, which
+ * are host pointers read only inside vba_create.  All calls are
+ * stream-ordered on the caller's cudaStream_t (passed as void*); the calls
+ * that return host scalars synchronise that stream.  No C++ exception
+ * crosses the ABI; errors are integer status codes (vba_last_error() gives
+ * the message).  A context is bound to one device and is not thread-safe.
+ */
+#ifndef VBA_H
+#define VBA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define VBA_API __attribute__((visibility("default")))
+#else
+#define VBA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define VBA_OK 0
+#define VBA_E_INVALID 1  /* invalid problem/options -> reference raises ValueError */
+#define VBA_E_CUDA 2     /* CUDA runtime failure */
+#define VBA_E_NOT_SPD 3  /* reduced system not positive definite -> reference's
+                            RuntimeError("singular reduced pose system"), solver.py:287-289 */
+#define VBA_E_COV 4      /* preintegration covariance not PD -> ValueError, residuals.py:337-341 */
+#define VBA_E_UNSUPPORTED 5
+
+#define VBA_PIX_GRID 0   /* pixel n of a keyframe = (ox + sx*(n % w), oy + sy*(n / w)) */
+#define VBA_PIX_KF 1     /* explicit per-keyframe coordinates (padded keyframe layout) */
+#define VBA_PIX_EDGE 2   /* explicit per-edge coordinates (padded edge-row layout) */
+
+/* Packed IMU factor record (fp64), one per preintegrated delta:
+ *  [0] dt  [1..4] dR quat wxyz  [5..7] dp  [8..10] dv  [11..19] J_rot 3x3 row-major
+ *  [20..37] J_pos 3x6  [38..55] J_vel 3x6  [56..136] cov[0:9,0:9]  [137..172] cov[9:15,9:15]
+ *  [173..178] bias linearisation point (gyro, accel)                                  */
+#define VBA_IMU_REC 180
+
+typedef struct vba_problem {
+  /* sizes */
+  int32_t n_kf;          /* K */
+  int32_t n_edges;       /* E (vision edges on this rank) */
+  int32_t n_imu;         /* F (inertial factors on this rank) */
+  int32_t pixel_mode;    /* VBA_PIX_* */
+  int64_t n_disp_pad;    /* disparity slots, per-keyframe segments padded to 4 */
+  int64_t n_rows_pad;    /* edge rows, per-edge segments padded to 4 */
+  int32_t grid_w;        /* VBA_PIX_GRID: columns */
+  int32_t has_Tcb;
+  double grid_ox, grid_oy, grid_sx, grid_sy;
+  double fx, fy, cx, cy;
+  double Tcb[7];         /* camera-from-body extrinsic T_cb: quat wxyz, translation */
+  /* device arrays (caller-owned) */
+  double* state;         /* [K,16]: q wxyz, p, v, b_g, b_a — read at create, updated by solve */
+  const double* ts;      /* [K] timestamps */
+  float* disp;           /* [n_disp_pad] disparities — read at create, updated by solve */
+  const float* pix;      /* [n_disp_pad,2] (VBA_PIX_KF) or [n_rows_pad,2] (VBA_PIX_EDGE) or NULL */
+  const float* tgt;      /* [n_rows_pad,2] flow targets relative to the source pixel: u* - u
+                            (the reference's VisionEdge.targets minus VisionEdge.pixels) */
+  const float* wts;      /* [n_rows_pad,2] confidence weights (>= 0) */
+  const double* imu;     /* [F, VBA_IMU_REC] */
+  double* grav;          /* [5]: R_wg quat wxyz, magnitude */
+  /* host topology (read in vba_create only) */
+  const int64_t* h_doff;   /* [K+1] padded disparity offsets */
+  const int32_t* h_npix;   /* [K]   real pixel count per keyframe */
+  const int32_t* h_edge_i; /* [E]   source keyframe index (edges sorted by source) */
+  const int32_t* h_edge_j; /* [E]   target keyframe index */
+  const int64_t* h_eoff;   /* [E]   padded row offset of each edge */
+  const int32_t* h_imu_i;  /* [F] */
+  const int32_t* h_imu_j;  /* [F] */
+  const int32_t* h_frozen; /* [K] 1 = frozen (gauge) keyframe */
+} vba_problem;
+
+typedef struct vba_options {       /* SolveOptions, solver.py:82-105 */
+  int32_t max_iterations;
+  double damping, damping_up, damping_down;
+  double rel_decrease_tol, step_tol, max_damping;
+  int32_t optimize_gravity;
+  int32_t optimize_velocity_bias;
+  int32_t use_schur;
+  double ridge;
+} vba_options;
+
+typedef struct vba_report {        /* SolveReport, solver.py:108-115 */
+  int32_t iterations;
+  int32_t termination;             /* 0 max_iterations, 1 converged,
+                                      2 no_decrease_at_max_damping, 3 singular */
+  int32_t n_costs;                 /* entries written to cost_trajectory */
+  int32_t n_warnings;              /* singular-system retries */
+  int32_t trials;                  /* LM trials run */
+  double initial_cost, final_cost;
+} vba_report;
+
+typedef struct vba_trial_result {
+  int32_t status;                  /* VBA_OK or VBA_E_NOT_SPD */
+  double new_cost;
+  double step_inf;                 /* max(|dx_full|, |dx_d|) */
+} vba_trial_result;
+
+/* Collective hook for edge-sharded multi-GPU solves: sum (op 0) or max (op 1)
+ * of `count` doubles at device pointer `buf` across ranks, stream-ordered.
+ * Supplied by the host (torch.distributed / NCCL); NULL for one GPU. */
+typedef int (*vba_allreduce_fn)(void* user, double* buf, int64_t count, int32_t op,
+                                void* stream);
+
+VBA_API const char* vba_last_error(void);
+VBA_API int vba_version(void);
+
+VBA_API int vba_create(void** ctx, const vba_problem* prob, const vba_options* opts, void* stream);
+VBA_API int vba_destroy(void* ctx);
+VBA_API int vba_set_collective(void* ctx, vba_allreduce_fn fn, void* user);
+/* free-variable count of the reduced system (solver.py:254-257) */
+VBA_API int64_t vba_reduced_dim(void* ctx);
+
+VBA_API int vba_energy(void* ctx, void* stream, double* out_total, double* out_vision,
+               double* out_inertial);
+VBA_API int vba_linearize(void* ctx, void* stream);
+/* Dense (reference-layout) normal equations of the last linearisation.  All
+ * outputs are device pointers in the reference's column layout
+ * (solver.py:139-170): H_pp [npv,npv] row-major, g_p [npv], H_dd/g_d [n_disp]
+ * in the *unpadded* keyframe order, H_pd [npv, n_disp] row-major (may be NULL). */
+VBA_API int vba_export_normal_eq(void* ctx, void* stream, double* H_pp, double* g_p, double* H_pd,
+                         double* H_dd, double* g_d);
+VBA_API int vba_solve_step(void* ctx, void* stream, double lam, int32_t use_schur);
+/* dx_full [npv] (zeros at frozen states) and dx_d [n_disp] unpadded, device pointers */
+VBA_API int vba_export_step(void* ctx, void* stream, double* dx_full, double* dx_d);
+VBA_API int vba_apply_step(void* ctx, void* stream);
+VBA_API int vba_restore(void* ctx, void* stream);
+VBA_API int vba_accept(void* ctx, void* stream);
+VBA_API int vba_trial(void* ctx, void* stream, double lam, int32_t use_schur, vba_trial_result* out);
+VBA_API int vba_solve(void* ctx, void* stream, vba_report* report, double* cost_trajectory,
+              int32_t traj_capacity);
+/* re-seed the current state from the caller's problem arrays (state, disp, grav) */
+VBA_API int vba_load_state(void* ctx, void* stream);
+/* enable per-stage CUDA-event timing of vba_solve / vba_trial (resets the counters) */
+VBA_API int vba_set_profiling(void* ctx, int32_t on);
+/* copy the current (accepted) state back to the caller's problem arrays */
+VBA_API int vba_download(void* ctx, void* stream);
+/* kernel launches issued by this context since creation (instrumentation) */
+VBA_API int64_t vba_launch_count(void* ctx);
+/* accumulated per-stage device time since vba_set_profiling, ms:
+ * [0] linearise  [1] Schur Gram + fill transform  [2] assembly + Cholesky
+ * [3] back-substitution + retraction  [4] trial energy  [5] vision linearisation
+ * kernel alone  [6] number of samples in [5]   (out must hold 7 doubles) */
+VBA_API int vba_stage_times(void* ctx, double* out5);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VBA_H */

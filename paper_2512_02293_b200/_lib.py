@@ -1,0 +1,119 @@
+"""ctypes binding of the C ABI in include/vba.h (libvba = ``_vba.so``, built in-tree).
+
+There is no fallback: if the shared library is missing, or no CUDA device is
+present, calls fail loudly (``VbaError`` / ``RuntimeError``).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_vba.so")
+
+VBA_OK, VBA_E_INVALID, VBA_E_CUDA, VBA_E_NOT_SPD, VBA_E_COV, VBA_E_UNSUPPORTED = range(6)
+PIX_GRID, PIX_KF, PIX_EDGE = 0, 1, 2
+IMU_REC = 180
+
+EXPORTED = ("vba_last_error", "vba_version", "vba_create", "vba_destroy", "vba_set_collective",
+            "vba_reduced_dim", "vba_energy", "vba_linearize", "vba_export_normal_eq",
+            "vba_solve_step", "vba_export_step", "vba_apply_step", "vba_restore", "vba_accept",
+            "vba_trial", "vba_solve", "vba_download", "vba_launch_count", "vba_stage_times",
+            "vba_load_state", "vba_set_profiling")
+
+
+class VbaProblem(C.Structure):
+    _fields_ = [
+        ("n_kf", C.c_int32), ("n_edges", C.c_int32), ("n_imu", C.c_int32), ("pixel_mode", C.c_int32),
+        ("n_disp_pad", C.c_int64), ("n_rows_pad", C.c_int64),
+        ("grid_w", C.c_int32), ("has_Tcb", C.c_int32),
+        ("grid_ox", C.c_double), ("grid_oy", C.c_double), ("grid_sx", C.c_double), ("grid_sy", C.c_double),
+        ("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+        ("Tcb", C.c_double * 7),
+        ("state", C.c_void_p), ("ts", C.c_void_p), ("disp", C.c_void_p), ("pix", C.c_void_p),
+        ("tgt", C.c_void_p), ("wts", C.c_void_p), ("imu", C.c_void_p), ("grav", C.c_void_p),
+        ("h_doff", C.c_void_p), ("h_npix", C.c_void_p), ("h_edge_i", C.c_void_p), ("h_edge_j", C.c_void_p),
+        ("h_eoff", C.c_void_p), ("h_imu_i", C.c_void_p), ("h_imu_j", C.c_void_p), ("h_frozen", C.c_void_p),
+    ]
+
+
+class VbaOptions(C.Structure):
+    _fields_ = [
+        ("max_iterations", C.c_int32),
+        ("damping", C.c_double), ("damping_up", C.c_double), ("damping_down", C.c_double),
+        ("rel_decrease_tol", C.c_double), ("step_tol", C.c_double), ("max_damping", C.c_double),
+        ("optimize_gravity", C.c_int32), ("optimize_velocity_bias", C.c_int32), ("use_schur", C.c_int32),
+        ("ridge", C.c_double),
+    ]
+
+
+class VbaReport(C.Structure):
+    _fields_ = [
+        ("iterations", C.c_int32), ("termination", C.c_int32), ("n_costs", C.c_int32),
+        ("n_warnings", C.c_int32), ("trials", C.c_int32),
+        ("initial_cost", C.c_double), ("final_cost", C.c_double),
+    ]
+
+
+class VbaTrialResult(C.Structure):
+    _fields_ = [("status", C.c_int32), ("new_cost", C.c_double), ("step_inf", C.c_double)]
+
+
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p)
+
+
+class VbaError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"vba error {code}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def load(path: str | None = None):
+    """Load libvba; raises if it has not been built (no CPU fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = path or LIB_PATH
+    if not os.path.exists(p):
+        raise RuntimeError(f"CUDA extension not built: {p} missing (run __graft_entry__.build())")
+    lib = C.CDLL(p)
+    v = C.c_void_p
+    sig = {
+        "vba_last_error": ([], C.c_char_p),
+        "vba_version": ([], C.c_int),
+        "vba_create": ([C.POINTER(C.c_void_p), C.POINTER(VbaProblem), C.POINTER(VbaOptions), v], C.c_int),
+        "vba_destroy": ([v], C.c_int),
+        "vba_set_collective": ([v, ALLREDUCE_FN, v], C.c_int),
+        "vba_reduced_dim": ([v], C.c_int64),
+        "vba_energy": ([v, v, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)], C.c_int),
+        "vba_linearize": ([v, v], C.c_int),
+        "vba_export_normal_eq": ([v, v, v, v, v, v, v], C.c_int),
+        "vba_solve_step": ([v, v, C.c_double, C.c_int32], C.c_int),
+        "vba_export_step": ([v, v, v, v], C.c_int),
+        "vba_apply_step": ([v, v], C.c_int),
+        "vba_restore": ([v, v], C.c_int),
+        "vba_accept": ([v, v], C.c_int),
+        "vba_trial": ([v, v, C.c_double, C.c_int32, C.POINTER(VbaTrialResult)], C.c_int),
+        "vba_solve": ([v, v, C.POINTER(VbaReport), C.POINTER(C.c_double), C.c_int32], C.c_int),
+        "vba_download": ([v, v], C.c_int),
+        "vba_launch_count": ([v], C.c_int64),
+        "vba_stage_times": ([v, C.POINTER(C.c_double)], C.c_int),
+        "vba_load_state": ([v, v], C.c_int),
+        "vba_set_profiling": ([v, C.c_int32], C.c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def check(rc: int):
+    if rc != VBA_OK:
+        msg = _lib.vba_last_error().decode() if _lib is not None else ""
+        raise VbaError(rc, msg)

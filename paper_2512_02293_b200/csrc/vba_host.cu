@@ -1,0 +1,919 @@
+// vba_host.cu — native runtime of the B200 VI-BA: planner, device workspace,
+// C ABI (include/vba.h) and the Levenberg–Marquardt driver.
+//
+// The driver restates solve_vi_ba (solver.py:344-411 in
+// /root/reference/pkg/src/vislam/) with device-resident, double-buffered
+// state: a trial writes the "next" buffers, acceptance swaps them in, and a
+// rejection simply discards them (the reference's _snapshot/_restore,
+// solver.py:311-323).  Exactly one device->host transfer (energy, step norm,
+// factorisation status) happens per LM trial, mirroring the accept test at
+// solver.py:383.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "vba_internal.cuh"
+
+namespace vba {
+
+static thread_local std::string g_err;
+static void set_err(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+#define VBA_CUDA(call)                                                                  \
+  do {                                                                                  \
+    cudaError_t _e = (call);                                                            \
+    if (_e != cudaSuccess) {                                                            \
+      set_err("%s failed: %s (%s:%d)", #call, cudaGetErrorString(_e), __FILE__, __LINE__); \
+      return VBA_E_CUDA;                                                                \
+    }                                                                                   \
+  } while (0)
+
+constexpr int kTileRt = 1024;   // pixels per per-pixel work tile (kPixBlock * 2 * kTP)
+constexpr int kGramBlock = 512;
+constexpr int kMaxOutDegree = 31;
+constexpr int NBc = 64;
+
+struct Result {       // device -> host once per trial
+  double energy[3];
+  unsigned long long step_bits;
+  int status;
+  int pad;
+};
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+};
+
+struct Ctx {
+  vba_problem P;
+  vba_options O;
+  int K = 0, E = 0, F = 0, sdof = 15, ngrav = 0, npv = 0, n_state = 0;
+  int nfree = 0, npad = 0, nt = 0, nfk = 0;
+  int64_t n_disp = 0, n_rows = 0;
+  Extr extr;
+  double grid[4];
+  double intr[4];
+  // host plan
+  std::vector<PixTile> tiles;
+  std::vector<int32_t> t0s, t1s, seb, see;
+  std::vector<GramTile> gtiles;
+  std::vector<int32_t> gsrc, g0, g1;
+  std::vector<int64_t> goff, foff;
+  int kmax = 0;
+  size_t gram_smem = 0;
+  int64_t n_part = 0, gram_part_len = 0, gram_len = 0, fill_len = 0;
+  int ibs = 0;
+  int64_t arena_vis = 0, arena_imu = 0, arena_fill = 0, arena_len = 0;
+  std::vector<int32_t> kf_col;   // column offset of each keyframe in the reduced system, -1 frozen
+  std::vector<int32_t> fmap;     // npv -> free index or -1
+  // device
+  std::vector<void*> allocs;
+  DevState S[2];
+  int cur = 0;
+  int32_t *d_ei = nullptr, *d_ej = nullptr, *d_fi = nullptr, *d_fj = nullptr, *d_frozen = nullptr;
+  int64_t *d_eoff = nullptr, *d_doff = nullptr;
+  PixTile* d_tiles = nullptr;
+  int32_t *d_t0s = nullptr, *d_t1s = nullptr, *d_seb = nullptr, *d_see = nullptr;
+  GramTile* d_gtiles = nullptr;
+  int32_t *d_gsrc = nullptr, *d_g0 = nullptr, *d_g1 = nullptr;
+  int64_t *d_goff = nullptr, *d_foff = nullptr;
+  double *d_part = nullptr, *d_tile_e = nullptr, *d_arena = nullptr, *d_gram_part = nullptr, *d_gram = nullptr;
+  float *d_Hdd = nullptr, *d_gd = nullptr, *d_ustep = nullptr, *d_dxd = nullptr;
+  double *d_L = nullptr;
+  int* d_imu_status = nullptr;
+  // reduced system
+  struct Plan {
+    int nbr = 0, nseg = 0;
+    int32_t *bptr = nullptr, *bnff = nullptr, *roff = nullptr, *rdim = nullptr;
+    Contrib* cs = nullptr;
+    int32_t *sptr = nullptr, *soff = nullptr;   // soff: [nseg offsets][nseg dims]
+    Vec* vs = nullptr;
+  } red, exp;
+  bool exp_built = false;
+  double *d_H = nullptr, *d_rhs = nullptr, *d_x = nullptr, *d_Ld = nullptr, *d_dx = nullptr;
+  int32_t* d_fmap = nullptr;
+  Result* d_res = nullptr;
+  Result* h_res = nullptr;
+  vba_allreduce_fn coll = nullptr;
+  void* coll_user = nullptr;
+  bool have_step = false;
+  double last_lam = 0.0;
+  // reference (unpadded) disparity layout, built on first export
+  int32_t* d_npix = nullptr;
+  int64_t* d_roff_real = nullptr;
+  int maxpix = 0;
+  int64_t n_real = 0;
+  // profiling
+  bool prof = false;
+  cudaEvent_t ev[10] = {};
+  double stage_ms[6] = {0, 0, 0, 0, 0, 0};
+  int64_t k1_launches = 0;
+  bool lin_pending = false;
+};
+
+template <class T>
+static int dalloc(Ctx* c, T** p, size_t n) {
+  *p = nullptr;
+  if (n == 0) n = 1;
+  VBA_CUDA(cudaMalloc((void**)p, n * sizeof(T)));
+  c->allocs.push_back((void*)*p);
+  return VBA_OK;
+}
+template <class T>
+static int dupload(Ctx* c, T** p, const std::vector<T>& h, cudaStream_t st) {
+  int rc = dalloc(c, p, h.size());
+  if (rc) return rc;
+  if (!h.empty()) VBA_CUDA(cudaMemcpyAsync(*p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+  return VBA_OK;
+}
+
+static void qmat_h(const double* q, double* R) {
+  const double w = q[0], x = q[1], y = q[2], z = q[3];
+  R[0] = 1 - 2 * (y * y + z * z); R[1] = 2 * (x * y - w * z);     R[2] = 2 * (x * z + w * y);
+  R[3] = 2 * (x * y + w * z);     R[4] = 1 - 2 * (x * x + z * z); R[5] = 2 * (y * z - w * x);
+  R[6] = 2 * (x * z - w * y);     R[7] = 2 * (y * z + w * x);     R[8] = 1 - 2 * (x * x + y * y);
+}
+
+// T_bc = T_cb^{-1}; R_bc^T, c2 = R_bc^T p_bc  (residuals.py:187-192, geometry.py:217-219)
+static void make_extr(const vba_problem& P, Extr& x) {
+  double qi[4] = {1, 0, 0, 0}, t[3] = {0, 0, 0};
+  if (P.has_Tcb) {
+    const double* q = P.Tcb;
+    double n = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    qi[0] = q[0] / n; qi[1] = -q[1] / n; qi[2] = -q[2] / n; qi[3] = -q[3] / n;
+    if (qi[0] < 0) for (double& v : qi) v = -v;
+    t[0] = P.Tcb[4]; t[1] = P.Tcb[5]; t[2] = P.Tcb[6];
+  }
+  qmat_h(qi, x.Rbc);
+  for (int a = 0; a < 3; ++a) {
+    x.pbc[a] = -(x.Rbc[a * 3 + 0] * t[0] + x.Rbc[a * 3 + 1] * t[1] + x.Rbc[a * 3 + 2] * t[2]);
+    for (int b = 0; b < 3; ++b) x.RbcT[a * 3 + b] = x.Rbc[b * 3 + a];
+  }
+  for (int a = 0; a < 3; ++a)
+    x.c2[a] = x.RbcT[a * 3 + 0] * x.pbc[0] + x.RbcT[a * 3 + 1] * x.pbc[1] + x.RbcT[a * 3 + 2] * x.pbc[2];
+}
+
+// ---------------------------------------------------------------------------
+// contribution-list planner for the block matrix (reduced or export layout)
+// ---------------------------------------------------------------------------
+struct BlkBuilder {
+  int nbr;
+  std::vector<std::vector<Contrib>> ff, fl;   // per lower block: H_ff-type, fill-type
+  std::vector<std::vector<Vec>> seg;
+  explicit BlkBuilder(int n) : nbr(n), ff((size_t)n * (n + 1) / 2), fl((size_t)n * (n + 1) / 2), seg(n) {}
+  static size_t id(int a, int b) { return (size_t)a * (a + 1) / 2 + b; }
+  // add matrix M (rows x cols, row-major ld) as block (a,b) of the symmetric matrix
+  void add(int a, int b, int64_t off, int ld, int rows, int cols, int sign, bool fill) {
+    if (a < 0 || b < 0) return;
+    auto& L = [&]() -> std::vector<std::vector<Contrib>>& { return fill ? fl : ff; }();
+    Contrib c{};
+    c.ld = ld;
+    c.sign = (int8_t)sign;
+    if (a > b) {
+      c.off = off; c.rows = (int16_t)rows; c.cols = (int16_t)cols; c.trans = 0;
+      L[id(a, b)].push_back(c);
+    } else if (a < b) {
+      c.off = off; c.rows = (int16_t)cols; c.cols = (int16_t)rows; c.trans = 1;
+      L[id(b, a)].push_back(c);
+    } else {
+      c.off = off; c.rows = (int16_t)rows; c.cols = (int16_t)cols; c.trans = 0;
+      L[id(a, a)].push_back(c);
+    }
+  }
+  // off-diagonal pair block that maps onto a diagonal block: add M and M^T
+  void add_both(int a, int b, int64_t off, int ld, int rows, int cols, int sign, bool fill) {
+    add(a, b, off, ld, rows, cols, sign, fill);
+    if (a == b && a >= 0) {
+      auto& L = fill ? fl : ff;
+      Contrib c{};
+      c.off = off; c.ld = ld; c.rows = (int16_t)cols; c.cols = (int16_t)rows; c.trans = 1; c.sign = (int8_t)sign;
+      L[id(a, a)].push_back(c);
+    }
+  }
+  void addv(int a, int64_t off, int len, int sign) {
+    if (a < 0) return;
+    seg[a].push_back(Vec{off, len, sign});
+  }
+};
+
+static int upload_plan(Ctx* c, BlkBuilder& B, const std::vector<int32_t>& roff, const std::vector<int32_t>& rdim,
+                       Ctx::Plan& pl, cudaStream_t st) {
+  pl.nbr = B.nbr;
+  pl.nseg = B.nbr;
+  std::vector<int32_t> bptr(1, 0), bnff;
+  std::vector<Contrib> cs;
+  for (size_t i = 0; i < B.ff.size(); ++i) {
+    for (auto& x : B.ff[i]) cs.push_back(x);
+    bnff.push_back((int32_t)B.ff[i].size());
+    for (auto& x : B.fl[i]) cs.push_back(x);
+    bptr.push_back((int32_t)cs.size());
+  }
+  std::vector<int32_t> sptr(1, 0), soff;
+  std::vector<Vec> vs;
+  for (int a = 0; a < B.nbr; ++a) {
+    for (auto& v : B.seg[a]) vs.push_back(v);
+    sptr.push_back((int32_t)vs.size());
+  }
+  soff = roff;
+  soff.insert(soff.end(), rdim.begin(), rdim.end());
+  int rc;
+  if ((rc = dupload(c, &pl.bptr, bptr, st)) || (rc = dupload(c, &pl.bnff, bnff, st)) ||
+      (rc = dupload(c, &pl.cs, cs, st)) || (rc = dupload(c, &pl.roff, roff, st)) ||
+      (rc = dupload(c, &pl.rdim, rdim, st)) || (rc = dupload(c, &pl.sptr, sptr, st)) ||
+      (rc = dupload(c, &pl.vs, vs, st)) || (rc = dupload(c, &pl.soff, soff, st)))
+    return rc;
+  return VBA_OK;
+}
+
+// Block indices: `bidx[n]` block of keyframe n (-1 = excluded), gravity block `gb` (-1 = none).
+static void add_all(Ctx* c, BlkBuilder& B, const std::vector<int>& bidx, int gb, bool with_fill) {
+  const int s = c->sdof;
+  const std::vector<int32_t>& ei = c->seb;  (void)ei;
+  // vision edges: [Hii 36][Hjj 36][Hij 36][gi 6][gj 6]
+  for (int e = 0; e < c->E; ++e) {
+    const int i = bidx[c->P.h_edge_i[e]], j = bidx[c->P.h_edge_j[e]];
+    const int64_t o = c->arena_vis + (int64_t)kVisBlock * e;
+    B.add(i, i, o, 6, 6, 6, 1, false);
+    B.add(j, j, o + 36, 6, 6, 6, 1, false);
+    if (c->P.h_edge_i[e] == c->P.h_edge_j[e]) B.add_both(i, j, o + 72, 6, 6, 6, 1, false);
+    else B.add(i, j, o + 72, 6, 6, 6, 1, false);
+    B.addv(i, o + 108, 6, 1);
+    B.addv(j, o + 114, 6, 1);
+  }
+  // IMU factors: [Hii][Hjj][Hij][gi][gj][Hgg 4][Hig s*2][Hjg s*2][gg 2][E]
+  for (int f = 0; f < c->F; ++f) {
+    const int i = bidx[c->P.h_imu_i[f]], j = bidx[c->P.h_imu_j[f]];
+    const int64_t o = c->arena_imu + (int64_t)c->ibs * f;
+    const int s2 = s * s;
+    B.add(i, i, o, s, s, s, 1, false);
+    B.add(j, j, o + s2, s, s, s, 1, false);
+    if (c->P.h_imu_i[f] == c->P.h_imu_j[f]) B.add_both(i, j, o + 2 * s2, s, s, s, 1, false);
+    else B.add(i, j, o + 2 * s2, s, s, s, 1, false);
+    B.addv(i, o + 3 * s2, s, 1);
+    B.addv(j, o + 3 * s2 + s, s, 1);
+    if (gb >= 0) {
+      B.add(gb, gb, o + 3 * s2 + 2 * s, 2, 2, 2, 1, false);
+      B.add(i, gb, o + 3 * s2 + 2 * s + 4, 2, s, 2, 1, false);
+      B.add(j, gb, o + 3 * s2 + 4 * s + 4, 2, s, 2, 1, false);
+      B.addv(gb, o + 3 * s2 + 6 * s + 4, 2, 1);
+    }
+  }
+  if (!with_fill) return;
+  // fill-in per source: [F_ii][F_ij k][F_jj npairs][gr_i][gr_j k], subtracted
+  for (size_t q = 0; q < c->gsrc.size(); ++q) {
+    const int src = c->gsrc[q];
+    const int eb = c->seb[src], k = c->see[src] - eb, np = k * (k + 1) / 2;
+    const int64_t o = c->arena_fill + c->foff[src];
+    const int bi = bidx[src];
+    B.add(bi, bi, o, 6, 6, 6, -1, true);
+    for (int e = 0; e < k; ++e) {
+      const int kj = c->P.h_edge_j[eb + e];
+      if (kj == src) B.add_both(bi, bidx[kj], o + 36 + 36 * e, 6, 6, 6, -1, true);
+      else B.add(bi, bidx[kj], o + 36 + 36 * e, 6, 6, 6, -1, true);
+    }
+    for (int e1 = 0; e1 < k; ++e1)
+      for (int e2 = 0; e2 <= e1; ++e2) {
+        const int p = e1 * (e1 + 1) / 2 + e2;
+        const int k1 = c->P.h_edge_j[eb + e1], k2 = c->P.h_edge_j[eb + e2];
+        const int64_t off = o + 36 + 36 * k + 36 * p;
+        if (k1 == k2 && e1 != e2) B.add_both(bidx[k1], bidx[k2], off, 6, 6, 6, -1, true);
+        else B.add(bidx[k1], bidx[k2], off, 6, 6, 6, -1, true);
+      }
+    const int64_t go = o + 36 + 36 * k + 36 * np;
+    B.addv(bi, go, 6, -1);
+    for (int e = 0; e < k; ++e) B.addv(bidx[c->P.h_edge_j[eb + e]], go + 6 + 6 * e, 6, -1);
+  }
+}
+
+static int build_plans(Ctx* c, cudaStream_t st) {
+  const vba_problem& P = c->P;
+  const int K = c->K, E = c->E;
+  // --- sources and per-pixel tiles
+  c->seb.assign(K, 0);
+  c->see.assign(K, 0);
+  for (int e = 0; e < E; ++e) {
+    const int i = P.h_edge_i[e], j = P.h_edge_j[e];
+    if (i < 0 || i >= K || j < 0 || j >= K) { set_err("edge %d references keyframe out of range", e); return VBA_E_INVALID; }
+    if (e > 0 && i < P.h_edge_i[e - 1]) { set_err("vision edges must be sorted by source keyframe"); return VBA_E_INVALID; }
+    if (P.h_eoff[e] % 4 != 0) { set_err("edge row offsets must be multiples of 4"); return VBA_E_INVALID; }
+  }
+  for (int n = 0; n < K; ++n) { c->seb[n] = 0; c->see[n] = 0; }
+  {
+    int e = 0;
+    for (int n = 0; n < K; ++n) {
+      c->seb[n] = e;
+      while (e < E && P.h_edge_i[e] == n) ++e;
+      c->see[n] = e;
+    }
+  }
+  c->t0s.assign(K, 0);
+  c->t1s.assign(K, 0);
+  int64_t poff = 0;
+  c->kmax = 0;
+  for (int n = 0; n < K; ++n) {
+    const int64_t npad = P.h_doff[n + 1] - P.h_doff[n];
+    if (npad % 4 != 0) { set_err("keyframe disparity segments must be padded to 4"); return VBA_E_INVALID; }
+    const int k = c->see[n] - c->seb[n];
+    if (k > kMaxOutDegree) {
+      set_err("keyframe %d has out-degree %d > %d (unsupported by the Gram kernel)", n, k, kMaxOutDegree);
+      return VBA_E_UNSUPPORTED;
+    }
+    c->kmax = std::max(c->kmax, k);
+    c->t0s[n] = (int)c->tiles.size();
+    for (int64_t n0 = 0; n0 < npad; n0 += kTileRt) {
+      PixTile t{};
+      t.src = n;
+      t.n0 = (int)n0;
+      t.cnt = (int)std::min<int64_t>(kTileRt, npad - n0);
+      t.eb = c->seb[n];
+      t.ee = c->see[n];
+      t.poff = poff;
+      poff += k;
+      c->tiles.push_back(t);
+    }
+    c->t1s[n] = (int)c->tiles.size();
+  }
+  c->n_part = poff;
+  // --- Gram tiles
+  int nsrc = 0;
+  int64_t work_px = 0;
+  for (int n = 0; n < K; ++n)
+    if (c->see[n] > c->seb[n] && P.h_npix[n] > 0) { ++nsrc; work_px += P.h_npix[n]; }
+  const int target = 2 * 148;
+  c->goff.assign(K, 0);
+  c->foff.assign(K, 0);
+  c->g0.assign(K, 0);
+  c->g1.assign(K, 0);
+  int64_t gpo = 0, go = 0, fo = 0;
+  c->gram_smem = 0;
+  for (int n = 0; n < K; ++n) {
+    const int k = c->see[n] - c->seb[n];
+    const int npix = P.h_npix[n];
+    c->g0[n] = c->g1[n] = (int)c->gtiles.size();
+    if (k == 0 || npix == 0) continue;
+    c->gsrc.push_back(n);
+    const int np = k * (k + 1) / 2;
+    int nsplit = std::max(1, std::min(16, kGramBlock / np));
+    while (nsplit > 1 && gram_smem_bytes(c->kmax, nsplit, np, k) > 200 * 1024) --nsplit;
+    c->gram_smem = std::max(c->gram_smem, gram_smem_bytes(c->kmax, nsplit, np, k));
+    int R = std::max(1, (int)((target + nsrc - 1) / nsrc));
+    R = std::min(R, std::max(1, npix / 256));
+    const int chunk = ((npix + R - 1) / R + 31) / 32 * 32;
+    for (int a = 0; a < npix; a += chunk) {
+      GramTile g{};
+      g.src = n;
+      g.n0 = a;
+      g.n1 = std::min(npix, a + chunk);
+      g.eb = c->seb[n];
+      g.ee = c->see[n];
+      g.nsplit = nsplit;
+      g.out = gpo;
+      gpo += (int64_t)np * 36 + 6 * k;
+      c->gtiles.push_back(g);
+    }
+    c->g1[n] = (int)c->gtiles.size();
+    c->goff[n] = go;
+    go += (int64_t)np * 36 + 6 * k;
+    c->foff[n] = fo;
+    fo += (int64_t)(1 + k + np) * 36 + 6 * (1 + k);
+  }
+  if (c->gram_smem > 227 * 1024) { set_err("Gram kernel shared memory too large"); return VBA_E_UNSUPPORTED; }
+  c->gram_part_len = gpo;
+  c->gram_len = go;
+  c->fill_len = fo;
+  // --- arena layout
+  const int s = c->sdof;
+  c->ibs = ((3 * s * s + 6 * s + 7) + 7) / 8 * 8;
+  c->arena_vis = 0;
+  c->arena_imu = (int64_t)kVisBlock * E;
+  c->arena_fill = c->arena_imu + (int64_t)c->ibs * c->F;
+  c->arena_len = c->arena_fill + c->fill_len;
+  // --- reduced-system layout (free keyframes, then gravity)
+  std::vector<int> bidx(K, -1);
+  std::vector<int32_t> roff, rdim;
+  c->kf_col.assign(K, -1);
+  int col = 0, nb = 0;
+  for (int n = 0; n < K; ++n) {
+    if (P.h_frozen[n]) continue;
+    bidx[n] = nb++;
+    c->kf_col[n] = col;
+    roff.push_back(col);
+    rdim.push_back(s);
+    col += s;
+  }
+  c->nfk = nb;
+  int gb = -1;
+  if (c->ngrav) {
+    gb = nb++;
+    roff.push_back(col);
+    rdim.push_back(2);
+    col += 2;
+  }
+  c->nfree = col;
+  c->npad = (col + NBc - 1) / NBc * NBc;
+  c->nt = c->npad / NBc;
+  c->fmap.assign(c->npv, -1);
+  for (int n = 0; n < K; ++n)
+    if (c->kf_col[n] >= 0)
+      for (int r = 0; r < s; ++r) c->fmap[n * s + r] = c->kf_col[n] + r;
+  if (c->ngrav)
+    for (int r = 0; r < 2; ++r) c->fmap[c->n_state + r] = c->nfree - 2 + r;
+  BlkBuilder B(nb);
+  add_all(c, B, bidx, gb, true);
+  return upload_plan(c, B, roff, rdim, c->red, st);
+}
+
+static int build_export_plan(Ctx* c, cudaStream_t st) {
+  if (c->exp_built) return VBA_OK;
+  const int K = c->K, s = c->sdof;
+  std::vector<int> bidx(K);
+  std::vector<int32_t> roff, rdim;
+  for (int n = 0; n < K; ++n) {
+    bidx[n] = n;
+    roff.push_back(n * s);
+    rdim.push_back(s);
+  }
+  int gb = -1;
+  if (c->ngrav) {
+    gb = K;
+    roff.push_back(K * s);
+    rdim.push_back(2);
+  }
+  BlkBuilder B(K + (c->ngrav ? 1 : 0));
+  add_all(c, B, bidx, gb, false);
+  int rc = upload_plan(c, B, roff, rdim, c->exp, st);
+  if (rc) return rc;
+  c->exp_built = true;
+  return VBA_OK;
+}
+
+// ---------------------------------------------------------------------------
+// stages
+// ---------------------------------------------------------------------------
+static DevState& CUR(Ctx* c) { return c->S[c->cur]; }
+static DevState& NXT(Ctx* c) { return c->S[c->cur ^ 1]; }
+
+// optional per-stage CUDA-event timing (vba_set_profiling), events on the launch stream:
+//   7 | 0 edge prep | 8 K1 kernel | 9 finalize + IMU | 1     (linearisation)
+//   2 gram+fill | 3 assemble+chol | 4 backsub+retract | 5 energy | 6     (trial)
+// stage_ms: [0] linearise (all) [1] gram+fill [2] assemble+chol [3] backsub+retract
+//           [4] energy [5] K1 kernel alone;  k1_launches counts [5]'s samples.
+static void mark(Ctx* c, int i, cudaStream_t st) {
+  if (c->prof) cudaEventRecord(c->ev[i], st);
+}
+static void prof_collect(Ctx* c, bool with_lin) {
+  if (!c->prof) return;
+  float ms;
+  if (with_lin && cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]) == cudaSuccess) c->stage_ms[0] += ms;
+  if (with_lin && cudaEventElapsedTime(&ms, c->ev[8], c->ev[9]) == cudaSuccess) {
+    c->stage_ms[5] += ms;
+    c->k1_launches += 1;
+  }
+  for (int s = 0; s < 4; ++s)
+    if (cudaEventElapsedTime(&ms, c->ev[2 + s], c->ev[3 + s]) == cudaSuccess) c->stage_ms[1 + s] += ms;
+}
+
+static int stage_energy(Ctx* c, DevState& s, cudaStream_t st) {
+  launch_edge_prep(s, c->d_ei, c->d_ej, c->E, c->extr, st);
+  launch_vision_energy(c->P.pixel_mode, c->d_tiles, (int)c->tiles.size(), s, c->P.pix, c->P.tgt, c->P.wts,
+                       c->d_eoff, c->d_doff, c->P.grid_w, c->grid, c->intr, c->d_tile_e, st);
+  launch_imu_factor(c->P.imu, c->d_L, c->d_fi, c->d_fj, c->F, s, c->P.ts, c->sdof, c->ibs, 1,
+                    c->d_arena + c->arena_imu, st);
+  const int oE = 3 * c->sdof * c->sdof + 6 * c->sdof + 6;
+  launch_energy_reduce(c->d_tile_e, (int)c->tiles.size(), c->d_arena + c->arena_imu, c->F, c->ibs, oE,
+                       c->d_res->energy, st);
+  return VBA_OK;
+}
+
+static int stage_linearize(Ctx* c, cudaStream_t st) {
+  DevState& s = CUR(c);
+  mark(c, 0, st);
+  c->lin_pending = true;
+  launch_edge_prep(s, c->d_ei, c->d_ej, c->E, c->extr, st);
+  mark(c, 8, st);
+  launch_vision_linearize(c->P.pixel_mode, c->d_tiles, (int)c->tiles.size(), s, c->P.pix, c->P.tgt, c->P.wts,
+                          c->d_eoff, c->d_doff, c->P.grid_w, c->grid, c->intr, c->d_part, c->d_Hdd, c->d_gd, st);
+  mark(c, 9, st);
+  launch_edge_finalize(c->d_t0s, c->d_t1s, c->d_tiles, c->d_ei, c->E, c->d_part, s, c->extr,
+                       c->d_arena + c->arena_vis, nullptr, st);
+  launch_imu_factor(c->P.imu, c->d_L, c->d_fi, c->d_fj, c->F, s, c->P.ts, c->sdof, c->ibs, 0,
+                    c->d_arena + c->arena_imu, st);
+  mark(c, 1, st);
+  return VBA_OK;
+}
+
+// reduced system + Cholesky + back-substitution into the NEXT buffers
+static int stage_step(Ctx* c, double lam, cudaStream_t st) {
+  DevState& s = CUR(c);
+  DevState& n = NXT(c);
+  mark(c, 2, st);
+  VBA_CUDA(cudaMemsetAsync(c->d_res, 0, sizeof(Result), st));
+  if (!c->gtiles.empty()) {
+    launch_gram(c->P.pixel_mode, c->d_gtiles, (int)c->gtiles.size(), kGramBlock, c->gram_smem, c->kmax, s,
+                c->P.pix, c->P.wts, c->d_eoff, c->d_doff, c->P.grid_w, c->grid, c->intr, c->d_Hdd, c->d_gd, lam,
+                c->O.ridge, c->d_gram_part, st);
+    launch_gram_reduce(c->d_gsrc, (int)c->gsrc.size(), c->d_g0, c->d_g1, c->d_gtiles, c->d_seb, c->d_see,
+                       c->d_goff, c->d_gram_part, c->d_gram, st);
+    launch_fill_transform(c->d_gsrc, (int)c->gsrc.size(), c->d_seb, c->d_see, c->d_goff, c->d_foff, c->d_gram, s,
+                          c->extr, c->d_arena + c->arena_fill, c->kmax, st);
+  }
+  mark(c, 3, st);
+  if (c->nfree > 0) {
+    const bool multi = c->coll != nullptr;
+    launch_assemble(c->red.bptr, c->red.bnff, c->red.cs, c->red.nbr, c->red.roff, c->red.rdim, c->d_arena, lam,
+                    c->O.ridge, multi ? 0 : 1, c->d_H, c->npad, 0, st);
+    // right-hand side -g_red: the step solves H_red dx = -g_red (solver.py:287)
+    launch_assemble_vec(c->red.sptr, c->red.vs, c->red.nseg, c->red.soff, c->d_arena, -1.0, c->d_rhs, st);
+    if (multi) {
+      if (c->coll(c->coll_user, c->d_H, (int64_t)c->npad * c->npad, 0, st)) { set_err("allreduce(H) failed"); return VBA_E_CUDA; }
+      if (c->coll(c->coll_user, c->d_rhs, c->npad, 0, st)) { set_err("allreduce(g) failed"); return VBA_E_CUDA; }
+      launch_add_ridge(c->d_H, c->npad, c->nfree, c->O.ridge, st);
+    }
+    chol_solve(c->d_H, c->npad, c->npad, c->d_rhs, c->d_x, c->d_Ld, &c->d_res->status, st);
+  }
+  mark(c, 4, st);
+  launch_scatter_dx(c->d_x, c->d_fmap, c->npv, c->d_dx, st);
+  launch_step_edges(c->d_ei, c->d_ej, c->E, s, c->extr, c->d_dx, c->sdof, c->d_ustep, st);
+  launch_backsub(c->P.pixel_mode, c->d_tiles, (int)c->tiles.size(), s, n, c->P.pix, c->P.wts, c->d_eoff,
+                 c->d_doff, c->P.grid_w, c->grid, c->intr, c->d_Hdd, c->d_gd, c->d_ustep, lam, c->O.ridge,
+                 c->d_dxd, &c->d_res->step_bits, st);
+  launch_retract(s, n, c->d_dx, c->d_frozen, c->K, c->sdof, c->ngrav, c->n_state, &c->d_res->step_bits, c->npv, st);
+  c->have_step = true;
+  c->last_lam = lam;
+  return VBA_OK;
+}
+
+static int run_trial(Ctx* c, double lam, vba_trial_result* out, cudaStream_t st) {
+  int rc = stage_step(c, lam, st);
+  if (rc) return rc;
+  mark(c, 5, st);
+  rc = stage_energy(c, NXT(c), st);
+  if (rc) return rc;
+  mark(c, 6, st);
+  if (c->coll) {
+    if (c->coll(c->coll_user, c->d_res->energy, 3, 0, st)) { set_err("allreduce(energy) failed"); return VBA_E_CUDA; }
+    if (c->coll(c->coll_user, (double*)&c->d_res->step_bits, 1, 1, st)) { set_err("allreduce(step) failed"); return VBA_E_CUDA; }
+  }
+  VBA_CUDA(cudaMemcpyAsync(c->h_res, c->d_res, sizeof(Result), cudaMemcpyDeviceToHost, st));
+  VBA_CUDA(cudaStreamSynchronize(st));
+  prof_collect(c, c->lin_pending);
+  c->lin_pending = false;
+  out->status = c->h_res->status ? VBA_E_NOT_SPD : VBA_OK;
+  out->new_cost = c->h_res->energy[0];
+  double si;
+  unsigned long long b = c->h_res->step_bits;
+  std::memcpy(&si, &b, sizeof(double));
+  out->step_inf = si;
+  return VBA_OK;
+}
+
+}  // namespace vba
+
+using namespace vba;
+
+extern "C" {
+
+const char* vba_last_error(void) { return g_err.c_str(); }
+int vba_version(void) { return 1; }
+
+int vba_create(void** out, const vba_problem* prob, const vba_options* opts, void* stream) {
+  *out = nullptr;
+  if (!prob || !opts) { set_err("null problem/options"); return VBA_E_INVALID; }
+  cudaStream_t st = (cudaStream_t)stream;
+  Ctx* c = new Ctx();
+  c->P = *prob;
+  c->O = *opts;
+  c->K = prob->n_kf;
+  c->E = prob->n_edges;
+  c->F = prob->n_imu;
+  c->sdof = opts->optimize_velocity_bias ? 15 : 6;
+  c->ngrav = opts->optimize_gravity ? 2 : 0;
+  c->n_state = c->K * c->sdof;
+  c->npv = c->n_state + c->ngrav;
+  c->n_disp = prob->n_disp_pad;
+  c->n_rows = prob->n_rows_pad;
+  c->grid[0] = prob->grid_ox; c->grid[1] = prob->grid_oy; c->grid[2] = prob->grid_sx; c->grid[3] = prob->grid_sy;
+  c->intr[0] = prob->fx; c->intr[1] = prob->fy; c->intr[2] = prob->cx; c->intr[3] = prob->cy;
+  auto fail = [&](int rc) { vba_destroy(c); return rc; };
+  if (c->K <= 0 || c->E < 0 || c->F < 0) { set_err("invalid sizes"); return fail(VBA_E_INVALID); }
+  if (prob->pixel_mode < 0 || prob->pixel_mode > 2 || (prob->pixel_mode == VBA_PIX_GRID && prob->grid_w <= 0) ||
+      (prob->pixel_mode != VBA_PIX_GRID && !prob->pix)) {
+    set_err("invalid pixel mode");
+    return fail(VBA_E_INVALID);
+  }
+  if (!(opts->ridge > 0) || !(opts->damping > 0)) { set_err("invalid options"); return fail(VBA_E_INVALID); }
+  make_extr(*prob, c->extr);
+  int rc = build_plans(c, st);
+  if (rc) return fail(rc);
+  // topology to device
+  std::vector<int32_t> ei(prob->h_edge_i, prob->h_edge_i + c->E), ej(prob->h_edge_j, prob->h_edge_j + c->E);
+  std::vector<int32_t> fi(prob->h_imu_i, prob->h_imu_i + c->F), fj(prob->h_imu_j, prob->h_imu_j + c->F);
+  std::vector<int32_t> fr(prob->h_frozen, prob->h_frozen + c->K);
+  std::vector<int64_t> eoff(prob->h_eoff, prob->h_eoff + c->E), doff(prob->h_doff, prob->h_doff + c->K + 1);
+  if ((rc = dupload(c, &c->d_ei, ei, st)) || (rc = dupload(c, &c->d_ej, ej, st)) ||
+      (rc = dupload(c, &c->d_fi, fi, st)) || (rc = dupload(c, &c->d_fj, fj, st)) ||
+      (rc = dupload(c, &c->d_frozen, fr, st)) || (rc = dupload(c, &c->d_eoff, eoff, st)) ||
+      (rc = dupload(c, &c->d_doff, doff, st)) || (rc = dupload(c, &c->d_tiles, c->tiles, st)) ||
+      (rc = dupload(c, &c->d_t0s, c->t0s, st)) || (rc = dupload(c, &c->d_t1s, c->t1s, st)) ||
+      (rc = dupload(c, &c->d_seb, c->seb, st)) || (rc = dupload(c, &c->d_see, c->see, st)) ||
+      (rc = dupload(c, &c->d_gtiles, c->gtiles, st)) || (rc = dupload(c, &c->d_gsrc, c->gsrc, st)) ||
+      (rc = dupload(c, &c->d_g0, c->g0, st)) || (rc = dupload(c, &c->d_g1, c->g1, st)) ||
+      (rc = dupload(c, &c->d_goff, c->goff, st)) || (rc = dupload(c, &c->d_foff, c->foff, st)) ||
+      (rc = dupload(c, &c->d_fmap, c->fmap, st)))
+    return fail(rc);
+  // state double buffers
+  for (int b = 0; b < 2; ++b) {
+    DevState& s = c->S[b];
+    if ((rc = dalloc(c, &s.state, (size_t)16 * c->K)) || (rc = dalloc(c, &s.disp, (size_t)c->n_disp)) ||
+        (rc = dalloc(c, &s.grav, 5)) || (rc = dalloc(c, &s.geo32, (size_t)c->E)) ||
+        (rc = dalloc(c, &s.geo64, (size_t)kGeo64 * c->E)))
+      return fail(rc);
+  }
+  if (cudaMemcpyAsync(c->S[0].state, prob->state, sizeof(double) * 16 * c->K, cudaMemcpyDeviceToDevice, st) ||
+      (c->n_disp && cudaMemcpyAsync(c->S[0].disp, prob->disp, sizeof(float) * c->n_disp, cudaMemcpyDeviceToDevice, st)) ||
+      cudaMemcpyAsync(c->S[0].grav, prob->grav, sizeof(double) * 5, cudaMemcpyDeviceToDevice, st)) {
+    set_err("state upload failed");
+    return fail(VBA_E_CUDA);
+  }
+  // workspace
+  if ((rc = dalloc(c, &c->d_part, (size_t)c->n_part * kPartStride)) ||
+      (rc = dalloc(c, &c->d_tile_e, c->tiles.size())) || (rc = dalloc(c, &c->d_arena, (size_t)c->arena_len)) ||
+      (rc = dalloc(c, &c->d_gram_part, (size_t)c->gram_part_len)) ||
+      (rc = dalloc(c, &c->d_gram, (size_t)c->gram_len)) || (rc = dalloc(c, &c->d_Hdd, (size_t)c->n_disp)) ||
+      (rc = dalloc(c, &c->d_gd, (size_t)c->n_disp)) || (rc = dalloc(c, &c->d_ustep, (size_t)8 * c->E)) ||
+      (rc = dalloc(c, &c->d_dxd, (size_t)c->n_disp)) || (rc = dalloc(c, &c->d_L, (size_t)kImuL * c->F)) ||
+      (rc = dalloc(c, &c->d_imu_status, 1)) || (rc = dalloc(c, &c->d_H, (size_t)c->npad * c->npad)) ||
+      (rc = dalloc(c, &c->d_rhs, (size_t)c->npad)) || (rc = dalloc(c, &c->d_x, (size_t)c->npad)) ||
+      (rc = dalloc(c, &c->d_Ld, (size_t)std::max(1, c->nt) * NBc * NBc)) ||
+      (rc = dalloc(c, &c->d_dx, (size_t)c->npv)) || (rc = dalloc(c, &c->d_res, 1)))
+    return fail(rc);
+  if (cudaMallocHost((void**)&c->h_res, sizeof(Result)) != cudaSuccess) { set_err("pinned alloc failed"); return fail(VBA_E_CUDA); }
+  cudaMemsetAsync(c->d_arena, 0, sizeof(double) * std::max<int64_t>(1, c->arena_len), st);
+  cudaMemsetAsync(c->d_Hdd, 0, sizeof(float) * std::max<int64_t>(1, c->n_disp), st);
+  cudaMemsetAsync(c->d_gd, 0, sizeof(float) * std::max<int64_t>(1, c->n_disp), st);
+  cudaMemsetAsync(c->d_x, 0, sizeof(double) * std::max(1, c->npad), st);
+  cudaMemsetAsync(c->d_rhs, 0, sizeof(double) * std::max(1, c->npad), st);
+  cudaMemsetAsync(c->d_H, 0, sizeof(double) * std::max<size_t>(1, (size_t)c->npad * c->npad), st);
+  launch_pad_identity(c->d_H, c->npad, c->nfree, c->npad, c->d_rhs, st);
+  // IMU whitening factors (constant over the solve)
+  cudaMemsetAsync(c->d_imu_status, 0, sizeof(int), st);
+  launch_imu_prep(prob->imu, c->F, c->d_L, c->d_imu_status, st);
+  int hs = 0;
+  if (cudaMemcpyAsync(&hs, c->d_imu_status, sizeof(int), cudaMemcpyDeviceToHost, st) ||
+      cudaStreamSynchronize(st) != cudaSuccess) {
+    set_err("create: %s", cudaGetErrorString(cudaGetLastError()));
+    return fail(VBA_E_CUDA);
+  }
+  if (hs) { set_err("non-PSD preintegration covariance"); return fail(VBA_E_COV); }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { set_err("create: %s", cudaGetErrorString(e)); return fail(VBA_E_CUDA); }
+  *out = c;
+  return VBA_OK;
+}
+
+int vba_destroy(void* ctx) {
+  Ctx* c = (Ctx*)ctx;
+  if (!c) return VBA_OK;
+  for (void* p : c->allocs) cudaFree(p);
+  if (c->h_res) cudaFreeHost(c->h_res);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  delete c;
+  return VBA_OK;
+}
+
+int vba_set_collective(void* ctx, vba_allreduce_fn fn, void* user) {
+  Ctx* c = (Ctx*)ctx;
+  c->coll = fn;
+  c->coll_user = user;
+  return VBA_OK;
+}
+
+int64_t vba_reduced_dim(void* ctx) { return ((Ctx*)ctx)->nfree; }
+int64_t vba_launch_count(void* /*ctx*/) { return launch_total(); }
+
+int vba_energy(void* ctx, void* stream, double* tot, double* vis, double* ine) {
+  Ctx* c = (Ctx*)ctx;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = stage_energy(c, CUR(c), st);
+  if (rc) return rc;
+  if (c->coll && c->coll(c->coll_user, c->d_res->energy, 3, 0, st)) { set_err("allreduce failed"); return VBA_E_CUDA; }
+  VBA_CUDA(cudaMemcpyAsync(c->h_res, c->d_res, sizeof(Result), cudaMemcpyDeviceToHost, st));
+  VBA_CUDA(cudaStreamSynchronize(st));
+  if (tot) *tot = c->h_res->energy[0];
+  if (vis) *vis = c->h_res->energy[1];
+  if (ine) *ine = c->h_res->energy[2];
+  return VBA_OK;
+}
+
+int vba_linearize(void* ctx, void* stream) {
+  Ctx* c = (Ctx*)ctx;
+  int rc = stage_linearize(c, (cudaStream_t)stream);
+  if (rc) return rc;
+  VBA_CUDA(cudaGetLastError());
+  return VBA_OK;
+}
+
+int vba_solve_step(void* ctx, void* stream, double lam, int32_t use_schur) {
+  Ctx* c = (Ctx*)ctx;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!use_schur) { set_err("dense (use_schur=False) path not available"); return VBA_E_UNSUPPORTED; }
+  int rc = stage_step(c, lam, st);
+  if (rc) return rc;
+  VBA_CUDA(cudaMemcpyAsync(c->h_res, c->d_res, sizeof(Result), cudaMemcpyDeviceToHost, st));
+  VBA_CUDA(cudaStreamSynchronize(st));
+  return c->h_res->status ? VBA_E_NOT_SPD : VBA_OK;
+}
+
+int vba_apply_step(void* ctx, void* /*stream*/) {
+  Ctx* c = (Ctx*)ctx;
+  if (!c->have_step) { set_err("no step computed"); return VBA_E_INVALID; }
+  c->cur ^= 1;   // the next buffers already hold the retracted state; the old ones are the snapshot
+  return VBA_OK;
+}
+
+int vba_restore(void* ctx, void* /*stream*/) {
+  Ctx* c = (Ctx*)ctx;
+  c->cur ^= 1;
+  return VBA_OK;
+}
+
+int vba_accept(void* ctx, void* /*stream*/) {
+  ((Ctx*)ctx)->cur ^= 1;
+  return VBA_OK;
+}
+
+int vba_trial(void* ctx, void* stream, double lam, int32_t use_schur, vba_trial_result* out) {
+  Ctx* c = (Ctx*)ctx;
+  if (!use_schur) { set_err("dense (use_schur=False) path not available"); return VBA_E_UNSUPPORTED; }
+  return run_trial(c, lam, out, (cudaStream_t)stream);
+}
+
+int vba_solve(void* ctx, void* stream, vba_report* rep, double* traj, int32_t cap) {
+  Ctx* c = (Ctx*)ctx;
+  cudaStream_t st = (cudaStream_t)stream;
+  const vba_options& o = c->O;
+  std::memset(rep, 0, sizeof(*rep));
+  if (!o.use_schur) { set_err("dense (use_schur=False) path not available"); return VBA_E_UNSUPPORTED; }
+  double cost;
+  int rc = vba_energy(ctx, stream, &cost, nullptr, nullptr);
+  if (rc) return rc;
+  std::vector<double> tr{cost};
+  auto finish = [&](int iters, int term, int warns, int trials) {
+    rep->iterations = iters;
+    rep->termination = term;
+    rep->n_warnings = warns;
+    rep->trials = trials;
+    rep->initial_cost = tr[0];
+    rep->final_cost = cost;
+    rep->n_costs = (int)tr.size();
+    for (int i = 0; i < (int)tr.size() && i < cap; ++i) traj[i] = tr[i];
+    return VBA_OK;
+  };
+  if (o.max_iterations == 0) return finish(0, 0, 0, 0);
+  double lam = o.damping;
+  int term = 0, iters = 0, warns = 0, trials = 0;
+  bool broke = false;
+  for (int it = 0; it < o.max_iterations; ++it) {
+    if ((rc = stage_linearize(c, st))) return rc;
+    bool accepted = false;
+    while (true) {
+      vba_trial_result r;
+      if ((rc = run_trial(c, lam, &r, st))) return rc;
+      ++trials;
+      if (r.status == VBA_E_NOT_SPD) {   // solver.py:373-379
+        ++warns;
+        lam *= o.damping_up;
+        if (lam > o.max_damping) return finish(iters, 3, warns, trials);
+        continue;
+      }
+      if (r.new_cost < cost) {             // solver.py:383-393
+        cost = r.new_cost;
+        tr.push_back(cost);
+        lam = std::max(lam * o.damping_down, 1e-12);
+        accepted = true;
+        iters = it + 1;
+        c->cur ^= 1;
+        if (r.step_inf < o.step_tol) term = 1;
+        break;
+      }
+      lam *= o.damping_up;                 // solver.py:394-398
+      if (lam > o.max_damping) { term = 2; break; }
+    }
+    if (!accepted) { broke = true; break; }
+    if (term == 1) { broke = true; break; }
+    const double prev = tr[tr.size() - 2];
+    if (prev > 0 && (prev - cost) / prev < o.rel_decrease_tol) { term = 1; broke = true; break; }
+  }
+  if (!broke) term = 0;
+  VBA_CUDA(cudaGetLastError());
+  return finish(iters, term, warns, trials);
+}
+
+int vba_download(void* ctx, void* stream) {
+  Ctx* c = (Ctx*)ctx;
+  cudaStream_t st = (cudaStream_t)stream;
+  DevState& s = CUR(c);
+  VBA_CUDA(cudaMemcpyAsync(c->P.state, s.state, sizeof(double) * 16 * c->K, cudaMemcpyDeviceToDevice, st));
+  if (c->n_disp) VBA_CUDA(cudaMemcpyAsync(c->P.disp, s.disp, sizeof(float) * c->n_disp, cudaMemcpyDeviceToDevice, st));
+  VBA_CUDA(cudaMemcpyAsync(c->P.grav, s.grav, sizeof(double) * 5, cudaMemcpyDeviceToDevice, st));
+  return VBA_OK;
+}
+
+static int ensure_real_layout(Ctx* c, cudaStream_t st) {
+  if (c->d_npix) return VBA_OK;
+  std::vector<int32_t> np(c->P.h_npix, c->P.h_npix + c->K);
+  std::vector<int64_t> ro(c->K + 1, 0);
+  c->maxpix = 0;
+  for (int n = 0; n < c->K; ++n) {
+    ro[n + 1] = ro[n] + np[n];
+    c->maxpix = std::max(c->maxpix, np[n]);
+  }
+  c->n_real = ro[c->K];
+  int rc;
+  if ((rc = dupload(c, &c->d_npix, np, st)) || (rc = dupload(c, &c->d_roff_real, ro, st))) return rc;
+  return VBA_OK;
+}
+
+int vba_export_normal_eq(void* ctx, void* stream, double* H_pp, double* g_p, double* H_pd, double* H_dd,
+                         double* g_d) {
+  Ctx* c = (Ctx*)ctx;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = build_export_plan(c, st);
+  if (rc) return rc;
+  if ((rc = ensure_real_layout(c, st))) return rc;
+  DevState& s = CUR(c);
+  if (H_pp) {
+    VBA_CUDA(cudaMemsetAsync(H_pp, 0, sizeof(double) * c->npv * c->npv, st));
+    launch_assemble(c->exp.bptr, c->exp.bnff, c->exp.cs, c->exp.nbr, c->exp.roff, c->exp.rdim, c->d_arena, 0.0,
+                    0.0, 0, H_pp, c->npv, 1, st);
+  }
+  if (g_p) launch_assemble_vec(c->exp.sptr, c->exp.vs, c->exp.nseg, c->exp.soff, c->d_arena, 1.0, g_p, st);
+  if (H_dd) launch_unpad(c->d_Hdd, c->d_doff, c->d_roff_real, c->d_npix, c->maxpix, c->K, H_dd, st);
+  if (g_d) launch_unpad(c->d_gd, c->d_doff, c->d_roff_real, c->d_npix, c->maxpix, c->K, g_d, st);
+  if (H_pd) {
+    VBA_CUDA(cudaMemsetAsync(H_pd, 0, sizeof(double) * c->npv * std::max<int64_t>(1, c->n_real), st));
+    launch_export_hpd(c->P.pixel_mode, c->d_seb, c->d_see, c->d_doff, c->d_roff_real, c->d_npix, c->maxpix, c->d_ej,
+                      c->K, s, c->extr, c->P.pix, c->P.wts, c->d_eoff, c->P.grid_w, c->grid, c->intr, c->sdof,
+                      c->n_real, H_pd, st);
+  }
+  VBA_CUDA(cudaStreamSynchronize(st));
+  return VBA_OK;
+}
+
+int vba_export_step(void* ctx, void* stream, double* dx_full, double* dx_d) {
+  Ctx* c = (Ctx*)ctx;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!c->have_step) { set_err("no step computed"); return VBA_E_INVALID; }
+  int rc = ensure_real_layout(c, st);
+  if (rc) return rc;
+  if (dx_full) VBA_CUDA(cudaMemcpyAsync(dx_full, c->d_dx, sizeof(double) * c->npv, cudaMemcpyDeviceToDevice, st));
+  if (dx_d) launch_unpad(c->d_dxd, c->d_doff, c->d_roff_real, c->d_npix, c->maxpix, c->K, dx_d, st);
+  VBA_CUDA(cudaStreamSynchronize(st));
+  return VBA_OK;
+}
+
+int vba_set_profiling(void* ctx, int32_t on) {
+  Ctx* c = (Ctx*)ctx;
+  if (on && !c->prof)
+    for (auto& e : c->ev) VBA_CUDA(cudaEventCreate(&e));
+  c->prof = on != 0;
+  for (double& v : c->stage_ms) v = 0.0;
+  c->k1_launches = 0;
+  return VBA_OK;
+}
+
+int vba_stage_times(void* ctx, double* out7) {
+  Ctx* c = (Ctx*)ctx;
+  for (int i = 0; i < 6; ++i) out7[i] = c->stage_ms[i];
+  out7[6] = (double)c->k1_launches;
+  return VBA_OK;
+}
+
+int vba_load_state(void* ctx, void* stream) {
+  Ctx* c = (Ctx*)ctx;
+  cudaStream_t st = (cudaStream_t)stream;
+  DevState& s = CUR(c);
+  VBA_CUDA(cudaMemcpyAsync(s.state, c->P.state, sizeof(double) * 16 * c->K, cudaMemcpyDeviceToDevice, st));
+  if (c->n_disp) VBA_CUDA(cudaMemcpyAsync(s.disp, c->P.disp, sizeof(float) * c->n_disp, cudaMemcpyDeviceToDevice, st));
+  VBA_CUDA(cudaMemcpyAsync(s.grav, c->P.grav, sizeof(double) * 5, cudaMemcpyDeviceToDevice, st));
+  c->have_step = false;
+  return VBA_OK;
+}
+
+}  // extern "C"

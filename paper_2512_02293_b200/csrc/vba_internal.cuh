@@ -1,0 +1,314 @@
+// vba_internal.cuh — shared device structs, fp64 Lie-group helpers and launchers.
+//
+// Numerical conventions restated from the reference (paths relative to
+// /root/reference/pkg/src/vislam/):
+//   quaternions wxyz, canonical w >= 0, renormalised on every product (geometry.py:94-107)
+//   small-angle cutoff 1e-8 for exp / Jr / Jr^-1 / log (geometry.py:20,38,62,75,117,163)
+//   right rotation perturbation, additive world translation (geometry.py:221-223)
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/vba.h"
+
+namespace vba {
+
+constexpr double kSmallAngle = 1e-8;
+constexpr float kDispFloor = 1e-4f;      // solver.py:32
+constexpr int kPartStride = 32;          // doubles per K1 (tile, edge) partial record
+constexpr int kVisBlock = 120;           // doubles per edge pose-space block record
+constexpr int kGeo64 = 24;               // doubles per EdgeGeo64 record
+constexpr int kImuL = 120;               // doubles per IMU whitening-factor record (81 + 36 + pad)
+
+// Per-edge camera-frame constants for the per-pixel loops (fp32):
+// X_h = ray + (M - I) ray + d t, with M = A R_i R_bc the camera-i -> camera-j rotation.
+struct __align__(16) EdgeGeo32 {
+  float M[9];   // M - I
+
+  float t[3];
+  float pad[4];
+};
+
+// Global extrinsic constants: R_bc^T and c2 = R_bc^T p_bc (residuals.py:187-204).
+struct Extr {
+  double RbcT[9];
+  double Rbc[9];
+  double pbc[3];
+  double c2[3];
+};
+
+// Work tile of the per-pixel kernels: `cnt` padded pixels of source keyframe `src`
+// starting at pixel `n0`, looping over that source's out-edges [eb, ee).
+struct PixTile {
+  int32_t src, n0, cnt, eb, ee;
+  int32_t pad;
+  int64_t poff;   // first K1 partial record of this tile (one per out-edge)
+};
+
+// Work tile of the Schur Gram kernel (one source keyframe, a pixel range).
+struct GramTile {
+  int32_t src, n0, n1, eb, ee, nsplit;
+  int64_t out;    // offset (doubles) of this tile's partial Gram output
+};
+
+// Assembly contribution: value(r,c) = sign * buf[off + (trans ? c*ld + r : r*ld + c)]
+struct Contrib {
+  int64_t off;
+  int32_t ld;
+  int16_t rows, cols;
+  int8_t trans, sign;
+  int8_t pad[6];
+};
+
+struct Vec {
+  int64_t off;
+  int32_t len;
+  int32_t sign;
+};
+
+// ---------------------------------------------------------------------------
+// fp64 SO(3) helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void mat3_mul(const double* A, const double* B, double* C) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      C[i * 3 + j] = A[i * 3 + 0] * B[0 * 3 + j] + A[i * 3 + 1] * B[1 * 3 + j] + A[i * 3 + 2] * B[2 * 3 + j];
+}
+__device__ __forceinline__ void mat3_mulT(const double* A, const double* B, double* C) {  // A B^T
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      C[i * 3 + j] = A[i * 3 + 0] * B[j * 3 + 0] + A[i * 3 + 1] * B[j * 3 + 1] + A[i * 3 + 2] * B[j * 3 + 2];
+}
+__device__ __forceinline__ void mat3_Tmul(const double* A, const double* B, double* C) {  // A^T B
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      C[i * 3 + j] = A[0 * 3 + i] * B[0 * 3 + j] + A[1 * 3 + i] * B[1 * 3 + j] + A[2 * 3 + i] * B[2 * 3 + j];
+}
+__device__ __forceinline__ void mat3_vec(const double* A, const double* x, double* y) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) y[i] = A[i * 3 + 0] * x[0] + A[i * 3 + 1] * x[1] + A[i * 3 + 2] * x[2];
+}
+__device__ __forceinline__ void mat3T_vec(const double* A, const double* x, double* y) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) y[i] = A[0 * 3 + i] * x[0] + A[1 * 3 + i] * x[1] + A[2 * 3 + i] * x[2];
+}
+__device__ __forceinline__ void hat3(const double* v, double* H) {
+  H[0] = 0.0;   H[1] = -v[2]; H[2] = v[1];
+  H[3] = v[2];  H[4] = 0.0;   H[5] = -v[0];
+  H[6] = -v[1]; H[7] = v[0];  H[8] = 0.0;
+}
+__device__ __forceinline__ void qmat(const double* q, double* R) {  // geometry.py:151-157
+  const double w = q[0], x = q[1], y = q[2], z = q[3];
+  R[0] = 1 - 2 * (y * y + z * z); R[1] = 2 * (x * y - w * z);     R[2] = 2 * (x * z + w * y);
+  R[3] = 2 * (x * y + w * z);     R[4] = 1 - 2 * (x * x + z * z); R[5] = 2 * (y * z - w * x);
+  R[6] = 2 * (x * z - w * y);     R[7] = 2 * (y * z + w * x);     R[8] = 1 - 2 * (x * x + y * y);
+}
+__device__ __forceinline__ void qcanon(double* q) {  // geometry.py:94-98
+  const double n = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+  const double s = (q[0] / n < 0.0) ? -1.0 : 1.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) q[k] = s * (q[k] / n);
+}
+__device__ __forceinline__ void qmul(const double* a, const double* b, double* o) {  // geometry.py:83-91
+  o[0] = a[0] * b[0] - a[1] * b[1] - a[2] * b[2] - a[3] * b[3];
+  o[1] = a[0] * b[1] + a[1] * b[0] + a[2] * b[3] - a[3] * b[2];
+  o[2] = a[0] * b[2] - a[1] * b[3] + a[2] * b[0] + a[3] * b[1];
+  o[3] = a[0] * b[3] + a[1] * b[2] - a[2] * b[1] + a[3] * b[0];
+}
+__device__ __forceinline__ void qexp(const double* w, double* q) {  // geometry.py:113-123
+  const double th = sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+  if (th < kSmallAngle) {
+    q[0] = 1.0; q[1] = 0.5 * w[0]; q[2] = 0.5 * w[1]; q[3] = 0.5 * w[2];
+  } else {
+    double s, c;
+    sincos(0.5 * th, &s, &c);
+    q[0] = c; q[1] = s * (w[0] / th); q[2] = s * (w[1] / th); q[3] = s * (w[2] / th);
+  }
+  qcanon(q);
+}
+__device__ __forceinline__ void so3_exp(const double* w, double* R) {  // geometry.py:33-43
+  const double th = sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+  double K[9], K2[9];
+  hat3(w, K);
+  mat3_mul(K, K, K2);
+  double a, b;
+  if (th < kSmallAngle) { a = 1.0; b = 0.5; }
+  else { a = sin(th) / th; b = (1.0 - cos(th)) / (th * th); }
+#pragma unroll
+  for (int k = 0; k < 9; ++k) R[k] = ((k % 4) == 0 ? 1.0 : 0.0) + a * K[k] + b * K2[k];
+}
+__device__ __forceinline__ void so3_jr(const double* w, double* J) {  // geometry.py:57-67
+  const double th = sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+  double K[9], K2[9];
+  hat3(w, K);
+  mat3_mul(K, K, K2);
+  double a, b;
+  if (th < kSmallAngle) { a = 0.5; b = 1.0 / 6.0; }
+  else { const double t2 = th * th; a = (1.0 - cos(th)) / t2; b = (th - sin(th)) / (t2 * th); }
+#pragma unroll
+  for (int k = 0; k < 9; ++k) J[k] = ((k % 4) == 0 ? 1.0 : 0.0) - a * K[k] + b * K2[k];
+}
+__device__ __forceinline__ void so3_jr_inv(const double* w, double* J) {  // geometry.py:70-80
+  const double th = sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+  double K[9], K2[9];
+  hat3(w, K);
+  mat3_mul(K, K, K2);
+  double b;
+  if (th < kSmallAngle) b = 1.0 / 12.0;
+  else b = (1.0 / (th * th)) * (1.0 - th * (1.0 / tan(0.5 * th)) / 2.0);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) J[k] = ((k % 4) == 0 ? 1.0 : 0.0) + 0.5 * K[k] + b * K2[k];
+}
+__device__ __forceinline__ void q_from_mat(const double* R, double* q) {  // geometry.py:125-149
+  const double t = R[0] + R[4] + R[8];
+  if (t > 0.0) {
+    const double s = sqrt(t + 1.0) * 2.0;
+    q[0] = 0.25 * s; q[1] = (R[7] - R[5]) / s; q[2] = (R[2] - R[6]) / s; q[3] = (R[3] - R[1]) / s;
+  } else {
+    int i = 0;
+    if (R[4] > R[0]) i = 1;
+    if (R[8] > R[i * 4]) i = 2;
+    if (i == 0) {
+      const double s = sqrt(1.0 + R[0] - R[4] - R[8]) * 2.0;
+      q[0] = (R[7] - R[5]) / s; q[1] = 0.25 * s; q[2] = (R[1] + R[3]) / s; q[3] = (R[2] + R[6]) / s;
+    } else if (i == 1) {
+      const double s = sqrt(1.0 + R[4] - R[0] - R[8]) * 2.0;
+      q[0] = (R[2] - R[6]) / s; q[1] = (R[1] + R[3]) / s; q[2] = 0.25 * s; q[3] = (R[5] + R[7]) / s;
+    } else {
+      const double s = sqrt(1.0 + R[8] - R[0] - R[4]) * 2.0;
+      q[0] = (R[3] - R[1]) / s; q[1] = (R[2] + R[6]) / s; q[2] = (R[5] + R[7]) / s; q[3] = 0.25 * s;
+    }
+  }
+  qcanon(q);
+}
+__device__ __forceinline__ void qlog(const double* q, double* w) {  // geometry.py:159-167
+  const double n = sqrt(q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+  if (n < kSmallAngle) {
+    const double s = 2.0 / q[0];
+    w[0] = s * q[1]; w[1] = s * q[2]; w[2] = s * q[3];
+  } else {
+    const double s = 2.0 * atan2(n, q[0]) / n;
+    w[0] = s * q[1]; w[1] = s * q[2]; w[2] = s * q[3];
+  }
+}
+
+// G matrices of the factorised vision Jacobian:
+//   J_i = K G_i,  J_j = -K G_j,  K = [P[X_j]x | -P]
+//   G_i = [[A R_i, 0], [-[c1]x A R_i, A]],  G_j = [[R_bc^T, 0], [-[c2]x R_bc^T, A]]
+__device__ __forceinline__ void build_G(const double* R3, const double* c, const double* A, double* G) {
+  double H[9], HR[9];
+  hat3(c, H);
+  mat3_mul(H, R3, HR);
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      G[r * 6 + k] = R3[r * 3 + k];
+      G[r * 6 + 3 + k] = 0.0;
+      G[(3 + r) * 6 + k] = -HR[r * 3 + k];
+      G[(3 + r) * 6 + 3 + k] = A[r * 3 + k];
+    }
+}
+
+// warp-level reduce-scatter of 32 per-lane values: afterwards lane l holds
+// sum over the warp of v[l] (31 shuffles instead of 160 for a naive butterfly).
+__device__ __forceinline__ float warp_reduce_scatter32(float (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const float keep = up ? v[i + o] : v[i];
+      const float send = up ? v[i] : v[i + o];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  return v[0];
+}
+
+}  // namespace vba
+
+// ---------------------------------------------------------------------------
+// launchers (defined in the .cu files, used by the host runtime)
+// ---------------------------------------------------------------------------
+namespace vba {
+
+struct DevState {      // one side of the double-buffered solver state
+  double* state;       // [K,16]
+  float* disp;         // [n_disp_pad]
+  double* grav;        // [5]
+  EdgeGeo32* geo32;    // [E]
+  double* geo64;       // [E, kGeo64]
+};
+
+void launch_edge_prep(const DevState& s, const int32_t* ei, const int32_t* ej, int E, const Extr& x,
+                      cudaStream_t st);
+void launch_vision_linearize(int pixel_mode, const PixTile* tiles, int ntiles, const DevState& s,
+                             const float* pix, const float* tgt, const float* wts, const int64_t* eoff,
+                             const int64_t* doff, int grid_w, const double* grid, const double* intr,
+                             double* partials, float* Hdd, float* gd, cudaStream_t st);
+void launch_vision_energy(int pixel_mode, const PixTile* tiles, int ntiles, const DevState& s,
+                          const float* pix, const float* tgt, const float* wts, const int64_t* eoff,
+                          const int64_t* doff, int grid_w, const double* grid, const double* intr,
+                          double* tile_energy, cudaStream_t st);
+void launch_edge_finalize(const int32_t* esrc_tile0, const int32_t* esrc_tile1, const PixTile* tiles,
+                          const int32_t* edge_i, int E, const double* partials, const DevState& s,
+                          const Extr& x, double* visblocks, double* edge_energy, cudaStream_t st);
+void launch_gram(int pixel_mode, const GramTile* gt, int ngt, int block, size_t smem, int kmax,
+                 const DevState& s, const float* pix, const float* wts, const int64_t* eoff,
+                 const int64_t* doff, int grid_w, const double* grid, const double* intr,
+                 const float* Hdd, const float* gd, double lam, double ridge, double* gram_part,
+                 cudaStream_t st);
+void launch_gram_reduce(const int32_t* src_list, int nsrc, const int32_t* src_gt0, const int32_t* src_gt1,
+                        const GramTile* gt, const int32_t* src_eb, const int32_t* src_ee,
+                        const int64_t* src_gram_off, const double* gram_part, double* gram,
+                        cudaStream_t st);
+void launch_fill_transform(const int32_t* src_list, int nsrc, const int32_t* src_eb, const int32_t* src_ee,
+                           const int64_t* src_gram_off, const int64_t* src_fill_off, const double* gram,
+                           const DevState& s, const Extr& x, double* fill, int kmax, cudaStream_t st);
+void launch_step_edges(const int32_t* ei, const int32_t* ej, int E, const DevState& s, const Extr& x,
+                       const double* dx_full, int sdof, float* ustep, cudaStream_t st);
+size_t gram_smem_bytes(int kmax, int nsplit, int npairs, int k);
+void launch_backsub(int pixel_mode, const PixTile* tiles, int ntiles, const DevState& cur, const DevState& nxt,
+                    const float* pix, const float* wts, const int64_t* eoff, const int64_t* doff, int grid_w,
+                    const double* grid, const double* intr, const float* Hdd, const float* gd,
+                    const float* ustep, double lam, double ridge, float* dxd_out,
+                    unsigned long long* step_max_bits, cudaStream_t st);
+void launch_retract(const DevState& cur, const DevState& nxt, const double* dx_full, const int32_t* frozen,
+                    int K, int sdof, int ngrav, int n_state, unsigned long long* step_max_bits,
+                    int npv, cudaStream_t st);
+void launch_energy_reduce(const double* tile_energy, int ntiles, const double* imu_blocks, int F, int ibs,
+                          int energy_off, double* out3, cudaStream_t st);
+// IMU
+void launch_imu_prep(const double* imu, int F, double* Lbuf, int* status, cudaStream_t st);
+void launch_imu_factor(const double* imu, const double* Lbuf, const int32_t* fi, const int32_t* fj, int F,
+                       const DevState& s, const double* ts, int sdof, int ibs, int energy_only,
+                       double* imu_blocks, cudaStream_t st);
+// dense
+void launch_assemble(const int32_t* blk_ptr, const int32_t* blk_nff, const Contrib* contribs, int nblk_rows,
+                     const int32_t* blk_row_off, const int32_t* blk_dim, const double* arena, double lam,
+                     double ridge, int add_ridge, double* H, int64_t ld, int symmetric_out, cudaStream_t st);
+void launch_assemble_vec(const int32_t* seg_ptr, const Vec* vecs, int nseg, const int32_t* seg_off,
+                         const double* arena, double scale, double* g, cudaStream_t st);
+void launch_add_ridge(double* H, int64_t ld, int n, double ridge, cudaStream_t st);
+void launch_pad_identity(double* H, int64_t ld, int n, int npad, double* rhs, cudaStream_t st);
+int chol_solve(double* H, int64_t ld, int npad, double* rhs, double* x, double* Ldiag, int* status,
+               cudaStream_t st);
+void launch_scatter_dx(const double* x, const int32_t* free_map, int npv, double* dx_full, cudaStream_t st);
+void launch_export_hpd(int mode, const int32_t* seb, const int32_t* see, const int64_t* doff, const int64_t* roff,
+                       const int32_t* npix, int maxpix, const int32_t* ej, int K, const DevState& s, const Extr& x,
+                       const float* pix, const float* wts, const int64_t* eoff, int grid_w, const double* grid,
+                       const double* intr, int sdof, int64_t ncol, double* H, cudaStream_t st);
+void launch_unpad(const float* src, const int64_t* doff, const int64_t* roff, const int32_t* npix, int maxpix, int K,
+                  double* dst, cudaStream_t st);
+void launch_count();   // instrumentation hook
+int64_t launch_total();
+
+}  // namespace vba

@@ -1,0 +1,1096 @@
+// vba_vision.cu — per-pixel vision kernels of the dense VI-BA (sm_100a).
+//
+// Restates the vision factor of residuals.py:172-263 and the vision part of
+// solver.py:173-220 / 276-290 (paths relative to /root/reference/pkg/src/vislam/)
+// in the factorised form documented in DESIGN.md §4.1:
+//
+//   X_h = M ray + d t            (= d * X_j, camera-j point scaled by the disparity)
+//   J_i = K G_i,  J_j = -K G_j,  J_d = -P t / d
+//   K   = [P [X_j]x | -P]  (2x6),  rows K0 = fx k0', K1 = fy k1'
+//
+// so each edge-pixel accumulates ONE 6x6 symmetric K-space Gram, a 6-vector
+// gradient and two per-pixel scalars; the 6x6 -> pose-space transforms happen
+// once per edge in fp64 (k_edge_finalize).  Per-pixel math is fp32, sums over
+// <= 256 edge-pixels are fp32 (8 sequential + 5-level tree), everything
+// beyond is fp64 with a fixed reduction order (bitwise deterministic).
+#include <cuda_runtime.h>
+
+#include "vba_internal.cuh"
+
+namespace vba {
+
+static int64_t g_launches = 0;
+void launch_count() { ++g_launches; }
+int64_t launch_total() { return g_launches; }
+
+constexpr int kPixBlock = 128;   // threads of the per-pixel kernels
+constexpr int kTP = 4;           // pixel pairs per thread (8 pixels)
+constexpr int kTile = 2 * kTP * kPixBlock;
+constexpr int kGramPC = 32;      // pixels per Gram staging chunk
+constexpr int kGramStride = 12;  // floats per (pixel, edge) in the Gram stage: u[6] v[6]
+
+struct GridP { double ox, oy, sx, sy; };
+
+// Gram stage pixel stride (floats): a multiple of 4 with an odd quad count, so
+// quarter-warp float4 accesses of consecutive pixels hit distinct bank groups.
+__host__ __device__ __forceinline__ int gram_px_stride(int kmax) {
+  const int s = kGramStride * kmax;
+  return ((s / 4) & 1) ? s : s + 4;
+}
+
+size_t gram_smem_bytes(int kmax, int nsplit, int npairs, int k) {
+  return (size_t)kGramPC * gram_px_stride(kmax) * 4 + kGramPC * 4 +
+         (size_t)nsplit * (npairs * 36 + k * 6) * 8;
+}
+struct IntrP { double fx, fy, cx, cy; };
+
+// ray (fp64 -> fp32) of pixel n of a keyframe segment
+template <int MODE>
+__device__ __forceinline__ void load_rays(const float* __restrict__ pix, int64_t kbase, int n, int grid_w,
+                                          const GridP& gp, const IntrP& in, float& rx0, float& ry0,
+                                          float& rx1, float& ry1) {
+  double u0, v0, u1, v1;
+  if (MODE == VBA_PIX_GRID) {
+    const int c0 = n % grid_w, r0 = n / grid_w;
+    const int c1 = (n + 1) % grid_w, r1 = (n + 1) / grid_w;
+    u0 = gp.ox + gp.sx * c0; v0 = gp.oy + gp.sy * r0;
+    u1 = gp.ox + gp.sx * c1; v1 = gp.oy + gp.sy * r1;
+  } else {
+    const float4 p = __ldg(reinterpret_cast<const float4*>(pix + 2 * (kbase + n)));
+    u0 = p.x; v0 = p.y; u1 = p.z; v1 = p.w;
+  }
+  rx0 = (float)((u0 - in.cx) / in.fx); ry0 = (float)((v0 - in.cy) / in.fy);
+  rx1 = (float)((u1 - in.cx) / in.fx); ry1 = (float)((v1 - in.cy) / in.fy);
+}
+
+struct PxGeom {  // per edge-pixel projection at the current estimate
+  float x, y, dx, dy, iz, izh;
+  bool valid;
+};
+
+// Displacement form of the reprojection.  With X_h = d X_j = ray + D,
+// D = (M - I) ray + d t (ray.z = 1):
+//   x = (rx + Dx) / (1 + Dz),   x - rx = (Dx - rx Dz) / (1 + Dz)
+// so the residual  r = u* - (cx + fx x) = flow - fx (x - rx)  only involves
+// the displacement, whose fp32 rounding error scales with the flow instead of
+// the absolute pixel coordinate (flow = u* - u is stored per row).
+__device__ __forceinline__ PxGeom project(const EdgeGeo32& g, float rx, float ry, float d) {
+  const float Dx = fmaf(d, g.t[0], fmaf(g.M[0], rx, fmaf(g.M[1], ry, g.M[2])));
+  const float Dy = fmaf(d, g.t[1], fmaf(g.M[3], rx, fmaf(g.M[4], ry, g.M[5])));
+  const float Dz = fmaf(d, g.t[2], fmaf(g.M[6], rx, fmaf(g.M[7], ry, g.M[8])));
+  const float Xz = 1.0f + Dz;
+  PxGeom o;
+  o.valid = Xz > 1e-6f * d;                // z_j = Xz / d > 1e-6  (residuals.py:206-209)
+  o.izh = o.valid ? 1.0f / Xz : 0.0f;      // invalid pixels: finite zeros, weight 0
+  o.dx = fmaf(-rx, Dz, Dx) * o.izh;
+  o.dy = fmaf(-ry, Dz, Dy) * o.izh;
+  o.x = rx + o.dx;
+  o.y = ry + o.dy;
+  o.iz = d * o.izh;
+  return o;
+}
+
+__device__ __forceinline__ EdgeGeo32 load_geo(const EdgeGeo32* __restrict__ geo, int e) {
+  const float4* p = reinterpret_cast<const float4*>(geo + e);
+  const float4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+  EdgeGeo32 g;
+  g.M[0] = a.x; g.M[1] = a.y; g.M[2] = a.z; g.M[3] = a.w;
+  g.M[4] = b.x; g.M[5] = b.y; g.M[6] = b.z; g.M[7] = b.w;
+  g.M[8] = c.x; g.t[0] = c.y; g.t[1] = c.z; g.t[2] = c.w;
+  return g;
+}
+
+// ---------------------------------------------------------------------------
+// per-edge geometry (fp64 -> fp32 constants), one thread per edge
+// ---------------------------------------------------------------------------
+__global__ void k_edge_prep(const double* __restrict__ state, const int32_t* __restrict__ ei,
+                            const int32_t* __restrict__ ej, int E, Extr x, EdgeGeo32* __restrict__ g32,
+                            double* __restrict__ g64) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const double* si = state + 16 * ei[e];
+  const double* sj = state + 16 * ej[e];
+  double Ri[9], Rj[9], A[9], ARi[9], M[9];
+  qmat(si, Ri);
+  qmat(sj, Rj);
+  mat3_mulT(x.RbcT, Rj, A);            // A = R_bc^T R_j^T            (residuals.py:202)
+  mat3_mul(A, Ri, ARi);
+  mat3_mul(ARi, x.Rbc, M);             // camera i -> camera j rotation
+  double dp[3] = {si[4] - sj[4], si[5] - sj[5], si[6] - sj[6]};
+  double t1[3], t2[3], t3[3];
+  mat3_vec(ARi, x.pbc, t1);
+  mat3_vec(A, dp, t2);
+  mat3_vec(x.RbcT, x.pbc, t3);
+  EdgeGeo32 o;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) o.M[k] = (float)(M[k] - ((k % 4) == 0 ? 1.0 : 0.0));   // M - I, exact small part
+#pragma unroll
+  for (int k = 0; k < 3; ++k) o.t[k] = (float)(t1[k] + t2[k] - t3[k]);
+  o.pad[0] = o.pad[1] = o.pad[2] = o.pad[3] = 0.f;
+  g32[e] = o;
+  double* q = g64 + (int64_t)kGeo64 * e;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) { q[k] = ARi[k]; q[9 + k] = A[k]; }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) q[18 + k] = -t2[k] + t3[k];   // c1 = A(p_j - p_i) + R_bc^T p_bc
+}
+
+void launch_edge_prep(const DevState& s, const int32_t* ei, const int32_t* ej, int E, const Extr& x,
+                      cudaStream_t st) {
+  if (E <= 0) return;
+  k_edge_prep<<<(E + 127) / 128, 128, 0, st>>>(s.state, ei, ej, E, x, s.geo32, s.geo64);
+  launch_count();
+}
+
+// ---------------------------------------------------------------------------
+// K1: vision linearisation.  One CTA per (source keyframe, 1024-pixel tile),
+// looping over the source's out-edges.  Per (tile, edge) it writes a 32-double
+// partial: 21 upper-triangular entries of S = sum w K^T K, 6 of s = sum w K^T r,
+// and the edge energy; per pixel it writes H_dd and g_d (sum over out-edges).
+// ---------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(kPixBlock) k_vision_linearize(
+    const PixTile* __restrict__ tiles, const float* __restrict__ disp, const EdgeGeo32* __restrict__ geo,
+    const float* __restrict__ pix, const float* __restrict__ tgt, const float* __restrict__ wts,
+    const int64_t* __restrict__ eoff, const int64_t* __restrict__ doff, int grid_w, GridP gp, IntrP in,
+    double* __restrict__ partials, float* __restrict__ Hdd, float* __restrict__ gdo) {
+  __shared__ double red[2][kPixBlock / 32][32];
+  const PixTile T = tiles[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t kbase = doff[T.src];
+  const float fx = (float)in.fx, fy = (float)in.fy;
+  const float fx2 = fx * fx, fy2 = fy * fy;
+
+  float rx[2 * kTP], ry[2 * kTP], dd[2 * kTP], hdd[2 * kTP], gdd[2 * kTP];
+  bool act[kTP];
+#pragma unroll
+  for (int m = 0; m < kTP; ++m) {
+    const int p = m * kPixBlock + tid;
+    const int n = T.n0 + 2 * p;
+    act[m] = 2 * p < T.cnt;
+    rx[2 * m] = ry[2 * m] = rx[2 * m + 1] = ry[2 * m + 1] = 0.f;
+    dd[2 * m] = dd[2 * m + 1] = 1.f;
+    if (act[m]) {
+      const float2 d2 = __ldg(reinterpret_cast<const float2*>(disp + kbase + n));
+      dd[2 * m] = d2.x;
+      dd[2 * m + 1] = d2.y;
+      if (MODE != VBA_PIX_EDGE)
+        load_rays<MODE>(pix, kbase, n, grid_w, gp, in, rx[2 * m], ry[2 * m], rx[2 * m + 1], ry[2 * m + 1]);
+    }
+    hdd[2 * m] = hdd[2 * m + 1] = gdd[2 * m] = gdd[2 * m + 1] = 0.f;
+  }
+
+  for (int e = T.eb; e < T.ee; ++e) {
+    const EdgeGeo32 g = load_geo(geo, e);
+    const int64_t rbase = eoff[e] + T.n0;
+    float acc[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) acc[k] = 0.f;
+    float4 tt[kTP], ww[kTP];
+#pragma unroll
+    for (int m = 0; m < kTP; ++m) {
+      const int p = m * kPixBlock + tid;
+      tt[m] = make_float4(0.f, 0.f, 0.f, 0.f);
+      ww[m] = tt[m];
+      if (act[m]) {
+        tt[m] = __ldcs(reinterpret_cast<const float4*>(tgt + 2 * (rbase + 2 * p)));
+        ww[m] = __ldcs(reinterpret_cast<const float4*>(wts + 2 * (rbase + 2 * p)));
+        if (MODE == VBA_PIX_EDGE)
+          load_rays<VBA_PIX_KF>(pix, rbase - T.n0, T.n0 + 2 * p, grid_w, gp, in, rx[2 * m], ry[2 * m],
+                                rx[2 * m + 1], ry[2 * m + 1]);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < kTP; ++m) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int q = 2 * m + h;
+        const PxGeom o = project(g, rx[q], ry[q], dd[q]);
+        const float tu = h ? tt[m].z : tt[m].x, tv = h ? tt[m].w : tt[m].y;
+        float w0 = h ? ww[m].z : ww[m].x, w1 = h ? ww[m].w : ww[m].y;
+        w0 = o.valid ? w0 : 0.f;
+        w1 = o.valid ? w1 : 0.f;
+        const float r0 = fmaf(-fx, o.dx, tu);    // flow - fx (x - rx)
+        const float r1 = fmaf(-fy, o.dy, tv);
+        const float xy = o.x * o.y;
+        const float a1 = -fmaf(o.x, o.x, 1.f);     // k0' = [xy, -(1+x^2), y, -iz, 0, x iz]
+        const float a5 = o.x * o.iz;
+        const float b0 = fmaf(o.y, o.y, 1.f);      // k1' = [1+y^2, -xy, -x, 0, -iz, y iz]
+        const float b5 = o.y * o.iz;
+        const float jd0 = fmaf(o.x, g.t[2], -g.t[0]) * o.izh;   // J_d = (fx jd0', fy jd1')
+        const float jd1 = fmaf(o.y, g.t[2], -g.t[1]) * o.izh;
+        const float W0 = w0 * fx2, W1 = w1 * fy2;
+        const float R0 = w0 * fx * r0, R1 = w1 * fy * r1;
+        // weighted rows
+        const float p0 = W0 * xy, p1 = W0 * a1, p2 = W0 * o.y, p3 = -W0 * o.iz, p5 = W0 * a5;
+        const float q0 = W1 * b0, q1 = -W1 * xy, q2 = -W1 * o.x, q4 = -W1 * o.iz, q5 = W1 * b5;
+        // S += W0 k0' k0'^T + W1 k1' k1'^T (upper triangle, structural zeros skipped)
+        acc[0] = fmaf(p0, xy, fmaf(q0, b0, acc[0]));
+        acc[1] = fmaf(p0, a1, fmaf(q0, -xy, acc[1]));
+        acc[2] = fmaf(p0, o.y, fmaf(q0, -o.x, acc[2]));
+        acc[3] = fmaf(p0, -o.iz, acc[3]);
+        acc[4] = fmaf(q0, -o.iz, acc[4]);
+        acc[5] = fmaf(p0, a5, fmaf(q0, b5, acc[5]));
+        acc[6] = fmaf(p1, a1, fmaf(q1, -xy, acc[6]));
+        acc[7] = fmaf(p1, o.y, fmaf(q1, -o.x, acc[7]));
+        acc[8] = fmaf(p1, -o.iz, acc[8]);
+        acc[9] = fmaf(q1, -o.iz, acc[9]);
+        acc[10] = fmaf(p1, a5, fmaf(q1, b5, acc[10]));
+        acc[11] = fmaf(p2, o.y, fmaf(q2, -o.x, acc[11]));
+        acc[12] = fmaf(p2, -o.iz, acc[12]);
+        acc[13] = fmaf(q2, -o.iz, acc[13]);
+        acc[14] = fmaf(p2, a5, fmaf(q2, b5, acc[14]));
+        acc[15] = fmaf(p3, -o.iz, acc[15]);
+        acc[17] = fmaf(p3, a5, acc[17]);
+        acc[18] = fmaf(q4, -o.iz, acc[18]);
+        acc[19] = fmaf(q4, b5, acc[19]);
+        acc[20] = fmaf(p5, a5, fmaf(q5, b5, acc[20]));
+        // s += w0 fx r0 k0' + w1 fy r1 k1'
+        acc[21] = fmaf(R0, xy, fmaf(R1, b0, acc[21]));
+        acc[22] = fmaf(R0, a1, fmaf(R1, -xy, acc[22]));
+        acc[23] = fmaf(R0, o.y, fmaf(R1, -o.x, acc[23]));
+        acc[24] = fmaf(R0, -o.iz, acc[24]);
+        acc[25] = fmaf(R1, -o.iz, acc[25]);
+        acc[26] = fmaf(R0, a5, fmaf(R1, b5, acc[26]));
+        acc[27] = fmaf(w0 * r0, r0, fmaf(w1 * r1, r1, acc[27]));
+        // per-pixel disparity block and gradient (summed over out-edges)
+        hdd[q] = fmaf(W0 * jd0, jd0, fmaf(W1 * jd1, jd1, hdd[q]));
+        gdd[q] = fmaf(R0, jd0, fmaf(R1, jd1, gdd[q]));
+      }
+    }
+    const float v = warp_reduce_scatter32(acc);
+    const int buf = (e - T.eb) & 1;
+    red[buf][warp][lane] = (double)v;
+    __syncthreads();
+    if (warp == 0) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < kPixBlock / 32; ++w) s += red[buf][w][lane];
+      partials[(T.poff + (e - T.eb)) * kPartStride + lane] = s;
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < kTP; ++m) {
+    if (!act[m]) continue;
+    const int64_t n = kbase + T.n0 + 2 * (m * kPixBlock + tid);
+    *reinterpret_cast<float2*>(Hdd + n) = make_float2(hdd[2 * m], hdd[2 * m + 1]);
+    *reinterpret_cast<float2*>(gdo + n) = make_float2(gdd[2 * m], gdd[2 * m + 1]);
+  }
+}
+
+void launch_vision_linearize(int mode, const PixTile* tiles, int ntiles, const DevState& s, const float* pix,
+                             const float* tgt, const float* wts, const int64_t* eoff, const int64_t* doff,
+                             int grid_w, const double* grid, const double* intr, double* partials, float* Hdd,
+                             float* gd, cudaStream_t st) {
+  if (ntiles <= 0) return;
+  GridP gp{grid[0], grid[1], grid[2], grid[3]};
+  IntrP in{intr[0], intr[1], intr[2], intr[3]};
+  if (mode == VBA_PIX_GRID)
+    k_vision_linearize<VBA_PIX_GRID><<<ntiles, kPixBlock, 0, st>>>(tiles, s.disp, s.geo32, pix, tgt, wts, eoff,
+                                                                   doff, grid_w, gp, in, partials, Hdd, gd);
+  else if (mode == VBA_PIX_KF)
+    k_vision_linearize<VBA_PIX_KF><<<ntiles, kPixBlock, 0, st>>>(tiles, s.disp, s.geo32, pix, tgt, wts, eoff,
+                                                                 doff, grid_w, gp, in, partials, Hdd, gd);
+  else
+    k_vision_linearize<VBA_PIX_EDGE><<<ntiles, kPixBlock, 0, st>>>(tiles, s.disp, s.geo32, pix, tgt, wts, eoff,
+                                                                   doff, grid_w, gp, in, partials, Hdd, gd);
+  launch_count();
+}
+
+// ---------------------------------------------------------------------------
+// K2: vision energy sum w r^2 (residual-only pass).  One fp64 partial per tile.
+// ---------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(kPixBlock) k_vision_energy(
+    const PixTile* __restrict__ tiles, const float* __restrict__ disp, const EdgeGeo32* __restrict__ geo,
+    const float* __restrict__ pix, const float* __restrict__ tgt, const float* __restrict__ wts,
+    const int64_t* __restrict__ eoff, const int64_t* __restrict__ doff, int grid_w, GridP gp, IntrP in,
+    double* __restrict__ tile_energy) {
+  __shared__ double red[kPixBlock / 32];
+  const PixTile T = tiles[blockIdx.x];
+  const int tid = threadIdx.x;
+  const int64_t kbase = doff[T.src];
+  const float fx = (float)in.fx, fy = (float)in.fy;
+  float rx[2 * kTP], ry[2 * kTP], dd[2 * kTP];
+  bool act[kTP];
+#pragma unroll
+  for (int m = 0; m < kTP; ++m) {
+    const int p = m * kPixBlock + tid;
+    const int n = T.n0 + 2 * p;
+    act[m] = 2 * p < T.cnt;
+    rx[2 * m] = ry[2 * m] = rx[2 * m + 1] = ry[2 * m + 1] = 0.f;
+    dd[2 * m] = dd[2 * m + 1] = 1.f;
+    if (act[m]) {
+      const float2 d2 = __ldg(reinterpret_cast<const float2*>(disp + kbase + n));
+      dd[2 * m] = d2.x;
+      dd[2 * m + 1] = d2.y;
+      if (MODE != VBA_PIX_EDGE)
+        load_rays<MODE>(pix, kbase, n, grid_w, gp, in, rx[2 * m], ry[2 * m], rx[2 * m + 1], ry[2 * m + 1]);
+    }
+  }
+  double etot = 0.0;
+  for (int e = T.eb; e < T.ee; ++e) {
+    const EdgeGeo32 g = load_geo(geo, e);
+    const int64_t rbase = eoff[e] + T.n0;
+    float4 tt[kTP], ww[kTP];
+#pragma unroll
+    for (int m = 0; m < kTP; ++m) {
+      const int p = m * kPixBlock + tid;
+      tt[m] = make_float4(0.f, 0.f, 0.f, 0.f);
+      ww[m] = tt[m];
+      if (act[m]) {
+        tt[m] = __ldcs(reinterpret_cast<const float4*>(tgt + 2 * (rbase + 2 * p)));
+        ww[m] = __ldcs(reinterpret_cast<const float4*>(wts + 2 * (rbase + 2 * p)));
+        if (MODE == VBA_PIX_EDGE)
+          load_rays<VBA_PIX_KF>(pix, rbase - T.n0, T.n0 + 2 * p, grid_w, gp, in, rx[2 * m], ry[2 * m],
+                                rx[2 * m + 1], ry[2 * m + 1]);
+      }
+    }
+    float ee = 0.f;
+#pragma unroll
+    for (int m = 0; m < kTP; ++m) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int q = 2 * m + h;
+        const PxGeom o = project(g, rx[q], ry[q], dd[q]);
+        const float tu = h ? tt[m].z : tt[m].x, tv = h ? tt[m].w : tt[m].y;
+        float w0 = h ? ww[m].z : ww[m].x, w1 = h ? ww[m].w : ww[m].y;
+        w0 = o.valid ? w0 : 0.f;
+        w1 = o.valid ? w1 : 0.f;
+        const float r0 = fmaf(-fx, o.dx, tu);    // flow - fx (x - rx)
+        const float r1 = fmaf(-fy, o.dy, tv);
+        ee = fmaf(w0 * r0, r0, fmaf(w1 * r1, r1, ee));
+      }
+    }
+    etot += (double)ee;
+  }
+  // fixed-order block reduction
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) etot += __shfl_xor_sync(0xffffffffu, etot, o);
+  if ((tid & 31) == 0) red[tid >> 5] = etot;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kPixBlock / 32; ++w) s += red[w];
+    tile_energy[blockIdx.x] = s;
+  }
+}
+
+void launch_vision_energy(int mode, const PixTile* tiles, int ntiles, const DevState& s, const float* pix,
+                          const float* tgt, const float* wts, const int64_t* eoff, const int64_t* doff,
+                          int grid_w, const double* grid, const double* intr, double* tile_energy,
+                          cudaStream_t st) {
+  if (ntiles <= 0) return;
+  GridP gp{grid[0], grid[1], grid[2], grid[3]};
+  IntrP in{intr[0], intr[1], intr[2], intr[3]};
+  if (mode == VBA_PIX_GRID)
+    k_vision_energy<VBA_PIX_GRID><<<ntiles, kPixBlock, 0, st>>>(tiles, s.disp, s.geo32, pix, tgt, wts, eoff,
+                                                                doff, grid_w, gp, in, tile_energy);
+  else if (mode == VBA_PIX_KF)
+    k_vision_energy<VBA_PIX_KF><<<ntiles, kPixBlock, 0, st>>>(tiles, s.disp, s.geo32, pix, tgt, wts, eoff,
+                                                              doff, grid_w, gp, in, tile_energy);
+  else
+    k_vision_energy<VBA_PIX_EDGE><<<ntiles, kPixBlock, 0, st>>>(tiles, s.disp, s.geo32, pix, tgt, wts, eoff,
+                                                                doff, grid_w, gp, in, tile_energy);
+  launch_count();
+}
+
+// ---------------------------------------------------------------------------
+// per-edge finalisation: sum K1 partials over the source's tiles (fixed order),
+// then H_ii = G_i^T S G_i, H_jj = G_j^T S G_j, H_ij = -G_i^T S G_j,
+// g_i = G_i^T s, g_j = -G_j^T s   (fp64; solver.py:201-219 in factorised form)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(64) k_edge_finalize(const int32_t* __restrict__ t0s,
+                                                      const int32_t* __restrict__ t1s,
+                                                      const PixTile* __restrict__ tiles,
+                                                      const int32_t* __restrict__ edge_i,
+                                                      const double* __restrict__ partials,
+                                                      const double* __restrict__ geo64, Extr x,
+                                                      double* __restrict__ vis, double* __restrict__ eng) {
+  __shared__ double v[32], S[36], Gi[36], Gj[36], T1[36], T2[36];
+  const int e = blockIdx.x, tid = threadIdx.x;
+  const int src = edge_i[e];
+  if (tid < 32) {
+    double s = 0.0;
+    for (int t = t0s[src]; t < t1s[src]; ++t)
+      s += partials[(tiles[t].poff + (e - tiles[t].eb)) * kPartStride + tid];
+    v[tid] = s;
+  }
+  if (tid == 32) {
+    const double* q = geo64 + (int64_t)kGeo64 * e;
+    build_G(q, q + 18, q + 9, Gi);           // G_i from (A R_i, c1, A)
+  }
+  if (tid == 33) {
+    const double* q = geo64 + (int64_t)kGeo64 * e;
+    build_G(x.RbcT, x.c2, q + 9, Gj);        // G_j from (R_bc^T, c2, A)
+  }
+  __syncthreads();
+  if (tid < 36) {  // unpack upper triangle -> full symmetric S
+    const int a = tid / 6, b = tid % 6;
+    const int lo = a < b ? a : b, hi = a < b ? b : a;
+    const int idx = lo * 6 - lo * (lo - 1) / 2 + (hi - lo);
+    S[tid] = v[idx];
+  }
+  __syncthreads();
+  if (tid < 36) {
+    const int a = tid / 6, b = tid % 6;
+    double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+    for (int m = 0; m < 6; ++m) {
+      s1 += S[a * 6 + m] * Gi[m * 6 + b];
+      s2 += S[a * 6 + m] * Gj[m * 6 + b];
+    }
+    T1[tid] = s1;
+    T2[tid] = s2;
+  }
+  __syncthreads();
+  double* out = vis + (int64_t)kVisBlock * e;
+  if (tid < 36) {
+    const int a = tid / 6, b = tid % 6;
+    double hii = 0.0, hjj = 0.0, hij = 0.0;
+#pragma unroll
+    for (int m = 0; m < 6; ++m) {
+      hii += Gi[m * 6 + a] * T1[m * 6 + b];
+      hjj += Gj[m * 6 + a] * T2[m * 6 + b];
+      hij += Gi[m * 6 + a] * T2[m * 6 + b];
+    }
+    out[tid] = hii;
+    out[36 + tid] = hjj;
+    out[72 + tid] = -hij;
+  } else if (tid < 48) {
+    const int a = (tid - 36) % 6;
+    const bool isj = tid >= 42;
+    const double* G = isj ? Gj : Gi;
+    double s = 0.0;
+#pragma unroll
+    for (int m = 0; m < 6; ++m) s += G[m * 6 + a] * v[21 + m];
+    out[108 + (isj ? 6 : 0) + a] = isj ? -s : s;
+  } else if (tid == 48 && eng) {
+    eng[e] = v[27];
+  }
+}
+
+void launch_edge_finalize(const int32_t* t0s, const int32_t* t1s, const PixTile* tiles, const int32_t* edge_i,
+                          int E, const double* partials, const DevState& s, const Extr& x, double* vis,
+                          double* eng, cudaStream_t st) {
+  if (E <= 0) return;
+  k_edge_finalize<<<E, 64, 0, st>>>(t0s, t1s, tiles, edge_i, partials, s.geo64, x, vis, eng);
+  launch_count();
+}
+
+// ---------------------------------------------------------------------------
+// K4: Schur fill-in Gram (per LM trial, λ-dependent).
+//   C_{e1 e2} = sum_n k_{n,e1} k_{n,e2}^T / Hdd_d(n),   b_e = sum_n k_{n,e} g_d(n) / Hdd_d(n)
+// with k_{n,e} = sum_c w_c K_c^T J_d,c the per-pixel coupling (K-space).  One CTA per
+// (source, pixel range); pixels are staged PC at a time in shared memory, each
+// thread owns one 6x6 block pair (e1 >= e2) for a pixel split, accumulating fp32
+// over the chunk and fp64 in shared memory across chunks.
+// ---------------------------------------------------------------------------
+template <int MODE>
+__global__ void k_gram(const GramTile* __restrict__ gts, const float* __restrict__ disp,
+                       const EdgeGeo32* __restrict__ geo, const float* __restrict__ pix,
+                       const float* __restrict__ wts, const int64_t* __restrict__ eoff,
+                       const int64_t* __restrict__ doff, int grid_w, GridP gp, IntrP in,
+                       const float* __restrict__ Hdd, const float* __restrict__ gd, double lam, double ridge,
+                       int kmax, double* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const GramTile T = gts[blockIdx.x];
+  const int k = T.ee - T.eb;
+  const int npairs = k * (k + 1) / 2;
+  const int nsplit = T.nsplit;
+  const int S = gram_px_stride(kmax);
+  float* stage = reinterpret_cast<float*>(smem_raw);                  // [PC][S]: per edge u[6] v[6]
+  float* sgd = stage + kGramPC * S;                                   // [PC]
+  double* acc = reinterpret_cast<double*>(sgd + kGramPC);             // [nsplit][npairs][36]
+  double* accb = acc + (int64_t)nsplit * npairs * 36;                 // [nsplit][k][6]
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int64_t kbase = doff[T.src];
+  const float fx = (float)in.fx, fy = (float)in.fy;
+  const float fx2 = fx * fx, fy2 = fy * fy;
+  const double damp = 1.0 + lam;
+
+  for (int i = tid; i < nsplit * (npairs * 36 + k * 6); i += nth) acc[i] = 0.0;
+
+  const int pidx = tid % npairs;
+  const int sp = tid / npairs;
+  const bool active = sp < nsplit;
+  int e1 = (int)((sqrtf(8.f * pidx + 1.f) - 1.f) * 0.5f);
+  while ((e1 + 1) * (e1 + 2) / 2 <= pidx) ++e1;
+  while (e1 * (e1 + 1) / 2 > pidx) --e1;
+  const int e2 = pidx - e1 * (e1 + 1) / 2;
+
+  for (int c0 = T.n0; c0 < T.n1; c0 += kGramPC) {
+    __syncthreads();
+    // phase 1: per-(pixel, edge) coupling vectors u = k, v = k / Hdd_d
+    for (int it = tid; it < kGramPC * k; it += nth) {
+      const int e = it / kGramPC, px = it % kGramPC;
+      const int n = c0 + px;
+      float* dst = stage + px * S + e * kGramStride;
+      float u[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      float inv = 0.f;
+      if (n < T.n1) {
+        const float d = disp[kbase + n];
+        float rx, ry, rx1, ry1;
+        if (MODE == VBA_PIX_EDGE)
+          load_rays<VBA_PIX_KF>(pix, eoff[T.eb + e], n & ~1, grid_w, gp, in, rx, ry, rx1, ry1);
+        else
+          load_rays<MODE>(pix, kbase, n & ~1, grid_w, gp, in, rx, ry, rx1, ry1);
+        if (n & 1) { rx = rx1; ry = ry1; }
+        const EdgeGeo32 g = load_geo(geo, T.eb + e);
+        const PxGeom o = project(g, rx, ry, d);
+        const float2 w = __ldg(reinterpret_cast<const float2*>(wts + 2 * (eoff[T.eb + e] + n)));
+        const float w0 = o.valid ? w.x : 0.f, w1 = o.valid ? w.y : 0.f;
+        const float jd0 = fmaf(o.x, g.t[2], -g.t[0]) * o.izh;
+        const float jd1 = fmaf(o.y, g.t[2], -g.t[1]) * o.izh;
+        const float c0w = w0 * fx2 * jd0, c1w = w1 * fy2 * jd1;
+        const float xy = o.x * o.y;
+        u[0] = fmaf(c0w, xy, c1w * fmaf(o.y, o.y, 1.f));
+        u[1] = fmaf(c0w, -fmaf(o.x, o.x, 1.f), c1w * -xy);
+        u[2] = fmaf(c0w, o.y, c1w * -o.x);
+        u[3] = c0w * -o.iz;
+        u[4] = c1w * -o.iz;
+        u[5] = fmaf(c0w, o.x * o.iz, c1w * (o.y * o.iz));
+        inv = (float)(1.0 / ((double)Hdd[kbase + n] * damp + ridge));
+        if (e == 0) sgd[px] = gd[kbase + n];
+      } else if (e == 0) {
+        sgd[px] = 0.f;
+      }
+      float4* d4 = reinterpret_cast<float4*>(dst);
+      d4[0] = make_float4(u[0], u[1], u[2], u[3]);
+      d4[1] = make_float4(u[4], u[5], u[0] * inv, u[1] * inv);
+      d4[2] = make_float4(u[2] * inv, u[3] * inv, u[4] * inv, u[5] * inv);
+    }
+    __syncthreads();
+    // phase 2: block-pair accumulation
+    if (active) {
+      float a[36];
+#pragma unroll
+      for (int i = 0; i < 36; ++i) a[i] = 0.f;
+      float bb[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      for (int px = sp; px < kGramPC; px += nsplit) {
+        const float* su = stage + px * S + e1 * kGramStride;
+        const float* sv = stage + px * S + e2 * kGramStride + 6;
+        const float4 u03 = *reinterpret_cast<const float4*>(su);
+        const float2 u45 = *reinterpret_cast<const float2*>(su + 4);
+        const float2 v01 = *reinterpret_cast<const float2*>(sv);
+        const float4 v25 = *reinterpret_cast<const float4*>(sv + 2);
+        const float uu[6] = {u03.x, u03.y, u03.z, u03.w, u45.x, u45.y};
+        const float vv[6] = {v01.x, v01.y, v25.x, v25.y, v25.z, v25.w};
+#pragma unroll
+        for (int r = 0; r < 6; ++r)
+#pragma unroll
+          for (int c = 0; c < 6; ++c) a[r * 6 + c] = fmaf(uu[r], vv[c], a[r * 6 + c]);
+        if (e1 == e2) {
+          const float gdn = sgd[px];
+#pragma unroll
+          for (int r = 0; r < 6; ++r) bb[r] = fmaf(vv[r], gdn, bb[r]);
+        }
+      }
+      double* my = acc + ((int64_t)sp * npairs + pidx) * 36;
+#pragma unroll
+      for (int i = 0; i < 36; ++i) my[i] += (double)a[i];
+      if (e1 == e2) {
+        double* mb = accb + ((int64_t)sp * k + e1) * 6;
+#pragma unroll
+        for (int r = 0; r < 6; ++r) mb[r] += (double)bb[r];
+      }
+    }
+  }
+  __syncthreads();
+  double* o = out + T.out;
+  for (int i = tid; i < npairs * 36; i += nth) {
+    double s = 0.0;
+    for (int q = 0; q < nsplit; ++q) s += acc[(int64_t)q * npairs * 36 + i];
+    o[i] = s;
+  }
+  for (int i = tid; i < k * 6; i += nth) {
+    double s = 0.0;
+    for (int q = 0; q < nsplit; ++q) s += accb[(int64_t)q * k * 6 + i];
+    o[npairs * 36 + i] = s;
+  }
+}
+
+void launch_gram(int mode, const GramTile* gt, int ngt, int block, size_t smem, int kmax, const DevState& s,
+                 const float* pix, const float* wts, const int64_t* eoff, const int64_t* doff, int grid_w,
+                 const double* grid, const double* intr, const float* Hdd, const float* gd, double lam,
+                 double ridge, double* gram_part, cudaStream_t st) {
+  if (ngt <= 0) return;
+  GridP gp{grid[0], grid[1], grid[2], grid[3]};
+  IntrP in{intr[0], intr[1], intr[2], intr[3]};
+  if (mode == VBA_PIX_GRID) {
+    cudaFuncSetAttribute(k_gram<VBA_PIX_GRID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_gram<VBA_PIX_GRID><<<ngt, block, smem, st>>>(gt, s.disp, s.geo32, pix, wts, eoff, doff, grid_w, gp, in,
+                                                   Hdd, gd, lam, ridge, kmax, gram_part);
+  } else if (mode == VBA_PIX_KF) {
+    cudaFuncSetAttribute(k_gram<VBA_PIX_KF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_gram<VBA_PIX_KF><<<ngt, block, smem, st>>>(gt, s.disp, s.geo32, pix, wts, eoff, doff, grid_w, gp, in, Hdd,
+                                                 gd, lam, ridge, kmax, gram_part);
+  } else {
+    cudaFuncSetAttribute(k_gram<VBA_PIX_EDGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_gram<VBA_PIX_EDGE><<<ngt, block, smem, st>>>(gt, s.disp, s.geo32, pix, wts, eoff, doff, grid_w, gp, in,
+                                                   Hdd, gd, lam, ridge, kmax, gram_part);
+  }
+  launch_count();
+}
+
+// sum the per-range Gram partials of each source (fixed order)
+__global__ void k_gram_reduce(const int32_t* __restrict__ srcs, const int32_t* __restrict__ g0,
+                              const int32_t* __restrict__ g1, const GramTile* __restrict__ gt,
+                              const int32_t* __restrict__ seb, const int32_t* __restrict__ see,
+                              const int64_t* __restrict__ goff, const double* __restrict__ part,
+                              double* __restrict__ gram) {
+  const int si = blockIdx.x;
+  const int s = srcs[si];
+  const int k = see[s] - seb[s];
+  const int len = k * (k + 1) / 2 * 36 + k * 6;
+  double* o = gram + goff[s];
+  for (int i = threadIdx.x; i < len; i += blockDim.x) {
+    double acc = 0.0;
+    for (int t = g0[s]; t < g1[s]; ++t) acc += part[gt[t].out + i];
+    o[i] = acc;
+  }
+}
+
+void launch_gram_reduce(const int32_t* srcs, int nsrc, const int32_t* g0, const int32_t* g1, const GramTile* gt,
+                        const int32_t* seb, const int32_t* see, const int64_t* goff, const double* part,
+                        double* gram, cudaStream_t st) {
+  if (nsrc <= 0) return;
+  k_gram_reduce<<<nsrc, 256, 0, st>>>(srcs, g0, g1, gt, seb, see, goff, part, gram);
+  launch_count();
+}
+
+// ---------------------------------------------------------------------------
+// fill-in transform (fp64, one CTA per source): K-space Gram -> pose-space blocks
+//   F_ii = sum_{e1,e2} G_{e1,i}^T C_{e1e2} G_{e2,i},  F_{i,j(e)} = -sum_{e1} G_{e1,i}^T C_{e1 e} G_{e,j}
+//   F_{j(e1),j(e2)} = G_{e1,j}^T C_{e1e2} G_{e2,j},   gr_i = sum_e G_{e,i}^T b_e,  gr_{j(e)} = -G_{e,j}^T b_e
+// layout: [F_ii 36][F_ij k*36][F_jj npairs*36][gr_i 6][gr_j k*6]
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double cblk(const double* C, int e1, int e2, int m, int b) {
+  // C(e1,e2)[m][b] with only e1 >= e2 stored
+  if (e1 >= e2) return C[(e1 * (e1 + 1) / 2 + e2) * 36 + m * 6 + b];
+  return C[(e2 * (e2 + 1) / 2 + e1) * 36 + b * 6 + m];
+}
+
+__global__ void k_fill_transform(const int32_t* __restrict__ srcs, const int32_t* __restrict__ seb,
+                                 const int32_t* __restrict__ see, const int64_t* __restrict__ goff,
+                                 const int64_t* __restrict__ foff, const double* __restrict__ gram,
+                                 const double* __restrict__ geo64, Extr x, double* __restrict__ fill) {
+  extern __shared__ double sm[];
+  const int s = srcs[blockIdx.x];
+  const int eb = seb[s], k = see[s] - eb;
+  const int npairs = k * (k + 1) / 2;
+  double* Gi = sm;
+  double* Gj = Gi + k * 36;
+  double* D = Gj + k * 36;
+  const double* C = gram + goff[s];
+  const double* b = C + npairs * 36;
+  double* o = fill + foff[s];
+  const int tid = threadIdx.x, nth = blockDim.x;
+  for (int e = tid; e < k; e += nth) {
+    const double* q = geo64 + (int64_t)kGeo64 * (eb + e);
+    build_G(q, q + 18, q + 9, Gi + e * 36);
+    build_G(x.RbcT, x.c2, q + 9, Gj + e * 36);
+  }
+  __syncthreads();
+  for (int it = tid; it < k * 36; it += nth) {  // D_{e2} = sum_{e1} G_{e1,i}^T C(e1,e2)
+    const int e2 = it / 36, a = (it % 36) / 6, bcol = it % 6;
+    double acc = 0.0;
+    for (int e1 = 0; e1 < k; ++e1)
+#pragma unroll
+      for (int m = 0; m < 6; ++m) acc += Gi[e1 * 36 + m * 6 + a] * cblk(C, e1, e2, m, bcol);
+    D[it] = acc;
+  }
+  __syncthreads();
+  if (tid < 36) {
+    const int a = tid / 6, bc = tid % 6;
+    double acc = 0.0;
+    for (int e = 0; e < k; ++e)
+#pragma unroll
+      for (int m = 0; m < 6; ++m) acc += D[e * 36 + a * 6 + m] * Gi[e * 36 + m * 6 + bc];
+    o[tid] = acc;
+  }
+  for (int it = tid; it < k * 36; it += nth) {
+    const int e = it / 36, a = (it % 36) / 6, bc = it % 6;
+    double acc = 0.0;
+#pragma unroll
+    for (int m = 0; m < 6; ++m) acc += D[e * 36 + a * 6 + m] * Gj[e * 36 + m * 6 + bc];
+    o[36 + it] = -acc;
+  }
+  for (int it = tid; it < npairs * 36; it += nth) {
+    const int p = it / 36, a = (it % 36) / 6, bc = it % 6;
+    int e1 = (int)((sqrt(8.0 * p + 1.0) - 1.0) * 0.5);
+    while ((e1 + 1) * (e1 + 2) / 2 <= p) ++e1;
+    while (e1 * (e1 + 1) / 2 > p) --e1;
+    const int e2 = p - e1 * (e1 + 1) / 2;
+    const double* Cb = C + p * 36;
+    const double* G1 = Gj + e1 * 36;
+    const double* G2 = Gj + e2 * 36;
+    double acc = 0.0;
+#pragma unroll
+    for (int l = 0; l < 6; ++l) {
+      double t = 0.0;
+#pragma unroll
+      for (int m = 0; m < 6; ++m) t += G1[m * 6 + a] * Cb[m * 6 + l];
+      acc += t * G2[l * 6 + bc];
+    }
+    o[36 + k * 36 + it] = acc;
+  }
+  const int goffs = 36 + k * 36 + npairs * 36;
+  if (tid < 6) {
+    double acc = 0.0;
+    for (int e = 0; e < k; ++e)
+#pragma unroll
+      for (int m = 0; m < 6; ++m) acc += Gi[e * 36 + m * 6 + tid] * b[e * 6 + m];
+    o[goffs + tid] = acc;
+  }
+  for (int it = tid; it < k * 6; it += nth) {
+    const int e = it / 6, a = it % 6;
+    double acc = 0.0;
+#pragma unroll
+    for (int m = 0; m < 6; ++m) acc += Gj[e * 36 + m * 6 + a] * b[e * 6 + m];
+    o[goffs + 6 + it] = -acc;
+  }
+}
+
+void launch_fill_transform(const int32_t* srcs, int nsrc, const int32_t* seb, const int32_t* see,
+                           const int64_t* goff, const int64_t* foff, const double* gram, const DevState& s,
+                           const Extr& x, double* fill, int kmax, cudaStream_t st) {
+  if (nsrc <= 0) return;
+  const size_t smem = (size_t)3 * kmax * 36 * sizeof(double);
+  cudaFuncSetAttribute(k_fill_transform, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_fill_transform<<<nsrc, 256, smem, st>>>(srcs, seb, see, goff, foff, gram, s.geo64, x, fill);
+  launch_count();
+}
+
+// ---------------------------------------------------------------------------
+// per-edge K-space step  u_e = G_{e,i} dx_i - G_{e,j} dx_j  (fp64 -> fp32)
+// ---------------------------------------------------------------------------
+__global__ void k_step_edges(const int32_t* __restrict__ ei, const int32_t* __restrict__ ej, int E,
+                             const double* __restrict__ geo64, Extr x, const double* __restrict__ dx_full,
+                             int sdof, float* __restrict__ ustep) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const double* q = geo64 + (int64_t)kGeo64 * e;
+  double Gi[36], Gj[36];
+  build_G(q, q + 18, q + 9, Gi);
+  build_G(x.RbcT, x.c2, q + 9, Gj);
+  const double* di = dx_full + (int64_t)sdof * ei[e];
+  const double* dj = dx_full + (int64_t)sdof * ej[e];
+#pragma unroll
+  for (int r = 0; r < 6; ++r) {
+    double acc = 0.0;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) acc += Gi[r * 6 + c] * di[c] - Gj[r * 6 + c] * dj[c];
+    ustep[e * 8 + r] = (float)acc;
+  }
+  ustep[e * 8 + 6] = 0.f;
+  ustep[e * 8 + 7] = 0.f;
+}
+
+void launch_step_edges(const int32_t* ei, const int32_t* ej, int E, const DevState& s, const Extr& x,
+                       const double* dx_full, int sdof, float* ustep, cudaStream_t st) {
+  if (E <= 0) return;
+  k_step_edges<<<(E + 127) / 128, 128, 0, st>>>(ei, ej, E, s.geo64, x, dx_full, sdof, ustep);
+  launch_count();
+}
+
+// ---------------------------------------------------------------------------
+// K6: disparity back-substitution + update (solver.py:290, 336-338)
+//   dx_d = (-g_d - sum_e k_{n,e} . u_e) / Hdd_d,   d' = max(d + dx_d, 1e-4)
+// ---------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(kPixBlock) k_backsub(
+    const PixTile* __restrict__ tiles, const float* __restrict__ disp, const EdgeGeo32* __restrict__ geo,
+    const float* __restrict__ pix, const float* __restrict__ wts, const int64_t* __restrict__ eoff,
+    const int64_t* __restrict__ doff, int grid_w, GridP gp, IntrP in, const float* __restrict__ Hdd,
+    const float* __restrict__ gd, const float* __restrict__ ustep, double lam, double ridge,
+    float* __restrict__ disp_out, float* __restrict__ dxd_out, unsigned long long* __restrict__ step_bits) {
+  const PixTile T = tiles[blockIdx.x];
+  const int tid = threadIdx.x;
+  const int64_t kbase = doff[T.src];
+  const float fx2 = (float)(in.fx * in.fx), fy2 = (float)(in.fy * in.fy);
+  float rx[2 * kTP], ry[2 * kTP], dd[2 * kTP], acc[2 * kTP];
+  bool act[kTP];
+#pragma unroll
+  for (int m = 0; m < kTP; ++m) {
+    const int p = m * kPixBlock + tid;
+    const int n = T.n0 + 2 * p;
+    act[m] = 2 * p < T.cnt;
+    rx[2 * m] = ry[2 * m] = rx[2 * m + 1] = ry[2 * m + 1] = 0.f;
+    dd[2 * m] = dd[2 * m + 1] = 1.f;
+    acc[2 * m] = acc[2 * m + 1] = 0.f;
+    if (act[m]) {
+      const float2 d2 = __ldg(reinterpret_cast<const float2*>(disp + kbase + n));
+      dd[2 * m] = d2.x;
+      dd[2 * m + 1] = d2.y;
+      if (MODE != VBA_PIX_EDGE)
+        load_rays<MODE>(pix, kbase, n, grid_w, gp, in, rx[2 * m], ry[2 * m], rx[2 * m + 1], ry[2 * m + 1]);
+    }
+  }
+  for (int e = T.eb; e < T.ee; ++e) {
+    const EdgeGeo32 g = load_geo(geo, e);
+    const float4 ua = __ldg(reinterpret_cast<const float4*>(ustep + 8 * e));
+    const float2 ub = __ldg(reinterpret_cast<const float2*>(ustep + 8 * e + 4));
+    const int64_t rbase = eoff[e] + T.n0;
+#pragma unroll
+    for (int m = 0; m < kTP; ++m) {
+      const int p = m * kPixBlock + tid;
+      float4 ww = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (act[m]) {
+        ww = __ldg(reinterpret_cast<const float4*>(wts + 2 * (rbase + 2 * p)));
+        if (MODE == VBA_PIX_EDGE)
+          load_rays<VBA_PIX_KF>(pix, rbase - T.n0, T.n0 + 2 * p, grid_w, gp, in, rx[2 * m], ry[2 * m],
+                                rx[2 * m + 1], ry[2 * m + 1]);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int q = 2 * m + h;
+        const PxGeom o = project(g, rx[q], ry[q], dd[q]);
+        float w0 = h ? ww.z : ww.x, w1 = h ? ww.w : ww.y;
+        w0 = o.valid ? w0 : 0.f;
+        w1 = o.valid ? w1 : 0.f;
+        const float jd0 = fmaf(o.x, g.t[2], -g.t[0]) * o.izh;
+        const float jd1 = fmaf(o.y, g.t[2], -g.t[1]) * o.izh;
+        const float c0w = w0 * fx2 * jd0, c1w = w1 * fy2 * jd1;
+        const float xy = o.x * o.y;
+        // k_{n,e} . u_e
+        float s = ua.x * fmaf(c0w, xy, c1w * fmaf(o.y, o.y, 1.f));
+        s = fmaf(ua.y, fmaf(c0w, -fmaf(o.x, o.x, 1.f), c1w * -xy), s);
+        s = fmaf(ua.z, fmaf(c0w, o.y, c1w * -o.x), s);
+        s = fmaf(ua.w, c0w * -o.iz, s);
+        s = fmaf(ub.x, c1w * -o.iz, s);
+        s = fmaf(ub.y, fmaf(c0w, o.x * o.iz, c1w * (o.y * o.iz)), s);
+        acc[q] += s;
+      }
+    }
+  }
+  double mx = 0.0;
+  const double damp = 1.0 + lam;
+#pragma unroll
+  for (int m = 0; m < kTP; ++m) {
+    if (!act[m]) continue;
+    const int64_t n = kbase + T.n0 + 2 * (m * kPixBlock + tid);
+    const float2 h2 = *reinterpret_cast<const float2*>(Hdd + n);
+    const float2 g2 = *reinterpret_cast<const float2*>(gd + n);
+    const double dx0 = (-(double)g2.x - (double)acc[2 * m]) / ((double)h2.x * damp + ridge);
+    const double dx1 = (-(double)g2.y - (double)acc[2 * m + 1]) / ((double)h2.y * damp + ridge);
+    const float n0v = fmaxf((float)((double)dd[2 * m] + dx0), kDispFloor);
+    const float n1v = fmaxf((float)((double)dd[2 * m + 1] + dx1), kDispFloor);
+    *reinterpret_cast<float2*>(disp_out + n) = make_float2(n0v, n1v);
+    if (dxd_out) *reinterpret_cast<float2*>(dxd_out + n) = make_float2((float)dx0, (float)dx1);
+    mx = fmax(mx, fmax(fabs(dx0), fabs(dx1)));
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((tid & 31) == 0 && mx > 0.0)
+    atomicMax(step_bits, (unsigned long long)__double_as_longlong(mx));   // max is order-independent
+}
+
+void launch_backsub(int mode, const PixTile* tiles, int ntiles, const DevState& cur, const DevState& nxt,
+                    const float* pix, const float* wts, const int64_t* eoff, const int64_t* doff, int grid_w,
+                    const double* grid, const double* intr, const float* Hdd, const float* gd, const float* ustep,
+                    double lam, double ridge, float* dxd_out, unsigned long long* step_bits, cudaStream_t st) {
+  if (ntiles <= 0) return;
+  GridP gp{grid[0], grid[1], grid[2], grid[3]};
+  IntrP in{intr[0], intr[1], intr[2], intr[3]};
+  if (mode == VBA_PIX_GRID)
+    k_backsub<VBA_PIX_GRID><<<ntiles, kPixBlock, 0, st>>>(tiles, cur.disp, cur.geo32, pix, wts, eoff, doff, grid_w,
+                                                          gp, in, Hdd, gd, ustep, lam, ridge, nxt.disp, dxd_out,
+                                                          step_bits);
+  else if (mode == VBA_PIX_KF)
+    k_backsub<VBA_PIX_KF><<<ntiles, kPixBlock, 0, st>>>(tiles, cur.disp, cur.geo32, pix, wts, eoff, doff, grid_w,
+                                                        gp, in, Hdd, gd, ustep, lam, ridge, nxt.disp, dxd_out,
+                                                        step_bits);
+  else
+    k_backsub<VBA_PIX_EDGE><<<ntiles, kPixBlock, 0, st>>>(tiles, cur.disp, cur.geo32, pix, wts, eoff, doff, grid_w,
+                                                          gp, in, Hdd, gd, ustep, lam, ridge, nxt.disp, dxd_out,
+                                                          step_bits);
+  launch_count();
+}
+
+// ---------------------------------------------------------------------------
+// retraction of keyframe states and gravity (solver.py:326-341, residuals.py:44-52,
+// geometry.py:221-223, residuals.py:132-134); frozen keyframes copied bitwise.
+// ---------------------------------------------------------------------------
+__global__ void k_retract(const double* __restrict__ cur, double* __restrict__ nxt, const double* __restrict__ dx,
+                          const int32_t* __restrict__ frozen, int K, int sdof, int ngrav, int n_state,
+                          const double* __restrict__ gcur, double* __restrict__ gnxt,
+                          unsigned long long* __restrict__ step_bits, int npv) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n < K) {
+    const double* s = cur + 16 * n;
+    double* o = nxt + 16 * n;
+    const double* d = dx + (int64_t)sdof * n;
+    if (frozen[n]) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) o[k] = s[k];
+    } else {
+      double qe[4], qn[4];
+      qexp(d, qe);
+      qmul(s, qe, qn);
+      qcanon(qn);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o[k] = qn[k];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) o[4 + k] = s[4 + k] + d[3 + k];
+      if (sdof == 15) {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) o[7 + k] = s[7 + k] + d[6 + k];
+      } else {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) o[7 + k] = s[7 + k];
+      }
+    }
+  }
+  if (n == K) {  // gravity (+ the |dx_full| max, thread-serial: npv is small)
+    for (int k = 0; k < 5; ++k) gnxt[k] = gcur[k];
+    if (ngrav) {
+      const double w[3] = {dx[n_state], dx[n_state + 1], 0.0};   // GRAVITY_TANGENT_BASIS @ dg
+      double qe[4], qn[4];
+      qexp(w, qe);
+      qmul(gcur, qe, qn);
+      qcanon(qn);
+      for (int k = 0; k < 4; ++k) gnxt[k] = qn[k];
+    }
+    double mx = 0.0;
+    for (int i = 0; i < npv; ++i) mx = fmax(mx, fabs(dx[i]));
+    if (mx > 0.0) atomicMax(step_bits, (unsigned long long)__double_as_longlong(mx));
+  }
+}
+
+void launch_retract(const DevState& cur, const DevState& nxt, const double* dx_full, const int32_t* frozen, int K,
+                    int sdof, int ngrav, int n_state, unsigned long long* step_bits, int npv, cudaStream_t st) {
+  k_retract<<<(K + 1 + 127) / 128, 128, 0, st>>>(cur.state, nxt.state, dx_full, frozen, K, sdof, ngrav, n_state,
+                                                 cur.grav, nxt.grav, step_bits, npv);
+  launch_count();
+}
+
+// ---------------------------------------------------------------------------
+// export of the dense pose-disparity coupling H_pd (reference layout,
+// solver.py:209-213): column = real disparity index, rows = 6 pose columns of
+// the source and of every edge target.  Test/diagnostic path only.
+// ---------------------------------------------------------------------------
+template <int MODE>
+__global__ void k_export_hpd(const int32_t* __restrict__ seb, const int32_t* __restrict__ see,
+                             const int64_t* __restrict__ doff, const int64_t* __restrict__ roff,
+                             const int32_t* __restrict__ npix, const int32_t* __restrict__ ej, int K,
+                             const float* __restrict__ disp, const EdgeGeo32* __restrict__ geo,
+                             const double* __restrict__ geo64, Extr x, const float* __restrict__ pix,
+                             const float* __restrict__ wts, const int64_t* __restrict__ eoff, int grid_w, GridP gp,
+                             IntrP in, int sdof, int64_t ncol, double* __restrict__ H) {
+  const int src = blockIdx.y;
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (src >= K || n >= npix[src]) return;
+  const int64_t kbase = doff[src];
+  const int64_t col = roff[src] + n;
+  const float fx2 = (float)(in.fx * in.fx), fy2 = (float)(in.fy * in.fy);
+  const float d = disp[kbase + n];
+  double hi[6] = {0, 0, 0, 0, 0, 0};
+  for (int e = seb[src]; e < see[src]; ++e) {
+    float rx, ry, rx1, ry1;
+    if (MODE == VBA_PIX_EDGE) load_rays<VBA_PIX_KF>(pix, eoff[e], n & ~1, grid_w, gp, in, rx, ry, rx1, ry1);
+    else load_rays<MODE>(pix, kbase, n & ~1, grid_w, gp, in, rx, ry, rx1, ry1);
+    if (n & 1) { rx = rx1; ry = ry1; }
+    const EdgeGeo32 g = load_geo(geo, e);
+    const PxGeom o = project(g, rx, ry, d);
+    const float2 w = __ldg(reinterpret_cast<const float2*>(wts + 2 * (eoff[e] + n)));
+    const float w0 = o.valid ? w.x : 0.f, w1 = o.valid ? w.y : 0.f;
+    const float jd0 = fmaf(o.x, g.t[2], -g.t[0]) * o.izh;
+    const float jd1 = fmaf(o.y, g.t[2], -g.t[1]) * o.izh;
+    const float c0w = w0 * fx2 * jd0, c1w = w1 * fy2 * jd1;
+    const float xy = o.x * o.y;
+    float u[6];
+    u[0] = fmaf(c0w, xy, c1w * fmaf(o.y, o.y, 1.f));
+    u[1] = fmaf(c0w, -fmaf(o.x, o.x, 1.f), c1w * -xy);
+    u[2] = fmaf(c0w, o.y, c1w * -o.x);
+    u[3] = c0w * -o.iz;
+    u[4] = c1w * -o.iz;
+    u[5] = fmaf(c0w, o.x * o.iz, c1w * (o.y * o.iz));
+    double Gi[36], Gj[36];
+    const double* q = geo64 + (int64_t)kGeo64 * e;
+    build_G(q, q + 18, q + 9, Gi);
+    build_G(x.RbcT, x.c2, q + 9, Gj);
+    const int j = ej[e];
+    for (int a = 0; a < 6; ++a) {
+      double si = 0.0, sj = 0.0;
+      for (int m = 0; m < 6; ++m) {
+        si += Gi[m * 6 + a] * (double)u[m];
+        sj += Gj[m * 6 + a] * (double)u[m];
+      }
+      hi[a] += si;
+      H[((int64_t)j * sdof + a) * ncol + col] -= sj;
+    }
+  }
+  for (int a = 0; a < 6; ++a) H[((int64_t)src * sdof + a) * ncol + col] += hi[a];
+}
+
+void launch_export_hpd(int mode, const int32_t* seb, const int32_t* see, const int64_t* doff, const int64_t* roff,
+                       const int32_t* npix, int maxpix, const int32_t* ej, int K, const DevState& s, const Extr& x,
+                       const float* pix, const float* wts, const int64_t* eoff, int grid_w, const double* grid,
+                       const double* intr, int sdof, int64_t ncol, double* H, cudaStream_t st) {
+  if (K <= 0 || maxpix <= 0) return;
+  GridP gp{grid[0], grid[1], grid[2], grid[3]};
+  IntrP in{intr[0], intr[1], intr[2], intr[3]};
+  dim3 grd((maxpix + 127) / 128, K);
+  // one source per grid row; sources are independent, edges of a source are serial per pixel
+  for (int m = 0; m < 1; ++m) {
+    if (mode == VBA_PIX_GRID)
+      k_export_hpd<VBA_PIX_GRID><<<grd, 128, 0, st>>>(seb, see, doff, roff, npix, ej, K, s.disp, s.geo32, s.geo64, x,
+                                                      pix, wts, eoff, grid_w, gp, in, sdof, ncol, H);
+    else if (mode == VBA_PIX_KF)
+      k_export_hpd<VBA_PIX_KF><<<grd, 128, 0, st>>>(seb, see, doff, roff, npix, ej, K, s.disp, s.geo32, s.geo64, x,
+                                                    pix, wts, eoff, grid_w, gp, in, sdof, ncol, H);
+    else
+      k_export_hpd<VBA_PIX_EDGE><<<grd, 128, 0, st>>>(seb, see, doff, roff, npix, ej, K, s.disp, s.geo32, s.geo64, x,
+                                                      pix, wts, eoff, grid_w, gp, in, sdof, ncol, H);
+  }
+  launch_count();
+}
+
+// padded per-keyframe fp32 array -> reference-order fp64 array
+__global__ void k_unpad(const float* __restrict__ src, const int64_t* __restrict__ doff,
+                        const int64_t* __restrict__ roff, const int32_t* __restrict__ npix, int K,
+                        double* __restrict__ dst) {
+  const int k = blockIdx.y;
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K || n >= npix[k]) return;
+  dst[roff[k] + n] = (double)src[doff[k] + n];
+}
+
+void launch_unpad(const float* src, const int64_t* doff, const int64_t* roff, const int32_t* npix, int maxpix, int K,
+                  double* dst, cudaStream_t st) {
+  if (K <= 0 || maxpix <= 0) return;
+  dim3 grd((maxpix + 255) / 256, K);
+  k_unpad<<<grd, 256, 0, st>>>(src, doff, roff, npix, K, dst);
+  launch_count();
+}
+
+// energy = sum over vision tiles (fixed order) + sum over IMU factors (fixed order)
+__global__ void k_energy_reduce(const double* __restrict__ te, int nt, const double* __restrict__ ib, int F,
+                                int ibs, int eoff, double* __restrict__ out) {
+  __shared__ double red[32];
+  double v = 0.0;
+  for (int i = threadIdx.x; i < nt; i += blockDim.x) v += te[i];
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    double si = 0.0;
+    for (int f = 0; f < F; ++f) si += ib[(int64_t)f * ibs + eoff];
+    out[0] = s + si;
+    out[1] = s;
+    out[2] = si;
+  }
+}
+
+void launch_energy_reduce(const double* te, int nt, const double* ib, int F, int ibs, int eoff, double* out3,
+                          cudaStream_t st) {
+  k_energy_reduce<<<1, 1024, 0, st>>>(te, nt, ib, F, ibs, eoff, out3);
+  launch_count();
+}
+
+}  // namespace vba

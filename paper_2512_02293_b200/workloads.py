@@ -5,7 +5,7 @@ with BASELINE.json's shapes and distributions (SURVEY.md §8(d) pins the
 choices BASELINE leaves open):
 
 * keyframes at 10 Hz, IMU at 200 Hz (20 intervals per keyframe pair);
-* a looping trajectory (1 m/s on a ~0.95 m circle, 60 keyframes per lap)
+* a looping trajectory (1 m/s on a ~1.15 m circle, 72 keyframes = 5° yaw per step)
   with a smooth 3° orientation wobble, so keyframes more than 30 apart
   revisit the same place and loop edges are covisible;
 * IMU white noise σ_gyro=0.002, σ_acc=0.02 per sample and a bias random walk
@@ -59,7 +59,8 @@ CONFIGS = {
 KF_DT = 0.1
 IMU_STEPS = 20
 GRAVITY = 9.81
-LAP_KF = 60
+LAP_KF = 72            # 5° of yaw per keyframe step
+FX_FULL = 320.0
 SIGMA_GYRO = 0.002
 SIGMA_ACC = 0.02
 RATE = IMU_STEPS / KF_DT
@@ -119,11 +120,14 @@ class _Motion:
     def __init__(self, rng):
         self.Om = 2.0 * np.pi / (LAP_KF * KF_DT)
         self.rho = 1.0 / self.Om
+        # wobble frequencies are integer multiples of the lap frequency, so a
+        # revisit one lap later reproduces the pose (covisible loop edges)
+        flap = 1.0 / (LAP_KF * KF_DT)
         self.A = np.deg2rad(3.0) * rng.uniform(0.5, 1.0, 3)
-        self.f = rng.uniform(0.05, 0.2, 3)
+        self.f = flap * rng.integers(1, 4, 3)
         self.ph = rng.uniform(0, 2 * np.pi, 3)
         self.B = 0.02 * rng.uniform(0.5, 1.0, 3)
-        self.g = rng.uniform(0.05, 0.2, 3)
+        self.g = flap * rng.integers(1, 4, 3)
         self.ps = rng.uniform(0, 2 * np.pi, 3)
 
     def theta(self, t):
@@ -273,7 +277,10 @@ def make_workload(cfg: int, grid=None, seed=None, with_truth=False):
 
     # --- intrinsics and per-keyframe disparity grids
     s = spec.intr_scale
-    fx = fy = 320.0 * s
+    # BASELINE: "fx=fy=320, cx=32, cy=24 at 1/8 resolution" — fx=320 is the
+    # full-resolution (512x384) focal length, so the 1/8 grid uses fx=40
+    # (77° FOV); cx, cy are already 1/8-resolution values.  DESIGN.md §7.
+    fx = fy = FX_FULL / 8.0 * s
     cx, cy = 32.0 * s, 24.0 * s
     W = max(cols, int(np.ceil(cx)) + 1)
     Hh = max(rows, int(np.ceil(cy)) + 1)
@@ -316,9 +323,11 @@ def make_workload(cfg: int, grid=None, seed=None, with_truth=False):
         Xw = (ray / disp_true[i][:, None]) @ Ri.T + pi_
         Xj = (Xw - pj) @ Rj
         z = Xj[:, 2]
-        ok = z > 0.05
-        zs = np.where(ok, z, 1.0)
+        zs = np.where(z > 0.05, z, 1.0)
         uv = np.stack([fx * Xj[:, 0] / zs + cx, fy * Xj[:, 1] / zs + cy], 1)
+        # reference provider visibility rule (synth.py:553-556): in front and inside the image
+        ok = ((z > 0.05) & (uv[:, 0] >= 0.0) & (uv[:, 0] <= W - 1.0)
+              & (uv[:, 1] >= 0.0) & (uv[:, 1] <= Hh - 1.0))
         tgt = uv + spec.sigma_px * rng.standard_normal((N, 2))
         w = rng.uniform(0.0, 1.0, (N, 2))
         if spec.outlier_rate > 0:

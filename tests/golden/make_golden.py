@@ -85,6 +85,21 @@ def ref_outputs(graph, opts, iters):
     out.update(H_pp=H_pp, H_pd=H_pd, H_dd=H_dd, g_p=g_p, g_d=g_d)
     dx, dxd = ref_solver._solve_step(layout, H_pp, H_pd, H_dd, g_p, g_d, opts.damping, True)
     out.update(dx=dx, dxd=dxd)
+    # conditioning floor: the reference's own step change when every flow target
+    # moves by less than one fp32 ulp (what any fp32 evaluation of r introduces)
+    rng = np.random.default_rng(7)
+    cdx = cdxd = 0.0
+    for _ in range(3):
+        g3 = copy.deepcopy(graph)
+        for e in g3.vision_edges:
+            sp = np.spacing(np.abs(e.targets.astype(np.float32))).astype(np.float64)
+            e.targets = e.targets + sp * rng.uniform(-1.0, 1.0, e.targets.shape)
+        lin3 = ref_solver._linearize(g3, ref_solver._Layout(g3, opts))
+        d3, dd3 = ref_solver._solve_step(layout, *lin3, opts.damping, True)
+        cdx = max(cdx, float(np.abs(d3 - dx).max() / max(np.abs(dx).max(), 1e-300)))
+        if len(dxd) and np.abs(dxd).max() > 0:
+            cdxd = max(cdxd, float(np.abs(dd3 - dxd).max() / np.abs(dxd).max()))
+    out.update(cond_dx=np.array(cdx), cond_dxd=np.array(cdxd))
     g2 = copy.deepcopy(graph)
     o2 = copy.deepcopy(opts)
     o2.max_iterations = iters
