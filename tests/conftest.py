@@ -34,6 +34,36 @@ def load_golden(name):
     return P, out, opts
 
 
+def graph_from_packed(P, truth=None):
+    """Rebuild a paper_2512_02293_b200.types FrameGraph from a packed problem dict."""
+    from paper_2512_02293_b200 import types as T
+    K = len(P["kid"])
+    kfs = []
+    for n in range(K):
+        st = T.PoseState(T.Pose(T.Rotation(P["q"][n]), P["p"][n]), P["v"][n],
+                         T.BiasState(P["bg"][n], P["ba"][n]), float(P["ts"][n]))
+        sl = slice(P["doff"][n], P["doff"][n + 1])
+        kfs.append(T.Keyframe(int(P["kid"][n]), st, P["pix"][sl], P["disp"][sl]))
+    kid = P["kid"]
+    edges = []
+    for e in range(len(P["ei"])):
+        r = slice(P["eoff"][e], P["eoff"][e + 1])
+        edges.append(T.VisionEdge(int(kid[P["ei"][e]]), int(kid[P["ej"][e]]), P["epix"][r], P["tgt"][r], P["w"][r]))
+    imu = []
+    for f in range(len(P["fi"])):
+        imu.append((int(kid[P["fi"][f]]), int(kid[P["fj"][f]]), T.PreintegratedDelta(
+            float(P["f_dt"][f]), T.Rotation(P["f_dR"][f]), P["f_dp"][f], P["f_dv"][f], P["f_Jr"][f], P["f_Jp"][f],
+            P["f_Jv"][f], P["f_cov"][f], T.BiasState(P["f_bhat"][f][:3], P["f_bhat"][f][3:]))))
+    fx, fy, cx, cy = P["intr"]
+    W = int(max(640, cx * 2 + 1))
+    Hh = int(max(480, cy * 2 + 1))
+    Tcb = None
+    if P.get("has_Tcb", False):
+        Tcb = T.Pose(T.Rotation(P["Tcb"][:4]), P["Tcb"][4:7])
+    return T.FrameGraph(kfs, edges, imu, T.GravityModel(T.Rotation(P["grav_q"]), float(P["grav_G"])),
+                        T.Intrinsics(fx, fy, cx, cy, W, Hh), Tcb)
+
+
 @pytest.fixture(scope="session")
 def cuda_ok():
     import torch
