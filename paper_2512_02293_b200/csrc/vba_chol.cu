@@ -1,0 +1,617 @@
+// vba_chol.cu — dense fp64 Cholesky solve of the reduced system as ONE persistent
+// kernel executing a tile-task DAG (sm_100a).
+//
+// Replaces np.linalg.solve(Hred, -gred) of solver.py:287 (/root/reference/pkg/src/vislam/)
+// for the symmetric positive-definite damped Schur complement.  The matrix is
+// column-major with 128x128 tiles; tasks (built once per solve on the host):
+//
+//   POTRF(k)      factor the diagonal tile, write L_kk^-1 to a side buffer,
+//                 forward-substitute y_k = L_kk^-1 rhs_k
+//   TRSM(i,k)     L_ik = A_ik L_kk^-T  (a GEMM with the inverse), rhs_i -= L_ik y_k
+//   GEMM(i,j,k)   A_ij -= L_ik L_jk^T  (SYRK when i == j)
+//   BUPD(j,k)     p_jk = L_kj^T x_k                (backward substitution, j < k)
+//   BSOL(k)       x_k = L_kk^-T (y_k - sum_k' p_kk')
+//
+// GEMM-shaped tasks run on the fp64 tensor cores (mma.sync m8n8k4 f64, DMMA)
+// with cp.async double-buffered operand chunks.  Persistent CTAs (one per SM,
+// all co-resident) take tasks in a topological order with lookahead (the next
+// panel column is updated and factored before the rest of the trailing
+// update) and wait on per-tile counters: upd[i][j] = updates applied,
+// done[i][j] = tile final.  Matrix data written inside the kernel is only read
+// through L2 (.cg), so no stale L1 lines are observed.  A non-positive pivot
+// sets *status (mapped to the reference's "singular reduced pose system").
+#include <cuda_runtime.h>
+
+#include "vba_internal.cuh"
+
+namespace vba {
+
+constexpr int CT = 128;          // tile size
+constexpr int KC = 32;           // K chunk per pipeline stage
+constexpr int SP = CT + 4;       // smem column stride (doubles): conflict-free fragment loads
+constexpr int CHOL_THREADS = 256;
+constexpr int SB = 36;           // 32x32 block stride in POTRF (doubles, = 4 mod 16)
+constexpr size_t CHOL_SMEM = (size_t)2 * 2 * KC * SP * sizeof(double);   // 2 stages x (A, B)
+
+enum TaskType { T_POTRF = 0, T_TRSM = 1, T_GEMM = 2, T_BUPD = 3, T_BSOL = 4 };
+
+struct CholTask {
+  int32_t type, i, j, k;
+  int32_t expect;   // updates expected on the target tile before this task (envelope-ready)
+  int32_t pad[3];
+};
+
+// ---------------------------------------------------------------------------
+// low-level helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
+__device__ __forceinline__ void stcg(double* p, double v) { __stcg(p, v); }
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// wait until *flag >= want (one thread), then CTA barrier
+__device__ __forceinline__ void wait_geq(const int* flag, int want) {
+  if (threadIdx.x == 0) {
+    int ns = 32;
+    while (ld_acquire(flag) < want) {
+      __nanosleep(ns);
+      if (ns < 1024) ns <<= 1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// GEMM core: acc(c, r) = sum_m opA(c, m) * opB(r, m) over m in [0, CT)
+//   opA / opB: 128x128 column-major tiles (element (row, m) at base[m*lda + row])
+// Warp w owns rows c in [64*(w%2), +64) and r in [32*(w/2), +32): 8 x 4 DMMA tiles.
+// acc[mt][nt][0/1] = (c = 64wm + 8mt + lane/4, r = 32wn + 8nt + 2*(lane%4) + {0,1})
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void load_chunk(double* sA, double* sB, const double* A, int64_t lda, const double* B,
+                                           int64_t ldb, int m0) {
+  // each operand chunk: 128 rows x KC cols -> smem [KC][SP]; 16-byte cp.async of 2 rows
+  for (int t = threadIdx.x; t < KC * (CT / 2); t += CHOL_THREADS) {
+    const int m = t / (CT / 2), r2 = (t % (CT / 2)) * 2;
+    cp_async16(sA + m * SP + r2, A + (int64_t)(m0 + m) * lda + r2);
+    cp_async16(sB + m * SP + r2, B + (int64_t)(m0 + m) * ldb + r2);
+  }
+  cp_async_commit();
+}
+
+__device__ __forceinline__ void gemm_tile(double* smem, const double* A, int64_t lda, const double* B, int64_t ldb,
+                                          double (&acc)[8][4][2]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int wm = w & 1, wn = w >> 1;
+  // stage s: A at smem + s*2*KC*SP, B right after it (arithmetic, no pointer arrays)
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  load_chunk(smem, smem + KC * SP, A, lda, B, ldb, 0);
+  const int ar = 64 * wm + (lane >> 2), br = 32 * wn + (lane >> 2), kq = lane & 3;
+#pragma unroll 1
+  for (int kc = 0; kc < CT / KC; ++kc) {
+    const int s = kc & 1;
+    if (kc + 1 < CT / KC) {
+      double* nxt = smem + (s ^ 1) * 2 * KC * SP;
+      load_chunk(nxt, nxt + KC * SP, A, lda, B, ldb, (kc + 1) * KC);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* pa = smem + s * 2 * KC * SP;
+    const double* pb = pa + KC * SP;
+#pragma unroll
+    for (int ks = 0; ks < KC / 4; ++ks) {
+      const int m = ks * 4 + kq;
+      double af[8], bf[4];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) af[a] = pa[m * SP + ar + 8 * a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bf[b] = pb[m * SP + br + 8 * b];
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// tasks
+// ---------------------------------------------------------------------------
+struct CholArgs {
+  double* A;
+  int64_t ld;
+  int nt;
+  double* rhs;       // [nt*CT]   in: -g_red, out: y (forward-substituted)
+  double* x;         // [nt*CT]   solution
+  double* Linv;      // [nt][CT*CT] column-major inverses of the diagonal factors
+  double* part;      // [nt][nt][CT] backward-substitution partials
+  int* upd;          // [nt*nt]
+  int* done;         // [nt*nt]
+  int* bcnt;         // [nt]  BUPD tasks completed for row block j
+  int* counter;      // task dispenser
+  const CholTask* tasks;
+  int ntasks;
+  int* status;
+  unsigned long long* trace;   // optional [ntasks][4]: t_grab, t_ready, t_done, smid
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ double* tile(const CholArgs& a, int i, int j) {
+  return a.A + (int64_t)j * CT * a.ld + (int64_t)i * CT;
+}
+
+// Warp-synchronous Cholesky + inverse of a 32x32 SPD block: lane r holds row r
+// of the block (a[]) and of the identity (m[]); 32 right-looking steps with
+// shuffles.  On return the block (column-major, stride sw) holds L and Ib
+// (column-major 32x32) holds L^-1.  Non-positive pivot -> *bad.
+// CTA-wide Cholesky + inverse of a 32x32 SPD block held in shared memory
+// (column-major, stride sw): right-looking elimination of [W | I] with all 256
+// threads (thread = (row r, column group cg), 4 columns each), two barriers per
+// step.  On return W holds L (lower) and Ib (column-major, stride SB) L^-1.
+__device__ __forceinline__ void cta_potrf32(double* W, int sw, double* Ib, int* bad) {
+  const int tid = threadIdx.x, r = tid & 31, cg = tid >> 5;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) Ib[(cg + 8 * q) * SB + r] = (cg + 8 * q == r) ? 1.0 : 0.0;
+  __syncthreads();
+#pragma unroll 1
+  for (int j = 0; j < 32; ++j) {
+    __syncthreads();                                   // updates of step j-1 complete
+    double piv = W[j * sw + j];
+    if (!(piv > 0.0)) {
+      if (tid == 0) *bad = 1;
+      piv = 1.0;
+    }
+    const double inv = rsqrt(piv);
+    __syncthreads();                                   // every thread has read the pivot
+    if (cg == 0) {                                     // column j of L
+      if (r > j) W[j * sw + r] *= inv;
+      else if (r == j) W[j * sw + j] = piv * inv;
+    } else if (cg == 1 && r <= j) {                    // row j of L^-1
+      Ib[r * SB + j] *= inv;
+    }
+    __syncthreads();
+    if (r > j) {
+      const double lr = W[j * sw + r];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = cg + 8 * q;
+        if (c > j && c <= r) W[c * sw + r] -= lr * W[j * sw + c];
+        else if (c <= j) Ib[c * SB + r] -= lr * Ib[c * SB + j];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Shared-memory DMMA GEMM for the in-tile block work of POTRF:
+//   C(M x N) = beta*C + alpha * A(M x K) * op(B)
+//   A(m, k) at A[k*lda + m];  BT: op(B)(k, n) = B(n, k) at B[k*ldb + n];  !BT: (k, n) at B[n*ldb + k]
+//   C(m, n) at C[n*ldc + m].  M, N multiples of 8, K of 4; strides = 4 mod 16 (conflict-free).
+//   lower: skip 8x8 output tiles strictly above the diagonal.
+// Warps take 8x8 output tiles two at a time (two independent DMMA chains).
+template <bool BT>
+__device__ __forceinline__ void sgemm8(const double* A, int lda, const double* B, int ldb, double* C, int ldc, int M,
+                                       int N, int K, double alpha, bool beta, bool lower) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tm = M >> 3, nt = tm * (N >> 3);
+  const int am = lane >> 2, ak = lane & 3;
+  for (int t = warp; t < nt; t += 16) {
+    const int t2 = t + 8;
+    const int bi0 = t % tm, bj0 = t / tm;
+    const bool v1 = t2 < nt;
+    const int bi1 = v1 ? t2 % tm : bi0, bj1 = v1 ? t2 / tm : bj0;
+    const bool on0 = !(lower && bj0 > bi0), on1 = v1 && !(lower && bj1 > bi1);
+    double c00 = 0, c01 = 0, c10 = 0, c11 = 0;
+    for (int k = 0; k < K; k += 4) {
+      const double a0 = A[(k + ak) * lda + bi0 * 8 + am];
+      const double a1 = A[(k + ak) * lda + bi1 * 8 + am];
+      const double b0 = BT ? B[(k + ak) * ldb + bj0 * 8 + am] : B[(bj0 * 8 + am) * ldb + k + ak];
+      const double b1 = BT ? B[(k + ak) * ldb + bj1 * 8 + am] : B[(bj1 * 8 + am) * ldb + k + ak];
+      dmma(c00, c01, a0, b0);
+      dmma(c10, c11, a1, b1);
+    }
+    const int r = am, cc = 2 * ak;
+    if (on0) {
+      double* p = C + (bj0 * 8 + cc) * ldc + bi0 * 8 + r;
+      p[0] = (beta ? p[0] : 0.0) + alpha * c00;
+      p[ldc] = (beta ? p[ldc] : 0.0) + alpha * c01;
+    }
+    if (on1) {
+      double* p = C + (bj1 * 8 + cc) * ldc + bi1 * 8 + r;
+      p[0] = (beta ? p[0] : 0.0) + alpha * c10;
+      p[ldc] = (beta ? p[ldc] : 0.0) + alpha * c11;
+    }
+  }
+}
+
+constexpr int SW = CT + 4;        // POTRF tile stride (doubles, = 4 mod 16)
+constexpr int TB = 100;           // TRSM temporary stride (96 rows)
+constexpr size_t POTRF_SMEM = (size_t)(CT * SW + 8 * 32 * SB) * sizeof(double);
+constexpr size_t DAG_SMEM = POTRF_SMEM > CHOL_SMEM ? POTRF_SMEM : CHOL_SMEM;
+
+// POTRF(k): blocked (4 panels of 32) factorisation of the diagonal tile in shared
+// memory.  Per panel: warp-synchronous factor + inverse of the 32x32 diagonal
+// block, in-tile TRSM of the rows below, SYRK of the trailing lower triangle.
+// Then M = L^-1 by block forward substitution, written to the side buffer, and
+// the forward substitution y_k = M rhs_k.
+__device__ void task_potrf(const CholArgs& a, int k, double* smem) {
+  double* W = smem;                      // 128 x 128 column-major (stride SW), lower part used
+  double* I = smem + CT * SW;            // 4 blocks: L_pp^-1 (stride SB)
+  double* Mc = I + 4 * 32 * SB;          // 4 blocks: column p of M (rows i >= p), or the TRSM temp (stride TB)
+  __shared__ double ys[CT];
+  __shared__ int bad;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const double* Ak = tile(a, k, k);
+  if (tid == 0) bad = 0;
+  // async tile load (all loads in flight at once; no register staging)
+  for (int t = tid; t < CT * (CT / 2); t += CHOL_THREADS) {
+    const int r2 = (t % (CT / 2)) * 2, c = t / (CT / 2);
+    cp_async16(W + c * SW + r2, Ak + (int64_t)c * a.ld + r2);
+  }
+  cp_async_commit();
+  if (tid < CT) ys[tid] = ldcg(a.rhs + (int64_t)k * CT + tid);
+  cp_async_wait<0>();
+  __syncthreads();
+  unsigned long long* ph = a.trace ? a.trace + 4 * (size_t)a.ntasks + 16 * (size_t)k : nullptr;   // phase stamps
+  if (ph && tid == 0) ph[0] = gtimer();
+  for (int p = 0; p < 4; ++p) {
+    const int c0 = 32 * p, r0 = c0 + 32, nr = CT - r0;
+    cta_potrf32(W + c0 * SW + c0, SW, I + p * 32 * SB, &bad);
+    if (ph && tid == 0) ph[1 + 2 * p] = gtimer();
+    if (nr > 0) {
+      // TRSM: X = W[r0:, c0:c0+32] * Ip^T   (Ip(c, m) at I[m*SB + c])
+      sgemm8<true>(W + c0 * SW + r0, SW, I + p * 32 * SB, SB, Mc, TB, nr, 32, 32, 1.0, false, false);
+      __syncthreads();
+      for (int t = tid; t < nr * 32; t += CHOL_THREADS) {
+        const int r = t % nr, c = t / nr;
+        W[(c0 + c) * SW + r0 + r] = Mc[c * TB + r];
+      }
+      __syncthreads();
+      // SYRK: W[r0:, r0:] -= X X^T   (lower 8x8 tiles)
+      sgemm8<true>(W + c0 * SW + r0, SW, W + c0 * SW + r0, SW, W + r0 * SW + r0, SW, nr, nr, 32, -1.0, true, true);
+      __syncthreads();
+    }
+    if (ph && tid == 0) ph[2 + 2 * p] = gtimer();
+  }
+  if (tid == 0 && bad) atomicExch(a.status, 1);
+  // M = L^-1 by column blocks:  M_pp = I_p,  M_ip = -I_i sum_{m=p}^{i-1} L_im M_mp;
+  // each finished column block goes to the side buffer and into y = M rhs.
+  double* Li = a.Linv + (int64_t)k * CT * CT;
+  double yacc = 0.0;   // thread r < CT accumulates y_r
+  for (int p = 0; p < 4; ++p) {
+    for (int i = p + 1; i < 4; ++i) {
+      double* T = Mc + i * 32 * SB;
+      for (int m = p; m < i; ++m) {
+        const double* Mmp = (m == p) ? I + p * 32 * SB : Mc + m * 32 * SB;
+        sgemm8<false>(W + (32 * m) * SW + 32 * i, SW, Mmp, SB, T, SB, 32, 32, 32, 1.0, m != p, false);
+        __syncthreads();
+      }
+      // M_ip = -I_i T on the tensor cores into the free slot Mc[p], then copied over T
+      double* tmp = Mc + p * 32 * SB;
+      sgemm8<false>(I + i * 32 * SB, SB, T, SB, tmp, SB, 32, 32, 32, -1.0, false, false);
+      __syncthreads();
+      {
+        const int r = tid & 31, cq = tid >> 5;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) T[(cq + 8 * q) * SB + r] = tmp[(cq + 8 * q) * SB + r];
+      }
+      __syncthreads();
+    }
+    // write column block p and accumulate y
+    for (int t = tid; t < CT * 32; t += CHOL_THREADS) {
+      const int r = t % CT, c = t / CT, i = r >> 5;
+      double v = 0.0;
+      if (i == p) v = I[p * 32 * SB + c * SB + (r & 31)];
+      else if (i > p) v = Mc[i * 32 * SB + c * SB + (r & 31)];
+      stcg(Li + (int64_t)(32 * p + c) * CT + r, v);
+    }
+    if (tid < CT) {
+      const int r = tid, i = r >> 5;
+      if (i >= p) {
+        const double* blk = (i == p) ? I + p * 32 * SB : Mc + i * 32 * SB;
+        for (int c = 0; c < 32; ++c) yacc += blk[c * SB + (r & 31)] * ys[32 * p + c];
+      }
+    }
+    __syncthreads();
+  }
+  if (tid < CT) stcg(a.rhs + (int64_t)k * CT + tid, yacc);
+  if (ph && tid == 0) ph[9] = gtimer();
+}
+
+// TRSM(i,k): L_ik = A_ik Linv^T ; rhs_i -= L_ik y_k
+__device__ void task_trsm(const CholArgs& a, int i, int k, double* smem) {
+  double acc[8][4][2];
+  double* Aik = tile(a, i, k);
+  const double* Li = a.Linv + (int64_t)k * CT * CT;
+  // acc(c, r) = sum_m Linv(c, m) * A_ik(r, m)  ==  L_ik(r, c)
+  gemm_tile(smem, Li, CT, Aik, a.ld, acc);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int wm = w & 1, wn = w >> 1;
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int c = 64 * wm + 8 * mt + (lane >> 2);
+      const int r = 32 * wn + 8 * nt + 2 * (lane & 3);
+      double* p = Aik + (int64_t)c * a.ld + r;
+      __stcg(reinterpret_cast<double2*>(p), make_double2(acc[mt][nt][0], acc[mt][nt][1]));
+    }
+  __threadfence();
+  __syncthreads();
+  // rhs_i -= L_ik y_k   (two threads per row, loads batched 16 at a time)
+  __shared__ double yk[CT];
+  if (threadIdx.x < CT) yk[threadIdx.x] = ldcg(a.rhs + (int64_t)k * CT + threadIdx.x);
+  __syncthreads();
+  {
+    const int r = threadIdx.x >> 1, h = threadIdx.x & 1;
+    double s = 0.0;
+#pragma unroll 16
+    for (int c = h; c < CT; c += 2) s += ldcg(Aik + (int64_t)c * a.ld + r) * yk[c];
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    if (h == 0) {
+      double* ri = a.rhs + (int64_t)i * CT + r;
+      stcg(ri, ldcg(ri) - s);
+    }
+  }
+}
+
+// GEMM(i,j,k): A_ij -= L_ik L_jk^T
+__device__ void task_gemm(const CholArgs& a, int i, int j, int k, double* smem) {
+  double acc[8][4][2];
+  // acc(c, r) = sum_m L_jk(c, m) L_ik(r, m) = (L_ik L_jk^T)(r, c)
+  gemm_tile(smem, tile(a, j, k), a.ld, tile(a, i, k), a.ld, acc);
+  double* C = tile(a, i, j);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int wm = w & 1, wn = w >> 1;
+  // read-modify-write in two batches of 16 independent loads (L2 latency overlapped)
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    double2 v[4][4];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int c = 64 * wm + 8 * (4 * h + mt) + (lane >> 2);
+        const int r = 32 * wn + 8 * nt + 2 * (lane & 3);
+        v[mt][nt] = __ldcg(reinterpret_cast<const double2*>(C + (int64_t)c * a.ld + r));
+      }
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int c = 64 * wm + 8 * (4 * h + mt) + (lane >> 2);
+        const int r = 32 * wn + 8 * nt + 2 * (lane & 3);
+        double2 o = v[mt][nt];
+        o.x -= acc[4 * h + mt][nt][0];
+        o.y -= acc[4 * h + mt][nt][1];
+        __stcg(reinterpret_cast<double2*>(C + (int64_t)c * a.ld + r), o);
+      }
+  }
+}
+
+// BUPD(j,k): part[j][k] = L_kj^T x_k
+__device__ void task_bupd(const CholArgs& a, int j, int k) {
+  __shared__ double xs[CT];
+  const double* Lkj = tile(a, k, j);
+  if (threadIdx.x < CT) xs[threadIdx.x] = ldcg(a.x + (int64_t)k * CT + threadIdx.x);
+  __syncthreads();
+  // warp per column: lanes read 4 x 32 consecutive rows (coalesced), then warp-reduce
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll 2
+  for (int c = warp; c < CT; c += CHOL_THREADS / 32) {
+    const double* col = Lkj + (int64_t)c * a.ld;
+    double s = ldcg(col + lane) * xs[lane] + ldcg(col + 32 + lane) * xs[32 + lane] +
+               ldcg(col + 64 + lane) * xs[64 + lane] + ldcg(col + 96 + lane) * xs[96 + lane];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) stcg(a.part + ((int64_t)j * a.nt + k) * CT + c, s);
+  }
+}
+
+// BSOL(k): x_k = Linv_k^T (y_k - sum_{k'>k} part[k][k'])
+__device__ void task_bsol(const CholArgs& a, int k) {
+  __shared__ double ys[CT];
+  const int tid = threadIdx.x;
+  if (tid < CT) {
+    double v = ldcg(a.rhs + (int64_t)k * CT + tid);
+#pragma unroll 8
+    for (int kk = k + 1; kk < a.nt; ++kk) v -= ldcg(a.part + ((int64_t)k * a.nt + kk) * CT + tid);
+    ys[tid] = v;
+  }
+  __syncthreads();
+  {   // x_k(c) = sum_{r >= c} Linv(r, c) y'(r): warp per column, coalesced
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int c = warp; c < CT; c += CHOL_THREADS / 32) {
+      const double* Li = a.Linv + (int64_t)k * CT * CT + (int64_t)c * CT;   // Linv zero above the diagonal
+      double s = ldcg(Li + lane) * ys[lane] + ldcg(Li + 32 + lane) * ys[32 + lane] +
+                 ldcg(Li + 64 + lane) * ys[64 + lane] + ldcg(Li + 96 + lane) * ys[96 + lane];
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) stcg(a.x + (int64_t)k * CT + c, s);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_dag(CholArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int tsk;
+  const int nt = a.nt;
+  while (true) {
+    if (threadIdx.x == 0) tsk = atomicAdd(a.counter, 1);
+    __syncthreads();
+    const int t = tsk;
+    __syncthreads();
+    if (t >= a.ntasks) break;
+    const CholTask T = a.tasks[t];
+    unsigned long long t0 = 0;
+    if (a.trace && threadIdx.x == 0) t0 = gtimer();
+    switch (T.type) {
+      case T_POTRF:
+        wait_geq(&a.upd[T.k * nt + T.k], T.expect);
+        __syncthreads();
+        if (a.trace && threadIdx.x == 0) a.trace[4 * t + 1] = gtimer();
+        task_potrf(a, T.k, smem);
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) st_release(&a.done[T.k * nt + T.k], 1);
+        break;
+      case T_TRSM:
+        wait_geq(&a.done[T.k * nt + T.k], 1);
+        wait_geq(&a.upd[T.i * nt + T.k], T.expect);
+        __syncthreads();
+        if (a.trace && threadIdx.x == 0) a.trace[4 * t + 1] = gtimer();
+        task_trsm(a, T.i, T.k, smem);
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) st_release(&a.done[T.i * nt + T.k], 1);
+        break;
+      case T_GEMM:
+        wait_geq(&a.done[T.i * nt + T.k], 1);
+        wait_geq(&a.done[T.j * nt + T.k], 1);
+        wait_geq(&a.upd[T.i * nt + T.j], T.expect);
+        __syncthreads();
+        if (a.trace && threadIdx.x == 0) a.trace[4 * t + 1] = gtimer();
+        task_gemm(a, T.i, T.j, T.k, smem);
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) st_release(&a.upd[T.i * nt + T.j], T.expect + 1);
+        break;
+      case T_BUPD:
+        wait_geq(&a.done[T.k * nt + T.k], 2);        // x_k solved (BSOL sets done[k][k] = 2)
+        wait_geq(&a.done[T.k * nt + T.j], 1);
+        __syncthreads();
+        if (a.trace && threadIdx.x == 0) a.trace[4 * t + 1] = gtimer();
+        task_bupd(a, T.j, T.k);
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) atomicAdd(&a.bcnt[T.j], 1);
+        break;
+      case T_BSOL:
+        wait_geq(&a.done[T.k * nt + T.k], 1);
+        wait_geq(&a.bcnt[T.k], T.expect);
+        __syncthreads();
+        if (a.trace && threadIdx.x == 0) a.trace[4 * t + 1] = gtimer();
+        task_bsol(a, T.k);
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) st_release(&a.done[T.k * nt + T.k], 2);
+        break;
+    }
+    if (a.trace && threadIdx.x == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+      a.trace[4 * t + 0] = t0;
+      a.trace[4 * t + 2] = gtimer();
+      a.trace[4 * t + 3] = smid;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side: task list (dense, lookahead 1) and launch
+// ---------------------------------------------------------------------------
+size_t chol_task_bytes() { return sizeof(CholTask); }
+
+int chol_plan_tasks(int nt, void* outv, int cap) {
+  CholTask* out = reinterpret_cast<CholTask*>(outv);
+  int n = 0;
+  auto push = [&](int type, int i, int j, int k, int expect) {
+    if (n < cap) out[n] = CholTask{type, i, j, k, expect, {0, 0, 0}};
+    ++n;
+  };
+  if (nt <= 0) return 0;
+  push(T_POTRF, 0, 0, 0, 0);
+  for (int i = 1; i < nt; ++i) push(T_TRSM, i, 0, 0, 0);
+  for (int k = 0; k + 1 < nt; ++k) {
+    for (int i = k + 1; i < nt; ++i) push(T_GEMM, i, k + 1, k, k);      // next panel column first
+    push(T_POTRF, k + 1, k + 1, k + 1, k + 1);
+    for (int i = k + 2; i < nt; ++i) push(T_TRSM, i, k + 1, k + 1, k + 1);
+    for (int j = k + 2; j < nt; ++j)
+      for (int i = j; i < nt; ++i) push(T_GEMM, i, j, k, k);
+  }
+  for (int k = nt - 1; k >= 0; --k) {
+    push(T_BSOL, k, k, k, nt - 1 - k);
+    for (int j = 0; j < k; ++j) push(T_BUPD, j, j, k, 0);
+  }
+  return n;
+}
+
+size_t chol_smem_bytes() { return CHOL_SMEM; }
+
+int chol_dag_launch(double* A, int64_t ld, int nt, double* rhs, double* x, double* Linv, double* part, int* flags,
+                    const void* tasks, int ntasks, int* status, cudaStream_t st, unsigned long long* trace) {
+  if (nt <= 0) return 0;
+  static int grid = 0;
+  if (grid == 0) {
+    cudaFuncSetAttribute(k_chol_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DAG_SMEM);
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_chol_dag, CHOL_THREADS, DAG_SMEM);
+    grid = sms * (per > 0 ? per : 1);
+  }
+  // flags: upd[nt*nt] done[nt*nt] bcnt[nt] counter[1]
+  cudaMemsetAsync(flags, 0, sizeof(int) * ((size_t)2 * nt * nt + nt + 1), st);
+  CholArgs a;
+  a.A = A;
+  a.ld = ld;
+  a.nt = nt;
+  a.rhs = rhs;
+  a.x = x;
+  a.Linv = Linv;
+  a.part = part;
+  a.upd = flags;
+  a.done = flags + (size_t)nt * nt;
+  a.bcnt = flags + (size_t)2 * nt * nt;
+  a.counter = flags + (size_t)2 * nt * nt + nt;
+  a.tasks = reinterpret_cast<const CholTask*>(tasks);
+  a.ntasks = ntasks;
+  a.status = status;
+  a.trace = trace;
+  const int g = ntasks < grid ? ntasks : grid;
+  k_chol_dag<<<g, CHOL_THREADS, DAG_SMEM, st>>>(a);
+  launch_count();
+  return 0;
+}
+
+}  // namespace vba
+
+namespace vba {
+void chol_task_fields(const void* tasks, int n, int* out4) {
+  const CholTask* t = reinterpret_cast<const CholTask*>(tasks);
+  for (int q = 0; q < n; ++q) {
+    out4[4 * q + 0] = t[q].type;
+    out4[4 * q + 1] = t[q].i;
+    out4[4 * q + 2] = t[q].j;
+    out4[4 * q + 3] = t[q].k;
+  }
+}
+}  // namespace vba

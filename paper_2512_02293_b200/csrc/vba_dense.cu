@@ -32,7 +32,8 @@ __global__ void __launch_bounds__(256) k_assemble(const int32_t* __restrict__ bp
   while ((int64_t)a * (a + 1) / 2 > id) --a;
   const int b = (int)(id - (int64_t)a * (a + 1) / 2);
   const int ra = rdim[a], cb = rdim[b];
-  const int p0 = bptr[id], p1 = bptr[id + 1], pf = p0 + bnff[id];
+  // sym bit 0: also write the upper triangle; bit 1: skip the Schur fill-in contributions
+  const int p0 = bptr[id], pf = p0 + bnff[id], p1 = (sym & 2) ? pf : bptr[id + 1];
   const double damp = 1.0 + lam;
   for (int t = threadIdx.x; t < ra * cb; t += blockDim.x) {
     const int r = t % ra, c = t / ra;
@@ -53,7 +54,7 @@ __global__ void __launch_bounds__(256) k_assemble(const int32_t* __restrict__ bp
     }
     const int64_t gr = roff[a] + r, gc = roff[b] + c;
     H[gc * ld + gr] = v;
-    if (sym) H[gr * ld + gc] = v;
+    if (sym & 1) H[gr * ld + gc] = v;
   }
 }
 
@@ -69,22 +70,49 @@ void launch_assemble(const int32_t* bptr, const int32_t* bnff, const Contrib* cs
 
 __global__ void k_assemble_vec(const int32_t* __restrict__ sptr, const Vec* __restrict__ vs,
                                const int32_t* __restrict__ soff, const int32_t* __restrict__ sdim,
-                               const double* __restrict__ arena, double scale, double* __restrict__ g) {
+                               const double* __restrict__ arena, double scale, int skip_fill,
+                               double* __restrict__ g) {
   const int a = blockIdx.x, r = threadIdx.x;
   if (r >= sdim[a]) return;
   double v = 0.0;
   for (int p = sptr[a]; p < sptr[a + 1]; ++p) {
     const Vec V = vs[p];
+    if (skip_fill && V.sign < 0) continue;   // fill-in contributions are the negative ones
     if (r < V.len) v += (double)V.sign * arena[V.off + r];
   }
   g[soff[a] + r] = scale * v;
 }
 
 void launch_assemble_vec(const int32_t* sptr, const Vec* vs, int nseg, const int32_t* soff, const double* arena,
-                         double scale, double* g, cudaStream_t st) {
+                         double scale, double* g, cudaStream_t st, int skip_fill) {
   // soff[nseg .. 2*nseg) holds the segment dims
   if (nseg <= 0) return;
-  k_assemble_vec<<<nseg, 32, 0, st>>>(sptr, vs, soff, soff + nseg, arena, scale, g);
+  k_assemble_vec<<<nseg, 32, 0, st>>>(sptr, vs, soff, soff + nseg, arena, scale, skip_fill, g);
+  launch_count();
+}
+
+// dense (use_schur=False) path: disparity update from the full solution x[nf + real index]
+__global__ void k_dense_dxd(const double* __restrict__ x, int nf, const int64_t* __restrict__ doff,
+                            const int64_t* __restrict__ roff, const int32_t* __restrict__ npix, int K,
+                            const float* __restrict__ dcur, float* __restrict__ dnxt, float* __restrict__ dxd,
+                            unsigned long long* __restrict__ step_bits) {
+  const int k = blockIdx.y;
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K || n >= npix[k]) return;
+  const double dx = x[nf + roff[k] + n];
+  const int64_t p = doff[k] + n;
+  dnxt[p] = fmaxf((float)((double)dcur[p] + dx), 1e-4f);
+  dxd[p] = (float)dx;
+  const double m = fabs(dx);
+  if (m > 0.0) atomicMax(step_bits, (unsigned long long)__double_as_longlong(m));
+}
+
+void launch_dense_dxd(const double* x, int nf, const int64_t* doff, const int64_t* roff, const int32_t* npix,
+                      int maxpix, int K, const float* dcur, float* dnxt, float* dxd, unsigned long long* step_bits,
+                      cudaStream_t st) {
+  if (K <= 0 || maxpix <= 0) return;
+  dim3 g((maxpix + 255) / 256, K);
+  k_dense_dxd<<<g, 256, 0, st>>>(x, nf, doff, roff, npix, K, dcur, dnxt, dxd, step_bits);
   launch_count();
 }
 

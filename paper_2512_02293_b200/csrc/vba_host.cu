@@ -44,7 +44,7 @@ static void set_err(const char* fmt, ...) {
 constexpr int kTileRt = 1024;   // pixels per per-pixel work tile (kPixBlock * 2 * kTP)
 constexpr int kGramBlock = 512;
 constexpr int kMaxOutDegree = 31;
-constexpr int NBc = 64;
+constexpr int NBc = 128;         // Cholesky tile (vba_chol.cu)
 
 struct Result {       // device -> host once per trial
   double energy[3];
@@ -106,6 +106,10 @@ struct Ctx {
   } red, exp;
   bool exp_built = false;
   double *d_H = nullptr, *d_rhs = nullptr, *d_x = nullptr, *d_Ld = nullptr, *d_dx = nullptr;
+  double* d_cpart = nullptr;       // Cholesky backward-substitution partials
+  int* d_cflags = nullptr;         // Cholesky DAG counters
+  void* d_ctasks = nullptr;        // Cholesky task list
+  int n_ctasks = 0;
   int32_t* d_fmap = nullptr;
   Result* d_res = nullptr;
   Result* h_res = nullptr;
@@ -118,6 +122,14 @@ struct Ctx {
   int64_t* d_roff_real = nullptr;
   int maxpix = 0;
   int64_t n_real = 0;
+  // dense (use_schur=False) verification path, built on first use
+  bool dn_ready = false;
+  int dn_N = 0, dn_npad = 0, dn_nt = 0, n_dtasks = 0;
+  double *d_D = nullptr, *d_drhs = nullptr, *d_dx2 = nullptr, *d_dLinv = nullptr, *d_dpart = nullptr;
+  int* d_dflags = nullptr;
+  void* d_dtasks = nullptr;
+  int32_t* d_kfcol = nullptr;
+  unsigned long long* d_trace = nullptr;   // VBA_CHOL_TRACE: per-task timestamps of the Cholesky DAG
   // profiling
   bool prof = false;
   cudaEvent_t ev[10] = {};
@@ -544,7 +556,12 @@ static int stage_step(Ctx* c, double lam, cudaStream_t st) {
       if (c->coll(c->coll_user, c->d_rhs, c->npad, 0, st)) { set_err("allreduce(g) failed"); return VBA_E_CUDA; }
       launch_add_ridge(c->d_H, c->npad, c->nfree, c->O.ridge, st);
     }
-    chol_solve(c->d_H, c->npad, c->npad, c->d_rhs, c->d_x, c->d_Ld, &c->d_res->status, st);
+    if (getenv("VBA_CHOL_TRACE") && !c->d_trace) {
+      if (dalloc(c, &c->d_trace, (size_t)4 * std::max(1, c->n_ctasks) + 16 * (size_t)std::max(1, c->nt)))
+        return VBA_E_CUDA;
+    }
+    chol_dag_launch(c->d_H, c->npad, c->nt, c->d_rhs, c->d_x, c->d_Ld, c->d_cpart, c->d_cflags, c->d_ctasks,
+                    c->n_ctasks, &c->d_res->status, st, c->d_trace);
   }
   mark(c, 4, st);
   launch_scatter_dx(c->d_x, c->d_fmap, c->npv, c->d_dx, st);
@@ -558,8 +575,96 @@ static int stage_step(Ctx* c, double lam, cudaStream_t st) {
   return VBA_OK;
 }
 
-static int run_trial(Ctx* c, double lam, vba_trial_result* out, cudaStream_t st) {
-  int rc = stage_step(c, lam, st);
+// ---------------------------------------------------------------------------
+// dense reference path (use_schur=False, solver.py:291-304): the full
+// [free poses | disparities] system is materialised and factorised with the
+// same DAG Cholesky.  Meant for small verification problems, like the reference's.
+// ---------------------------------------------------------------------------
+static int ensure_real_layout(Ctx* c, cudaStream_t st) {
+  if (c->d_npix) return VBA_OK;
+  std::vector<int32_t> np(c->P.h_npix, c->P.h_npix + c->K);
+  std::vector<int64_t> ro(c->K + 1, 0);
+  c->maxpix = 0;
+  for (int n = 0; n < c->K; ++n) {
+    ro[n + 1] = ro[n] + np[n];
+    c->maxpix = std::max(c->maxpix, np[n]);
+  }
+  c->n_real = ro[c->K];
+  int rc;
+  if ((rc = dupload(c, &c->d_npix, np, st)) || (rc = dupload(c, &c->d_roff_real, ro, st))) return rc;
+  return VBA_OK;
+}
+
+
+static int ensure_dense(Ctx* c, cudaStream_t st) {
+  if (c->dn_ready) return VBA_OK;
+  int rc = ensure_real_layout(c, st);
+  if (rc) return rc;
+  const int64_t N = c->nfree + c->n_real;
+  if (N > 32768) {
+    set_err("use_schur=False: dense system of %lld unknowns exceeds the verification-path limit", (long long)N);
+    return VBA_E_UNSUPPORTED;
+  }
+  c->dn_N = (int)N;
+  c->dn_npad = (int)((N + NBc - 1) / NBc * NBc);
+  c->dn_nt = c->dn_npad / NBc;
+  const size_t np = (size_t)c->dn_npad;
+  if ((rc = dalloc(c, &c->d_D, np * np)) || (rc = dalloc(c, &c->d_drhs, np)) || (rc = dalloc(c, &c->d_dx2, np)) ||
+      (rc = dalloc(c, &c->d_dLinv, (size_t)c->dn_nt * NBc * NBc)) ||
+      (rc = dalloc(c, &c->d_dpart, (size_t)c->dn_nt * c->dn_nt * NBc)) ||
+      (rc = dalloc(c, &c->d_dflags, (size_t)2 * c->dn_nt * c->dn_nt + c->dn_nt + 1)) ||
+      (rc = dupload(c, &c->d_kfcol, c->kf_col, st)))
+    return rc;
+  const int cap = chol_plan_tasks(c->dn_nt, nullptr, 0);
+  std::vector<char> buf((size_t)std::max(cap, 1) * chol_task_bytes());
+  c->n_dtasks = chol_plan_tasks(c->dn_nt, buf.data(), cap);
+  if ((rc = dalloc(c, (char**)&c->d_dtasks, buf.size()))) return rc;
+  VBA_CUDA(cudaMemcpyAsync(c->d_dtasks, buf.data(), buf.size(), cudaMemcpyHostToDevice, st));
+  c->dn_ready = true;
+  return VBA_OK;
+}
+
+static int stage_step_dense(Ctx* c, double lam, cudaStream_t st) {
+  if (c->coll) { set_err("use_schur=False is single-GPU only"); return VBA_E_UNSUPPORTED; }
+  int rc = ensure_dense(c, st);
+  if (rc) return rc;
+  DevState& s = CUR(c);
+  DevState& n = NXT(c);
+  mark(c, 2, st);
+  VBA_CUDA(cudaMemsetAsync(c->d_res, 0, sizeof(Result), st));
+  VBA_CUDA(cudaMemsetAsync(c->d_D, 0, sizeof(double) * (size_t)c->dn_npad * c->dn_npad, st));
+  VBA_CUDA(cudaMemsetAsync(c->d_drhs, 0, sizeof(double) * c->dn_npad, st));
+  launch_pad_identity(c->d_D, c->dn_npad, c->dn_N, c->dn_npad, c->d_drhs, st);
+  mark(c, 3, st);
+  if (c->nfree > 0) {   // damped H_ff (no fill-in) and -g_f
+    launch_assemble(c->red.bptr, c->red.bnff, c->red.cs, c->red.nbr, c->red.roff, c->red.rdim, c->d_arena, lam,
+                    c->O.ridge, 1, c->d_D, c->dn_npad, 2, st);
+    launch_assemble_vec(c->red.sptr, c->red.vs, c->red.nseg, c->red.soff, c->d_arena, -1.0, c->d_drhs, st, 1);
+  }
+  HpdOut o{c->d_D, c->dn_npad, c->nfree, c->sdof, c->d_kfcol, c->d_Hdd, c->d_gd, c->d_drhs, lam, c->O.ridge};
+  launch_export_hpd(c->P.pixel_mode, c->d_seb, c->d_see, c->d_doff, c->d_roff_real, c->d_npix, c->maxpix, c->d_ej,
+                    c->K, s, c->extr, c->P.pix, c->P.wts, c->d_eoff, c->P.grid_w, c->grid, c->intr, o, st);
+  chol_dag_launch(c->d_D, c->dn_npad, c->dn_nt, c->d_drhs, c->d_dx2, c->d_dLinv, c->d_dpart, c->d_dflags,
+                  c->d_dtasks, c->n_dtasks, &c->d_res->status, st);
+  mark(c, 4, st);
+  launch_scatter_dx(c->d_dx2, c->d_fmap, c->npv, c->d_dx, st);
+  if (c->n_disp) VBA_CUDA(cudaMemcpyAsync(n.disp, s.disp, sizeof(float) * c->n_disp, cudaMemcpyDeviceToDevice, st));
+  launch_dense_dxd(c->d_dx2, c->nfree, c->d_doff, c->d_roff_real, c->d_npix, c->maxpix, c->K, s.disp, n.disp,
+                   c->d_dxd, &c->d_res->step_bits, st);
+  launch_retract(s, n, c->d_dx, c->d_frozen, c->K, c->sdof, c->ngrav, c->n_state, &c->d_res->step_bits, c->npv, st);
+  c->have_step = true;
+  c->last_lam = lam;
+  return VBA_OK;
+}
+
+static int stage_step_any(Ctx* c, double lam, int use_schur, cudaStream_t st) {
+  // the reference takes the Schur path only when there are disparities (solver.py:281)
+  if (use_schur || c->n_disp == 0) return stage_step(c, lam, st);
+  return stage_step_dense(c, lam, st);
+}
+
+static int run_trial(Ctx* c, double lam, int use_schur, vba_trial_result* out, cudaStream_t st) {
+  int rc = stage_step_any(c, lam, use_schur, st);
   if (rc) return rc;
   mark(c, 5, st);
   rc = stage_energy(c, NXT(c), st);
@@ -573,6 +678,48 @@ static int run_trial(Ctx* c, double lam, vba_trial_result* out, cudaStream_t st)
   VBA_CUDA(cudaStreamSynchronize(st));
   prof_collect(c, c->lin_pending);
   c->lin_pending = false;
+  if (c->d_trace && use_schur) {   // Cholesky DAG task timing summary (diagnostics)
+    std::vector<unsigned long long> tr((size_t)4 * c->n_ctasks);
+    std::vector<char> tb((size_t)c->n_ctasks * chol_task_bytes());
+    std::vector<int> f4((size_t)4 * c->n_ctasks);
+    cudaMemcpy(tr.data(), c->d_trace, tr.size() * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(tb.data(), c->d_ctasks, tb.size(), cudaMemcpyDeviceToHost);
+    chol_task_fields(tb.data(), c->n_ctasks, f4.data());
+    unsigned long long t0 = ~0ull, t1 = 0;
+    double busy[5] = {0, 0, 0, 0, 0}, wait[5] = {0, 0, 0, 0, 0};
+    int cnt[5] = {0, 0, 0, 0, 0};
+    for (int q = 0; q < c->n_ctasks; ++q) {
+      t0 = std::min(t0, tr[4 * q]);
+      t1 = std::max(t1, tr[4 * q + 2]);
+      const int ty = f4[4 * q];
+      busy[ty] += (double)(tr[4 * q + 2] - tr[4 * q + 1]) * 1e-3;
+      wait[ty] += (double)(tr[4 * q + 1] - tr[4 * q]) * 1e-3;
+      cnt[ty] += 1;
+    }
+    const char* nm[5] = {"POTRF", "TRSM", "GEMM", "BUPD", "BSOL"};
+    fprintf(stderr, "[chol trace] nt=%d tasks=%d span %.1f us\n", c->nt, c->n_ctasks, (double)(t1 - t0) * 1e-3);
+    {  // POTRF phase stamps: [0] start [1+2p] factor32 done [2+2p] panel done [9] end
+      std::vector<unsigned long long> ph((size_t)16 * c->nt);
+      cudaMemcpy(ph.data(), c->d_trace + 4 * (size_t)c->n_ctasks, ph.size() * 8, cudaMemcpyDeviceToHost);
+      double f = 0, u = 0, inv = 0;
+      for (int k = 0; k < c->nt; ++k) {
+        const unsigned long long* q = &ph[16 * (size_t)k];
+        unsigned long long prev = q[0];
+        for (int p = 0; p < 4; ++p) {
+          f += (double)(q[1 + 2 * p] - prev) * 1e-3;
+          u += (double)(q[2 + 2 * p] - q[1 + 2 * p]) * 1e-3;
+          prev = q[2 + 2 * p];
+        }
+        inv += (double)(q[9] - q[8]) * 1e-3;
+      }
+      fprintf(stderr, "  POTRF phases (avg us): factor32 x4 %.2f | trsm+syrk %.2f | inverse+y %.2f\n", f / c->nt,
+              u / c->nt, inv / c->nt);
+    }
+    for (int ty = 0; ty < 5; ++ty)
+      if (cnt[ty])
+        fprintf(stderr, "  %-5s n=%6d  avg busy %8.2f us  avg wait %8.2f us\n", nm[ty], cnt[ty], busy[ty] / cnt[ty],
+                wait[ty] / cnt[ty]);
+  }
   out->status = c->h_res->status ? VBA_E_NOT_SPD : VBA_OK;
   out->new_cost = c->h_res->energy[0];
   double si;
@@ -660,9 +807,21 @@ int vba_create(void** out, const vba_problem* prob, const vba_options* opts, voi
       (rc = dalloc(c, &c->d_imu_status, 1)) || (rc = dalloc(c, &c->d_H, (size_t)c->npad * c->npad)) ||
       (rc = dalloc(c, &c->d_rhs, (size_t)c->npad)) || (rc = dalloc(c, &c->d_x, (size_t)c->npad)) ||
       (rc = dalloc(c, &c->d_Ld, (size_t)std::max(1, c->nt) * NBc * NBc)) ||
+      (rc = dalloc(c, &c->d_cpart, (size_t)std::max(1, c->nt * c->nt) * NBc)) ||
+      (rc = dalloc(c, &c->d_cflags, (size_t)2 * c->nt * c->nt + c->nt + 1)) ||
       (rc = dalloc(c, &c->d_dx, (size_t)c->npv)) || (rc = dalloc(c, &c->d_res, 1)))
     return fail(rc);
   if (cudaMallocHost((void**)&c->h_res, sizeof(Result)) != cudaSuccess) { set_err("pinned alloc failed"); return fail(VBA_E_CUDA); }
+  {  // Cholesky task DAG (dense, lookahead 1)
+    const int cap = chol_plan_tasks(c->nt, nullptr, 0);
+    std::vector<char> buf((size_t)std::max(cap, 1) * chol_task_bytes());
+    c->n_ctasks = chol_plan_tasks(c->nt, buf.data(), cap);
+    if ((rc = dalloc(c, (char**)&c->d_ctasks, buf.size()))) return fail(rc);
+    if (cudaMemcpyAsync(c->d_ctasks, buf.data(), buf.size(), cudaMemcpyHostToDevice, st) != cudaSuccess) {
+      set_err("task upload failed");
+      return fail(VBA_E_CUDA);
+    }
+  }
   cudaMemsetAsync(c->d_arena, 0, sizeof(double) * std::max<int64_t>(1, c->arena_len), st);
   cudaMemsetAsync(c->d_Hdd, 0, sizeof(float) * std::max<int64_t>(1, c->n_disp), st);
   cudaMemsetAsync(c->d_gd, 0, sizeof(float) * std::max<int64_t>(1, c->n_disp), st);
@@ -732,8 +891,7 @@ int vba_linearize(void* ctx, void* stream) {
 int vba_solve_step(void* ctx, void* stream, double lam, int32_t use_schur) {
   Ctx* c = (Ctx*)ctx;
   cudaStream_t st = (cudaStream_t)stream;
-  if (!use_schur) { set_err("dense (use_schur=False) path not available"); return VBA_E_UNSUPPORTED; }
-  int rc = stage_step(c, lam, st);
+  int rc = stage_step_any(c, lam, use_schur, st);
   if (rc) return rc;
   VBA_CUDA(cudaMemcpyAsync(c->h_res, c->d_res, sizeof(Result), cudaMemcpyDeviceToHost, st));
   VBA_CUDA(cudaStreamSynchronize(st));
@@ -760,8 +918,7 @@ int vba_accept(void* ctx, void* /*stream*/) {
 
 int vba_trial(void* ctx, void* stream, double lam, int32_t use_schur, vba_trial_result* out) {
   Ctx* c = (Ctx*)ctx;
-  if (!use_schur) { set_err("dense (use_schur=False) path not available"); return VBA_E_UNSUPPORTED; }
-  return run_trial(c, lam, out, (cudaStream_t)stream);
+  return run_trial(c, lam, use_schur, out, (cudaStream_t)stream);
 }
 
 int vba_solve(void* ctx, void* stream, vba_report* rep, double* traj, int32_t cap) {
@@ -769,7 +926,6 @@ int vba_solve(void* ctx, void* stream, vba_report* rep, double* traj, int32_t ca
   cudaStream_t st = (cudaStream_t)stream;
   const vba_options& o = c->O;
   std::memset(rep, 0, sizeof(*rep));
-  if (!o.use_schur) { set_err("dense (use_schur=False) path not available"); return VBA_E_UNSUPPORTED; }
   double cost;
   int rc = vba_energy(ctx, stream, &cost, nullptr, nullptr);
   if (rc) return rc;
@@ -794,7 +950,7 @@ int vba_solve(void* ctx, void* stream, vba_report* rep, double* traj, int32_t ca
     bool accepted = false;
     while (true) {
       vba_trial_result r;
-      if ((rc = run_trial(c, lam, &r, st))) return rc;
+      if ((rc = run_trial(c, lam, o.use_schur, &r, st))) return rc;
       ++trials;
       if (r.status == VBA_E_NOT_SPD) {   // solver.py:373-379
         ++warns;
@@ -835,21 +991,6 @@ int vba_download(void* ctx, void* stream) {
   return VBA_OK;
 }
 
-static int ensure_real_layout(Ctx* c, cudaStream_t st) {
-  if (c->d_npix) return VBA_OK;
-  std::vector<int32_t> np(c->P.h_npix, c->P.h_npix + c->K);
-  std::vector<int64_t> ro(c->K + 1, 0);
-  c->maxpix = 0;
-  for (int n = 0; n < c->K; ++n) {
-    ro[n + 1] = ro[n] + np[n];
-    c->maxpix = std::max(c->maxpix, np[n]);
-  }
-  c->n_real = ro[c->K];
-  int rc;
-  if ((rc = dupload(c, &c->d_npix, np, st)) || (rc = dupload(c, &c->d_roff_real, ro, st))) return rc;
-  return VBA_OK;
-}
-
 int vba_export_normal_eq(void* ctx, void* stream, double* H_pp, double* g_p, double* H_pd, double* H_dd,
                          double* g_d) {
   Ctx* c = (Ctx*)ctx;
@@ -868,9 +1009,9 @@ int vba_export_normal_eq(void* ctx, void* stream, double* H_pp, double* g_p, dou
   if (g_d) launch_unpad(c->d_gd, c->d_doff, c->d_roff_real, c->d_npix, c->maxpix, c->K, g_d, st);
   if (H_pd) {
     VBA_CUDA(cudaMemsetAsync(H_pd, 0, sizeof(double) * c->npv * std::max<int64_t>(1, c->n_real), st));
+    HpdOut o{H_pd, c->n_real, 0, c->sdof, nullptr, nullptr, nullptr, nullptr, 0.0, 0.0};
     launch_export_hpd(c->P.pixel_mode, c->d_seb, c->d_see, c->d_doff, c->d_roff_real, c->d_npix, c->maxpix, c->d_ej,
-                      c->K, s, c->extr, c->P.pix, c->P.wts, c->d_eoff, c->P.grid_w, c->grid, c->intr, c->sdof,
-                      c->n_real, H_pd, st);
+                      c->K, s, c->extr, c->P.pix, c->P.wts, c->d_eoff, c->P.grid_w, c->grid, c->intr, o, st);
   }
   VBA_CUDA(cudaStreamSynchronize(st));
   return VBA_OK;

@@ -296,16 +296,41 @@ void launch_assemble(const int32_t* blk_ptr, const int32_t* blk_nff, const Contr
                      const int32_t* blk_row_off, const int32_t* blk_dim, const double* arena, double lam,
                      double ridge, int add_ridge, double* H, int64_t ld, int symmetric_out, cudaStream_t st);
 void launch_assemble_vec(const int32_t* seg_ptr, const Vec* vecs, int nseg, const int32_t* seg_off,
-                         const double* arena, double scale, double* g, cudaStream_t st);
+                         const double* arena, double scale, double* g, cudaStream_t st, int skip_fill = 0);
 void launch_add_ridge(double* H, int64_t ld, int n, double ridge, cudaStream_t st);
 void launch_pad_identity(double* H, int64_t ld, int n, int npad, double* rhs, cudaStream_t st);
+// tile-task DAG Cholesky (vba_chol.cu): plan writes up to `cap` task records into `out`
+// (opaque, chol_task_bytes() each) and returns the task count
+int chol_plan_tasks(int nt, void* out, int cap);
+size_t chol_task_bytes();
+int chol_dag_launch(double* A, int64_t ld, int nt, double* rhs, double* x, double* Linv, double* part, int* flags,
+                    const void* tasks, int ntasks, int* status, cudaStream_t st,
+                    unsigned long long* trace = nullptr);
+// copy the task list back (for trace decoding): type,i,j,k per task
+void chol_task_fields(const void* tasks, int n, int* out4);
 int chol_solve(double* H, int64_t ld, int npad, double* rhs, double* x, double* Ldiag, int* status,
                cudaStream_t st);
 void launch_scatter_dx(const double* x, const int32_t* free_map, int npv, double* dx_full, cudaStream_t st);
+// pose-disparity coupling writer: reference-layout export (colmap == NULL, rows k*sdof+a) or the
+// free-layout full dense system of the use_schur=False path (rows colmap[k]+a, plus the damped
+// disparity diagonal and right-hand side when Hdd != NULL).  Entry (row, base+col) at H[row*ld + base+col].
+struct HpdOut {
+  double* H;
+  int64_t ld, base;
+  int sdof;
+  const int32_t* colmap;
+  const float* Hdd;
+  const float* gd;
+  double* rhs;
+  double lam, ridge;
+};
 void launch_export_hpd(int mode, const int32_t* seb, const int32_t* see, const int64_t* doff, const int64_t* roff,
                        const int32_t* npix, int maxpix, const int32_t* ej, int K, const DevState& s, const Extr& x,
                        const float* pix, const float* wts, const int64_t* eoff, int grid_w, const double* grid,
-                       const double* intr, int sdof, int64_t ncol, double* H, cudaStream_t st);
+                       const double* intr, const HpdOut& out, cudaStream_t st);
+void launch_dense_dxd(const double* x, int nf, const int64_t* doff, const int64_t* roff, const int32_t* npix,
+                      int maxpix, int K, const float* dcur, float* dnxt, float* dxd, unsigned long long* step_bits,
+                      cudaStream_t st);
 void launch_unpad(const float* src, const int64_t* doff, const int64_t* roff, const int32_t* npix, int maxpix, int K,
                   double* dst, cudaStream_t st);
 void launch_count();   // instrumentation hook

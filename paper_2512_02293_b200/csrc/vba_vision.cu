@@ -978,14 +978,19 @@ __global__ void k_export_hpd(const int32_t* __restrict__ seb, const int32_t* __r
                              const float* __restrict__ disp, const EdgeGeo32* __restrict__ geo,
                              const double* __restrict__ geo64, Extr x, const float* __restrict__ pix,
                              const float* __restrict__ wts, const int64_t* __restrict__ eoff, int grid_w, GridP gp,
-                             IntrP in, int sdof, int64_t ncol, double* __restrict__ H) {
+                             IntrP in, HpdOut out) {
   const int src = blockIdx.y;
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (src >= K || n >= npix[src]) return;
   const int64_t kbase = doff[src];
-  const int64_t col = roff[src] + n;
+  const int64_t col = out.base + roff[src] + n;
   const float fx2 = (float)(in.fx * in.fx), fy2 = (float)(in.fy * in.fy);
   const float d = disp[kbase + n];
+  // pose row of keyframe k, entry a: reference layout k*sdof + a, or the free layout (frozen -> skip)
+  auto prow = [&](int k, int a) -> int64_t {
+    if (!out.colmap) return (int64_t)k * out.sdof + a;
+    return out.colmap[k] < 0 ? -1 : (int64_t)out.colmap[k] + a;
+  };
   double hi[6] = {0, 0, 0, 0, 0, 0};
   for (int e = seb[src]; e < see[src]; ++e) {
     float rx, ry, rx1, ry1;
@@ -1019,32 +1024,37 @@ __global__ void k_export_hpd(const int32_t* __restrict__ seb, const int32_t* __r
         sj += Gj[m * 6 + a] * (double)u[m];
       }
       hi[a] += si;
-      H[((int64_t)j * sdof + a) * ncol + col] -= sj;
+      const int64_t r = prow(j, a);
+      if (r >= 0) out.H[r * out.ld + col] -= sj;
     }
   }
-  for (int a = 0; a < 6; ++a) H[((int64_t)src * sdof + a) * ncol + col] += hi[a];
+  for (int a = 0; a < 6; ++a) {
+    const int64_t r = prow(src, a);
+    if (r >= 0) out.H[r * out.ld + col] += hi[a];
+  }
+  if (out.Hdd) {   // dense system: damped disparity diagonal and right-hand side (solver.py:292-301)
+    out.H[col * out.ld + col] = (double)out.Hdd[kbase + n] * (1.0 + out.lam) + out.ridge;
+    out.rhs[col] = -(double)out.gd[kbase + n];
+  }
 }
 
 void launch_export_hpd(int mode, const int32_t* seb, const int32_t* see, const int64_t* doff, const int64_t* roff,
                        const int32_t* npix, int maxpix, const int32_t* ej, int K, const DevState& s, const Extr& x,
                        const float* pix, const float* wts, const int64_t* eoff, int grid_w, const double* grid,
-                       const double* intr, int sdof, int64_t ncol, double* H, cudaStream_t st) {
+                       const double* intr, const HpdOut& out, cudaStream_t st) {
   if (K <= 0 || maxpix <= 0) return;
   GridP gp{grid[0], grid[1], grid[2], grid[3]};
   IntrP in{intr[0], intr[1], intr[2], intr[3]};
-  dim3 grd((maxpix + 127) / 128, K);
-  // one source per grid row; sources are independent, edges of a source are serial per pixel
-  for (int m = 0; m < 1; ++m) {
-    if (mode == VBA_PIX_GRID)
-      k_export_hpd<VBA_PIX_GRID><<<grd, 128, 0, st>>>(seb, see, doff, roff, npix, ej, K, s.disp, s.geo32, s.geo64, x,
-                                                      pix, wts, eoff, grid_w, gp, in, sdof, ncol, H);
-    else if (mode == VBA_PIX_KF)
-      k_export_hpd<VBA_PIX_KF><<<grd, 128, 0, st>>>(seb, see, doff, roff, npix, ej, K, s.disp, s.geo32, s.geo64, x,
-                                                    pix, wts, eoff, grid_w, gp, in, sdof, ncol, H);
-    else
-      k_export_hpd<VBA_PIX_EDGE><<<grd, 128, 0, st>>>(seb, see, doff, roff, npix, ej, K, s.disp, s.geo32, s.geo64, x,
-                                                      pix, wts, eoff, grid_w, gp, in, sdof, ncol, H);
-  }
+  dim3 grd((maxpix + 127) / 128, K);   // one source per grid row; a pixel's edges are serial in its thread
+  if (mode == VBA_PIX_GRID)
+    k_export_hpd<VBA_PIX_GRID><<<grd, 128, 0, st>>>(seb, see, doff, roff, npix, ej, K, s.disp, s.geo32, s.geo64, x,
+                                                    pix, wts, eoff, grid_w, gp, in, out);
+  else if (mode == VBA_PIX_KF)
+    k_export_hpd<VBA_PIX_KF><<<grd, 128, 0, st>>>(seb, see, doff, roff, npix, ej, K, s.disp, s.geo32, s.geo64, x,
+                                                  pix, wts, eoff, grid_w, gp, in, out);
+  else
+    k_export_hpd<VBA_PIX_EDGE><<<grd, 128, 0, st>>>(seb, see, doff, roff, npix, ej, K, s.disp, s.geo32, s.geo64, x,
+                                                    pix, wts, eoff, grid_w, gp, in, out);
   launch_count();
 }
 

@@ -90,6 +90,17 @@ def test_solve_step(name, cuda_ok):
     assert rel(dxd, out["dxd"]) < tol_update(name, out, "dxd")
 
 
+@pytest.mark.parametrize("name", ["win8_px30", "win5_gravity", "win6_frozen2", "cfg0_grid12x16"])
+def test_dense_path_step(name, cuda_ok):
+    """use_schur=False (solver.py:291-304) gives the reference's step too."""
+    P, out, opts = load_golden(name)
+    dp = _dp(P, dict(opts, use_schur=False))
+    dp.linearize()
+    dx, dxd = dp.solve_step(opts["damping"], use_schur=False)
+    assert rel(dx, out["dx"]) < tol_update(name, out, "dx")
+    assert rel(dxd, out["dxd"]) < tol_update(name, out, "dxd")
+
+
 def test_baseline_shaped_step_within_north_star(cuda_ok):
     """The BASELINE-shaped fixture meets 1e-5 on both update families outright."""
     P, out, opts = load_golden("cfg0_grid12x16")
