@@ -38,7 +38,8 @@ enum TaskType { T_POTRF = 0, T_TRSM = 1, T_GEMM = 2, T_BUPD = 3, T_BSOL = 4 };
 struct CholTask {
   int32_t type, i, j, k;
   int32_t expect;   // updates expected on the target tile before this task (envelope-ready)
-  int32_t pad[3];
+  int32_t k2;       // GEMM: second update column applied in the same task (-1: none)
+  int32_t pad[2];
 };
 
 // ---------------------------------------------------------------------------
@@ -97,14 +98,16 @@ __device__ __forceinline__ void load_chunk(double* sA, double* sB, const double*
 }
 
 __device__ __forceinline__ void gemm_tile(double* smem, const double* A, int64_t lda, const double* B, int64_t ldb,
-                                          double (&acc)[8][4][2]) {
+                                          double (&acc)[8][4][2], bool zero = true) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int wm = w & 1, wn = w >> 1;
   // stage s: A at smem + s*2*KC*SP, B right after it (arithmetic, no pointer arrays)
+  if (zero) {
 #pragma unroll
-  for (int a = 0; a < 8; ++a)
+    for (int a = 0; a < 8; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+      for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  }
   load_chunk(smem, smem + KC * SP, A, lda, B, ldb, 0);
   const int ar = 64 * wm + (lane >> 2), br = 32 * wn + (lane >> 2), kq = lane & 3;
 #pragma unroll 1
@@ -177,10 +180,9 @@ __device__ __forceinline__ double* tile(const CholArgs& a, int i, int j) {
 // threads (thread = (row r, column group cg), 4 columns each), two barriers per
 // step.  On return W holds L (lower) and Ib (column-major, stride SB) L^-1.
 __device__ __forceinline__ void cta_potrf32(double* W, int sw, double* Ib, int* bad) {
-  const int tid = threadIdx.x, r = tid & 31, cg = tid >> 5;
+  const int tid = threadIdx.x, r = tid & 31, cg = tid >> 5;   // 4 columns per thread: c = cg + 8q
 #pragma unroll
   for (int q = 0; q < 4; ++q) Ib[(cg + 8 * q) * SB + r] = (cg + 8 * q == r) ? 1.0 : 0.0;
-  __syncthreads();
 #pragma unroll 1
   for (int j = 0; j < 32; ++j) {
     __syncthreads();                                   // updates of step j-1 complete
@@ -199,12 +201,23 @@ __device__ __forceinline__ void cta_potrf32(double* W, int sw, double* Ib, int* 
     }
     __syncthreads();
     if (r > j) {
+      // all loads first (independent), then the updates: no aliasing-serialised RMW chains
       const double lr = W[j * sw + r];
+      double cur[4], piv4[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int c = cg + 8 * q;
-        if (c > j && c <= r) W[c * sw + r] -= lr * W[j * sw + c];
-        else if (c <= j) Ib[c * SB + r] -= lr * Ib[c * SB + j];
+        double* dst = (c > j) ? &W[c * sw + r] : &Ib[c * SB + r];
+        cur[q] = *dst;
+        piv4[q] = (c > j) ? W[j * sw + c] : Ib[c * SB + j];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = cg + 8 * q;
+        if (c <= r) {
+          double* dst = (c > j) ? &W[c * sw + r] : &Ib[c * SB + r];
+          *dst = cur[q] - lr * piv4[q];
+        }
       }
     }
   }
@@ -383,11 +396,12 @@ __device__ void task_trsm(const CholArgs& a, int i, int k, double* smem) {
   }
 }
 
-// GEMM(i,j,k): A_ij -= L_ik L_jk^T
-__device__ void task_gemm(const CholArgs& a, int i, int j, int k, double* smem) {
+// GEMM(i,j,k[,k2]): A_ij -= L_ik L_jk^T (+ L_ik2 L_jk2^T), one read-modify-write of A_ij
+__device__ void task_gemm(const CholArgs& a, int i, int j, int k, int k2, double* smem) {
   double acc[8][4][2];
   // acc(c, r) = sum_m L_jk(c, m) L_ik(r, m) = (L_ik L_jk^T)(r, c)
   gemm_tile(smem, tile(a, j, k), a.ld, tile(a, i, k), a.ld, acc);
+  if (k2 >= 0) gemm_tile(smem, tile(a, j, k2), a.ld, tile(a, i, k2), a.ld, acc, false);
   double* C = tile(a, i, j);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int wm = w & 1, wn = w >> 1;
@@ -496,13 +510,17 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_dag(CholArgs a) {
       case T_GEMM:
         wait_geq(&a.done[T.i * nt + T.k], 1);
         wait_geq(&a.done[T.j * nt + T.k], 1);
+        if (T.k2 >= 0) {
+          wait_geq(&a.done[T.i * nt + T.k2], 1);
+          wait_geq(&a.done[T.j * nt + T.k2], 1);
+        }
         wait_geq(&a.upd[T.i * nt + T.j], T.expect);
         __syncthreads();
         if (a.trace && threadIdx.x == 0) a.trace[4 * t + 1] = gtimer();
-        task_gemm(a, T.i, T.j, T.k, smem);
+        task_gemm(a, T.i, T.j, T.k, T.k2, smem);
         __threadfence();
         __syncthreads();
-        if (threadIdx.x == 0) st_release(&a.upd[T.i * nt + T.j], T.expect + 1);
+        if (threadIdx.x == 0) st_release(&a.upd[T.i * nt + T.j], T.expect + (T.k2 >= 0 ? 2 : 1));
         break;
       case T_BUPD:
         wait_geq(&a.done[T.k * nt + T.k], 2);        // x_k solved (BSOL sets done[k][k] = 2)
@@ -543,19 +561,27 @@ size_t chol_task_bytes() { return sizeof(CholTask); }
 int chol_plan_tasks(int nt, void* outv, int cap) {
   CholTask* out = reinterpret_cast<CholTask*>(outv);
   int n = 0;
-  auto push = [&](int type, int i, int j, int k, int expect) {
-    if (n < cap) out[n] = CholTask{type, i, j, k, expect, {0, 0, 0}};
+  auto push = [&](int type, int i, int j, int k, int expect, int k2 = -1) {
+    if (n < cap) out[n] = CholTask{type, i, j, k, expect, k2, {0, 0}};
     ++n;
   };
   if (nt <= 0) return 0;
+  // Lookahead-1 order.  Tile (i,j) receives updates k = 0..j-1: the last one
+  // (k = j-1, the next panel column) is a single high-priority task; the earlier
+  // ones are merged statically in pairs (0,1), (2,3), ... (a lone last one when
+  // j-2 is even), placed at the step of their second column.  Static pairing keeps
+  // the summation order — and the result — bitwise reproducible.
   push(T_POTRF, 0, 0, 0, 0);
   for (int i = 1; i < nt; ++i) push(T_TRSM, i, 0, 0, 0);
-  for (int k = 0; k + 1 < nt; ++k) {
-    for (int i = k + 1; i < nt; ++i) push(T_GEMM, i, k + 1, k, k);      // next panel column first
-    push(T_POTRF, k + 1, k + 1, k + 1, k + 1);
-    for (int i = k + 2; i < nt; ++i) push(T_TRSM, i, k + 1, k + 1, k + 1);
-    for (int j = k + 2; j < nt; ++j)
-      for (int i = j; i < nt; ++i) push(T_GEMM, i, j, k, k);
+  for (int s = 0; s + 1 < nt; ++s) {
+    for (int i = s + 1; i < nt; ++i) push(T_GEMM, i, s + 1, s, s);      // next panel column first
+    push(T_POTRF, s + 1, s + 1, s + 1, s + 1);
+    for (int i = s + 2; i < nt; ++i) push(T_TRSM, i, s + 1, s + 1, s + 1);
+    for (int j = s + 2; j < nt; ++j)
+      for (int i = j; i < nt; ++i) {
+        if (s & 1) push(T_GEMM, i, j, s - 1, s - 1, s);                  // pair (s-1, s)
+        else if (s == j - 2) push(T_GEMM, i, j, s, s);                   // lone last non-critical update
+      }
   }
   for (int k = nt - 1; k >= 0; --k) {
     push(T_BSOL, k, k, k, nt - 1 - k);

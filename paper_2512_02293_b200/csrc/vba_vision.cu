@@ -38,9 +38,9 @@ __host__ __device__ __forceinline__ int gram_px_stride(int kmax) {
   return ((s / 4) & 1) ? s : s + 4;
 }
 
-size_t gram_smem_bytes(int kmax, int nsplit, int npairs, int k) {
-  return (size_t)kGramPC * gram_px_stride(kmax) * 4 + kGramPC * 4 +
-         (size_t)nsplit * (npairs * 36 + k * 6) * 8;
+// dynamic shared memory of the DMMA Gram kernel: U and V, (6 kmax + 1 -> 8) columns x (PC + 4) pixels, fp64
+size_t gram_smem_bytes(int kmax, int /*nsplit*/, int /*npairs*/, int /*k*/) {
+  return (size_t)2 * ((6 * kmax + 1 + 7) / 8 * 8) * (kGramPC + 4) * sizeof(double);
 }
 struct IntrP { double fx, fy, cx, cy; };
 
@@ -480,55 +480,79 @@ void launch_edge_finalize(const int32_t* t0s, const int32_t* t1s, const PixTile*
 }
 
 // ---------------------------------------------------------------------------
-// K4: Schur fill-in Gram (per LM trial, λ-dependent).
+// K4: Schur fill-in Gram (per LM trial, λ-dependent), on the fp64 tensor cores.
 //   C_{e1 e2} = sum_n k_{n,e1} k_{n,e2}^T / Hdd_d(n),   b_e = sum_n k_{n,e} g_d(n) / Hdd_d(n)
-// with k_{n,e} = sum_c w_c K_c^T J_d,c the per-pixel coupling (K-space).  One CTA per
-// (source, pixel range); pixels are staged PC at a time in shared memory, each
-// thread owns one 6x6 block pair (e1 >= e2) for a pixel split, accumulating fp32
-// over the chunk and fp64 in shared memory across chunks.
+// with k_{n,e} = sum_c w_c K_c^T J_d,c the per-pixel coupling (K-space).  One CTA
+// (16 warps) per (source, pixel range).  Per 32-pixel chunk the CTA computes the
+// fp32 coupling vectors and widens them exactly to fp64 in shared memory as
+//   U = [k_{n,e} (6k columns) | g_d(n)]   and   V = k_{n,e} / Hdd_d(n)
+// (column-major [column][pixel], stride GPX = 36 ≡ 4 mod 16: conflict-free DMMA
+// fragments), then C = U^T V accumulates with mma.sync m8n8k4 f64 in registers
+// across all chunks (each warp owns up to GMAXT 8x8 output tiles of the lower
+// band).  The last row of C is b.  fp64 products of fp32 factors are exact and
+// all sums are fp64: no fp32 partial-sum error, fixed order (deterministic).
 // ---------------------------------------------------------------------------
+constexpr int GPX = kGramPC + 4;   // pixel stride of the U / V columns (doubles)
+constexpr int GMAXT = 22;          // 8x8 output tiles per warp (k <= 31)
+constexpr int GWARPS = 16;
+
+__device__ __forceinline__ void gdmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
 template <int MODE>
-__global__ void k_gram(const GramTile* __restrict__ gts, const float* __restrict__ disp,
-                       const EdgeGeo32* __restrict__ geo, const float* __restrict__ pix,
-                       const float* __restrict__ wts, const int64_t* __restrict__ eoff,
-                       const int64_t* __restrict__ doff, int grid_w, GridP gp, IntrP in,
-                       const float* __restrict__ Hdd, const float* __restrict__ gd, double lam, double ridge,
-                       int kmax, double* __restrict__ out) {
+__global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
+    const GramTile* __restrict__ gts, const float* __restrict__ disp, const EdgeGeo32* __restrict__ geo,
+    const float* __restrict__ pix, const float* __restrict__ wts, const int64_t* __restrict__ eoff,
+    const int64_t* __restrict__ doff, int grid_w, GridP gp, IntrP in, const float* __restrict__ Hdd,
+    const float* __restrict__ gd, double lam, double ridge, int kmax, double* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const GramTile T = gts[blockIdx.x];
   const int k = T.ee - T.eb;
   const int npairs = k * (k + 1) / 2;
-  const int nsplit = T.nsplit;
-  const int S = gram_px_stride(kmax);
-  float* stage = reinterpret_cast<float*>(smem_raw);                  // [PC][S]: per edge u[6] v[6]
-  float* sgd = stage + kGramPC * S;                                   // [PC]
-  double* acc = reinterpret_cast<double*>(sgd + kGramPC);             // [nsplit][npairs][36]
-  double* accb = acc + (int64_t)nsplit * npairs * 36;                 // [nsplit][k][6]
-  const int tid = threadIdx.x, nth = blockDim.x;
+  const int NRmax = (6 * kmax + 1 + 7) / 8 * 8;
+  double* U = reinterpret_cast<double*>(smem_raw);   // [NRmax][GPX]
+  double* V = U + (size_t)NRmax * GPX;               // [NRmax][GPX]
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int64_t kbase = doff[T.src];
   const float fx = (float)in.fx, fy = (float)in.fy;
   const float fx2 = fx * fx, fy2 = fy * fy;
   const double damp = 1.0 + lam;
-
-  for (int i = tid; i < nsplit * (npairs * 36 + k * 6); i += nth) acc[i] = 0.0;
-
-  const int pidx = tid % npairs;
-  const int sp = tid / npairs;
-  const bool active = sp < nsplit;
-  int e1 = (int)((sqrtf(8.f * pidx + 1.f) - 1.f) * 0.5f);
-  while ((e1 + 1) * (e1 + 2) / 2 <= pidx) ++e1;
-  while (e1 * (e1 + 1) / 2 > pidx) --e1;
-  const int e2 = pidx - e1 * (e1 + 1) / 2;
+  const int nc = 6 * k;
+  const int NRt = (nc + 1 + 7) / 8, NCt = (nc + 7) / 8;   // row / column tiles of C
+  // output tiles: lower band tj <= ti + 1 (6x6 blocks may straddle the 8-tile diagonal);
+  // tile t belongs to warp t % GWARPS, slot t / GWARPS
+  __shared__ short tile_i[GWARPS * GMAXT], tile_j[GWARPS * GMAXT];
+  __shared__ int ntiles_s;
+  if (tid == 0) {
+    int t = 0;
+    for (int ti = 0; ti < NRt; ++ti)
+      for (int tj = 0; tj <= ti + 1 && tj < NCt; ++tj)
+        if (t < GWARPS * GMAXT) {
+          tile_i[t] = (short)ti;
+          tile_j[t] = (short)tj;
+          ++t;
+        }
+    ntiles_s = t;
+  }
+  __syncthreads();
+  const int ntl = ntiles_s;
+  const int nmine = (ntl - warp + GWARPS - 1) / GWARPS;
+  double acc[GMAXT][2];
+#pragma unroll
+  for (int q = 0; q < GMAXT; ++q) acc[q][0] = acc[q][1] = 0.0;
+  for (int i = tid; i < 2 * NRmax * GPX; i += nth) U[i] = 0.0;   // padding columns stay zero
 
   for (int c0 = T.n0; c0 < T.n1; c0 += kGramPC) {
     __syncthreads();
-    // phase 1: per-(pixel, edge) coupling vectors u = k, v = k / Hdd_d
+    // phase 1: coupling vectors of (pixel, edge) items, widened to fp64
     for (int it = tid; it < kGramPC * k; it += nth) {
       const int e = it / kGramPC, px = it % kGramPC;
       const int n = c0 + px;
-      float* dst = stage + px * S + e * kGramStride;
       float u[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      float inv = 0.f;
+      double inv = 0.0;
       if (n < T.n1) {
         const float d = disp[kbase + n];
         float rx, ry, rx1, ry1;
@@ -551,63 +575,47 @@ __global__ void k_gram(const GramTile* __restrict__ gts, const float* __restrict
         u[3] = c0w * -o.iz;
         u[4] = c1w * -o.iz;
         u[5] = fmaf(c0w, o.x * o.iz, c1w * (o.y * o.iz));
-        inv = (float)(1.0 / ((double)Hdd[kbase + n] * damp + ridge));
-        if (e == 0) sgd[px] = gd[kbase + n];
+        inv = 1.0 / ((double)Hdd[kbase + n] * damp + ridge);
+        if (e == 0) U[(size_t)nc * GPX + px] = (double)gd[kbase + n];
       } else if (e == 0) {
-        sgd[px] = 0.f;
+        U[(size_t)nc * GPX + px] = 0.0;
       }
-      float4* d4 = reinterpret_cast<float4*>(dst);
-      d4[0] = make_float4(u[0], u[1], u[2], u[3]);
-      d4[1] = make_float4(u[4], u[5], u[0] * inv, u[1] * inv);
-      d4[2] = make_float4(u[2] * inv, u[3] * inv, u[4] * inv, u[5] * inv);
+#pragma unroll
+      for (int r = 0; r < 6; ++r) {
+        U[(size_t)(6 * e + r) * GPX + px] = (double)u[r];
+        V[(size_t)(6 * e + r) * GPX + px] = (double)u[r] * inv;
+      }
     }
     __syncthreads();
-    // phase 2: block-pair accumulation
-    if (active) {
-      float a[36];
+    // phase 2: C += U^T V on the fp64 tensor cores, 8 pixel-steps of 4
+    const int am = lane >> 2, ak = lane & 3;
 #pragma unroll
-      for (int i = 0; i < 36; ++i) a[i] = 0.f;
-      float bb[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      for (int px = sp; px < kGramPC; px += nsplit) {
-        const float* su = stage + px * S + e1 * kGramStride;
-        const float* sv = stage + px * S + e2 * kGramStride + 6;
-        const float4 u03 = *reinterpret_cast<const float4*>(su);
-        const float2 u45 = *reinterpret_cast<const float2*>(su + 4);
-        const float2 v01 = *reinterpret_cast<const float2*>(sv);
-        const float4 v25 = *reinterpret_cast<const float4*>(sv + 2);
-        const float uu[6] = {u03.x, u03.y, u03.z, u03.w, u45.x, u45.y};
-        const float vv[6] = {v01.x, v01.y, v25.x, v25.y, v25.z, v25.w};
+    for (int q = 0; q < GMAXT; ++q) {
+      if (q < nmine) {
+        const double* pa = U + (size_t)(tile_i[warp + GWARPS * q] * 8 + am) * GPX + ak;
+        const double* pb = V + (size_t)(tile_j[warp + GWARPS * q] * 8 + am) * GPX + ak;
 #pragma unroll
-        for (int r = 0; r < 6; ++r)
-#pragma unroll
-          for (int c = 0; c < 6; ++c) a[r * 6 + c] = fmaf(uu[r], vv[c], a[r * 6 + c]);
-        if (e1 == e2) {
-          const float gdn = sgd[px];
-#pragma unroll
-          for (int r = 0; r < 6; ++r) bb[r] = fmaf(vv[r], gdn, bb[r]);
-        }
-      }
-      double* my = acc + ((int64_t)sp * npairs + pidx) * 36;
-#pragma unroll
-      for (int i = 0; i < 36; ++i) my[i] += (double)a[i];
-      if (e1 == e2) {
-        double* mb = accb + ((int64_t)sp * k + e1) * 6;
-#pragma unroll
-        for (int r = 0; r < 6; ++r) mb[r] += (double)bb[r];
+        for (int ks = 0; ks < kGramPC / 4; ++ks) gdmma(acc[q][0], acc[q][1], pa[4 * ks], pb[4 * ks]);
       }
     }
   }
-  __syncthreads();
+  // epilogue: scatter the lower 6x6 blocks (e1 >= e2) and the b row into the output layout
   double* o = out + T.out;
-  for (int i = tid; i < npairs * 36; i += nth) {
-    double s = 0.0;
-    for (int q = 0; q < nsplit; ++q) s += acc[(int64_t)q * npairs * 36 + i];
-    o[i] = s;
-  }
-  for (int i = tid; i < k * 6; i += nth) {
-    double s = 0.0;
-    for (int q = 0; q < nsplit; ++q) s += accb[(int64_t)q * k * 6 + i];
-    o[npairs * 36 + i] = s;
+#pragma unroll
+  for (int q = 0; q < GMAXT; ++q) {
+    if (q >= nmine) continue;
+    const int a = tile_i[warp + GWARPS * q] * 8 + (lane >> 2);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int b = tile_j[warp + GWARPS * q] * 8 + 2 * (lane & 3) + h;
+      if (b >= nc) continue;
+      if (a < nc) {
+        const int e1 = a / 6, e2 = b / 6;
+        if (e1 >= e2) o[(e1 * (e1 + 1) / 2 + e2) * 36 + (a % 6) * 6 + (b % 6)] = acc[q][h];
+      } else if (a == nc) {
+        o[npairs * 36 + b] = acc[q][h];
+      }
+    }
   }
 }
 
