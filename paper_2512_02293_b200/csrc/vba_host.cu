@@ -70,6 +70,11 @@ struct Ctx {
   double intr[4];
   // host plan
   std::vector<PixTile> tiles;
+  std::vector<PixTile> chunks;      // K1/K2 work units (tiles or edge halves of tiles)
+  bool k1_split = false;
+  std::vector<int32_t> soff, sids, ioff;
+  std::vector<StreamItem> sitems;   // K1/K2 static LPT schedule: CTA b owns sids[soff[b] .. soff[b+1])
+  int ncta = 0;
   std::vector<int32_t> t0s, t1s, seb, see;
   std::vector<GramTile> gtiles;
   std::vector<int32_t> gsrc, g0, g1;
@@ -88,6 +93,9 @@ struct Ctx {
   int32_t *d_ei = nullptr, *d_ej = nullptr, *d_fi = nullptr, *d_fj = nullptr, *d_frozen = nullptr;
   int64_t *d_eoff = nullptr, *d_doff = nullptr;
   PixTile* d_tiles = nullptr;
+  int32_t *d_soff = nullptr, *d_sids = nullptr, *d_ioff = nullptr;
+  StreamItem* d_sitems = nullptr;
+  PixTile* d_chunks = nullptr;
   int32_t *d_t0s = nullptr, *d_t1s = nullptr, *d_seb = nullptr, *d_see = nullptr;
   GramTile* d_gtiles = nullptr;
   int32_t *d_gsrc = nullptr, *d_g0 = nullptr, *d_g1 = nullptr;
@@ -361,6 +369,71 @@ static int build_plans(Ctx* c, cudaStream_t st) {
     c->t1s[n] = (int)c->tiles.size();
   }
   c->n_part = poff;
+  {  // K1/K2 schedule.  Work units ("chunks") are tiles with out-edges, split into two
+     // halves of their edge list when there are too few tiles per CTA to balance
+     // (then H_dd / g_d get the two partial sums by atomic adds onto zero: two
+     // addends, so the result is order-independent); longest first, each to the
+     // least-loaded CTA (LPT).
+    const int G = vision_stream_ctas();
+    int nt_edges = 0;
+    for (const PixTile& T : c->tiles) nt_edges += T.ee > T.eb;
+    const bool split = nt_edges < 8 * G;
+    c->chunks.clear();
+    c->k1_split = false;
+    for (const PixTile& T : c->tiles) {
+      const int k = T.ee - T.eb;
+      if (k <= 0) continue;
+      if (split && k >= 2) {
+        PixTile a = T, b = T;
+        a.ee = T.eb + (k + 1) / 2;
+        b.eb = a.ee;
+        b.poff = T.poff + (b.eb - T.eb);
+        a.pad = b.pad = 1;   // partial H_dd / g_d: accumulate atomically
+        c->chunks.push_back(a);
+        c->chunks.push_back(b);
+        c->k1_split = true;
+      } else {
+        PixTile a = T;
+        a.pad = 0;
+        c->chunks.push_back(a);
+      }
+    }
+    std::vector<int32_t> order(c->chunks.size());
+    for (int t = 0; t < (int)order.size(); ++t) order[t] = t;
+    auto work = [&](int t) {   // edge-pixels plus ~2 edges' worth of per-chunk setup
+      return (int64_t)(c->chunks[t].ee - c->chunks[t].eb + 2) * c->chunks[t].cnt;
+    };
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return work(a) > work(b); });
+    c->ncta = std::min<int>(G, (int)order.size());
+    std::vector<std::vector<int32_t>> bins(c->ncta);
+    std::vector<std::pair<int64_t, int>> heap;
+    for (int b = 0; b < c->ncta; ++b) heap.push_back({0, b});
+    auto cmp = [](const std::pair<int64_t, int>& x, const std::pair<int64_t, int>& y) { return x > y; };
+    std::make_heap(heap.begin(), heap.end(), cmp);
+    for (int t : order) {
+      std::pop_heap(heap.begin(), heap.end(), cmp);
+      heap.back().first += work(t);
+      bins[heap.back().second].push_back(t);
+      std::push_heap(heap.begin(), heap.end(), cmp);
+    }
+    c->soff.assign(1, 0);
+    c->sids.clear();
+    c->ioff.assign(1, 0);
+    c->sitems.clear();
+    for (auto& bn : bins) {
+      c->sids.insert(c->sids.end(), bn.begin(), bn.end());
+      c->soff.push_back((int32_t)c->sids.size());
+      for (int t : bn) {
+        const PixTile& T = c->chunks[t];
+        for (int e = T.eb; e < T.ee; ++e)
+          c->sitems.push_back(StreamItem{2 * (P.h_eoff[e] + T.n0), 8 * T.cnt, e});
+      }
+      c->ioff.push_back((int32_t)c->sitems.size());
+    }
+    if (c->sids.empty()) c->sids.push_back(0);
+    if (c->sitems.empty()) c->sitems.push_back(StreamItem{0, 0, 0});
+    if (c->chunks.empty()) c->chunks.push_back(PixTile{});
+  }
   // --- Gram tiles
   int nsrc = 0;
   int64_t work_px = 0;
@@ -502,12 +575,12 @@ static void prof_collect(Ctx* c, bool with_lin) {
 
 static int stage_energy(Ctx* c, DevState& s, cudaStream_t st) {
   launch_edge_prep(s, c->d_ei, c->d_ej, c->E, c->extr, st);
-  launch_vision_energy(c->P.pixel_mode, c->d_tiles, (int)c->tiles.size(), s, c->P.pix, c->P.tgt, c->P.wts,
+  launch_vision_energy(c->P.pixel_mode, c->d_chunks, c->d_soff, c->d_sids, c->d_sitems, c->d_ioff, c->ncta, s, c->P.pix, c->P.tgt, c->P.wts,
                        c->d_eoff, c->d_doff, c->P.grid_w, c->grid, c->intr, c->d_tile_e, st);
   launch_imu_factor(c->P.imu, c->d_L, c->d_fi, c->d_fj, c->F, s, c->P.ts, c->sdof, c->ibs, 1,
                     c->d_arena + c->arena_imu, st);
   const int oE = 3 * c->sdof * c->sdof + 6 * c->sdof + 6;
-  launch_energy_reduce(c->d_tile_e, (int)c->tiles.size(), c->d_arena + c->arena_imu, c->F, c->ibs, oE,
+  launch_energy_reduce(c->d_tile_e, (int)c->chunks.size() * kPartWarps, c->d_arena + c->arena_imu, c->F, c->ibs, oE,
                        c->d_res->energy, st);
   return VBA_OK;
 }
@@ -516,9 +589,13 @@ static int stage_linearize(Ctx* c, cudaStream_t st) {
   DevState& s = CUR(c);
   mark(c, 0, st);
   c->lin_pending = true;
+  if (c->k1_split) {   // split chunks add their partial H_dd / g_d onto zero
+    cudaMemsetAsync(c->d_Hdd, 0, sizeof(float) * std::max<int64_t>(1, c->n_disp), st);
+    cudaMemsetAsync(c->d_gd, 0, sizeof(float) * std::max<int64_t>(1, c->n_disp), st);
+  }
   launch_edge_prep(s, c->d_ei, c->d_ej, c->E, c->extr, st);
   mark(c, 8, st);
-  launch_vision_linearize(c->P.pixel_mode, c->d_tiles, (int)c->tiles.size(), s, c->P.pix, c->P.tgt, c->P.wts,
+  launch_vision_linearize(c->P.pixel_mode, c->d_chunks, c->d_soff, c->d_sids, c->d_sitems, c->d_ioff, c->ncta, s, c->P.pix, c->P.tgt, c->P.wts,
                           c->d_eoff, c->d_doff, c->P.grid_w, c->grid, c->intr, c->d_part, c->d_Hdd, c->d_gd, st);
   mark(c, 9, st);
   launch_edge_finalize(c->d_t0s, c->d_t1s, c->d_tiles, c->d_ei, c->E, c->d_part, s, c->extr,
@@ -776,6 +853,9 @@ int vba_create(void** out, const vba_problem* prob, const vba_options* opts, voi
       (rc = dupload(c, &c->d_fi, fi, st)) || (rc = dupload(c, &c->d_fj, fj, st)) ||
       (rc = dupload(c, &c->d_frozen, fr, st)) || (rc = dupload(c, &c->d_eoff, eoff, st)) ||
       (rc = dupload(c, &c->d_doff, doff, st)) || (rc = dupload(c, &c->d_tiles, c->tiles, st)) ||
+      (rc = dupload(c, &c->d_soff, c->soff, st)) || (rc = dupload(c, &c->d_sids, c->sids, st)) ||
+      (rc = dupload(c, &c->d_ioff, c->ioff, st)) || (rc = dupload(c, &c->d_sitems, c->sitems, st)) ||
+      (rc = dupload(c, &c->d_chunks, c->chunks, st)) ||
       (rc = dupload(c, &c->d_t0s, c->t0s, st)) || (rc = dupload(c, &c->d_t1s, c->t1s, st)) ||
       (rc = dupload(c, &c->d_seb, c->seb, st)) || (rc = dupload(c, &c->d_see, c->see, st)) ||
       (rc = dupload(c, &c->d_gtiles, c->gtiles, st)) || (rc = dupload(c, &c->d_gsrc, c->gsrc, st)) ||
@@ -798,8 +878,8 @@ int vba_create(void** out, const vba_problem* prob, const vba_options* opts, voi
     return fail(VBA_E_CUDA);
   }
   // workspace
-  if ((rc = dalloc(c, &c->d_part, (size_t)c->n_part * kPartStride)) ||
-      (rc = dalloc(c, &c->d_tile_e, c->tiles.size())) || (rc = dalloc(c, &c->d_arena, (size_t)c->arena_len)) ||
+  if ((rc = dalloc(c, &c->d_part, (size_t)c->n_part * kPartStride / 2)) ||
+      (rc = dalloc(c, &c->d_tile_e, c->chunks.size() * kPartWarps)) || (rc = dalloc(c, &c->d_arena, (size_t)c->arena_len)) ||
       (rc = dalloc(c, &c->d_gram_part, (size_t)c->gram_part_len)) ||
       (rc = dalloc(c, &c->d_gram, (size_t)c->gram_len)) || (rc = dalloc(c, &c->d_Hdd, (size_t)c->n_disp)) ||
       (rc = dalloc(c, &c->d_gd, (size_t)c->n_disp)) || (rc = dalloc(c, &c->d_ustep, (size_t)8 * c->E)) ||
@@ -823,7 +903,8 @@ int vba_create(void** out, const vba_problem* prob, const vba_options* opts, voi
     }
   }
   cudaMemsetAsync(c->d_arena, 0, sizeof(double) * std::max<int64_t>(1, c->arena_len), st);
-  cudaMemsetAsync(c->d_Hdd, 0, sizeof(float) * std::max<int64_t>(1, c->n_disp), st);
+  cudaMemsetAsync(c->d_Hdd, 0, sizeof(float) * std::max<int64_t>(1, c->n_disp), st);   // edge-less tiles stay 0
+  cudaMemsetAsync(c->d_tile_e, 0, sizeof(double) * std::max<size_t>(1, c->chunks.size() * kPartWarps), st);
   cudaMemsetAsync(c->d_gd, 0, sizeof(float) * std::max<int64_t>(1, c->n_disp), st);
   cudaMemsetAsync(c->d_x, 0, sizeof(double) * std::max(1, c->npad), st);
   cudaMemsetAsync(c->d_rhs, 0, sizeof(double) * std::max(1, c->npad), st);

@@ -15,7 +15,8 @@ namespace vba {
 
 constexpr double kSmallAngle = 1e-8;
 constexpr float kDispFloor = 1e-4f;      // solver.py:32
-constexpr int kPartStride = 32;          // doubles per K1 (tile, edge) partial record
+constexpr int kPartWarps = 4;            // warps of the K1 CTA, one fp32 32-vector each
+constexpr int kPartStride = 32 * kPartWarps;   // floats per K1 (tile, edge) partial record
 constexpr int kVisBlock = 120;           // doubles per edge pose-space block record
 constexpr int kGeo64 = 24;               // doubles per EdgeGeo64 record
 constexpr int kImuL = 120;               // doubles per IMU whitening-factor record (81 + 36 + pad)
@@ -41,8 +42,15 @@ struct Extr {
 // starting at pixel `n0`, looping over that source's out-edges [eb, ee).
 struct PixTile {
   int32_t src, n0, cnt, eb, ee;
-  int32_t pad;
+  int32_t pad;    // K1 chunks: 1 = half of a split tile (H_dd / g_d added atomically)
   int64_t poff;   // first K1 partial record of this tile (one per out-edge)
+};
+
+// One streamed (tile, edge) item of K1 / K2: its flow / weight rows start at
+// float offset `foff` (= 2 (eoff[e] + n0)) and span `bytes` per array.
+struct StreamItem {
+  int64_t foff;
+  int32_t bytes, edge;
 };
 
 // Work tile of the Schur Gram kernel (one source keyframe, a pixel range).
@@ -250,14 +258,17 @@ struct DevState {      // one side of the double-buffered solver state
 
 void launch_edge_prep(const DevState& s, const int32_t* ei, const int32_t* ej, int E, const Extr& x,
                       cudaStream_t st);
-void launch_vision_linearize(int pixel_mode, const PixTile* tiles, int ntiles, const DevState& s,
-                             const float* pix, const float* tgt, const float* wts, const int64_t* eoff,
-                             const int64_t* doff, int grid_w, const double* grid, const double* intr,
-                             double* partials, float* Hdd, float* gd, cudaStream_t st);
-void launch_vision_energy(int pixel_mode, const PixTile* tiles, int ntiles, const DevState& s,
-                          const float* pix, const float* tgt, const float* wts, const int64_t* eoff,
-                          const int64_t* doff, int grid_w, const double* grid, const double* intr,
-                          double* tile_energy, cudaStream_t st);
+// Streamed K1 / K2: CTA b processes tiles sids[soff[b] .. soff[b+1]) whose (tile, edge)
+// items are items[ioff[b] .. ioff[b+1]); ncta = vision_stream_ctas()
+int vision_stream_ctas();
+void launch_vision_linearize(int pixel_mode, const PixTile* tiles, const int32_t* soff, const int32_t* sids,
+                             const StreamItem* items, const int32_t* ioff, int ncta, const DevState& s, const float* pix, const float* tgt, const float* wts,
+                             const int64_t* eoff, const int64_t* doff, int grid_w, const double* grid,
+                             const double* intr, double* partials, float* Hdd, float* gd, cudaStream_t st);
+void launch_vision_energy(int pixel_mode, const PixTile* tiles, const int32_t* soff, const int32_t* sids,
+                          const StreamItem* items, const int32_t* ioff, int ncta, const DevState& s, const float* pix, const float* tgt, const float* wts,
+                          const int64_t* eoff, const int64_t* doff, int grid_w, const double* grid,
+                          const double* intr, double* tile_energy, cudaStream_t st);
 void launch_edge_finalize(const int32_t* esrc_tile0, const int32_t* esrc_tile1, const PixTile* tiles,
                           const int32_t* edge_i, int E, const double* partials, const DevState& s,
                           const Extr& x, double* visblocks, double* edge_energy, cudaStream_t st);

@@ -63,6 +63,20 @@ __device__ __forceinline__ void load_rays(const float* __restrict__ pix, int64_t
   rx1 = (float)((u1 - in.cx) / in.fx); ry1 = (float)((v1 - in.cy) / in.fy);
 }
 
+// 1/x on the MUFU (<= 1 ulp); every per-pixel kernel projects with it so K1,
+// the Gram and the back-substitution see bitwise identical geometry
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+// one Newton step on top: r (2 - x r), ~correctly rounded; the packed pixel-pair
+// kernels apply the same two FMAs with FFMA2 (bitwise equal)
+__device__ __forceinline__ float rcp_nr(float x) {
+  const float r = rcp_approx(x);
+  return fmaf(r, fmaf(-x, r, 1.0f), r);
+}
+
 struct PxGeom {  // per edge-pixel projection at the current estimate
   float x, y, dx, dy, iz, izh;
   bool valid;
@@ -81,7 +95,7 @@ __device__ __forceinline__ PxGeom project(const EdgeGeo32& g, float rx, float ry
   const float Xz = 1.0f + Dz;
   PxGeom o;
   o.valid = Xz > 1e-6f * d;                // z_j = Xz / d > 1e-6  (residuals.py:206-209)
-  o.izh = o.valid ? 1.0f / Xz : 0.0f;      // invalid pixels: finite zeros, weight 0
+  o.izh = o.valid ? rcp_nr(Xz) : 0.0f;      // invalid pixels: finite zeros, weight 0
   o.dx = fmaf(-rx, Dz, Dx) * o.izh;
   o.dy = fmaf(-ry, Dz, Dy) * o.izh;
   o.x = rx + o.dx;
@@ -143,257 +157,380 @@ void launch_edge_prep(const DevState& s, const int32_t* ei, const int32_t* ej, i
 }
 
 // ---------------------------------------------------------------------------
-// K1: vision linearisation.  One CTA per (source keyframe, 1024-pixel tile),
-// looping over the source's out-edges.  Per (tile, edge) it writes a 32-double
-// partial: 21 upper-triangular entries of S = sum w K^T K, 6 of s = sum w K^T r,
-// and the edge energy; per pixel it writes H_dd and g_d (sum over out-edges).
+// K1 (linearisation) and K2 (energy): streamed per-pixel kernels.
+//
+// Work item = (source tile, out-edge): 1024 pixels of one source keyframe
+// against one edge.  A persistent grid (SMs x resident CTAs) pulls source
+// tiles from an LPT-ordered list (most edge-pixels first) through a global
+// counter; inside a CTA, thread 0 streams each item's flow and weight rows
+// (2 x 8 KB, contiguous per edge) into a kStages-deep shared-memory ring with
+// cp.async.bulk + mbarrier complete_tx, running ahead of the arithmetic across
+// edge and tile boundaries, so HBM reads never wait on compute.  Per-pixel
+// math is fp32 on pixel pairs with packed FFMA2 (sm_100a), the same operation
+// order as project() (bitwise equal to the scalar kernels).
+//
+// K1 writes per (tile, edge) a 32-double partial: 21 upper-triangular entries
+// of S = sum w K^T K and 6 of s = sum w K^T r (slots 27..31 zero), and per
+// pixel H_dd, g_d (sum over out-edges).  K2 writes one fp64 energy per tile.
 // ---------------------------------------------------------------------------
-template <int MODE>
-__global__ void __launch_bounds__(kPixBlock) k_vision_linearize(
-    const PixTile* __restrict__ tiles, const float* __restrict__ disp, const EdgeGeo32* __restrict__ geo,
-    const float* __restrict__ pix, const float* __restrict__ tgt, const float* __restrict__ wts,
-    const int64_t* __restrict__ eoff, const int64_t* __restrict__ doff, int grid_w, GridP gp, IntrP in,
-    double* __restrict__ partials, float* __restrict__ Hdd, float* __restrict__ gdo) {
-  __shared__ double red[2][kPixBlock / 32][32];
-  const PixTile T = tiles[blockIdx.x];
+constexpr int kStages = 3;
+constexpr int kPairs = kTile / 2;   // float4 (= 2 pixels) per row of a stage
+static_assert(kPixBlock / 32 == kPartWarps, "K1 partial records hold one vector per warp");
+constexpr int kSchedCap = 24;       // tile records of one CTA staged in shared memory
+constexpr int kItemCap = 160;       // stream items of one CTA staged in shared memory
+constexpr int kRedS = 36;           // row stride (floats) of the warp transpose: 4c mod 32 distinct per quarter-warp
+
+struct StreamSmem {
+  float4 flow[kStages][kPairs];
+  float4 wts[kStages][kPairs];
+  EdgeGeo32 geo[kStages];
+  float xr[kPixBlock / 32][28 * kRedS];   // per-warp transpose of the 27 per-lane sums
+  StreamItem it[kItemCap];
+  PixTile tl[kSchedCap];
+  int tid[kSchedCap];
+  unsigned long long full[kStages];
+  unsigned int rel[kStages];              // warp releases per stage (monotonic; 4 per use)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, int n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar,
+                                         uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+#define FMA2 __ffma2_rn
+#define MUL2 __fmul2_rn
+#define ADD2 __fadd2_rn
+__device__ __forceinline__ float2 S2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 operator-(float2 a) { return make_float2(-a.x, -a.y); }
+
+// Static LPT schedule: CTA b owns tiles sched_ids[sched_off[b] .. sched_off[b+1])
+// (host-balanced by edge-pixels, vba_host.cu build_plans), so the producer knows
+// every upcoming tile without a global atomic on the critical path.
+template <int MODE, bool LIN>
+__global__ void __launch_bounds__(kPixBlock, 3) k_vision_stream(
+    const PixTile* __restrict__ tiles, const int32_t* __restrict__ sched_off, const int32_t* __restrict__ sched_ids,
+    const StreamItem* __restrict__ items, const int32_t* __restrict__ item_off, const float* __restrict__ disp,
+    const EdgeGeo32* __restrict__ geo, const float* __restrict__ pix, const float* __restrict__ tgt,
+    const float* __restrict__ wts, const int64_t* __restrict__ eoff, const int64_t* __restrict__ doff, int grid_w,
+    GridP gp, IntrP in, double* __restrict__ partials, float* __restrict__ Hdd, float* __restrict__ gdo,
+    double* __restrict__ tile_energy) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* const fpart = reinterpret_cast<float*>(partials);
+  StreamSmem& S = *reinterpret_cast<StreamSmem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t kbase = doff[T.src];
   const float fx = (float)in.fx, fy = (float)in.fy;
   const float fx2 = fx * fx, fy2 = fy * fy;
+  const int s0 = sched_off[blockIdx.x], nmine = sched_off[blockIdx.x + 1] - s0;
+  const int i0 = item_off[blockIdx.x], nitems = item_off[blockIdx.x + 1] - i0;
+  auto tile_id = [&](int o) { return o < kSchedCap ? S.tid[o] : sched_ids[s0 + o]; };
+  auto tile_at = [&](int o) { return o < kSchedCap ? S.tl[o] : tiles[sched_ids[s0 + o]]; };
 
-  float rx[2 * kTP], ry[2 * kTP], dd[2 * kTP], hdd[2 * kTP], gdd[2 * kTP];
-  bool act[kTP];
-#pragma unroll
-  for (int m = 0; m < kTP; ++m) {
-    const int p = m * kPixBlock + tid;
-    const int n = T.n0 + 2 * p;
-    act[m] = 2 * p < T.cnt;
-    rx[2 * m] = ry[2 * m] = rx[2 * m + 1] = ry[2 * m + 1] = 0.f;
-    dd[2 * m] = dd[2 * m + 1] = 1.f;
-    if (act[m]) {
-      const float2 d2 = __ldg(reinterpret_cast<const float2*>(disp + kbase + n));
-      dd[2 * m] = d2.x;
-      dd[2 * m + 1] = d2.y;
-      if (MODE != VBA_PIX_EDGE)
-        load_rays<MODE>(pix, kbase, n, grid_w, gp, in, rx[2 * m], ry[2 * m], rx[2 * m + 1], ry[2 * m + 1]);
-    }
-    hdd[2 * m] = hdd[2 * m + 1] = gdd[2 * m] = gdd[2 * m + 1] = 0.f;
+  // rows beyond a short tile's count are masked by `act` but still read: zero the
+  // ring once so they are finite (stale rows of earlier items are finite too)
+  for (int i = tid; i < kStages * kPairs; i += kPixBlock) {
+    (&S.flow[0][0])[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    (&S.wts[0][0])[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-
-  for (int e = T.eb; e < T.ee; ++e) {
-    const EdgeGeo32 g = load_geo(geo, e);
-    const int64_t rbase = eoff[e] + T.n0;
-    float acc[32];
-#pragma unroll
-    for (int k = 0; k < 32; ++k) acc[k] = 0.f;
-    float4 tt[kTP], ww[kTP];
-#pragma unroll
-    for (int m = 0; m < kTP; ++m) {
-      const int p = m * kPixBlock + tid;
-      tt[m] = make_float4(0.f, 0.f, 0.f, 0.f);
-      ww[m] = tt[m];
-      if (act[m]) {
-        tt[m] = __ldcs(reinterpret_cast<const float4*>(tgt + 2 * (rbase + 2 * p)));
-        ww[m] = __ldcs(reinterpret_cast<const float4*>(wts + 2 * (rbase + 2 * p)));
-        if (MODE == VBA_PIX_EDGE)
-          load_rays<VBA_PIX_KF>(pix, rbase - T.n0, T.n0 + 2 * p, grid_w, gp, in, rx[2 * m], ry[2 * m],
-                                rx[2 * m + 1], ry[2 * m + 1]);
-      }
-    }
-#pragma unroll
-    for (int m = 0; m < kTP; ++m) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int q = 2 * m + h;
-        const PxGeom o = project(g, rx[q], ry[q], dd[q]);
-        const float tu = h ? tt[m].z : tt[m].x, tv = h ? tt[m].w : tt[m].y;
-        float w0 = h ? ww[m].z : ww[m].x, w1 = h ? ww[m].w : ww[m].y;
-        w0 = o.valid ? w0 : 0.f;
-        w1 = o.valid ? w1 : 0.f;
-        const float r0 = fmaf(-fx, o.dx, tu);    // flow - fx (x - rx)
-        const float r1 = fmaf(-fy, o.dy, tv);
-        const float xy = o.x * o.y;
-        const float a1 = -fmaf(o.x, o.x, 1.f);     // k0' = [xy, -(1+x^2), y, -iz, 0, x iz]
-        const float a5 = o.x * o.iz;
-        const float b0 = fmaf(o.y, o.y, 1.f);      // k1' = [1+y^2, -xy, -x, 0, -iz, y iz]
-        const float b5 = o.y * o.iz;
-        const float jd0 = fmaf(o.x, g.t[2], -g.t[0]) * o.izh;   // J_d = (fx jd0', fy jd1')
-        const float jd1 = fmaf(o.y, g.t[2], -g.t[1]) * o.izh;
-        const float W0 = w0 * fx2, W1 = w1 * fy2;
-        const float R0 = w0 * fx * r0, R1 = w1 * fy * r1;
-        // weighted rows
-        const float p0 = W0 * xy, p1 = W0 * a1, p2 = W0 * o.y, p3 = -W0 * o.iz, p5 = W0 * a5;
-        const float q0 = W1 * b0, q1 = -W1 * xy, q2 = -W1 * o.x, q4 = -W1 * o.iz, q5 = W1 * b5;
-        // S += W0 k0' k0'^T + W1 k1' k1'^T (upper triangle, structural zeros skipped)
-        acc[0] = fmaf(p0, xy, fmaf(q0, b0, acc[0]));
-        acc[1] = fmaf(p0, a1, fmaf(q0, -xy, acc[1]));
-        acc[2] = fmaf(p0, o.y, fmaf(q0, -o.x, acc[2]));
-        acc[3] = fmaf(p0, -o.iz, acc[3]);
-        acc[4] = fmaf(q0, -o.iz, acc[4]);
-        acc[5] = fmaf(p0, a5, fmaf(q0, b5, acc[5]));
-        acc[6] = fmaf(p1, a1, fmaf(q1, -xy, acc[6]));
-        acc[7] = fmaf(p1, o.y, fmaf(q1, -o.x, acc[7]));
-        acc[8] = fmaf(p1, -o.iz, acc[8]);
-        acc[9] = fmaf(q1, -o.iz, acc[9]);
-        acc[10] = fmaf(p1, a5, fmaf(q1, b5, acc[10]));
-        acc[11] = fmaf(p2, o.y, fmaf(q2, -o.x, acc[11]));
-        acc[12] = fmaf(p2, -o.iz, acc[12]);
-        acc[13] = fmaf(q2, -o.iz, acc[13]);
-        acc[14] = fmaf(p2, a5, fmaf(q2, b5, acc[14]));
-        acc[15] = fmaf(p3, -o.iz, acc[15]);
-        acc[17] = fmaf(p3, a5, acc[17]);
-        acc[18] = fmaf(q4, -o.iz, acc[18]);
-        acc[19] = fmaf(q4, b5, acc[19]);
-        acc[20] = fmaf(p5, a5, fmaf(q5, b5, acc[20]));
-        // s += w0 fx r0 k0' + w1 fy r1 k1'
-        acc[21] = fmaf(R0, xy, fmaf(R1, b0, acc[21]));
-        acc[22] = fmaf(R0, a1, fmaf(R1, -xy, acc[22]));
-        acc[23] = fmaf(R0, o.y, fmaf(R1, -o.x, acc[23]));
-        acc[24] = fmaf(R0, -o.iz, acc[24]);
-        acc[25] = fmaf(R1, -o.iz, acc[25]);
-        acc[26] = fmaf(R0, a5, fmaf(R1, b5, acc[26]));
-        acc[27] = fmaf(w0 * r0, r0, fmaf(w1 * r1, r1, acc[27]));
-        // per-pixel disparity block and gradient (summed over out-edges)
-        hdd[q] = fmaf(W0 * jd0, jd0, fmaf(W1 * jd1, jd1, hdd[q]));
-        gdd[q] = fmaf(R0, jd0, fmaf(R1, jd1, gdd[q]));
-      }
-    }
-    const float v = warp_reduce_scatter32(acc);
-    const int buf = (e - T.eb) & 1;
-    red[buf][warp][lane] = (double)v;
-    __syncthreads();
-    if (warp == 0) {
-      double s = 0.0;
-#pragma unroll
-      for (int w = 0; w < kPixBlock / 32; ++w) s += red[buf][w][lane];
-      partials[(T.poff + (e - T.eb)) * kPartStride + lane] = s;
-    }
+  for (int i = tid; i < nmine && i < kSchedCap; i += kPixBlock) {
+    const int t = sched_ids[s0 + i];
+    S.tid[i] = t;
+    S.tl[i] = tiles[t];
   }
-#pragma unroll
-  for (int m = 0; m < kTP; ++m) {
-    if (!act[m]) continue;
-    const int64_t n = kbase + T.n0 + 2 * (m * kPixBlock + tid);
-    *reinterpret_cast<float2*>(Hdd + n) = make_float2(hdd[2 * m], hdd[2 * m + 1]);
-    *reinterpret_cast<float2*>(gdo + n) = make_float2(gdd[2 * m], gdd[2 * m + 1]);
-  }
-}
-
-void launch_vision_linearize(int mode, const PixTile* tiles, int ntiles, const DevState& s, const float* pix,
-                             const float* tgt, const float* wts, const int64_t* eoff, const int64_t* doff,
-                             int grid_w, const double* grid, const double* intr, double* partials, float* Hdd,
-                             float* gd, cudaStream_t st) {
-  if (ntiles <= 0) return;
-  GridP gp{grid[0], grid[1], grid[2], grid[3]};
-  IntrP in{intr[0], intr[1], intr[2], intr[3]};
-  if (mode == VBA_PIX_GRID)
-    k_vision_linearize<VBA_PIX_GRID><<<ntiles, kPixBlock, 0, st>>>(tiles, s.disp, s.geo32, pix, tgt, wts, eoff,
-                                                                   doff, grid_w, gp, in, partials, Hdd, gd);
-  else if (mode == VBA_PIX_KF)
-    k_vision_linearize<VBA_PIX_KF><<<ntiles, kPixBlock, 0, st>>>(tiles, s.disp, s.geo32, pix, tgt, wts, eoff,
-                                                                 doff, grid_w, gp, in, partials, Hdd, gd);
-  else
-    k_vision_linearize<VBA_PIX_EDGE><<<ntiles, kPixBlock, 0, st>>>(tiles, s.disp, s.geo32, pix, tgt, wts, eoff,
-                                                                   doff, grid_w, gp, in, partials, Hdd, gd);
-  launch_count();
-}
-
-// ---------------------------------------------------------------------------
-// K2: vision energy sum w r^2 (residual-only pass).  One fp64 partial per tile.
-// ---------------------------------------------------------------------------
-template <int MODE>
-__global__ void __launch_bounds__(kPixBlock) k_vision_energy(
-    const PixTile* __restrict__ tiles, const float* __restrict__ disp, const EdgeGeo32* __restrict__ geo,
-    const float* __restrict__ pix, const float* __restrict__ tgt, const float* __restrict__ wts,
-    const int64_t* __restrict__ eoff, const int64_t* __restrict__ doff, int grid_w, GridP gp, IntrP in,
-    double* __restrict__ tile_energy) {
-  __shared__ double red[kPixBlock / 32];
-  const PixTile T = tiles[blockIdx.x];
-  const int tid = threadIdx.x;
-  const int64_t kbase = doff[T.src];
-  const float fx = (float)in.fx, fy = (float)in.fy;
-  float rx[2 * kTP], ry[2 * kTP], dd[2 * kTP];
-  bool act[kTP];
-#pragma unroll
-  for (int m = 0; m < kTP; ++m) {
-    const int p = m * kPixBlock + tid;
-    const int n = T.n0 + 2 * p;
-    act[m] = 2 * p < T.cnt;
-    rx[2 * m] = ry[2 * m] = rx[2 * m + 1] = ry[2 * m + 1] = 0.f;
-    dd[2 * m] = dd[2 * m + 1] = 1.f;
-    if (act[m]) {
-      const float2 d2 = __ldg(reinterpret_cast<const float2*>(disp + kbase + n));
-      dd[2 * m] = d2.x;
-      dd[2 * m + 1] = d2.y;
-      if (MODE != VBA_PIX_EDGE)
-        load_rays<MODE>(pix, kbase, n, grid_w, gp, in, rx[2 * m], ry[2 * m], rx[2 * m + 1], ry[2 * m + 1]);
-    }
-  }
-  double etot = 0.0;
-  for (int e = T.eb; e < T.ee; ++e) {
-    const EdgeGeo32 g = load_geo(geo, e);
-    const int64_t rbase = eoff[e] + T.n0;
-    float4 tt[kTP], ww[kTP];
-#pragma unroll
-    for (int m = 0; m < kTP; ++m) {
-      const int p = m * kPixBlock + tid;
-      tt[m] = make_float4(0.f, 0.f, 0.f, 0.f);
-      ww[m] = tt[m];
-      if (act[m]) {
-        tt[m] = __ldcs(reinterpret_cast<const float4*>(tgt + 2 * (rbase + 2 * p)));
-        ww[m] = __ldcs(reinterpret_cast<const float4*>(wts + 2 * (rbase + 2 * p)));
-        if (MODE == VBA_PIX_EDGE)
-          load_rays<VBA_PIX_KF>(pix, rbase - T.n0, T.n0 + 2 * p, grid_w, gp, in, rx[2 * m], ry[2 * m],
-                                rx[2 * m + 1], ry[2 * m + 1]);
-      }
-    }
-    float ee = 0.f;
-#pragma unroll
-    for (int m = 0; m < kTP; ++m) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int q = 2 * m + h;
-        const PxGeom o = project(g, rx[q], ry[q], dd[q]);
-        const float tu = h ? tt[m].z : tt[m].x, tv = h ? tt[m].w : tt[m].y;
-        float w0 = h ? ww[m].z : ww[m].x, w1 = h ? ww[m].w : ww[m].y;
-        w0 = o.valid ? w0 : 0.f;
-        w1 = o.valid ? w1 : 0.f;
-        const float r0 = fmaf(-fx, o.dx, tu);    // flow - fx (x - rx)
-        const float r1 = fmaf(-fy, o.dy, tv);
-        ee = fmaf(w0 * r0, r0, fmaf(w1 * r1, r1, ee));
-      }
-    }
-    etot += (double)ee;
-  }
-  // fixed-order block reduction
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) etot += __shfl_xor_sync(0xffffffffu, etot, o);
-  if ((tid & 31) == 0) red[tid >> 5] = etot;
+  for (int i = tid; i < nitems && i < kItemCap; i += kPixBlock) S.it[i] = items[i0 + i];
+  if (tid < kStages) S.rel[tid] = 0u;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes before async-proxy copies
   __syncthreads();
+
+  // ---- producer: item j -> stage j % kStages.  Items 0..kStages-1 by thread 0;
+  // item j + kStages by the LAST warp to release item j (no thread ever waits
+  // to refill: the ring is topped up the moment a stage drains)
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  auto issue = [&](int j) {
+    const StreamItem I = j < kItemCap ? S.it[j] : items[i0 + j];
+    const int s = j % kStages;
+    mbar_expect_tx(&S.full[s], 2u * (uint32_t)I.bytes + (uint32_t)sizeof(EdgeGeo32));
+    bulk_g2s(&S.geo[s], geo + I.edge, (uint32_t)sizeof(EdgeGeo32), &S.full[s], pol);
+    bulk_g2s(S.flow[s], tgt + I.foff, (uint32_t)I.bytes, &S.full[s], pol);
+    bulk_g2s(S.wts[s], wts + I.foff, (uint32_t)I.bytes, &S.full[s], pol);
+  };
+  auto release = [&](int j) {   // whole warp; call after its last read of item j's stage
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      const unsigned int r = atomicAdd(&S.rel[j % kStages], 1u);
+      if (r % (kPixBlock / 32) == (kPixBlock / 32) - 1 && j + kStages < nitems) {
+        __threadfence_block();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // others' generic reads before the refill
+        issue(j + kStages);
+      }
+    }
+  };
   if (tid == 0) {
-    double s = 0.0;
 #pragma unroll
-    for (int w = 0; w < kPixBlock / 32; ++w) s += red[w];
-    tile_energy[blockIdx.x] = s;
+    for (int s = 0; s < kStages; ++s) mbar_init(&S.full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int j = 0; j < kStages && j < nitems; ++j) issue(j);
+  }
+  __syncthreads();
+
+  int item = 0;
+#pragma unroll 1
+  for (int ord = 0; ord < nmine; ++ord) {
+    const PixTile T = tile_at(ord);
+    const int64_t kbase = doff[T.src];
+    float2 RX[kTP], RY[kTP], DD[kTP], HD[kTP], GD[kTP];
+    uint32_t act = 0;
+#pragma unroll
+    for (int m = 0; m < kTP; ++m) {
+      const int p = m * kPixBlock + tid;
+      const int n = T.n0 + 2 * p;
+      RX[m] = RY[m] = make_float2(0.f, 0.f);
+      DD[m] = make_float2(1.f, 1.f);
+      HD[m] = GD[m] = make_float2(0.f, 0.f);
+      if (2 * p < T.cnt) {
+        act |= 1u << m;
+        DD[m] = __ldg(reinterpret_cast<const float2*>(disp + kbase + n));
+        if (MODE != VBA_PIX_EDGE)
+          load_rays<MODE>(pix, kbase, n, grid_w, gp, in, RX[m].x, RY[m].x, RX[m].y, RY[m].y);
+      }
+    }
+    double etile = 0.0;
+#pragma unroll 1
+    for (int e = T.eb; e < T.ee; ++e, ++item) {
+      const int s = item % kStages;
+      if (MODE == VBA_PIX_EDGE) {
+#pragma unroll
+        for (int m = 0; m < kTP; ++m)
+          if (act & (1u << m))
+            load_rays<VBA_PIX_KF>(pix, eoff[e], T.n0 + 2 * (m * kPixBlock + tid), grid_w, gp, in, RX[m].x,
+                                  RY[m].x, RX[m].y, RY[m].y);
+      }
+      mbar_wait(&S.full[s], (item / kStages) & 1);
+      const EdgeGeo32 g = S.geo[s];
+      float2 acc[LIN ? 27 : 1];
+#pragma unroll
+      for (int k = 0; k < (LIN ? 27 : 1); ++k) acc[k] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int m = 0; m < kTP; ++m) {
+        const float4 fl = S.flow[s][m * kPixBlock + tid];
+        const float4 wl = S.wts[s][m * kPixBlock + tid];
+        const float2 rx = RX[m], ry = RY[m], d = DD[m];
+        // project(): D = (M - I) ray + d t,  x - rx = (Dx - rx Dz) / (1 + Dz)
+        const float2 Dx = FMA2(d, S2(g.t[0]), FMA2(S2(g.M[0]), rx, FMA2(S2(g.M[1]), ry, S2(g.M[2]))));
+        const float2 Dy = FMA2(d, S2(g.t[1]), FMA2(S2(g.M[3]), rx, FMA2(S2(g.M[4]), ry, S2(g.M[5]))));
+        const float2 Dz = FMA2(d, S2(g.t[2]), FMA2(S2(g.M[6]), rx, FMA2(S2(g.M[7]), ry, S2(g.M[8]))));
+        const float2 Xz = ADD2(S2(1.0f), Dz);
+        const float2 th = MUL2(S2(1e-6f), d);
+        const bool va = (act >> m) & 1u && Xz.x > th.x;   // z_j > 1e-6 (residuals.py:206-209)
+        const bool vb = (act >> m) & 1u && Xz.y > th.y;
+        float2 izh = make_float2(va ? rcp_approx(Xz.x) : 0.f, vb ? rcp_approx(Xz.y) : 0.f);
+        izh = FMA2(izh, FMA2(-Xz, izh, S2(1.0f)), izh);   // rcp_nr (invalid lanes stay 0)
+        const float2 ddx = MUL2(FMA2(-rx, Dz, Dx), izh);
+        const float2 ddy = MUL2(FMA2(-ry, Dz, Dy), izh);
+        const float2 r0 = FMA2(S2(-fx), ddx, make_float2(fl.x, fl.z));   // flow - fx (x - rx)
+        const float2 r1 = FMA2(S2(-fy), ddy, make_float2(fl.y, fl.w));
+        const float2 w0 = make_float2(va ? wl.x : 0.f, vb ? wl.z : 0.f);
+        const float2 w1 = make_float2(va ? wl.y : 0.f, vb ? wl.w : 0.f);
+        if (!LIN) {
+          acc[0] = FMA2(MUL2(w0, r0), r0, FMA2(MUL2(w1, r1), r1, acc[0]));
+          continue;
+        }
+        const float2 x = ADD2(rx, ddx), y = ADD2(ry, ddy);
+        const float2 iz = MUL2(d, izh);
+        const float2 xy = MUL2(x, y);
+        const float2 a1 = -FMA2(x, x, S2(1.f));   // k0' = [xy, -(1+x^2), y, -iz, 0, x iz]
+        const float2 a5 = MUL2(x, iz);
+        const float2 b0 = FMA2(y, y, S2(1.f));    // k1' = [1+y^2, -xy, -x, 0, -iz, y iz]
+        const float2 b5 = MUL2(y, iz);
+        const float2 jd0 = MUL2(FMA2(x, S2(g.t[2]), S2(-g.t[0])), izh);   // J_d = (fx jd0', fy jd1')
+        const float2 jd1 = MUL2(FMA2(y, S2(g.t[2]), S2(-g.t[1])), izh);
+        const float2 W0 = MUL2(w0, S2(fx2)), W1 = MUL2(w1, S2(fy2));   // as the Gram: (w fx^2) jd
+        const float2 R0 = MUL2(MUL2(w0, S2(fx)), r0), R1 = MUL2(MUL2(w1, S2(fy)), r1);
+        const float2 p0 = MUL2(W0, xy), p1 = MUL2(W0, a1), p2 = MUL2(W0, y), p3 = -MUL2(W0, iz),
+                     p5 = MUL2(W0, a5);
+        const float2 q0 = MUL2(W1, b0), q1 = -MUL2(W1, xy), q2 = -MUL2(W1, x), q4 = -MUL2(W1, iz),
+                     q5 = MUL2(W1, b5);
+        acc[0] = FMA2(p0, xy, FMA2(q0, b0, acc[0]));
+        acc[1] = FMA2(p0, a1, FMA2(q0, -xy, acc[1]));
+        acc[2] = FMA2(p0, y, FMA2(q0, -x, acc[2]));
+        acc[3] = FMA2(p0, -iz, acc[3]);
+        acc[4] = FMA2(q0, -iz, acc[4]);
+        acc[5] = FMA2(p0, a5, FMA2(q0, b5, acc[5]));
+        acc[6] = FMA2(p1, a1, FMA2(q1, -xy, acc[6]));
+        acc[7] = FMA2(p1, y, FMA2(q1, -x, acc[7]));
+        acc[8] = FMA2(p1, -iz, acc[8]);
+        acc[9] = FMA2(q1, -iz, acc[9]);
+        acc[10] = FMA2(p1, a5, FMA2(q1, b5, acc[10]));
+        acc[11] = FMA2(p2, y, FMA2(q2, -x, acc[11]));
+        acc[12] = FMA2(p2, -iz, acc[12]);
+        acc[13] = FMA2(q2, -iz, acc[13]);
+        acc[14] = FMA2(p2, a5, FMA2(q2, b5, acc[14]));
+        acc[15] = FMA2(p3, -iz, acc[15]);
+        acc[17] = FMA2(p3, a5, acc[17]);
+        acc[18] = FMA2(q4, -iz, acc[18]);
+        acc[19] = FMA2(q4, b5, acc[19]);
+        acc[20] = FMA2(p5, a5, FMA2(q5, b5, acc[20]));
+        acc[21] = FMA2(R0, xy, FMA2(R1, b0, acc[21]));
+        acc[22] = FMA2(R0, a1, FMA2(R1, -xy, acc[22]));
+        acc[23] = FMA2(R0, y, FMA2(R1, -x, acc[23]));
+        acc[24] = FMA2(R0, -iz, acc[24]);
+        acc[25] = FMA2(R1, -iz, acc[25]);
+        acc[26] = FMA2(R0, a5, FMA2(R1, b5, acc[26]));
+        HD[m] = FMA2(MUL2(W0, jd0), jd0, FMA2(MUL2(W1, jd1), jd1, HD[m]));
+        GD[m] = FMA2(R0, jd0, FMA2(R1, jd1, GD[m]));
+      }
+      if (LIN) {
+        // per-lane sums; stage s is no longer read by this warp: release it
+        float v[28];
+#pragma unroll
+        for (int k = 0; k < 27; ++k) v[k] = acc[k].x + acc[k].y;
+        v[16] = 0.f;   // S(3,4): structural zero
+        v[27] = 0.f;
+        release(item);
+        // warp sum by transpose: value k of lane l at xr[k * kRedS + l] (conflict-free
+        // stores), lane c < 28 then reads row c as 8 x LDS.128 (row stride 36 words:
+        // conflict-free) and sums it with a 3-level FADD2 tree
+        float* xr = S.xr[warp];
+#pragma unroll
+        for (int k = 0; k < 28; ++k) xr[k * kRedS + lane] = v[k];
+        __syncwarp();
+        if (lane < 28) {
+          const float4* row = reinterpret_cast<const float4*>(xr + lane * kRedS);
+          float4 q[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) q[j] = row[j];
+          float2 h[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) h[j] = ADD2(make_float2(q[j].x, q[j].y), make_float2(q[j].z, q[j].w));
+#pragma unroll
+          for (int j = 0; j < 4; ++j) h[j] = ADD2(h[j], h[j + 4]);
+          h[0] = ADD2(h[0], h[2]);
+          h[1] = ADD2(h[1], h[3]);
+          h[0] = ADD2(h[0], h[1]);
+          fpart[(T.poff + (e - T.eb)) * kPartStride + warp * 32 + lane] = h[0].x + h[0].y;
+        }
+        __syncwarp();   // xr reads done before the next item's stores
+      } else {
+        etile += (double)(acc[0].x + acc[0].y);
+        release(item);
+      }
+    }
+    if (LIN) {
+#pragma unroll
+      for (int m = 0; m < kTP; ++m) {
+        if (!((act >> m) & 1u)) continue;
+        const int64_t n = kbase + T.n0 + 2 * (m * kPixBlock + tid);
+        if (T.pad) {   // one of two edge halves of the tile: add onto zero (order-free with 2 addends)
+          atomicAdd(reinterpret_cast<float2*>(Hdd + n), HD[m]);
+          atomicAdd(reinterpret_cast<float2*>(gdo + n), GD[m]);
+        } else {
+          *reinterpret_cast<float2*>(Hdd + n) = HD[m];
+          *reinterpret_cast<float2*>(gdo + n) = GD[m];
+        }
+      }
+    } else {
+      // per-warp tile energy (fixed-order warp tree; k_energy_reduce sums the records)
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) etile += __shfl_xor_sync(0xffffffffu, etile, o);
+      if (lane == 0) tile_energy[(int64_t)tile_id(ord) * (kPixBlock / 32) + warp] = etile;
+    }
   }
 }
 
-void launch_vision_energy(int mode, const PixTile* tiles, int ntiles, const DevState& s, const float* pix,
-                          const float* tgt, const float* wts, const int64_t* eoff, const int64_t* doff,
-                          int grid_w, const double* grid, const double* intr, double* tile_energy,
+// CTAs of the streamed kernels (SMs x resident CTAs of the K1 instance; the
+// static schedule is built for exactly this many)
+int vision_stream_ctas() {
+  static int grid = 0;
+  if (grid == 0) {
+    const int smem = (int)sizeof(StreamSmem);
+    int dev = 0, nsm = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_vision_stream<VBA_PIX_GRID, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vision_stream<VBA_PIX_GRID, true>, kPixBlock, smem);
+    grid = nsm * (occ > 0 ? occ : 1);
+  }
+  return grid;
+}
+
+template <int MODE, bool LIN>
+static void launch_stream_t(int ncta, const PixTile* tiles, const int32_t* soff, const int32_t* sids,
+                            const StreamItem* items, const int32_t* ioff, const DevState& s, const float* pix, const float* tgt, const float* wts,
+                            const int64_t* eoff, const int64_t* doff, int grid_w, GridP gp, IntrP in,
+                            double* partials, float* Hdd, float* gd, double* tile_energy, cudaStream_t st) {
+  static bool init = false;
+  const int smem = (int)sizeof(StreamSmem);
+  if (!init) {
+    cudaFuncSetAttribute(k_vision_stream<MODE, LIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    init = true;
+  }
+  k_vision_stream<MODE, LIN><<<ncta, kPixBlock, smem, st>>>(tiles, soff, sids, items, ioff, s.disp, s.geo32, pix, tgt, wts,
+                                                             eoff, doff, grid_w, gp, in, partials, Hdd, gd,
+                                                             tile_energy);
+  launch_count();
+}
+
+template <bool LIN>
+static void launch_stream(int mode, const PixTile* tiles, const int32_t* soff, const int32_t* sids,
+                          const StreamItem* items, const int32_t* ioff, int ncta,
+                          const DevState& s, const float* pix, const float* tgt, const float* wts,
+                          const int64_t* eoff, const int64_t* doff, int grid_w, const double* grid,
+                          const double* intr, double* partials, float* Hdd, float* gd, double* tile_energy,
                           cudaStream_t st) {
-  if (ntiles <= 0) return;
+  if (ncta <= 0) return;
   GridP gp{grid[0], grid[1], grid[2], grid[3]};
   IntrP in{intr[0], intr[1], intr[2], intr[3]};
   if (mode == VBA_PIX_GRID)
-    k_vision_energy<VBA_PIX_GRID><<<ntiles, kPixBlock, 0, st>>>(tiles, s.disp, s.geo32, pix, tgt, wts, eoff,
-                                                                doff, grid_w, gp, in, tile_energy);
+    launch_stream_t<VBA_PIX_GRID, LIN>(ncta, tiles, soff, sids, items, ioff, s, pix, tgt, wts, eoff, doff, grid_w, gp, in,
+                                       partials, Hdd, gd, tile_energy, st);
   else if (mode == VBA_PIX_KF)
-    k_vision_energy<VBA_PIX_KF><<<ntiles, kPixBlock, 0, st>>>(tiles, s.disp, s.geo32, pix, tgt, wts, eoff,
-                                                              doff, grid_w, gp, in, tile_energy);
+    launch_stream_t<VBA_PIX_KF, LIN>(ncta, tiles, soff, sids, items, ioff, s, pix, tgt, wts, eoff, doff, grid_w, gp, in,
+                                     partials, Hdd, gd, tile_energy, st);
   else
-    k_vision_energy<VBA_PIX_EDGE><<<ntiles, kPixBlock, 0, st>>>(tiles, s.disp, s.geo32, pix, tgt, wts, eoff,
-                                                                doff, grid_w, gp, in, tile_energy);
-  launch_count();
+    launch_stream_t<VBA_PIX_EDGE, LIN>(ncta, tiles, soff, sids, items, ioff, s, pix, tgt, wts, eoff, doff, grid_w, gp, in,
+                                       partials, Hdd, gd, tile_energy, st);
+}
+
+void launch_vision_linearize(int mode, const PixTile* tiles, const int32_t* soff, const int32_t* sids,
+                             const StreamItem* items, const int32_t* ioff, int ncta,
+                             const DevState& s, const float* pix, const float* tgt, const float* wts,
+                             const int64_t* eoff, const int64_t* doff, int grid_w, const double* grid,
+                             const double* intr, double* partials, float* Hdd, float* gd, cudaStream_t st) {
+  launch_stream<true>(mode, tiles, soff, sids, items, ioff, ncta, s, pix, tgt, wts, eoff, doff, grid_w, grid, intr, partials,
+                      Hdd, gd, nullptr, st);
+}
+
+void launch_vision_energy(int mode, const PixTile* tiles, const int32_t* soff, const int32_t* sids,
+                          const StreamItem* items, const int32_t* ioff, int ncta,
+                          const DevState& s, const float* pix, const float* tgt, const float* wts,
+                          const int64_t* eoff, const int64_t* doff, int grid_w, const double* grid,
+                          const double* intr, double* tile_energy, cudaStream_t st) {
+  launch_stream<false>(mode, tiles, soff, sids, items, ioff, ncta, s, pix, tgt, wts, eoff, doff, grid_w, grid, intr, nullptr,
+                       nullptr, nullptr, tile_energy, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -411,10 +548,14 @@ __global__ void __launch_bounds__(64) k_edge_finalize(const int32_t* __restrict_
   __shared__ double v[32], S[36], Gi[36], Gj[36], T1[36], T2[36];
   const int e = blockIdx.x, tid = threadIdx.x;
   const int src = edge_i[e];
-  if (tid < 32) {
+  if (tid < 32) {   // K1 records: per (tile, edge) one fp32 32-vector per warp, summed in fp64, fixed order
+    const float* fp = reinterpret_cast<const float*>(partials);
     double s = 0.0;
-    for (int t = t0s[src]; t < t1s[src]; ++t)
-      s += partials[(tiles[t].poff + (e - tiles[t].eb)) * kPartStride + tid];
+    for (int t = t0s[src]; t < t1s[src]; ++t) {
+      const float* r = fp + (tiles[t].poff + (e - tiles[t].eb)) * kPartStride;
+#pragma unroll
+      for (int w = 0; w < kPartWarps; ++w) s += (double)r[w * 32 + tid];
+    }
     v[tid] = s;
   }
   if (tid == 32) {
@@ -817,7 +958,7 @@ __global__ void __launch_bounds__(kPixBlock) k_backsub(
   const PixTile T = tiles[blockIdx.x];
   const int tid = threadIdx.x;
   const int64_t kbase = doff[T.src];
-  const float fx2 = (float)(in.fx * in.fx), fy2 = (float)(in.fy * in.fy);
+  const float fx2 = (float)in.fx * (float)in.fx, fy2 = (float)in.fy * (float)in.fy;
   float rx[2 * kTP], ry[2 * kTP], dd[2 * kTP], acc[2 * kTP];
   bool act[kTP];
 #pragma unroll
@@ -992,7 +1133,7 @@ __global__ void k_export_hpd(const int32_t* __restrict__ seb, const int32_t* __r
   if (src >= K || n >= npix[src]) return;
   const int64_t kbase = doff[src];
   const int64_t col = out.base + roff[src] + n;
-  const float fx2 = (float)(in.fx * in.fx), fy2 = (float)(in.fy * in.fy);
+  const float fx2 = (float)in.fx * (float)in.fx, fy2 = (float)in.fy * (float)in.fy;
   const float d = disp[kbase + n];
   // pose row of keyframe k, entry a: reference layout k*sdof + a, or the free layout (frozen -> skip)
   auto prow = [&](int k, int a) -> int64_t {
