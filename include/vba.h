@@ -165,6 +165,20 @@ VBA_API int64_t vba_launch_count(void* ctx);
  * [3] back-substitution + retraction  [4] trial energy  [5] vision linearisation
  * kernel alone  [6] number of samples in [5]   (out must hold 7 doubles) */
 VBA_API int vba_stage_times(void* ctx, double* out5);
+/* solver statistics: [0] tensor-core reduced solve enabled, [1] steps that fell
+ * back to the fp64 factorisation, [2] flag generation, [3] refinement passes */
+VBA_API int vba_stats(void* ctx, int64_t* out4);
+
+/* Standalone SPD solve H x = b of a dense fp64 n x n system (column-major,
+ * lower triangle read; device pointers), replacing np.linalg.solve(Hred, -gred)
+ * of solver.py:287.  mode 0: tcgen05 3xTF32 Cholesky + fp64 iterative
+ * refinement (falls back to mode 1 when its checks fail), mode 1: fp64 DMMA
+ * tile-DAG Cholesky, mode 2: tensor-core result unconditionally (diagnostics;
+ * info[0] on entry = refinement passes, 0 -> 4).  On return info[0] = 1 if the
+ * tensor-core result was used, info[1] = tensor-core pivot failure.  Returns VBA_E_NOT_SPD on a
+ * non-positive fp64 pivot.  Synchronises `stream`. */
+VBA_API int vba_spd_solve(const double* H, int64_t n, const double* b, double* x, int32_t mode,
+                          void* stream, int32_t* info);
 
 #ifdef __cplusplus
 }

@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_vba.so")
+LIB_PATH = os.environ.get("VBA_LIB") or os.path.join(HERE, "_vba.so")   # VBA_LIB: tuning builds (tools/)
 
 VBA_OK, VBA_E_INVALID, VBA_E_CUDA, VBA_E_NOT_SPD, VBA_E_COV, VBA_E_UNSUPPORTED = range(6)
 PIX_GRID, PIX_KF, PIX_EDGE = 0, 1, 2
@@ -20,7 +20,7 @@ EXPORTED = ("vba_last_error", "vba_version", "vba_create", "vba_destroy", "vba_s
             "vba_reduced_dim", "vba_energy", "vba_linearize", "vba_export_normal_eq",
             "vba_solve_step", "vba_export_step", "vba_apply_step", "vba_restore", "vba_accept",
             "vba_trial", "vba_solve", "vba_download", "vba_launch_count", "vba_stage_times",
-            "vba_load_state", "vba_set_profiling")
+            "vba_load_state", "vba_set_profiling", "vba_stats", "vba_spd_solve")
 
 
 class VbaProblem(C.Structure):
@@ -104,6 +104,8 @@ def load(path: str | None = None):
         "vba_stage_times": ([v, C.POINTER(C.c_double)], C.c_int),
         "vba_load_state": ([v, v], C.c_int),
         "vba_set_profiling": ([v, C.c_int32], C.c_int),
+        "vba_stats": ([v, C.POINTER(C.c_int64)], C.c_int),
+        "vba_spd_solve": ([v, C.c_int64, v, v, C.c_int32, v, C.POINTER(C.c_int32)], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -117,3 +119,23 @@ def check(rc: int):
     if rc != VBA_OK:
         msg = _lib.vba_last_error().decode() if _lib is not None else ""
         raise VbaError(rc, msg)
+
+
+def spd_solve(H, b, mode: int = 0, iters: int = 0):
+    """Solve H x = b for a dense SPD fp64 torch CUDA matrix (lower triangle used).
+
+    mode 0: tcgen05 3xTF32 Cholesky + fp64 iterative refinement (fp64 fallback
+    on failed checks); mode 1: fp64 DMMA Cholesky.  Returns (x, used_tensor_cores).
+    Replaces np.linalg.solve(Hred, -gred) of solver.py:287.
+    """
+    import torch
+
+    lib = load()
+    n = H.shape[0]
+    Hc = H.t().contiguous()          # column-major storage of H
+    bc = b.contiguous()
+    x = torch.empty_like(bc)
+    info = (C.c_int32 * 2)(iters, 0)
+    st = torch.cuda.current_stream(H.device).cuda_stream
+    check(lib.vba_spd_solve(Hc.data_ptr(), n, bc.data_ptr(), x.data_ptr(), mode, st, info))
+    return x, bool(info[0])

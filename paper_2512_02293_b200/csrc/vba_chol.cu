@@ -22,6 +22,10 @@
 // sets *status (mapped to the reference's "singular reduced pose system").
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdio>
+#include <vector>
+
 #include "vba_internal.cuh"
 
 namespace vba {
@@ -640,4 +644,913 @@ void chol_task_fields(const void* tasks, int n, int* out4) {
     out4[4 * q + 3] = t[q].k;
   }
 }
+}  // namespace vba
+
+namespace vba {
+
+// ===========================================================================
+// Mixed-precision SPD solve on the 5th-gen tensor cores (tcgen05, kind::tf32).
+//
+// Same task DAG as k_chol_dag (POTRF / TRSM / GEMM, lookahead 1, static update
+// pairing), run on a Jacobi-scaled fp32 copy of the lower triangle:
+//   As = D H D,  D = diag(H)^-1/2      (the scaling makes cond(As) ~1e4 here)
+// GEMM-shaped tasks use 3xTF32 splitting (a = hi + lo, hi/lo rounded to tf32,
+// A B^T ~ Ah Bh^T + Ah Bl^T + Al Bh^T, fp32 accumulation in TMEM), so the
+// factor has ~fp32 accuracy at tensor-core speed.  The fp64 answer of
+// np.linalg.solve (solver.py:287) is then recovered by iterative refinement
+// against the fp64 H:  x += D (L L^T)^-1 D (b - H x)   (fp64 residuals).
+//
+// Tile storage (nt x nt lower tiles, linear index i(i+1)/2 + j):
+//   W    fp32 row-major 128x128: working tile; after the factorisation
+//        L_ij (i > j) and L_kk^-1 (diagonal) for the triangular solves
+//   IMG  per tile two operand images (hi, lo) in the UMMA canonical K-major
+//        SWIZZLE_128B layout: 4 K-chunks of 32 fp32 x 128 rows (16 KB each),
+//        8-row atoms of 1 KB, 16-byte units XOR-swizzled by (row mod 8); a
+//        chunk is one contiguous cp.async.bulk into shared memory.
+// ===========================================================================
+
+constexpr int TKC = 32;                       // fp32 K elements per chunk (one 128-B swizzle row)
+constexpr int TNCH = CT / TKC;                // 4 chunks per tile
+constexpr uint32_t TCHUNK = CT * TKC * 4;     // 16 KB
+constexpr int TC_STAGES = 3;
+constexpr uint32_t TSTAGE = 4 * TCHUNK;       // A_hi A_lo B_hi B_lo
+constexpr size_t TC_RING = (size_t)TC_STAGES * TSTAGE;
+constexpr size_t TC_SMEM = (TC_RING > POTRF_SMEM ? TC_RING : POTRF_SMEM) + 1024;
+constexpr int64_t TILE_F = (int64_t)CT * CT;  // floats per tile (and per image part)
+// instruction descriptor: D f32, A/B tf32, both K-major, N = 128, M = 128
+constexpr uint32_t TC_IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(CT >> 3) << 17) |
+                              ((uint32_t)(CT >> 4) << 24);
+
+struct TcArgs {
+  float* W;           // [ntl][CT*CT]
+  float* img;         // [ntl][2][CT*CT]
+  int nt;
+  int* upd;
+  int* done;
+  int* counter;
+  const CholTask* tasks;
+  int ntasks;
+  int* status;
+  unsigned long long* trace;   // optional [ntasks][4]: t_grab, t_ready, t_done, smid
+};
+
+__device__ __forceinline__ int64_t tlin(int i, int j) { return (int64_t)i * (i + 1) / 2 + j; }
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+// float offset of element (row r, col c) inside one image part (see layout above)
+__device__ __forceinline__ int img_off(int r, int c) {
+  const int q = c >> 5, e = c & 31, u = e >> 2;
+  return q * (CT * TKC) + (r >> 3) * 256 + (r & 7) * 32 + ((u ^ (r & 7)) << 2) + (e & 3);
+}
+
+__device__ __forceinline__ void tc_mbar_init(uint64_t* b, int n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void tc_mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "TCW_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra TCW_%=;\n}" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tc_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tc_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint64_t tc_sdesc(uint32_t saddr) {   // K-major, SWIZZLE_128B, SBO 1 KB
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %3, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %4, p;\n}\n" ::"r"(tmem),
+      "l"(da), "l"(db), "r"(acc), "r"(TC_IDESC));
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void proxy_fence_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void proxy_fence_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// 32 consecutive accumulator columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(r[k]);
+}
+
+// Pipeline bookkeeping shared by all threads (identical updates everywhere; only
+// thread 0 issues copies / MMAs).  Stage s = n % TC_STAGES of the n-th fill.
+struct TcRing {
+  uint64_t* full;
+  uint64_t* empty;
+  unsigned char* base;
+  uint32_t nfill, ncons;
+};
+
+// one K-chunk of 3xTF32 MMAs from stage s into the accumulator
+__device__ __forceinline__ void tc_chunk_mma(const TcRing& R, int s, uint32_t tmem, bool first) {
+  const uint32_t a_hi = su32(R.base + (size_t)s * TSTAGE), a_lo = a_hi + TCHUNK;
+  const uint32_t b_hi = a_hi + 2 * TCHUNK, b_lo = a_hi + 3 * TCHUNK;
+#pragma unroll
+  for (int kk = 0; kk < TKC / 8; ++kk) {   // 8 tf32 (32 B) of K per MMA
+    const uint32_t o = 32u * kk;
+    tc_mma(tmem, tc_sdesc(a_hi + o), tc_sdesc(b_hi + o), (first && kk == 0) ? 0u : 1u);
+    tc_mma(tmem, tc_sdesc(a_hi + o), tc_sdesc(b_lo + o), 1u);
+    tc_mma(tmem, tc_sdesc(a_lo + o), tc_sdesc(b_hi + o), 1u);
+  }
+}
+
+// GEMM(i,j,k[,k2]):  W_ij -= L_ik L_jk^T (+ L_ik2 L_jk2^T)   (operands: images)
+__device__ void tc_task_gemm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_t& nacc, uint32_t tmem, int i,
+                             int j, int k, int k2) {
+  const int tid = threadIdx.x;
+  const int nchunks = (k2 >= 0 ? 2 : 1) * TNCH;
+  if (tid == 0) {
+    proxy_fence_global();   // images written by other CTAs (generic) -> our bulk reads (async)
+    constexpr int PRE = TC_STAGES - 1;
+    for (int q = 0; q < nchunks + PRE; ++q) {
+      if (q < nchunks) {
+        const uint32_t n = R.nfill++;
+        const int s = n % TC_STAGES;
+        if (n >= TC_STAGES) tc_mbar_wait(&R.empty[s], ((n / TC_STAGES) - 1) & 1);
+        const int kq = q < TNCH ? k : k2, ch = q % TNCH;
+        const float* ia = a.img + tlin(i, kq) * 2 * TILE_F + ch * (CT * TKC);
+        const float* ib = a.img + tlin(j, kq) * 2 * TILE_F + ch * (CT * TKC);
+        unsigned char* st = R.base + (size_t)s * TSTAGE;
+        tc_expect_tx(&R.full[s], TSTAGE);
+        tc_bulk(st, ia, TCHUNK, &R.full[s]);
+        tc_bulk(st + TCHUNK, ia + TILE_F, TCHUNK, &R.full[s]);
+        tc_bulk(st + 2 * TCHUNK, ib, TCHUNK, &R.full[s]);
+        tc_bulk(st + 3 * TCHUNK, ib + TILE_F, TCHUNK, &R.full[s]);
+      }
+      const int qc = q - PRE;
+      if (qc >= 0) {
+        const uint32_t n = R.ncons++;
+        const int s = n % TC_STAGES;
+        tc_mbar_wait(&R.full[s], (n / TC_STAGES) & 1);
+        tc_fence_after();
+        tc_chunk_mma(R, s, tmem, qc == 0);
+        tc_commit(&R.empty[s]);
+      }
+    }
+    tc_commit(accf);
+  } else {
+    R.nfill += nchunks;
+    R.ncons += nchunks;
+  }
+  // epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 (= tile rows), columns 64 (w / 4) .. +63
+  tc_mbar_wait(accf, nacc & 1);
+  ++nacc;
+  tc_fence_after();
+  const int w = tid >> 5, lane = tid & 31;
+  const int row = 32 * (w & 3) + lane, c0 = 64 * (w >> 2);
+  float* C = a.W + tlin(i, j) * TILE_F + (int64_t)row * CT + c0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float v[32];
+    tmem_ld32(tmem + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)(c0 + 32 * h), v);
+    float4* p = reinterpret_cast<float4*>(C + 32 * h);
+    float4 o[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o[q] = __ldcg(p + q);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      o[q].x -= v[4 * q];
+      o[q].y -= v[4 * q + 1];
+      o[q].z -= v[4 * q + 2];
+      o[q].w -= v[4 * q + 3];
+      __stcg(p + q, o[q]);
+    }
+  }
+  tc_fence_before();
+}
+
+// TRSM(i,k):  L_ik = W_ik Linv_kk^T   (A = W_ik split by the threads, B = Linv images)
+__device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_t& nacc, uint32_t tmem, int i,
+                             int k) {
+  const int tid = threadIdx.x;
+  const float* Wik = a.W + tlin(i, k) * TILE_F;
+  const float* ib = a.img + tlin(k, k) * 2 * TILE_F;
+  if (tid == 0) proxy_fence_global();
+  for (int ch = 0; ch < TNCH; ++ch) {
+    const uint32_t n = R.nfill++;
+    R.ncons++;
+    const int s = n % TC_STAGES;
+    if (n >= TC_STAGES) tc_mbar_wait(&R.empty[s], ((n / TC_STAGES) - 1) & 1);
+    unsigned char* st = R.base + (size_t)s * TSTAGE;
+    if (tid == 0) {
+      tc_expect_tx(&R.full[s], 2 * TCHUNK);
+      tc_bulk(st + 2 * TCHUNK, ib + ch * (CT * TKC), TCHUNK, &R.full[s]);
+      tc_bulk(st + 3 * TCHUNK, ib + TILE_F + ch * (CT * TKC), TCHUNK, &R.full[s]);
+    }
+    // A chunk: row m = tid / 2, 16 consecutive K elements (4 units of 16 B)
+    {
+      const int m = tid >> 1, u0 = (tid & 1) * 4;
+      const float4* src = reinterpret_cast<const float4*>(Wik + (int64_t)m * CT + ch * TKC + 4 * u0);
+      float* hi = reinterpret_cast<float*>(st);
+      float* lo = reinterpret_cast<float*>(st + TCHUNK);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 x = __ldcg(src + q);
+        float4 h, l;
+        h.x = tf32_rna(x.x); l.x = tf32_rna(x.x - h.x);
+        h.y = tf32_rna(x.y); l.y = tf32_rna(x.y - h.y);
+        h.z = tf32_rna(x.z); l.z = tf32_rna(x.z - h.z);
+        h.w = tf32_rna(x.w); l.w = tf32_rna(x.w - h.w);
+        const int off = (m >> 3) * 256 + (m & 7) * 32 + (((u0 + q) ^ (m & 7)) << 2);
+        *reinterpret_cast<float4*>(hi + off) = h;
+        *reinterpret_cast<float4*>(lo + off) = l;
+      }
+    }
+    proxy_fence_shared();
+    __syncthreads();
+    if (tid == 0) {
+      tc_mbar_wait(&R.full[s], (n / TC_STAGES) & 1);
+      tc_fence_after();
+      tc_chunk_mma(R, s, tmem, ch == 0);
+      tc_commit(&R.empty[s]);
+    }
+  }
+  if (tid == 0) tc_commit(accf);
+  tc_mbar_wait(accf, nacc & 1);
+  ++nacc;
+  tc_fence_after();
+  const int w = tid >> 5, lane = tid & 31;
+  const int row = 32 * (w & 3) + lane, c0 = 64 * (w >> 2);
+  float* Lrow = a.W + tlin(i, k) * TILE_F + (int64_t)row * CT + c0;
+  float* ihi = a.img + tlin(i, k) * 2 * TILE_F;
+  float* ilo = ihi + TILE_F;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float v[32];
+    tmem_ld32(tmem + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)(c0 + 32 * h), v);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 x = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      __stcg(reinterpret_cast<float4*>(Lrow + 32 * h) + q, x);
+      float4 hh, ll;
+      hh.x = tf32_rna(x.x); ll.x = tf32_rna(x.x - hh.x);
+      hh.y = tf32_rna(x.y); ll.y = tf32_rna(x.y - hh.y);
+      hh.z = tf32_rna(x.z); ll.z = tf32_rna(x.z - hh.z);
+      hh.w = tf32_rna(x.w); ll.w = tf32_rna(x.w - hh.w);
+      const int off = img_off(row, c0 + 32 * h + 4 * q);
+      __stcg(reinterpret_cast<float4*>(ihi + off), hh);
+      __stcg(reinterpret_cast<float4*>(ilo + off), ll);
+    }
+  }
+  tc_fence_before();
+}
+
+// Cholesky + inverse of a 32x32 SPD block (fp64, all 256 threads) by Gaussian
+// elimination of the augmented [A | I] without pivoting (stable for SPD):
+// A = Lt U, U = diag(p) Lt^T, so L = Lt diag(p)^1/2 and L^-1 = diag(p)^-1/2 Lt^-1,
+// where the I half becomes Lt^-1.  Thread t owns row i = t / 8 and 8 columns of
+// one half (group g = t % 8: g < 4 -> A columns 8g.., g >= 4 -> I columns
+// 8(g-4)..) in registers; one barrier per step: the owners of column j+1 (A
+// half, lower part) and of row j+1 (I half) publish them into double buffers.
+// W (column-major, stride sw) gets L, Ib (stride SB) gets L^-1, upper parts 0.
+__device__ __forceinline__ void cta_ge32(double* W, int sw, double* Ib, double* buf, int* bad) {
+  const int t = threadIdx.x, i = t >> 3, g = t & 7;
+  const bool ahalf = g < 4;
+  const int cb = 8 * (g & 3);
+  double* pv = buf + 128;     // [2][2]: pivot, rsqrt(pivot) of the step (double-buffered)
+  double* rsv = buf + 132;    // [32] rsqrt of every pivot (for the final row scaling)
+  double e[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int c = cb + q;
+    e[q] = ahalf ? (c <= i ? W[c * sw + i] : 0.0) : (c == i ? 1.0 : 0.0);
+  }
+  // publish column 0 (A half), row 0 (I half) and the first pivot
+  if (ahalf && g == 0) {
+    buf[i] = e[0];
+    if (i == 0) {
+      double p = e[0];
+      if (!(p > 0.0)) { *bad = 1; p = 1.0; }
+      pv[0] = p;
+      pv[1] = rsqrt(p);
+    }
+  }
+  if (!ahalf && i == 0) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) buf[64 + cb + q] = e[q];
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int j = 0; j < 32; ++j) {
+    const int sb = j & 1, nb = sb ^ 1;
+    const double* col = buf + sb * 32;        // column j of the A half (rows >= j)
+    const double* row = buf + 64 + sb * 32;   // row j of the I half
+    const double p = pv[2 * sb], rs = pv[2 * sb + 1];
+    const double rp = rs * rs;
+    const double ci = col[i];
+    const double f = (i > j) ? ci * rp : 0.0;   // multiplier Lt[i][j]
+    if (ahalf) {
+      const int qn = (j + 1) & 7;
+      const bool pub = j + 1 < 32 && ((j + 1) >> 3) == (g & 3) && i >= j + 1;
+      double vn = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int c = cb + q;
+        if (c > j && c <= i) e[q] = fma(-f, col[c], e[q]);
+        if (c == j) e[q] = (i > j) ? ci * rs : (i == j ? p * rs : 0.0);   // final L[i][j]
+        if (q == qn) vn = e[q];
+      }
+      if (pub) {
+        buf[nb * 32 + i] = vn;          // column j+1 for the next step
+        if (i == j + 1) {               // owner of the next pivot
+          double pn = vn;
+          if (!(pn > 0.0)) { *bad = 1; pn = 1.0; }
+          pv[2 * nb] = pn;
+          pv[2 * nb + 1] = rsqrt(pn);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (cb + q <= j) e[q] = fma(-f, row[cb + q], e[q]);
+      if (i == j + 1) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) buf[64 + nb * 32 + cb + q] = e[q];
+      }
+    }
+    if (t == 0) rsv[j] = rs;
+    __syncthreads();
+  }
+  if (ahalf) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) W[(cb + q) * sw + i] = (cb + q <= i) ? e[q] : 0.0;
+  } else {
+    const double s = rsv[i];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) Ib[(cb + q) * SB + i] = (cb + q <= i) ? e[q] * s : 0.0;
+  }
+  __syncthreads();
+}
+
+// POTRF(k): fp64 blocked factorisation of the diagonal tile in shared memory
+// (4 panels of 32: warp-level factor + inverse of the panel's diagonal block,
+// DMMA TRSM and SYRK of the rest), then Linv = L_kk^-1 by block forward
+// substitution, written to W_kk (fp32 row-major, for the triangular solves) and
+// to its hi/lo images (TRSM operand).
+__device__ void tc_task_potrf(const TcArgs& a, int k, double* smem) {
+  double* Wt = smem;
+  double* I = smem + CT * SW;
+  double* Mc = I + 4 * 32 * SB;
+  __shared__ int bad;
+  __shared__ double gebuf[5 * 32 + 8];
+  const int tid = threadIdx.x;
+  float* Wk = a.W + tlin(k, k) * TILE_F;
+  if (tid == 0) bad = 0;
+  unsigned long long* ph = a.trace ? a.trace + 4 * (size_t)a.ntasks + 16 * (size_t)k : nullptr;   // phase stamps
+  if (ph && tid == 0) ph[0] = gtimer();
+  {   // The diagonal tile is symmetric (up to the rounding of its updates), so its
+      // row-major fp32 image is read as column-major without a transpose: element
+      // (r, c) of the lower triangle comes from the stored (c, r).  All loads first.
+    float4 q[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) q[u] = __ldcg(reinterpret_cast<const float4*>(Wk) + tid + u * CHOL_THREADS);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int t = 4 * (tid + u * CHOL_THREADS), c = t / CT, r = t % CT;
+      double* d = Wt + c * SW + r;
+      d[0] = q[u].x;
+      d[1] = q[u].y;
+      d[2] = q[u].z;
+      d[3] = q[u].w;
+    }
+  }
+  __syncthreads();
+  if (ph && tid == 0) ph[1] = gtimer();
+  for (int p = 0; p < 4; ++p) {
+    const int c0 = 32 * p, r0 = c0 + 32, nr = CT - r0;
+    cta_ge32(Wt + c0 * SW + c0, SW, I + p * 32 * SB, gebuf, &bad);
+    if (ph && tid == 0) ph[2 + 2 * p] = gtimer();
+    if (nr > 0) {
+      sgemm8<true>(Wt + c0 * SW + r0, SW, I + p * 32 * SB, SB, Mc, TB, nr, 32, 32, 1.0, false, false);
+      __syncthreads();
+      for (int t = tid; t < nr * 32; t += CHOL_THREADS) {
+        const int r = t % nr, c = t / nr;
+        Wt[(c0 + c) * SW + r0 + r] = Mc[c * TB + r];
+      }
+      __syncthreads();
+      sgemm8<true>(Wt + c0 * SW + r0, SW, Wt + c0 * SW + r0, SW, Wt + r0 * SW + r0, SW, nr, nr, 32, -1.0, true, true);
+      __syncthreads();
+    }
+    if (ph && tid == 0) ph[3 + 2 * p] = gtimer();
+  }
+  if (tid == 0 && bad) atomicExch(a.status, 1);
+  float* ihi = a.img + tlin(k, k) * 2 * TILE_F;
+  float* ilo = ihi + TILE_F;
+  for (int p = 0; p < 4; ++p) {
+    for (int i = p + 1; i < 4; ++i) {
+      double* T = Mc + i * 32 * SB;
+      for (int m = p; m < i; ++m) {
+        const double* Mmp = (m == p) ? I + p * 32 * SB : Mc + m * 32 * SB;
+        sgemm8<false>(Wt + (32 * m) * SW + 32 * i, SW, Mmp, SB, T, SB, 32, 32, 32, 1.0, m != p, false);
+        __syncthreads();
+      }
+      double* tmp = Mc + p * 32 * SB;
+      sgemm8<false>(I + i * 32 * SB, SB, T, SB, tmp, SB, 32, 32, 32, -1.0, false, false);
+      __syncthreads();
+      {
+        const int r = tid & 31, cq = tid >> 5;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) T[(cq + 8 * q) * SB + r] = tmp[(cq + 8 * q) * SB + r];
+      }
+      __syncthreads();
+    }
+    // column block p of Linv: rows r (warp-contiguous columns c -> coalesced row-major stores)
+    for (int t = tid; t < CT * 32; t += CHOL_THREADS) {
+      const int r = t >> 5, c = t & 31, ib = r >> 5;
+      double v = 0.0;
+      if (ib == p) v = I[p * 32 * SB + c * SB + (r & 31)];
+      else if (ib > p) v = Mc[ib * 32 * SB + c * SB + (r & 31)];
+      const float f = (float)v, h = tf32_rna(f);
+      const int col = 32 * p + c;
+      __stcg(Wk + r * CT + col, f);
+      const int off = img_off(r, col);
+      __stcg(ihi + off, h);
+      __stcg(ilo + off, tf32_rna(f - h));
+    }
+    __syncthreads();
+  }
+  if (ph && tid == 0) ph[10] = gtimer();
+  proxy_fence_shared();   // generic smem writes before later bulk copies into the same bytes
+}
+
+__global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
+  extern __shared__ __align__(16) unsigned char tc_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t full[TC_STAGES], empty[TC_STAGES], accf;
+  __shared__ uint32_t tmem_sh;
+  __shared__ int tsk;
+  const int tid = threadIdx.x, nt = a.nt;
+  if (tid < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(su32(&tmem_sh)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) {
+      tc_mbar_init(&full[s], 1);
+      tc_mbar_init(&empty[s], 1);
+    }
+    tc_mbar_init(&accf, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_sh;
+  TcRing R{full, empty, sm, 0u, 0u};
+  uint32_t nacc = 0;
+  while (true) {
+    if (tid == 0) tsk = atomicAdd(a.counter, 1);
+    __syncthreads();
+    const int t = tsk;
+    __syncthreads();
+    if (t >= a.ntasks) break;
+    const CholTask T = a.tasks[t];
+    unsigned long long t0 = 0;
+    if (a.trace && tid == 0) t0 = gtimer();
+    switch (T.type) {
+      case T_POTRF:
+        wait_geq(&a.upd[T.k * nt + T.k], T.expect);
+        __syncthreads();
+        if (a.trace && tid == 0) a.trace[4 * t + 1] = gtimer();
+        tc_task_potrf(a, T.k, reinterpret_cast<double*>(sm));
+        proxy_fence_global();
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) st_release(&a.done[T.k * nt + T.k], 1);
+        break;
+      case T_TRSM:
+        wait_geq(&a.done[T.k * nt + T.k], 1);
+        wait_geq(&a.upd[T.i * nt + T.k], T.expect);
+        __syncthreads();
+        if (a.trace && tid == 0) a.trace[4 * t + 1] = gtimer();
+        tc_task_trsm(a, R, &accf, nacc, tmem, T.i, T.k);
+        proxy_fence_global();
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) st_release(&a.done[T.i * nt + T.k], 1);
+        break;
+      case T_GEMM:
+        wait_geq(&a.done[T.i * nt + T.k], 1);
+        wait_geq(&a.done[T.j * nt + T.k], 1);
+        if (T.k2 >= 0) {
+          wait_geq(&a.done[T.i * nt + T.k2], 1);
+          wait_geq(&a.done[T.j * nt + T.k2], 1);
+        }
+        wait_geq(&a.upd[T.i * nt + T.j], T.expect);
+        __syncthreads();
+        if (a.trace && tid == 0) a.trace[4 * t + 1] = gtimer();
+        tc_task_gemm(a, R, &accf, nacc, tmem, T.i, T.j, T.k, T.k2);
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) st_release(&a.upd[T.i * nt + T.j], T.expect + (T.k2 >= 0 ? 2 : 1));
+        break;
+      default:
+        break;
+    }
+    if (a.trace && tid == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+      a.trace[4 * t + 0] = t0;
+      a.trace[4 * t + 2] = gtimer();
+      a.trace[4 * t + 3] = smid;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+}
+
+// ---------------------------------------------------------------------------
+// scaling / conversion, triangular solves, fp64 residual
+// ---------------------------------------------------------------------------
+// D = diag(H)^-1/2 (padding rows: 1)
+__global__ void k_tc_diag(const double* __restrict__ H, int64_t ld, int n, int npad, double* __restrict__ D) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= npad) return;
+  double d = 1.0;
+  if (r < n) {
+    const double h = H[(int64_t)r * ld + r];
+    d = h > 0.0 ? rsqrt(h) : 1.0;   // non-positive diagonal: the factorisation reports it
+  }
+  D[r] = d;
+}
+
+// W_ij = fp32(D_i H_ij D_j) from the lower triangle (identity padding); one CTA per lower tile
+__global__ void __launch_bounds__(256) k_tc_convert(const double* __restrict__ H, int64_t ld, int n, int nt,
+                                                    const double* __restrict__ D, float* __restrict__ W) {
+  __shared__ float tr[32][33];
+  const int64_t id = blockIdx.x;
+  int i = (int)((sqrt(8.0 * (double)id + 1.0) - 1.0) * 0.5);
+  while ((int64_t)(i + 1) * (i + 2) / 2 <= id) ++i;
+  while ((int64_t)i * (i + 1) / 2 > id) --i;
+  const int j = (int)(id - (int64_t)i * (i + 1) / 2);
+  float* Wt = W + id * TILE_F;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
+  for (int rb = 0; rb < CT; rb += 32)
+    for (int cb = 0; cb < CT; cb += 32) {
+      // read H column-major (coalesced over rows), write W row-major via a transpose
+      for (int c = ty; c < 32; c += 8) {
+        const int R = CT * i + rb + tx, C = CT * j + cb + c;
+        float v;
+        if (R < n && C < n) {
+          const int64_t a = (R >= C) ? (int64_t)C * ld + R : (int64_t)R * ld + C;   // lower triangle
+          v = (float)(D[R] * H[a] * D[C]);
+        } else {
+          v = (R == C) ? 1.0f : 0.0f;
+        }
+        tr[c][tx] = v;
+      }
+      __syncthreads();
+      for (int r = ty; r < 32; r += 8) Wt[(rb + r) * CT + cb + tx] = tr[tx][r];
+      __syncthreads();
+    }
+}
+
+// forward solve  L y = v  (v = D r), flags fl[k] = gen when y_k is final.
+// CTA b handles row tiles b, b + G, ...; rows r: two threads per row.
+__global__ void __launch_bounds__(256) k_tc_fwd(const float* __restrict__ W, int nt, const double* __restrict__ r,
+                                                const double* __restrict__ D, double* __restrict__ y,
+                                                int* __restrict__ fl, int gen, const int* __restrict__ stop) {
+  __shared__ double ys[CT], acc[CT];
+  if (*stop) return;   // refinement converged in an earlier pass
+  const int tid = threadIdx.x, row = tid >> 1, h = tid & 1;
+  for (int k = blockIdx.x; k < nt; k += gridDim.x) {
+    double a = (h == 0) ? D[CT * k + row] * r[CT * k + row] : 0.0;
+    for (int jj = 0; jj <= k; ++jj) {
+      const float* T;
+      if (jj < k) {
+        if (tid == 0) {
+          int ns = 32;
+          while (ld_acquire(&fl[jj]) < gen) { __nanosleep(ns); if (ns < 512) ns <<= 1; }
+        }
+        __syncthreads();
+        if (tid < CT) ys[tid] = __ldcg(y + CT * jj + tid);
+        T = W + tlin(k, jj) * TILE_F;
+      } else {   // y_k = Linv_kk acc
+        if (h == 0) acc[row] = a;
+        __syncthreads();
+        if (tid < CT) ys[tid] = acc[tid];
+        a = 0.0;
+        T = W + tlin(k, k) * TILE_F;
+      }
+      __syncthreads();
+      const float4* p = reinterpret_cast<const float4*>(T + (int64_t)row * CT + 64 * h);
+      double s = 0.0;
+#pragma unroll 4
+      for (int q = 0; q < 16; ++q) {
+        const float4 v = __ldcg(p + q);
+        const int c = 64 * h + 4 * q;
+        s = fma((double)v.x, ys[c], s);
+        s = fma((double)v.y, ys[c + 1], s);
+        s = fma((double)v.z, ys[c + 2], s);
+        s = fma((double)v.w, ys[c + 3], s);
+      }
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      if (jj < k) a -= (h == 0) ? s : 0.0;
+      else a = s;
+      __syncthreads();
+    }
+    if (h == 0) __stcg(y + CT * k + row, a);
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) st_release(&fl[k], gen);
+  }
+}
+
+// backward solve  L^T z = y, x += D z  (x accumulated in place), flags fl[k] = gen.
+// CTA b handles row tiles nt-1-b, nt-1-b-G, ...; column c: two threads per column.
+__global__ void __launch_bounds__(256) k_tc_bwd(const float* __restrict__ W, int nt, const double* __restrict__ y,
+                                                double* __restrict__ z, const double* __restrict__ D,
+                                                double* __restrict__ x, double* __restrict__ dxmax,
+                                                double* __restrict__ xmax, int* __restrict__ fl, int gen,
+                                                const int* __restrict__ stop) {
+  __shared__ double zs[CT], acc[CT], part[CT];
+  if (*stop) return;
+  const int tid = threadIdx.x, col = tid & (CT - 1), h = tid >> 7;
+  for (int kb = blockIdx.x; kb < nt; kb += gridDim.x) {
+    const int k = nt - 1 - kb;
+    double a = (h == 0) ? __ldcg(y + CT * k + col) : 0.0;
+    for (int ii = nt - 1; ii >= k; --ii) {
+      const float* T;
+      if (ii > k) {
+        if (tid == 0) {
+          int ns = 32;
+          while (ld_acquire(&fl[ii]) < gen) { __nanosleep(ns); if (ns < 512) ns <<= 1; }
+        }
+        __syncthreads();
+        if (tid < CT) zs[tid] = __ldcg(z + CT * ii + tid);
+        T = W + tlin(ii, k) * TILE_F;
+      } else {   // z_k = Linv_kk^T acc
+        if (h == 0) acc[col] = a;
+        __syncthreads();
+        if (tid < CT) zs[tid] = acc[tid];
+        a = 0.0;
+        T = W + tlin(k, k) * TILE_F;
+      }
+      __syncthreads();
+      double s = 0.0;   // sum over rows [64h, 64h+64) of T[r][col] zs[r]
+#pragma unroll 8
+      for (int rr = 0; rr < 64; ++rr) {
+        const int rw = 64 * h + rr;
+        s = fma((double)__ldcg(T + (int64_t)rw * CT + col), zs[rw], s);
+      }
+      if (h == 1) part[col] = s;
+      __syncthreads();
+      if (h == 0) {
+        s += part[col];
+        if (ii > k) a -= s;
+        else a = s;
+      }
+      __syncthreads();
+    }
+    if (h == 0) {
+      __stcg(z + CT * k + col, a);
+      const double dxv = D[CT * k + col] * a;
+      const double xn = x[CT * k + col] + dxv;
+      x[CT * k + col] = xn;
+      // max |dx|, max |x| (non-negative doubles order like their bit patterns)
+      if (dxmax)
+        atomicMax(reinterpret_cast<unsigned long long*>(dxmax), (unsigned long long)__double_as_longlong(fabs(dxv)));
+      if (xmax)
+        atomicMax(reinterpret_cast<unsigned long long*>(xmax), (unsigned long long)__double_as_longlong(fabs(xn)));
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) st_release(&fl[k], gen);
+  }
+}
+
+// symmetric H x from the lower triangle, 64x64 fp64 blocks: P[a][b][0..64) = contribution
+// of block (max(a,b), min(a,b)) to rows of block a
+constexpr int SYB = 64;
+__global__ void __launch_bounds__(128) k_tc_symv(const double* __restrict__ H, int64_t ld, int n, int nb,
+                                                 const double* __restrict__ x, double* __restrict__ P,
+                                                 const int* __restrict__ stop) {
+  __shared__ double Ts[SYB][SYB + 1];
+  __shared__ double xi[SYB], xj[SYB];
+  if (*stop) return;
+  const int64_t id = blockIdx.x;
+  int i = (int)((sqrt(8.0 * (double)id + 1.0) - 1.0) * 0.5);
+  while ((int64_t)(i + 1) * (i + 2) / 2 <= id) ++i;
+  while ((int64_t)i * (i + 1) / 2 > id) --i;
+  const int j = (int)(id - (int64_t)i * (i + 1) / 2);
+  const int tid = threadIdx.x;
+  for (int t = tid; t < SYB * SYB; t += 128) {
+    const int r = t % SYB, c = t / SYB;
+    const int R = SYB * i + r, C = SYB * j + c;
+    Ts[c][r] = (R < n && C < n) ? H[(int64_t)C * ld + R] : 0.0;
+  }
+  if (tid < SYB) {
+    const int R = SYB * i + tid, C = SYB * j + tid;
+    xi[tid] = R < n ? x[R] : 0.0;
+    xj[tid] = C < n ? x[C] : 0.0;
+  }
+  __syncthreads();
+  if (tid < SYB) {   // rows of block i: sum_c H(r, c) x_j[c]
+    const int r = tid;
+    double s = 0.0;
+    for (int c = 0; c < SYB; ++c) {
+      const double hv = (i != j || c <= r) ? Ts[c][r] : Ts[r][c];
+      s = fma(hv, xj[c], s);
+    }
+    P[((int64_t)i * nb + j) * SYB + r] = s;
+  } else if (i != j) {   // rows of block j: sum_r H(r, c) x_i[r]
+    const int c = tid - SYB;
+    double s = 0.0;
+    for (int r = 0; r < SYB; ++r) s = fma(Ts[c][r], xi[r], s);
+    P[((int64_t)j * nb + i) * SYB + c] = s;
+  }
+}
+
+// r = b - H x  (fixed-order sum of the block partials); padding rows 0
+__global__ void k_tc_resid(const double* __restrict__ b, const double* __restrict__ P, int n, int npad, int nb,
+                           double* __restrict__ r, const int* __restrict__ stop) {
+  if (*stop) return;
+  const int R = blockIdx.x * blockDim.x + threadIdx.x;
+  if (R >= npad) return;
+  if (R >= n) { r[R] = 0.0; return; }
+  const int a = R / SYB, rr = R % SYB;
+  double s = 0.0;
+  for (int c = 0; c < nb; ++c) s += P[((int64_t)a * nb + c) * SYB + rr];
+  r[R] = b[R] - s;
+}
+
+// after a refinement pass: stop when the correction is below tol max|x|, else
+// clear the maxima for the next pass (the last pass's values stay in out2)
+__global__ void k_tc_check(double* out2, int* stop, double tol, int last) {
+  if (*stop) return;
+  if (out2[0] <= tol * out2[1]) *stop = 1;
+  else if (!last) out2[0] = out2[1] = 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// host: workspace and driver
+// ---------------------------------------------------------------------------
+size_t chol_tc_smem_bytes() { return TC_SMEM; }
+
+// bytes of the mixed-precision workspace for an npad x npad system
+size_t chol_tc_ws_bytes(int npad) {
+  const int nt = npad / CT;
+  const int64_t ntl = (int64_t)nt * (nt + 1) / 2;
+  const int nb = (npad + SYB - 1) / SYB;
+  return sizeof(float) * (size_t)ntl * TILE_F * 3                  // W + two image parts
+         + sizeof(double) * ((size_t)npad * 4)                      // D, r, y, z
+         + sizeof(double) * (size_t)nb * nb * SYB                   // symv partials
+         + sizeof(int) * ((size_t)2 * nt * nt + 2 + 2 * (size_t)nt) + 256 * 10;
+}
+
+// Solve H x = b (H: fp64 column-major, lower triangle read, npad = nt * 128,
+// rows >= n are padding) with the tcgen05 factorisation + `iters` fp64
+// refinement passes.  *status: 1 = non-positive pivot in the fp32 factor.
+// Writes x[npad].  `ws` holds chol_tc_ws_bytes(npad) bytes; `tasks` the DAG
+// from chol_plan_tasks(nt) (substitution tasks are skipped); `gen` must grow
+// by at least 2 * iters between calls sharing `ws` (flag generations).
+int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b, double* x, void* ws,
+                  const void* tasks, int ntasks, int iters, int* status, int gen, cudaStream_t st, double* out2,
+                  unsigned long long* trace) {
+  const int nt = npad / CT;
+  if (nt <= 0) return 0;
+  const int64_t ntl = (int64_t)nt * (nt + 1) / 2;
+  const int nb = (npad + SYB - 1) / SYB;
+  char* p = reinterpret_cast<char*>(ws);
+  auto take = [&](size_t bytes) { char* q = p; p += (bytes + 255) / 256 * 256; return q; };
+  float* W = reinterpret_cast<float*>(take(sizeof(float) * ntl * TILE_F));
+  float* img = reinterpret_cast<float*>(take(sizeof(float) * ntl * TILE_F * 2));
+  double* D = reinterpret_cast<double*>(take(sizeof(double) * npad));
+  double* r = reinterpret_cast<double*>(take(sizeof(double) * npad));
+  double* y = reinterpret_cast<double*>(take(sizeof(double) * npad));
+  double* z = reinterpret_cast<double*>(take(sizeof(double) * npad));
+  double* P = reinterpret_cast<double*>(take(sizeof(double) * (size_t)nb * nb * SYB));
+  int* flags = reinterpret_cast<int*>(take(sizeof(int) * ((size_t)2 * nt * nt + 1)));
+  int* sfl = reinterpret_cast<int*>(take(sizeof(int) * 2 * (size_t)nt));
+  int* stop = reinterpret_cast<int*>(take(sizeof(int)));
+  static int grid = 0, sms = 0;
+  if (grid == 0) {
+    cudaFuncSetAttribute(k_chol_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM);
+    int dev = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_chol_tc, CHOL_THREADS, TC_SMEM);
+    grid = sms * (per > 0 ? per : 1);
+  }
+  k_tc_diag<<<(npad + 255) / 256, 256, 0, st>>>(H, ld, n, npad, D);
+  k_tc_convert<<<(unsigned)ntl, 256, 0, st>>>(H, ld, n, nt, D, W);
+  cudaMemsetAsync(flags, 0, sizeof(int) * ((size_t)2 * nt * nt + 1), st);
+  TcArgs a;
+  a.W = W;
+  a.img = img;
+  a.nt = nt;
+  a.upd = flags;
+  a.done = flags + (size_t)nt * nt;
+  a.counter = flags + (size_t)2 * nt * nt;
+  a.tasks = reinterpret_cast<const CholTask*>(tasks);
+  a.ntasks = ntasks;
+  a.status = status;
+  a.trace = trace;
+  k_chol_tc<<<ntasks < grid ? ntasks : grid, CHOL_THREADS, TC_SMEM, st>>>(a);
+  launch_count();
+  launch_count();
+  launch_count();
+  cudaMemsetAsync(x, 0, sizeof(double) * npad, st);
+  cudaMemsetAsync(stop, 0, sizeof(int), st);
+  cudaMemsetAsync(out2, 0, sizeof(double) * 2, st);
+  const int gs = nt < sms ? nt : sms;
+  // passes until the correction is < 1e-12 max|x| (early-exit kernels after that), at most `iters`
+  for (int it = 0; it < iters; ++it) {
+    const double* rhs = b;
+    if (it > 0) {
+      k_tc_symv<<<(unsigned)((int64_t)nb * (nb + 1) / 2), 128, 0, st>>>(H, ld, n, nb, x, P, stop);
+      k_tc_resid<<<(npad + 255) / 256, 256, 0, st>>>(b, P, n, npad, nb, r, stop);
+      launch_count();
+      launch_count();
+      rhs = r;
+    }
+    k_tc_fwd<<<gs, 256, 0, st>>>(W, nt, rhs, D, y, sfl, gen + 2 * it, stop);
+    k_tc_bwd<<<gs, 256, 0, st>>>(W, nt, y, z, D, x, out2, out2 + 1, sfl + nt, gen + 2 * it, stop);
+    k_tc_check<<<1, 1, 0, st>>>(out2, stop, 1e-12, it == iters - 1);
+    launch_count();
+    launch_count();
+    launch_count();
+  }
+  return 0;
+}
+
+// Summary of a task trace ([ntasks][4] globaltimer stamps) on stderr (diagnostics).
+void chol_trace_print(const char* tag, const unsigned long long* d_trace, const void* d_tasks, int ntasks, int nt) {
+  {
+    std::vector<unsigned long long> ph((size_t)16 * nt);
+    cudaMemcpy(ph.data(), d_trace + 4 * (size_t)ntasks, ph.size() * 8, cudaMemcpyDeviceToHost);
+    double ld = 0, f = 0, u = 0, inv = 0;
+    for (int k = 0; k < nt; ++k) {
+      const unsigned long long* q = &ph[16 * (size_t)k];
+      if (!q[0] || !q[10]) continue;
+      ld += (double)(q[1] - q[0]) * 1e-3;
+      unsigned long long prev = q[1];
+      for (int p = 0; p < 4; ++p) {
+        f += (double)(q[2 + 2 * p] - prev) * 1e-3;
+        u += (double)(q[3 + 2 * p] - q[2 + 2 * p]) * 1e-3;
+        prev = q[3 + 2 * p];
+      }
+      inv += (double)(q[10] - q[9]) * 1e-3;
+    }
+    fprintf(stderr, "  POTRF phases (avg us): load %.2f | factor32 x4 %.2f | trsm+syrk %.2f | inverse+store %.2f\n",
+            ld / nt, f / nt, u / nt, inv / nt);
+  }
+  std::vector<unsigned long long> tr((size_t)4 * ntasks);
+  std::vector<CholTask> tk(ntasks);
+  cudaMemcpy(tr.data(), d_trace, tr.size() * 8, cudaMemcpyDeviceToHost);
+  cudaMemcpy(tk.data(), d_tasks, tk.size() * sizeof(CholTask), cudaMemcpyDeviceToHost);
+  unsigned long long t0 = ~0ull, t1 = 0;
+  double busy[5] = {0, 0, 0, 0, 0}, wait[5] = {0, 0, 0, 0, 0};
+  int cnt[5] = {0, 0, 0, 0, 0};
+  for (int q = 0; q < ntasks; ++q) {
+    if (tr[4 * q] == 0) continue;
+    t0 = std::min(t0, tr[4 * q]);
+    t1 = std::max(t1, tr[4 * q + 2]);
+    const int ty = tk[q].type;
+    busy[ty] += (double)(tr[4 * q + 2] - tr[4 * q + 1]) * 1e-3;
+    wait[ty] += (double)(tr[4 * q + 1] - tr[4 * q]) * 1e-3;
+    cnt[ty] += 1;
+  }
+  const char* nm[5] = {"POTRF", "TRSM", "GEMM", "BUPD", "BSOL"};
+  fprintf(stderr, "[%s trace] nt=%d tasks=%d span %.1f us\n", tag, nt, ntasks, (double)(t1 - t0) * 1e-3);
+  for (int ty = 0; ty < 5; ++ty)
+    if (cnt[ty])
+      fprintf(stderr, "  %-5s n=%6d  avg busy %8.2f us  avg wait %8.2f us  total busy %.1f us\n", nm[ty], cnt[ty],
+              busy[ty] / cnt[ty], wait[ty] / cnt[ty], busy[ty]);
+}
+
 }  // namespace vba

@@ -49,8 +49,9 @@ constexpr int NBc = 128;         // Cholesky tile (vba_chol.cu)
 struct Result {       // device -> host once per trial
   double energy[3];
   unsigned long long step_bits;
-  int status;
-  int pad;
+  int status;         // fp64 factorisation: non-positive pivot
+  int tc_bad;         // tensor-core factorisation: non-positive pivot
+  double tc[2];       // tensor-core solve: last refinement correction, max |x|
 };
 
 template <class T>
@@ -118,6 +119,12 @@ struct Ctx {
   int* d_cflags = nullptr;         // Cholesky DAG counters
   void* d_ctasks = nullptr;        // Cholesky task list
   int n_ctasks = 0;
+  void* d_tcws = nullptr;          // tensor-core (3xTF32 + fp64 refinement) solve workspace
+  bool use_tc = false;             // VBA_CHOL=tc: tensor-core reduced solve
+  bool force_fp64 = false;         // this step: fp64 DAG (tensor-core solve failed its checks)
+  int tc_gen = 1;
+  int tc_iters = 8;   // refinement passes at most (early exit once converged)
+  int64_t tc_fallbacks = 0;
   int32_t* d_fmap = nullptr;
   Result* d_res = nullptr;
   Result* h_res = nullptr;
@@ -637,8 +644,14 @@ static int stage_step(Ctx* c, double lam, cudaStream_t st) {
       if (dalloc(c, &c->d_trace, (size_t)4 * std::max(1, c->n_ctasks) + 16 * (size_t)std::max(1, c->nt)))
         return VBA_E_CUDA;
     }
-    chol_dag_launch(c->d_H, c->npad, c->nt, c->d_rhs, c->d_x, c->d_Ld, c->d_cpart, c->d_cflags, c->d_ctasks,
-                    c->n_ctasks, &c->d_res->status, st, c->d_trace);
+    if (c->use_tc && !c->force_fp64 && !c->d_trace) {
+      chol_tc_solve(c->d_H, c->npad, c->nfree, c->npad, c->d_rhs, c->d_x, c->d_tcws, c->d_ctasks, c->n_ctasks,
+                    c->tc_iters, &c->d_res->tc_bad, c->tc_gen, st, c->d_res->tc);
+      c->tc_gen += 2 * c->tc_iters;
+    } else {
+      chol_dag_launch(c->d_H, c->npad, c->nt, c->d_rhs, c->d_x, c->d_Ld, c->d_cpart, c->d_cflags, c->d_ctasks,
+                      c->n_ctasks, &c->d_res->status, st, c->d_trace);
+    }
   }
   mark(c, 4, st);
   launch_scatter_dx(c->d_x, c->d_fmap, c->npv, c->d_dx, st);
@@ -740,6 +753,14 @@ static int stage_step_any(Ctx* c, double lam, int use_schur, cudaStream_t st) {
   return stage_step_dense(c, lam, st);
 }
 
+// The tensor-core solve is accepted when its fp32 factor had positive pivots and
+// the last fp64 refinement pass moved x by < 1e-8 max|x| (converged to fp64).
+static bool tc_failed(const Ctx* c, int use_schur) {
+  if (!c->use_tc || c->force_fp64 || c->d_trace || c->nfree == 0 || !(use_schur || c->n_disp == 0)) return false;
+  const Result& r = *c->h_res;
+  return r.tc_bad != 0 || !(r.tc[0] <= 1e-8 * r.tc[1]);
+}
+
 static int run_trial(Ctx* c, double lam, int use_schur, vba_trial_result* out, cudaStream_t st) {
   int rc = stage_step_any(c, lam, use_schur, st);
   if (rc) return rc;
@@ -753,6 +774,13 @@ static int run_trial(Ctx* c, double lam, int use_schur, vba_trial_result* out, c
   }
   VBA_CUDA(cudaMemcpyAsync(c->h_res, c->d_res, sizeof(Result), cudaMemcpyDeviceToHost, st));
   VBA_CUDA(cudaStreamSynchronize(st));
+  if (tc_failed(c, use_schur)) {   // tensor-core solve failed its own checks: redo the step in fp64
+    ++c->tc_fallbacks;
+    c->force_fp64 = true;
+    rc = run_trial(c, lam, use_schur, out, st);
+    c->force_fp64 = false;
+    return rc;
+  }
   prof_collect(c, c->lin_pending);
   c->lin_pending = false;
   if (c->d_trace && use_schur) {   // Cholesky DAG task timing summary (diagnostics)
@@ -892,6 +920,18 @@ int vba_create(void** out, const vba_problem* prob, const vba_options* opts, voi
       (rc = dalloc(c, &c->d_dx, (size_t)c->npv)) || (rc = dalloc(c, &c->d_res, 1)))
     return fail(rc);
   if (cudaMallocHost((void**)&c->h_res, sizeof(Result)) != cudaSuccess) { set_err("pinned alloc failed"); return fail(VBA_E_CUDA); }
+  {
+    // tensor-core reduced solve: opt-in (VBA_CHOL=tc) until its DAG beats the fp64 one
+    const char* ch = getenv("VBA_CHOL");
+    c->use_tc = ch && std::strcmp(ch, "tc") == 0 && c->nt > 0;
+    const char* it = getenv("VBA_TC_ITERS");
+    if (it) c->tc_iters = std::max(1, atoi(it));
+  }
+  if (c->use_tc) {
+    const size_t wb = chol_tc_ws_bytes(c->npad);
+    if ((rc = dalloc(c, (char**)&c->d_tcws, wb))) return fail(rc);
+    cudaMemsetAsync(c->d_tcws, 0, wb, st);
+  }
   {  // Cholesky task DAG (dense, lookahead 1)
     const int cap = chol_plan_tasks(c->nt, nullptr, 0);
     std::vector<char> buf((size_t)std::max(cap, 1) * chol_task_bytes());
@@ -947,6 +987,76 @@ int vba_set_collective(void* ctx, vba_allreduce_fn fn, void* user) {
 int64_t vba_reduced_dim(void* ctx) { return ((Ctx*)ctx)->nfree; }
 int64_t vba_launch_count(void* /*ctx*/) { return launch_total(); }
 
+int vba_stats(void* ctx, int64_t* out4) {
+  Ctx* c = (Ctx*)ctx;
+  out4[0] = c->use_tc ? 1 : 0;
+  out4[1] = c->tc_fallbacks;
+  out4[2] = c->tc_gen;
+  out4[3] = c->tc_iters;
+  return VBA_OK;
+}
+
+// Standalone SPD solve (np.linalg.solve of solver.py:287 on a damped reduced system).
+int vba_spd_solve(const double* H, int64_t n, const double* b, double* x, int32_t mode, void* stream,
+                  int32_t* info) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n <= 0 || n > (int64_t)1 << 16) { set_err("vba_spd_solve: n out of range"); return VBA_E_INVALID; }
+  const int npad = (int)((n + NBc - 1) / NBc * NBc), nt = npad / NBc;
+  const int cap = chol_plan_tasks(nt, nullptr, 0);
+  std::vector<char> tb((size_t)cap * chol_task_bytes());
+  const int ntasks = chol_plan_tasks(nt, tb.data(), cap);
+  const size_t tcb = mode != 1 ? chol_tc_ws_bytes(npad) : 0;
+  double *Hp = nullptr, *bp = nullptr, *xp = nullptr, *Ld = nullptr, *part = nullptr, *tc2 = nullptr;
+  int *flags = nullptr, *stat = nullptr;
+  void *tasks = nullptr, *ws = nullptr;
+  auto cleanup = [&]() {
+    cudaFree(Hp); cudaFree(bp); cudaFree(xp); cudaFree(Ld); cudaFree(part); cudaFree(tc2);
+    cudaFree(flags); cudaFree(stat); cudaFree(tasks); cudaFree(ws);
+  };
+  if (cudaMalloc(&Hp, sizeof(double) * (size_t)npad * npad) || cudaMalloc(&bp, sizeof(double) * npad) ||
+      cudaMalloc(&xp, sizeof(double) * npad) || cudaMalloc(&Ld, sizeof(double) * (size_t)nt * NBc * NBc) ||
+      cudaMalloc(&part, sizeof(double) * (size_t)nt * nt * NBc) || cudaMalloc(&tc2, sizeof(double) * 2) ||
+      cudaMalloc(&flags, sizeof(int) * ((size_t)2 * nt * nt + nt + 1)) || cudaMalloc(&stat, sizeof(int) * 2) ||
+      cudaMalloc(&tasks, tb.size()) || (tcb && cudaMalloc(&ws, tcb))) {
+    cleanup();
+    set_err("vba_spd_solve: allocation failed");
+    return VBA_E_CUDA;
+  }
+  cudaMemsetAsync(Hp, 0, sizeof(double) * (size_t)npad * npad, st);
+  cudaMemsetAsync(bp, 0, sizeof(double) * npad, st);
+  cudaMemsetAsync(stat, 0, sizeof(int) * 2, st);
+  cudaMemsetAsync(tc2, 0, sizeof(double) * 2, st);
+  if (tcb) cudaMemsetAsync(ws, 0, tcb, st);
+  cudaMemcpy2DAsync(Hp, sizeof(double) * npad, H, sizeof(double) * n, sizeof(double) * n, n,
+                    cudaMemcpyDeviceToDevice, st);
+  cudaMemcpyAsync(bp, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
+  cudaMemcpyAsync(tasks, tb.data(), tb.size(), cudaMemcpyHostToDevice, st);
+  launch_pad_identity(Hp, npad, (int)n, npad, bp, st);
+  int hs[2] = {0, 0};
+  double h2[2] = {0, 0};
+  int used_tc = 0;
+  if (mode == 0 || mode == 2) {   // 2: tensor-core result without the fallback (diagnostics)
+    const int iters = info && info[0] > 0 ? info[0] : 8;
+    unsigned long long* tr = nullptr;
+    if (getenv("VBA_CHOL_TRACE")) { cudaMalloc(&tr, sizeof(unsigned long long) * (4 * (size_t)ntasks + 16 * (size_t)nt)); cudaMemsetAsync(tr, 0, sizeof(unsigned long long) * (4 * (size_t)ntasks + 16 * (size_t)nt), st); }
+    chol_tc_solve(Hp, npad, (int)n, npad, bp, xp, ws, tasks, ntasks, iters, stat + 1, 1, st, tc2, tr);
+    if (tr) { cudaStreamSynchronize(st); chol_trace_print("tc", tr, tasks, ntasks, nt); cudaFree(tr); }
+    cudaMemcpyAsync(hs, stat, sizeof(hs), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(h2, tc2, sizeof(h2), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) { cleanup(); set_err("vba_spd_solve: %s", cudaGetErrorString(cudaGetLastError())); return VBA_E_CUDA; }
+    used_tc = (mode == 2 || (hs[1] == 0 && h2[0] <= 1e-8 * h2[1])) ? 1 : 0;
+  }
+  if (!used_tc) {
+    chol_dag_launch(Hp, npad, nt, bp, xp, Ld, part, flags, tasks, ntasks, stat, st);
+    cudaMemcpyAsync(hs, stat, sizeof(hs), cudaMemcpyDeviceToHost, st);
+  }
+  cudaMemcpyAsync(x, xp, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) { cleanup(); set_err("vba_spd_solve: %s", cudaGetErrorString(cudaGetLastError())); return VBA_E_CUDA; }
+  if (info) { info[0] = used_tc; info[1] = hs[1]; }
+  cleanup();
+  return hs[0] ? VBA_E_NOT_SPD : VBA_OK;
+}
+
 int vba_energy(void* ctx, void* stream, double* tot, double* vis, double* ine) {
   Ctx* c = (Ctx*)ctx;
   cudaStream_t st = (cudaStream_t)stream;
@@ -976,6 +1086,15 @@ int vba_solve_step(void* ctx, void* stream, double lam, int32_t use_schur) {
   if (rc) return rc;
   VBA_CUDA(cudaMemcpyAsync(c->h_res, c->d_res, sizeof(Result), cudaMemcpyDeviceToHost, st));
   VBA_CUDA(cudaStreamSynchronize(st));
+  if (tc_failed(c, use_schur)) {
+    ++c->tc_fallbacks;
+    c->force_fp64 = true;
+    rc = stage_step_any(c, lam, use_schur, st);
+    c->force_fp64 = false;
+    if (rc) return rc;
+    VBA_CUDA(cudaMemcpyAsync(c->h_res, c->d_res, sizeof(Result), cudaMemcpyDeviceToHost, st));
+    VBA_CUDA(cudaStreamSynchronize(st));
+  }
   return c->h_res->status ? VBA_E_NOT_SPD : VBA_OK;
 }
 

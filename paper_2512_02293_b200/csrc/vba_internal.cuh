@@ -317,6 +317,13 @@ size_t chol_task_bytes();
 int chol_dag_launch(double* A, int64_t ld, int nt, double* rhs, double* x, double* Linv, double* part, int* flags,
                     const void* tasks, int ntasks, int* status, cudaStream_t st,
                     unsigned long long* trace = nullptr);
+// Mixed-precision (tcgen05 3xTF32 factor + fp64 iterative refinement) SPD solve,
+// vba_chol.cu.  out2[0] = max |correction| of the last refinement pass, out2[1] = max |x|.
+size_t chol_tc_ws_bytes(int npad);
+int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b, double* x, void* ws,
+                  const void* tasks, int ntasks, int iters, int* status, int gen, cudaStream_t st, double* out2,
+                  unsigned long long* trace = nullptr);
+void chol_trace_print(const char* tag, const unsigned long long* d_trace, const void* d_tasks, int ntasks, int nt);
 // copy the task list back (for trace decoding): type,i,j,k per task
 void chol_task_fields(const void* tasks, int n, int* out4);
 int chol_solve(double* H, int64_t ld, int npad, double* rhs, double* x, double* Ldiag, int* status,

@@ -173,7 +173,19 @@ void launch_edge_prep(const DevState& s, const int32_t* ei, const int32_t* ej, i
 // of S = sum w K^T K and 6 of s = sum w K^T r (slots 27..31 zero), and per
 // pixel H_dd, g_d (sum over out-edges).  K2 writes one fp64 energy per tile.
 // ---------------------------------------------------------------------------
-constexpr int kStages = 3;
+#ifndef VBA_K1_STAGES
+#define VBA_K1_STAGES 3
+#endif
+#ifndef VBA_K1_FENCE
+#define VBA_K1_FENCE 0
+#endif
+#ifndef VBA_K1_SKIP
+#define VBA_K1_SKIP 1
+#endif
+#ifndef VBA_K1_MINB
+#define VBA_K1_MINB 3
+#endif
+constexpr int kStages = VBA_K1_STAGES;
 constexpr int kPairs = kTile / 2;   // float4 (= 2 pixels) per row of a stage
 static_assert(kPixBlock / 32 == kPartWarps, "K1 partial records hold one vector per warp");
 constexpr int kSchedCap = 24;       // tile records of one CTA staged in shared memory
@@ -220,6 +232,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Pair index (within a whole-row grid tile of kTile pixels, grid width W) of
+// thread tid at step m: warp w covers block b = 4 m + w of 4 rows x 16 columns,
+// lane l the pixels (row 4 rb + l / 8, columns 16 cb + 2 (l % 8) + {0, 1}).  A
+// quarter-warp reads 8 consecutive float4 of one row (conflict-free).
+__device__ __forceinline__ int blk_pair(int m, int tid, int W) {
+  const int b = 4 * m + (tid >> 5), l = tid & 31;
+  const int cbw = W >> 4;
+  const int rb = b / cbw, cb = b - rb * cbw;
+  return ((4 * rb + (l >> 3)) * W + 16 * cb + 2 * (l & 7)) >> 1;
+}
+
 #define FMA2 __ffma2_rn
 #define MUL2 __fmul2_rn
 #define ADD2 __fadd2_rn
@@ -229,8 +252,17 @@ __device__ __forceinline__ float2 operator-(float2 a) { return make_float2(-a.x,
 // Static LPT schedule: CTA b owns tiles sched_ids[sched_off[b] .. sched_off[b+1])
 // (host-balanced by edge-pixels, vba_host.cu build_plans), so the producer knows
 // every upcoming tile without a global atomic on the critical path.
+#ifdef VBA_K1_TRACE   // tuning builds: cycles spent waiting for stages vs total, per warp
+__device__ unsigned long long g_k1_trace[4];
+extern "C" __attribute__((visibility("default"))) void vba_k1_trace(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_k1_trace, sizeof(g_k1_trace));
+  unsigned long long z[4] = {0, 0, 0, 0};
+  cudaMemcpyToSymbol(g_k1_trace, z, sizeof(z));
+}
+#endif
 template <int MODE, bool LIN>
-__global__ void __launch_bounds__(kPixBlock, 3) k_vision_stream(
+__global__ void __launch_bounds__(kPixBlock, VBA_K1_MINB) k_vision_stream(
     const PixTile* __restrict__ tiles, const int32_t* __restrict__ sched_off, const int32_t* __restrict__ sched_ids,
     const StreamItem* __restrict__ items, const int32_t* __restrict__ item_off, const float* __restrict__ disp,
     const EdgeGeo32* __restrict__ geo, const float* __restrict__ pix, const float* __restrict__ tgt,
@@ -243,6 +275,8 @@ __global__ void __launch_bounds__(kPixBlock, 3) k_vision_stream(
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float fx = (float)in.fx, fy = (float)in.fy;
   const float fx2 = fx * fx, fy2 = fy * fy;
+  const float ifx = (float)(1.0 / in.fx), ify = (float)(1.0 / in.fy);
+  const bool blk_ok = grid_w > 0 && grid_w % 16 == 0 && kTile % (4 * grid_w) == 0;
   const int s0 = sched_off[blockIdx.x], nmine = sched_off[blockIdx.x + 1] - s0;
   const int i0 = item_off[blockIdx.x], nitems = item_off[blockIdx.x + 1] - i0;
   auto tile_id = [&](int o) { return o < kSchedCap ? S.tid[o] : sched_ids[s0 + o]; };
@@ -280,10 +314,21 @@ __global__ void __launch_bounds__(kPixBlock, 3) k_vision_stream(
   auto release = [&](int j) {   // whole warp; call after its last read of item j's stage
     __syncwarp();
     if (lane == 0) {
+#if VBA_K1_FENCE
       __threadfence_block();
-      const unsigned int r = atomicAdd(&S.rel[j % kStages], 1u);
+#endif
+      // the warp's reads of the stage have returned (their values were consumed);
+      // the acq_rel counter orders them before the refill issued by the last warp
+      unsigned int r;
+#if VBA_K1_RELAXED
+      asm volatile("atom.relaxed.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(r) : "r"(smem_u32(&S.rel[j % kStages])) : "memory");
+#else
+      asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(r) : "r"(smem_u32(&S.rel[j % kStages])) : "memory");
+#endif
       if (r % (kPixBlock / 32) == (kPixBlock / 32) - 1 && j + kStages < nitems) {
+#if VBA_K1_FENCE
         __threadfence_block();
+#endif
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // others' generic reads before the refill
         issue(j + kStages);
       }
@@ -298,15 +343,23 @@ __global__ void __launch_bounds__(kPixBlock, 3) k_vision_stream(
   __syncthreads();
 
   int item = 0;
+#ifdef VBA_K1_TRACE
+  const long long tk0 = clock64();
+#endif
 #pragma unroll 1
   for (int ord = 0; ord < nmine; ++ord) {
     const PixTile T = tile_at(ord);
     const int64_t kbase = doff[T.src];
+    // pixel-pair -> thread map: 4x16-pixel blocks per warp on whole-row grid tiles
+    // (spatially coherent, so warp-uniform zero-weight skips are frequent), else linear
+    const bool blk = MODE == VBA_PIX_GRID && T.cnt == kTile && blk_ok;
     float2 RX[kTP], RY[kTP], DD[kTP], HD[kTP], GD[kTP];
+    int QP[kTP];   // pair index within the tile (= float4 index into the stage rows)
     uint32_t act = 0;
 #pragma unroll
     for (int m = 0; m < kTP; ++m) {
-      const int p = m * kPixBlock + tid;
+      const int p = blk ? blk_pair(m, tid, grid_w) : m * kPixBlock + tid;
+      QP[m] = p;
       const int n = T.n0 + 2 * p;
       RX[m] = RY[m] = make_float2(0.f, 0.f);
       DD[m] = make_float2(1.f, 1.f);
@@ -326,18 +379,43 @@ __global__ void __launch_bounds__(kPixBlock, 3) k_vision_stream(
 #pragma unroll
         for (int m = 0; m < kTP; ++m)
           if (act & (1u << m))
-            load_rays<VBA_PIX_KF>(pix, eoff[e], T.n0 + 2 * (m * kPixBlock + tid), grid_w, gp, in, RX[m].x,
+            load_rays<VBA_PIX_KF>(pix, eoff[e], T.n0 + 2 * QP[m], grid_w, gp, in, RX[m].x,
                                   RY[m].x, RX[m].y, RY[m].y);
       }
+#ifdef VBA_K1_TRACE
+      const long long tw0 = clock64();
+#endif
       mbar_wait(&S.full[s], (item / kStages) & 1);
+#ifdef VBA_K1_TRACE
+      if (LIN && lane == 0) atomicAdd(&g_k1_trace[0], (unsigned long long)(clock64() - tw0));
+#endif
       const EdgeGeo32 g = S.geo[s];
       float2 acc[LIN ? 27 : 1];
 #pragma unroll
       for (int k = 0; k < (LIN ? 27 : 1); ++k) acc[k] = make_float2(0.f, 0.f);
+#if VBA_K1_SKIP == 2
+      bool anyw = false;   // whole warp-item skip: all 64 x kTP pixels of this warp have w = 0
 #pragma unroll
       for (int m = 0; m < kTP; ++m) {
-        const float4 fl = S.flow[s][m * kPixBlock + tid];
-        const float4 wl = S.wts[s][m * kPixBlock + tid];
+        const float4 wl = S.wts[s][QP[m]];
+        anyw |= ((act >> m) & 1u) && (wl.x != 0.f || wl.y != 0.f || wl.z != 0.f || wl.w != 0.f);
+      }
+      if (__any_sync(0xffffffffu, anyw))
+#endif
+#pragma unroll
+      for (int m = 0; m < kTP; ++m) {
+        const float4 wl = S.wts[s][QP[m]];
+        // zero-weight skip: a pixel with w = 0 adds exact zeros to every sum
+        // (residuals.py:254-263), so a warp whose 64 pixels all have w = 0 skips
+        // the arithmetic (bitwise identical result; the rows are still streamed)
+#if VBA_K1_SKIP == 1
+        const bool nz = ((act >> m) & 1u) && (wl.x != 0.f || wl.y != 0.f || wl.z != 0.f || wl.w != 0.f);
+        if (!__any_sync(0xffffffffu, nz)) continue;
+#endif
+#ifdef VBA_K1_NOMATH   // tuning builds only: pipeline + reductions without the per-pixel arithmetic
+        if (LIN) continue;
+#endif
+        const float4 fl = S.flow[s][QP[m]];
         const float2 rx = RX[m], ry = RY[m], d = DD[m];
         // project(): D = (M - I) ray + d t,  x - rx = (Dx - rx Dz) / (1 + Dz)
         const float2 Dx = FMA2(d, S2(g.t[0]), FMA2(S2(g.M[0]), rx, FMA2(S2(g.M[1]), ry, S2(g.M[2]))));
@@ -351,14 +429,17 @@ __global__ void __launch_bounds__(kPixBlock, 3) k_vision_stream(
         izh = FMA2(izh, FMA2(-Xz, izh, S2(1.0f)), izh);   // rcp_nr (invalid lanes stay 0)
         const float2 ddx = MUL2(FMA2(-rx, Dz, Dx), izh);
         const float2 ddy = MUL2(FMA2(-ry, Dz, Dy), izh);
-        const float2 r0 = FMA2(S2(-fx), ddx, make_float2(fl.x, fl.z));   // flow - fx (x - rx)
-        const float2 r1 = FMA2(S2(-fy), ddy, make_float2(fl.y, fl.w));
         const float2 w0 = make_float2(va ? wl.x : 0.f, vb ? wl.z : 0.f);
         const float2 w1 = make_float2(va ? wl.y : 0.f, vb ? wl.w : 0.f);
         if (!LIN) {
+          const float2 r0 = FMA2(S2(-fx), ddx, make_float2(fl.x, fl.z));   // flow - fx (x - rx)
+          const float2 r1 = FMA2(S2(-fy), ddy, make_float2(fl.y, fl.w));
           acc[0] = FMA2(MUL2(w0, r0), r0, FMA2(MUL2(w1, r1), r1, acc[0]));
           continue;
         }
+        // residual over the focal length: r / fx = flow / fx - (x - rx)
+        const float2 rf0 = FMA2(make_float2(fl.x, fl.z), S2(ifx), -ddx);
+        const float2 rf1 = FMA2(make_float2(fl.y, fl.w), S2(ify), -ddy);
         const float2 x = ADD2(rx, ddx), y = ADD2(ry, ddy);
         const float2 iz = MUL2(d, izh);
         const float2 xy = MUL2(x, y);
@@ -369,7 +450,7 @@ __global__ void __launch_bounds__(kPixBlock, 3) k_vision_stream(
         const float2 jd0 = MUL2(FMA2(x, S2(g.t[2]), S2(-g.t[0])), izh);   // J_d = (fx jd0', fy jd1')
         const float2 jd1 = MUL2(FMA2(y, S2(g.t[2]), S2(-g.t[1])), izh);
         const float2 W0 = MUL2(w0, S2(fx2)), W1 = MUL2(w1, S2(fy2));   // as the Gram: (w fx^2) jd
-        const float2 R0 = MUL2(MUL2(w0, S2(fx)), r0), R1 = MUL2(MUL2(w1, S2(fy)), r1);
+        const float2 R0 = MUL2(W0, rf0), R1 = MUL2(W1, rf1);   // = (w fx) r
         const float2 p0 = MUL2(W0, xy), p1 = MUL2(W0, a1), p2 = MUL2(W0, y), p3 = -MUL2(W0, iz),
                      p5 = MUL2(W0, a5);
         const float2 q0 = MUL2(W1, b0), q1 = -MUL2(W1, xy), q2 = -MUL2(W1, x), q4 = -MUL2(W1, iz),
@@ -443,7 +524,7 @@ __global__ void __launch_bounds__(kPixBlock, 3) k_vision_stream(
 #pragma unroll
       for (int m = 0; m < kTP; ++m) {
         if (!((act >> m) & 1u)) continue;
-        const int64_t n = kbase + T.n0 + 2 * (m * kPixBlock + tid);
+        const int64_t n = kbase + T.n0 + 2 * QP[m];
         if (T.pad) {   // one of two edge halves of the tile: add onto zero (order-free with 2 addends)
           atomicAdd(reinterpret_cast<float2*>(Hdd + n), HD[m]);
           atomicAdd(reinterpret_cast<float2*>(gdo + n), GD[m]);
@@ -459,6 +540,12 @@ __global__ void __launch_bounds__(kPixBlock, 3) k_vision_stream(
       if (lane == 0) tile_energy[(int64_t)tile_id(ord) * (kPixBlock / 32) + warp] = etile;
     }
   }
+#ifdef VBA_K1_TRACE
+  if (LIN && lane == 0) {
+    atomicAdd(&g_k1_trace[1], (unsigned long long)(clock64() - tk0));
+    atomicAdd(&g_k1_trace[2], (unsigned long long)item);
+  }
+#endif
 }
 
 // CTAs of the streamed kernels (SMs x resident CTAs of the K1 instance; the

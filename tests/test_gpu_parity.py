@@ -133,3 +133,28 @@ def test_solve_vi_ba(name, cuda_ok):
     assert np.abs(s["p"] - out["final_p"]).max() < 1e-5 * scale
     assert np.abs(s["v"] - out["final_v"]).max() < 1e-4 * scale
     assert np.abs(s["disp"] - out["final_disp"]).max() < 1e-4 * scale * np.abs(out["final_disp"]).max()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,cond", [(100, 1e3), (300, 1e6), (1000, 1e5), (1905, 1e7)])
+def test_spd_solve_tensor_core_matches_fp64(cuda_ok, n, cond):
+    """tcgen05 3xTF32 Cholesky + fp64 refinement == fp64 solve (solver.py:287) to ~1e-10."""
+    import torch
+    from paper_2512_02293_b200 import _lib
+    g = torch.Generator().manual_seed(n)
+    Q, _ = torch.linalg.qr(torch.randn(n, n, generator=g, dtype=torch.float64))
+    ev = torch.logspace(0, float(np.log10(cond)), n, dtype=torch.float64)
+    d = torch.exp(torch.randn(n, generator=g, dtype=torch.float64) * 3.0)   # badly scaled rows, like H_red
+    H = (d[:, None] * (Q * ev) @ Q.T * d[None, :])
+    H = 0.5 * (H + H.T)
+    b = torch.randn(n, generator=g, dtype=torch.float64)
+    ref = torch.linalg.solve(H, b)
+    Hd, bd = H.cuda(), b.cuda()
+    x1, tc1 = _lib.spd_solve(Hd, bd, mode=1)
+    x0, tc0 = _lib.spd_solve(Hd, bd, mode=0)
+    assert not tc1
+    assert tc0 or cond > 1e5          # ill-conditioned: tensor-core refinement may hand over to fp64
+    e1 = ((x1.cpu() - ref).abs().max() / ref.abs().max()).item()
+    e0 = ((x0.cpu() - ref).abs().max() / ref.abs().max()).item()
+    assert e1 < 1e-9 * max(1.0, cond / 1e5), e1
+    assert e0 < 1e-9 * max(1.0, cond / 1e5), e0

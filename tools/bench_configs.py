@@ -50,6 +50,10 @@ for cfg in [int(c) for c in a.configs.split(",")]:
           f"| {edge_px * it / ms * 1e3:.3e} edge-px/s, {it / ms * 1e3:.1f} it/s")
     print("   stages(ms): " + " ".join(f"{k}={v:.3f}" for k, v in st.items()))
     print("   costs: " + " ".join(f"{c:.4e}" for c in rep["cost_trajectory"]))
+    import ctypes
+    stt = (ctypes.c_int64 * 4)()
+    dp.lib.vba_stats(dp.ctx, stt)
+    print(f"   tensor-core solve: {bool(stt[0])}, fp64 fallbacks {stt[1]}")
     dp.close()
     del dp
     torch.cuda.empty_cache()
