@@ -166,7 +166,8 @@ VBA_API int64_t vba_launch_count(void* ctx);
  * kernel alone  [6] number of samples in [5]   (out must hold 7 doubles) */
 VBA_API int vba_stage_times(void* ctx, double* out5);
 /* solver statistics: [0] tensor-core reduced solve enabled, [1] steps that fell
- * back to the fp64 factorisation, [2] flag generation, [3] refinement passes */
+ * back to the fp64 factorisation, [2] tensor-core solves, [3] refinement passes
+ * summed over them */
 VBA_API int vba_stats(void* ctx, int64_t* out4);
 
 /* Standalone SPD solve H x = b of a dense fp64 n x n system (column-major,

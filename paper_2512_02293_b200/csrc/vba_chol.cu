@@ -37,7 +37,7 @@ constexpr int CHOL_THREADS = 256;
 constexpr int SB = 36;           // 32x32 block stride in POTRF (doubles, = 4 mod 16)
 constexpr size_t CHOL_SMEM = (size_t)2 * 2 * KC * SP * sizeof(double);   // 2 stages x (A, B)
 
-enum TaskType { T_POTRF = 0, T_TRSM = 1, T_GEMM = 2, T_BUPD = 3, T_BSOL = 4 };
+enum TaskType { T_POTRF = 0, T_TRSM = 1, T_GEMM = 2, T_BUPD = 3, T_BSOL = 4, T_DIAG = 5 };
 
 struct CholTask {
   int32_t type, i, j, k;
@@ -594,6 +594,33 @@ int chol_plan_tasks(int nt, void* outv, int cap) {
   return n;
 }
 
+// Task list of the tensor-core DAG: as chol_plan_tasks, but the critical chain of
+// each step -- POTRF(k), TRSM(k+1,k), GEMM(k+1,k+1,k) -- is one DIAG(k) task run
+// back to back by one CTA (no flag hand-offs or task grabs between them), and
+// there is no substitution (the triangular solves are separate kernels).
+int chol_plan_tasks_tc(int nt, void* outv, int cap) {
+  CholTask* out = reinterpret_cast<CholTask*>(outv);
+  int n = 0;
+  auto push = [&](int type, int i, int j, int k, int expect, int k2 = -1) {
+    if (n < cap) out[n] = CholTask{type, i, j, k, expect, k2, {0, 0}};
+    ++n;
+  };
+  if (nt <= 0) return 0;
+  push(T_DIAG, 0, 0, 0, 0);
+  for (int i = 2; i < nt; ++i) push(T_TRSM, i, 0, 0, 0);
+  for (int s = 0; s + 1 < nt; ++s) {
+    for (int i = s + 2; i < nt; ++i) push(T_GEMM, i, s + 1, s, s);      // next panel column (off-diagonal)
+    push(T_DIAG, s + 1, s + 1, s + 1, s + 1);
+    for (int i = s + 3; i < nt; ++i) push(T_TRSM, i, s + 1, s + 1, s + 1);
+    for (int j = s + 2; j < nt; ++j)
+      for (int i = j; i < nt; ++i) {
+        if (s & 1) push(T_GEMM, i, j, s - 1, s - 1, s);
+        else if (s == j - 2) push(T_GEMM, i, j, s, s);
+      }
+  }
+  return n;
+}
+
 size_t chol_smem_bytes() { return CHOL_SMEM; }
 
 int chol_dag_launch(double* A, int64_t ld, int nt, double* rhs, double* x, double* Linv, double* part, int* flags,
@@ -927,34 +954,44 @@ __device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
   tc_fence_before();
 }
 
-// Cholesky + inverse of a 32x32 SPD block (fp64, all 256 threads) by Gaussian
-// elimination of the augmented [A | I] without pivoting (stable for SPD):
-// A = Lt U, U = diag(p) Lt^T, so L = Lt diag(p)^1/2 and L^-1 = diag(p)^-1/2 Lt^-1,
-// where the I half becomes Lt^-1.  Thread t owns row i = t / 8 and 8 columns of
-// one half (group g = t % 8: g < 4 -> A columns 8g.., g >= 4 -> I columns
-// 8(g-4)..) in registers; one barrier per step: the owners of column j+1 (A
-// half, lower part) and of row j+1 (I half) publish them into double buffers.
-// W (column-major, stride sw) gets L, Ib (stride SB) gets L^-1, upper parts 0.
-__device__ __forceinline__ void cta_ge32(double* W, int sw, double* Ib, double* buf, int* bad) {
-  const int t = threadIdx.x, i = t >> 3, g = t & 7;
-  const bool ahalf = g < 4;
+// ---------------------------------------------------------------------------
+// POTRF(k) of the tensor-core DAG, fp32 (the factor is fp32-accurate anyway;
+// iterative refinement restores fp64).  Shared-memory layout (floats):
+//   Ws  128 x 128 column-major, stride SWF: the tile, then L (lower)
+//   Xs  4 x 4 blocks of 32x32 (row-major, stride XBS): X = L^-1 blocks (i >= j)
+//   Ts  32x32 temporary (stride XBS)
+// ---------------------------------------------------------------------------
+constexpr int SWF = CT + 4;      // 132: float4-aligned columns
+constexpr int XBS = 36;          // 32x32 block row stride (float4-aligned)
+constexpr int XB = 32 * XBS;     // floats per 32x32 block
+
+// Cholesky + inverse of a 32x32 SPD block by Gaussian elimination of the
+// augmented [A | I] without pivoting (stable for SPD): A = Lt U, U = diag(p) Lt^T,
+// so L = Lt diag(p)^1/2 and L^-1 = diag(p)^-1/2 Lt^-1 (the I half becomes Lt^-1).
+// Thread t owns row i = t / 8 and 8 columns of one half (t % 8 < 4: A columns,
+// else I columns) in registers; one barrier per step: the owners of column j+1
+// (A half) and row j+1 (I half) publish them, with the next pivot's rsqrt, into
+// double buffers.  A (column-major, stride sw) gets L; X (row-major, XBS) L^-1.
+__device__ __forceinline__ void cta_ge32(float* A, int sw, float* X, float* buf, int* bad) {
+  // warp-uniform halves: threads 0..127 own A columns, 128..255 I columns
+  const int t = threadIdx.x, i = (t & 127) >> 2, g = (t & 3) + 4 * (t >> 7);
+  const bool ahalf = t < 128;
   const int cb = 8 * (g & 3);
-  double* pv = buf + 128;     // [2][2]: pivot, rsqrt(pivot) of the step (double-buffered)
-  double* rsv = buf + 132;    // [32] rsqrt of every pivot (for the final row scaling)
-  double e[8];
+  float* pv = buf + 128;     // [2][2]: pivot, rsqrt(pivot)
+  float* rsv = buf + 132;    // [32]: rsqrt of every pivot
+  float e[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const int c = cb + q;
-    e[q] = ahalf ? (c <= i ? W[c * sw + i] : 0.0) : (c == i ? 1.0 : 0.0);
+    e[q] = ahalf ? (c <= i ? A[c * sw + i] : 0.f) : (c == i ? 1.f : 0.f);
   }
-  // publish column 0 (A half), row 0 (I half) and the first pivot
   if (ahalf && g == 0) {
     buf[i] = e[0];
     if (i == 0) {
-      double p = e[0];
-      if (!(p > 0.0)) { *bad = 1; p = 1.0; }
+      float p = e[0];
+      if (!(p > 0.f)) { *bad = 1; p = 1.f; }
       pv[0] = p;
-      pv[1] = rsqrt(p);
+      pv[1] = rsqrtf(p);
     }
   }
   if (!ahalf && i == 0) {
@@ -965,39 +1002,46 @@ __device__ __forceinline__ void cta_ge32(double* W, int sw, double* Ib, double* 
 #pragma unroll 1
   for (int j = 0; j < 32; ++j) {
     const int sb = j & 1, nb = sb ^ 1;
-    const double* col = buf + sb * 32;        // column j of the A half (rows >= j)
-    const double* row = buf + 64 + sb * 32;   // row j of the I half
-    const double p = pv[2 * sb], rs = pv[2 * sb + 1];
-    const double rp = rs * rs;
-    const double ci = col[i];
-    const double f = (i > j) ? ci * rp : 0.0;   // multiplier Lt[i][j]
+    const float* col = buf + sb * 32;
+    const float* row = buf + 64 + sb * 32;
+    const float2 prs = *reinterpret_cast<const float2*>(pv + 2 * sb);   // pivot, rsqrt(pivot)
+    const float p = prs.x, rs = prs.y;
+    const float ci = col[i];
+    const float f = (i > j) ? ci * (rs * rs) : 0.f;   // multiplier Lt[i][j]
     if (ahalf) {
+      // critical path first: the owners of column j+1 publish its updated entries
+      // (and the diagonal owner the next pivot) before the rest of the update
       const int qn = (j + 1) & 7;
-      const bool pub = j + 1 < 32 && ((j + 1) >> 3) == (g & 3) && i >= j + 1;
-      double vn = 0.0;
+      if (j + 1 < 32 && ((j + 1) >> 3) == (g & 3) && i >= j + 1) {
+        float en = e[0];
+#pragma unroll
+        for (int q = 1; q < 8; ++q) en = (q == qn) ? e[q] : en;
+        const float vn = fmaf(-f, col[j + 1], en);
+        buf[nb * 32 + i] = vn;
+        if (i == j + 1) {
+          float pn = vn;
+          if (!(pn > 0.f)) { *bad = 1; pn = 1.f; }
+          *reinterpret_cast<float2*>(pv + 2 * nb) = make_float2(pn, rsqrtf(pn));
+        }
+      }
+      const float lij = (i > j) ? ci * rs : (i == j ? p * rs : 0.f);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int c = cb + q;
-        if (c > j && c <= i) e[q] = fma(-f, col[c], e[q]);
-        if (c == j) e[q] = (i > j) ? ci * rs : (i == j ? p * rs : 0.0);   // final L[i][j]
-        if (q == qn) vn = e[q];
-      }
-      if (pub) {
-        buf[nb * 32 + i] = vn;          // column j+1 for the next step
-        if (i == j + 1) {               // owner of the next pivot
-          double pn = vn;
-          if (!(pn > 0.0)) { *bad = 1; pn = 1.0; }
-          pv[2 * nb] = pn;
-          pv[2 * nb + 1] = rsqrt(pn);
-        }
+        if (c > j && c <= i) e[q] = fmaf(-f, col[c], e[q]);
+        if (c == j) e[q] = lij;   // final L[i][j]
       }
     } else {
+      if (i == j + 1) {   // row j+1 of the I half: final update first, then publish
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (cb + q <= j) e[q] = fma(-f, row[cb + q], e[q]);
-      if (i == j + 1) {
+        for (int q = 0; q < 8; ++q)
+          if (cb + q <= j) e[q] = fmaf(-f, row[cb + q], e[q]);
+        *reinterpret_cast<float4*>(buf + 64 + nb * 32 + cb) = make_float4(e[0], e[1], e[2], e[3]);
+        *reinterpret_cast<float4*>(buf + 64 + nb * 32 + cb + 4) = make_float4(e[4], e[5], e[6], e[7]);
+      } else {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) buf[64 + nb * 32 + cb + q] = e[q];
+        for (int q = 0; q < 8; ++q)
+          if (cb + q <= j) e[q] = fmaf(-f, row[cb + q], e[q]);
       }
     }
     if (t == 0) rsv[j] = rs;
@@ -1005,103 +1049,242 @@ __device__ __forceinline__ void cta_ge32(double* W, int sw, double* Ib, double* 
   }
   if (ahalf) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) W[(cb + q) * sw + i] = (cb + q <= i) ? e[q] : 0.0;
+    for (int q = 0; q < 8; ++q) A[(cb + q) * sw + i] = (cb + q <= i) ? e[q] : 0.f;
   } else {
-    const double s = rsv[i];
+    const float s = rsv[i];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) Ib[(cb + q) * SB + i] = (cb + q <= i) ? e[q] * s : 0.0;
+    for (int q = 0; q < 8; ++q) X[i * XBS + cb + q] = (cb + q <= i) ? e[q] * s : 0.f;
   }
   __syncthreads();
 }
 
-// POTRF(k): fp64 blocked factorisation of the diagonal tile in shared memory
-// (4 panels of 32: warp-level factor + inverse of the panel's diagonal block,
-// DMMA TRSM and SYRK of the rest), then Linv = L_kk^-1 by block forward
-// substitution, written to W_kk (fp32 row-major, for the triangular solves) and
-// to its hi/lo images (TRSM operand).
-__device__ void tc_task_potrf(const TcArgs& a, int k, double* smem) {
-  double* Wt = smem;
-  double* I = smem + CT * SW;
-  double* Mc = I + 4 * 32 * SB;
+// C (32x32, row-major XBS) = alpha * A B (+ C if acc), A(r, m) = A[r * ars + m * ams],
+// B(m, c) = B[m * bms + c * bcs]; 256 threads, 2x2 outputs each.  Caller syncs.
+__device__ __forceinline__ void blk32_gemm(float* C, const float* A, int ars, int ams, const float* B, int bms,
+                                           int bcs, float alpha, bool acc) {
+  const int t = threadIdx.x, r = 2 * (t >> 4), c = 2 * (t & 15);
+  float s00 = 0.f, s01 = 0.f, s10 = 0.f, s11 = 0.f;
+#pragma unroll 8
+  for (int m = 0; m < 32; ++m) {
+    const float a0 = A[r * ars + m * ams], a1 = A[(r + 1) * ars + m * ams];
+    const float b0 = B[m * bms + c * bcs], b1 = B[m * bms + (c + 1) * bcs];
+    s00 = fmaf(a0, b0, s00);
+    s01 = fmaf(a0, b1, s01);
+    s10 = fmaf(a1, b0, s10);
+    s11 = fmaf(a1, b1, s11);
+  }
+  float* o = C + r * XBS + c;
+  if (acc) {
+    o[0] += alpha * s00; o[1] += alpha * s01; o[XBS] += alpha * s10; o[XBS + 1] += alpha * s11;
+  } else {
+    o[0] = alpha * s00; o[1] = alpha * s01; o[XBS] = alpha * s10; o[XBS + 1] = alpha * s11;
+  }
+}
+
+// 8x8 Cholesky + inverse of the diagonal block at (c0, c0) by ONE thread in
+// registers (no barriers): L overwrites the block of Ws (upper part zeroed), the
+// inverse goes to the same block of Xf.  Both column-major, stride SWF.
+__device__ __forceinline__ void diag8(float* Ws, float* Xf, int c0, int* bad) {
+  float l[8][8], x[8][8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+#pragma unroll
+    for (int r = 0; r < 8; ++r) l[r][c] = (r >= c) ? Ws[(c0 + c) * SWF + c0 + r] : 0.f;
+  float rinv[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    float d = l[j][j];
+    if (!(d > 0.f)) { *bad = 1; d = 1.f; }
+    const float rs = rsqrtf(d);
+    rinv[j] = rs;                                 // 1 / L[j][j]
+    l[j][j] = d * rs;
+#pragma unroll
+    for (int r = j + 1; r < 8; ++r) l[r][j] *= rs;
+#pragma unroll
+    for (int c = j + 1; c < 8; ++c)
+#pragma unroll
+      for (int r = c; r < 8; ++r) l[r][c] = fmaf(-l[r][j], l[c][j], l[r][c]);
+  }
+  // X = L^-1, column by column of X (forward substitution of L x = e_c)
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      if (r < c) { x[r][c] = 0.f; continue; }
+      float s = (r == c) ? 1.f : 0.f;
+#pragma unroll
+      for (int m = c; m < r; ++m) s = fmaf(-l[r][m], x[m][c], s);
+      x[r][c] = s * rinv[r];
+    }
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      Ws[(c0 + c) * SWF + c0 + r] = l[r][c];
+      Xf[(c0 + c) * SWF + c0 + r] = x[r][c];
+    }
+}
+
+// POTRF(k) of the tensor-core DAG, fp32 (the factor is fp32-accurate anyway;
+// iterative refinement restores fp64): right-looking over 16 panels of 8
+// columns.  Per panel, three barrier-separated phases:
+//   1. one thread factors and inverts the 8x8 diagonal block in registers;
+//   2. panel TRSM (a row per thread) and, on other threads, Y_s <- X_ss Y_s for
+//      the panel's block row of Y (a column per thread);
+//   3. rank-8 trailing update of A and the matching update of Y's rows below,
+//      Y_t -= L_ts Y_s (4x4 register blocks),
+// where Y starts as I and ends as L^-1 (forward substitution L Y = I fused into
+// the factorisation).  Linv goes to W_kk (fp32 row-major, zeros above the
+// diagonal, for the triangular solves) and to its hi/lo images (TRSM operand).
+__device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d) {
+  float* Ws = reinterpret_cast<float*>(smem_d);   // tile, then L (column-major, SWF)
+  float* Xf = Ws + CT * SWF;                      // Y -> Linv (column-major, SWF)
   __shared__ int bad;
-  __shared__ double gebuf[5 * 32 + 8];
   const int tid = threadIdx.x;
   float* Wk = a.W + tlin(k, k) * TILE_F;
   if (tid == 0) bad = 0;
   unsigned long long* ph = a.trace ? a.trace + 4 * (size_t)a.ntasks + 16 * (size_t)k : nullptr;   // phase stamps
-  if (ph && tid == 0) ph[0] = gtimer();
+  if (ph && tid == 0) { ph[0] = gtimer(); ph[11] = clock64(); }
   {   // The diagonal tile is symmetric (up to the rounding of its updates), so its
-      // row-major fp32 image is read as column-major without a transpose: element
-      // (r, c) of the lower triangle comes from the stored (c, r).  All loads first.
+      // row-major image is read as column-major without a transpose.  Loads first.
     float4 q[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) q[u] = __ldcg(reinterpret_cast<const float4*>(Wk) + tid + u * CHOL_THREADS);
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
-      const int t = 4 * (tid + u * CHOL_THREADS), c = t / CT, r = t % CT;
-      double* d = Wt + c * SW + r;
-      d[0] = q[u].x;
-      d[1] = q[u].y;
-      d[2] = q[u].z;
-      d[3] = q[u].w;
+      const int t4 = 4 * (tid + u * CHOL_THREADS), c = t4 / CT, r = t4 % CT;
+      *reinterpret_cast<float4*>(Ws + c * SWF + r) = q[u];
+      const float4 id = make_float4(r == c ? 1.f : 0.f, r + 1 == c ? 1.f : 0.f, r + 2 == c ? 1.f : 0.f,
+                                    r + 3 == c ? 1.f : 0.f);
+      *reinterpret_cast<float4*>(Xf + c * SWF + r) = id;
     }
   }
   __syncthreads();
-  if (ph && tid == 0) ph[1] = gtimer();
-  for (int p = 0; p < 4; ++p) {
-    const int c0 = 32 * p, r0 = c0 + 32, nr = CT - r0;
-    cta_ge32(Wt + c0 * SW + c0, SW, I + p * 32 * SB, gebuf, &bad);
-    if (ph && tid == 0) ph[2 + 2 * p] = gtimer();
-    if (nr > 0) {
-      sgemm8<true>(Wt + c0 * SW + r0, SW, I + p * 32 * SB, SB, Mc, TB, nr, 32, 32, 1.0, false, false);
-      __syncthreads();
-      for (int t = tid; t < nr * 32; t += CHOL_THREADS) {
-        const int r = t % nr, c = t / nr;
-        Wt[(c0 + c) * SW + r0 + r] = Mc[c * TB + r];
-      }
-      __syncthreads();
-      sgemm8<true>(Wt + c0 * SW + r0, SW, Wt + c0 * SW + r0, SW, Wt + r0 * SW + r0, SW, nr, nr, 32, -1.0, true, true);
-      __syncthreads();
-    }
-    if (ph && tid == 0) ph[3 + 2 * p] = gtimer();
-  }
-  if (tid == 0 && bad) atomicExch(a.status, 1);
-  float* ihi = a.img + tlin(k, k) * 2 * TILE_F;
-  float* ilo = ihi + TILE_F;
-  for (int p = 0; p < 4; ++p) {
-    for (int i = p + 1; i < 4; ++i) {
-      double* T = Mc + i * 32 * SB;
-      for (int m = p; m < i; ++m) {
-        const double* Mmp = (m == p) ? I + p * 32 * SB : Mc + m * 32 * SB;
-        sgemm8<false>(Wt + (32 * m) * SW + 32 * i, SW, Mmp, SB, T, SB, 32, 32, 32, 1.0, m != p, false);
-        __syncthreads();
-      }
-      double* tmp = Mc + p * 32 * SB;
-      sgemm8<false>(I + i * 32 * SB, SB, T, SB, tmp, SB, 32, 32, 32, -1.0, false, false);
-      __syncthreads();
-      {
-        const int r = tid & 31, cq = tid >> 5;
+  if (ph && tid == 0) ph[1] = ph[2] = gtimer();
+  for (int sp = 0; sp < CT / 8; ++sp) {
+    const int c0 = 8 * sp, r0 = c0 + 8, nr = CT - r0;
+#ifdef VBA_POTRF_PROF
+    long long q0 = clock64();
+#endif
+    if (tid == 0) diag8(Ws, Xf, c0, &bad);   // L_ss and X_ss (= final Y_ss)
+    __syncthreads();
+#ifdef VBA_POTRF_PROF
+    long long q1 = clock64();
+#endif
+    if (tid < nr) {   // panel TRSM: L[r][c0+c] = sum_{m<=c} A[r][c0+m] X[c][m]
+      const int r = r0 + tid;
+      float av[8];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) T[(cq + 8 * q) * SB + r] = tmp[(cq + 8 * q) * SB + r];
+      for (int m = 0; m < 8; ++m) av[m] = Ws[(c0 + m) * SWF + r];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        float sum = 0.f;
+#pragma unroll
+        for (int m = 0; m <= c; ++m) sum = fmaf(av[m], Xf[(c0 + m) * SWF + c0 + c], sum);
+        Ws[(c0 + c) * SWF + r] = sum;
       }
-      __syncthreads();
-    }
-    // column block p of Linv: rows r (warp-contiguous columns c -> coalesced row-major stores)
-    for (int t = tid; t < CT * 32; t += CHOL_THREADS) {
-      const int r = t >> 5, c = t & 31, ib = r >> 5;
-      double v = 0.0;
-      if (ib == p) v = I[p * 32 * SB + c * SB + (r & 31)];
-      else if (ib > p) v = Mc[ib * 32 * SB + c * SB + (r & 31)];
-      const float f = (float)v, h = tf32_rna(f);
-      const int col = 32 * p + c;
-      __stcg(Wk + r * CT + col, f);
-      const int off = img_off(r, col);
-      __stcg(ihi + off, h);
-      __stcg(ilo + off, tf32_rna(f - h));
+    } else if (tid >= 128 && tid - 128 < c0) {   // Y_s[:, c] <- X_ss Y_s[:, c] for columns c < c0
+      const int c = tid - 128;
+      float yv[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) yv[m] = Xf[c * SWF + c0 + m];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        float sum = 0.f;
+#pragma unroll
+        for (int m = 0; m <= r; ++m) sum = fmaf(Xf[(c0 + m) * SWF + c0 + r], yv[m], sum);
+        Xf[c * SWF + c0 + r] = sum;
+      }
     }
     __syncthreads();
+#ifdef VBA_POTRF_PROF
+    long long q2 = clock64();
+#endif
+    if (nr == 0) break;
+    // rank-8 updates (4x4 blocks): A[r][c] -= sum_m L[r][c0+m] L[c][c0+m] (r0 <= c <= r), then
+    // Y[r][c] -= sum_m L[r][c0+m] Y[c0+m][c] (r >= r0, c < r0)
+    const int nb4 = nr / 4, nsy = nb4 * (nb4 + 1) / 2, nyc = r0 / 4, nblk = nsy + nb4 * nyc;
+    for (int b = tid; b < nblk; b += CHOL_THREADS) {
+      float acc[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = 0.f;
+      if (b < nsy) {
+        int rb = (int)((sqrtf(8.f * b + 1.f) - 1.f) * 0.5f);
+        while ((rb + 1) * (rb + 2) / 2 <= b) ++rb;
+        while (rb * (rb + 1) / 2 > b) --rb;
+        const int cbk = b - rb * (rb + 1) / 2;
+        const int r = r0 + 4 * rb, c = r0 + 4 * cbk;
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const float4 lr = *reinterpret_cast<const float4*>(Ws + (c0 + m) * SWF + r);
+          const float4 lc = *reinterpret_cast<const float4*>(Ws + (c0 + m) * SWF + c);
+          const float ra[4] = {lr.x, lr.y, lr.z, lr.w}, ca[4] = {lc.x, lc.y, lc.z, lc.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(ra[u], ca[v], acc[u][v]);
+        }
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          float4* d = reinterpret_cast<float4*>(Ws + (c + v) * SWF + r);
+          float4 o = *d;
+          o.x -= acc[0][v]; o.y -= acc[1][v]; o.z -= acc[2][v]; o.w -= acc[3][v];
+          *d = o;
+        }
+      } else {
+        const int bb = b - nsy, rb = bb / nyc, cbk = bb % nyc;
+        const int r = r0 + 4 * rb, c = 4 * cbk;
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const float4 lr = *reinterpret_cast<const float4*>(Ws + (c0 + m) * SWF + r);
+          const float ra[4] = {lr.x, lr.y, lr.z, lr.w};
+          float ya[4];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) ya[v] = Xf[(c + v) * SWF + c0 + m];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(ra[u], ya[v], acc[u][v]);
+        }
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          float4* d = reinterpret_cast<float4*>(Xf + (c + v) * SWF + r);
+          float4 o = *d;
+          o.x -= acc[0][v]; o.y -= acc[1][v]; o.z -= acc[2][v]; o.w -= acc[3][v];
+          *d = o;
+        }
+      }
+    }
+    __syncthreads();
+#ifdef VBA_POTRF_PROF
+    if (tid == 0 && ph) { ph[13] += q1 - q0; ph[14] += q2 - q1; ph[15] += clock64() - q2; }
+#endif
   }
-  if (ph && tid == 0) ph[10] = gtimer();
+  if (tid == 0 && bad) atomicExch(a.status, 1);
+  if (ph && tid == 0) ph[3] = ph[4] = ph[5] = ph[6] = ph[7] = ph[8] = ph[9] = gtimer();
+  // outputs: Linv row-major fp32 (+ hi/lo images), zeros above the diagonal
+  float* ihi = a.img + tlin(k, k) * 2 * TILE_F;
+  float* ilo = ihi + TILE_F;
+  for (int t4 = tid; t4 < CT * CT / 4; t4 += CHOL_THREADS) {
+    const int r = t4 / (CT / 4), c = 4 * (t4 % (CT / 4));
+    float v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = (c + u <= r) ? Xf[(c + u) * SWF + r] : 0.f;
+    const float4 x = make_float4(v[0], v[1], v[2], v[3]);
+    __stcg(reinterpret_cast<float4*>(Wk + r * CT + c), x);
+    float4 hh, ll;
+    hh.x = tf32_rna(x.x); ll.x = tf32_rna(x.x - hh.x);
+    hh.y = tf32_rna(x.y); ll.y = tf32_rna(x.y - hh.y);
+    hh.z = tf32_rna(x.z); ll.z = tf32_rna(x.z - hh.z);
+    hh.w = tf32_rna(x.w); ll.w = tf32_rna(x.w - hh.w);
+    const int off = img_off(r, c);
+    __stcg(reinterpret_cast<float4*>(ihi + off), hh);
+    __stcg(reinterpret_cast<float4*>(ilo + off), ll);
+  }
+  if (ph && tid == 0) { ph[10] = gtimer(); ph[12] = clock64(); }
+  __syncthreads();
   proxy_fence_shared();   // generic smem writes before later bulk copies into the same bytes
 }
 
@@ -1161,6 +1344,33 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
         __syncthreads();
         if (tid == 0) st_release(&a.done[T.i * nt + T.k], 1);
         break;
+      case T_DIAG: {   // POTRF(k) -> TRSM(k+1,k) -> GEMM(k+1,k+1,k) in one CTA
+        const int k = T.k;
+        wait_geq(&a.upd[k * nt + k], T.expect);
+        __syncthreads();
+        if (a.trace && tid == 0) a.trace[4 * t + 1] = gtimer();
+        tc_task_potrf(a, k, reinterpret_cast<double*>(sm));
+        proxy_fence_global();
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) st_release(&a.done[k * nt + k], 1);
+        if (k + 1 < nt) {
+          wait_geq(&a.upd[(k + 1) * nt + k], k);
+          __syncthreads();
+          tc_task_trsm(a, R, &accf, nacc, tmem, k + 1, k);
+          proxy_fence_global();
+          __threadfence();
+          __syncthreads();
+          if (tid == 0) st_release(&a.done[(k + 1) * nt + k], 1);
+          wait_geq(&a.upd[(k + 1) * nt + k + 1], k);
+          __syncthreads();
+          tc_task_gemm(a, R, &accf, nacc, tmem, k + 1, k + 1, k, -1);
+          __threadfence();
+          __syncthreads();
+          if (tid == 0) st_release(&a.upd[(k + 1) * nt + k + 1], k + 1);
+        }
+        break;
+      }
       case T_GEMM:
         wait_geq(&a.done[T.i * nt + T.k], 1);
         wait_geq(&a.done[T.j * nt + T.k], 1);
@@ -1239,117 +1449,241 @@ __global__ void __launch_bounds__(256) k_tc_convert(const double* __restrict__ H
     }
 }
 
-// forward solve  L y = v  (v = D r), flags fl[k] = gen when y_k is final.
-// CTA b handles row tiles b, b + G, ...; rows r: two threads per row.
-__global__ void __launch_bounds__(256) k_tc_fwd(const float* __restrict__ W, int nt, const double* __restrict__ r,
-                                                const double* __restrict__ D, double* __restrict__ y,
-                                                int* __restrict__ fl, int gen, const int* __restrict__ stop) {
-  __shared__ double ys[CT], acc[CT];
-  if (*stop) return;   // refinement converged in an earlier pass
-  const int tid = threadIdx.x, row = tid >> 1, h = tid & 1;
-  for (int k = blockIdx.x; k < nt; k += gridDim.x) {
-    double a = (h == 0) ? D[CT * k + row] * r[CT * k + row] : 0.0;
-    for (int jj = 0; jj <= k; ++jj) {
-      const float* T;
-      if (jj < k) {
-        if (tid == 0) {
-          int ns = 32;
-          while (ld_acquire(&fl[jj]) < gen) { __nanosleep(ns); if (ns < 512) ns <<= 1; }
-        }
-        __syncthreads();
-        if (tid < CT) ys[tid] = __ldcg(y + CT * jj + tid);
-        T = W + tlin(k, jj) * TILE_F;
-      } else {   // y_k = Linv_kk acc
-        if (h == 0) acc[row] = a;
-        __syncthreads();
-        if (tid < CT) ys[tid] = acc[tid];
-        a = 0.0;
-        T = W + tlin(k, k) * TILE_F;
-      }
-      __syncthreads();
-      const float4* p = reinterpret_cast<const float4*>(T + (int64_t)row * CT + 64 * h);
-      double s = 0.0;
+// Triangular solves with the fp32 factor.  The solves only need the factor's
+// (fp32) accuracy -- the fp64 residual of the refinement does the rest -- so the
+// vectors are fp32.  One CTA per row tile (grid = nt <= #SMs, all resident).
+// Hand-offs carry their own flag: every element of a published block is a
+// 64-bit word (value, generation), written with one single-copy-atomic store,
+// and the consumer polls the words of the block it needs (no memory fence on the
+// critical chain).  Off the chain, each CTA folds its neighbour tile into the
+// inverse of its diagonal tile (M = Linv_kk L_{k,k-1}, resp. T = L_{k+1,k} Linv_kk),
+// so that one 128x128 matvec per step remains on the chain.
+constexpr size_t TRI_SMEM = 3 * (size_t)TILE_F * sizeof(float) + 64;
+
+__device__ __forceinline__ void put_tagged(unsigned long long* p, float v, int gen) {
+  const unsigned long long w = ((unsigned long long)(unsigned)gen << 32) | __float_as_uint(v);
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+__device__ __forceinline__ float get_tagged(const unsigned long long* p, int gen) {
+  unsigned long long w;
+  do {
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+  } while ((int)(w >> 32) < gen);
+  return __uint_as_float((unsigned)w);
+}
+// block of 128 tagged values -> shared memory (threads < CT poll one word each)
+__device__ __forceinline__ void fetch_block(const unsigned long long* src, float* dst, int gen) {
+  if (threadIdx.x < CT) dst[threadIdx.x] = get_tagged(src + threadIdx.x, gen);
+  __syncthreads();
+}
+// out[r] = sum_c A[r][c] v[c] for a row-major 128x128 smem tile (2 threads per row)
+__device__ __forceinline__ float rowdot(const float* A, const float* v) {
+  const int row = threadIdx.x >> 1, h = threadIdx.x & 1;
+  const float4* p = reinterpret_cast<const float4*>(A + row * CT + 64 * h);
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const float4 a = p[q];
+    const int c = 64 * h + 4 * q;
+    s0 = fmaf(a.x, v[c], s0);
+    s1 = fmaf(a.y, v[c + 1], s1);
+    s2 = fmaf(a.z, v[c + 2], s2);
+    s3 = fmaf(a.w, v[c + 3], s3);
+  }
+  float s = (s0 + s1) + (s2 + s3);
+  return s + __shfl_xor_sync(0xffffffffu, s, 1);
+}
+// out[c] = sum_r A[r][c] v[r] (column sums; threads c and c + 128 take row halves)
+__device__ __forceinline__ float coldot(const float* A, const float* v, float* part, bool glob) {
+  const int col = threadIdx.x & (CT - 1), h = threadIdx.x >> 7;
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll 4
-      for (int q = 0; q < 16; ++q) {
-        const float4 v = __ldcg(p + q);
-        const int c = 64 * h + 4 * q;
-        s = fma((double)v.x, ys[c], s);
-        s = fma((double)v.y, ys[c + 1], s);
-        s = fma((double)v.z, ys[c + 2], s);
-        s = fma((double)v.w, ys[c + 3], s);
-      }
-      s += __shfl_xor_sync(0xffffffffu, s, 1);
-      if (jj < k) a -= (h == 0) ? s : 0.0;
-      else a = s;
-      __syncthreads();
-    }
-    if (h == 0) __stcg(y + CT * k + row, a);
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) st_release(&fl[k], gen);
+  for (int rr = 0; rr < 64; rr += 4) {
+    const int r = 64 * h + rr;
+    const float a0 = glob ? __ldcg(A + r * CT + col) : A[r * CT + col];
+    const float a1 = glob ? __ldcg(A + (r + 1) * CT + col) : A[(r + 1) * CT + col];
+    const float a2 = glob ? __ldcg(A + (r + 2) * CT + col) : A[(r + 2) * CT + col];
+    const float a3 = glob ? __ldcg(A + (r + 3) * CT + col) : A[(r + 3) * CT + col];
+    s0 = fmaf(a0, v[r], s0);
+    s1 = fmaf(a1, v[r + 1], s1);
+    s2 = fmaf(a2, v[r + 2], s2);
+    s3 = fmaf(a3, v[r + 3], s3);
+  }
+  const float s = (s0 + s1) + (s2 + s3);
+  if (h == 1) part[col] = s;
+  __syncthreads();
+  const float t = (h == 0) ? s + part[col] : 0.f;
+  __syncthreads();
+  return t;   // valid on threads < 128
+}
+// C = A B for row-major 128x128 smem tiles; A lower triangular if lowA, B lower if lowB
+__device__ __forceinline__ void smem_gemm128(float* C, const float* A, const float* B, bool lowA, bool lowB) {
+  const int t = threadIdx.x, r0 = 8 * (t >> 4), c0 = 8 * (t & 15);
+  float acc[8][8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int v = 0; v < 8; ++v) acc[u][v] = 0.f;
+  const int qlo = lowB ? c0 : 0, qhi = lowA ? r0 + 8 : CT;
+  for (int q = qlo; q < qhi; ++q) {
+    float av[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) av[u] = A[(r0 + u) * CT + q];
+    const float4 b0 = *reinterpret_cast<const float4*>(B + q * CT + c0);
+    const float4 b1 = *reinterpret_cast<const float4*>(B + q * CT + c0 + 4);
+    const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int v = 0; v < 8; ++v) acc[u][v] = fmaf(av[u], bv[v], acc[u][v]);
+  }
+  __syncthreads();   // all reads of A / B done (C may alias B)
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    *reinterpret_cast<float4*>(C + (r0 + u) * CT + c0) = make_float4(acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
+    *reinterpret_cast<float4*>(C + (r0 + u) * CT + c0 + 4) = make_float4(acc[u][4], acc[u][5], acc[u][6], acc[u][7]);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void tri_prefetch(float* d0, const float* s0, float* d1, const float* s1, float* d2,
+                                             const float* s2, uint64_t* bar) {
+  if (threadIdx.x == 0) {
+    tc_mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint32_t tb = (uint32_t)(TILE_F * sizeof(float));
+    tc_expect_tx(bar, tb * (1u + (s1 ? 1u : 0u) + (s2 ? 1u : 0u)));
+    tc_bulk(d0, s0, tb, bar);
+    if (s1) tc_bulk(d1, s1, tb, bar);
+    if (s2) tc_bulk(d2, s2, tb, bar);
   }
 }
 
-// backward solve  L^T z = y, x += D z  (x accumulated in place), flags fl[k] = gen.
-// CTA b handles row tiles nt-1-b, nt-1-b-G, ...; column c: two threads per column.
-__global__ void __launch_bounds__(256) k_tc_bwd(const float* __restrict__ W, int nt, const double* __restrict__ y,
-                                                double* __restrict__ z, const double* __restrict__ D,
-                                                double* __restrict__ x, double* __restrict__ dxmax,
-                                                double* __restrict__ xmax, int* __restrict__ fl, int gen,
-                                                const int* __restrict__ stop) {
-  __shared__ double zs[CT], acc[CT], part[CT];
-  if (*stop) return;
-  const int tid = threadIdx.x, col = tid & (CT - 1), h = tid >> 7;
-  for (int kb = blockIdx.x; kb < nt; kb += gridDim.x) {
-    const int k = nt - 1 - kb;
-    double a = (h == 0) ? __ldcg(y + CT * k + col) : 0.0;
-    for (int ii = nt - 1; ii >= k; --ii) {
-      const float* T;
-      if (ii > k) {
-        if (tid == 0) {
-          int ns = 32;
-          while (ld_acquire(&fl[ii]) < gen) { __nanosleep(ns); if (ns < 512) ns <<= 1; }
-        }
-        __syncthreads();
-        if (tid < CT) zs[tid] = __ldcg(z + CT * ii + tid);
-        T = W + tlin(ii, k) * TILE_F;
-      } else {   // z_k = Linv_kk^T acc
-        if (h == 0) acc[col] = a;
-        __syncthreads();
-        if (tid < CT) zs[tid] = acc[tid];
-        a = 0.0;
-        T = W + tlin(k, k) * TILE_F;
-      }
-      __syncthreads();
-      double s = 0.0;   // sum over rows [64h, 64h+64) of T[r][col] zs[r]
-#pragma unroll 8
-      for (int rr = 0; rr < 64; ++rr) {
-        const int rw = 64 * h + rr;
-        s = fma((double)__ldcg(T + (int64_t)rw * CT + col), zs[rw], s);
-      }
-      if (h == 1) part[col] = s;
-      __syncthreads();
-      if (h == 0) {
-        s += part[col];
-        if (ii > k) a -= s;
-        else a = s;
-      }
-      __syncthreads();
+// forward: L y = v, v = D r.  With M1 = Linv_kk L_{k,k-1}, M2 = Linv_kk L_{k,k-2}:
+//   y_k = Linv_kk (v_k - sum_{j<k-2} L_kj y_j) - M2 y_{k-2} - M1 y_{k-1}
+// the chain only sees one 128x128 shared-memory matvec per step.
+__global__ void __launch_bounds__(256, 1) k_tc_fwd(const float* __restrict__ W, int nt, const double* __restrict__ r,
+                                                   const double* __restrict__ D, unsigned long long* __restrict__ y,
+                                                   int gen, const int* __restrict__ stop) {
+  extern __shared__ __align__(16) unsigned char tri_raw[];
+  float* Lin = reinterpret_cast<float*>(tri_raw);     // Linv_kk
+  float* M1 = Lin + TILE_F;                           // L_{k,k-1} -> M1
+  float* M2 = M1 + TILE_F;                            // L_{k,k-2} -> M2
+  uint64_t* bar = reinterpret_cast<uint64_t*>(M2 + TILE_F);
+  __shared__ float vs[CT], acc[CT], base[CT];
+  if (*stop) return;   // refinement converged in an earlier pass
+  const int tid = threadIdx.x, k = blockIdx.x;
+  if (k >= nt) return;
+  tri_prefetch(Lin, W + tlin(k, k) * TILE_F, M1, k > 0 ? W + tlin(k, k - 1) * TILE_F : nullptr, M2,
+               k > 1 ? W + tlin(k, k - 2) * TILE_F : nullptr, bar);
+  if (tid < CT) acc[tid] = (float)(D[CT * k + tid] * r[CT * k + tid]);
+  __syncthreads();
+  tc_mbar_wait(bar, 0);
+  if (k > 0) smem_gemm128(M1, Lin, M1, true, false);   // in place: reads complete before the writes
+  if (k > 1) smem_gemm128(M2, Lin, M2, true, false);
+  for (int j = 0; j + 2 < k; ++j) {   // off the chain: global tiles
+    fetch_block(y + CT * j, vs, gen);
+    const int row = tid >> 1, h = tid & 1;
+    const float4* p = reinterpret_cast<const float4*>(W + tlin(k, j) * TILE_F + row * CT + 64 * h);
+    float4 av[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) av[q] = __ldcg(p + q);
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int c = 64 * h + 4 * q;
+      s0 = fmaf(av[q].x, vs[c], s0);
+      s1 = fmaf(av[q].y, vs[c + 1], s1);
+      s2 = fmaf(av[q].z, vs[c + 2], s2);
+      s3 = fmaf(av[q].w, vs[c + 3], s3);
     }
-    if (h == 0) {
-      __stcg(z + CT * k + col, a);
-      const double dxv = D[CT * k + col] * a;
-      const double xn = x[CT * k + col] + dxv;
-      x[CT * k + col] = xn;
-      // max |dx|, max |x| (non-negative doubles order like their bit patterns)
-      if (dxmax)
-        atomicMax(reinterpret_cast<unsigned long long*>(dxmax), (unsigned long long)__double_as_longlong(fabs(dxv)));
-      if (xmax)
-        atomicMax(reinterpret_cast<unsigned long long*>(xmax), (unsigned long long)__double_as_longlong(fabs(xn)));
-    }
-    __threadfence();
+    float s = (s0 + s1) + (s2 + s3);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
     __syncthreads();
-    if (tid == 0) st_release(&fl[k], gen);
+    if (h == 0) acc[row] -= s;
+    __syncthreads();
+  }
+  {
+    const float b = rowdot(Lin, acc);
+    if ((tid & 1) == 0) base[tid >> 1] = b;
+  }
+  __syncthreads();
+  if (k > 1) {
+    fetch_block(y + CT * (k - 2), vs, gen);
+    const float s = rowdot(M2, vs);
+    __syncthreads();
+    if ((tid & 1) == 0) base[tid >> 1] -= s;
+    __syncthreads();
+  }
+  if (k > 0) {   // the chain: y_k = base - M1 y_{k-1}
+    fetch_block(y + CT * (k - 1), vs, gen);
+    const float s = rowdot(M1, vs);
+    if ((tid & 1) == 0) put_tagged(y + CT * k + (tid >> 1), base[tid >> 1] - s, gen);
+  } else if (tid < CT) {
+    put_tagged(y + CT * k + tid, base[tid], gen);
+  }
+}
+
+// backward: L^T z = y.  With T1 = L_{k+1,k} Linv_kk, T2 = L_{k+2,k} Linv_kk:
+//   z_k = Linv^T (y_k - sum_{i>k+2} L_ik^T z_i) - T2^T z_{k+2} - T1^T z_{k+1};
+// then x += D z (fp64) with max |dx|, max |x|.
+__global__ void __launch_bounds__(256, 1) k_tc_bwd(const float* __restrict__ W, int nt,
+                                                   const unsigned long long* __restrict__ y,
+                                                   unsigned long long* __restrict__ z, const double* __restrict__ D,
+                                                   double* __restrict__ x, double* __restrict__ dxmax,
+                                                   double* __restrict__ xmax, int gen, const int* __restrict__ stop) {
+  extern __shared__ __align__(16) unsigned char tri_raw[];
+  float* Lin = reinterpret_cast<float*>(tri_raw);     // Linv_kk
+  float* T1 = Lin + TILE_F;                           // L_{k+1,k} -> T1
+  float* T2 = T1 + TILE_F;                            // L_{k+2,k} -> T2
+  uint64_t* bar = reinterpret_cast<uint64_t*>(T2 + TILE_F);
+  __shared__ float vs[CT], acc[CT], base[CT], part[CT];
+  if (*stop) return;
+  const int tid = threadIdx.x;
+  if ((int)blockIdx.x >= nt) return;
+  const int k = nt - 1 - blockIdx.x;
+  tri_prefetch(Lin, W + tlin(k, k) * TILE_F, T1, k + 1 < nt ? W + tlin(k + 1, k) * TILE_F : nullptr, T2,
+               k + 2 < nt ? W + tlin(k + 2, k) * TILE_F : nullptr, bar);
+  if (tid < CT) acc[tid] = get_tagged(y + CT * k + tid, gen);   // y_k (the forward pass is complete)
+  __syncthreads();
+  tc_mbar_wait(bar, 0);
+  if (k + 1 < nt) smem_gemm128(T1, T1, Lin, false, true);   // in place (C aliases A: reads finish first)
+  if (k + 2 < nt) smem_gemm128(T2, T2, Lin, false, true);
+  for (int i = nt - 1; i > k + 2; --i) {   // off the chain: global tiles, column sums
+    fetch_block(z + CT * i, vs, gen);
+    const float s = coldot(W + tlin(i, k) * TILE_F, vs, part, true);
+    if (tid < CT) acc[tid] -= s;
+    __syncthreads();
+  }
+  {
+    const float b = coldot(Lin, acc, part, false);
+    if (tid < CT) base[tid] = b;
+  }
+  __syncthreads();
+  if (k + 2 < nt) {
+    fetch_block(z + CT * (k + 2), vs, gen);
+    const float s = coldot(T2, vs, part, false);
+    if (tid < CT) base[tid] -= s;
+    __syncthreads();
+  }
+  float zk = 0.f;
+  if (k + 1 < nt) {   // the chain: z_k = base - T1^T z_{k+1}
+    fetch_block(z + CT * (k + 1), vs, gen);
+    const float s = coldot(T1, vs, part, false);
+    zk = (tid < CT) ? base[tid] - s : 0.f;
+  } else {
+    zk = (tid < CT) ? base[tid] : 0.f;
+  }
+  if (tid < CT) {
+    put_tagged(z + CT * k + tid, zk, gen);
+    const double dxv = D[CT * k + tid] * (double)zk;
+    const double xn = x[CT * k + tid] + dxv;
+    x[CT * k + tid] = xn;
+    // max |dx|, max |x| (non-negative doubles order like their bit patterns)
+    if (dxmax)
+      atomicMax(reinterpret_cast<unsigned long long*>(dxmax), (unsigned long long)__double_as_longlong(fabs(dxv)));
+    if (xmax)
+      atomicMax(reinterpret_cast<unsigned long long*>(xmax), (unsigned long long)__double_as_longlong(fabs(xn)));
   }
 }
 
@@ -1412,6 +1746,7 @@ __global__ void k_tc_resid(const double* __restrict__ b, const double* __restric
 // clear the maxima for the next pass (the last pass's values stay in out2)
 __global__ void k_tc_check(double* out2, int* stop, double tol, int last) {
   if (*stop) return;
+  out2[2] += 1.0;   // passes run
   if (out2[0] <= tol * out2[1]) *stop = 1;
   else if (!last) out2[0] = out2[1] = 0.0;
 }
@@ -1451,8 +1786,8 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
   float* img = reinterpret_cast<float*>(take(sizeof(float) * ntl * TILE_F * 2));
   double* D = reinterpret_cast<double*>(take(sizeof(double) * npad));
   double* r = reinterpret_cast<double*>(take(sizeof(double) * npad));
-  double* y = reinterpret_cast<double*>(take(sizeof(double) * npad));
-  double* z = reinterpret_cast<double*>(take(sizeof(double) * npad));
+  unsigned long long* y = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * npad));
+  unsigned long long* z = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * npad));
   double* P = reinterpret_cast<double*>(take(sizeof(double) * (size_t)nb * nb * SYB));
   int* flags = reinterpret_cast<int*>(take(sizeof(int) * ((size_t)2 * nt * nt + 1)));
   int* sfl = reinterpret_cast<int*>(take(sizeof(int) * 2 * (size_t)nt));
@@ -1460,6 +1795,8 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
   static int grid = 0, sms = 0;
   if (grid == 0) {
     cudaFuncSetAttribute(k_chol_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM);
+    cudaFuncSetAttribute(k_tc_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRI_SMEM);
+    cudaFuncSetAttribute(k_tc_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRI_SMEM);
     int dev = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1486,8 +1823,8 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
   launch_count();
   cudaMemsetAsync(x, 0, sizeof(double) * npad, st);
   cudaMemsetAsync(stop, 0, sizeof(int), st);
-  cudaMemsetAsync(out2, 0, sizeof(double) * 2, st);
-  const int gs = nt < sms ? nt : sms;
+  cudaMemsetAsync(out2, 0, sizeof(double) * 3, st);
+  if (nt > sms) return 1;   // one resident CTA per row tile (n <= 148 * 128 here)
   // passes until the correction is < 1e-12 max|x| (early-exit kernels after that), at most `iters`
   for (int it = 0; it < iters; ++it) {
     const double* rhs = b;
@@ -1498,9 +1835,9 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
       launch_count();
       rhs = r;
     }
-    k_tc_fwd<<<gs, 256, 0, st>>>(W, nt, rhs, D, y, sfl, gen + 2 * it, stop);
-    k_tc_bwd<<<gs, 256, 0, st>>>(W, nt, y, z, D, x, out2, out2 + 1, sfl + nt, gen + 2 * it, stop);
-    k_tc_check<<<1, 1, 0, st>>>(out2, stop, 1e-12, it == iters - 1);
+    k_tc_fwd<<<nt, 256, TRI_SMEM, st>>>(W, nt, rhs, D, y, gen + 2 * it, stop);
+    k_tc_bwd<<<nt, 256, TRI_SMEM, st>>>(W, nt, y, z, D, x, out2, out2 + 1, gen + 2 * it, stop);
+    k_tc_check<<<1, 1, 0, st>>>(out2, stop, 1e-10, it == iters - 1);
     launch_count();
     launch_count();
     launch_count();
@@ -1513,7 +1850,7 @@ void chol_trace_print(const char* tag, const unsigned long long* d_trace, const 
   {
     std::vector<unsigned long long> ph((size_t)16 * nt);
     cudaMemcpy(ph.data(), d_trace + 4 * (size_t)ntasks, ph.size() * 8, cudaMemcpyDeviceToHost);
-    double ld = 0, f = 0, u = 0, inv = 0;
+    double ld = 0, f = 0, u = 0, inv = 0, clk = 0, ns = 0;
     for (int k = 0; k < nt; ++k) {
       const unsigned long long* q = &ph[16 * (size_t)k];
       if (!q[0] || !q[10]) continue;
@@ -1525,7 +1862,9 @@ void chol_trace_print(const char* tag, const unsigned long long* d_trace, const 
         prev = q[3 + 2 * p];
       }
       inv += (double)(q[10] - q[9]) * 1e-3;
+      if (q[12] > q[11]) { clk += (double)(q[12] - q[11]); ns += (double)(q[10] - q[0]); }
     }
+    if (ns > 0) fprintf(stderr, "  POTRF SM clock %.0f MHz\n", 1e3 * clk / ns);
     fprintf(stderr, "  POTRF phases (avg us): load %.2f | factor32 x4 %.2f | trsm+syrk %.2f | inverse+store %.2f\n",
             ld / nt, f / nt, u / nt, inv / nt);
   }
@@ -1534,8 +1873,8 @@ void chol_trace_print(const char* tag, const unsigned long long* d_trace, const 
   cudaMemcpy(tr.data(), d_trace, tr.size() * 8, cudaMemcpyDeviceToHost);
   cudaMemcpy(tk.data(), d_tasks, tk.size() * sizeof(CholTask), cudaMemcpyDeviceToHost);
   unsigned long long t0 = ~0ull, t1 = 0;
-  double busy[5] = {0, 0, 0, 0, 0}, wait[5] = {0, 0, 0, 0, 0};
-  int cnt[5] = {0, 0, 0, 0, 0};
+  double busy[6] = {0, 0, 0, 0, 0, 0}, wait[6] = {0, 0, 0, 0, 0, 0};
+  int cnt[6] = {0, 0, 0, 0, 0, 0};
   for (int q = 0; q < ntasks; ++q) {
     if (tr[4 * q] == 0) continue;
     t0 = std::min(t0, tr[4 * q]);
@@ -1545,9 +1884,9 @@ void chol_trace_print(const char* tag, const unsigned long long* d_trace, const 
     wait[ty] += (double)(tr[4 * q + 1] - tr[4 * q]) * 1e-3;
     cnt[ty] += 1;
   }
-  const char* nm[5] = {"POTRF", "TRSM", "GEMM", "BUPD", "BSOL"};
+  const char* nm[6] = {"POTRF", "TRSM", "GEMM", "BUPD", "BSOL", "DIAG"};
   fprintf(stderr, "[%s trace] nt=%d tasks=%d span %.1f us\n", tag, nt, ntasks, (double)(t1 - t0) * 1e-3);
-  for (int ty = 0; ty < 5; ++ty)
+  for (int ty = 0; ty < 6; ++ty)
     if (cnt[ty])
       fprintf(stderr, "  %-5s n=%6d  avg busy %8.2f us  avg wait %8.2f us  total busy %.1f us\n", nm[ty], cnt[ty],
               busy[ty] / cnt[ty], wait[ty] / cnt[ty], busy[ty]);

@@ -45,13 +45,14 @@ constexpr int kTileRt = 1024;   // pixels per per-pixel work tile (kPixBlock * 2
 constexpr int kGramBlock = 512;
 constexpr int kMaxOutDegree = 31;
 constexpr int NBc = 128;         // Cholesky tile (vba_chol.cu)
+constexpr int kTcMinTiles = 32;  // tensor-core reduced solve from this many 128-tiles up
 
 struct Result {       // device -> host once per trial
   double energy[3];
   unsigned long long step_bits;
   int status;         // fp64 factorisation: non-positive pivot
   int tc_bad;         // tensor-core factorisation: non-positive pivot
-  double tc[2];       // tensor-core solve: last refinement correction, max |x|
+  double tc[3];       // tensor-core solve: last refinement correction, max |x|, passes
 };
 
 template <class T>
@@ -120,11 +121,14 @@ struct Ctx {
   void* d_ctasks = nullptr;        // Cholesky task list
   int n_ctasks = 0;
   void* d_tcws = nullptr;          // tensor-core (3xTF32 + fp64 refinement) solve workspace
+  void* d_tctasks = nullptr;       // its task DAG (DIAG-fused critical chain)
+  int n_tctasks = 0;
   bool use_tc = false;             // VBA_CHOL=tc: tensor-core reduced solve
   bool force_fp64 = false;         // this step: fp64 DAG (tensor-core solve failed its checks)
   int tc_gen = 1;
   int tc_iters = 8;   // refinement passes at most (early exit once converged)
   int64_t tc_fallbacks = 0;
+  int64_t tc_solves = 0, tc_passes = 0;
   int32_t* d_fmap = nullptr;
   Result* d_res = nullptr;
   Result* h_res = nullptr;
@@ -645,7 +649,7 @@ static int stage_step(Ctx* c, double lam, cudaStream_t st) {
         return VBA_E_CUDA;
     }
     if (c->use_tc && !c->force_fp64 && !c->d_trace) {
-      chol_tc_solve(c->d_H, c->npad, c->nfree, c->npad, c->d_rhs, c->d_x, c->d_tcws, c->d_ctasks, c->n_ctasks,
+      chol_tc_solve(c->d_H, c->npad, c->nfree, c->npad, c->d_rhs, c->d_x, c->d_tcws, c->d_tctasks, c->n_tctasks,
                     c->tc_iters, &c->d_res->tc_bad, c->tc_gen, st, c->d_res->tc);
       c->tc_gen += 2 * c->tc_iters;
     } else {
@@ -755,9 +759,11 @@ static int stage_step_any(Ctx* c, double lam, int use_schur, cudaStream_t st) {
 
 // The tensor-core solve is accepted when its fp32 factor had positive pivots and
 // the last fp64 refinement pass moved x by < 1e-8 max|x| (converged to fp64).
-static bool tc_failed(const Ctx* c, int use_schur) {
+static bool tc_failed(Ctx* c, int use_schur) {
   if (!c->use_tc || c->force_fp64 || c->d_trace || c->nfree == 0 || !(use_schur || c->n_disp == 0)) return false;
   const Result& r = *c->h_res;
+  ++c->tc_solves;
+  c->tc_passes += (int64_t)r.tc[2];
   return r.tc_bad != 0 || !(r.tc[0] <= 1e-8 * r.tc[1]);
 }
 
@@ -921,9 +927,13 @@ int vba_create(void** out, const vba_problem* prob, const vba_options* opts, voi
     return fail(rc);
   if (cudaMallocHost((void**)&c->h_res, sizeof(Result)) != cudaSuccess) { set_err("pinned alloc failed"); return fail(VBA_E_CUDA); }
   {
-    // tensor-core reduced solve: opt-in (VBA_CHOL=tc) until its DAG beats the fp64 one
+    // tensor-core reduced solve for large reduced systems (its fixed costs -- refinement
+    // passes, extra launches -- lose to the fp64 DAG below ~32 tiles, n ~ 4000);
+    // VBA_CHOL=tc / fp64 forces either
     const char* ch = getenv("VBA_CHOL");
-    c->use_tc = ch && std::strcmp(ch, "tc") == 0 && c->nt > 0;
+    if (ch && std::strcmp(ch, "tc") == 0) c->use_tc = c->nt > 0;
+    else if (ch && std::strcmp(ch, "fp64") == 0) c->use_tc = false;
+    else c->use_tc = c->nt >= kTcMinTiles;
     const char* it = getenv("VBA_TC_ITERS");
     if (it) c->tc_iters = std::max(1, atoi(it));
   }
@@ -931,6 +941,14 @@ int vba_create(void** out, const vba_problem* prob, const vba_options* opts, voi
     const size_t wb = chol_tc_ws_bytes(c->npad);
     if ((rc = dalloc(c, (char**)&c->d_tcws, wb))) return fail(rc);
     cudaMemsetAsync(c->d_tcws, 0, wb, st);
+    const int cap = chol_plan_tasks_tc(c->nt, nullptr, 0);
+    std::vector<char> buf((size_t)std::max(cap, 1) * chol_task_bytes());
+    c->n_tctasks = chol_plan_tasks_tc(c->nt, buf.data(), cap);
+    if ((rc = dalloc(c, (char**)&c->d_tctasks, buf.size()))) return fail(rc);
+    if (cudaMemcpyAsync(c->d_tctasks, buf.data(), buf.size(), cudaMemcpyHostToDevice, st) != cudaSuccess) {
+      set_err("task upload failed");
+      return fail(VBA_E_CUDA);
+    }
   }
   {  // Cholesky task DAG (dense, lookahead 1)
     const int cap = chol_plan_tasks(c->nt, nullptr, 0);
@@ -991,8 +1009,8 @@ int vba_stats(void* ctx, int64_t* out4) {
   Ctx* c = (Ctx*)ctx;
   out4[0] = c->use_tc ? 1 : 0;
   out4[1] = c->tc_fallbacks;
-  out4[2] = c->tc_gen;
-  out4[3] = c->tc_iters;
+  out4[2] = c->tc_solves;
+  out4[3] = c->tc_passes;
   return VBA_OK;
 }
 
@@ -1005,19 +1023,22 @@ int vba_spd_solve(const double* H, int64_t n, const double* b, double* x, int32_
   const int cap = chol_plan_tasks(nt, nullptr, 0);
   std::vector<char> tb((size_t)cap * chol_task_bytes());
   const int ntasks = chol_plan_tasks(nt, tb.data(), cap);
+  const int cap2 = chol_plan_tasks_tc(nt, nullptr, 0);
+  std::vector<char> tb2((size_t)cap2 * chol_task_bytes());
+  const int ntasks2 = chol_plan_tasks_tc(nt, tb2.data(), cap2);
   const size_t tcb = mode != 1 ? chol_tc_ws_bytes(npad) : 0;
   double *Hp = nullptr, *bp = nullptr, *xp = nullptr, *Ld = nullptr, *part = nullptr, *tc2 = nullptr;
   int *flags = nullptr, *stat = nullptr;
-  void *tasks = nullptr, *ws = nullptr;
+  void *tasks = nullptr, *tasks2 = nullptr, *ws = nullptr;
   auto cleanup = [&]() {
     cudaFree(Hp); cudaFree(bp); cudaFree(xp); cudaFree(Ld); cudaFree(part); cudaFree(tc2);
-    cudaFree(flags); cudaFree(stat); cudaFree(tasks); cudaFree(ws);
+    cudaFree(flags); cudaFree(stat); cudaFree(tasks); cudaFree(tasks2); cudaFree(ws);
   };
   if (cudaMalloc(&Hp, sizeof(double) * (size_t)npad * npad) || cudaMalloc(&bp, sizeof(double) * npad) ||
       cudaMalloc(&xp, sizeof(double) * npad) || cudaMalloc(&Ld, sizeof(double) * (size_t)nt * NBc * NBc) ||
-      cudaMalloc(&part, sizeof(double) * (size_t)nt * nt * NBc) || cudaMalloc(&tc2, sizeof(double) * 2) ||
+      cudaMalloc(&part, sizeof(double) * (size_t)nt * nt * NBc) || cudaMalloc(&tc2, sizeof(double) * 3) ||
       cudaMalloc(&flags, sizeof(int) * ((size_t)2 * nt * nt + nt + 1)) || cudaMalloc(&stat, sizeof(int) * 2) ||
-      cudaMalloc(&tasks, tb.size()) || (tcb && cudaMalloc(&ws, tcb))) {
+      cudaMalloc(&tasks, tb.size()) || cudaMalloc(&tasks2, tb2.size()) || (tcb && cudaMalloc(&ws, tcb))) {
     cleanup();
     set_err("vba_spd_solve: allocation failed");
     return VBA_E_CUDA;
@@ -1025,12 +1046,13 @@ int vba_spd_solve(const double* H, int64_t n, const double* b, double* x, int32_
   cudaMemsetAsync(Hp, 0, sizeof(double) * (size_t)npad * npad, st);
   cudaMemsetAsync(bp, 0, sizeof(double) * npad, st);
   cudaMemsetAsync(stat, 0, sizeof(int) * 2, st);
-  cudaMemsetAsync(tc2, 0, sizeof(double) * 2, st);
+  cudaMemsetAsync(tc2, 0, sizeof(double) * 3, st);
   if (tcb) cudaMemsetAsync(ws, 0, tcb, st);
   cudaMemcpy2DAsync(Hp, sizeof(double) * npad, H, sizeof(double) * n, sizeof(double) * n, n,
                     cudaMemcpyDeviceToDevice, st);
   cudaMemcpyAsync(bp, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
   cudaMemcpyAsync(tasks, tb.data(), tb.size(), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(tasks2, tb2.data(), tb2.size(), cudaMemcpyHostToDevice, st);
   launch_pad_identity(Hp, npad, (int)n, npad, bp, st);
   int hs[2] = {0, 0};
   double h2[2] = {0, 0};
@@ -1038,9 +1060,9 @@ int vba_spd_solve(const double* H, int64_t n, const double* b, double* x, int32_
   if (mode == 0 || mode == 2) {   // 2: tensor-core result without the fallback (diagnostics)
     const int iters = info && info[0] > 0 ? info[0] : 8;
     unsigned long long* tr = nullptr;
-    if (getenv("VBA_CHOL_TRACE")) { cudaMalloc(&tr, sizeof(unsigned long long) * (4 * (size_t)ntasks + 16 * (size_t)nt)); cudaMemsetAsync(tr, 0, sizeof(unsigned long long) * (4 * (size_t)ntasks + 16 * (size_t)nt), st); }
-    chol_tc_solve(Hp, npad, (int)n, npad, bp, xp, ws, tasks, ntasks, iters, stat + 1, 1, st, tc2, tr);
-    if (tr) { cudaStreamSynchronize(st); chol_trace_print("tc", tr, tasks, ntasks, nt); cudaFree(tr); }
+    if (getenv("VBA_CHOL_TRACE")) { cudaMalloc(&tr, sizeof(unsigned long long) * (4 * (size_t)ntasks2 + 16 * (size_t)nt)); cudaMemsetAsync(tr, 0, sizeof(unsigned long long) * (4 * (size_t)ntasks2 + 16 * (size_t)nt), st); }
+    chol_tc_solve(Hp, npad, (int)n, npad, bp, xp, ws, tasks2, ntasks2, iters, stat + 1, 1, st, tc2, tr);
+    if (tr) { cudaStreamSynchronize(st); chol_trace_print("tc", tr, tasks2, ntasks2, nt); cudaFree(tr); }
     cudaMemcpyAsync(hs, stat, sizeof(hs), cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(h2, tc2, sizeof(h2), cudaMemcpyDeviceToHost, st);
     if (cudaStreamSynchronize(st) != cudaSuccess) { cleanup(); set_err("vba_spd_solve: %s", cudaGetErrorString(cudaGetLastError())); return VBA_E_CUDA; }

@@ -318,8 +318,10 @@ int chol_dag_launch(double* A, int64_t ld, int nt, double* rhs, double* x, doubl
                     const void* tasks, int ntasks, int* status, cudaStream_t st,
                     unsigned long long* trace = nullptr);
 // Mixed-precision (tcgen05 3xTF32 factor + fp64 iterative refinement) SPD solve,
-// vba_chol.cu.  out2[0] = max |correction| of the last refinement pass, out2[1] = max |x|.
+// vba_chol.cu.  out2[0] = max |correction| of the last refinement pass, out2[1] = max |x|,
+// out2[2] = refinement passes run.
 size_t chol_tc_ws_bytes(int npad);
+int chol_plan_tasks_tc(int nt, void* out, int cap);
 int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b, double* x, void* ws,
                   const void* tasks, int ntasks, int iters, int* status, int gen, cudaStream_t st, double* out2,
                   unsigned long long* trace = nullptr);

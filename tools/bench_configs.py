@@ -53,7 +53,8 @@ for cfg in [int(c) for c in a.configs.split(",")]:
     import ctypes
     stt = (ctypes.c_int64 * 4)()
     dp.lib.vba_stats(dp.ctx, stt)
-    print(f"   tensor-core solve: {bool(stt[0])}, fp64 fallbacks {stt[1]}")
+    print(f"   tensor-core solve: {bool(stt[0])}, fp64 fallbacks {stt[1]}, solves {stt[2]}, "
+          f"refinement passes/solve {stt[3] / max(stt[2], 1):.1f}")
     dp.close()
     del dp
     torch.cuda.empty_cache()
