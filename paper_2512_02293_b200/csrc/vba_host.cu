@@ -450,7 +450,7 @@ static int build_plans(Ctx* c, cudaStream_t st) {
   int64_t work_px = 0;
   for (int n = 0; n < K; ++n)
     if (c->see[n] > c->seb[n] && P.h_npix[n] > 0) { ++nsrc; work_px += P.h_npix[n]; }
-  const int target = 2 * 148;
+  const int target = getenv("VBA_GRAM_TARGET") ? atoi(getenv("VBA_GRAM_TARGET")) : 2 * 148;
   c->goff.assign(K, 0);
   c->foff.assign(K, 0);
   c->g0.assign(K, 0);

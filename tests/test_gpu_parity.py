@@ -158,3 +158,71 @@ def test_spd_solve_tensor_core_matches_fp64(cuda_ok, n, cond):
     e0 = ((x0.cpu() - ref).abs().max() / ref.abs().max()).item()
     assert e1 < 1e-9 * max(1.0, cond / 1e5), e1
     assert e0 < 1e-9 * max(1.0, cond / 1e5), e0
+
+
+@pytest.fixture
+def force_tc(monkeypatch):
+    """Force the tensor-core reduced solve (3xTF32 factor + fp64 refinement) on the
+    small golden systems; by default it is only used from 32 Cholesky tiles up."""
+    monkeypatch.setenv("VBA_CHOL", "tc")
+    yield
+
+
+def _stats(dp):
+    import ctypes
+    s = (ctypes.c_int64 * 4)()
+    dp.lib.vba_stats(dp.ctx, s)
+    return list(s)
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_solve_step_tensor_core(name, cuda_ok, force_tc):
+    P, out, opts = load_golden(name)
+    dp = _dp(P, opts)
+    dp.linearize()
+    dx, dxd = dp.solve_step(opts["damping"])
+    st = _stats(dp)
+    assert st[0] == 1 and st[2] >= 1, st                    # the tensor-core path ran
+    assert rel(dx, out["dx"]) < tol_update(name, out, "dx")
+    assert rel(dxd, out["dxd"]) < tol_update(name, out, "dxd")
+
+
+@pytest.mark.parametrize("name", ["win8_px30", "cfg0_grid12x16", "win5_gravity"])
+def test_solve_vi_ba_tensor_core(name, cuda_ok, force_tc):
+    P, out, opts = load_golden(name)
+    dp = _dp(copy.deepcopy(P), opts)
+    rep = dp.solve()
+    ref = out["report"]
+    s = dp.download()
+    c, cr = rep["cost_trajectory"], ref["cost_trajectory"]
+    for k in range(min(len(cr), len(c))):
+        if cr[k] < 1e-6 * cr[0]:
+            break
+        assert abs(c[k] - cr[k]) <= 1e-3 * cr[k], (k, c, cr)
+    assert np.abs(s["p"] - out["final_p"]).max() < 1e-5
+    assert _stats(dp)[1] == 0                                 # no fp64 fallback
+
+
+def test_large_window_uses_tensor_core_solve_without_fallback(cuda_ok):
+    """BASELINE config 3 (n_f = 1905 -> 15 tiles) forced onto the tensor-core solve: the
+    solve converges (no fp64 fallback) and every step equals the fp64 DAG's to 1e-8."""
+    import os
+    from paper_2512_02293_b200.problem import pack_graph
+    from paper_2512_02293_b200.workloads import make_workload
+    P = pack_graph(make_workload(3))
+    opts = {"max_iterations": 1}
+    steps = {}
+    for mode in ("fp64", "tc"):
+        os.environ["VBA_CHOL"] = mode
+        try:
+            dp = _dp(copy.deepcopy(P), opts)
+            dp.linearize()
+            steps[mode] = dp.solve_step(1e-4)
+            if mode == "tc":
+                st = _stats(dp)
+                assert st[0] == 1 and st[1] == 0 and st[2] >= 1, st
+            dp.close()
+        finally:
+            os.environ.pop("VBA_CHOL", None)
+    assert rel(steps["tc"][0], steps["fp64"][0]) < 1e-8
+    assert rel(steps["tc"][1], steps["fp64"][1]) < 1e-8
