@@ -268,6 +268,8 @@ def main():
     launches = dp.launch_count() - n0
     clocks = clk.stop()
     st = dp.stage_times()
+    sv = dp.solve_times()
+    sstat = dp.stats()
     dp.set_profiling(False)
     t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -317,6 +319,28 @@ def main():
     b_lin = 16.0 * rows_r + 12.0 * Kr * N
     hbm, kind = peaks()
     achieved = b_lin / (k1_ms / 1e3) / 1e9 if k1_ms > 0 else 0.0
+    # dominant kernel: the tensor-core tile-DAG Cholesky of the reduced system (3xTF32 on
+    # tcgen05).  Useful work n^3/3 fp32-equivalent flops per factorisation; the tensor
+    # cores execute 3x that in tf32.  Peak: dense tf32 = half the measured bf16 GEMM peak.
+    dom = None
+    if sv["solves"] > 0:
+        n_red = sv["n"]
+        f_ms = sv["factor_ms"] / sv["solves"]
+        bf16 = tf32 = None
+        pp = os.path.join(REPO, "MEASURED_PEAKS.json")
+        if os.path.exists(pp):
+            with open(pp) as f:
+                bf16 = float(json.load(f).get("bf16_tflops", 0.0)) or None
+        tf32 = (bf16 or 1590.0) / 2.0
+        useful = n_red ** 3 / 3.0 / (f_ms / 1e3) / 1e12
+        dom = {"kernel": "k_chol_tc (reduced-system Cholesky, tcgen05 kind::tf32, 3xTF32)", "bound": "tensor",
+               "achieved_tc_tflops": 3.0 * useful, "useful_fp32_tflops": useful, "peak": tf32,
+               "peak_kind": ("half of measured bf16" if bf16 else "half of fallback bf16"), "unit": "TFLOP/s",
+               "frac": 3.0 * useful / tf32, "factor_ms": f_ms,
+               "refine_ms_per_solve": sv["refine_ms"] / sv["solves"],
+               "refine_passes_per_solve": sstat["refine_passes"] / max(sstat["tc_solves"], 1),
+               "fp64_fallbacks": sstat["fallbacks"], "n": n_red,
+               "note": "n^3/3 useful flops per factorisation; critical-path (tile DAG) bound, see DESIGN.md"}
     solve_ms = tmax / a.steps
     stage_share = {k: v / max(sum(st[x] for x in ("linearize", "gram_fill", "assemble_chol", "backsub_retract",
                                                     "energy")), 1e-9)
@@ -341,6 +365,7 @@ def main():
                          "traffic": committed_traffic(a.config),
                          "algorithmic_bytes_per_launch": b_lin, "avg_launch_ms": k1_ms,
                          "note": "B_lin = 16 B per edge-pixel (flow + weight fp32) + 12 B per keyframe-pixel"},
+            "roofline_dominant": dom,
             "stage_ms_per_step": {k: v / a.steps for k, v in st.items() if k != "k1_launches"},
             "stage_share": stage_share,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},

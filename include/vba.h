@@ -165,6 +165,10 @@ VBA_API int64_t vba_launch_count(void* ctx);
  * [3] back-substitution + retraction  [4] trial energy  [5] vision linearisation
  * kernel alone  [6] number of samples in [5]   (out must hold 7 doubles) */
 VBA_API int vba_stage_times(void* ctx, double* out5);
+/* tensor-core reduced solve timing since vba_set_profiling, ms: [0] tile-DAG
+ * factorisation kernel, [1] refinement passes (triangular solves + fp64
+ * residuals), [2] number of solves timed, [3] reduced dimension n */
+VBA_API int vba_solve_times(void* ctx, double* out4);
 /* solver statistics: [0] tensor-core reduced solve enabled, [1] steps that fell
  * back to the fp64 factorisation, [2] tensor-core solves, [3] refinement passes
  * summed over them */

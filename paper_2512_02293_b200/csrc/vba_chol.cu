@@ -1599,68 +1599,99 @@ __device__ __forceinline__ void tri_prefetch(float* d0, const float* s0, float* 
   }
 }
 
+// Per factorisation (not per pass): the folded neighbour matrices of the solves,
+// one CTA per (k, kind), written to global memory in the layout their matvec
+// reads conflict-free (out[r] = sum_c X[c][r] v[c], i.e. transposed for the
+// forward solve):
+//   kind 0: LinvT_k                     (forward base, Linv_kk acc)
+//   kind 1: (Linv_kk L_{k,k-1})^T       (forward chain)
+//   kind 2: (Linv_kk L_{k,k-2})^T
+//   kind 3: L_{k+1,k} Linv_kk           (backward chain, read as column sums)
+//   kind 4: L_{k+2,k} Linv_kk
+__global__ void __launch_bounds__(256, 1) k_tc_prep(const float* __restrict__ W, int nt, float* __restrict__ F) {
+  extern __shared__ __align__(16) unsigned char tri_raw[];
+  float* A = reinterpret_cast<float*>(tri_raw);
+  float* B = A + TILE_F;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(B + 2 * TILE_F);
+  const int k = blockIdx.x, kind = blockIdx.y;
+  float* out = F + ((int64_t)kind * nt + k) * TILE_F;
+  const float* Lin = W + tlin(k, k) * TILE_F;
+  const float* other = nullptr;
+  if (kind == 1 && k >= 1) other = W + tlin(k, k - 1) * TILE_F;
+  if (kind == 2 && k >= 2) other = W + tlin(k, k - 2) * TILE_F;
+  if (kind == 3 && k + 1 < nt) other = W + tlin(k + 1, k) * TILE_F;
+  if (kind == 4 && k + 2 < nt) other = W + tlin(k + 2, k) * TILE_F;
+  if (kind != 0 && !other) return;
+  // kinds 1, 2: C = Lin X (A = Lin, B = X);  kinds 3, 4: C = X Lin (A = X, B = Lin)
+  tri_prefetch(kind >= 3 ? B : A, Lin, kind >= 3 ? A : B, other, nullptr, nullptr, bar);
+  __syncthreads();   // barrier initialised before anyone waits on it
+  tc_mbar_wait(bar, 0);
+  if (kind == 0) {
+    smem_transpose128(A);
+  } else {
+    smem_gemm128(A, A, B, kind <= 2, kind >= 3, kind <= 2);   // in place; transposed output for kinds 1, 2
+  }
+  for (int e = threadIdx.x; e < TILE_F / 4; e += 256)
+    __stcg(reinterpret_cast<float4*>(out) + e, reinterpret_cast<const float4*>(A)[e]);
+}
+
 // forward: L y = v, v = D r.  With M1 = Linv_kk L_{k,k-1}, M2 = Linv_kk L_{k,k-2}:
 //   y_k = Linv_kk (v_k - sum_{j<k-2} L_kj y_j) - M2 y_{k-2} - M1 y_{k-1}
-// the chain only sees one 128x128 shared-memory matvec per step.
-__global__ void __launch_bounds__(256, 1) k_tc_fwd(const float* __restrict__ W, int nt, const double* __restrict__ r,
+// LinvT, M1^T, M2^T come precomputed (k_tc_prep); the chain sees one 128x128
+// shared-memory matvec per step.  Off-chain tiles are register-prefetched two deep.
+__global__ void __launch_bounds__(256, 1) k_tc_fwd(const float* __restrict__ W, const float* __restrict__ F,
+                                                   int nt, const double* __restrict__ r,
                                                    const double* __restrict__ D, unsigned long long* __restrict__ y,
                                                    int gen, const int* __restrict__ stop) {
   extern __shared__ __align__(16) unsigned char tri_raw[];
-  float* Lin = reinterpret_cast<float*>(tri_raw);     // Linv_kk
-  float* M1 = Lin + TILE_F;                           // L_{k,k-1} -> M1
-  float* M2 = M1 + TILE_F;                            // L_{k,k-2} -> M2
+  float* Lin = reinterpret_cast<float*>(tri_raw);     // Linv_kk^T
+  float* M1 = Lin + TILE_F;                           // M1^T
+  float* M2 = M1 + TILE_F;                            // M2^T
   uint64_t* bar = reinterpret_cast<uint64_t*>(M2 + TILE_F);
   __shared__ float vs[CT], acc[CT], base[CT], part[CT];
   if (*stop) return;   // refinement converged in an earlier pass
   const int tid = threadIdx.x, k = blockIdx.x;
   if (k >= nt) return;
   TRI_STAMP(0, 0, k)
-  tri_prefetch(Lin, W + tlin(k, k) * TILE_F, M1, k > 0 ? W + tlin(k, k - 1) * TILE_F : nullptr, M2,
-               k > 1 ? W + tlin(k, k - 2) * TILE_F : nullptr, bar);
+  tri_prefetch(Lin, F + (int64_t)k * TILE_F, M1, k > 0 ? F + ((int64_t)nt + k) * TILE_F : nullptr, M2,
+               k > 1 ? F + ((int64_t)2 * nt + k) * TILE_F : nullptr, bar);
   if (tid < CT) acc[tid] = (float)(D[CT * k + tid] * r[CT * k + tid]);
+  // off the chain: tiles L_kj, j < k-2, two ahead in registers (they do not depend on y)
+  const int row = tid >> 1, h = tid & 1;
+  auto ld_tile = [&](int j, float4* dst) {
+    const float4* p = reinterpret_cast<const float4*>(W + tlin(k, j) * TILE_F + row * CT + 64 * h);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) dst[q] = __ldcg(p + q);
+  };
+  // ping-pong register buffers: tile j+2's loads are issued while tile j is used
+  float4 bx[16], by[16];
+  if (k > 2) ld_tile(0, bx);
+  if (k > 3) ld_tile(1, by);
   __syncthreads();
-  tc_mbar_wait(bar, 0);
-  // M1, M2 and Linv stored transposed: every matvec reads consecutive addresses per warp
-  if (k > 0) smem_gemm128(M1, Lin, M1, true, false, true);
-  if (k > 1) smem_gemm128(M2, Lin, M2, true, false, true);
-  smem_transpose128(Lin);
-  TRI_STAMP(0, 1, k)
-  // off the chain: global tiles L_kj (j < k-2), the next tile's registers loaded while
-  // waiting for the current y_j (the tiles do not depend on the solve)
-  float4 av[16], an[16];
-  {
-    const int row = tid >> 1, h = tid & 1;
-    if (k > 2) {
-      const float4* p = reinterpret_cast<const float4*>(W + tlin(k, 0) * TILE_F + row * CT + 64 * h);
-#pragma unroll
-      for (int q = 0; q < 16; ++q) an[q] = __ldcg(p + q);
-    }
-  }
-  for (int j = 0; j + 2 < k; ++j) {
-    const int row = tid >> 1, h = tid & 1;
-#pragma unroll
-    for (int q = 0; q < 16; ++q) av[q] = an[q];
-    if (j + 3 < k) {
-      const float4* p = reinterpret_cast<const float4*>(W + tlin(k, j + 1) * TILE_F + row * CT + 64 * h);
-#pragma unroll
-      for (int q = 0; q < 16; ++q) an[q] = __ldcg(p + q);
-    }
+  auto fold = [&](int j, float4* buf) {
     fetch_block(y + CT * j, vs, gen);
     float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
       const int c = 64 * h + 4 * q;
-      s0 = fmaf(av[q].x, vs[c], s0);
-      s1 = fmaf(av[q].y, vs[c + 1], s1);
-      s2 = fmaf(av[q].z, vs[c + 2], s2);
-      s3 = fmaf(av[q].w, vs[c + 3], s3);
+      s0 = fmaf(buf[q].x, vs[c], s0);
+      s1 = fmaf(buf[q].y, vs[c + 1], s1);
+      s2 = fmaf(buf[q].z, vs[c + 2], s2);
+      s3 = fmaf(buf[q].w, vs[c + 3], s3);
     }
-    float s = (s0 + s1) + (s2 + s3);
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    float sp = (s0 + s1) + (s2 + s3);
+    sp += __shfl_xor_sync(0xffffffffu, sp, 1);
     __syncthreads();
-    if (h == 0) acc[row] -= s;
-    __syncthreads();
+    if (h == 0) acc[row] -= sp;
+    if (j + 4 < k) ld_tile(j + 2, buf);
+  };
+  for (int j = 0; j + 2 < k; j += 2) {
+    fold(j, bx);
+    if (j + 3 < k) fold(j + 1, by);
   }
+  __syncthreads();
+  TRI_STAMP(0, 1, k)
+  tc_mbar_wait(bar, 0);
   TRI_STAMP(0, 2, k)
   {
     const float b = coldot(Lin, acc, part, false);   // (Linv acc)[r] = sum_c LinvT[c][r] acc[c]
@@ -1685,62 +1716,60 @@ __global__ void __launch_bounds__(256, 1) k_tc_fwd(const float* __restrict__ W, 
 
 // backward: L^T z = y.  With T1 = L_{k+1,k} Linv_kk, T2 = L_{k+2,k} Linv_kk:
 //   z_k = Linv^T (y_k - sum_{i>k+2} L_ik^T z_i) - T2^T z_{k+2} - T1^T z_{k+1};
-// then x += D z (fp64) with max |dx|, max |x|.
-__global__ void __launch_bounds__(256, 1) k_tc_bwd(const float* __restrict__ W, int nt,
-                                                   const unsigned long long* __restrict__ y,
+// then x += D z (fp64) with max |dx|, max |x|.  T1, T2 precomputed (k_tc_prep).
+__global__ void __launch_bounds__(256, 1) k_tc_bwd(const float* __restrict__ W, const float* __restrict__ F,
+                                                   int nt, const unsigned long long* __restrict__ y,
                                                    unsigned long long* __restrict__ z, const double* __restrict__ D,
                                                    double* __restrict__ x, double* __restrict__ dxmax,
                                                    double* __restrict__ xmax, int gen, const int* __restrict__ stop) {
   extern __shared__ __align__(16) unsigned char tri_raw[];
   float* Lin = reinterpret_cast<float*>(tri_raw);     // Linv_kk
-  float* T1 = Lin + TILE_F;                           // L_{k+1,k} -> T1
-  float* T2 = T1 + TILE_F;                            // L_{k+2,k} -> T2
+  float* T1 = Lin + TILE_F;
+  float* T2 = T1 + TILE_F;
   uint64_t* bar = reinterpret_cast<uint64_t*>(T2 + TILE_F);
   __shared__ float vs[CT], acc[CT], base[CT], part[CT];
   if (*stop) return;
   const int tid = threadIdx.x;
   if ((int)blockIdx.x >= nt) return;
   const int k = nt - 1 - blockIdx.x;
-  tri_prefetch(Lin, W + tlin(k, k) * TILE_F, T1, k + 1 < nt ? W + tlin(k + 1, k) * TILE_F : nullptr, T2,
-               k + 2 < nt ? W + tlin(k + 2, k) * TILE_F : nullptr, bar);
+  tri_prefetch(Lin, W + tlin(k, k) * TILE_F, T1, k + 1 < nt ? F + ((int64_t)3 * nt + k) * TILE_F : nullptr, T2,
+               k + 2 < nt ? F + ((int64_t)4 * nt + k) * TILE_F : nullptr, bar);
   if (tid < CT) acc[tid] = get_tagged(y + CT * k + tid, gen);   // y_k (the forward pass is complete)
   __syncthreads();
-  tc_mbar_wait(bar, 0);
-  if (k + 1 < nt) smem_gemm128(T1, T1, Lin, false, true);   // in place (C aliases A: reads finish first)
-  if (k + 2 < nt) smem_gemm128(T2, T2, Lin, false, true);
-  // off the chain: global tiles L_ik (i > k+2), column sums; next tile prefetched in registers
+  // off the chain: global tiles L_ik (i > k+2), column sums; two tiles ahead in registers
   {
     const int col = tid & (CT - 1), h = tid >> 7;
-    float cv[64], cn[64];
-    if (nt - 1 > k + 2) {
-      const float* T = W + tlin(nt - 1, k) * TILE_F;
+    float cx[64], cy[64];   // ping-pong: tile i-2's loads issued while tile i is used
+    auto ld_col = [&](int i, float* dst) {
+      const float* T = W + tlin(i, k) * TILE_F;
 #pragma unroll
-      for (int rr = 0; rr < 64; ++rr) cn[rr] = __ldcg(T + (64 * h + rr) * CT + col);
-    }
-    for (int i = nt - 1; i > k + 2; --i) {
-#pragma unroll
-      for (int rr = 0; rr < 64; ++rr) cv[rr] = cn[rr];
-      if (i - 1 > k + 2) {
-        const float* T = W + tlin(i - 1, k) * TILE_F;
-#pragma unroll
-        for (int rr = 0; rr < 64; ++rr) cn[rr] = __ldcg(T + (64 * h + rr) * CT + col);
-      }
+      for (int rr = 0; rr < 64; ++rr) dst[rr] = __ldcg(T + (64 * h + rr) * CT + col);
+    };
+    auto fold = [&](int i, float* buf) {
       fetch_block(z + CT * i, vs, gen);
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
       for (int rr = 0; rr < 64; rr += 4) {
-        s0 = fmaf(cv[rr], vs[64 * h + rr], s0);
-        s1 = fmaf(cv[rr + 1], vs[64 * h + rr + 1], s1);
-        s2 = fmaf(cv[rr + 2], vs[64 * h + rr + 2], s2);
-        s3 = fmaf(cv[rr + 3], vs[64 * h + rr + 3], s3);
+        s0 = fmaf(buf[rr], vs[64 * h + rr], s0);
+        s1 = fmaf(buf[rr + 1], vs[64 * h + rr + 1], s1);
+        s2 = fmaf(buf[rr + 2], vs[64 * h + rr + 2], s2);
+        s3 = fmaf(buf[rr + 3], vs[64 * h + rr + 3], s3);
       }
       const float sp = (s0 + s1) + (s2 + s3);
       if (h == 1) part[col] = sp;
       __syncthreads();
       if (h == 0) acc[col] -= sp + part[col];
       __syncthreads();
+      if (i - 2 > k + 2) ld_col(i - 2, buf);
+    };
+    if (nt - 1 > k + 2) ld_col(nt - 1, cx);
+    if (nt - 2 > k + 2) ld_col(nt - 2, cy);
+    for (int i = nt - 1; i > k + 2; i -= 2) {
+      fold(i, cx);
+      if (i - 1 > k + 2) fold(i - 1, cy);
     }
   }
+  tc_mbar_wait(bar, 0);
   {
     const float b = coldot(Lin, acc, part, false);
     if (tid < CT) base[tid] = b;
@@ -1848,6 +1877,7 @@ size_t chol_tc_ws_bytes(int npad) {
   const int64_t ntl = (int64_t)nt * (nt + 1) / 2;
   const int nb = (npad + SYB - 1) / SYB;
   return sizeof(float) * (size_t)ntl * TILE_F * 3                  // W + two image parts
+         + sizeof(float) * (size_t)5 * nt * TILE_F                  // folded solve matrices
          + sizeof(double) * ((size_t)npad * 4)                      // D, r, y, z
          + sizeof(double) * (size_t)nb * nb * SYB                   // symv partials
          + sizeof(int) * ((size_t)2 * nt * nt + 2 + 2 * (size_t)nt) + 256 * 10;
@@ -1861,7 +1891,7 @@ size_t chol_tc_ws_bytes(int npad) {
 // by at least 2 * iters between calls sharing `ws` (flag generations).
 int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b, double* x, void* ws,
                   const void* tasks, int ntasks, int iters, int* status, int gen, cudaStream_t st, double* out2,
-                  unsigned long long* trace) {
+                  unsigned long long* trace, cudaEvent_t* ev3) {
   const int nt = npad / CT;
   if (nt <= 0) return 0;
   const int64_t ntl = (int64_t)nt * (nt + 1) / 2;
@@ -1870,6 +1900,7 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
   auto take = [&](size_t bytes) { char* q = p; p += (bytes + 255) / 256 * 256; return q; };
   float* W = reinterpret_cast<float*>(take(sizeof(float) * ntl * TILE_F));
   float* img = reinterpret_cast<float*>(take(sizeof(float) * ntl * TILE_F * 2));
+  float* Fm = reinterpret_cast<float*>(take(sizeof(float) * (size_t)5 * nt * TILE_F));
   double* D = reinterpret_cast<double*>(take(sizeof(double) * npad));
   double* r = reinterpret_cast<double*>(take(sizeof(double) * npad));
   unsigned long long* y = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * npad));
@@ -1882,6 +1913,7 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
   if (grid == 0) {
     cudaFuncSetAttribute(k_chol_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM);
     cudaFuncSetAttribute(k_tc_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRI_SMEM);
+    cudaFuncSetAttribute(k_tc_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRI_SMEM);
     cudaFuncSetAttribute(k_tc_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRI_SMEM);
     int dev = 0, per = 0;
     cudaGetDevice(&dev);
@@ -1903,9 +1935,13 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
   a.ntasks = ntasks;
   a.status = status;
   a.trace = trace;
+  if (ev3) cudaEventRecord(ev3[0], st);
   k_chol_tc<<<ntasks < grid ? ntasks : grid, CHOL_THREADS, TC_SMEM, st>>>(a);
   launch_count();
   launch_count();
+  launch_count();
+  if (ev3) cudaEventRecord(ev3[1], st);
+  k_tc_prep<<<dim3(nt, 5), 256, TRI_SMEM, st>>>(W, nt, Fm);
   launch_count();
   cudaMemsetAsync(x, 0, sizeof(double) * npad, st);
   cudaMemsetAsync(stop, 0, sizeof(int), st);
@@ -1921,8 +1957,8 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
       launch_count();
       rhs = r;
     }
-    k_tc_fwd<<<nt, 256, TRI_SMEM, st>>>(W, nt, rhs, D, y, gen + 2 * it, stop);
-    k_tc_bwd<<<nt, 256, TRI_SMEM, st>>>(W, nt, y, z, D, x, out2, out2 + 1, gen + 2 * it, stop);
+    k_tc_fwd<<<nt, 256, TRI_SMEM, st>>>(W, Fm, nt, rhs, D, y, gen + 2 * it, stop);
+    k_tc_bwd<<<nt, 256, TRI_SMEM, st>>>(W, Fm, nt, y, z, D, x, out2, out2 + 1, gen + 2 * it, stop);
 #ifdef VBA_TRI_PROF
     if (it == 0) {
       unsigned long long h[2][4][256];
@@ -1930,7 +1966,7 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
       cudaMemcpyFromSymbol(h, g_tri_ts, sizeof(h));
       const unsigned long long t0 = h[0][0][0];
       for (int k = 0; k < nt; k += (nt > 20 ? 6 : 1))
-        fprintf(stderr, "fwd k=%2d start %7.1f ready %7.1f offchain %7.1f publish %7.1f us\n", k, (h[0][0][k] - t0) * 1e-3,
+        fprintf(stderr, "fwd k=%2d start %7.1f offchain-done %7.1f tiles-in %7.1f publish %7.1f us\n", k, (h[0][0][k] - t0) * 1e-3,
                 (h[0][1][k] - t0) * 1e-3, (h[0][2][k] - t0) * 1e-3, (h[0][3][k] - t0) * 1e-3);
     }
 #endif
@@ -1941,6 +1977,7 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
     launch_count();
     launch_count();
   }
+  if (ev3) cudaEventRecord(ev3[2], st);
   return 0;
 }
 

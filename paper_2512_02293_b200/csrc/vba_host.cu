@@ -152,6 +152,10 @@ struct Ctx {
   // profiling
   bool prof = false;
   cudaEvent_t ev[10] = {};
+  cudaEvent_t sev[3] = {};          // tensor-core solve: factor start, factor end, refinement end
+  bool sev_pending = false;
+  double solve_ms[2] = {0, 0};      // factorisation kernel, refinement passes
+  int64_t solve_samples = 0;
   double stage_ms[6] = {0, 0, 0, 0, 0, 0};
   int64_t k1_launches = 0;
   bool lin_pending = false;
@@ -450,7 +454,8 @@ static int build_plans(Ctx* c, cudaStream_t st) {
   int64_t work_px = 0;
   for (int n = 0; n < K; ++n)
     if (c->see[n] > c->seb[n] && P.h_npix[n] > 0) { ++nsrc; work_px += P.h_npix[n]; }
-  const int target = getenv("VBA_GRAM_TARGET") ? atoi(getenv("VBA_GRAM_TARGET")) : 2 * 148;
+  // ~7 waves of CTAs on 148 SMs (wave quantisation of the 1-CTA-per-SM Gram kernel)
+  const int target = getenv("VBA_GRAM_TARGET") ? atoi(getenv("VBA_GRAM_TARGET")) : 1024;
   c->goff.assign(K, 0);
   c->foff.assign(K, 0);
   c->g0.assign(K, 0);
@@ -582,6 +587,16 @@ static void prof_collect(Ctx* c, bool with_lin) {
   }
   for (int s = 0; s < 4; ++s)
     if (cudaEventElapsedTime(&ms, c->ev[2 + s], c->ev[3 + s]) == cudaSuccess) c->stage_ms[1 + s] += ms;
+  if (c->sev_pending) {
+    float f = 0.f, r = 0.f;
+    if (cudaEventElapsedTime(&f, c->sev[0], c->sev[1]) == cudaSuccess &&
+        cudaEventElapsedTime(&r, c->sev[1], c->sev[2]) == cudaSuccess) {
+      c->solve_ms[0] += f;
+      c->solve_ms[1] += r;
+      c->solve_samples += 1;
+    }
+    c->sev_pending = false;
+  }
 }
 
 static int stage_energy(Ctx* c, DevState& s, cudaStream_t st) {
@@ -650,7 +665,9 @@ static int stage_step(Ctx* c, double lam, cudaStream_t st) {
     }
     if (c->use_tc && !c->force_fp64 && !c->d_trace) {
       chol_tc_solve(c->d_H, c->npad, c->nfree, c->npad, c->d_rhs, c->d_x, c->d_tcws, c->d_tctasks, c->n_tctasks,
-                    c->tc_iters, &c->d_res->tc_bad, c->tc_gen, st, c->d_res->tc);
+                    c->tc_iters, &c->d_res->tc_bad, c->tc_gen, st, c->d_res->tc, nullptr,
+                    c->prof ? c->sev : nullptr);
+      c->sev_pending = c->prof;
       c->tc_gen += 2 * c->tc_iters;
     } else {
       chol_dag_launch(c->d_H, c->npad, c->nt, c->d_rhs, c->d_x, c->d_Ld, c->d_cpart, c->d_cflags, c->d_ctasks,
@@ -991,6 +1008,8 @@ int vba_destroy(void* ctx) {
   if (c->h_res) cudaFreeHost(c->h_res);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : c->sev)
+    if (e) cudaEventDestroy(e);
   delete c;
   return VBA_OK;
 }
@@ -1253,11 +1272,25 @@ int vba_export_step(void* ctx, void* stream, double* dx_full, double* dx_d) {
 
 int vba_set_profiling(void* ctx, int32_t on) {
   Ctx* c = (Ctx*)ctx;
-  if (on && !c->prof)
+  if (on && !c->ev[0]) {
     for (auto& e : c->ev) VBA_CUDA(cudaEventCreate(&e));
+    for (auto& e : c->sev) VBA_CUDA(cudaEventCreate(&e));
+  }
   c->prof = on != 0;
   for (double& v : c->stage_ms) v = 0.0;
   c->k1_launches = 0;
+  c->solve_ms[0] = c->solve_ms[1] = 0.0;
+  c->solve_samples = 0;
+  c->sev_pending = false;
+  return VBA_OK;
+}
+
+int vba_solve_times(void* ctx, double* out4) {
+  Ctx* c = (Ctx*)ctx;
+  out4[0] = c->solve_ms[0];
+  out4[1] = c->solve_ms[1];
+  out4[2] = (double)c->solve_samples;
+  out4[3] = (double)c->nfree;
   return VBA_OK;
 }
 

@@ -324,7 +324,7 @@ size_t chol_tc_ws_bytes(int npad);
 int chol_plan_tasks_tc(int nt, void* out, int cap);
 int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b, double* x, void* ws,
                   const void* tasks, int ntasks, int iters, int* status, int gen, cudaStream_t st, double* out2,
-                  unsigned long long* trace = nullptr);
+                  unsigned long long* trace = nullptr, cudaEvent_t* ev3 = nullptr);
 void chol_trace_print(const char* tag, const unsigned long long* d_trace, const void* d_tasks, int ntasks, int nt);
 // copy the task list back (for trace decoding): type,i,j,k per task
 void chol_task_fields(const void* tasks, int n, int* out4);

@@ -333,6 +333,18 @@ class DeviceProblem:
         return dict(zip(("linearize", "gram_fill", "assemble_chol", "backsub_retract", "energy", "k1_kernel",
                          "k1_launches"), list(out)))
 
+    def solve_times(self):
+        """Tensor-core reduced solve: factorisation / refinement ms, solves timed, n."""
+        out = (C.c_double * 4)()
+        L.check(self.lib.vba_solve_times(self.ctx, out))
+        return dict(zip(("factor_ms", "refine_ms", "solves", "n"), list(out)))
+
+    def stats(self):
+        """[tensor-core solve enabled, fp64 fallbacks, tensor-core solves, refinement passes]."""
+        out = (C.c_int64 * 4)()
+        L.check(self.lib.vba_stats(self.ctx, out))
+        return dict(zip(("tc_enabled", "fallbacks", "tc_solves", "refine_passes"), list(out)))
+
     def upload_inputs(self, H: "HostLayout" = None):
         """Re-upload the per-step inputs (host -> device copies of flow, weights,
         disparities, states, IMU records, gravity) from the host layout."""
