@@ -10,7 +10,7 @@ mkdir -p $out
 [ -n "$NOLAUNCH" ] || python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $out/ncu_plain_$tag.log 2>&1 || { echo "plain bench failed"; tail $out/ncu_plain_$tag.log; exit 1; }
 [ -n "$NOLAUNCH" ] || ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches_$tag.csv \
   python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $out/ncu_launch_$tag.log 2>&1
-specs=(${SPECS:-k1:regex:k_vision_stream.*bool.1 k2:regex:k_vision_stream.*bool.0 gram:regex:k_gram< chol:regex:k_chol_dag})
+specs=(${SPECS:-k1:regex:k_vision_stream.*bool.1 k2:regex:k_vision_stream.*bool.0 gram:regex:k_gram< chol:regex:k_chol_tc})
 for spec in "${specs[@]}"; do
   name=${spec%%:*}; filt=${spec#*:}
   ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "$filt" -s ${SKIP:-2} -c 1 \
