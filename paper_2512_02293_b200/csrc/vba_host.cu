@@ -413,10 +413,42 @@ static int build_plans(Ctx* c, cudaStream_t st) {
         c->chunks.push_back(a);
       }
     }
+    // Cost of an item = a fixed per-item part + its 64-pixel blocks holding any non-zero
+    // weight (K1 skips all-zero blocks, so invisible regions are nearly free); counted once
+    // per solve on the device from the caller's weights (tiles x out-edges = the K1 partials).
+    std::vector<int32_t> nzb((size_t)std::max<int64_t>(c->n_part, 1), kTileRt / 64);
+    if (c->n_part > 0 && c->P.wts) {
+      std::vector<int64_t> prow((size_t)c->n_part);
+      std::vector<int32_t> pcnt((size_t)c->n_part);
+      for (const PixTile& T : c->tiles)
+        for (int e = T.eb; e < T.ee; ++e) {
+          prow[T.poff + (e - T.eb)] = P.h_eoff[e] + T.n0;
+          pcnt[T.poff + (e - T.eb)] = T.cnt;
+        }
+      int64_t* d_prow = nullptr;
+      int32_t *d_pcnt = nullptr, *d_nz = nullptr;
+      if (cudaMalloc(&d_prow, sizeof(int64_t) * prow.size()) || cudaMalloc(&d_pcnt, sizeof(int32_t) * pcnt.size()) ||
+          cudaMalloc(&d_nz, sizeof(int32_t) * pcnt.size())) {
+        cudaFree(d_prow); cudaFree(d_pcnt); cudaFree(d_nz);
+        set_err("planner allocation failed");
+        return VBA_E_CUDA;
+      }
+      cudaMemcpyAsync(d_prow, prow.data(), sizeof(int64_t) * prow.size(), cudaMemcpyHostToDevice, st);
+      cudaMemcpyAsync(d_pcnt, pcnt.data(), sizeof(int32_t) * pcnt.size(), cudaMemcpyHostToDevice, st);
+      launch_count_nz_blocks(c->P.wts, d_prow, d_pcnt, (int)pcnt.size(),
+                             P.pixel_mode == VBA_PIX_GRID ? P.grid_w : 0, d_nz, st);
+      cudaMemcpyAsync(nzb.data(), d_nz, sizeof(int32_t) * pcnt.size(), cudaMemcpyDeviceToHost, st);
+      const cudaError_t err = cudaStreamSynchronize(st);
+      cudaFree(d_prow); cudaFree(d_pcnt); cudaFree(d_nz);
+      if (err != cudaSuccess) { set_err("planner: %s", cudaGetErrorString(err)); return VBA_E_CUDA; }
+    }
     std::vector<int32_t> order(c->chunks.size());
     for (int t = 0; t < (int)order.size(); ++t) order[t] = t;
-    auto work = [&](int t) {   // edge-pixels plus ~2 edges' worth of per-chunk setup
-      return (int64_t)(c->chunks[t].ee - c->chunks[t].eb + 2) * c->chunks[t].cnt;
+    auto work = [&](int t) {   // per item: ~10 blocks' worth of fixed cost + the non-zero blocks
+      const PixTile& T = c->chunks[t];
+      int64_t w = 2 * kTileRt / 64;   // per-chunk setup
+      for (int e = T.eb; e < T.ee; ++e) w += 10 + nzb[T.poff + (e - T.eb)];
+      return w;
     };
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return work(a) > work(b); });
     c->ncta = std::min<int>(G, (int)order.size());

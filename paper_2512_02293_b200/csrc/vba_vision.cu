@@ -233,11 +233,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // Pair index (within a whole-row grid tile of kTile pixels, grid width W) of
-// thread tid at step m: warp w covers block b = 4 m + w of 4 rows x 16 columns,
+// thread tid at step m: warp w covers block b = 4 m + (w + m) % 4 of 4 rows x 16 columns,
 // lane l the pixels (row 4 rb + l / 8, columns 16 cb + 2 (l % 8) + {0, 1}).  A
 // quarter-warp reads 8 consecutive float4 of one row (conflict-free).
 __device__ __forceinline__ int blk_pair(int m, int tid, int W) {
-  const int b = 4 * m + (tid >> 5), l = tid & 31;
+  // the 4 warps rotate over the 4 blocks of step m, so every warp visits every
+  // 16-column strip: invisible image strips (w = 0, skipped) are spread over the
+  // warps instead of idling some while others carry the whole item
+  const int b = 4 * m + (((tid >> 5) + m) & 3), l = tid & 31;
   const int cbw = W >> 4;
   const int rb = b / cbw, cb = b - rb * cbw;
   return ((4 * rb + (l >> 3)) * W + 16 * cb + 2 * (l & 7)) >> 1;
@@ -254,6 +257,11 @@ __device__ __forceinline__ float2 operator-(float2 a) { return make_float2(-a.x,
 // every upcoming tile without a global atomic on the critical path.
 #ifdef VBA_K1_TRACE   // tuning builds: cycles spent waiting for stages vs total, per warp
 __device__ unsigned long long g_k1_trace[4];
+__device__ unsigned long long g_k1_end[1024];   // per-CTA finish time (globaltimer)
+extern "C" __attribute__((visibility("default"))) void vba_k1_ends(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_k1_end, sizeof(g_k1_end));
+}
 extern "C" __attribute__((visibility("default"))) void vba_k1_trace(unsigned long long* out) {
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(out, g_k1_trace, sizeof(g_k1_trace));
@@ -410,10 +418,16 @@ __global__ void __launch_bounds__(kPixBlock, VBA_K1_MINB) k_vision_stream(
         // the arithmetic (bitwise identical result; the rows are still streamed)
 #if VBA_K1_SKIP == 1
         const bool nz = ((act >> m) & 1u) && (wl.x != 0.f || wl.y != 0.f || wl.z != 0.f || wl.w != 0.f);
+#ifdef VBA_K1_TRACE
+        if (LIN && lane == 0) atomicAdd(&g_k1_trace[3], __any_sync(0xffffffffu, nz) ? 0ull : 1ull);
+#endif
         if (!__any_sync(0xffffffffu, nz)) continue;
 #endif
 #ifdef VBA_K1_NOMATH   // tuning builds only: pipeline + reductions without the per-pixel arithmetic
         if (LIN) continue;
+#endif
+#ifdef VBA_K1_QUARTER  // tuning builds only: arithmetic of one pixel pair in four
+        if (LIN && m > 0) continue;
 #endif
         const float4 fl = S.flow[s][QP[m]];
         const float2 rx = RX[m], ry = RY[m], d = DD[m];
@@ -545,7 +559,46 @@ __global__ void __launch_bounds__(kPixBlock, VBA_K1_MINB) k_vision_stream(
     atomicAdd(&g_k1_trace[1], (unsigned long long)(clock64() - tk0));
     atomicAdd(&g_k1_trace[2], (unsigned long long)item);
   }
+  if (LIN && tid == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    g_k1_end[blockIdx.x] = t;
+  }
 #endif
+}
+
+// Planner helper: number of 64-pixel blocks with any non-zero weight per (tile, edge)
+// item, in K1's pixel -> warp mapping (4x16 blocks on whole-row grid tiles, else 64
+// consecutive pixels).  One warp per item.
+__global__ void k_count_nz_blocks(const float* __restrict__ wts, const int64_t* __restrict__ row0,
+                                  const int32_t* __restrict__ cnt, int n, int grid_w, int32_t* __restrict__ out) {
+  const int item = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (item >= n) return;
+  const int c = cnt[item];
+  const bool blk = grid_w > 0 && grid_w % 16 == 0 && kTile % (4 * grid_w) == 0 && c == kTile;
+  int nz = 0;
+  for (int b = 0; b < kTile / 64; ++b) {
+    int q;   // pair index of this lane in block b (as K1: block b = 4 m + warp)
+    if (blk) {   // block index b is a position in the tile; the counts do not depend on which warp
+      const int cbw = grid_w >> 4, rb = b / cbw, cb = b - rb * cbw;
+      q = ((4 * rb + (lane >> 3)) * grid_w + 16 * cb + 2 * (lane & 7)) >> 1;
+    } else {
+      q = (b >> 2) * kPixBlock + (b & 3) * 32 + lane;
+    }
+    bool any = false;
+    if (2 * q < c) {
+      const float4 w = __ldg(reinterpret_cast<const float4*>(wts + 2 * (row0[item] + 2 * q)));
+      any = w.x != 0.f || w.y != 0.f || w.z != 0.f || w.w != 0.f;
+    }
+    nz += __any_sync(0xffffffffu, any) ? 1 : 0;
+  }
+  if (lane == 0) out[item] = nz;
+}
+void launch_count_nz_blocks(const float* wts, const int64_t* row0, const int32_t* cnt, int n, int grid_w,
+                            int32_t* out, cudaStream_t st) {
+  if (n <= 0) return;
+  k_count_nz_blocks<<<(n + 7) / 8, 256, 0, st>>>(wts, row0, cnt, n, grid_w, out);
+  launch_count();
 }
 
 // CTAs of the streamed kernels (SMs x resident CTAs of the K1 instance; the
