@@ -120,6 +120,8 @@ struct Ctx {
   int* d_cflags = nullptr;         // Cholesky DAG counters
   void* d_ctasks = nullptr;        // Cholesky task list
   int n_ctasks = 0;
+  float* d_raytab = nullptr;       // VBA_PIX_GRID: per-column / per-row rays (replaces P.pix)
+  const float* pix = nullptr;      // pixel argument of the per-pixel kernels
   void* d_tcws = nullptr;          // tensor-core (3xTF32 + fp64 refinement) solve workspace
   void* d_tctasks = nullptr;       // its task DAG (DIAG-fused critical chain)
   int n_tctasks = 0;
@@ -633,7 +635,7 @@ static void prof_collect(Ctx* c, bool with_lin) {
 
 static int stage_energy(Ctx* c, DevState& s, cudaStream_t st) {
   launch_edge_prep(s, c->d_ei, c->d_ej, c->E, c->extr, st);
-  launch_vision_energy(c->P.pixel_mode, c->d_chunks, c->d_soff, c->d_sids, c->d_sitems, c->d_ioff, c->ncta, s, c->P.pix, c->P.tgt, c->P.wts,
+  launch_vision_energy(c->P.pixel_mode, c->d_chunks, c->d_soff, c->d_sids, c->d_sitems, c->d_ioff, c->ncta, s, c->pix, c->P.tgt, c->P.wts,
                        c->d_eoff, c->d_doff, c->P.grid_w, c->grid, c->intr, c->d_tile_e, st);
   launch_imu_factor(c->P.imu, c->d_L, c->d_fi, c->d_fj, c->F, s, c->P.ts, c->sdof, c->ibs, 1,
                     c->d_arena + c->arena_imu, st);
@@ -653,7 +655,7 @@ static int stage_linearize(Ctx* c, cudaStream_t st) {
   }
   launch_edge_prep(s, c->d_ei, c->d_ej, c->E, c->extr, st);
   mark(c, 8, st);
-  launch_vision_linearize(c->P.pixel_mode, c->d_chunks, c->d_soff, c->d_sids, c->d_sitems, c->d_ioff, c->ncta, s, c->P.pix, c->P.tgt, c->P.wts,
+  launch_vision_linearize(c->P.pixel_mode, c->d_chunks, c->d_soff, c->d_sids, c->d_sitems, c->d_ioff, c->ncta, s, c->pix, c->P.tgt, c->P.wts,
                           c->d_eoff, c->d_doff, c->P.grid_w, c->grid, c->intr, c->d_part, c->d_Hdd, c->d_gd, st);
   mark(c, 9, st);
   launch_edge_finalize(c->d_t0s, c->d_t1s, c->d_tiles, c->d_ei, c->E, c->d_part, s, c->extr,
@@ -672,7 +674,7 @@ static int stage_step(Ctx* c, double lam, cudaStream_t st) {
   VBA_CUDA(cudaMemsetAsync(c->d_res, 0, sizeof(Result), st));
   if (!c->gtiles.empty()) {
     launch_gram(c->P.pixel_mode, c->d_gtiles, (int)c->gtiles.size(), kGramBlock, c->gram_smem, c->kmax, s,
-                c->P.pix, c->P.wts, c->d_eoff, c->d_doff, c->P.grid_w, c->grid, c->intr, c->d_Hdd, c->d_gd, lam,
+                c->pix, c->P.wts, c->d_eoff, c->d_doff, c->P.grid_w, c->grid, c->intr, c->d_Hdd, c->d_gd, lam,
                 c->O.ridge, c->d_gram_part, st);
     launch_gram_reduce(c->d_gsrc, (int)c->gsrc.size(), c->d_g0, c->d_g1, c->d_gtiles, c->d_seb, c->d_see,
                        c->d_goff, c->d_gram_part, c->d_gram, st);
@@ -709,7 +711,7 @@ static int stage_step(Ctx* c, double lam, cudaStream_t st) {
   mark(c, 4, st);
   launch_scatter_dx(c->d_x, c->d_fmap, c->npv, c->d_dx, st);
   launch_step_edges(c->d_ei, c->d_ej, c->E, s, c->extr, c->d_dx, c->sdof, c->d_ustep, st);
-  launch_backsub(c->P.pixel_mode, c->d_tiles, (int)c->tiles.size(), s, n, c->P.pix, c->P.wts, c->d_eoff,
+  launch_backsub(c->P.pixel_mode, c->d_tiles, (int)c->tiles.size(), s, n, c->pix, c->P.wts, c->d_eoff,
                  c->d_doff, c->P.grid_w, c->grid, c->intr, c->d_Hdd, c->d_gd, c->d_ustep, lam, c->O.ridge,
                  c->d_dxd, &c->d_res->step_bits, st);
   launch_retract(s, n, c->d_dx, c->d_frozen, c->K, c->sdof, c->ngrav, c->n_state, &c->d_res->step_bits, c->npv, st);
@@ -786,7 +788,7 @@ static int stage_step_dense(Ctx* c, double lam, cudaStream_t st) {
   }
   HpdOut o{c->d_D, c->dn_npad, c->nfree, c->sdof, c->d_kfcol, c->d_Hdd, c->d_gd, c->d_drhs, lam, c->O.ridge};
   launch_export_hpd(c->P.pixel_mode, c->d_seb, c->d_see, c->d_doff, c->d_roff_real, c->d_npix, c->maxpix, c->d_ej,
-                    c->K, s, c->extr, c->P.pix, c->P.wts, c->d_eoff, c->P.grid_w, c->grid, c->intr, o, st);
+                    c->K, s, c->extr, c->pix, c->P.wts, c->d_eoff, c->P.grid_w, c->grid, c->intr, o, st);
   chol_dag_launch(c->d_D, c->dn_npad, c->dn_nt, c->d_drhs, c->d_dx2, c->d_dLinv, c->d_dpart, c->d_dflags,
                   c->d_dtasks, c->n_dtasks, &c->d_res->status, st);
   mark(c, 4, st);
@@ -975,6 +977,15 @@ int vba_create(void** out, const vba_problem* prob, const vba_options* opts, voi
       (rc = dalloc(c, &c->d_dx, (size_t)c->npv)) || (rc = dalloc(c, &c->d_res, 1)))
     return fail(rc);
   if (cudaMallocHost((void**)&c->h_res, sizeof(Result)) != cudaSuccess) { set_err("pinned alloc failed"); return fail(VBA_E_CUDA); }
+  c->pix = prob->pix;
+  if (prob->pixel_mode == VBA_PIX_GRID) {   // ray table: columns, then rows up to the longest segment
+    int64_t maxpad = 0;
+    for (int n = 0; n < c->K; ++n) maxpad = std::max<int64_t>(maxpad, prob->h_doff[n + 1] - prob->h_doff[n]);
+    const int rows = (int)((maxpad + prob->grid_w - 1) / prob->grid_w) + 1;
+    if ((rc = dalloc(c, &c->d_raytab, (size_t)prob->grid_w + rows))) return fail(rc);
+    launch_ray_table(c->d_raytab, prob->grid_w, rows, c->grid, c->intr, st);
+    c->pix = c->d_raytab;
+  }
   {
     // tensor-core reduced solve for large reduced systems (its fixed costs -- refinement
     // passes, extra launches -- lose to the fp64 DAG below ~32 tiles, n ~ 4000);
@@ -1284,7 +1295,7 @@ int vba_export_normal_eq(void* ctx, void* stream, double* H_pp, double* g_p, dou
     VBA_CUDA(cudaMemsetAsync(H_pd, 0, sizeof(double) * c->npv * std::max<int64_t>(1, c->n_real), st));
     HpdOut o{H_pd, c->n_real, 0, c->sdof, nullptr, nullptr, nullptr, nullptr, 0.0, 0.0};
     launch_export_hpd(c->P.pixel_mode, c->d_seb, c->d_see, c->d_doff, c->d_roff_real, c->d_npix, c->maxpix, c->d_ej,
-                      c->K, s, c->extr, c->P.pix, c->P.wts, c->d_eoff, c->P.grid_w, c->grid, c->intr, o, st);
+                      c->K, s, c->extr, c->pix, c->P.wts, c->d_eoff, c->P.grid_w, c->grid, c->intr, o, st);
   }
   VBA_CUDA(cudaStreamSynchronize(st));
   return VBA_OK;

@@ -261,6 +261,7 @@ void launch_edge_prep(const DevState& s, const int32_t* ei, const int32_t* ej, i
 // Streamed K1 / K2: CTA b processes tiles sids[soff[b] .. soff[b+1]) whose (tile, edge)
 // items are items[ioff[b] .. ioff[b+1]); ncta = vision_stream_ctas()
 int vision_stream_ctas();
+void launch_ray_table(float* tab, int W, int rows, const double* grid, const double* intr, cudaStream_t st);
 void launch_count_nz_blocks(const float* wts, const int64_t* row0, const int32_t* cnt, int n, int grid_w,
                             int32_t* out, cudaStream_t st);
 void launch_vision_linearize(int pixel_mode, const PixTile* tiles, const int32_t* soff, const int32_t* sids,

@@ -51,16 +51,39 @@ __device__ __forceinline__ void load_rays(const float* __restrict__ pix, int64_t
                                           float& rx1, float& ry1) {
   double u0, v0, u1, v1;
   if (MODE == VBA_PIX_GRID) {
+    // `pix` is the ray table of the grid (k_ray_table: the same fp64 expression as
+    // below, evaluated once per column / row): [grid_w column rays | row rays]
     const int c0 = n % grid_w, r0 = n / grid_w;
     const int c1 = (n + 1) % grid_w, r1 = (n + 1) / grid_w;
-    u0 = gp.ox + gp.sx * c0; v0 = gp.oy + gp.sy * r0;
-    u1 = gp.ox + gp.sx * c1; v1 = gp.oy + gp.sy * r1;
+    rx0 = __ldg(pix + c0); ry0 = __ldg(pix + grid_w + r0);
+    rx1 = __ldg(pix + c1); ry1 = __ldg(pix + grid_w + r1);
+    return;
   } else {
     const float4 p = __ldg(reinterpret_cast<const float4*>(pix + 2 * (kbase + n)));
     u0 = p.x; v0 = p.y; u1 = p.z; v1 = p.w;
   }
   rx0 = (float)((u0 - in.cx) / in.fx); ry0 = (float)((v0 - in.cy) / in.fy);
   rx1 = (float)((u1 - in.cx) / in.fx); ry1 = (float)((v1 - in.cy) / in.fy);
+}
+
+// Ray table of a regular pixel grid: column c -> (float)((ox + sx c - cx) / fx),
+// row r -> (float)((oy + sy r - cy) / fy), in fp64 then rounded (the per-pixel
+// kernels read it instead of recomputing the fp64 division per pixel).
+__global__ void k_ray_table(float* __restrict__ tab, int W, int rows, GridP gp, IntrP in) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < W) {
+    const double u = gp.ox + gp.sx * i;
+    tab[i] = (float)((u - in.cx) / in.fx);
+  } else if (i < W + rows) {
+    const double v = gp.oy + gp.sy * (i - W);
+    tab[i] = (float)((v - in.cy) / in.fy);
+  }
+}
+void launch_ray_table(float* tab, int W, int rows, const double* grid, const double* intr, cudaStream_t st) {
+  GridP gp{grid[0], grid[1], grid[2], grid[3]};
+  IntrP in{intr[0], intr[1], intr[2], intr[3]};
+  k_ray_table<<<(W + rows + 255) / 256, 256, 0, st>>>(tab, W, rows, gp, in);
+  launch_count();
 }
 
 // 1/x on the MUFU (<= 1 ulp); every per-pixel kernel projects with it so K1,
