@@ -41,7 +41,7 @@ static void set_err(const char* fmt, ...) {
     }                                                                                   \
   } while (0)
 
-constexpr int kTileRt = 1024;   // pixels per per-pixel work tile (kPixBlock * 2 * kTP)
+constexpr int kTileRt = kTilePx;   // pixels per per-pixel work tile (vba_internal.cuh)
 constexpr int kGramBlock = 512;
 constexpr int kMaxOutDegree = 31;
 constexpr int NBc = 128;         // Cholesky tile (vba_chol.cu)

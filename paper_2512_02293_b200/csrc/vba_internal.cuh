@@ -13,6 +13,10 @@
 
 namespace vba {
 
+#ifndef VBA_TP
+#define VBA_TP 4                          // pixel pairs per thread of the per-pixel kernels
+#endif
+constexpr int kTilePx = 2 * VBA_TP * 128;   // pixels per per-pixel work tile (128-thread CTAs)
 constexpr double kSmallAngle = 1e-8;
 constexpr float kDispFloor = 1e-4f;      // solver.py:32
 constexpr int kPartWarps = 4;            // warps of the K1 CTA, one fp32 32-vector each

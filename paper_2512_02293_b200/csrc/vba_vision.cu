@@ -24,8 +24,9 @@ void launch_count() { ++g_launches; }
 int64_t launch_total() { return g_launches; }
 
 constexpr int kPixBlock = 128;   // threads of the per-pixel kernels
-constexpr int kTP = 4;           // pixel pairs per thread (8 pixels)
+constexpr int kTP = VBA_TP;      // pixel pairs per thread
 constexpr int kTile = 2 * kTP * kPixBlock;
+static_assert(kTile == kTilePx, "tile size shared with the host planner");
 constexpr int kGramPC = 32;      // pixels per Gram staging chunk
 constexpr int kGramStride = 12;  // floats per (pixel, edge) in the Gram stage: u[6] v[6]
 
