@@ -25,8 +25,9 @@ __global__ void __launch_bounds__(256) k_assemble(const int32_t* __restrict__ bp
                                                   const Contrib* __restrict__ cs, int nbr,
                                                   const int32_t* __restrict__ roff, const int32_t* __restrict__ rdim,
                                                   const double* __restrict__ arena, double lam, double ridge,
-                                                  int add_ridge, double* __restrict__ H, int64_t ld, int sym) {
-  const int64_t id = blockIdx.x;
+                                                  int add_ridge, double* __restrict__ H, int64_t ld, int sym,
+                                                  const int32_t* __restrict__ blist) {
+  const int64_t id = blist ? blist[blockIdx.x] : blockIdx.x;   // blist: blocks with contributions
   int a = (int)((sqrt(8.0 * (double)id + 1.0) - 1.0) * 0.5);
   while ((int64_t)(a + 1) * (a + 2) / 2 <= id) ++a;
   while ((int64_t)a * (a + 1) / 2 > id) --a;
@@ -60,11 +61,11 @@ __global__ void __launch_bounds__(256) k_assemble(const int32_t* __restrict__ bp
 
 void launch_assemble(const int32_t* bptr, const int32_t* bnff, const Contrib* cs, int nbr, const int32_t* roff,
                      const int32_t* rdim, const double* arena, double lam, double ridge, int add_ridge, double* H,
-                     int64_t ld, int sym, cudaStream_t st) {
-  const int64_t nblk = (int64_t)nbr * (nbr + 1) / 2;
+                     int64_t ld, int sym, cudaStream_t st, const int32_t* blist, int nblist) {
+  const int64_t nblk = blist ? (int64_t)nblist : (int64_t)nbr * (nbr + 1) / 2;
   if (nblk <= 0) return;
   k_assemble<<<(unsigned)nblk, 256, 0, st>>>(bptr, bnff, cs, nbr, roff, rdim, arena, lam, ridge, add_ridge, H, ld,
-                                             sym);
+                                             sym, blist);
   launch_count();
 }
 

@@ -113,6 +113,8 @@ struct Ctx {
     Contrib* cs = nullptr;
     int32_t *sptr = nullptr, *soff = nullptr;   // soff: [nseg offsets][nseg dims]
     Vec* vs = nullptr;
+    int32_t* blist = nullptr;                    // lower blocks with contributions (+ diagonal)
+    int nblist = 0;
   } red, exp;
   bool exp_built = false;
   double *d_H = nullptr, *d_rhs = nullptr, *d_x = nullptr, *d_Ld = nullptr, *d_dx = nullptr;
@@ -268,7 +270,16 @@ static int upload_plan(Ctx* c, BlkBuilder& B, const std::vector<int32_t>& roff, 
   }
   soff = roff;
   soff.insert(soff.end(), rdim.begin(), rdim.end());
+  std::vector<int32_t> blist;
+  {
+    int64_t id = 0;
+    for (int a = 0; a < B.nbr; ++a)
+      for (int b = 0; b <= a; ++b, ++id)
+        if (a == b || bptr[id + 1] > bptr[id]) blist.push_back((int32_t)id);
+  }
+  pl.nblist = (int)blist.size();
   int rc;
+  if ((rc = dupload(c, &pl.blist, blist, st))) return rc;
   if ((rc = dupload(c, &pl.bptr, bptr, st)) || (rc = dupload(c, &pl.bnff, bnff, st)) ||
       (rc = dupload(c, &pl.cs, cs, st)) || (rc = dupload(c, &pl.roff, roff, st)) ||
       (rc = dupload(c, &pl.rdim, rdim, st)) || (rc = dupload(c, &pl.sptr, sptr, st)) ||
@@ -684,8 +695,12 @@ static int stage_step(Ctx* c, double lam, cudaStream_t st) {
   mark(c, 3, st);
   if (c->nfree > 0) {
     const bool multi = c->coll != nullptr;
+    // single GPU: only the blocks with contributions are written (the others stay at the
+    // zeros of vba_create); ranks of a sharded solve rewrite every block (the in-place
+    // all-reduce leaves sums in their buffers).  Both solves read the lower triangle only.
     launch_assemble(c->red.bptr, c->red.bnff, c->red.cs, c->red.nbr, c->red.roff, c->red.rdim, c->d_arena, lam,
-                    c->O.ridge, multi ? 0 : 1, c->d_H, c->npad, 0, st);
+                    c->O.ridge, multi ? 0 : 1, c->d_H, c->npad, 0, st, multi ? nullptr : c->red.blist,
+                    c->red.nblist);
     // right-hand side -g_red: the step solves H_red dx = -g_red (solver.py:287)
     launch_assemble_vec(c->red.sptr, c->red.vs, c->red.nseg, c->red.soff, c->d_arena, -1.0, c->d_rhs, st);
     if (multi) {

@@ -311,8 +311,9 @@ void launch_imu_factor(const double* imu, const double* Lbuf, const int32_t* fi,
                        double* imu_blocks, cudaStream_t st);
 // dense
 void launch_assemble(const int32_t* blk_ptr, const int32_t* blk_nff, const Contrib* contribs, int nblk_rows,
-                     const int32_t* blk_row_off, const int32_t* blk_dim, const double* arena, double lam,
-                     double ridge, int add_ridge, double* H, int64_t ld, int symmetric_out, cudaStream_t st);
+                     const int32_t* roff, const int32_t* rdim, const double* arena, double lam, double ridge,
+                     int add_ridge, double* H, int64_t ld, int sym, cudaStream_t st, const int32_t* blist = nullptr,
+                     int nblist = 0);
 void launch_assemble_vec(const int32_t* seg_ptr, const Vec* vecs, int nseg, const int32_t* seg_off,
                          const double* arena, double scale, double* g, cudaStream_t st, int skip_fill = 0);
 void launch_add_ridge(double* H, int64_t ld, int n, double ridge, cudaStream_t st);

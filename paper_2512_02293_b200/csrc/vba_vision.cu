@@ -1231,6 +1231,17 @@ __global__ void k_retract(const double* __restrict__ cur, double* __restrict__ n
                           const double* __restrict__ gcur, double* __restrict__ gnxt,
                           unsigned long long* __restrict__ step_bits, int npv) {
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  // max |dx_full| over this thread's slice (sdof entries; the last thread also the
+  // gravity columns), then a warp max and one integer atomicMax per warp (the bit
+  // patterns of non-negative doubles order like the values: order-independent)
+  double mx = 0.0;
+  if (n < K)
+    for (int k = 0; k < sdof; ++k) mx = fmax(mx, fabs(dx[(int64_t)sdof * n + k]));
+  if (n == K)
+    for (int i = n_state; i < npv; ++i) mx = fmax(mx, fabs(dx[i]));
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx > 0.0) atomicMax(step_bits, (unsigned long long)__double_as_longlong(mx));
   if (n < K) {
     const double* s = cur + 16 * n;
     double* o = nxt + 16 * n;
@@ -1256,7 +1267,7 @@ __global__ void k_retract(const double* __restrict__ cur, double* __restrict__ n
       }
     }
   }
-  if (n == K) {  // gravity (+ the |dx_full| max, thread-serial: npv is small)
+  if (n == K) {  // gravity
     for (int k = 0; k < 5; ++k) gnxt[k] = gcur[k];
     if (ngrav) {
       const double w[3] = {dx[n_state], dx[n_state + 1], 0.0};   // GRAVITY_TANGENT_BASIS @ dg
@@ -1266,9 +1277,6 @@ __global__ void k_retract(const double* __restrict__ cur, double* __restrict__ n
       qcanon(qn);
       for (int k = 0; k < 4; ++k) gnxt[k] = qn[k];
     }
-    double mx = 0.0;
-    for (int i = 0; i < npv; ++i) mx = fmax(mx, fabs(dx[i]));
-    if (mx > 0.0) atomicMax(step_bits, (unsigned long long)__double_as_longlong(mx));
   }
 }
 
