@@ -881,7 +881,7 @@ __device__ void tc_task_gemm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
 
 // TRSM(i,k):  L_ik = W_ik Linv_kk^T   (A = W_ik split by the threads, B = Linv images)
 __device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_t& nacc, uint32_t tmem, int i,
-                             int k) {
+                             int k, bool keep_smem = false) {
   const int tid = threadIdx.x;
   const float* Wik = a.W + tlin(i, k) * TILE_F;
   const float* ib = a.img + tlin(k, k) * 2 * TILE_F;
@@ -956,9 +956,65 @@ __device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
       const int off = img_off(row, c0 + 32 * h + 4 * q);
       __stcg(reinterpret_cast<float4*>(ihi + off), hh);
       __stcg(reinterpret_cast<float4*>(ilo + off), ll);
+      if (keep_smem) {   // chunk images also into the ring: chunk ch at 2 ch TCHUNK (hi), + TCHUNK (lo)
+        const int cc = c0 + 32 * h + 4 * q, ch = cc >> 5, o2 = off - ch * (CT * TKC);
+        float* sh = reinterpret_cast<float*>(R.base + (size_t)2 * ch * TCHUNK);
+        *reinterpret_cast<float4*>(sh + o2) = hh;
+        *reinterpret_cast<float4*>(sh + CT * TKC + o2) = ll;
+      }
     }
   }
   tc_fence_before();
+  if (keep_smem) {
+    proxy_fence_shared();   // generic writes -> tcgen05 operand reads
+    __syncthreads();
+  }
+}
+
+// Diagonal SYRK of DIAG(k): W_{k+1,k+1} -= L L^T with L = L_{k+1,k} already in shared
+// memory as chunk images (tc_task_trsm keep_smem): A and B descriptors share them.
+__device__ void tc_task_syrk_smem(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_t& nacc, uint32_t tmem,
+                                  int i) {
+  const int tid = threadIdx.x;
+  const int w = tid >> 5, lane = tid & 31;
+  const int row = 32 * (w & 3) + lane, c0 = 64 * (w >> 2);
+  float4* C4 = reinterpret_cast<float4*>(a.W + tlin(i, i) * TILE_F + (int64_t)row * CT + c0);
+  float4 o[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) o[q] = __ldcg(C4 + q);
+  if (tid == 0) {
+    tc_fence_after();
+    for (int ch = 0; ch < TNCH; ++ch) {
+      const uint32_t hi = su32(R.base + (size_t)2 * ch * TCHUNK), lo = hi + TCHUNK;
+#pragma unroll
+      for (int kk = 0; kk < TKC / 8; ++kk) {
+        const uint32_t off = 32u * kk;
+        tc_mma(tmem, tc_sdesc(hi + off), tc_sdesc(hi + off), (ch == 0 && kk == 0) ? 0u : 1u);
+        tc_mma(tmem, tc_sdesc(hi + off), tc_sdesc(lo + off), 1u);
+        tc_mma(tmem, tc_sdesc(lo + off), tc_sdesc(hi + off), 1u);
+      }
+    }
+    tc_commit(accf);
+  }
+  tc_mbar_wait(accf, nacc & 1);
+  ++nacc;
+  tc_fence_after();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float v[32];
+    tmem_ld32(tmem + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)(c0 + 32 * h), v);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float4 t = o[8 * h + q];
+      t.x -= v[4 * q];
+      t.y -= v[4 * q + 1];
+      t.z -= v[4 * q + 2];
+      t.w -= v[4 * q + 3];
+      __stcg(C4 + 8 * h + q, t);
+    }
+  }
+  tc_fence_before();
+  proxy_fence_shared();   // the ring is refilled by bulk copies after these generic writes
 }
 
 // ---------------------------------------------------------------------------
@@ -1364,14 +1420,14 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
         if (k + 1 < nt) {
           wait_geq(&a.upd[(k + 1) * nt + k], k);
           __syncthreads();
-          tc_task_trsm(a, R, &accf, nacc, tmem, k + 1, k);
+          tc_task_trsm(a, R, &accf, nacc, tmem, k + 1, k, true);
           proxy_fence_global();
           __threadfence();
           __syncthreads();
           if (tid == 0) st_release(&a.done[(k + 1) * nt + k], 1);
           wait_geq(&a.upd[(k + 1) * nt + k + 1], k);
           __syncthreads();
-          tc_task_gemm(a, R, &accf, nacc, tmem, k + 1, k + 1, k, -1);
+          tc_task_syrk_smem(a, R, &accf, nacc, tmem, k + 1);
           __threadfence();
           __syncthreads();
           if (tid == 0) st_release(&a.upd[(k + 1) * nt + k + 1], k + 1);
