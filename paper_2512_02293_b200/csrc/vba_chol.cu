@@ -1145,8 +1145,8 @@ __device__ __forceinline__ void blk32_gemm(float* C, const float* A, int ars, in
 }
 
 // 8x8 Cholesky + inverse of the diagonal block at (c0, c0) by ONE thread in
-// registers (no barriers): L overwrites the block of Ws (upper part zeroed), the
-// inverse goes to the same block of Xf.  Both column-major, stride SWF.
+// registers (no barriers): L overwrites the block of Ws (column-major, upper part
+// zeroed), the inverse goes to the same block of Xf (row-major).  Stride SWF.
 __device__ __forceinline__ void diag8(float* Ws, float* Xf, int c0, int* bad) {
   float l[8][8], x[8][8];
 #pragma unroll
@@ -1184,7 +1184,7 @@ __device__ __forceinline__ void diag8(float* Ws, float* Xf, int c0, int* bad) {
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       Ws[(c0 + c) * SWF + c0 + r] = l[r][c];
-      Xf[(c0 + c) * SWF + c0 + r] = x[r][c];
+      Xf[(c0 + r) * SWF + c0 + c] = x[r][c];
     }
 }
 
@@ -1201,7 +1201,7 @@ __device__ __forceinline__ void diag8(float* Ws, float* Xf, int c0, int* bad) {
 // diagonal, for the triangular solves) and to its hi/lo images (TRSM operand).
 __device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d) {
   float* Ws = reinterpret_cast<float*>(smem_d);   // tile, then L (column-major, SWF)
-  float* Xf = Ws + CT * SWF;                      // Y -> Linv (column-major, SWF)
+  float* Xf = Ws + CT * SWF;                      // Y -> Linv (row-major, SWF)
   __shared__ int bad;
   const int tid = threadIdx.x;
   float* Wk = a.W + tlin(k, k) * TILE_F;
@@ -1243,20 +1243,20 @@ __device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d) {
       for (int c = 0; c < 8; ++c) {
         float sum = 0.f;
 #pragma unroll
-        for (int m = 0; m <= c; ++m) sum = fmaf(av[m], Xf[(c0 + m) * SWF + c0 + c], sum);
+        for (int m = 0; m <= c; ++m) sum = fmaf(av[m], Xf[(c0 + c) * SWF + c0 + m], sum);
         Ws[(c0 + c) * SWF + r] = sum;
       }
     } else if (tid >= 128 && tid - 128 < c0) {   // Y_s[:, c] <- X_ss Y_s[:, c] for columns c < c0
       const int c = tid - 128;
       float yv[8];
 #pragma unroll
-      for (int m = 0; m < 8; ++m) yv[m] = Xf[c * SWF + c0 + m];
+      for (int m = 0; m < 8; ++m) yv[m] = Xf[(c0 + m) * SWF + c];
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
         float sum = 0.f;
 #pragma unroll
-        for (int m = 0; m <= r; ++m) sum = fmaf(Xf[(c0 + m) * SWF + c0 + r], yv[m], sum);
-        Xf[c * SWF + c0 + r] = sum;
+        for (int m = 0; m <= r; ++m) sum = fmaf(Xf[(c0 + r) * SWF + c0 + m], yv[m], sum);
+        Xf[(c0 + r) * SWF + c] = sum;
       }
     }
     __syncthreads();
@@ -1277,8 +1277,10 @@ __device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d) {
         int rb = (int)((sqrtf(8.f * b + 1.f) - 1.f) * 0.5f);
         while ((rb + 1) * (rb + 2) / 2 <= b) ++rb;
         while (rb * (rb + 1) / 2 > b) --rb;
-        const int cbk = b - rb * (rb + 1) / 2;
-        const int r = r0 + 4 * rb, c = r0 + 4 * cbk;
+        // mirrored so that consecutive b (lanes) walk down a block column: contiguous
+        // float4 rows of the column-major tile, conflict-free
+        const int cbk = nb4 - 1 - rb, rbk = nb4 - 1 - (b - rb * (rb + 1) / 2);
+        const int r = r0 + 4 * rbk, c = r0 + 4 * cbk;
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
           const float4 lr = *reinterpret_cast<const float4*>(Ws + (c0 + m) * SWF + r);
@@ -1303,19 +1305,18 @@ __device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d) {
         for (int m = 0; m < 8; ++m) {
           const float4 lr = *reinterpret_cast<const float4*>(Ws + (c0 + m) * SWF + r);
           const float ra[4] = {lr.x, lr.y, lr.z, lr.w};
-          float ya[4];
-#pragma unroll
-          for (int v = 0; v < 4; ++v) ya[v] = Xf[(c + v) * SWF + c0 + m];
+          const float4 yc = *reinterpret_cast<const float4*>(Xf + (c0 + m) * SWF + c);
+          const float ya[4] = {yc.x, yc.y, yc.z, yc.w};
 #pragma unroll
           for (int u = 0; u < 4; ++u)
 #pragma unroll
             for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(ra[u], ya[v], acc[u][v]);
         }
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          float4* d = reinterpret_cast<float4*>(Xf + (c + v) * SWF + r);
+        for (int u = 0; u < 4; ++u) {
+          float4* d = reinterpret_cast<float4*>(Xf + (r + u) * SWF + c);
           float4 o = *d;
-          o.x -= acc[0][v]; o.y -= acc[1][v]; o.z -= acc[2][v]; o.w -= acc[3][v];
+          o.x -= acc[u][0]; o.y -= acc[u][1]; o.z -= acc[u][2]; o.w -= acc[u][3];
           *d = o;
         }
       }
@@ -1332,10 +1333,9 @@ __device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d) {
   float* ilo = ihi + TILE_F;
   for (int t4 = tid; t4 < CT * CT / 4; t4 += CHOL_THREADS) {
     const int r = t4 / (CT / 4), c = 4 * (t4 % (CT / 4));
-    float v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = (c + u <= r) ? Xf[(c + u) * SWF + r] : 0.f;
-    const float4 x = make_float4(v[0], v[1], v[2], v[3]);
+    const float4 y = *reinterpret_cast<const float4*>(Xf + r * SWF + c);
+    const float4 x = make_float4(c <= r ? y.x : 0.f, c + 1 <= r ? y.y : 0.f, c + 2 <= r ? y.z : 0.f,
+                                 c + 3 <= r ? y.w : 0.f);
     __stcg(reinterpret_cast<float4*>(Wk + r * CT + c), x);
     float4 hh, ll;
     hh.x = tf32_rna(x.x); ll.x = tf32_rna(x.x - hh.x);
