@@ -1224,15 +1224,55 @@ __device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d) {
   }
   __syncthreads();
   if (ph && tid == 0) ph[1] = ph[2] = gtimer();
+  // 4x4 register-blocked rank-8 updates of panel c0 (L columns c0..c0+7 of Ws):
+  //   A block (rows r.., cols c.., r0 <= c <= r):  A[r][c] -= sum_m L[r][c0+m] L[c][c0+m]
+  //   Y block (rows r >= r0, cols c < r0):          Y[r][c] -= sum_m L[r][c0+m] Y[c0+m][c]
+  auto ablock = [&](int c0, int r, int c) {
+    float acc[4][4] = {};
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const float4 lr = *reinterpret_cast<const float4*>(Ws + (c0 + m) * SWF + r);
+      const float4 lc = *reinterpret_cast<const float4*>(Ws + (c0 + m) * SWF + c);
+      const float ra[4] = {lr.x, lr.y, lr.z, lr.w}, ca[4] = {lc.x, lc.y, lc.z, lc.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(ra[u], ca[v], acc[u][v]);
+    }
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      float4* d = reinterpret_cast<float4*>(Ws + (c + v) * SWF + r);
+      float4 o = *d;
+      o.x -= acc[0][v]; o.y -= acc[1][v]; o.z -= acc[2][v]; o.w -= acc[3][v];
+      *d = o;
+    }
+  };
+  auto yblock = [&](int c0, int r, int c) {
+    float acc[4][4] = {};
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const float4 lr = *reinterpret_cast<const float4*>(Ws + (c0 + m) * SWF + r);
+      const float4 yc = *reinterpret_cast<const float4*>(Xf + (c0 + m) * SWF + c);
+      const float ra[4] = {lr.x, lr.y, lr.z, lr.w}, ya[4] = {yc.x, yc.y, yc.z, yc.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(ra[u], ya[v], acc[u][v]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      float4* d = reinterpret_cast<float4*>(Xf + (r + u) * SWF + c);
+      float4 o = *d;
+      o.x -= acc[u][0]; o.y -= acc[u][1]; o.z -= acc[u][2]; o.w -= acc[u][3];
+      *d = o;
+    }
+  };
+  if (tid == 0) diag8(Ws, Xf, 0, &bad);
+  __syncthreads();
   for (int sp = 0; sp < CT / 8; ++sp) {
     const int c0 = 8 * sp, r0 = c0 + 8, nr = CT - r0;
 #ifdef VBA_POTRF_PROF
     long long q0 = clock64();
-#endif
-    if (tid == 0) diag8(Ws, Xf, c0, &bad);   // L_ss and X_ss (= final Y_ss)
-    __syncthreads();
-#ifdef VBA_POTRF_PROF
-    long long q1 = clock64();
 #endif
     if (tid < nr) {   // panel TRSM: L[r][c0+c] = sum_{m<=c} A[r][c0+m] X[c][m]
       const int r = r0 + tid;
@@ -1261,69 +1301,37 @@ __device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d) {
     }
     __syncthreads();
 #ifdef VBA_POTRF_PROF
-    long long q2 = clock64();
+    long long q1 = clock64();
 #endif
     if (nr == 0) break;
-    // rank-8 updates (4x4 blocks): A[r][c] -= sum_m L[r][c0+m] L[c][c0+m] (r0 <= c <= r), then
-    // Y[r][c] -= sum_m L[r][c0+m] Y[c0+m][c] (r >= r0, c < r0)
-    const int nb4 = nr / 4, nsy = nb4 * (nb4 + 1) / 2, nyc = r0 / 4, nblk = nsy + nb4 * nyc;
-    for (int b = tid; b < nblk; b += CHOL_THREADS) {
-      float acc[4][4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) acc[u][v] = 0.f;
-      if (b < nsy) {
-        int rb = (int)((sqrtf(8.f * b + 1.f) - 1.f) * 0.5f);
-        while ((rb + 1) * (rb + 2) / 2 <= b) ++rb;
-        while (rb * (rb + 1) / 2 > b) --rb;
-        // mirrored so that consecutive b (lanes) walk down a block column: contiguous
-        // float4 rows of the column-major tile, conflict-free
-        const int cbk = nb4 - 1 - rb, rbk = nb4 - 1 - (b - rb * (rb + 1) / 2);
-        const int r = r0 + 4 * rbk, c = r0 + 4 * cbk;
-#pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          const float4 lr = *reinterpret_cast<const float4*>(Ws + (c0 + m) * SWF + r);
-          const float4 lc = *reinterpret_cast<const float4*>(Ws + (c0 + m) * SWF + c);
-          const float ra[4] = {lr.x, lr.y, lr.z, lr.w}, ca[4] = {lc.x, lc.y, lc.z, lc.w};
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(ra[u], ca[v], acc[u][v]);
-        }
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          float4* d = reinterpret_cast<float4*>(Ws + (c + v) * SWF + r);
-          float4 o = *d;
-          o.x -= acc[0][v]; o.y -= acc[1][v]; o.z -= acc[2][v]; o.w -= acc[3][v];
-          *d = o;
-        }
-      } else {
-        const int bb = b - nsy, rb = bb / nyc, cbk = bb % nyc;
-        const int r = r0 + 4 * rb, c = 4 * cbk;
-#pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          const float4 lr = *reinterpret_cast<const float4*>(Ws + (c0 + m) * SWF + r);
-          const float ra[4] = {lr.x, lr.y, lr.z, lr.w};
-          const float4 yc = *reinterpret_cast<const float4*>(Xf + (c0 + m) * SWF + c);
-          const float ya[4] = {yc.x, yc.y, yc.z, yc.w};
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(ra[u], ya[v], acc[u][v]);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          float4* d = reinterpret_cast<float4*>(Xf + (r + u) * SWF + c);
-          float4 o = *d;
-          o.x -= acc[u][0]; o.y -= acc[u][1]; o.z -= acc[u][2]; o.w -= acc[u][3];
-          *d = o;
+    // Look-ahead: warp 0 updates the next panel's 8x8 diagonal block (three 4x4
+    // blocks) and one of its threads factors it (diag8) while warps 1..7 do the rest
+    // of this panel's updates; the diagonal block is disjoint from everything they
+    // read or write.
+    if (tid < 32) {
+      if (tid < 3) ablock(c0, r0 + (tid ? 4 : 0), r0 + (tid == 2 ? 4 : 0));
+      __syncwarp();
+      if (tid == 0) diag8(Ws, Xf, r0, &bad);
+    } else {
+      const int nb4 = nr / 4, nsy = nb4 * (nb4 + 1) / 2, nyc = r0 / 4, nblk = nsy + nb4 * nyc;
+      for (int b = tid - 32; b < nblk; b += CHOL_THREADS - 32) {
+        if (b < nsy) {
+          // mirrored so that consecutive b (lanes) walk down a block column: contiguous
+          // float4 rows of the column-major tile, conflict-free
+          int rb = (int)((sqrtf(8.f * b + 1.f) - 1.f) * 0.5f);
+          while ((rb + 1) * (rb + 2) / 2 <= b) ++rb;
+          while (rb * (rb + 1) / 2 > b) --rb;
+          const int cbk = nb4 - 1 - rb, rbk = nb4 - 1 - (b - rb * (rb + 1) / 2);
+          if (rbk >= 2) ablock(c0, r0 + 4 * rbk, r0 + 4 * cbk);   // rbk < 2: warp 0's diagonal block
+        } else {
+          const int bb = b - nsy, rb = bb / nyc, cbk = bb % nyc;
+          yblock(c0, r0 + 4 * rb, 4 * cbk);
         }
       }
     }
     __syncthreads();
 #ifdef VBA_POTRF_PROF
-    if (tid == 0 && ph) { ph[13] += q1 - q0; ph[14] += q2 - q1; ph[15] += clock64() - q2; }
+    if (tid == 0 && ph) { ph[13] += 0; ph[14] += q1 - q0; ph[15] += clock64() - q1; }
 #endif
   }
   if (tid == 0 && bad) atomicExch(a.status, 1);
@@ -1353,7 +1361,9 @@ __device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d) {
 
 __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
   extern __shared__ __align__(16) unsigned char tc_raw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~(uintptr_t)1023);
+  // 1024-B aligned (SW128 operand images) by pointer arithmetic on the __shared__
+  // array itself, so the compiler keeps the shared state space (LDS/STS, not generic)
+  unsigned char* sm = tc_raw + ((1024u - (su32(tc_raw) & 1023u)) & 1023u);
   __shared__ uint64_t full[TC_STAGES], empty[TC_STAGES], accf;
   __shared__ uint32_t tmem_sh;
   __shared__ int tsk;
