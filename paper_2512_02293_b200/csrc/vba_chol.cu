@@ -702,7 +702,11 @@ constexpr uint32_t TCHUNK = CT * TKC * 4;     // 16 KB
 constexpr int TC_STAGES = 3;
 constexpr uint32_t TSTAGE = 4 * TCHUNK;       // A_hi A_lo B_hi B_lo
 constexpr size_t TC_RING = (size_t)TC_STAGES * TSTAGE;
-constexpr size_t TC_SMEM = (TC_RING > POTRF_SMEM ? TC_RING : POTRF_SMEM) + 1024;
+// epilogue staging (fp32 128 x 132, padded rows) after the 4 hi/lo chunk images of a TRSM result
+constexpr size_t TC_EPI_OFF = (size_t)8 * TCHUNK;
+constexpr size_t TC_EPI_END = TC_EPI_OFF + (size_t)CT * (CT + 4) * 4;
+constexpr size_t TC_SMEM_0 = TC_RING > POTRF_SMEM ? TC_RING : POTRF_SMEM;
+constexpr size_t TC_SMEM = (TC_SMEM_0 > TC_EPI_END ? TC_SMEM_0 : TC_EPI_END) + 1024;
 constexpr int64_t TILE_F = (int64_t)CT * CT;  // floats per tile (and per image part)
 // instruction descriptor: D f32, A/B tf32, both K-major, N = 128, M = 128
 constexpr uint32_t TC_IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(CT >> 3) << 17) |
@@ -791,6 +795,51 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(r[k]);
 }
 
+// Coalesced epilogue.  The accumulator comes out of TMEM as rows per lane
+// (32x32b shape: lane = tile row), which would make every lane touch its own
+// 512-B row in global memory; it is staged through a padded shared-memory tile
+// (row stride CT + 4 floats: conflict-free both ways) and global memory is read
+// and written a full 512-B row per warp instruction.  Thread (w, lane) owns rows
+// 16 w .. 16 w + 15, float4 column `lane`.
+constexpr int EPS = CT + 4;
+__device__ __forceinline__ void tc_epi_prefetch(const float* Cg, float4 (&o)[16]) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) o[q] = __ldcg(reinterpret_cast<const float4*>(Cg) + (16 * w + q) * (CT / 4) + lane);
+}
+// TMEM accumulator -> S (fp32, row stride EPS); caller syncs before reading S
+__device__ __forceinline__ void tc_epi_stage(uint32_t tmem, float* S) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = 32 * (w & 3) + lane, c0 = 64 * (w >> 2);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float v[32];
+    tmem_ld32(tmem + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)(c0 + 32 * h), v);
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      *reinterpret_cast<float4*>(S + row * EPS + c0 + 32 * h + 4 * q) =
+          make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  }
+}
+// Cg -= S (o = the prefetched Cg), coalesced
+__device__ __forceinline__ void tc_epi_sub_store(float* Cg, const float4 (&o)[16], const float* S) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const float4 d = *reinterpret_cast<const float4*>(S + (16 * w + q) * EPS + 4 * lane);
+    float4 t = o[q];
+    t.x -= d.x; t.y -= d.y; t.z -= d.z; t.w -= d.w;
+    __stcg(reinterpret_cast<float4*>(Cg) + (16 * w + q) * (CT / 4) + lane, t);
+  }
+}
+__device__ __forceinline__ void tc_bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(su32(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tc_bulk_commit_wait() {
+  asm volatile("cp.async.bulk.commit_group;\n cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // Pipeline bookkeeping shared by all threads (identical updates everywhere; only
 // thread 0 issues copies / MMAs).  Stage s = n % TC_STAGES of the n-th fill.
 struct TcRing {
@@ -851,34 +900,25 @@ __device__ void tc_task_gemm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
     R.nfill += nchunks;
     R.ncons += nchunks;
   }
-  // epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 (= tile rows), columns 64 (w / 4) .. +63.
-  // The thread's 64 C values are loaded before waiting for the accumulator.
-  const int w = tid >> 5, lane = tid & 31;
-  const int row = 32 * (w & 3) + lane, c0 = 64 * (w >> 2);
-  float4* C4 = reinterpret_cast<float4*>(a.W + tlin(i, j) * TILE_F + (int64_t)row * CT + c0);
+  // epilogue (C prefetched before waiting for the accumulator); the ring is idle
+  // once the accumulator is complete, so the staging tile may overlap it
+  float* Cg = a.W + tlin(i, j) * TILE_F;
   float4 o[16];
-#pragma unroll
-  for (int q = 0; q < 16; ++q) o[q] = __ldcg(C4 + q);
+  tc_epi_prefetch(Cg, o);
   tc_mbar_wait(accf, nacc & 1);
   ++nacc;
   tc_fence_after();
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    float v[32];
-    tmem_ld32(tmem + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)(c0 + 32 * h), v);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      float4 t = o[8 * h + q];
-      t.x -= v[4 * q];
-      t.y -= v[4 * q + 1];
-      t.z -= v[4 * q + 2];
-      t.w -= v[4 * q + 3];
-      __stcg(C4 + 8 * h + q, t);
-    }
-  }
+  float* S = reinterpret_cast<float*>(R.base + TC_EPI_OFF);
+  tc_epi_stage(tmem, S);
   tc_fence_before();
+  __syncthreads();
+  tc_epi_sub_store(Cg, o, S);
+  proxy_fence_shared();   // generic staging writes before later bulk copies into the ring
 }
 
+#ifdef VBA_TRSM_PROF
+__device__ unsigned long long g_trsm_prof[8];
+#endif
 // TRSM(i,k):  L_ik = W_ik Linv_kk^T   (A = W_ik split by the threads, B = Linv images)
 __device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_t& nacc, uint32_t tmem, int i,
                              int k, bool keep_smem = false) {
@@ -886,6 +926,9 @@ __device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
   const float* Wik = a.W + tlin(i, k) * TILE_F;
   const float* ib = a.img + tlin(k, k) * 2 * TILE_F;
   if (tid == 0) proxy_fence_global();
+#ifdef VBA_TRSM_PROF
+  long long tp0 = clock64();
+#endif
   // the thread's share of A (row m = tid / 2, 16 K elements of each chunk): all loads first
   const int m = tid >> 1, u0 = (tid & 1) * 4;
   float4 areg[TNCH][4];
@@ -932,43 +975,81 @@ __device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
     }
   }
   if (tid == 0) tc_commit(accf);
+#ifdef VBA_TRSM_PROF
+  long long tp1 = clock64();
+#endif
   tc_mbar_wait(accf, nacc & 1);
   ++nacc;
   tc_fence_after();
-  const int w = tid >> 5, lane = tid & 31;
-  const int row = 32 * (w & 3) + lane, c0 = 64 * (w >> 2);
-  float* Lrow = a.W + tlin(i, k) * TILE_F + (int64_t)row * CT + c0;
-  float* ihi = a.img + tlin(i, k) * 2 * TILE_F;
-  float* ilo = ihi + TILE_F;
+#ifdef VBA_TRSM_PROF
+  long long tp2 = clock64();
+#endif
+  // epilogue: L_ik (fp32) staged row-padded at TC_EPI_OFF and its hi/lo chunk images
+  // (the global image layout) at 2 ch TCHUNK (hi), + TCHUNK (lo) of the idle ring;
+  // then the images leave by bulk copies and the fp32 rows by coalesced stores.
+  // keep_smem: the images stay for the following SYRK of the DIAG task.
+  {
+    const int w = tid >> 5, lane = tid & 31;
+    const int row = 32 * (w & 3) + lane, c0 = 64 * (w >> 2);
+    float* S = reinterpret_cast<float*>(R.base + TC_EPI_OFF);
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    float v[32];
-    tmem_ld32(tmem + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)(c0 + 32 * h), v);
+    for (int h = 0; h < 2; ++h) {
+      float v[32];
+      tmem_ld32(tmem + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)(c0 + 32 * h), v);
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const float4 x = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-      __stcg(reinterpret_cast<float4*>(Lrow + 32 * h) + q, x);
-      float4 hh, ll;
-      hh.x = tf32_rna(x.x); ll.x = tf32_rna(x.x - hh.x);
-      hh.y = tf32_rna(x.y); ll.y = tf32_rna(x.y - hh.y);
-      hh.z = tf32_rna(x.z); ll.z = tf32_rna(x.z - hh.z);
-      hh.w = tf32_rna(x.w); ll.w = tf32_rna(x.w - hh.w);
-      const int off = img_off(row, c0 + 32 * h + 4 * q);
-      __stcg(reinterpret_cast<float4*>(ihi + off), hh);
-      __stcg(reinterpret_cast<float4*>(ilo + off), ll);
-      if (keep_smem) {   // chunk images also into the ring: chunk ch at 2 ch TCHUNK (hi), + TCHUNK (lo)
-        const int cc = c0 + 32 * h + 4 * q, ch = cc >> 5, o2 = off - ch * (CT * TKC);
+      for (int q = 0; q < 8; ++q) {
+        const int cc = c0 + 32 * h + 4 * q, ch = cc >> 5;
+        const float4 x = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        *reinterpret_cast<float4*>(S + row * EPS + cc) = x;
+        float4 hh, ll;
+        hh.x = tf32_rna(x.x); ll.x = tf32_rna(x.x - hh.x);
+        hh.y = tf32_rna(x.y); ll.y = tf32_rna(x.y - hh.y);
+        hh.z = tf32_rna(x.z); ll.z = tf32_rna(x.z - hh.z);
+        hh.w = tf32_rna(x.w); ll.w = tf32_rna(x.w - hh.w);
+        const int o2 = img_off(row, cc) - ch * (CT * TKC);
         float* sh = reinterpret_cast<float*>(R.base + (size_t)2 * ch * TCHUNK);
         *reinterpret_cast<float4*>(sh + o2) = hh;
         *reinterpret_cast<float4*>(sh + CT * TKC + o2) = ll;
       }
     }
-  }
-  tc_fence_before();
-  if (keep_smem) {
-    proxy_fence_shared();   // generic writes -> tcgen05 operand reads
+    tc_fence_before();
+    proxy_fence_shared();   // generic writes -> bulk-copy / tcgen05 reads of the images
     __syncthreads();
+#ifdef VBA_TRSM_PROF
+    if (tid == 0) atomicAdd(&g_trsm_prof[5], (unsigned long long)(clock64() - tp2));
+#endif
+    float* ihi = a.img + tlin(i, k) * 2 * TILE_F;
+    if (tid == 0) {
+#pragma unroll
+      for (int ch = 0; ch < TNCH; ++ch) {
+        tc_bulk_store(ihi + ch * (CT * TKC), R.base + (size_t)2 * ch * TCHUNK, TCHUNK);
+        tc_bulk_store(ihi + TILE_F + ch * (CT * TKC), R.base + (size_t)(2 * ch + 1) * TCHUNK, TCHUNK);
+      }
+    }
+    float* Lg = a.W + tlin(i, k) * TILE_F;
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+      __stcg(reinterpret_cast<float4*>(Lg) + (16 * w + q) * (CT / 4) + lane,
+             *reinterpret_cast<const float4*>(S + (16 * w + q) * EPS + 4 * lane));
+#ifdef VBA_TRSM_PROF
+    if (tid == 0) atomicAdd(&g_trsm_prof[6], (unsigned long long)(clock64() - tp2));
+#endif
+    if (tid == 0) tc_bulk_commit_wait();   // image writes complete before the caller's fences
   }
+#ifdef VBA_TRSM_PROF
+  __syncthreads();
+  long long tp3 = clock64();
+  __threadfence();
+  __syncthreads();
+  long long tp4 = clock64();
+  if (tid == 0) {
+    atomicAdd(&g_trsm_prof[0], (unsigned long long)(tp1 - tp0));
+    atomicAdd(&g_trsm_prof[1], (unsigned long long)(tp2 - tp1));
+    atomicAdd(&g_trsm_prof[2], (unsigned long long)(tp3 - tp2));
+    atomicAdd(&g_trsm_prof[3], (unsigned long long)(tp4 - tp3));
+    atomicAdd(&g_trsm_prof[4], 1ull);
+  }
+#endif
 }
 
 // Diagonal SYRK of DIAG(k): W_{k+1,k+1} -= L L^T with L = L_{k+1,k} already in shared
@@ -976,12 +1057,9 @@ __device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
 __device__ void tc_task_syrk_smem(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_t& nacc, uint32_t tmem,
                                   int i) {
   const int tid = threadIdx.x;
-  const int w = tid >> 5, lane = tid & 31;
-  const int row = 32 * (w & 3) + lane, c0 = 64 * (w >> 2);
-  float4* C4 = reinterpret_cast<float4*>(a.W + tlin(i, i) * TILE_F + (int64_t)row * CT + c0);
+  float* Cg = a.W + tlin(i, i) * TILE_F;
   float4 o[16];
-#pragma unroll
-  for (int q = 0; q < 16; ++q) o[q] = __ldcg(C4 + q);
+  tc_epi_prefetch(Cg, o);
   if (tid == 0) {
     tc_fence_after();
     for (int ch = 0; ch < TNCH; ++ch) {
@@ -999,21 +1077,11 @@ __device__ void tc_task_syrk_smem(const TcArgs& a, TcRing& R, uint64_t* accf, ui
   tc_mbar_wait(accf, nacc & 1);
   ++nacc;
   tc_fence_after();
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    float v[32];
-    tmem_ld32(tmem + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)(c0 + 32 * h), v);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      float4 t = o[8 * h + q];
-      t.x -= v[4 * q];
-      t.y -= v[4 * q + 1];
-      t.z -= v[4 * q + 2];
-      t.w -= v[4 * q + 3];
-      __stcg(C4 + 8 * h + q, t);
-    }
-  }
+  float* S = reinterpret_cast<float*>(R.base + TC_EPI_OFF);
+  tc_epi_stage(tmem, S);
   tc_fence_before();
+  __syncthreads();
+  tc_epi_sub_store(Cg, o, S);
   proxy_fence_shared();   // the ring is refilled by bulk copies after these generic writes
 }
 
@@ -1223,47 +1291,57 @@ __device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d) {
     }
   }
   __syncthreads();
-  if (ph && tid == 0) ph[1] = ph[2] = gtimer();
+  if (ph && tid == 0) ph[1] = gtimer();
   // 4x4 register-blocked rank-8 updates of panel c0 (L columns c0..c0+7 of Ws):
   //   A block (rows r.., cols c.., r0 <= c <= r):  A[r][c] -= sum_m L[r][c0+m] L[c][c0+m]
   //   Y block (rows r >= r0, cols c < r0):          Y[r][c] -= sum_m L[r][c0+m] Y[c0+m][c]
-  auto ablock = [&](int c0, int r, int c) {
-    float acc[4][4] = {};
+  auto ablock = [&](int c0, int r, int c) {   // packed FFMA2 over row pairs (u, u+1)
+    float2 acc[2][4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[u][v] = make_float2(0.f, 0.f);
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
       const float4 lr = *reinterpret_cast<const float4*>(Ws + (c0 + m) * SWF + r);
       const float4 lc = *reinterpret_cast<const float4*>(Ws + (c0 + m) * SWF + c);
-      const float ra[4] = {lr.x, lr.y, lr.z, lr.w}, ca[4] = {lc.x, lc.y, lc.z, lc.w};
+      const float2 ra[2] = {make_float2(lr.x, lr.y), make_float2(lr.z, lr.w)};
+      const float ca[4] = {lc.x, lc.y, lc.z, lc.w};
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < 2; ++u)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(ra[u], ca[v], acc[u][v]);
+        for (int v = 0; v < 4; ++v) acc[u][v] = __ffma2_rn(ra[u], make_float2(ca[v], ca[v]), acc[u][v]);
     }
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       float4* d = reinterpret_cast<float4*>(Ws + (c + v) * SWF + r);
       float4 o = *d;
-      o.x -= acc[0][v]; o.y -= acc[1][v]; o.z -= acc[2][v]; o.w -= acc[3][v];
+      o.x -= acc[0][v].x; o.y -= acc[0][v].y; o.z -= acc[1][v].x; o.w -= acc[1][v].y;
       *d = o;
     }
   };
-  auto yblock = [&](int c0, int r, int c) {
-    float acc[4][4] = {};
+  auto yblock = [&](int c0, int r, int c) {   // packed FFMA2 over column pairs (v, v+1)
+    float2 acc[4][2];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) acc[u][v] = make_float2(0.f, 0.f);
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
       const float4 lr = *reinterpret_cast<const float4*>(Ws + (c0 + m) * SWF + r);
       const float4 yc = *reinterpret_cast<const float4*>(Xf + (c0 + m) * SWF + c);
-      const float ra[4] = {lr.x, lr.y, lr.z, lr.w}, ya[4] = {yc.x, yc.y, yc.z, yc.w};
+      const float ra[4] = {lr.x, lr.y, lr.z, lr.w};
+      const float2 ya[2] = {make_float2(yc.x, yc.y), make_float2(yc.z, yc.w)};
 #pragma unroll
       for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(ra[u], ya[v], acc[u][v]);
+        for (int v = 0; v < 2; ++v) acc[u][v] = __ffma2_rn(make_float2(ra[u], ra[u]), ya[v], acc[u][v]);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       float4* d = reinterpret_cast<float4*>(Xf + (r + u) * SWF + c);
       float4 o = *d;
-      o.x -= acc[u][0]; o.y -= acc[u][1]; o.z -= acc[u][2]; o.w -= acc[u][3];
+      o.x -= acc[u][0].x; o.y -= acc[u][0].y; o.z -= acc[u][1].x; o.w -= acc[u][1].y;
       *d = o;
     }
   };
@@ -1329,13 +1407,16 @@ __device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d) {
         }
       }
     }
+#ifdef VBA_POTRF_PROF
+    if ((tid & 31) == 0 && ph) atomicAdd(&ph[tid == 0 ? 2 : 3], (unsigned long long)(clock64() - q1));
+#endif
     __syncthreads();
 #ifdef VBA_POTRF_PROF
     if (tid == 0 && ph) { ph[13] += 0; ph[14] += q1 - q0; ph[15] += clock64() - q1; }
 #endif
   }
   if (tid == 0 && bad) atomicExch(a.status, 1);
-  if (ph && tid == 0) ph[3] = ph[4] = ph[5] = ph[6] = ph[7] = ph[8] = ph[9] = gtimer();
+  if (ph && tid == 0) ph[9] = gtimer();
   // outputs: Linv row-major fp32 (+ hi/lo images), zeros above the diagonal
   float* ihi = a.img + tlin(k, k) * 2 * TILE_F;
   float* ilo = ihi + TILE_F;
@@ -1428,19 +1509,24 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
         __syncthreads();
         if (tid == 0) st_release(&a.done[k * nt + k], 1);
         if (k + 1 < nt) {
+          unsigned long long* ph = a.trace ? a.trace + 4 * (size_t)a.ntasks + 16 * (size_t)k : nullptr;
           wait_geq(&a.upd[(k + 1) * nt + k], k);
           __syncthreads();
+          if (ph && tid == 0) ph[4] = gtimer();
           tc_task_trsm(a, R, &accf, nacc, tmem, k + 1, k, true);
           proxy_fence_global();
           __threadfence();
           __syncthreads();
           if (tid == 0) st_release(&a.done[(k + 1) * nt + k], 1);
+          if (ph && tid == 0) ph[5] = gtimer();
           wait_geq(&a.upd[(k + 1) * nt + k + 1], k);
           __syncthreads();
+          if (ph && tid == 0) ph[6] = gtimer();
           tc_task_syrk_smem(a, R, &accf, nacc, tmem, k + 1);
           __threadfence();
           __syncthreads();
           if (tid == 0) st_release(&a.upd[(k + 1) * nt + k + 1], k + 1);
+          if (ph && tid == 0) ph[7] = gtimer();
         }
         break;
       }
@@ -2052,23 +2138,29 @@ void chol_trace_print(const char* tag, const unsigned long long* d_trace, const 
   {
     std::vector<unsigned long long> ph((size_t)16 * nt);
     cudaMemcpy(ph.data(), d_trace + 4 * (size_t)ntasks, ph.size() * 8, cudaMemcpyDeviceToHost);
-    double ld = 0, f = 0, u = 0, inv = 0, clk = 0, ns = 0;
+    double ld = 0, u = 0, inv = 0, clk = 0, ns = 0, d[4] = {0, 0, 0, 0};
+    int nd = 0;
     for (int k = 0; k < nt; ++k) {
       const unsigned long long* q = &ph[16 * (size_t)k];
       if (!q[0] || !q[10]) continue;
       ld += (double)(q[1] - q[0]) * 1e-3;
-      unsigned long long prev = q[1];
-      for (int p = 0; p < 4; ++p) {
-        f += (double)(q[2 + 2 * p] - prev) * 1e-3;
-        u += (double)(q[3 + 2 * p] - q[2 + 2 * p]) * 1e-3;
-        prev = q[3 + 2 * p];
-      }
+      u += (double)(q[9] - q[1]) * 1e-3;
       inv += (double)(q[10] - q[9]) * 1e-3;
       if (q[12] > q[11]) { clk += (double)(q[12] - q[11]); ns += (double)(q[10] - q[0]); }
+      if (q[4] && q[7]) {   // DIAG task: wait for TRSM(k+1,k) operand, TRSM, wait for SYRK target, SYRK
+        d[0] += (double)(q[4] - q[10]) * 1e-3;
+        d[1] += (double)(q[5] - q[4]) * 1e-3;
+        d[2] += (double)(q[6] - q[5]) * 1e-3;
+        d[3] += (double)(q[7] - q[6]) * 1e-3;
+        ++nd;
+      }
     }
     if (ns > 0) fprintf(stderr, "  POTRF SM clock %.0f MHz\n", 1e3 * clk / ns);
-    fprintf(stderr, "  POTRF phases (avg us): load %.2f | factor32 x4 %.2f | trsm+syrk %.2f | inverse+store %.2f\n",
-            ld / nt, f / nt, u / nt, inv / nt);
+    fprintf(stderr, "  POTRF phases (avg us): load %.2f | panels %.2f | inverse+store %.2f\n", ld / nt, u / nt,
+            inv / nt);
+    if (nd)
+      fprintf(stderr, "  DIAG after POTRF (avg us): wait %.2f | TRSM %.2f | wait %.2f | SYRK %.2f\n", d[0] / nd,
+              d[1] / nd, d[2] / nd, d[3] / nd);
   }
   std::vector<unsigned long long> tr((size_t)4 * ntasks);
   std::vector<CholTask> tk(ntasks);
