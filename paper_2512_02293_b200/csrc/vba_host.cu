@@ -519,7 +519,7 @@ static int build_plans(Ctx* c, cudaStream_t st) {
     c->gram_smem = std::max(c->gram_smem, gram_smem_bytes(c->kmax, nsplit, np, k));
     int R = std::max(1, (int)((target + nsrc - 1) / nsrc));
     R = std::min(R, std::max(1, npix / 256));
-    const int chunk = ((npix + R - 1) / R + 31) / 32 * 32;
+    const int chunk = ((npix + R - 1) / R + 31) / 32 * 32;   // whole k_gram staging chunks (kGramPC)
     for (int a = 0; a < npix; a += chunk) {
       GramTile g{};
       g.src = n;

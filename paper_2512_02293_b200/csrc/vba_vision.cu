@@ -41,7 +41,7 @@ __host__ __device__ __forceinline__ int gram_px_stride(int kmax) {
 
 // dynamic shared memory of the DMMA Gram kernel: U and V, (6 kmax + 1 -> 8) columns x (PC + 4) pixels, fp64
 size_t gram_smem_bytes(int kmax, int /*nsplit*/, int /*npairs*/, int /*k*/) {
-  return (size_t)2 * ((6 * kmax + 1 + 7) / 8 * 8) * (kGramPC + 4) * sizeof(double);
+  return (size_t)4 * ((6 * kmax + 1 + 7) / 8 * 8) * (kGramPC + 4) * sizeof(double);   // U, V double-buffered
 }
 struct IntrP { double fx, fy, cx, cy; };
 
@@ -128,9 +128,11 @@ __device__ __forceinline__ PxGeom project(const EdgeGeo32& g, float rx, float ry
   return o;
 }
 
+static_assert(sizeof(EdgeGeo32) == 64, "EdgeGeo32 records are 4 float4");
+template <bool SMEM = false>
 __device__ __forceinline__ EdgeGeo32 load_geo(const EdgeGeo32* __restrict__ geo, int e) {
   const float4* p = reinterpret_cast<const float4*>(geo + e);
-  const float4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+  const float4 a = SMEM ? p[0] : __ldg(p), b = SMEM ? p[1] : __ldg(p + 1), c = SMEM ? p[2] : __ldg(p + 2);
   EdgeGeo32 g;
   g.M[0] = a.x; g.M[1] = a.y; g.M[2] = a.z; g.M[3] = a.w;
   g.M[4] = b.x; g.M[5] = b.y; g.M[6] = b.z; g.M[7] = b.w;
@@ -807,6 +809,18 @@ __device__ __forceinline__ void gdmma(double& c0, double& c1, double a, double b
                : "d"(a), "d"(b));
 }
 
+#ifdef VBA_GRAM_PROF   // tuning builds: per-warp cycles in phase 1 / barrier / phase 2 / barrier
+__device__ unsigned long long g_gram_prof[5];
+extern "C" __attribute__((visibility("default"))) void vba_gram_prof(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_gram_prof, sizeof(g_gram_prof));
+  unsigned long long z[5] = {0, 0, 0, 0, 0};
+  cudaMemcpyToSymbol(g_gram_prof, z, sizeof(z));
+}
+#define GPROF(i, v) if ((threadIdx.x & 31) == 0) atomicAdd(&g_gram_prof[i], (unsigned long long)(v))
+#else
+#define GPROF(i, v)
+#endif
 template <int MODE>
 __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
     const GramTile* __restrict__ gts, const float* __restrict__ disp, const EdgeGeo32* __restrict__ geo,
@@ -818,8 +832,9 @@ __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
   const int k = T.ee - T.eb;
   const int npairs = k * (k + 1) / 2;
   const int NRmax = (6 * kmax + 1 + 7) / 8 * 8;
-  double* U = reinterpret_cast<double*>(smem_raw);   // [NRmax][GPX]
-  double* V = U + (size_t)NRmax * GPX;               // [NRmax][GPX]
+  // U / V staging, double-buffered by chunk: buffer b at smem_raw + b * 2 * NRmax * GPX doubles
+  double* const UV = reinterpret_cast<double*>(smem_raw);
+  const size_t uvs = (size_t)NRmax * GPX;   // doubles per U (or V) buffer
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int64_t kbase = doff[T.src];
   const float fx = (float)in.fx, fy = (float)in.fy;
@@ -831,6 +846,9 @@ __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
   // tile t belongs to warp t % GWARPS, slot t / GWARPS
   __shared__ short tile_i[GWARPS * GMAXT], tile_j[GWARPS * GMAXT];
   __shared__ int ntiles_s;
+  __shared__ double invs[2][kGramPC];   // 1 / (Hdd (1 + lam) + ridge) per pixel, double-buffered by chunk
+  __shared__ float4 geos[32 * 4];       // the source's out-edge geometry (k <= 31), EdgeGeo32 records
+  auto pixel_inv = [&](int n) { return n < T.n1 ? 1.0 / ((double)Hdd[kbase + n] * damp + ridge) : 0.0; };
   if (tid == 0) {
     int t = 0;
     for (int ti = 0; ti < NRt; ++ti)
@@ -842,67 +860,116 @@ __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
         }
     ntiles_s = t;
   }
-  __syncthreads();
-  const int ntl = ntiles_s;
-  const int nmine = (ntl - warp + GWARPS - 1) / GWARPS;
   double acc[GMAXT][2];
 #pragma unroll
   for (int q = 0; q < GMAXT; ++q) acc[q][0] = acc[q][1] = 0.0;
-  for (int i = tid; i < 2 * NRmax * GPX; i += nth) U[i] = 0.0;   // padding columns stay zero
+  for (int i = tid; i < 4 * (int)uvs; i += nth) UV[i] = 0.0;   // padding columns stay zero
+  if (tid < kGramPC) invs[0][tid] = pixel_inv(T.n0 + tid);
+  if (tid < 4 * k) geos[tid] = __ldg(reinterpret_cast<const float4*>(geo + T.eb) + tid);
+  __syncthreads();
+  const int ntl = ntiles_s;
+  const int nmine = (ntl - warp + GWARPS - 1) / GWARPS;
 
-  for (int c0 = T.n0; c0 < T.n1; c0 += kGramPC) {
-    __syncthreads();
-    // phase 1: coupling vectors of (pixel, edge) items, widened to fp64
-    for (int it = tid; it < kGramPC * k; it += nth) {
-      const int e = it / kGramPC, px = it % kGramPC;
-      const int n = c0 + px;
-      float u[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      double inv = 0.0;
-      if (n < T.n1) {
-        const float d = disp[kbase + n];
-        float rx, ry, rx1, ry1;
-        if (MODE == VBA_PIX_EDGE)
-          load_rays<VBA_PIX_KF>(pix, eoff[T.eb + e], n & ~1, grid_w, gp, in, rx, ry, rx1, ry1);
-        else
-          load_rays<MODE>(pix, kbase, n & ~1, grid_w, gp, in, rx, ry, rx1, ry1);
-        if (n & 1) { rx = rx1; ry = ry1; }
-        const EdgeGeo32 g = load_geo(geo, T.eb + e);
-        const PxGeom o = project(g, rx, ry, d);
-        const float2 w = __ldg(reinterpret_cast<const float2*>(wts + 2 * (eoff[T.eb + e] + n)));
-        const float w0 = o.valid ? w.x : 0.f, w1 = o.valid ? w.y : 0.f;
-        const float jd0 = fmaf(o.x, g.t[2], -g.t[0]) * o.izh;
-        const float jd1 = fmaf(o.y, g.t[2], -g.t[1]) * o.izh;
-        const float c0w = w0 * fx2 * jd0, c1w = w1 * fy2 * jd1;
-        const float xy = o.x * o.y;
-        u[0] = fmaf(c0w, xy, c1w * fmaf(o.y, o.y, 1.f));
-        u[1] = fmaf(c0w, -fmaf(o.x, o.x, 1.f), c1w * -xy);
-        u[2] = fmaf(c0w, o.y, c1w * -o.x);
-        u[3] = c0w * -o.iz;
-        u[4] = c1w * -o.iz;
-        u[5] = fmaf(c0w, o.x * o.iz, c1w * (o.y * o.iz));
-        inv = 1.0 / ((double)Hdd[kbase + n] * damp + ridge);
-        if (e == 0) U[(size_t)nc * GPX + px] = (double)gd[kbase + n];
-      } else if (e == 0) {
-        U[(size_t)nc * GPX + px] = 0.0;
-      }
+  // Phase 1 of a chunk: coupling vectors of its (pixel, edge) items (at most kGramItems
+  // per thread), widened to fp64 into buffer b.  Loads of all items first (gload),
+  // arithmetic + stores per item (gitem), so the arithmetic can be interleaved with
+  // the DMMAs of the previous chunk.
+  constexpr int kGramItems = (kGramPC * 31 + GWARPS * 32 - 1) / (GWARPS * 32);
+  float d_[kGramItems], rx_[kGramItems], ry_[kGramItems], gd_[kGramItems];
+  float2 w_[kGramItems];
+  auto gload = [&](int c0) {
 #pragma unroll
-      for (int r = 0; r < 6; ++r) {
-        U[(size_t)(6 * e + r) * GPX + px] = (double)u[r];
-        V[(size_t)(6 * e + r) * GPX + px] = (double)u[r] * inv;
+    for (int j = 0; j < kGramItems; ++j) {
+      const int it = tid + j * nth;
+      const int e = it / kGramPC, px = it % kGramPC, n = c0 + px;
+      d_[j] = rx_[j] = ry_[j] = gd_[j] = 0.f;
+      w_[j] = make_float2(0.f, 0.f);
+      if (it < kGramPC * k && n < T.n1) {
+        d_[j] = disp[kbase + n];
+        if (e == 0) gd_[j] = gd[kbase + n];
+        float rx1, ry1;
+        if (MODE == VBA_PIX_EDGE)
+          load_rays<VBA_PIX_KF>(pix, eoff[T.eb + e], n & ~1, grid_w, gp, in, rx_[j], ry_[j], rx1, ry1);
+        else
+          load_rays<MODE>(pix, kbase, n & ~1, grid_w, gp, in, rx_[j], ry_[j], rx1, ry1);
+        if (n & 1) { rx_[j] = rx1; ry_[j] = ry1; }
+        w_[j] = __ldg(reinterpret_cast<const float2*>(wts + 2 * (eoff[T.eb + e] + n)));
       }
     }
+  };
+  auto gitem = [&](int j, int c0, int b) {
+    const int it = tid + j * nth;
+    if (it >= kGramPC * k) return;
+    double* U = UV + (size_t)b * 2 * uvs;
+    double* V = U + uvs;
+    const int e = it / kGramPC, px = it % kGramPC;
+    const int n = c0 + px;
+    float u[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    double inv = 0.0;
+    if (n < T.n1) {
+      const EdgeGeo32 g = load_geo<true>(reinterpret_cast<const EdgeGeo32*>(geos), e);
+      const PxGeom o = project(g, rx_[j], ry_[j], d_[j]);
+      const float w0 = o.valid ? w_[j].x : 0.f, w1 = o.valid ? w_[j].y : 0.f;
+      const float jd0 = fmaf(o.x, g.t[2], -g.t[0]) * o.izh;
+      const float jd1 = fmaf(o.y, g.t[2], -g.t[1]) * o.izh;
+      const float c0w = w0 * fx2 * jd0, c1w = w1 * fy2 * jd1;
+      const float xy = o.x * o.y;
+      u[0] = fmaf(c0w, xy, c1w * fmaf(o.y, o.y, 1.f));
+      u[1] = fmaf(c0w, -fmaf(o.x, o.x, 1.f), c1w * -xy);
+      u[2] = fmaf(c0w, o.y, c1w * -o.x);
+      u[3] = c0w * -o.iz;
+      u[4] = c1w * -o.iz;
+      u[5] = fmaf(c0w, o.x * o.iz, c1w * (o.y * o.iz));
+      inv = invs[b][px];
+      if (e == 0) U[(size_t)nc * GPX + px] = (double)gd_[j];
+    } else if (e == 0) {
+      U[(size_t)nc * GPX + px] = 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+      U[(size_t)(6 * e + r) * GPX + px] = (double)u[r];
+      V[(size_t)(6 * e + r) * GPX + px] = (double)u[r] * inv;
+    }
+  };
+  // prologue: phase 1 of chunk 0 (buffer 0) and the pixel inverses of chunk 1
+  gload(T.n0);
+#pragma unroll
+  for (int j = 0; j < kGramItems; ++j) gitem(j, T.n0, 0);
+  if (tid >= nth - kGramPC) invs[1][tid - (nth - kGramPC)] = pixel_inv(T.n0 + kGramPC + tid - (nth - kGramPC));
+#ifdef VBA_GRAM_PROF
+  long long gt_d = clock64();
+#endif
+  for (int c0 = T.n0, cb = 0; c0 < T.n1; c0 += kGramPC, cb ^= 1) {
     __syncthreads();
-    // phase 2: C += U^T V on the fp64 tensor cores, 8 pixel-steps of 4
+#ifdef VBA_GRAM_PROF
+    long long gt_a = clock64();
+    GPROF(3, gt_a - gt_d);
+    GPROF(4, 1);
+#endif
+    // C += U^T V (buffer cb) on the fp64 tensor cores, 8 pixel-steps of 4, with the
+    // phase-1 items of chunk c + 1 (buffer cb ^ 1) interleaved between the tiles
+    const int cn = c0 + kGramPC;
+    const bool more = cn < T.n1;
+    if (more) gload(cn);
+    const double* Ub = UV + (size_t)cb * 2 * uvs;
+    const double* Vb = Ub + uvs;
     const int am = lane >> 2, ak = lane & 3;
 #pragma unroll
     for (int q = 0; q < GMAXT; ++q) {
       if (q < nmine) {
-        const double* pa = U + (size_t)(tile_i[warp + GWARPS * q] * 8 + am) * GPX + ak;
-        const double* pb = V + (size_t)(tile_j[warp + GWARPS * q] * 8 + am) * GPX + ak;
+        const double* pa = Ub + (size_t)(tile_i[warp + GWARPS * q] * 8 + am) * GPX + ak;
+        const double* pb = Vb + (size_t)(tile_j[warp + GWARPS * q] * 8 + am) * GPX + ak;
 #pragma unroll
         for (int ks = 0; ks < kGramPC / 4; ++ks) gdmma(acc[q][0], acc[q][1], pa[4 * ks], pb[4 * ks]);
       }
+      if (q % 3 == 1 && q / 3 < kGramItems && more) gitem(q / 3, cn, cb ^ 1);
     }
+    // pixel inverses of chunk c + 2 (buffer cb: chunk c's items are done)
+    if (tid >= nth - kGramPC) invs[cb][tid - (nth - kGramPC)] = pixel_inv(cn + kGramPC + tid - (nth - kGramPC));
+#ifdef VBA_GRAM_PROF
+    gt_d = clock64();
+    GPROF(2, gt_d - gt_a);
+#endif
   }
   // epilogue: scatter the lower 6x6 blocks (e1 >= e2) and the b row into the output layout
   double* o = out + T.out;
