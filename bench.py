@@ -282,30 +282,21 @@ def main():
     pinned = {k: torch.from_numpy(np.ascontiguousarray(v).reshape(-1)).pin_memory()
               for k, v in (("state", H.state), ("disp", H.disp), ("tgt", H.tgt), ("w", H.w), ("imu", H.imu),
                            ("grav", H.grav))}
-    out_state = torch.empty(dp.d_state.numel(), dtype=torch.float64).pin_memory()
-    out_disp = torch.empty(dp.d_disp.numel(), dtype=torch.float32).pin_memory()
-    dsts = {"state": dp.d_state, "disp": dp.d_disp, "tgt": dp.d_tgt, "w": dp.d_w, "imu": dp.d_imu,
-            "grav": dp.d_grav}
     h2d = sum(v.numel() * v.element_size() for v in pinned.values())
-    d2h = out_state.numel() * 8 + out_disp.numel() * 4
-    e2e_ms = 0.0
-    e2e_iters = 0
-    for k in range(a.steps + 1):
-        barrier()
-        ev0.record(stream)
-        for name, src in pinned.items():
-            dsts[name].view(-1).copy_(src, non_blocking=True)
-        dp.load_state()
-        rep = dp.solve()
-        from paper_2512_02293_b200 import _lib as L
-        L.check(dp.lib.vba_download(dp.ctx, dp._sptr()))
-        out_state.copy_(dp.d_state.view(-1), non_blocking=True)
-        out_disp.copy_(dp.d_disp.view(-1), non_blocking=True)
-        ev1.record(stream)
-        barrier()
-        if k > 0:   # first pass warms the pinned path
-            e2e_ms += ev0.elapsed_time(ev1)
-            e2e_iters += rep["iterations"]
+    d2h = dp.d_state.numel() * 8 + dp.d_disp.numel() * 4
+    # every step uploads its window from pinned host memory and reads its result back;
+    # solve_windows streams window s+1's flow/weight upload on a copy stream while
+    # window s is solved (the public streaming API, paper_2512_02293_b200.device)
+    outs = [(torch.empty(dp.d_state.shape, dtype=torch.float64).pin_memory(),
+             torch.empty(dp.d_disp.shape, dtype=torch.float32).pin_memory()) for _ in range(a.steps)]
+    dp.solve_windows([pinned], outputs=outs[:1])   # warms the pinned path and the copy stream
+    barrier()
+    ev0.record(stream)
+    reps = dp.solve_windows([pinned] * a.steps, outputs=outs)
+    ev1.record(stream)
+    barrier()
+    e2e_ms = ev0.elapsed_time(ev1)
+    e2e_iters = sum(r["iterations"] for r in reps)
     t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -154,6 +154,12 @@ VBA_API int vba_solve(void* ctx, void* stream, vba_report* report, double* cost_
               int32_t traj_capacity);
 /* re-seed the current state from the caller's problem arrays (state, disp, grav) */
 VBA_API int vba_load_state(void* ctx, void* stream);
+/* (new, streaming) bind another window's per-edge-pixel inputs of the same topology:
+ * flow targets and weights (device pointers, the layout of vba_problem.tgt / .wts).
+ * refresh_imu != 0 re-derives the IMU whitening factors from vba_problem.imu (its
+ * contents may have changed); returns VBA_E_COV for a non-PSD covariance.  The
+ * static per-pixel schedule built at create is kept (valid for any weights). */
+VBA_API int vba_bind_inputs(void* ctx, void* stream, const float* tgt, const float* wts, int32_t refresh_imu);
 /* enable per-stage CUDA-event timing of vba_solve / vba_trial (resets the counters) */
 VBA_API int vba_set_profiling(void* ctx, int32_t on);
 /* copy the current (accepted) state back to the caller's problem arrays */

@@ -20,7 +20,7 @@ EXPORTED = ("vba_last_error", "vba_version", "vba_create", "vba_destroy", "vba_s
             "vba_reduced_dim", "vba_energy", "vba_linearize", "vba_export_normal_eq",
             "vba_solve_step", "vba_export_step", "vba_apply_step", "vba_restore", "vba_accept",
             "vba_trial", "vba_solve", "vba_download", "vba_launch_count", "vba_stage_times",
-            "vba_load_state", "vba_set_profiling", "vba_stats", "vba_spd_solve", "vba_solve_times")
+            "vba_load_state", "vba_bind_inputs", "vba_set_profiling", "vba_stats", "vba_spd_solve", "vba_solve_times")
 
 
 class VbaProblem(C.Structure):
@@ -103,6 +103,7 @@ def load(path: str | None = None):
         "vba_launch_count": ([v], C.c_int64),
         "vba_stage_times": ([v, C.POINTER(C.c_double)], C.c_int),
         "vba_load_state": ([v, v], C.c_int),
+        "vba_bind_inputs": ([v, v, v, v, C.c_int32], C.c_int),
         "vba_set_profiling": ([v, C.c_int32], C.c_int),
         "vba_stats": ([v, C.POINTER(C.c_int64)], C.c_int),
         "vba_solve_times": ([v, C.POINTER(C.c_double)], C.c_int),

@@ -1359,6 +1359,23 @@ int vba_stage_times(void* ctx, double* out7) {
   return VBA_OK;
 }
 
+int vba_bind_inputs(void* ctx, void* stream, const float* tgt, const float* wts, int32_t refresh_imu) {
+  Ctx* c = (Ctx*)ctx;
+  if (!c || !tgt || !wts) { set_err("vba_bind_inputs: null argument"); return VBA_E_INVALID; }
+  cudaStream_t st = (cudaStream_t)stream;
+  c->P.tgt = tgt;
+  c->P.wts = wts;
+  if (refresh_imu && c->F > 0) {
+    cudaMemsetAsync(c->d_imu_status, 0, sizeof(int), st);
+    launch_imu_prep(c->P.imu, c->F, c->d_L, c->d_imu_status, st);
+    int hs = 0;
+    VBA_CUDA(cudaMemcpyAsync(&hs, c->d_imu_status, sizeof(int), cudaMemcpyDeviceToHost, st));
+    VBA_CUDA(cudaStreamSynchronize(st));
+    if (hs) { set_err("non-PSD preintegration covariance"); return VBA_E_COV; }
+  }
+  return VBA_OK;
+}
+
 int vba_load_state(void* ctx, void* stream) {
   Ctx* c = (Ctx*)ctx;
   cudaStream_t st = (cudaStream_t)stream;

@@ -306,6 +306,68 @@ class DeviceProblem:
                     condition_warnings=["singular reduced pose system"] * rep.n_warnings,
                     trials=rep.trials)
 
+    def solve_windows(self, windows, outputs=None, copy_stream=None):
+        """Solve a sequence of windows of this problem's topology end to end from host memory.
+
+        ``windows``: dicts of (ideally pinned) host tensors in HostLayout order and dtype,
+        keys ``state, disp, tgt, w, imu, grav``.  Window s+1's flow targets and weights
+        (the bulk of the bytes) are uploaded on ``copy_stream`` into a second device set
+        while window s is solved (``vba_bind_inputs`` swaps the sets); the small arrays are
+        uploaded on the solve stream.  Each window's solved state and disparities are read
+        back into ``outputs[s] = (state, disp)`` (pinned host tensors, allocated when not
+        given) before the next window starts.  Returns the per-window reports."""
+        if not windows:
+            return []
+        dev, st = self.device, self.stream
+        cs = copy_stream if copy_stream is not None else torch.cuda.Stream(dev)
+        if getattr(self, "_stage", None) is None:
+            self._stage = (torch.empty_like(self.d_tgt), torch.empty_like(self.d_w))
+        sets = ((self.d_tgt, self.d_w), self._stage)
+        up = [torch.cuda.Event(), torch.cuda.Event()]
+        free = [torch.cuda.Event(), torch.cuda.Event()]
+        used = [False, False]
+
+        def upload(s, b):
+            with torch.cuda.stream(cs):
+                if used[b]:
+                    cs.wait_event(free[b])
+                sets[b][0].copy_(windows[s]["tgt"].reshape(-1), non_blocking=True)
+                sets[b][1].copy_(windows[s]["w"].reshape(-1), non_blocking=True)
+                up[b].record(cs)
+
+        if outputs is None:
+            outputs = [(torch.empty(self.d_state.shape, dtype=torch.float64).pin_memory(),
+                        torch.empty(self.d_disp.shape, dtype=torch.float32).pin_memory()) for _ in windows]
+        cs.wait_stream(st)
+        upload(0, 0)
+        reps = []
+        for s, win in enumerate(windows):
+            b = s & 1
+            if s + 1 < len(windows):
+                upload(s + 1, b ^ 1)
+            st.wait_event(up[b])
+            with torch.cuda.stream(st):
+                self.d_state.copy_(win["state"].reshape(self.d_state.shape), non_blocking=True)
+                self.d_disp.copy_(win["disp"].reshape(self.d_disp.shape), non_blocking=True)
+                self.d_imu.copy_(win["imu"].reshape(-1), non_blocking=True)
+                self.d_grav.copy_(win["grav"].reshape(-1), non_blocking=True)
+            rc = self.lib.vba_bind_inputs(self.ctx, self._sptr(), sets[b][0].data_ptr(), sets[b][1].data_ptr(), 1)
+            if rc == L.VBA_E_COV:
+                raise ValueError("non-PSD preintegration covariance")
+            L.check(rc)
+            self.load_state()
+            reps.append(self.solve())
+            L.check(self.lib.vba_download(self.ctx, self._sptr()))
+            with torch.cuda.stream(st):
+                outputs[s][0].copy_(self.d_state, non_blocking=True)
+                outputs[s][1].copy_(self.d_disp, non_blocking=True)
+            free[b].record(st)
+            used[b] = True
+        # leave the problem bound to its own arrays (window 0's set)
+        st.wait_event(up[0])
+        L.check(self.lib.vba_bind_inputs(self.ctx, self._sptr(), self.d_tgt.data_ptr(), self.d_w.data_ptr(), 0))
+        return reps
+
     def download(self):
         """Current state as numpy: (q, p, v, bg, ba, disp[unpadded], grav_q)."""
         L.check(self.lib.vba_download(self.ctx, self._sptr()))

@@ -228,3 +228,42 @@ def test_large_window_uses_tensor_core_solve_without_fallback(cuda_ok):
             os.environ.pop("VBA_CHOL", None)
     assert rel(steps["tc"][0], steps["fp64"][0]) < 1e-7
     assert rel(steps["tc"][1], steps["fp64"][1]) < 1e-7
+
+
+def test_solve_windows_streams_bitwise_equal(cuda_ok):
+    """The streaming entry point (device.solve_windows: window s+1 uploaded on a copy
+    stream while window s is solved, inputs rebound with vba_bind_inputs) returns,
+    for every window, exactly the state of a plain upload + solve of that window."""
+    import torch
+    from paper_2512_02293_b200.problem import pack_graph
+    from paper_2512_02293_b200.workloads import make_workload
+    P = pack_graph(make_workload(1))
+    opts = {"max_iterations": 2}
+    dp = _dp(copy.deepcopy(P), opts)
+    H = dp.H
+    base = {k: np.ascontiguousarray(v) for k, v in (("state", H.state), ("disp", H.disp), ("tgt", H.tgt),
+                                                   ("w", H.w), ("imu", H.imu), ("grav", H.grav))}
+    rng = np.random.default_rng(7)
+    wins = []
+    for s in range(3):   # three different windows: perturbed flow targets
+        w = dict(base)
+        w["tgt"] = (base["tgt"] + rng.normal(0.0, 0.2, base["tgt"].shape)).astype(base["tgt"].dtype)
+        wins.append({k: torch.from_numpy(np.ascontiguousarray(v).reshape(-1)).pin_memory() for k, v in w.items()})
+    outs = [(torch.empty(dp.d_state.shape, dtype=torch.float64).pin_memory(),
+             torch.empty(dp.d_disp.shape, dtype=torch.float32).pin_memory()) for _ in wins]
+    reps = dp.solve_windows(wins, outputs=outs)
+    torch.cuda.synchronize()
+    assert len(reps) == 3
+    for s in range(3):
+        ref = _dp(copy.deepcopy(P), opts)
+        ref.d_tgt.copy_(wins[s]["tgt"].reshape(ref.d_tgt.shape))
+        torch.cuda.synchronize()
+        ref.load_state()
+        r = ref.solve()
+        ref.lib.vba_download(ref.ctx, ref._sptr())
+        torch.cuda.synchronize()
+        assert r["final_cost"] == reps[s]["final_cost"]
+        assert torch.equal(ref.d_state.cpu(), outs[s][0])
+        assert torch.equal(ref.d_disp.cpu(), outs[s][1])
+        ref.close()
+    dp.close()
