@@ -709,8 +709,17 @@ constexpr size_t TC_SMEM_0 = TC_RING > POTRF_SMEM ? TC_RING : POTRF_SMEM;
 constexpr size_t TC_SMEM = (TC_SMEM_0 > TC_EPI_END ? TC_SMEM_0 : TC_EPI_END) + 1024;
 constexpr int64_t TILE_F = (int64_t)CT * CT;  // floats per tile (and per image part)
 // instruction descriptor: D f32, A/B tf32, both K-major, N = 128, M = 128
-constexpr uint32_t TC_IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(CT >> 3) << 17) |
-                              ((uint32_t)(CT >> 4) << 24);
+constexpr uint32_t tc_idesc(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(CT >> 4) << 24);
+}
+constexpr uint32_t TC_IDESC = tc_idesc(CT);        // M = N = 128
+constexpr uint32_t TC_IDESC2 = tc_idesc(2 * CT);   // M = 128, N = 256
+// The accumulator spans 256 TMEM columns: 3xTF32 is issued as
+//   D[:, 0:256] (+)= A_hi [B_hi; B_lo]^T   (one N = 256 MMA: B_lo is stored right after B_hi)
+//   D[:, 0:128]  += A_lo B_hi^T
+// and the epilogue adds the two 128-column halves (an N = 256 MMA costs one N = 128
+// MMA's issue slot twice over, measured: 130 vs 3 x 97-130 cycles per K-step).
+constexpr int TC_TMEM_COLS = 2 * CT;
 
 struct TcArgs {
   float* W;           // [ntl][CT*CT]
@@ -764,11 +773,17 @@ __device__ __forceinline__ uint64_t tc_sdesc(uint32_t saddr) {   // K-major, SWI
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
-__device__ __forceinline__ void tc_mma(uint32_t tmem, uint64_t da, uint64_t db, uint32_t acc) {
+__device__ __forceinline__ void tc_mma(uint32_t tmem, uint64_t da, uint64_t db, uint32_t acc,
+                                       uint32_t idesc = TC_IDESC) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %3, 0;\n"
       " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %4, p;\n}\n" ::"r"(tmem),
-      "l"(da), "l"(db), "r"(acc), "r"(TC_IDESC));
+      "l"(da), "l"(db), "r"(acc), "r"(idesc));
+}
+// one K-step (8 tf32) of 3xTF32 into the 256-column accumulator; b_hi is followed by b_lo
+__device__ __forceinline__ void tc_mma3(uint32_t tmem, uint32_t a_hi, uint32_t a_lo, uint32_t b_hi, bool first) {
+  tc_mma(tmem, tc_sdesc(a_hi), tc_sdesc(b_hi), first ? 0u : 1u, TC_IDESC2);
+  tc_mma(tmem, tc_sdesc(a_lo), tc_sdesc(b_hi), 1u, TC_IDESC);
 }
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
@@ -795,6 +810,15 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(r[k]);
 }
 
+// columns c .. c+31 of the 3xTF32 result: accumulator columns c and c + 128 summed
+__device__ __forceinline__ void tmem_ld_sum(uint32_t taddr, float* v) {
+  float u[32];
+  tmem_ld32(taddr, v);
+  tmem_ld32(taddr + CT, u);
+#pragma unroll
+  for (int k = 0; k < 32; ++k) v[k] += u[k];
+}
+
 // Coalesced epilogue.  The accumulator comes out of TMEM as rows per lane
 // (32x32b shape: lane = tile row), which would make every lane touch its own
 // 512-B row in global memory; it is staged through a padded shared-memory tile
@@ -814,7 +838,7 @@ __device__ __forceinline__ void tc_epi_stage(uint32_t tmem, float* S) {
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     float v[32];
-    tmem_ld32(tmem + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)(c0 + 32 * h), v);
+    tmem_ld_sum(tmem + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)(c0 + 32 * h), v);
 #pragma unroll
     for (int q = 0; q < 8; ++q)
       *reinterpret_cast<float4*>(S + row * EPS + c0 + 32 * h + 4 * q) =
@@ -856,9 +880,7 @@ __device__ __forceinline__ void tc_chunk_mma(const TcRing& R, int s, uint32_t tm
 #pragma unroll
   for (int kk = 0; kk < TKC / 8; ++kk) {   // 8 tf32 (32 B) of K per MMA
     const uint32_t o = 32u * kk;
-    tc_mma(tmem, tc_sdesc(a_hi + o), tc_sdesc(b_hi + o), (first && kk == 0) ? 0u : 1u);
-    tc_mma(tmem, tc_sdesc(a_hi + o), tc_sdesc(b_lo + o), 1u);
-    tc_mma(tmem, tc_sdesc(a_lo + o), tc_sdesc(b_hi + o), 1u);
+    tc_mma3(tmem, a_hi + o, a_lo + o, b_hi + o, first && kk == 0);
   }
 }
 
@@ -995,7 +1017,7 @@ __device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       float v[32];
-      tmem_ld32(tmem + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)(c0 + 32 * h), v);
+      tmem_ld_sum(tmem + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)(c0 + 32 * h), v);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int cc = c0 + 32 * h + 4 * q, ch = cc >> 5;
@@ -1067,9 +1089,7 @@ __device__ void tc_task_syrk_smem(const TcArgs& a, TcRing& R, uint64_t* accf, ui
 #pragma unroll
       for (int kk = 0; kk < TKC / 8; ++kk) {
         const uint32_t off = 32u * kk;
-        tc_mma(tmem, tc_sdesc(hi + off), tc_sdesc(hi + off), (ch == 0 && kk == 0) ? 0u : 1u);
-        tc_mma(tmem, tc_sdesc(hi + off), tc_sdesc(lo + off), 1u);
-        tc_mma(tmem, tc_sdesc(lo + off), tc_sdesc(hi + off), 1u);
+        tc_mma3(tmem, hi + off, lo + off, hi + off, ch == 0 && kk == 0);
       }
     }
     tc_commit(accf);
@@ -1450,7 +1470,8 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
   __shared__ int tsk;
   const int tid = threadIdx.x, nt = a.nt;
   if (tid < 32) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(su32(&tmem_sh)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_sh)),
+                 "n"(TC_TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
@@ -1559,7 +1580,7 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+  if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TC_TMEM_COLS));
 }
 
 // ---------------------------------------------------------------------------
