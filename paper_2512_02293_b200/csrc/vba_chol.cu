@@ -1812,10 +1812,32 @@ __global__ void __launch_bounds__(256, 1) k_tc_prep(const float* __restrict__ W,
 //   y_k = Linv_kk (v_k - sum_{j<k-2} L_kj y_j) - M2 y_{k-2} - M1 y_{k-1}
 // LinvT, M1^T, M2^T come precomputed (k_tc_prep); the chain sees one 128x128
 // shared-memory matvec per step.  Off-chain tiles are register-prefetched two deep.
+// one butterfly stage of a warp transpose-reduction: lanes with bit LB set keep the
+// upper ST values (adding their partner's), the others the lower ST
+template <int ST, int LB>
+__device__ __forceinline__ void bfly_stage(float* pr, int ln) {
+  const bool up = ln & LB;
+#pragma unroll
+  for (int m = 0; m < ST; ++m) {
+    const float give = up ? pr[m] : pr[m + ST];
+    const float keep = up ? pr[m + ST] : pr[m];
+    pr[m] = keep + __shfl_xor_sync(0xffffffffu, give, LB);
+  }
+}
+
+// forward: L y = D r (row tile k; one CTA per row tile, all co-resident).
+//   acc_k = D r_k - sum_{j <= k-3} V[k][j],   V[k][j] = L_kj y_j
+//   y_k = Linv_kk acc_k - M2 y_{k-2} - M1 y_{k-1}     (M1, M2 folded by k_tc_prep)
+// The off-chain products V[i][k] (i >= k+3) are computed by CTA k right after it
+// publishes y_k (a column sweep over tiles L_ik, prefetched before y_k is known) and
+// handed over as tagged words, so every row tile's off-chain sum is ready long
+// before the chain reaches it; the chain step is fetch y_{k-1}, one 128x128
+// shared-memory matvec, publish.  Sums run in fixed order (deterministic).
 __global__ void __launch_bounds__(256, 1) k_tc_fwd(const float* __restrict__ W, const float* __restrict__ F,
                                                    int nt, const double* __restrict__ r,
                                                    const double* __restrict__ D, unsigned long long* __restrict__ y,
-                                                   int gen, const int* __restrict__ stop) {
+                                                   unsigned long long* __restrict__ V, int gen,
+                                                   const int* __restrict__ stop) {
   extern __shared__ __align__(16) unsigned char tri_raw[];
   float* Lin = reinterpret_cast<float*>(tri_raw);     // Linv_kk^T
   float* M1 = Lin + TILE_F;                           // M1^T
@@ -1828,39 +1850,29 @@ __global__ void __launch_bounds__(256, 1) k_tc_fwd(const float* __restrict__ W, 
   TRI_STAMP(0, 0, k)
   tri_prefetch(Lin, F + (int64_t)k * TILE_F, M1, k > 0 ? F + ((int64_t)nt + k) * TILE_F : nullptr, M2,
                k > 1 ? F + ((int64_t)2 * nt + k) * TILE_F : nullptr, bar);
-  if (tid < CT) acc[tid] = (float)(D[CT * k + tid] * r[CT * k + tid]);
-  // off the chain: tiles L_kj, j < k-2, two ahead in registers (they do not depend on y)
-  const int row = tid >> 1, h = tid & 1;
-  auto ld_tile = [&](int j, float4* dst) {
-    const float4* p = reinterpret_cast<const float4*>(W + tlin(k, j) * TILE_F + row * CT + 64 * h);
+  // the first two tiles of this CTA's column sweep (independent of y); coalesced:
+  // warp w reads rows 16 w .. 16 w + 15, lane l the float4 column l of each
+  const int wq = tid >> 5, ln = tid & 31;
+  auto ld_tile = [&](int i, float4* dst) {
+    const float4* p = reinterpret_cast<const float4*>(W + tlin(i, k) * TILE_F) + 16 * wq * (CT / 4) + ln;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) dst[q] = __ldcg(p + q);
+    for (int q = 0; q < 16; ++q) dst[q] = __ldcg(p + q * (CT / 4));
   };
-  // ping-pong register buffers: tile j+2's loads are issued while tile j is used
   float4 bx[16], by[16];
-  if (k > 2) ld_tile(0, bx);
-  if (k > 3) ld_tile(1, by);
-  __syncthreads();
-  auto fold = [&](int j, float4* buf) {
-    fetch_block(y + CT * j, vs, gen);
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int c = 64 * h + 4 * q;
-      s0 = fmaf(buf[q].x, vs[c], s0);
-      s1 = fmaf(buf[q].y, vs[c + 1], s1);
-      s2 = fmaf(buf[q].z, vs[c + 2], s2);
-      s3 = fmaf(buf[q].w, vs[c + 3], s3);
+  if (k + 3 < nt) ld_tile(k + 3, bx);
+  if (k + 4 < nt) ld_tile(k + 4, by);
+  // off-chain sum, slots in order j = 0 .. k-3 (four polls in flight)
+  if (tid < CT) {
+    float a = (float)(D[CT * k + tid] * r[CT * k + tid]);
+    const unsigned long long* src = V + (int64_t)k * nt * CT + tid;
+    int j = 0;
+    for (; j + 3 + 2 < k; j += 4) {
+      const float v0 = get_tagged(src + (int64_t)j * CT, gen), v1 = get_tagged(src + (int64_t)(j + 1) * CT, gen);
+      const float v2 = get_tagged(src + (int64_t)(j + 2) * CT, gen), v3 = get_tagged(src + (int64_t)(j + 3) * CT, gen);
+      a -= v0; a -= v1; a -= v2; a -= v3;
     }
-    float sp = (s0 + s1) + (s2 + s3);
-    sp += __shfl_xor_sync(0xffffffffu, sp, 1);
-    __syncthreads();
-    if (h == 0) acc[row] -= sp;
-    if (j + 4 < k) ld_tile(j + 2, buf);
-  };
-  for (int j = 0; j + 2 < k; j += 2) {
-    fold(j, bx);
-    if (j + 3 < k) fold(j + 1, by);
+    for (; j + 2 < k; ++j) a -= get_tagged(src + (int64_t)j * CT, gen);
+    acc[tid] = a;
   }
   __syncthreads();
   TRI_STAMP(0, 1, k)
@@ -1880,11 +1892,40 @@ __global__ void __launch_bounds__(256, 1) k_tc_fwd(const float* __restrict__ W, 
   if (k > 0) {   // the chain: y_k = base - M1 y_{k-1}
     fetch_block(y + CT * (k - 1), vs, gen);
     const float s = coldot(M1, vs, part, false);
-    if (tid < CT) put_tagged(y + CT * k + tid, base[tid] - s, gen);
+    __syncthreads();   // vs is reused for y_k below
+    if (tid < CT) {
+      const float yk = base[tid] - s;
+      put_tagged(y + CT * k + tid, yk, gen);
+      vs[tid] = yk;
+    }
   } else if (tid < CT) {
     put_tagged(y + CT * k + tid, base[tid], gen);
+    vs[tid] = base[tid];
   }
   TRI_STAMP(0, 3, k)
+  __syncthreads();
+  // column sweep: V[i][k] = L_ik y_k for i >= k+3.  Each lane dots its float4 of 16
+  // rows with y, then a 5-stage butterfly (16 shuffles) leaves row
+  // 16 w + (l4 l3 l2 l1) summed over the warp in lanes with l0 = 0 (fixed order).
+  const float4 yv = reinterpret_cast<const float4*>(vs)[ln];
+  auto sweep = [&](int i, float4* buf) {
+    float pr[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+      pr[q] = fmaf(buf[q].w, yv.w, fmaf(buf[q].z, yv.z, fmaf(buf[q].y, yv.y, buf[q].x * yv.x)));
+    bfly_stage<8, 16>(pr, ln);
+    bfly_stage<4, 8>(pr, ln);
+    bfly_stage<2, 4>(pr, ln);
+    bfly_stage<1, 2>(pr, ln);
+    const float sp = pr[0] + __shfl_xor_sync(0xffffffffu, pr[0], 1);
+    const int r = 16 * wq + (((ln >> 4) & 1) << 3 | ((ln >> 3) & 1) << 2 | ((ln >> 2) & 1) << 1 | ((ln >> 1) & 1));
+    if ((ln & 1) == 0) put_tagged(V + ((int64_t)i * nt + k) * CT + r, sp, gen);
+    if (i + 2 < nt) ld_tile(i + 2, buf);
+  };
+  for (int i = k + 3; i < nt; i += 2) {
+    sweep(i, bx);
+    if (i + 1 < nt) sweep(i + 1, by);
+  }
 }
 
 // backward: L^T z = y.  With T1 = L_{k+1,k} Linv_kk, T2 = L_{k+2,k} Linv_kk:
@@ -1892,7 +1933,8 @@ __global__ void __launch_bounds__(256, 1) k_tc_fwd(const float* __restrict__ W, 
 // then x += D z (fp64) with max |dx|, max |x|.  T1, T2 precomputed (k_tc_prep).
 __global__ void __launch_bounds__(256, 1) k_tc_bwd(const float* __restrict__ W, const float* __restrict__ F,
                                                    int nt, const unsigned long long* __restrict__ y,
-                                                   unsigned long long* __restrict__ z, const double* __restrict__ D,
+                                                   unsigned long long* __restrict__ z,
+                                                   unsigned long long* __restrict__ U, const double* __restrict__ D,
                                                    double* __restrict__ x, double* __restrict__ dxmax,
                                                    double* __restrict__ xmax, int gen, const int* __restrict__ stop) {
   extern __shared__ __align__(16) unsigned char tri_raw[];
@@ -1907,41 +1949,31 @@ __global__ void __launch_bounds__(256, 1) k_tc_bwd(const float* __restrict__ W, 
   const int k = nt - 1 - blockIdx.x;
   tri_prefetch(Lin, W + tlin(k, k) * TILE_F, T1, k + 1 < nt ? F + ((int64_t)3 * nt + k) * TILE_F : nullptr, T2,
                k + 2 < nt ? F + ((int64_t)4 * nt + k) * TILE_F : nullptr, bar);
-  if (tid < CT) acc[tid] = get_tagged(y + CT * k + tid, gen);   // y_k (the forward pass is complete)
-  __syncthreads();
-  // off the chain: global tiles L_ik (i > k+2), column sums; two tiles ahead in registers
-  {
-    const int col = tid & (CT - 1), h = tid >> 7;
-    float cx[64], cy[64];   // ping-pong: tile i-2's loads issued while tile i is used
-    auto ld_col = [&](int i, float* dst) {
-      const float* T = W + tlin(i, k) * TILE_F;
+  // the first two tiles of this CTA's row sweep L_{k,kk}, kk = k-3, k-4, ... (contiguous);
+  // coalesced: warp w reads rows 16 w .. 16 w + 15, lane l the float4 column l of each
+  const int wq = tid >> 5, ln = tid & 31;
+  float4 cx[16], cy[16];
+  auto ld_col = [&](int kk, float4* dst) {
+    const float4* p = reinterpret_cast<const float4*>(W + tlin(k, kk) * TILE_F) + 16 * wq * (CT / 4) + ln;
 #pragma unroll
-      for (int rr = 0; rr < 64; ++rr) dst[rr] = __ldcg(T + (64 * h + rr) * CT + col);
-    };
-    auto fold = [&](int i, float* buf) {
-      fetch_block(z + CT * i, vs, gen);
-      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-#pragma unroll
-      for (int rr = 0; rr < 64; rr += 4) {
-        s0 = fmaf(buf[rr], vs[64 * h + rr], s0);
-        s1 = fmaf(buf[rr + 1], vs[64 * h + rr + 1], s1);
-        s2 = fmaf(buf[rr + 2], vs[64 * h + rr + 2], s2);
-        s3 = fmaf(buf[rr + 3], vs[64 * h + rr + 3], s3);
-      }
-      const float sp = (s0 + s1) + (s2 + s3);
-      if (h == 1) part[col] = sp;
-      __syncthreads();
-      if (h == 0) acc[col] -= sp + part[col];
-      __syncthreads();
-      if (i - 2 > k + 2) ld_col(i - 2, buf);
-    };
-    if (nt - 1 > k + 2) ld_col(nt - 1, cx);
-    if (nt - 2 > k + 2) ld_col(nt - 2, cy);
-    for (int i = nt - 1; i > k + 2; i -= 2) {
-      fold(i, cx);
-      if (i - 1 > k + 2) fold(i - 1, cy);
+    for (int q = 0; q < 16; ++q) dst[q] = __ldcg(p + q * (CT / 4));
+  };
+  if (k - 3 >= 0) ld_col(k - 3, cx);
+  if (k - 4 >= 0) ld_col(k - 4, cy);
+  // off-chain sum: acc = y_k - sum_{i = nt-1 down to k+3} U[k][i],  U[k][i] = L_ik^T z_i
+  if (tid < CT) {
+    float a = get_tagged(y + CT * k + tid, gen);   // y_k (the forward pass is complete)
+    const unsigned long long* src = U + (int64_t)k * nt * CT + tid;
+    int i = nt - 1;
+    for (; i - 3 > k + 2; i -= 4) {
+      const float v0 = get_tagged(src + (int64_t)i * CT, gen), v1 = get_tagged(src + (int64_t)(i - 1) * CT, gen);
+      const float v2 = get_tagged(src + (int64_t)(i - 2) * CT, gen), v3 = get_tagged(src + (int64_t)(i - 3) * CT, gen);
+      a -= v0; a -= v1; a -= v2; a -= v3;
     }
+    for (; i > k + 2; --i) a -= get_tagged(src + (int64_t)i * CT, gen);
+    acc[tid] = a;
   }
+  __syncthreads();
   tc_mbar_wait(bar, 0);
   {
     const float b = coldot(Lin, acc, part, false);
@@ -1962,8 +1994,10 @@ __global__ void __launch_bounds__(256, 1) k_tc_bwd(const float* __restrict__ W, 
   } else {
     zk = (tid < CT) ? base[tid] : 0.f;
   }
+  __syncthreads();   // vs is reused for z_k below
   if (tid < CT) {
     put_tagged(z + CT * k + tid, zk, gen);
+    vs[tid] = zk;
     const double dxv = D[CT * k + tid] * (double)zk;
     const double xn = x[CT * k + tid] + dxv;
     x[CT * k + tid] = xn;
@@ -1972,6 +2006,36 @@ __global__ void __launch_bounds__(256, 1) k_tc_bwd(const float* __restrict__ W, 
       atomicMax(reinterpret_cast<unsigned long long*>(dxmax), (unsigned long long)__double_as_longlong(fabs(dxv)));
     if (xmax)
       atomicMax(reinterpret_cast<unsigned long long*>(xmax), (unsigned long long)__double_as_longlong(fabs(xn)));
+  }
+  __syncthreads();
+  // row sweep: U[kk][k] = L_{k,kk}^T z_k for kk <= k-3 (column sums): per-warp float4
+  // partials over 16 rows, then the 8 warps' partials summed in order through smem
+  __shared__ float4 red[8][CT / 4];
+  auto sweep = [&](int kk, float4* buf) {
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const float zr = vs[16 * wq + q];
+      a.x = fmaf(buf[q].x, zr, a.x);
+      a.y = fmaf(buf[q].y, zr, a.y);
+      a.z = fmaf(buf[q].z, zr, a.z);
+      a.w = fmaf(buf[q].w, zr, a.w);
+    }
+    red[wq][ln] = a;
+    __syncthreads();
+    if (tid < CT) {
+      const float* rf = reinterpret_cast<const float*>(red);
+      float sp = rf[tid];
+#pragma unroll
+      for (int w2 = 1; w2 < 8; ++w2) sp += rf[w2 * CT + tid];
+      put_tagged(U + ((int64_t)kk * nt + k) * CT + tid, sp, gen);
+    }
+    __syncthreads();
+    if (kk - 2 >= 0) ld_col(kk - 2, buf);
+  };
+  for (int kk = k - 3; kk >= 0; kk -= 2) {
+    sweep(kk, cx);
+    if (kk - 1 >= 0) sweep(kk - 1, cy);
   }
 }
 
@@ -2052,8 +2116,9 @@ size_t chol_tc_ws_bytes(int npad) {
   return sizeof(float) * (size_t)ntl * TILE_F * 3                  // W + two image parts
          + sizeof(float) * (size_t)5 * nt * TILE_F                  // folded solve matrices
          + sizeof(double) * ((size_t)npad * 4)                      // D, r, y, z
+         + sizeof(unsigned long long) * (size_t)2 * nt * npad       // off-chain slots of the solves
          + sizeof(double) * (size_t)nb * nb * SYB                   // symv partials
-         + sizeof(int) * ((size_t)2 * nt * nt + 2 + 2 * (size_t)nt) + 256 * 10;
+         + sizeof(int) * ((size_t)2 * nt * nt + 2 + 2 * (size_t)nt) + 256 * 12;
 }
 
 // Solve H x = b (H: fp64 column-major, lower triangle read, npad = nt * 128,
@@ -2078,6 +2143,8 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
   double* r = reinterpret_cast<double*>(take(sizeof(double) * npad));
   unsigned long long* y = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * npad));
   unsigned long long* z = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * npad));
+  unsigned long long* Vs = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * (size_t)nt * npad));
+  unsigned long long* Us = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * (size_t)nt * npad));
   double* P = reinterpret_cast<double*>(take(sizeof(double) * (size_t)nb * nb * SYB));
   int* flags = reinterpret_cast<int*>(take(sizeof(int) * ((size_t)2 * nt * nt + 1)));
   int* sfl = reinterpret_cast<int*>(take(sizeof(int) * 2 * (size_t)nt));
@@ -2130,8 +2197,8 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
       launch_count();
       rhs = r;
     }
-    k_tc_fwd<<<nt, 256, TRI_SMEM, st>>>(W, Fm, nt, rhs, D, y, gen + 2 * it, stop);
-    k_tc_bwd<<<nt, 256, TRI_SMEM, st>>>(W, Fm, nt, y, z, D, x, out2, out2 + 1, gen + 2 * it, stop);
+    k_tc_fwd<<<nt, 256, TRI_SMEM, st>>>(W, Fm, nt, rhs, D, y, Vs, gen + 2 * it, stop);
+    k_tc_bwd<<<nt, 256, TRI_SMEM, st>>>(W, Fm, nt, y, z, Us, D, x, out2, out2 + 1, gen + 2 * it, stop);
 #ifdef VBA_TRI_PROF
     if (it == 0) {
       unsigned long long h[2][4][256];
