@@ -1837,7 +1837,7 @@ __global__ void __launch_bounds__(256, 1) k_tc_fwd(const float* __restrict__ W, 
                                                    int nt, const double* __restrict__ r,
                                                    const double* __restrict__ D, unsigned long long* __restrict__ y,
                                                    unsigned long long* __restrict__ V, int gen,
-                                                   const int* __restrict__ stop) {
+                                                   const int* __restrict__ stop, int helpers) {
   extern __shared__ __align__(16) unsigned char tri_raw[];
   float* Lin = reinterpret_cast<float*>(tri_raw);     // Linv_kk^T
   float* M1 = Lin + TILE_F;                           // M1^T
@@ -1845,11 +1845,16 @@ __global__ void __launch_bounds__(256, 1) k_tc_fwd(const float* __restrict__ W, 
   uint64_t* bar = reinterpret_cast<uint64_t*>(M2 + TILE_F);
   __shared__ float vs[CT], acc[CT], base[CT], part[CT];
   if (*stop) return;   // refinement converged in an earlier pass
-  const int tid = threadIdx.x, k = blockIdx.x;
+  // CTAs nt .. 2 nt - 1 (when helpers): sweep-only helpers taking every other tile of column k
+  const int tid = threadIdx.x;
+  const bool helper = (int)blockIdx.x >= nt;
+  const int k = helper ? (int)blockIdx.x - nt : (int)blockIdx.x;
   if (k >= nt) return;
+  const int sstep = helpers ? 2 : 1, i0 = k + 3 + (helper ? 1 : 0);
   TRI_STAMP(0, 0, k)
-  tri_prefetch(Lin, F + (int64_t)k * TILE_F, M1, k > 0 ? F + ((int64_t)nt + k) * TILE_F : nullptr, M2,
-               k > 1 ? F + ((int64_t)2 * nt + k) * TILE_F : nullptr, bar);
+  if (!helper)
+    tri_prefetch(Lin, F + (int64_t)k * TILE_F, M1, k > 0 ? F + ((int64_t)nt + k) * TILE_F : nullptr, M2,
+                 k > 1 ? F + ((int64_t)2 * nt + k) * TILE_F : nullptr, bar);
   // the first two tiles of this CTA's column sweep (independent of y); coalesced:
   // warp w reads rows 16 w .. 16 w + 15, lane l the float4 column l of each
   const int wq = tid >> 5, ln = tid & 31;
@@ -1859,8 +1864,11 @@ __global__ void __launch_bounds__(256, 1) k_tc_fwd(const float* __restrict__ W, 
     for (int q = 0; q < 16; ++q) dst[q] = __ldcg(p + q * (CT / 4));
   };
   float4 bx[16], by[16];
-  if (k + 3 < nt) ld_tile(k + 3, bx);
-  if (k + 4 < nt) ld_tile(k + 4, by);
+  if (i0 < nt) ld_tile(i0, bx);
+  if (i0 + sstep < nt) ld_tile(i0 + sstep, by);
+  if (helper) {
+    fetch_block(y + CT * k, vs, gen);
+  } else {
   // off-chain sum, slots in order j = 0 .. k-3 (four polls in flight)
   if (tid < CT) {
     float a = (float)(D[CT * k + tid] * r[CT * k + tid]);
@@ -1904,6 +1912,7 @@ __global__ void __launch_bounds__(256, 1) k_tc_fwd(const float* __restrict__ W, 
   }
   TRI_STAMP(0, 3, k)
   __syncthreads();
+  }   // chain CTA
   // column sweep: V[i][k] = L_ik y_k for i >= k+3.  Each lane dots its float4 of 16
   // rows with y, then a 5-stage butterfly (16 shuffles) leaves row
   // 16 w + (l4 l3 l2 l1) summed over the warp in lanes with l0 = 0 (fixed order).
@@ -1920,11 +1929,11 @@ __global__ void __launch_bounds__(256, 1) k_tc_fwd(const float* __restrict__ W, 
     const float sp = pr[0] + __shfl_xor_sync(0xffffffffu, pr[0], 1);
     const int r = 16 * wq + (((ln >> 4) & 1) << 3 | ((ln >> 3) & 1) << 2 | ((ln >> 2) & 1) << 1 | ((ln >> 1) & 1));
     if ((ln & 1) == 0) put_tagged(V + ((int64_t)i * nt + k) * CT + r, sp, gen);
-    if (i + 2 < nt) ld_tile(i + 2, buf);
+    if (i + 2 * sstep < nt) ld_tile(i + 2 * sstep, buf);
   };
-  for (int i = k + 3; i < nt; i += 2) {
+  for (int i = i0; i < nt; i += 2 * sstep) {
     sweep(i, bx);
-    if (i + 1 < nt) sweep(i + 1, by);
+    if (i + sstep < nt) sweep(i + sstep, by);
   }
 }
 
@@ -1936,7 +1945,8 @@ __global__ void __launch_bounds__(256, 1) k_tc_bwd(const float* __restrict__ W, 
                                                    unsigned long long* __restrict__ z,
                                                    unsigned long long* __restrict__ U, const double* __restrict__ D,
                                                    double* __restrict__ x, double* __restrict__ dxmax,
-                                                   double* __restrict__ xmax, int gen, const int* __restrict__ stop) {
+                                                   double* __restrict__ xmax, int gen, const int* __restrict__ stop,
+                                                   int helpers) {
   extern __shared__ __align__(16) unsigned char tri_raw[];
   float* Lin = reinterpret_cast<float*>(tri_raw);     // Linv_kk
   float* T1 = Lin + TILE_F;
@@ -1945,10 +1955,15 @@ __global__ void __launch_bounds__(256, 1) k_tc_bwd(const float* __restrict__ W, 
   __shared__ float vs[CT], acc[CT], base[CT], part[CT];
   if (*stop) return;
   const int tid = threadIdx.x;
-  if ((int)blockIdx.x >= nt) return;
-  const int k = nt - 1 - blockIdx.x;
-  tri_prefetch(Lin, W + tlin(k, k) * TILE_F, T1, k + 1 < nt ? F + ((int64_t)3 * nt + k) * TILE_F : nullptr, T2,
-               k + 2 < nt ? F + ((int64_t)4 * nt + k) * TILE_F : nullptr, bar);
+  // CTAs nt .. 2 nt - 1 (when helpers): sweep-only helpers taking every other tile of row k
+  const bool helper = (int)blockIdx.x >= nt;
+  const int bk = helper ? (int)blockIdx.x - nt : (int)blockIdx.x;
+  if (bk >= nt) return;
+  const int k = nt - 1 - bk;
+  const int sstep = helpers ? 2 : 1, k0 = k - 3 - (helper ? 1 : 0);
+  if (!helper)
+    tri_prefetch(Lin, W + tlin(k, k) * TILE_F, T1, k + 1 < nt ? F + ((int64_t)3 * nt + k) * TILE_F : nullptr, T2,
+                 k + 2 < nt ? F + ((int64_t)4 * nt + k) * TILE_F : nullptr, bar);
   // the first two tiles of this CTA's row sweep L_{k,kk}, kk = k-3, k-4, ... (contiguous);
   // coalesced: warp w reads rows 16 w .. 16 w + 15, lane l the float4 column l of each
   const int wq = tid >> 5, ln = tid & 31;
@@ -1958,8 +1973,11 @@ __global__ void __launch_bounds__(256, 1) k_tc_bwd(const float* __restrict__ W, 
 #pragma unroll
     for (int q = 0; q < 16; ++q) dst[q] = __ldcg(p + q * (CT / 4));
   };
-  if (k - 3 >= 0) ld_col(k - 3, cx);
-  if (k - 4 >= 0) ld_col(k - 4, cy);
+  if (k0 >= 0) ld_col(k0, cx);
+  if (k0 - sstep >= 0) ld_col(k0 - sstep, cy);
+  if (helper) {
+    fetch_block(z + CT * k, vs, gen);
+  } else {
   // off-chain sum: acc = y_k - sum_{i = nt-1 down to k+3} U[k][i],  U[k][i] = L_ik^T z_i
   if (tid < CT) {
     float a = get_tagged(y + CT * k + tid, gen);   // y_k (the forward pass is complete)
@@ -2001,13 +2019,20 @@ __global__ void __launch_bounds__(256, 1) k_tc_bwd(const float* __restrict__ W, 
     const double dxv = D[CT * k + tid] * (double)zk;
     const double xn = x[CT * k + tid] + dxv;
     x[CT * k + tid] = xn;
-    // max |dx|, max |x| (non-negative doubles order like their bit patterns)
-    if (dxmax)
-      atomicMax(reinterpret_cast<unsigned long long*>(dxmax), (unsigned long long)__double_as_longlong(fabs(dxv)));
-    if (xmax)
-      atomicMax(reinterpret_cast<unsigned long long*>(xmax), (unsigned long long)__double_as_longlong(fabs(xn)));
+    // max |dx|, max |x| (non-negative doubles order like their bit patterns): warp max, one atomic per warp
+    double m1 = fabs(dxv), m2 = fabs(xn);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      m1 = fmax(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+      m2 = fmax(m2, __shfl_xor_sync(0xffffffffu, m2, o));
+    }
+    if ((tid & 31) == 0) {
+      if (dxmax) atomicMax(reinterpret_cast<unsigned long long*>(dxmax), (unsigned long long)__double_as_longlong(m1));
+      if (xmax) atomicMax(reinterpret_cast<unsigned long long*>(xmax), (unsigned long long)__double_as_longlong(m2));
+    }
   }
   __syncthreads();
+  }   // chain CTA
   // row sweep: U[kk][k] = L_{k,kk}^T z_k for kk <= k-3 (column sums): per-warp float4
   // partials over 16 rows, then the 8 warps' partials summed in order through smem
   __shared__ float4 red[8][CT / 4];
@@ -2031,22 +2056,23 @@ __global__ void __launch_bounds__(256, 1) k_tc_bwd(const float* __restrict__ W, 
       put_tagged(U + ((int64_t)kk * nt + k) * CT + tid, sp, gen);
     }
     __syncthreads();
-    if (kk - 2 >= 0) ld_col(kk - 2, buf);
+    if (kk - 2 * sstep >= 0) ld_col(kk - 2 * sstep, buf);
   };
-  for (int kk = k - 3; kk >= 0; kk -= 2) {
+  for (int kk = k0; kk >= 0; kk -= 2 * sstep) {
     sweep(kk, cx);
-    if (kk - 1 >= 0) sweep(kk - 1, cy);
+    if (kk - sstep >= 0) sweep(kk - sstep, cy);
   }
 }
 
 // symmetric H x from the lower triangle, 64x64 fp64 blocks: P[a][b][0..64) = contribution
 // of block (max(a,b), min(a,b)) to rows of block a
 constexpr int SYB = 64;
-__global__ void __launch_bounds__(128) k_tc_symv(const double* __restrict__ H, int64_t ld, int n, int nb,
+__global__ void __launch_bounds__(256) k_tc_symv(const double* __restrict__ H, int64_t ld, int n, int nb,
                                                  const double* __restrict__ x, double* __restrict__ P,
                                                  const int* __restrict__ stop) {
-  __shared__ double Ts[SYB][SYB + 1];
+  __shared__ double Ts[SYB][SYB + 1];   // Ts[c][r] = H(64 i + r, 64 j + c)
   __shared__ double xi[SYB], xj[SYB];
+  __shared__ double red[2][4][SYB];
   if (*stop) return;
   const int64_t id = blockIdx.x;
   int i = (int)((sqrt(8.0 * (double)id + 1.0) - 1.0) * 0.5);
@@ -2054,30 +2080,51 @@ __global__ void __launch_bounds__(128) k_tc_symv(const double* __restrict__ H, i
   while ((int64_t)i * (i + 1) / 2 > id) --i;
   const int j = (int)(id - (int64_t)i * (i + 1) / 2);
   const int tid = threadIdx.x;
-  for (int t = tid; t < SYB * SYB; t += 128) {
-    const int r = t % SYB, c = t / SYB;
-    const int R = SYB * i + r, C = SYB * j + c;
-    Ts[c][r] = (R < n && C < n) ? H[(int64_t)C * ld + R] : 0.0;
+  // 16-B loads, a warp reads 512 contiguous bytes (one column); all loads before the stores
+  double2 v[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int t2 = tid + 256 * q, c = t2 >> 5, r2 = t2 & 31;
+    v[q] = __ldcg(reinterpret_cast<const double2*>(H + (int64_t)(SYB * j + c) * ld + SYB * i) + r2);
   }
   if (tid < SYB) {
     const int R = SYB * i + tid, C = SYB * j + tid;
     xi[tid] = R < n ? x[R] : 0.0;
     xj[tid] = C < n ? x[C] : 0.0;
   }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int t2 = tid + 256 * q, c = t2 >> 5, r = 2 * (t2 & 31);
+    const bool cin = SYB * j + c < n;
+    Ts[c][r] = (cin && SYB * i + r < n) ? v[q].x : 0.0;
+    Ts[c][r + 1] = (cin && SYB * i + r + 1 < n) ? v[q].y : 0.0;
+  }
   __syncthreads();
-  if (tid < SYB) {   // rows of block i: sum_c H(r, c) x_j[c]
-    const int r = tid;
+  const int l = tid & (SYB - 1), qq = tid >> 6;   // 4 quarters of 16
+  {   // rows of block i: sum_c H(r, c) x_j[c], c in quarter qq
+    const int r = l;
     double s = 0.0;
-    for (int c = 0; c < SYB; ++c) {
+#pragma unroll
+    for (int cc = 0; cc < 16; ++cc) {
+      const int c = 16 * qq + cc;
       const double hv = (i != j || c <= r) ? Ts[c][r] : Ts[r][c];
       s = fma(hv, xj[c], s);
     }
-    P[((int64_t)i * nb + j) * SYB + r] = s;
-  } else if (i != j) {   // rows of block j: sum_r H(r, c) x_i[r]
-    const int c = tid - SYB;
+    red[0][qq][r] = s;
+  }
+  if (i != j) {   // rows of block j: sum_r H(r, c) x_i[r], r in quarter qq
+    const int c = l;
     double s = 0.0;
-    for (int r = 0; r < SYB; ++r) s = fma(Ts[c][r], xi[r], s);
-    P[((int64_t)j * nb + i) * SYB + c] = s;
+#pragma unroll
+    for (int rr = 0; rr < 16; ++rr) s = fma(Ts[c][16 * qq + rr], xi[16 * qq + rr], s);
+    red[1][qq][c] = s;
+  }
+  __syncthreads();
+  if (tid < SYB) {
+    P[((int64_t)i * nb + j) * SYB + tid] = ((red[0][0][tid] + red[0][1][tid]) + red[0][2][tid]) + red[0][3][tid];
+  } else if (tid < 2 * SYB && i != j) {
+    const int c = tid - SYB;
+    P[((int64_t)j * nb + i) * SYB + c] = ((red[1][0][c] + red[1][1][c]) + red[1][2][c]) + red[1][3][c];
   }
 }
 
@@ -2191,14 +2238,18 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
   for (int it = 0; it < iters; ++it) {
     const double* rhs = b;
     if (it > 0) {
-      k_tc_symv<<<(unsigned)((int64_t)nb * (nb + 1) / 2), 128, 0, st>>>(H, ld, n, nb, x, P, stop);
+      k_tc_symv<<<(unsigned)((int64_t)nb * (nb + 1) / 2), 256, 0, st>>>(H, ld, n, nb, x, P, stop);
       k_tc_resid<<<(npad + 255) / 256, 256, 0, st>>>(b, P, n, npad, nb, r, stop);
       launch_count();
       launch_count();
       rhs = r;
     }
-    k_tc_fwd<<<nt, 256, TRI_SMEM, st>>>(W, Fm, nt, rhs, D, y, Vs, gen + 2 * it, stop);
-    k_tc_bwd<<<nt, 256, TRI_SMEM, st>>>(W, Fm, nt, y, z, Us, D, x, out2, out2 + 1, gen + 2 * it, stop);
+    // one chain CTA per block row, plus a sweep helper per block row when 2 nt CTAs
+    // fit on the GPU at once (all CTAs of these kernels must be co-resident)
+    const int hlp = 2 * nt <= sms ? 1 : 0;
+    k_tc_fwd<<<nt * (1 + hlp), 256, TRI_SMEM, st>>>(W, Fm, nt, rhs, D, y, Vs, gen + 2 * it, stop, hlp);
+    k_tc_bwd<<<nt * (1 + hlp), 256, TRI_SMEM, st>>>(W, Fm, nt, y, z, Us, D, x, out2, out2 + 1, gen + 2 * it,
+                                                    stop, hlp);
 #ifdef VBA_TRI_PROF
     if (it == 0) {
       unsigned long long h[2][4][256];
