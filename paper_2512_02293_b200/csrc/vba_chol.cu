@@ -951,14 +951,15 @@ __device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
 #ifdef VBA_TRSM_PROF
   long long tp0 = clock64();
 #endif
-  // the thread's share of A (row m = tid / 2, 16 K elements of each chunk): all loads first
-  const int m = tid >> 1, u0 = (tid & 1) * 4;
+  // the thread's share of A: 16-B unit u = tid % 8 of rows tid / 8 + 32 q of each chunk
+  // (a warp reads four full 128-B chunk rows per instruction); all loads first
+  const int u0 = tid & 7, m0 = tid >> 3;
   float4 areg[TNCH][4];
 #pragma unroll
   for (int ch = 0; ch < TNCH; ++ch)
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      areg[ch][q] = __ldcg(reinterpret_cast<const float4*>(Wik + (int64_t)m * CT + ch * TKC + 4 * u0) + q);
+      areg[ch][q] = __ldcg(reinterpret_cast<const float4*>(Wik + (int64_t)(m0 + 32 * q) * CT + ch * TKC + 4 * u0));
 #pragma unroll
   for (int ch = 0; ch < TNCH; ++ch) {
     const uint32_t n = R.nfill++;
@@ -982,7 +983,8 @@ __device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
         h.y = tf32_rna(x.y); l.y = tf32_rna(x.y - h.y);
         h.z = tf32_rna(x.z); l.z = tf32_rna(x.z - h.z);
         h.w = tf32_rna(x.w); l.w = tf32_rna(x.w - h.w);
-        const int off = (m >> 3) * 256 + (m & 7) * 32 + (((u0 + q) ^ (m & 7)) << 2);
+        const int m = m0 + 32 * q;
+        const int off = (m >> 3) * 256 + (m & 7) * 32 + ((u0 ^ (m & 7)) << 2);
         *reinterpret_cast<float4*>(hi + off) = h;
         *reinterpret_cast<float4*>(lo + off) = l;
       }
