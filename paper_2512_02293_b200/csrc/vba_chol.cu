@@ -24,7 +24,9 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
+#include <tuple>
 
 #include "vba_internal.cuh"
 
@@ -860,6 +862,7 @@ __device__ __forceinline__ void tc_bulk_store(void* gdst, const void* ssrc, uint
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(su32(ssrc)), "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void tc_bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void tc_bulk_commit_wait() {
   asm volatile("cp.async.bulk.commit_group;\n cp.async.bulk.wait_group 0;" ::: "memory");
 }
@@ -1078,6 +1081,111 @@ __device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
 
 // Diagonal SYRK of DIAG(k): W_{k+1,k+1} -= L L^T with L = L_{k+1,k} already in shared
 // memory as chunk images (tc_task_trsm keep_smem): A and B descriptors share them.
+// TRSM(i,k) of the DIAG task: B = Linv_kk images already in shared memory at
+// 2 ch TCHUNK (POTRF's output), A = W_ik split into two 32-KB chunk buffers at
+// TC_EPI_OFF (chunk ch in buffer ch & 1; chunk ch >= 2 waits for the MMAs of ch - 2 on
+// dbar).  While the MMAs run, POTRF's bulk stores are drained and done[k][k] is
+// published.  The epilogue leaves L_ik's images in shared memory for the SYRK and
+// starts (does not wait for) their bulk stores.
+__device__ void tc_diag_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_t& nacc, uint32_t tmem, int i,
+                             int k, uint64_t* dbar, uint32_t* dcnt) {
+  const int tid = threadIdx.x;
+  const float* Wik = a.W + tlin(i, k) * TILE_F;
+  const int u0 = tid & 7, m0 = tid >> 3;
+  float4 areg[TNCH][4];
+#pragma unroll
+  for (int ch = 0; ch < TNCH; ++ch)
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      areg[ch][q] = __ldcg(reinterpret_cast<const float4*>(Wik + (int64_t)(m0 + 32 * q) * CT + ch * TKC + 4 * u0));
+#pragma unroll
+  for (int ch = 0; ch < TNCH; ++ch) {
+    const int b = ch & 1;
+    if (ch >= 2) tc_mbar_wait(&dbar[b], (dcnt[b] - 1) & 1);
+    unsigned char* abuf = R.base + TC_EPI_OFF + (size_t)b * 2 * TCHUNK;
+    float* hi = reinterpret_cast<float*>(abuf);
+    float* lo = reinterpret_cast<float*>(abuf + TCHUNK);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 x = areg[ch][q];
+      float4 h, l;
+      h.x = tf32_rna(x.x); l.x = tf32_rna(x.x - h.x);
+      h.y = tf32_rna(x.y); l.y = tf32_rna(x.y - h.y);
+      h.z = tf32_rna(x.z); l.z = tf32_rna(x.z - h.z);
+      h.w = tf32_rna(x.w); l.w = tf32_rna(x.w - h.w);
+      const int m = m0 + 32 * q;
+      const int off = (m >> 3) * 256 + (m & 7) * 32 + ((u0 ^ (m & 7)) << 2);
+      *reinterpret_cast<float4*>(hi + off) = h;
+      *reinterpret_cast<float4*>(lo + off) = l;
+    }
+    proxy_fence_shared();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t ah = su32(abuf), al = ah + TCHUNK, bh = su32(R.base + (size_t)2 * ch * TCHUNK);
+#pragma unroll
+      for (int kk = 0; kk < TKC / 8; ++kk) tc_mma3(tmem, ah + 32u * kk, al + 32u * kk, bh + 32u * kk, ch == 0 && kk == 0);
+      tc_commit(&dbar[b]);
+    }
+    ++dcnt[b];
+  }
+  if (tid == 0) tc_commit(accf);
+  // publish POTRF(k): its bulk image stores and W_kk stores complete, then done[k][k]
+  if (tid == 0) {
+    tc_bulk_wait_all();
+    proxy_fence_global();
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) st_release(&a.done[k * a.nt + k], 1);
+  tc_mbar_wait(accf, nacc & 1);
+  ++nacc;
+  tc_fence_after();
+  {
+    const int w = tid >> 5, lane = tid & 31;
+    const int row = 32 * (w & 3) + lane, c0 = 64 * (w >> 2);
+    float* S = reinterpret_cast<float*>(R.base + TC_EPI_OFF);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float v[32];
+      tmem_ld_sum(tmem + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)(c0 + 32 * h), v);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int cc = c0 + 32 * h + 4 * q, ch = cc >> 5;
+        const float4 x = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        *reinterpret_cast<float4*>(S + row * EPS + cc) = x;
+        float4 hh, ll;
+        hh.x = tf32_rna(x.x); ll.x = tf32_rna(x.x - hh.x);
+        hh.y = tf32_rna(x.y); ll.y = tf32_rna(x.y - hh.y);
+        hh.z = tf32_rna(x.z); ll.z = tf32_rna(x.z - hh.z);
+        hh.w = tf32_rna(x.w); ll.w = tf32_rna(x.w - hh.w);
+        const int o2 = img_off(row, cc) - ch * (CT * TKC);
+        float* sh = reinterpret_cast<float*>(R.base + (size_t)2 * ch * TCHUNK);
+        *reinterpret_cast<float4*>(sh + o2) = hh;
+        *reinterpret_cast<float4*>(sh + CT * TKC + o2) = ll;
+      }
+    }
+    tc_fence_before();
+    proxy_fence_shared();
+    __syncthreads();
+    if (tid == 0) {
+      float* ihi = a.img + tlin(i, k) * 2 * TILE_F;
+#pragma unroll
+      for (int ch = 0; ch < TNCH; ++ch) {
+        tc_bulk_store(ihi + ch * (CT * TKC), R.base + (size_t)2 * ch * TCHUNK, TCHUNK);
+        tc_bulk_store(ihi + TILE_F + ch * (CT * TKC), R.base + (size_t)(2 * ch + 1) * TCHUNK, TCHUNK);
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    float* Lg = a.W + tlin(i, k) * TILE_F;
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+      __stcg(reinterpret_cast<float4*>(Lg) + (16 * w + q) * (CT / 4) + lane,
+             *reinterpret_cast<const float4*>(S + (16 * w + q) * EPS + 4 * lane));
+  }
+  __syncthreads();   // S is reused by the SYRK epilogue
+}
+
 __device__ void tc_task_syrk_smem(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_t& nacc, uint32_t tmem,
                                   int i) {
   const int tid = threadIdx.x;
@@ -1289,7 +1397,7 @@ __device__ __forceinline__ void diag8(float* Ws, float* Xf, int c0, int* bad) {
 // where Y starts as I and ends as L^-1 (forward substitution L Y = I fused into
 // the factorisation).  Linv goes to W_kk (fp32 row-major, zeros above the
 // diagonal, for the triangular solves) and to its hi/lo images (TRSM operand).
-__device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d) {
+__device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d, bool defer = false) {
   float* Ws = reinterpret_cast<float*>(smem_d);   // tile, then L (column-major, SWF)
   float* Xf = Ws + CT * SWF;                      // Y -> Linv (row-major, SWF)
   __shared__ int bad;
@@ -1439,27 +1547,48 @@ __device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d) {
   }
   if (tid == 0 && bad) atomicExch(a.status, 1);
   if (ph && tid == 0) ph[9] = gtimer();
-  // outputs: Linv row-major fp32 (+ hi/lo images), zeros above the diagonal
-  float* ihi = a.img + tlin(k, k) * 2 * TILE_F;
-  float* ilo = ihi + TILE_F;
-  for (int t4 = tid; t4 < CT * CT / 4; t4 += CHOL_THREADS) {
-    const int r = t4 / (CT / 4), c = 4 * (t4 % (CT / 4));
+  // outputs: Linv row-major fp32 to W_kk (coalesced stores) and its hi/lo chunk images,
+  // built in shared memory at 2 ch TCHUNK (hi) / + TCHUNK (lo) -- the B operand of the
+  // DIAG task's TRSM -- and copied out by bulk stores.  With `defer` the caller waits
+  // for the bulk stores (tc_bulk_commit_wait) and fences before publishing done[k][k].
+  float4 xo[CT * CT / 4 / CHOL_THREADS];
+#pragma unroll
+  for (int u = 0; u < CT * CT / 4 / CHOL_THREADS; ++u) {
+    const int t4 = tid + u * CHOL_THREADS, r = t4 / (CT / 4), c = 4 * (t4 % (CT / 4));
     const float4 y = *reinterpret_cast<const float4*>(Xf + r * SWF + c);
-    const float4 x = make_float4(c <= r ? y.x : 0.f, c + 1 <= r ? y.y : 0.f, c + 2 <= r ? y.z : 0.f,
-                                 c + 3 <= r ? y.w : 0.f);
+    xo[u] = make_float4(c <= r ? y.x : 0.f, c + 1 <= r ? y.y : 0.f, c + 2 <= r ? y.z : 0.f, c + 3 <= r ? y.w : 0.f);
+  }
+  __syncthreads();   // Ws / Xf are dead: the images overwrite them
+  unsigned char* sbase = reinterpret_cast<unsigned char*>(smem_d);
+#pragma unroll
+  for (int u = 0; u < CT * CT / 4 / CHOL_THREADS; ++u) {
+    const int t4 = tid + u * CHOL_THREADS, r = t4 / (CT / 4), c = 4 * (t4 % (CT / 4)), ch = c >> 5;
+    const float4 x = xo[u];
     __stcg(reinterpret_cast<float4*>(Wk + r * CT + c), x);
     float4 hh, ll;
     hh.x = tf32_rna(x.x); ll.x = tf32_rna(x.x - hh.x);
     hh.y = tf32_rna(x.y); ll.y = tf32_rna(x.y - hh.y);
     hh.z = tf32_rna(x.z); ll.z = tf32_rna(x.z - hh.z);
     hh.w = tf32_rna(x.w); ll.w = tf32_rna(x.w - hh.w);
-    const int off = img_off(r, c);
-    __stcg(reinterpret_cast<float4*>(ihi + off), hh);
-    __stcg(reinterpret_cast<float4*>(ilo + off), ll);
+    const int o2 = img_off(r, c) - ch * (CT * TKC);
+    float* sh = reinterpret_cast<float*>(sbase + (size_t)2 * ch * TCHUNK);
+    *reinterpret_cast<float4*>(sh + o2) = hh;
+    *reinterpret_cast<float4*>(sh + CT * TKC + o2) = ll;
+  }
+  proxy_fence_shared();   // generic image writes -> bulk-copy / tcgen05 reads
+  __syncthreads();
+  if (tid == 0) {
+    float* ihi = a.img + tlin(k, k) * 2 * TILE_F;
+#pragma unroll
+    for (int ch = 0; ch < TNCH; ++ch) {
+      tc_bulk_store(ihi + ch * (CT * TKC), sbase + (size_t)2 * ch * TCHUNK, TCHUNK);
+      tc_bulk_store(ihi + TILE_F + ch * (CT * TKC), sbase + (size_t)(2 * ch + 1) * TCHUNK, TCHUNK);
+    }
+    if (!defer) tc_bulk_commit_wait();
+    else asm volatile("cp.async.bulk.commit_group;" ::: "memory");
   }
   if (ph && tid == 0) { ph[10] = gtimer(); ph[12] = clock64(); }
-  __syncthreads();
-  proxy_fence_shared();   // generic smem writes before later bulk copies into the same bytes
+  if (!defer) __syncthreads();
 }
 
 __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
@@ -1467,10 +1596,11 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
   // 1024-B aligned (SW128 operand images) by pointer arithmetic on the __shared__
   // array itself, so the compiler keeps the shared state space (LDS/STS, not generic)
   unsigned char* sm = tc_raw + ((1024u - (su32(tc_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t full[TC_STAGES], empty[TC_STAGES], accf;
+  __shared__ uint64_t full[TC_STAGES], empty[TC_STAGES], accf, dbar[2];
   __shared__ uint32_t tmem_sh;
   __shared__ int tsk;
   const int tid = threadIdx.x, nt = a.nt;
+  uint32_t dcnt[2] = {0u, 0u};   // commits issued on dbar[0..1] (identical in every thread)
   if (tid < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_sh)),
                  "n"(TC_TMEM_COLS));
@@ -1482,6 +1612,8 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
       tc_mbar_init(&empty[s], 1);
     }
     tc_mbar_init(&accf, 1);
+    tc_mbar_init(&dbar[0], 1);
+    tc_mbar_init(&dbar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   tc_fence_before();
@@ -1526,31 +1658,61 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
         wait_geq(&a.upd[k * nt + k], T.expect);
         __syncthreads();
         if (a.trace && tid == 0) a.trace[4 * t + 1] = gtimer();
-        tc_task_potrf(a, k, reinterpret_cast<double*>(sm));
-        proxy_fence_global();
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) st_release(&a.done[k * nt + k], 1);
-        if (k + 1 < nt) {
-          unsigned long long* ph = a.trace ? a.trace + 4 * (size_t)a.ntasks + 16 * (size_t)k : nullptr;
-          wait_geq(&a.upd[(k + 1) * nt + k], k);
-          __syncthreads();
-          if (ph && tid == 0) ph[4] = gtimer();
-          tc_task_trsm(a, R, &accf, nacc, tmem, k + 1, k, true);
+        if (k + 1 >= nt) {
+          tc_task_potrf(a, k, reinterpret_cast<double*>(sm));
           proxy_fence_global();
           __threadfence();
           __syncthreads();
-          if (tid == 0) st_release(&a.done[(k + 1) * nt + k], 1);
-          if (ph && tid == 0) ph[5] = gtimer();
-          wait_geq(&a.upd[(k + 1) * nt + k + 1], k);
-          __syncthreads();
-          if (ph && tid == 0) ph[6] = gtimer();
-          tc_task_syrk_smem(a, R, &accf, nacc, tmem, k + 1);
-          __threadfence();
-          __syncthreads();
-          if (tid == 0) st_release(&a.upd[(k + 1) * nt + k + 1], k + 1);
-          if (ph && tid == 0) ph[7] = gtimer();
+          if (tid == 0) st_release(&a.done[k * nt + k], 1);
+          break;
         }
+        // POTRF's outputs stay in shared memory as the TRSM's B operand; done[k][k] is
+        // published inside tc_diag_trsm once POTRF's stores have drained
+        tc_task_potrf(a, k, reinterpret_cast<double*>(sm), true);
+        unsigned long long* ph = a.trace ? a.trace + 4 * (size_t)a.ntasks + 16 * (size_t)k : nullptr;
+        wait_geq(&a.upd[(k + 1) * nt + k], k);
+        __syncthreads();
+        if (ph && tid == 0) ph[4] = gtimer();
+        tc_diag_trsm(a, R, &accf, nacc, tmem, k + 1, k, dbar, dcnt);
+        if (ph && tid == 0) ph[5] = gtimer();
+        wait_geq(&a.upd[(k + 1) * nt + k + 1], k);
+        __syncthreads();
+        if (ph && tid == 0) ph[6] = gtimer();
+        {   // SYRK(k+1) from the images in shared memory; L_{k+1,k} is published while it runs
+          float* Cg = a.W + tlin(k + 1, k + 1) * TILE_F;
+          if (tid == 0) {
+            tc_fence_after();
+            for (int ch = 0; ch < TNCH; ++ch) {
+              const uint32_t hi = su32(R.base + (size_t)2 * ch * TCHUNK), lo = hi + TCHUNK;
+#pragma unroll
+              for (int kk = 0; kk < TKC / 8; ++kk)
+                tc_mma3(tmem, hi + 32u * kk, lo + 32u * kk, hi + 32u * kk, ch == 0 && kk == 0);
+            }
+            tc_commit(&accf);
+          }
+          float4 o[16];
+          tc_epi_prefetch(Cg, o);
+          if (tid == 0) {
+            tc_bulk_wait_all();   // L_{k+1,k} images out
+            proxy_fence_global();
+          }
+          __threadfence();        // L_{k+1,k} fp32 rows out
+          __syncthreads();
+          if (tid == 0) st_release(&a.done[(k + 1) * nt + k], 1);
+          tc_mbar_wait(&accf, nacc & 1);
+          ++nacc;
+          tc_fence_after();
+          float* S = reinterpret_cast<float*>(R.base + TC_EPI_OFF);
+          tc_epi_stage(tmem, S);
+          tc_fence_before();
+          __syncthreads();
+          tc_epi_sub_store(Cg, o, S);
+          proxy_fence_shared();
+        }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) st_release(&a.upd[(k + 1) * nt + k + 1], k + 1);
+        if (ph && tid == 0) ph[7] = gtimer();
         break;
       }
       case T_GEMM:
@@ -2318,6 +2480,41 @@ void chol_trace_print(const char* tag, const unsigned long long* d_trace, const 
     busy[ty] += (double)(tr[4 * q + 2] - tr[4 * q + 1]) * 1e-3;
     wait[ty] += (double)(tr[4 * q + 1] - tr[4 * q]) * 1e-3;
     cnt[ty] += 1;
+  }
+  {   // the DIAG chain: idle gaps between DIAG(k) done and DIAG(k+1) ready
+    std::vector<std::pair<int, int>> dg;
+    for (int q = 0; q < ntasks; ++q)
+      if (tk[q].type == T_DIAG && tr[4 * q]) dg.push_back({tk[q].k, q});
+    std::sort(dg.begin(), dg.end());
+    double gap = 0.0, gmax = 0.0;
+    int kmax = -1;
+    for (size_t u = 1; u < dg.size(); ++u) {
+      const double g = ((double)tr[4 * dg[u].second + 1] - (double)tr[4 * dg[u - 1].second + 2]) * 1e-3;
+      gap += g;
+      if (g > gmax) { gmax = g; kmax = dg[u].first; }
+    }
+    if (getenv("VBA_CHOL_TRACE_TILE")) {   // all tasks on the tiles (k,k), (k+1,k) of one DIAG(k)
+      const int kk = atoi(getenv("VBA_CHOL_TRACE_TILE"));
+      for (int q = 0; q < ntasks; ++q) {
+        const CholTask& T = tk[q];
+        const bool hit = (T.type == T_GEMM && T.j == kk && (T.i == kk || T.i == kk + 1)) ||
+                         (T.type == T_TRSM && (T.i == kk || T.i == kk + 1)) || (T.type == T_DIAG && T.k >= kk - 2 && T.k <= kk);
+        if (hit && tr[4 * q])
+          fprintf(stderr, "   task %6d type %d (i %d j %d k %d k2 %d exp %d): grab %8.1f ready %8.1f done %8.1f sm %llu\n", q,
+                  T.type, T.i, T.j, T.k, T.k2, T.expect, ((double)tr[4 * q] - (double)t0) * 1e-3,
+                  ((double)tr[4 * q + 1] - (double)t0) * 1e-3, ((double)tr[4 * q + 2] - (double)t0) * 1e-3, tr[4 * q + 3]);
+      }
+    }
+    if (getenv("VBA_CHOL_TRACE_GAPS")) {
+      fprintf(stderr, "  gaps:");
+      for (size_t u = 1; u < dg.size(); ++u)
+        fprintf(stderr, " %.0f", ((double)tr[4 * dg[u].second + 1] - (double)tr[4 * dg[u - 1].second + 2]) * 1e-3);
+      fprintf(stderr, "\n");
+    }
+    if (!dg.empty())
+      fprintf(stderr, "  DIAG chain: first ready at %.1f us, gaps %.1f us total (max %.1f us before k=%d), last done %.1f us\n",
+              ((double)tr[4 * dg[0].second + 1] - (double)t0) * 1e-3, gap, gmax, kmax,
+              ((double)tr[4 * dg.back().second + 2] - (double)t0) * 1e-3);
   }
   const char* nm[6] = {"POTRF", "TRSM", "GEMM", "BUPD", "BSOL", "DIAG"};
   fprintf(stderr, "[%s trace] nt=%d tasks=%d span %.1f us\n", tag, nt, ntasks, (double)(t1 - t0) * 1e-3);
