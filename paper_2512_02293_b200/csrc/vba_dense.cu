@@ -127,6 +127,24 @@ void launch_add_ridge(double* H, int64_t ld, int n, double ridge, cudaStream_t s
   launch_count();
 }
 
+// Lower triangle of the leading n x n block of a column-major matrix <-> a packed
+// buffer (column c at c n - c (c - 1) / 2, rows c .. n-1): the multi-GPU all-reduce
+// moves n (n + 1) / 2 doubles instead of npad^2.  One CTA per column, coalesced.
+__global__ void k_pack_lower(double* H, int64_t ld, int n, double* buf, int unpack) {
+  const int c = blockIdx.x;
+  const int64_t off = (int64_t)c * n - (int64_t)c * (c - 1) / 2;
+  double* col = H + (int64_t)c * ld;
+  for (int r = c + threadIdx.x; r < n; r += blockDim.x) {
+    if (unpack) col[r] = buf[off + (r - c)];
+    else buf[off + (r - c)] = col[r];
+  }
+}
+void launch_pack_lower(double* H, int64_t ld, int n, double* buf, int unpack, cudaStream_t st) {
+  if (n <= 0) return;
+  k_pack_lower<<<n, 256, 0, st>>>(H, ld, n, buf, unpack);
+  launch_count();
+}
+
 // identity padding of the tile-padded matrix (rows/cols n..npad) and zero rhs padding
 __global__ void k_pad_identity(double* H, int64_t ld, int n, int npad, double* rhs) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

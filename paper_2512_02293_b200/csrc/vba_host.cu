@@ -137,6 +137,7 @@ struct Ctx {
   Result* d_res = nullptr;
   Result* h_res = nullptr;
   vba_allreduce_fn coll = nullptr;
+  double* d_hpack = nullptr;   // packed lower triangle of H_red for the multi-GPU all-reduce
   void* coll_user = nullptr;
   bool have_step = false;
   double last_lam = 0.0;
@@ -704,7 +705,12 @@ static int stage_step(Ctx* c, double lam, cudaStream_t st) {
     // right-hand side -g_red: the step solves H_red dx = -g_red (solver.py:287)
     launch_assemble_vec(c->red.sptr, c->red.vs, c->red.nseg, c->red.soff, c->d_arena, -1.0, c->d_rhs, st);
     if (multi) {
-      if (c->coll(c->coll_user, c->d_H, (int64_t)c->npad * c->npad, 0, st)) { set_err("allreduce(H) failed"); return VBA_E_CUDA; }
+      // only the lower triangle of the nfree x nfree block is read by the solves: it is
+      // packed for the all-reduce (half the bytes of the square matrix)
+      if (!c->d_hpack && dalloc(c, &c->d_hpack, (size_t)c->nfree * (c->nfree + 1) / 2)) return VBA_E_CUDA;
+      launch_pack_lower(c->d_H, c->npad, c->nfree, c->d_hpack, 0, st);
+      if (c->coll(c->coll_user, c->d_hpack, (int64_t)c->nfree * (c->nfree + 1) / 2, 0, st)) { set_err("allreduce(H) failed"); return VBA_E_CUDA; }
+      launch_pack_lower(c->d_H, c->npad, c->nfree, c->d_hpack, 1, st);
       if (c->coll(c->coll_user, c->d_rhs, c->npad, 0, st)) { set_err("allreduce(g) failed"); return VBA_E_CUDA; }
       launch_add_ridge(c->d_H, c->npad, c->nfree, c->O.ridge, st);
     }

@@ -317,6 +317,7 @@ void launch_assemble(const int32_t* blk_ptr, const int32_t* blk_nff, const Contr
 void launch_assemble_vec(const int32_t* seg_ptr, const Vec* vecs, int nseg, const int32_t* seg_off,
                          const double* arena, double scale, double* g, cudaStream_t st, int skip_fill = 0);
 void launch_add_ridge(double* H, int64_t ld, int n, double ridge, cudaStream_t st);
+void launch_pack_lower(double* H, int64_t ld, int n, double* buf, int unpack, cudaStream_t st);
 void launch_pad_identity(double* H, int64_t ld, int n, int npad, double* rhs, cudaStream_t st);
 // tile-task DAG Cholesky (vba_chol.cu): plan writes up to `cap` task records into `out`
 // (opaque, chol_task_bytes() each) and returns the task count

@@ -267,3 +267,32 @@ def test_solve_windows_streams_bitwise_equal(cuda_ok):
         assert torch.equal(ref.d_disp.cpu(), outs[s][1])
         ref.close()
     dp.close()
+
+
+def test_sharded_reduction_path_with_identity_collective(cuda_ok):
+    """The multi-GPU assembly path (all blocks written, lower triangle packed for the
+    all-reduce, unpacked, ridge added after the reduction) run on one GPU through an
+    identity collective (a world of one) gives exactly the single-GPU step."""
+    from paper_2512_02293_b200 import _lib as Lb
+    from paper_2512_02293_b200.problem import pack_graph
+    from paper_2512_02293_b200.workloads import make_workload
+    P = pack_graph(make_workload(1))
+    opts = {"max_iterations": 1}
+    calls = []
+
+    def _ident(user, buf, count, op, stream):
+        calls.append(int(count))
+        return 0
+
+    cfn = Lb.ALLREDUCE_FN(_ident)
+    a = _dp(copy.deepcopy(P), opts)
+    b = _dp(copy.deepcopy(P), opts)
+    Lb.check(b.lib.vba_set_collective(b.ctx, cfn, None))
+    a.linearize()
+    b.linearize()
+    sa = a.solve_step(1e-3)
+    sb = b.solve_step(1e-3)
+    assert calls and max(calls) < a.H.K * 15 * (a.H.K * 15 + 1) // 2 + 1   # packed, not npad^2
+    assert np.array_equal(sa[0], sb[0]) and np.array_equal(sa[1], sb[1])
+    a.close()
+    b.close()
