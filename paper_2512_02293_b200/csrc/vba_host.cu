@@ -688,10 +688,8 @@ static int stage_step(Ctx* c, double lam, cudaStream_t st) {
     launch_gram(c->P.pixel_mode, c->d_gtiles, (int)c->gtiles.size(), kGramBlock, c->gram_smem, c->kmax, s,
                 c->pix, c->P.wts, c->d_eoff, c->d_doff, c->P.grid_w, c->grid, c->intr, c->d_Hdd, c->d_gd, lam,
                 c->O.ridge, c->d_gram_part, st);
-    launch_gram_reduce(c->d_gsrc, (int)c->gsrc.size(), c->d_g0, c->d_g1, c->d_gtiles, c->d_seb, c->d_see,
-                       c->d_goff, c->d_gram_part, c->d_gram, st);
-    launch_fill_transform(c->d_gsrc, (int)c->gsrc.size(), c->d_seb, c->d_see, c->d_goff, c->d_foff, c->d_gram, s,
-                          c->extr, c->d_arena + c->arena_fill, c->kmax, st);
+    launch_fill_transform(c->d_gsrc, (int)c->gsrc.size(), c->d_seb, c->d_see, c->d_g0, c->d_g1, c->d_gtiles,
+                          c->d_foff, c->d_gram_part, s, c->extr, c->d_arena + c->arena_fill, c->kmax, st);
   }
   mark(c, 3, st);
   if (c->nfree > 0) {
@@ -987,7 +985,7 @@ int vba_create(void** out, const vba_problem* prob, const vba_options* opts, voi
   if ((rc = dalloc(c, &c->d_part, (size_t)c->n_part * kPartStride / 2)) ||
       (rc = dalloc(c, &c->d_tile_e, c->chunks.size() * kPartWarps)) || (rc = dalloc(c, &c->d_arena, (size_t)c->arena_len)) ||
       (rc = dalloc(c, &c->d_gram_part, (size_t)c->gram_part_len)) ||
-      (rc = dalloc(c, &c->d_gram, (size_t)c->gram_len)) || (rc = dalloc(c, &c->d_Hdd, (size_t)c->n_disp)) ||
+      (rc = dalloc(c, &c->d_gram, (size_t)1)) || (rc = dalloc(c, &c->d_Hdd, (size_t)c->n_disp)) ||
       (rc = dalloc(c, &c->d_gd, (size_t)c->n_disp)) || (rc = dalloc(c, &c->d_ustep, (size_t)8 * c->E)) ||
       (rc = dalloc(c, &c->d_dxd, (size_t)c->n_disp)) || (rc = dalloc(c, &c->d_L, (size_t)kImuL * c->F)) ||
       (rc = dalloc(c, &c->d_imu_status, 1)) || (rc = dalloc(c, &c->d_H, (size_t)c->npad * c->npad)) ||

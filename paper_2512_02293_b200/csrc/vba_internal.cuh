@@ -289,8 +289,9 @@ void launch_gram_reduce(const int32_t* src_list, int nsrc, const int32_t* src_gt
                         const int64_t* src_gram_off, const double* gram_part, double* gram,
                         cudaStream_t st);
 void launch_fill_transform(const int32_t* src_list, int nsrc, const int32_t* src_eb, const int32_t* src_ee,
-                           const int64_t* src_gram_off, const int64_t* src_fill_off, const double* gram,
-                           const DevState& s, const Extr& x, double* fill, int kmax, cudaStream_t st);
+                           const int32_t* src_gt0, const int32_t* src_gt1, const GramTile* gt, const int64_t* foff,
+                           const double* part, const DevState& s, const Extr& x, double* fill, int kmax,
+                           cudaStream_t st);
 void launch_step_edges(const int32_t* ei, const int32_t* ej, int E, const DevState& s, const Extr& x,
                        const double* dx_full, int sdof, float* ustep, cudaStream_t st);
 size_t gram_smem_bytes(int kmax, int nsplit, int npairs, int k);

@@ -1052,18 +1052,31 @@ __device__ __forceinline__ double cblk(const double* C, int e1, int e2, int m, i
   return C[(e2 * (e2 + 1) / 2 + e1) * 36 + b * 6 + m];
 }
 
+// The source's Gram C (and b) is the fixed-order sum of its pixel-range partials,
+// formed while staging it into shared memory (no separate reduction pass).
 __global__ void k_fill_transform(const int32_t* __restrict__ srcs, const int32_t* __restrict__ seb,
-                                 const int32_t* __restrict__ see, const int64_t* __restrict__ goff,
-                                 const int64_t* __restrict__ foff, const double* __restrict__ gram,
+                                 const int32_t* __restrict__ see, const int32_t* __restrict__ g0,
+                                 const int32_t* __restrict__ g1, const GramTile* __restrict__ gt,
+                                 const int64_t* __restrict__ foff, const double* __restrict__ part, int kmax,
                                  const double* __restrict__ geo64, Extr x, double* __restrict__ fill) {
   extern __shared__ double sm[];
   const int s = srcs[blockIdx.x];
   const int eb = seb[s], k = see[s] - eb;
   const int npairs = k * (k + 1) / 2;
   double* Gi = sm;
-  double* Gj = Gi + k * 36;
-  double* D = Gj + k * 36;
-  const double* C = gram + goff[s];
+  double* Gj = Gi + kmax * 36;
+  double* D = Gj + kmax * 36;
+  double* Cs = D + kmax * 36;
+  {
+    const int len = npairs * 36 + 6 * k, t0 = g0[s], t1 = g1[s];
+    const double* p0 = part + gt[t0].out;
+    for (int i = threadIdx.x; i < len; i += blockDim.x) {
+      double acc = p0[i];
+      for (int t = t0 + 1; t < t1; ++t) acc += part[gt[t].out + i];
+      Cs[i] = acc;
+    }
+  }
+  const double* C = Cs;
   const double* b = C + npairs * 36;
   double* o = fill + foff[s];
   const int tid = threadIdx.x, nth = blockDim.x;
@@ -1073,13 +1086,20 @@ __global__ void k_fill_transform(const int32_t* __restrict__ srcs, const int32_t
     build_G(x.RbcT, x.c2, q + 9, Gj + e * 36);
   }
   __syncthreads();
-  for (int it = tid; it < k * 36; it += nth) {  // D_{e2} = sum_{e1} G_{e1,i}^T C(e1,e2)
-    const int e2 = it / 36, a = (it % 36) / 6, bcol = it % 6;
-    double acc = 0.0;
-    for (int e1 = 0; e1 < k; ++e1)
+  // D_{e2} = sum_{e1} G_{e1,i}^T C(e1,e2): a thread per (e2, row a) computes the row's 6 entries
+  for (int it = tid; it < k * 6; it += nth) {
+    const int e2 = it / 6, a = it % 6;
+    double r[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int e1 = 0; e1 < k; ++e1) {
 #pragma unroll
-      for (int m = 0; m < 6; ++m) acc += Gi[e1 * 36 + m * 6 + a] * cblk(C, e1, e2, m, bcol);
-    D[it] = acc;
+      for (int m = 0; m < 6; ++m) {
+        const double g = Gi[e1 * 36 + m * 6 + a];
+#pragma unroll
+        for (int bc = 0; bc < 6; ++bc) r[bc] = fma(g, cblk(C, e1, e2, m, bc), r[bc]);
+      }
+    }
+#pragma unroll
+    for (int bc = 0; bc < 6; ++bc) D[e2 * 36 + a * 6 + bc] = r[bc];
   }
   __syncthreads();
   if (tid < 36) {
@@ -1097,8 +1117,10 @@ __global__ void k_fill_transform(const int32_t* __restrict__ srcs, const int32_t
     for (int m = 0; m < 6; ++m) acc += D[e * 36 + a * 6 + m] * Gj[e * 36 + m * 6 + bc];
     o[36 + it] = -acc;
   }
-  for (int it = tid; it < npairs * 36; it += nth) {
-    const int p = it / 36, a = (it % 36) / 6, bc = it % 6;
+  // F_{j(e1) j(e2)} = G_{e1,j}^T C(e1,e2) G_{e2,j}: a thread per (pair, row a): row a of
+  // T = G1^T C (6 x 6 MACs), then row a of T G2
+  for (int it = tid; it < npairs * 6; it += nth) {
+    const int p = it / 6, a = it % 6;
     int e1 = (int)((sqrt(8.0 * p + 1.0) - 1.0) * 0.5);
     while ((e1 + 1) * (e1 + 2) / 2 <= p) ++e1;
     while (e1 * (e1 + 1) / 2 > p) --e1;
@@ -1106,15 +1128,20 @@ __global__ void k_fill_transform(const int32_t* __restrict__ srcs, const int32_t
     const double* Cb = C + p * 36;
     const double* G1 = Gj + e1 * 36;
     const double* G2 = Gj + e2 * 36;
-    double acc = 0.0;
+    double t[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int l = 0; l < 6; ++l) {
-      double t = 0.0;
+    for (int m = 0; m < 6; ++m) {
+      const double g = G1[m * 6 + a];
 #pragma unroll
-      for (int m = 0; m < 6; ++m) t += G1[m * 6 + a] * Cb[m * 6 + l];
-      acc += t * G2[l * 6 + bc];
+      for (int l = 0; l < 6; ++l) t[l] = fma(g, Cb[m * 6 + l], t[l]);
     }
-    o[36 + k * 36 + it] = acc;
+    double f[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int l = 0; l < 6; ++l)
+#pragma unroll
+      for (int bc = 0; bc < 6; ++bc) f[bc] = fma(t[l], G2[l * 6 + bc], f[bc]);
+#pragma unroll
+    for (int bc = 0; bc < 6; ++bc) o[36 + k * 36 + p * 36 + a * 6 + bc] = f[bc];
   }
   const int goffs = 36 + k * 36 + npairs * 36;
   if (tid < 6) {
@@ -1134,12 +1161,13 @@ __global__ void k_fill_transform(const int32_t* __restrict__ srcs, const int32_t
 }
 
 void launch_fill_transform(const int32_t* srcs, int nsrc, const int32_t* seb, const int32_t* see,
-                           const int64_t* goff, const int64_t* foff, const double* gram, const DevState& s,
-                           const Extr& x, double* fill, int kmax, cudaStream_t st) {
+                           const int32_t* g0, const int32_t* g1, const GramTile* gt, const int64_t* foff,
+                           const double* part, const DevState& s, const Extr& x, double* fill, int kmax,
+                           cudaStream_t st) {
   if (nsrc <= 0) return;
-  const size_t smem = (size_t)3 * kmax * 36 * sizeof(double);
+  const size_t smem = ((size_t)3 * kmax * 36 + (size_t)kmax * (kmax + 1) / 2 * 36 + 6 * kmax) * sizeof(double);
   cudaFuncSetAttribute(k_fill_transform, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_fill_transform<<<nsrc, 256, smem, st>>>(srcs, seb, see, goff, foff, gram, s.geo64, x, fill);
+  k_fill_transform<<<nsrc, 512, smem, st>>>(srcs, seb, see, g0, g1, gt, foff, part, kmax, s.geo64, x, fill);
   launch_count();
 }
 
@@ -1467,18 +1495,27 @@ void launch_unpad(const float* src, const int64_t* doff, const int64_t* roff, co
 // energy = sum over vision tiles (fixed order) + sum over IMU factors (fixed order)
 __global__ void k_energy_reduce(const double* __restrict__ te, int nt, const double* __restrict__ ib, int F,
                                 int ibs, int eoff, double* __restrict__ out) {
-  __shared__ double red[32];
-  double v = 0.0;
+  // both sums as strided per-thread partials + fixed-order warp / block trees (deterministic)
+  __shared__ double red[2][32];
+  double v = 0.0, u = 0.0;
   for (int i = threadIdx.x; i < nt; i += blockDim.x) v += te[i];
+  for (int f = threadIdx.x; f < F; f += blockDim.x) u += ib[(int64_t)f * ibs + eoff];
 #pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  for (int o = 16; o >= 1; o >>= 1) {
+    v += __shfl_xor_sync(0xffffffffu, v, o);
+    u += __shfl_xor_sync(0xffffffffu, u, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = v;
+    red[1][threadIdx.x >> 5] = u;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
-    double si = 0.0;
-    for (int f = 0; f < F; ++f) si += ib[(int64_t)f * ibs + eoff];
+    double s = 0.0, si = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      s += red[0][w];
+      si += red[1][w];
+    }
     out[0] = s + si;
     out[1] = s;
     out[2] = si;
