@@ -1236,17 +1236,30 @@ __global__ void __launch_bounds__(kPixBlock) k_backsub(
         load_rays<MODE>(pix, kbase, n, grid_w, gp, in, rx[2 * m], ry[2 * m], rx[2 * m + 1], ry[2 * m + 1]);
     }
   }
+  // the weight rows of edge e + 1 are loaded while edge e is computed
+  float4 wn[kTP];
+  auto ldw = [&](int e) {
+    const int64_t rb = eoff[e] + T.n0;
+#pragma unroll
+    for (int m = 0; m < kTP; ++m)
+      wn[m] = act[m] ? __ldg(reinterpret_cast<const float4*>(wts + 2 * (rb + 2 * (m * kPixBlock + tid))))
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  if (T.eb < T.ee) ldw(T.eb);
   for (int e = T.eb; e < T.ee; ++e) {
     const EdgeGeo32 g = load_geo(geo, e);
     const float4 ua = __ldg(reinterpret_cast<const float4*>(ustep + 8 * e));
     const float2 ub = __ldg(reinterpret_cast<const float2*>(ustep + 8 * e + 4));
     const int64_t rbase = eoff[e] + T.n0;
+    float4 wc[kTP];
+#pragma unroll
+    for (int m = 0; m < kTP; ++m) wc[m] = wn[m];
+    if (e + 1 < T.ee) ldw(e + 1);
 #pragma unroll
     for (int m = 0; m < kTP; ++m) {
       const int p = m * kPixBlock + tid;
-      float4 ww = make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 ww = wc[m];
       if (act[m]) {
-        ww = __ldg(reinterpret_cast<const float4*>(wts + 2 * (rbase + 2 * p)));
         if (MODE == VBA_PIX_EDGE)
           load_rays<VBA_PIX_KF>(pix, rbase - T.n0, T.n0 + 2 * p, grid_w, gp, in, rx[2 * m], ry[2 * m],
                                 rx[2 * m + 1], ry[2 * m + 1]);
