@@ -310,24 +310,26 @@ def main():
     b_lin = 16.0 * rows_r + 12.0 * Kr * N
     hbm, kind = peaks()
     achieved = b_lin / (k1_ms / 1e3) / 1e9 if k1_ms > 0 else 0.0
-    # dominant kernel: the tensor-core tile-DAG Cholesky of the reduced system (3xTF32 on
-    # tcgen05).  Useful work n^3/3 fp32-equivalent flops per factorisation; the tensor
-    # cores execute 3x that in tf32.  Peak: dense tf32 = half the measured bf16 GEMM peak.
+    # dominant kernel: the tensor-core tile-DAG Cholesky of the reduced system (fp32 operands
+    # split into fp16 hi + lo, three fp16 products per tile product on tcgen05 kind::f16).
+    # Useful work n^3/3 fp32-equivalent flops per factorisation; the tensor cores execute
+    # 3x that in fp16.  Peak: dense fp16 = the measured bf16 GEMM peak (same tcgen05 rate).
     dom = None
     if sv["solves"] > 0:
         n_red = sv["n"]
         f_ms = sv["factor_ms"] / sv["solves"]
-        bf16 = tf32 = None
+        bf16 = None
         pp = os.path.join(REPO, "MEASURED_PEAKS.json")
         if os.path.exists(pp):
             with open(pp) as f:
                 bf16 = float(json.load(f).get("bf16_tflops", 0.0)) or None
-        tf32 = (bf16 or 1590.0) / 2.0
+        f16 = bf16 or 1590.0
         useful = n_red ** 3 / 3.0 / (f_ms / 1e3) / 1e12
-        dom = {"kernel": "k_chol_tc (reduced-system Cholesky, tcgen05 kind::tf32, 3xTF32)", "bound": "tensor",
-               "achieved_tc_tflops": 3.0 * useful, "useful_fp32_tflops": useful, "peak": tf32,
-               "peak_kind": ("half of measured bf16" if bf16 else "half of fallback bf16"), "unit": "TFLOP/s",
-               "frac": 3.0 * useful / tf32, "factor_ms": f_ms,
+        dom = {"kernel": "k_chol_tc (reduced-system Cholesky, tcgen05 kind::f16, fp32 as fp16 hi+lo, 3 products)",
+               "bound": "tensor",
+               "achieved_tc_tflops": 3.0 * useful, "useful_fp32_tflops": useful, "peak": f16,
+               "peak_kind": ("measured bf16 (= fp16 rate)" if bf16 else "fallback bf16"), "unit": "TFLOP/s",
+               "frac": 3.0 * useful / f16, "factor_ms": f_ms,
                "refine_ms_per_solve": sv["refine_ms"] / sv["solves"],
                "refine_passes_per_solve": sstat["refine_passes"] / max(sstat["tc_solves"], 1),
                "fp64_fallbacks": sstat["fallbacks"], "n": n_red,

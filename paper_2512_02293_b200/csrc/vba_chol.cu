@@ -21,6 +21,7 @@
 // through L2 (.cg), so no stale L1 lines are observed.  A non-positive pivot
 // sets *status (mapped to the reference's "singular reduced pose system").
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -698,8 +699,8 @@ namespace vba {
 //        chunk is one contiguous cp.async.bulk into shared memory.
 // ===========================================================================
 
-constexpr int TKC = 32;                       // fp32 K elements per chunk (one 128-B swizzle row)
-constexpr int TNCH = CT / TKC;                // 4 chunks per tile
+constexpr int TKC = 32;                       // 4-byte words per chunk row (one 128-B swizzle row = 64 fp16)
+constexpr int TNCH = CT / (2 * TKC);          // 2 K-chunks of 64 per tile
 constexpr uint32_t TCHUNK = CT * TKC * 4;     // 16 KB
 constexpr int TC_STAGES = 3;
 constexpr uint32_t TSTAGE = 4 * TCHUNK;       // A_hi A_lo B_hi B_lo
@@ -709,10 +710,11 @@ constexpr size_t TC_EPI_OFF = (size_t)8 * TCHUNK;
 constexpr size_t TC_EPI_END = TC_EPI_OFF + (size_t)CT * (CT + 4) * 4;
 constexpr size_t TC_SMEM_0 = TC_RING > POTRF_SMEM ? TC_RING : POTRF_SMEM;
 constexpr size_t TC_SMEM = (TC_SMEM_0 > TC_EPI_END ? TC_SMEM_0 : TC_EPI_END) + 1024;
-constexpr int64_t TILE_F = (int64_t)CT * CT;  // floats per tile (and per image part)
+constexpr int64_t TILE_F = (int64_t)CT * CT;  // floats per tile (= the two fp16 image parts of a tile)
+constexpr int64_t IMGP_F = TILE_F / 2;        // one fp16 image part, in 4-byte words
 // instruction descriptor: D f32, A/B tf32, both K-major, N = 128, M = 128
-constexpr uint32_t tc_idesc(int n) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(CT >> 4) << 24);
+constexpr uint32_t tc_idesc(int n) {   // D f32, A/B f16 (format 0), both K-major, M = 128
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(CT >> 4) << 24);
 }
 constexpr uint32_t TC_IDESC = tc_idesc(CT);        // M = N = 128
 constexpr uint32_t TC_IDESC2 = tc_idesc(2 * CT);   // M = 128, N = 256
@@ -744,10 +746,23 @@ __device__ __forceinline__ float tf32_rna(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
-// float offset of element (row r, col c) inside one image part (see layout above)
+// fp16 offset of element (row r, col c) inside one image part (see layout above):
+// 64-column K-chunks, 8-row atoms of 1 KB, 16-byte units (8 fp16) XOR-swizzled by row
 __device__ __forceinline__ int img_off(int r, int c) {
-  const int q = c >> 5, e = c & 31, u = e >> 2;
-  return q * (CT * TKC) + (r >> 3) * 256 + (r & 7) * 32 + ((u ^ (r & 7)) << 2) + (e & 3);
+  const int q = c >> 6, e = c & 63, u = e >> 3;
+  return q * (CT * 64) + (r >> 3) * 512 + (r & 7) * 64 + ((u ^ (r & 7)) << 3) + (e & 7);
+}
+// x = hi + lo with hi, lo fp16 (2 x 11 significant bits; the Jacobi-scaled factors are
+// O(1), well inside the fp16 range): 4 values -> 4 hi + 4 lo halves (8 B each)
+__device__ __forceinline__ void split4_h(const float4 x, uint2& hi, uint2& lo) {
+  const __half h0 = __float2half_rn(x.x), h1 = __float2half_rn(x.y), h2 = __float2half_rn(x.z),
+               h3 = __float2half_rn(x.w);
+  const __half l0 = __float2half_rn(x.x - __half2float(h0)), l1 = __float2half_rn(x.y - __half2float(h1)),
+               l2 = __float2half_rn(x.z - __half2float(h2)), l3 = __float2half_rn(x.w - __half2float(h3));
+  hi.x = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+  hi.y = (uint32_t)__half_as_ushort(h2) | ((uint32_t)__half_as_ushort(h3) << 16);
+  lo.x = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+  lo.y = (uint32_t)__half_as_ushort(l2) | ((uint32_t)__half_as_ushort(l3) << 16);
 }
 
 __device__ __forceinline__ void tc_mbar_init(uint64_t* b, int n) {
@@ -779,7 +794,7 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem, uint64_t da, uint64_t db, 
                                        uint32_t idesc = TC_IDESC) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %3, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %4, p;\n}\n" ::"r"(tmem),
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %4, p;\n}\n" ::"r"(tmem),
       "l"(da), "l"(db), "r"(acc), "r"(idesc));
 }
 // one K-step (8 tf32) of 3xTF32 into the 256-column accumulator; b_hi is followed by b_lo
@@ -881,7 +896,7 @@ __device__ __forceinline__ void tc_chunk_mma(const TcRing& R, int s, uint32_t tm
   const uint32_t a_hi = su32(R.base + (size_t)s * TSTAGE), a_lo = a_hi + TCHUNK;
   const uint32_t b_hi = a_hi + 2 * TCHUNK, b_lo = a_hi + 3 * TCHUNK;
 #pragma unroll
-  for (int kk = 0; kk < TKC / 8; ++kk) {   // 8 tf32 (32 B) of K per MMA
+  for (int kk = 0; kk < TKC / 8; ++kk) {   // 16 fp16 (32 B) of K per MMA
     const uint32_t o = 32u * kk;
     tc_mma3(tmem, a_hi + o, a_lo + o, b_hi + o, first && kk == 0);
   }
@@ -901,14 +916,14 @@ __device__ void tc_task_gemm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
         const int s = n % TC_STAGES;
         if (n >= TC_STAGES) tc_mbar_wait(&R.empty[s], ((n / TC_STAGES) - 1) & 1);
         const int kq = q < TNCH ? k : k2, ch = q % TNCH;
-        const float* ia = a.img + tlin(i, kq) * 2 * TILE_F + ch * (CT * TKC);
-        const float* ib = a.img + tlin(j, kq) * 2 * TILE_F + ch * (CT * TKC);
+        const float* ia = a.img + tlin(i, kq) * TILE_F + ch * (CT * TKC);
+        const float* ib = a.img + tlin(j, kq) * TILE_F + ch * (CT * TKC);
         unsigned char* st = R.base + (size_t)s * TSTAGE;
         tc_expect_tx(&R.full[s], TSTAGE);
         tc_bulk(st, ia, TCHUNK, &R.full[s]);
-        tc_bulk(st + TCHUNK, ia + TILE_F, TCHUNK, &R.full[s]);
+        tc_bulk(st + TCHUNK, ia + IMGP_F, TCHUNK, &R.full[s]);
         tc_bulk(st + 2 * TCHUNK, ib, TCHUNK, &R.full[s]);
-        tc_bulk(st + 3 * TCHUNK, ib + TILE_F, TCHUNK, &R.full[s]);
+        tc_bulk(st + 3 * TCHUNK, ib + IMGP_F, TCHUNK, &R.full[s]);
       }
       const int qc = q - PRE;
       if (qc >= 0) {
@@ -949,7 +964,7 @@ __device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
                              int k, bool keep_smem = false) {
   const int tid = threadIdx.x;
   const float* Wik = a.W + tlin(i, k) * TILE_F;
-  const float* ib = a.img + tlin(k, k) * 2 * TILE_F;
+  const float* ib = a.img + tlin(k, k) * TILE_F;
   if (tid == 0) proxy_fence_global();
 #ifdef VBA_TRSM_PROF
   long long tp0 = clock64();
@@ -957,12 +972,15 @@ __device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
   // the thread's share of A: 16-B unit u = tid % 8 of rows tid / 8 + 32 q of each chunk
   // (a warp reads four full 128-B chunk rows per instruction); all loads first
   const int u0 = tid & 7, m0 = tid >> 3;
-  float4 areg[TNCH][4];
+  float4 areg[TNCH][4][2];   // unit u0 (8 columns) of rows m0 + 32 q of each 64-column chunk
 #pragma unroll
   for (int ch = 0; ch < TNCH; ++ch)
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      areg[ch][q] = __ldcg(reinterpret_cast<const float4*>(Wik + (int64_t)(m0 + 32 * q) * CT + ch * TKC + 4 * u0));
+#pragma unroll
+      for (int v = 0; v < 2; ++v)
+        areg[ch][q][v] =
+            __ldcg(reinterpret_cast<const float4*>(Wik + (int64_t)(m0 + 32 * q) * CT + 64 * ch + 8 * u0 + 4 * v));
 #pragma unroll
   for (int ch = 0; ch < TNCH; ++ch) {
     const uint32_t n = R.nfill++;
@@ -973,23 +991,20 @@ __device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
     if (tid == 0) {
       tc_expect_tx(&R.full[s], 2 * TCHUNK);
       tc_bulk(st + 2 * TCHUNK, ib + ch * (CT * TKC), TCHUNK, &R.full[s]);
-      tc_bulk(st + 3 * TCHUNK, ib + TILE_F + ch * (CT * TKC), TCHUNK, &R.full[s]);
+      tc_bulk(st + 3 * TCHUNK, ib + IMGP_F + ch * (CT * TKC), TCHUNK, &R.full[s]);
     }
     {
-      float* hi = reinterpret_cast<float*>(st);
-      float* lo = reinterpret_cast<float*>(st + TCHUNK);
+      unsigned char* hi = st;
+      unsigned char* lo = st + TCHUNK;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const float4 x = areg[ch][q];
-        float4 h, l;
-        h.x = tf32_rna(x.x); l.x = tf32_rna(x.x - h.x);
-        h.y = tf32_rna(x.y); l.y = tf32_rna(x.y - h.y);
-        h.z = tf32_rna(x.z); l.z = tf32_rna(x.z - h.z);
-        h.w = tf32_rna(x.w); l.w = tf32_rna(x.w - h.w);
+        uint2 h0, l0, h1, l1;
+        split4_h(areg[ch][q][0], h0, l0);
+        split4_h(areg[ch][q][1], h1, l1);
         const int m = m0 + 32 * q;
-        const int off = (m >> 3) * 256 + (m & 7) * 32 + ((u0 ^ (m & 7)) << 2);
-        *reinterpret_cast<float4*>(hi + off) = h;
-        *reinterpret_cast<float4*>(lo + off) = l;
+        const int off = (m >> 3) * 1024 + (m & 7) * 128 + ((u0 ^ (m & 7)) << 4);   // bytes
+        *reinterpret_cast<uint4*>(hi + off) = make_uint4(h0.x, h0.y, h1.x, h1.y);
+        *reinterpret_cast<uint4*>(lo + off) = make_uint4(l0.x, l0.y, l1.x, l1.y);
       }
     }
     proxy_fence_shared();
@@ -1025,18 +1040,15 @@ __device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
       tmem_ld_sum(tmem + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)(c0 + 32 * h), v);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const int cc = c0 + 32 * h + 4 * q, ch = cc >> 5;
+        const int cc = c0 + 32 * h + 4 * q, ch = cc >> 6;
         const float4 x = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         *reinterpret_cast<float4*>(S + row * EPS + cc) = x;
-        float4 hh, ll;
-        hh.x = tf32_rna(x.x); ll.x = tf32_rna(x.x - hh.x);
-        hh.y = tf32_rna(x.y); ll.y = tf32_rna(x.y - hh.y);
-        hh.z = tf32_rna(x.z); ll.z = tf32_rna(x.z - hh.z);
-        hh.w = tf32_rna(x.w); ll.w = tf32_rna(x.w - hh.w);
-        const int o2 = img_off(row, cc) - ch * (CT * TKC);
-        float* sh = reinterpret_cast<float*>(R.base + (size_t)2 * ch * TCHUNK);
-        *reinterpret_cast<float4*>(sh + o2) = hh;
-        *reinterpret_cast<float4*>(sh + CT * TKC + o2) = ll;
+        uint2 hh, ll;
+        split4_h(x, hh, ll);
+        const int o2 = img_off(row, cc) - ch * (CT * 64);   // fp16 units within the chunk
+        unsigned char* sh = R.base + (size_t)2 * ch * TCHUNK;
+        *reinterpret_cast<uint2*>(sh + 2 * o2) = hh;
+        *reinterpret_cast<uint2*>(sh + TCHUNK + 2 * o2) = ll;
       }
     }
     tc_fence_before();
@@ -1045,12 +1057,12 @@ __device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
 #ifdef VBA_TRSM_PROF
     if (tid == 0) atomicAdd(&g_trsm_prof[5], (unsigned long long)(clock64() - tp2));
 #endif
-    float* ihi = a.img + tlin(i, k) * 2 * TILE_F;
+    float* ihi = a.img + tlin(i, k) * TILE_F;
     if (tid == 0) {
 #pragma unroll
       for (int ch = 0; ch < TNCH; ++ch) {
         tc_bulk_store(ihi + ch * (CT * TKC), R.base + (size_t)2 * ch * TCHUNK, TCHUNK);
-        tc_bulk_store(ihi + TILE_F + ch * (CT * TKC), R.base + (size_t)(2 * ch + 1) * TCHUNK, TCHUNK);
+        tc_bulk_store(ihi + IMGP_F + ch * (CT * TKC), R.base + (size_t)(2 * ch + 1) * TCHUNK, TCHUNK);
       }
     }
     float* Lg = a.W + tlin(i, k) * TILE_F;
@@ -1092,31 +1104,31 @@ __device__ void tc_diag_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
   const int tid = threadIdx.x;
   const float* Wik = a.W + tlin(i, k) * TILE_F;
   const int u0 = tid & 7, m0 = tid >> 3;
-  float4 areg[TNCH][4];
+  float4 areg[TNCH][4][2];   // unit u0 (8 columns) of rows m0 + 32 q of each 64-column chunk
 #pragma unroll
   for (int ch = 0; ch < TNCH; ++ch)
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      areg[ch][q] = __ldcg(reinterpret_cast<const float4*>(Wik + (int64_t)(m0 + 32 * q) * CT + ch * TKC + 4 * u0));
+#pragma unroll
+      for (int v = 0; v < 2; ++v)
+        areg[ch][q][v] =
+            __ldcg(reinterpret_cast<const float4*>(Wik + (int64_t)(m0 + 32 * q) * CT + 64 * ch + 8 * u0 + 4 * v));
 #pragma unroll
   for (int ch = 0; ch < TNCH; ++ch) {
     const int b = ch & 1;
     if (ch >= 2) tc_mbar_wait(&dbar[b], (dcnt[b] - 1) & 1);
     unsigned char* abuf = R.base + TC_EPI_OFF + (size_t)b * 2 * TCHUNK;
-    float* hi = reinterpret_cast<float*>(abuf);
-    float* lo = reinterpret_cast<float*>(abuf + TCHUNK);
+    unsigned char* hi = abuf;
+    unsigned char* lo = abuf + TCHUNK;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const float4 x = areg[ch][q];
-      float4 h, l;
-      h.x = tf32_rna(x.x); l.x = tf32_rna(x.x - h.x);
-      h.y = tf32_rna(x.y); l.y = tf32_rna(x.y - h.y);
-      h.z = tf32_rna(x.z); l.z = tf32_rna(x.z - h.z);
-      h.w = tf32_rna(x.w); l.w = tf32_rna(x.w - h.w);
+      uint2 h0, l0, h1, l1;
+      split4_h(areg[ch][q][0], h0, l0);
+      split4_h(areg[ch][q][1], h1, l1);
       const int m = m0 + 32 * q;
-      const int off = (m >> 3) * 256 + (m & 7) * 32 + ((u0 ^ (m & 7)) << 2);
-      *reinterpret_cast<float4*>(hi + off) = h;
-      *reinterpret_cast<float4*>(lo + off) = l;
+      const int off = (m >> 3) * 1024 + (m & 7) * 128 + ((u0 ^ (m & 7)) << 4);   // bytes
+      *reinterpret_cast<uint4*>(hi + off) = make_uint4(h0.x, h0.y, h1.x, h1.y);
+      *reinterpret_cast<uint4*>(lo + off) = make_uint4(l0.x, l0.y, l1.x, l1.y);
     }
     proxy_fence_shared();
     __syncthreads();
@@ -1151,29 +1163,26 @@ __device__ void tc_diag_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
       tmem_ld_sum(tmem + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)(c0 + 32 * h), v);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const int cc = c0 + 32 * h + 4 * q, ch = cc >> 5;
+        const int cc = c0 + 32 * h + 4 * q, ch = cc >> 6;
         const float4 x = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         *reinterpret_cast<float4*>(S + row * EPS + cc) = x;
-        float4 hh, ll;
-        hh.x = tf32_rna(x.x); ll.x = tf32_rna(x.x - hh.x);
-        hh.y = tf32_rna(x.y); ll.y = tf32_rna(x.y - hh.y);
-        hh.z = tf32_rna(x.z); ll.z = tf32_rna(x.z - hh.z);
-        hh.w = tf32_rna(x.w); ll.w = tf32_rna(x.w - hh.w);
-        const int o2 = img_off(row, cc) - ch * (CT * TKC);
-        float* sh = reinterpret_cast<float*>(R.base + (size_t)2 * ch * TCHUNK);
-        *reinterpret_cast<float4*>(sh + o2) = hh;
-        *reinterpret_cast<float4*>(sh + CT * TKC + o2) = ll;
+        uint2 hh, ll;
+        split4_h(x, hh, ll);
+        const int o2 = img_off(row, cc) - ch * (CT * 64);   // fp16 units within the chunk
+        unsigned char* sh = R.base + (size_t)2 * ch * TCHUNK;
+        *reinterpret_cast<uint2*>(sh + 2 * o2) = hh;
+        *reinterpret_cast<uint2*>(sh + TCHUNK + 2 * o2) = ll;
       }
     }
     tc_fence_before();
     proxy_fence_shared();
     __syncthreads();
     if (tid == 0) {
-      float* ihi = a.img + tlin(i, k) * 2 * TILE_F;
+      float* ihi = a.img + tlin(i, k) * TILE_F;
 #pragma unroll
       for (int ch = 0; ch < TNCH; ++ch) {
         tc_bulk_store(ihi + ch * (CT * TKC), R.base + (size_t)2 * ch * TCHUNK, TCHUNK);
-        tc_bulk_store(ihi + TILE_F + ch * (CT * TKC), R.base + (size_t)(2 * ch + 1) * TCHUNK, TCHUNK);
+        tc_bulk_store(ihi + IMGP_F + ch * (CT * TKC), R.base + (size_t)(2 * ch + 1) * TCHUNK, TCHUNK);
       }
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
@@ -1562,27 +1571,24 @@ __device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d, bool defer
   unsigned char* sbase = reinterpret_cast<unsigned char*>(smem_d);
 #pragma unroll
   for (int u = 0; u < CT * CT / 4 / CHOL_THREADS; ++u) {
-    const int t4 = tid + u * CHOL_THREADS, r = t4 / (CT / 4), c = 4 * (t4 % (CT / 4)), ch = c >> 5;
+    const int t4 = tid + u * CHOL_THREADS, r = t4 / (CT / 4), c = 4 * (t4 % (CT / 4)), ch = c >> 6;
     const float4 x = xo[u];
     __stcg(reinterpret_cast<float4*>(Wk + r * CT + c), x);
-    float4 hh, ll;
-    hh.x = tf32_rna(x.x); ll.x = tf32_rna(x.x - hh.x);
-    hh.y = tf32_rna(x.y); ll.y = tf32_rna(x.y - hh.y);
-    hh.z = tf32_rna(x.z); ll.z = tf32_rna(x.z - hh.z);
-    hh.w = tf32_rna(x.w); ll.w = tf32_rna(x.w - hh.w);
-    const int o2 = img_off(r, c) - ch * (CT * TKC);
-    float* sh = reinterpret_cast<float*>(sbase + (size_t)2 * ch * TCHUNK);
-    *reinterpret_cast<float4*>(sh + o2) = hh;
-    *reinterpret_cast<float4*>(sh + CT * TKC + o2) = ll;
+    uint2 hh, ll;
+    split4_h(x, hh, ll);
+    const int o2 = img_off(r, c) - ch * (CT * 64);   // fp16 units within the chunk
+    unsigned char* sh = sbase + (size_t)2 * ch * TCHUNK;
+    *reinterpret_cast<uint2*>(sh + 2 * o2) = hh;
+    *reinterpret_cast<uint2*>(sh + TCHUNK + 2 * o2) = ll;
   }
   proxy_fence_shared();   // generic image writes -> bulk-copy / tcgen05 reads
   __syncthreads();
   if (tid == 0) {
-    float* ihi = a.img + tlin(k, k) * 2 * TILE_F;
+    float* ihi = a.img + tlin(k, k) * TILE_F;
 #pragma unroll
     for (int ch = 0; ch < TNCH; ++ch) {
       tc_bulk_store(ihi + ch * (CT * TKC), sbase + (size_t)2 * ch * TCHUNK, TCHUNK);
-      tc_bulk_store(ihi + TILE_F + ch * (CT * TKC), sbase + (size_t)(2 * ch + 1) * TCHUNK, TCHUNK);
+      tc_bulk_store(ihi + IMGP_F + ch * (CT * TKC), sbase + (size_t)(2 * ch + 1) * TCHUNK, TCHUNK);
     }
     if (!defer) tc_bulk_commit_wait();
     else asm volatile("cp.async.bulk.commit_group;" ::: "memory");
