@@ -40,7 +40,7 @@ constexpr int CHOL_THREADS = 256;
 constexpr int SB = 36;           // 32x32 block stride in POTRF (doubles, = 4 mod 16)
 constexpr size_t CHOL_SMEM = (size_t)2 * 2 * KC * SP * sizeof(double);   // 2 stages x (A, B)
 
-enum TaskType { T_POTRF = 0, T_TRSM = 1, T_GEMM = 2, T_BUPD = 3, T_BSOL = 4, T_DIAG = 5 };
+enum TaskType { T_POTRF = 0, T_TRSM = 1, T_GEMM = 2, T_BUPD = 3, T_BSOL = 4, T_DIAG = 5, T_CHAIN = 6 };
 
 struct CholTask {
   int32_t type, i, j, k;
@@ -609,11 +609,12 @@ int chol_plan_tasks_tc(int nt, void* outv, int cap) {
     ++n;
   };
   if (nt <= 0) return 0;
-  push(T_DIAG, 0, 0, 0, 0);
+  // the whole POTRF -> TRSM -> SYRK chain is one task (one CTA, the diagonal tile handed
+  // from each SYRK to the next POTRF in shared memory), claimed first
+  push(T_CHAIN, 0, 0, 0, 0);
   for (int i = 2; i < nt; ++i) push(T_TRSM, i, 0, 0, 0);
   for (int s = 0; s + 1 < nt; ++s) {
     for (int i = s + 2; i < nt; ++i) push(T_GEMM, i, s + 1, s, s);      // next panel column (off-diagonal)
-    push(T_DIAG, s + 1, s + 1, s + 1, s + 1);
     for (int i = s + 3; i < nt; ++i) push(T_TRSM, i, s + 1, s + 1, s + 1);
     for (int j = s + 2; j < nt; ++j)
       for (int i = j; i < nt; ++i) {
@@ -1406,7 +1407,8 @@ __device__ __forceinline__ void diag8(float* Ws, float* Xf, int c0, int* bad) {
 // where Y starts as I and ends as L^-1 (forward substitution L Y = I fused into
 // the factorisation).  Linv goes to W_kk (fp32 row-major, zeros above the
 // diagonal, for the triangular solves) and to its hi/lo images (TRSM operand).
-__device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d, bool defer = false) {
+// from_smem: the updated diagonal tile is already in Ws (handed over by the chain's SYRK)
+__device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d, bool defer = false, bool from_smem = false) {
   float* Ws = reinterpret_cast<float*>(smem_d);   // tile, then L (column-major, SWF)
   float* Xf = Ws + CT * SWF;                      // Y -> Linv (row-major, SWF)
   __shared__ int bad;
@@ -1418,12 +1420,14 @@ __device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d, bool defer
   {   // The diagonal tile is symmetric (up to the rounding of its updates), so its
       // row-major image is read as column-major without a transpose.  Loads first.
     float4 q[16];
+    if (!from_smem) {
 #pragma unroll
-    for (int u = 0; u < 16; ++u) q[u] = __ldcg(reinterpret_cast<const float4*>(Wk) + tid + u * CHOL_THREADS);
+      for (int u = 0; u < 16; ++u) q[u] = __ldcg(reinterpret_cast<const float4*>(Wk) + tid + u * CHOL_THREADS);
+    }
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
       const int t4 = 4 * (tid + u * CHOL_THREADS), c = t4 / CT, r = t4 % CT;
-      *reinterpret_cast<float4*>(Ws + c * SWF + r) = q[u];
+      if (!from_smem) *reinterpret_cast<float4*>(Ws + c * SWF + r) = q[u];
       const float4 id = make_float4(r == c ? 1.f : 0.f, r + 1 == c ? 1.f : 0.f, r + 2 == c ? 1.f : 0.f,
                                     r + 3 == c ? 1.f : 0.f);
       *reinterpret_cast<float4*>(Xf + c * SWF + r) = id;
@@ -1659,66 +1663,89 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
         __syncthreads();
         if (tid == 0) st_release(&a.done[T.i * nt + T.k], 1);
         break;
-      case T_DIAG: {   // POTRF(k) -> TRSM(k+1,k) -> GEMM(k+1,k+1,k) in one CTA
-        const int k = T.k;
-        wait_geq(&a.upd[k * nt + k], T.expect);
-        __syncthreads();
-        if (a.trace && tid == 0) a.trace[4 * t + 1] = gtimer();
-        if (k + 1 >= nt) {
-          tc_task_potrf(a, k, reinterpret_cast<double*>(sm));
-          proxy_fence_global();
-          __threadfence();
-          __syncthreads();
-          if (tid == 0) st_release(&a.done[k * nt + k], 1);
-          break;
-        }
-        // POTRF's outputs stay in shared memory as the TRSM's B operand; done[k][k] is
-        // published inside tc_diag_trsm once POTRF's stores have drained
-        tc_task_potrf(a, k, reinterpret_cast<double*>(sm), true);
-        unsigned long long* ph = a.trace ? a.trace + 4 * (size_t)a.ntasks + 16 * (size_t)k : nullptr;
-        wait_geq(&a.upd[(k + 1) * nt + k], k);
-        __syncthreads();
-        if (ph && tid == 0) ph[4] = gtimer();
-        tc_diag_trsm(a, R, &accf, nacc, tmem, k + 1, k, dbar, dcnt);
-        if (ph && tid == 0) ph[5] = gtimer();
-        wait_geq(&a.upd[(k + 1) * nt + k + 1], k);
-        __syncthreads();
-        if (ph && tid == 0) ph[6] = gtimer();
-        {   // SYRK(k+1) from the images in shared memory; L_{k+1,k} is published while it runs
-          float* Cg = a.W + tlin(k + 1, k + 1) * TILE_F;
-          if (tid == 0) {
-            tc_fence_after();
-            for (int ch = 0; ch < TNCH; ++ch) {
-              const uint32_t hi = su32(R.base + (size_t)2 * ch * TCHUNK), lo = hi + TCHUNK;
-#pragma unroll
-              for (int kk = 0; kk < TKC / 8; ++kk)
-                tc_mma3(tmem, hi + 32u * kk, lo + 32u * kk, hi + 32u * kk, ch == 0 && kk == 0);
-            }
-            tc_commit(&accf);
+      case T_DIAG:
+      case T_CHAIN: {   // DIAG(k) = POTRF(k) -> TRSM(k+1,k) -> SYRK(k+1); T_CHAIN: every k in one CTA
+        const bool chain = T.type == T_CHAIN;
+        const int kend = chain ? nt : T.k + 1;
+        for (int k = T.k; k < kend; ++k) {
+          const bool cont = chain && k > T.k;   // the tile is in Ws: the previous step's SYRK put it there
+          if (!cont) {
+            wait_geq(&a.upd[k * nt + k], chain ? k : T.expect);
+            __syncthreads();
+            if (a.trace && tid == 0) a.trace[4 * t + 1] = gtimer();
           }
-          float4 o[16];
-          tc_epi_prefetch(Cg, o);
-          if (tid == 0) {
-            tc_bulk_wait_all();   // L_{k+1,k} images out
+          if (k + 1 >= nt) {
+            tc_task_potrf(a, k, reinterpret_cast<double*>(sm), false, cont);
             proxy_fence_global();
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) st_release(&a.done[k * nt + k], 1);
+            break;
           }
-          __threadfence();        // L_{k+1,k} fp32 rows out
+          // POTRF's outputs stay in shared memory as the TRSM's B operand; done[k][k] is
+          // published inside tc_diag_trsm once POTRF's stores have drained
+          tc_task_potrf(a, k, reinterpret_cast<double*>(sm), true, cont);
+          unsigned long long* ph = a.trace ? a.trace + 4 * (size_t)a.ntasks + 16 * (size_t)k : nullptr;
+          wait_geq(&a.upd[(k + 1) * nt + k], k);
           __syncthreads();
-          if (tid == 0) st_release(&a.done[(k + 1) * nt + k], 1);
-          tc_mbar_wait(&accf, nacc & 1);
-          ++nacc;
-          tc_fence_after();
-          float* S = reinterpret_cast<float*>(R.base + TC_EPI_OFF);
-          tc_epi_stage(tmem, S);
-          tc_fence_before();
+          if (ph && tid == 0) ph[4] = gtimer();
+          tc_diag_trsm(a, R, &accf, nacc, tmem, k + 1, k, dbar, dcnt);
+          if (ph && tid == 0) ph[5] = gtimer();
+          wait_geq(&a.upd[(k + 1) * nt + k + 1], k);
           __syncthreads();
-          tc_epi_sub_store(Cg, o, S);
-          proxy_fence_shared();
+          if (ph && tid == 0) ph[6] = gtimer();
+          {   // SYRK(k+1) from the images in shared memory; L_{k+1,k} is published while it runs
+            float* Cg = a.W + tlin(k + 1, k + 1) * TILE_F;
+            if (tid == 0) {
+              tc_fence_after();
+              for (int ch = 0; ch < TNCH; ++ch) {
+                const uint32_t hi = su32(R.base + (size_t)2 * ch * TCHUNK), lo = hi + TCHUNK;
+#pragma unroll
+                for (int kk = 0; kk < TKC / 8; ++kk)
+                  tc_mma3(tmem, hi + 32u * kk, lo + 32u * kk, hi + 32u * kk, ch == 0 && kk == 0);
+              }
+              tc_commit(&accf);
+            }
+            float4 o[16];
+            tc_epi_prefetch(Cg, o);
+            if (tid == 0) {
+              tc_bulk_wait_all();   // L_{k+1,k} images out
+              proxy_fence_global();
+            }
+            __threadfence();        // L_{k+1,k} fp32 rows out
+            __syncthreads();
+            if (tid == 0) st_release(&a.done[(k + 1) * nt + k], 1);
+            tc_mbar_wait(&accf, nacc & 1);
+            ++nacc;
+            tc_fence_after();
+            float* S = reinterpret_cast<float*>(R.base + TC_EPI_OFF);
+            tc_epi_stage(tmem, S);
+            tc_fence_before();
+            __syncthreads();
+            if (chain) {
+              // next POTRF's input straight into Ws (symmetric tile: row-major = column-major)
+              float* Wn = reinterpret_cast<float*>(sm);
+              const int w = tid >> 5, lane = tid & 31;
+#pragma unroll
+              for (int q = 0; q < 16; ++q) {
+                const float4 d = *reinterpret_cast<const float4*>(S + (16 * w + q) * EPS + 4 * lane);
+                float4 v = o[q];
+                v.x -= d.x; v.y -= d.y; v.z -= d.z; v.w -= d.w;
+                *reinterpret_cast<float4*>(Wn + (16 * w + q) * SWF + 4 * lane) = v;
+              }
+              __syncthreads();
+            } else {
+              tc_epi_sub_store(Cg, o, S);
+              proxy_fence_shared();
+            }
+          }
+          if (!chain) {
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) st_release(&a.upd[(k + 1) * nt + k + 1], k + 1);
+          }
+          if (ph && tid == 0) ph[7] = gtimer();
         }
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) st_release(&a.upd[(k + 1) * nt + k + 1], k + 1);
-        if (ph && tid == 0) ph[7] = gtimer();
         break;
       }
       case T_GEMM:
@@ -2476,8 +2503,8 @@ void chol_trace_print(const char* tag, const unsigned long long* d_trace, const 
   cudaMemcpy(tr.data(), d_trace, tr.size() * 8, cudaMemcpyDeviceToHost);
   cudaMemcpy(tk.data(), d_tasks, tk.size() * sizeof(CholTask), cudaMemcpyDeviceToHost);
   unsigned long long t0 = ~0ull, t1 = 0;
-  double busy[6] = {0, 0, 0, 0, 0, 0}, wait[6] = {0, 0, 0, 0, 0, 0};
-  int cnt[6] = {0, 0, 0, 0, 0, 0};
+  double busy[7] = {0, 0, 0, 0, 0, 0, 0}, wait[7] = {0, 0, 0, 0, 0, 0, 0};
+  int cnt[7] = {0, 0, 0, 0, 0, 0, 0};
   for (int q = 0; q < ntasks; ++q) {
     if (tr[4 * q] == 0) continue;
     t0 = std::min(t0, tr[4 * q]);
@@ -2522,9 +2549,9 @@ void chol_trace_print(const char* tag, const unsigned long long* d_trace, const 
               ((double)tr[4 * dg[0].second + 1] - (double)t0) * 1e-3, gap, gmax, kmax,
               ((double)tr[4 * dg.back().second + 2] - (double)t0) * 1e-3);
   }
-  const char* nm[6] = {"POTRF", "TRSM", "GEMM", "BUPD", "BSOL", "DIAG"};
+  const char* nm[7] = {"POTRF", "TRSM", "GEMM", "BUPD", "BSOL", "DIAG", "CHAIN"};
   fprintf(stderr, "[%s trace] nt=%d tasks=%d span %.1f us\n", tag, nt, ntasks, (double)(t1 - t0) * 1e-3);
-  for (int ty = 0; ty < 6; ++ty)
+  for (int ty = 0; ty < 7; ++ty)
     if (cnt[ty])
       fprintf(stderr, "  %-5s n=%6d  avg busy %8.2f us  avg wait %8.2f us  total busy %.1f us\n", nm[ty], cnt[ty],
               busy[ty] / cnt[ty], wait[ty] / cnt[ty], busy[ty]);
