@@ -613,14 +613,26 @@ int chol_plan_tasks_tc(int nt, void* outv, int cap) {
   // from each SYRK to the next POTRF in shared memory), claimed first
   push(T_CHAIN, 0, 0, 0, 0);
   for (int i = 2; i < nt; ++i) push(T_TRSM, i, 0, 0, 0);
+  // trailing update of tile (i, j) from column(s) s: a pair (s-1, s) for odd s, the single
+  // column s for even s and j = s + 2 (else none)
+  auto tupd = [&](int s, int i, int j) {
+    if (s & 1) push(T_GEMM, i, j, s - 1, s - 1, s);
+    else if (s == j - 2) push(T_GEMM, i, j, s, s);
+  };
   for (int s = 0; s + 1 < nt; ++s) {
-    for (int i = s + 2; i < nt; ++i) push(T_GEMM, i, s + 1, s, s);      // next panel column (off-diagonal)
+    // next panel column (off-diagonal); its first task GEMM(s+2, s+1, s) -- what the chain's
+    // TRSM(s+2, s+1) waits for -- was queued ahead of the previous step's trailing updates
+    for (int i = s == 0 ? 2 : s + 3; i < nt; ++i) push(T_GEMM, i, s + 1, s, s);
     for (int i = s + 3; i < nt; ++i) push(T_TRSM, i, s + 1, s + 1, s + 1);
+    // hoisted ahead of this step's trailing updates: the next step's first next-panel update
+    // and the next step's update of the chain's SYRK target tile (s+3, s+3)
+    if (s + 3 < nt) {
+      push(T_GEMM, s + 3, s + 2, s + 1, s + 1);
+      tupd(s + 1, s + 3, s + 3);
+    }
     for (int j = s + 2; j < nt; ++j)
-      for (int i = j; i < nt; ++i) {
-        if (s & 1) push(T_GEMM, i, j, s - 1, s - 1, s);
-        else if (s == j - 2) push(T_GEMM, i, j, s, s);
-      }
+      for (int i = j; i < nt; ++i)
+        if (!(s >= 1 && i == s + 2 && j == s + 2)) tupd(s, i, j);   // (s+2, s+2) was hoisted
   }
   return n;
 }
