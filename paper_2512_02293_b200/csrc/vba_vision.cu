@@ -842,23 +842,28 @@ __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
   const double damp = 1.0 + lam;
   const int nc = 6 * k;
   const int NRt = (nc + 1 + 7) / 8, NCt = (nc + 7) / 8;   // row / column tiles of C
-  // output tiles: lower band tj <= ti + 1 (6x6 blocks may straddle the 8-tile diagonal);
-  // tile t belongs to warp t % GWARPS, slot t / GWARPS
+  // output tiles: lower band tj <= ti + 1 (6x6 blocks may straddle the 8-tile diagonal),
+  // grouped in units of two vertically adjacent tiles (ti, tj), (ti + 1, tj) that share
+  // their B fragments (3 shared-memory loads per 2 DMMAs); unit u belongs to warp
+  // u % GWARPS, tile slots 2 (u / GWARPS) and 2 (u / GWARPS) + 1 (tile_i = -1: empty)
   __shared__ short tile_i[GWARPS * GMAXT], tile_j[GWARPS * GMAXT];
   __shared__ int ntiles_s;
   __shared__ double invs[2][kGramPC];   // 1 / (Hdd (1 + lam) + ridge) per pixel, double-buffered by chunk
   __shared__ float4 geos[32 * 4];       // the source's out-edge geometry (k <= 31), EdgeGeo32 records
   auto pixel_inv = [&](int n) { return n < T.n1 ? 1.0 / ((double)Hdd[kbase + n] * damp + ridge) : 0.0; };
   if (tid == 0) {
-    int t = 0;
-    for (int ti = 0; ti < NRt; ++ti)
-      for (int tj = 0; tj <= ti + 1 && tj < NCt; ++tj)
-        if (t < GWARPS * GMAXT) {
-          tile_i[t] = (short)ti;
-          tile_j[t] = (short)tj;
-          ++t;
+    int u = 0;
+    for (int tj = 0; tj < NCt; ++tj)
+      for (int ti = tj > 0 ? tj - 1 : 0; ti < NRt; ti += 2)
+        if (u < GWARPS * GMAXT / 2) {
+          const int w = u % GWARPS, sl = 2 * (u / GWARPS);
+          tile_i[w + GWARPS * sl] = (short)ti;
+          tile_j[w + GWARPS * sl] = (short)tj;
+          tile_i[w + GWARPS * (sl + 1)] = (short)(ti + 1 < NRt ? ti + 1 : -1);
+          tile_j[w + GWARPS * (sl + 1)] = (short)tj;
+          ++u;
         }
-    ntiles_s = t;
+    ntiles_s = u;   // units
   }
   double acc[GMAXT][2];
 #pragma unroll
@@ -868,7 +873,7 @@ __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
   if (tid < 4 * k) geos[tid] = __ldg(reinterpret_cast<const float4*>(geo + T.eb) + tid);
   __syncthreads();
   const int ntl = ntiles_s;
-  const int nmine = (ntl - warp + GWARPS - 1) / GWARPS;
+  const int nmine = 2 * ((ntl - warp + GWARPS - 1) / GWARPS);   // tile slots of this warp
 
   // Phase 1 of a chunk: coupling vectors of its (pixel, edge) items (at most kGramItems
   // per thread), widened to fp64 into buffer b.  Loads of all items first (gload),
@@ -955,14 +960,25 @@ __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
     const double* Vb = Ub + uvs;
     const int am = lane >> 2, ak = lane & 3;
 #pragma unroll
-    for (int q = 0; q < GMAXT; ++q) {
+    for (int q = 0; q < GMAXT; q += 2) {
       if (q < nmine) {
-        const double* pa = Ub + (size_t)(tile_i[warp + GWARPS * q] * 8 + am) * GPX + ak;
+        const int t1 = tile_i[warp + GWARPS * (q + 1)];
+        const double* pa0 = Ub + (size_t)(tile_i[warp + GWARPS * q] * 8 + am) * GPX + ak;
+        const double* pa1 = Ub + (size_t)((t1 >= 0 ? t1 : 0) * 8 + am) * GPX + ak;
         const double* pb = Vb + (size_t)(tile_j[warp + GWARPS * q] * 8 + am) * GPX + ak;
+        if (t1 >= 0) {
 #pragma unroll
-        for (int ks = 0; ks < kGramPC / 4; ++ks) gdmma(acc[q][0], acc[q][1], pa[4 * ks], pb[4 * ks]);
+          for (int ks = 0; ks < kGramPC / 4; ++ks) {
+            const double b = pb[4 * ks];
+            gdmma(acc[q][0], acc[q][1], pa0[4 * ks], b);
+            gdmma(acc[q + 1][0], acc[q + 1][1], pa1[4 * ks], b);
+          }
+        } else {
+#pragma unroll
+          for (int ks = 0; ks < kGramPC / 4; ++ks) gdmma(acc[q][0], acc[q][1], pa0[4 * ks], pb[4 * ks]);
+        }
       }
-      if (q % 3 == 1 && q / 3 < kGramItems && more) gitem(q / 3, cn, cb ^ 1);
+      if (q % 6 == 2 && q / 6 < kGramItems && more) gitem(q / 6, cn, cb ^ 1);
     }
     // pixel inverses of chunk c + 2 (buffer cb: chunk c's items are done)
     if (tid >= nth - kGramPC) invs[cb][tid - (nth - kGramPC)] = pixel_inv(cn + kGramPC + tid - (nth - kGramPC));
@@ -975,7 +991,7 @@ __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
   double* o = out + T.out;
 #pragma unroll
   for (int q = 0; q < GMAXT; ++q) {
-    if (q >= nmine) continue;
+    if (q >= nmine || tile_i[warp + GWARPS * q] < 0) continue;
     const int a = tile_i[warp + GWARPS * q] * 8 + (lane >> 2);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
