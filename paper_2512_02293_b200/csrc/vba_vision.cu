@@ -41,7 +41,7 @@ __host__ __device__ __forceinline__ int gram_px_stride(int kmax) {
 
 // dynamic shared memory of the DMMA Gram kernel: U and V, (6 kmax + 1 -> 8) columns x (PC + 4) pixels, fp64
 size_t gram_smem_bytes(int kmax, int /*nsplit*/, int /*npairs*/, int /*k*/) {
-  return (size_t)4 * ((6 * kmax + 1 + 7) / 8 * 8) * (kGramPC + 4) * sizeof(double);   // U, V double-buffered
+  return (size_t)2 * ((6 * kmax + 1 + 7) / 8 * 8) * (kGramPC + 4) * sizeof(double);   // W, double-buffered
 }
 struct IntrP { double fx, fy, cx, cy; };
 
@@ -850,7 +850,8 @@ __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
   __shared__ int ntiles_s;
   __shared__ double invs[2][kGramPC];   // 1 / (Hdd (1 + lam) + ridge) per pixel, double-buffered by chunk
   __shared__ float4 geos[32 * 4];       // the source's out-edge geometry (k <= 31), EdgeGeo32 records
-  auto pixel_inv = [&](int n) { return n < T.n1 ? 1.0 / ((double)Hdd[kbase + n] * damp + ridge) : 0.0; };
+  // C = sum_n u_n u_n^T / h_n is formed as W^T W with W = u / sqrt(h_n) (one staged matrix)
+  auto pixel_inv = [&](int n) { return n < T.n1 ? 1.0 / sqrt((double)Hdd[kbase + n] * damp + ridge) : 0.0; };
   if (tid == 0) {
     int u = 0;
     for (int tj = 0; tj < NCt; ++tj)
@@ -868,7 +869,7 @@ __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
   double acc[GMAXT][2];
 #pragma unroll
   for (int q = 0; q < GMAXT; ++q) acc[q][0] = acc[q][1] = 0.0;
-  for (int i = tid; i < 4 * (int)uvs; i += nth) UV[i] = 0.0;   // padding columns stay zero
+  for (int i = tid; i < 2 * (int)uvs; i += nth) UV[i] = 0.0;   // padding columns stay zero
   if (tid < kGramPC) invs[0][tid] = pixel_inv(T.n0 + tid);
   if (tid < 4 * k) geos[tid] = __ldg(reinterpret_cast<const float4*>(geo + T.eb) + tid);
   __syncthreads();
@@ -905,12 +906,11 @@ __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
   auto gitem = [&](int j, int c0, int b) {
     const int it = tid + j * nth;
     if (it >= kGramPC * k) return;
-    double* U = UV + (size_t)b * 2 * uvs;
-    double* V = U + uvs;
+    double* U = UV + (size_t)b * uvs;
     const int e = it / kGramPC, px = it % kGramPC;
     const int n = c0 + px;
     float u[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    double inv = 0.0;
+    double sc = 0.0;   // 1 / sqrt(h_n)
     if (n < T.n1) {
       const EdgeGeo32 g = load_geo<true>(reinterpret_cast<const EdgeGeo32*>(geos), e);
       const PxGeom o = project(g, rx_[j], ry_[j], d_[j]);
@@ -925,16 +925,13 @@ __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
       u[3] = c0w * -o.iz;
       u[4] = c1w * -o.iz;
       u[5] = fmaf(c0w, o.x * o.iz, c1w * (o.y * o.iz));
-      inv = invs[b][px];
-      if (e == 0) U[(size_t)nc * GPX + px] = (double)gd_[j];
+      sc = invs[b][px];
+      if (e == 0) U[(size_t)nc * GPX + px] = (double)gd_[j] * sc;
     } else if (e == 0) {
       U[(size_t)nc * GPX + px] = 0.0;
     }
 #pragma unroll
-    for (int r = 0; r < 6; ++r) {
-      U[(size_t)(6 * e + r) * GPX + px] = (double)u[r];
-      V[(size_t)(6 * e + r) * GPX + px] = (double)u[r] * inv;
-    }
+    for (int r = 0; r < 6; ++r) U[(size_t)(6 * e + r) * GPX + px] = (double)u[r] * sc;
   };
   // prologue: phase 1 of chunk 0 (buffer 0) and the pixel inverses of chunk 1
   gload(T.n0);
@@ -956,8 +953,8 @@ __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
     const int cn = c0 + kGramPC;
     const bool more = cn < T.n1;
     if (more) gload(cn);
-    const double* Ub = UV + (size_t)cb * 2 * uvs;
-    const double* Vb = Ub + uvs;
+    const double* Ub = UV + (size_t)cb * uvs;
+    const double* Vb = Ub;   // C = W^T W
     const int am = lane >> 2, ak = lane & 3;
 #pragma unroll
     for (int q = 0; q < GMAXT; q += 2) {
