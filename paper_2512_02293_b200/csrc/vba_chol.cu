@@ -1810,32 +1810,43 @@ __global__ void k_tc_diag(const double* __restrict__ H, int64_t ld, int n, int n
 // W_ij = fp32(D_i H_ij D_j) from the lower triangle (identity padding); one CTA per lower tile
 __global__ void __launch_bounds__(256) k_tc_convert(const double* __restrict__ H, int64_t ld, int n, int nt,
                                                     const double* __restrict__ D, float* __restrict__ W) {
-  __shared__ float tr[32][33];
+  // one 128x128 tile per CTA: H read column-major (a warp reads 32 consecutive rows of a
+  // column), 32 loads in flight per thread, transposed through a padded shared tile and
+  // written row-major a full row per warp instruction
+  extern __shared__ float ttile[];   // [CT][CT + 1]
   const int64_t id = blockIdx.x;
   int i = (int)((sqrt(8.0 * (double)id + 1.0) - 1.0) * 0.5);
   while ((int64_t)(i + 1) * (i + 2) / 2 <= id) ++i;
   while ((int64_t)i * (i + 1) / 2 > id) --i;
   const int j = (int)(id - (int64_t)i * (i + 1) / 2);
   float* Wt = W + id * TILE_F;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
-  for (int rb = 0; rb < CT; rb += 32)
-    for (int cb = 0; cb < CT; cb += 32) {
-      // read H column-major (coalesced over rows), write W row-major via a transpose
-      for (int c = ty; c < 32; c += 8) {
-        const int R = CT * i + rb + tx, C = CT * j + cb + c;
-        float v;
-        if (R < n && C < n) {
-          const int64_t a = (R >= C) ? (int64_t)C * ld + R : (int64_t)R * ld + C;   // lower triangle
-          v = (float)(D[R] * H[a] * D[C]);
-        } else {
-          v = (R == C) ? 1.0f : 0.0f;
-        }
-        tr[c][tx] = v;
+  const int tid = threadIdx.x;
+#pragma unroll 1
+  for (int half = 0; half < 2; ++half) {
+    float v[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int idx = tid + 256 * (q + 32 * half), c = idx >> 7, r = idx & 127;
+      const int R = CT * i + r, C = CT * j + c;
+      if (R < n && C < n) {
+        const int64_t a = (R >= C) ? (int64_t)C * ld + R : (int64_t)R * ld + C;   // lower triangle
+        v[q] = (float)(D[R] * __ldcs(H + a) * D[C]);
+      } else {
+        v[q] = (R == C) ? 1.0f : 0.0f;
       }
-      __syncthreads();
-      for (int r = ty; r < 32; r += 8) Wt[(rb + r) * CT + cb + tx] = tr[tx][r];
-      __syncthreads();
     }
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int idx = tid + 256 * (q + 32 * half), c = idx >> 7, r = idx & 127;
+      ttile[r * (CT + 1) + c] = v[q];
+    }
+  }
+  __syncthreads();
+#pragma unroll 4
+  for (int q = 0; q < 64; ++q) {
+    const int idx = tid + 256 * q, r = idx >> 7, c = idx & 127;
+    Wt[r * CT + c] = ttile[r * (CT + 1) + c];
+  }
 }
 
 // Triangular solves with the fp32 factor.  The solves only need the factor's
@@ -2411,6 +2422,8 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
     cudaFuncSetAttribute(k_tc_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRI_SMEM);
     cudaFuncSetAttribute(k_tc_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRI_SMEM);
     cudaFuncSetAttribute(k_tc_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRI_SMEM);
+    cudaFuncSetAttribute(k_tc_convert, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)((size_t)CT * (CT + 1) * sizeof(float)));
     int dev = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -2418,7 +2431,7 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
     grid = sms * (per > 0 ? per : 1);
   }
   k_tc_diag<<<(npad + 255) / 256, 256, 0, st>>>(H, ld, n, npad, D);
-  k_tc_convert<<<(unsigned)ntl, 256, 0, st>>>(H, ld, n, nt, D, W);
+  k_tc_convert<<<(unsigned)ntl, 256, (size_t)CT * (CT + 1) * sizeof(float), st>>>(H, ld, n, nt, D, W);
   cudaMemsetAsync(flags, 0, sizeof(int) * ((size_t)2 * nt * nt + 1), st);
   TcArgs a;
   a.W = W;
