@@ -296,3 +296,31 @@ def test_sharded_reduction_path_with_identity_collective(cuda_ok):
     assert np.array_equal(sa[0], sb[0]) and np.array_equal(sa[1], sb[1])
     a.close()
     b.close()
+
+
+def test_largest_config_properties(cuda_ok):
+    """BASELINE config 4 at full size (n_f = 7665, 37.7 M edge-pixels), where the fp64
+    oracle cannot run: size-independent properties of the path.
+    * determinism: two linearise + reduced-solve passes give bitwise-equal steps;
+    * the LM solve decreases the energy monotonically and reports exactly the energy the
+      energy kernel returns for the final state;
+    * no fp64 fallback of the tensor-core reduced solve."""
+    from paper_2512_02293_b200.problem import pack_graph
+    from paper_2512_02293_b200.workloads import CONFIGS, make_workload
+    P = pack_graph(make_workload(4))
+    opts = {"max_iterations": CONFIGS[4].iterations}
+    dp = _dp(P, opts)
+    dp.linearize()
+    a = dp.solve_step(1e-4)
+    dp.linearize()
+    b = dp.solve_step(1e-4)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    dp.load_state()
+    rep = dp.solve()
+    traj = rep["cost_trajectory"]
+    assert all(t1 <= t0 for t0, t1 in zip(traj, traj[1:]))
+    assert rep["final_cost"] < rep["initial_cost"]
+    assert abs(dp.energy()[0] - rep["final_cost"]) <= 1e-12 * rep["final_cost"]
+    st = _stats(dp)
+    assert st[1] == 0, st   # no fp64 fallbacks
+    dp.close()
