@@ -45,7 +45,7 @@ constexpr int kTileRt = kTilePx;   // pixels per per-pixel work tile (vba_intern
 constexpr int kGramBlock = 512;
 constexpr int kMaxOutDegree = 31;
 constexpr int NBc = 128;         // Cholesky tile (vba_chol.cu)
-constexpr int kTcMinTiles = 32;  // tensor-core reduced solve from this many 128-tiles up
+constexpr int kTcMinTiles = 4;   // tensor-core reduced solve from this many 128-tiles up (n >= 385; config 3: 8.2 -> 4.5 ms)
 
 struct Result {       // device -> host once per trial
   double energy[3];
