@@ -182,7 +182,7 @@ VBA_API int vba_stats(void* ctx, int64_t* out4);
 
 /* Standalone SPD solve H x = b of a dense fp64 n x n system (column-major,
  * lower triangle read; device pointers), replacing np.linalg.solve(Hred, -gred)
- * of solver.py:287.  mode 0: tcgen05 3xTF32 Cholesky + fp64 iterative
+ * of solver.py:287.  mode 0: tcgen05 split-fp16 (3-product) Cholesky + fp64 iterative
  * refinement (falls back to mode 1 when its checks fail), mode 1: fp64 DMMA
  * tile-DAG Cholesky, mode 2: tensor-core result unconditionally (diagnostics;
  * info[0] on entry = refinement passes, 0 -> 4).  On return info[0] = 1 if the
@@ -190,6 +190,19 @@ VBA_API int vba_stats(void* ctx, int64_t* out4);
  * non-positive fp64 pivot.  Synchronises `stream`. */
 VBA_API int vba_spd_solve(const double* H, int64_t n, const double* b, double* x, int32_t mode,
                           void* stream, int32_t* info);
+
+/* IMU preintegration of F keyframe pairs, replacing vislam/imu.py:77-167
+ * (`preintegrate`, called per pair by the tracking frontend).  Pair f owns the
+ * samples soff[f] .. soff[f+1]-1 of ts [S] (seconds), gyro [S,3] and accel [S,3];
+ * bias [F,6] = (b_g, b_a); noise [4] = (gyro, accel, gyro random walk, accel random
+ * walk) densities.  Writes out [F, VBA_PREINT_REC] = dt_total, delta_R quaternion
+ * (w,x,y,z; w >= 0), delta_p (3), delta_v (3), J_rot (3x3), J_pos (3x6), J_vel (3x6),
+ * covariance (15x15), row-major, fp64.  All pointers are device pointers.  Returns
+ * VBA_E_INVALID (the reference's ValueError) for a pair with fewer than two samples
+ * or non-increasing timestamps.  Synchronises `stream`. */
+#define VBA_PREINT_REC 281
+VBA_API int vba_preintegrate(const double* ts, const double* gyro, const double* accel, const int64_t* soff,
+                             int32_t n_pairs, const double* bias, const double* noise, double* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -15,12 +15,14 @@ LIB_PATH = os.environ.get("VBA_LIB") or os.path.join(HERE, "_vba.so")   # VBA_LI
 VBA_OK, VBA_E_INVALID, VBA_E_CUDA, VBA_E_NOT_SPD, VBA_E_COV, VBA_E_UNSUPPORTED = range(6)
 PIX_GRID, PIX_KF, PIX_EDGE = 0, 1, 2
 IMU_REC = 180
+PREINT_REC = 281
 
 EXPORTED = ("vba_last_error", "vba_version", "vba_create", "vba_destroy", "vba_set_collective",
             "vba_reduced_dim", "vba_energy", "vba_linearize", "vba_export_normal_eq",
             "vba_solve_step", "vba_export_step", "vba_apply_step", "vba_restore", "vba_accept",
             "vba_trial", "vba_solve", "vba_download", "vba_launch_count", "vba_stage_times",
-            "vba_load_state", "vba_bind_inputs", "vba_set_profiling", "vba_stats", "vba_spd_solve", "vba_solve_times")
+            "vba_load_state", "vba_bind_inputs", "vba_set_profiling", "vba_stats", "vba_spd_solve", "vba_solve_times",
+            "vba_preintegrate")
 
 
 class VbaProblem(C.Structure):
@@ -108,6 +110,7 @@ def load(path: str | None = None):
         "vba_stats": ([v, C.POINTER(C.c_int64)], C.c_int),
         "vba_solve_times": ([v, C.POINTER(C.c_double)], C.c_int),
         "vba_spd_solve": ([v, C.c_int64, v, v, C.c_int32, v, C.POINTER(C.c_int32)], C.c_int),
+        "vba_preintegrate": ([v, v, v, v, C.c_int32, v, v, v, v], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -126,7 +129,7 @@ def check(rc: int):
 def spd_solve(H, b, mode: int = 0, iters: int = 0):
     """Solve H x = b for a dense SPD fp64 torch CUDA matrix (lower triangle used).
 
-    mode 0: tcgen05 3xTF32 Cholesky + fp64 iterative refinement (fp64 fallback
+    mode 0: tcgen05 split-fp16 (3-product) Cholesky + fp64 iterative refinement (fp64 fallback
     on failed checks); mode 1: fp64 DMMA Cholesky.  Returns (x, used_tensor_cores).
     Replaces np.linalg.solve(Hred, -gred) of solver.py:287.
     """

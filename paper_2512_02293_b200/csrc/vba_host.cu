@@ -1160,6 +1160,29 @@ int vba_spd_solve(const double* H, int64_t n, const double* b, double* x, int32_
   return hs[0] ? VBA_E_NOT_SPD : VBA_OK;
 }
 
+int vba_preintegrate(const double* ts, const double* gyro, const double* accel, const int64_t* soff,
+                     int32_t n_pairs, const double* bias, const double* noise, double* out, void* stream) {
+  static_assert(VBA_PREINT_REC == kPreintRec, "preintegration record size");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_pairs < 0) { set_err("vba_preintegrate: negative pair count"); return VBA_E_INVALID; }
+  if (n_pairs == 0) return VBA_OK;
+  if (!ts || !gyro || !accel || !soff || !bias || !noise || !out) {
+    set_err("vba_preintegrate: null buffer");
+    return VBA_E_INVALID;
+  }
+  int* stat = nullptr;
+  VBA_CUDA(cudaMallocAsync((void**)&stat, sizeof(int), st));
+  cudaMemsetAsync(stat, 0, sizeof(int), st);
+  launch_preintegrate(ts, gyro, accel, soff, n_pairs, bias, noise, out, stat, st);
+  int hs = 0;
+  cudaMemcpyAsync(&hs, stat, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(stat, st);
+  VBA_CUDA(cudaStreamSynchronize(st));
+  if (hs & 1) { set_err("Need at least two IMU samples to preintegrate"); return VBA_E_INVALID; }
+  if (hs & 2) { set_err("IMU timestamps must be strictly increasing"); return VBA_E_INVALID; }
+  return VBA_OK;
+}
+
 int vba_energy(void* ctx, void* stream, double* tot, double* vis, double* ine) {
   Ctx* c = (Ctx*)ctx;
   cudaStream_t st = (cudaStream_t)stream;

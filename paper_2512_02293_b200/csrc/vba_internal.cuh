@@ -363,6 +363,10 @@ void launch_dense_dxd(const double* x, int nf, const int64_t* doff, const int64_
                       cudaStream_t st);
 void launch_unpad(const float* src, const int64_t* doff, const int64_t* roff, const int32_t* npix, int maxpix, int K,
                   double* dst, cudaStream_t st);
+// IMU preintegration (vba_preint.cu): record per keyframe pair, see include/vba.h.
+constexpr int kPreintRec = 281;
+void launch_preintegrate(const double* ts, const double* gyro, const double* accel, const int64_t* soff, int F,
+                         const double* bias, const double* noise, double* out, int* status, cudaStream_t st);
 void launch_count();   // instrumentation hook
 int64_t launch_total();
 

@@ -1,0 +1,64 @@
+"""IMU preintegration (reference vislam/imu.py:77-167).
+
+CPU: the oracle restatement against the reference's own outputs (tests/golden/imu/imu_preint.npz,
+made by tests/golden/make_imu_golden.py).  GPU: the batched device kernel
+(`vba_preintegrate`, one thread per keyframe pair) against the same goldens, and its errors."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle.imu import preintegrate as oracle_preintegrate
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+FIELDS = ("delta_q", "delta_p", "delta_v", "J_rot", "J_pos", "J_vel", "covariance")
+
+
+def _cases():
+    z = np.load(os.path.join(HERE, "golden", "imu", "imu_preint.npz"))
+    return z["noise"], [{k[len(f"c{i}_"):]: z[k] for k in z.files if k.startswith(f"c{i}_")}
+                        for i in range(int(z["n"]))]
+
+
+def _rel(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    s = max(np.abs(b).max(initial=0.0), 1e-300)
+    return float(np.abs(a - b).max(initial=0.0) / s)
+
+
+def test_oracle_matches_reference_goldens():
+    noise, cases = _cases()
+    for c in cases:
+        d = oracle_preintegrate(c["ts"], c["gyro"], c["accel"], c["bias"], noise)
+        assert abs(d["dt_total"] - float(c["dt_total"])) <= 1e-15
+        for f in FIELDS:
+            assert _rel(d[f], c[f]) < 1e-13, f
+
+
+def test_oracle_rejects_like_reference():
+    with pytest.raises(ValueError):
+        oracle_preintegrate([0.0], np.zeros((1, 3)), np.zeros((1, 3)), np.zeros(6), (1, 1, 1, 1))
+    with pytest.raises(ValueError):
+        oracle_preintegrate([0.0, 0.0], np.zeros((2, 3)), np.zeros((2, 3)), np.zeros(6), (1, 1, 1, 1))
+
+
+@pytest.mark.gpu
+def test_device_preintegration_matches_reference(cuda_ok):
+    from paper_2512_02293_b200.imu import preintegrate_batch
+    noise, cases = _cases()
+    out = preintegrate_batch([c["ts"] for c in cases], [c["gyro"] for c in cases],
+                             [c["accel"] for c in cases], np.stack([c["bias"] for c in cases]), noise)
+    for i, c in enumerate(cases):
+        assert abs(out["dt_total"][i] - float(c["dt_total"])) <= 1e-15
+        for f in FIELDS:
+            assert _rel(out[f][i], c[f]) < 1e-12, (i, f)
+
+
+@pytest.mark.gpu
+def test_device_preintegration_errors(cuda_ok):
+    from paper_2512_02293_b200.imu import preintegrate_batch
+    z3 = np.zeros((2, 3))
+    with pytest.raises(ValueError):
+        preintegrate_batch([np.array([0.0, 0.0])], [z3], [z3], np.zeros((1, 6)), (1, 1, 1, 1))
+    with pytest.raises(ValueError):
+        preintegrate_batch([np.array([0.0])], [z3[:1]], [z3[:1]], np.zeros((1, 6)), (1, 1, 1, 1))
