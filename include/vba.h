@@ -193,16 +193,19 @@ VBA_API int vba_spd_solve(const double* H, int64_t n, const double* b, double* x
 
 /* IMU preintegration of F keyframe pairs, replacing vislam/imu.py:77-167
  * (`preintegrate`, called per pair by the tracking frontend).  Pair f owns the
- * samples soff[f] .. soff[f+1]-1 of ts [S] (seconds), gyro [S,3] and accel [S,3];
+ * samples soff[f] .. soff[f+1]-1 of ts [S = n_samples = soff[F]] (seconds), gyro [S,3] and accel [S,3];
  * bias [F,6] = (b_g, b_a); noise [4] = (gyro, accel, gyro random walk, accel random
  * walk) densities.  Writes out [F, VBA_PREINT_REC] = dt_total, delta_R quaternion
  * (w,x,y,z; w >= 0), delta_p (3), delta_v (3), J_rot (3x3), J_pos (3x6), J_vel (3x6),
- * covariance (15x15), row-major, fp64.  All pointers are device pointers.  Returns
+ * covariance (15x15), row-major, fp64.  All pointers are device pointers; `scratch`
+ * holds vba_preint_scratch_bytes(n_samples) bytes (caller-owned, reusable).  Returns
  * VBA_E_INVALID (the reference's ValueError) for a pair with fewer than two samples
  * or non-increasing timestamps.  Synchronises `stream`. */
 #define VBA_PREINT_REC 281
-VBA_API int vba_preintegrate(const double* ts, const double* gyro, const double* accel, const int64_t* soff,
-                             int32_t n_pairs, const double* bias, const double* noise, double* out, void* stream);
+VBA_API int64_t vba_preint_scratch_bytes(int64_t n_samples);
+VBA_API int vba_preintegrate(const double* ts, const double* gyro, const double* accel, int64_t n_samples,
+                             const int64_t* soff, int32_t n_pairs, const double* bias, const double* noise,
+                             void* scratch, double* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -22,7 +22,7 @@ EXPORTED = ("vba_last_error", "vba_version", "vba_create", "vba_destroy", "vba_s
             "vba_solve_step", "vba_export_step", "vba_apply_step", "vba_restore", "vba_accept",
             "vba_trial", "vba_solve", "vba_download", "vba_launch_count", "vba_stage_times",
             "vba_load_state", "vba_bind_inputs", "vba_set_profiling", "vba_stats", "vba_spd_solve", "vba_solve_times",
-            "vba_preintegrate")
+            "vba_preintegrate", "vba_preint_scratch_bytes")
 
 
 class VbaProblem(C.Structure):
@@ -110,7 +110,8 @@ def load(path: str | None = None):
         "vba_stats": ([v, C.POINTER(C.c_int64)], C.c_int),
         "vba_solve_times": ([v, C.POINTER(C.c_double)], C.c_int),
         "vba_spd_solve": ([v, C.c_int64, v, v, C.c_int32, v, C.POINTER(C.c_int32)], C.c_int),
-        "vba_preintegrate": ([v, v, v, v, C.c_int32, v, v, v, v], C.c_int),
+        "vba_preintegrate": ([v, v, v, C.c_int64, v, C.c_int32, v, v, v, v, v], C.c_int),
+        "vba_preint_scratch_bytes": ([C.c_int64], C.c_int64),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

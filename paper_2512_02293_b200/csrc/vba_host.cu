@@ -1160,26 +1160,31 @@ int vba_spd_solve(const double* H, int64_t n, const double* b, double* x, int32_
   return hs[0] ? VBA_E_NOT_SPD : VBA_OK;
 }
 
-int vba_preintegrate(const double* ts, const double* gyro, const double* accel, const int64_t* soff,
-                     int32_t n_pairs, const double* bias, const double* noise, double* out, void* stream) {
+int64_t vba_preint_scratch_bytes(int64_t n_samples) {
+  return n_samples < 0 ? -1 : (int64_t)(preint_scratch_bytes(n_samples) + 256);
+}
+
+int vba_preintegrate(const double* ts, const double* gyro, const double* accel, int64_t n_samples,
+                     const int64_t* soff, int32_t n_pairs, const double* bias, const double* noise, void* scratch,
+                     double* out, void* stream) {
   static_assert(VBA_PREINT_REC == kPreintRec, "preintegration record size");
   cudaStream_t st = (cudaStream_t)stream;
-  if (n_pairs < 0) { set_err("vba_preintegrate: negative pair count"); return VBA_E_INVALID; }
+  if (n_pairs < 0 || n_samples < 0) { set_err("vba_preintegrate: negative size"); return VBA_E_INVALID; }
   if (n_pairs == 0) return VBA_OK;
-  if (!ts || !gyro || !accel || !soff || !bias || !noise || !out) {
+  if ((n_samples && (!ts || !gyro || !accel)) || !soff || !bias || !noise || !out || !scratch) {
     set_err("vba_preintegrate: null buffer");
     return VBA_E_INVALID;
   }
-  int* stat = nullptr;
-  VBA_CUDA(cudaMallocAsync((void**)&stat, sizeof(int), st));
-  cudaMemsetAsync(stat, 0, sizeof(int), st);
-  launch_preintegrate(ts, gyro, accel, soff, n_pairs, bias, noise, out, stat, st);
+  int* stat = (int*)scratch;                            // status word, then the step records
+  double* steps = (double*)((char*)scratch + 256);
+  VBA_CUDA(cudaMemsetAsync(stat, 0, sizeof(int), st));
+  launch_preintegrate(ts, gyro, accel, n_samples, soff, n_pairs, bias, noise, steps, out, stat, st);
   int hs = 0;
-  cudaMemcpyAsync(&hs, stat, sizeof(int), cudaMemcpyDeviceToHost, st);
-  cudaFreeAsync(stat, st);
+  VBA_CUDA(cudaMemcpyAsync(&hs, stat, sizeof(int), cudaMemcpyDeviceToHost, st));
   VBA_CUDA(cudaStreamSynchronize(st));
   if (hs & 1) { set_err("Need at least two IMU samples to preintegrate"); return VBA_E_INVALID; }
   if (hs & 2) { set_err("IMU timestamps must be strictly increasing"); return VBA_E_INVALID; }
+  if (hs & 4) { set_err("vba_preintegrate: soff[n_pairs] != n_samples"); return VBA_E_INVALID; }
   return VBA_OK;
 }
 

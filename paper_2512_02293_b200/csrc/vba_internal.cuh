@@ -365,8 +365,10 @@ void launch_unpad(const float* src, const int64_t* doff, const int64_t* roff, co
                   double* dst, cudaStream_t st);
 // IMU preintegration (vba_preint.cu): record per keyframe pair, see include/vba.h.
 constexpr int kPreintRec = 281;
-void launch_preintegrate(const double* ts, const double* gyro, const double* accel, const int64_t* soff, int F,
-                         const double* bias, const double* noise, double* out, int* status, cudaStream_t st);
+size_t preint_scratch_bytes(int64_t S);
+void launch_preintegrate(const double* ts, const double* gyro, const double* accel, int64_t S, const int64_t* soff,
+                         int F, const double* bias, const double* noise, double* scratch, double* out, int* status,
+                         cudaStream_t st);
 void launch_count();   // instrumentation hook
 int64_t launch_total();
 

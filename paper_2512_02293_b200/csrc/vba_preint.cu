@@ -110,114 +110,221 @@ __device__ void quat_from_matrix(const M3& R, double* q) {
 }
 }  // namespace
 
-__global__ void __launch_bounds__(64) k_preintegrate(const double* __restrict__ ts, const double* __restrict__ gyro,
-                                                     const double* __restrict__ accel,
-                                                     const int64_t* __restrict__ soff, int F,
-                                                     const double* __restrict__ bias, const double* __restrict__ noise,
-                                                     double* __restrict__ out, int* __restrict__ status) {
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= F) return;
-  const int64_t s0 = soff[f], S = soff[f + 1] - s0;
-  double* o = out + (int64_t)kPreintRec * f;
-  if (S < 2) { atomicOr(status, 1); return; }                    // imu.py:87-88
-  for (int64_t k = 0; k + 1 < S; ++k)
-    if (!(ts[s0 + k + 1] - ts[s0 + k] > 0.0)) { atomicOr(status, 2); return; }   // imu.py:89-91
-  const double bg[3] = {bias[6 * f + 0], bias[6 * f + 1], bias[6 * f + 2]};
-  const double ba[3] = {bias[6 * f + 3], bias[6 * f + 4], bias[6 * f + 5]};
-  const double sg2 = noise[0] * noise[0], sa2 = noise[1] * noise[1];
-  M3 dR = meye(), Jr = mzero(), Jvg = mzero(), Jva = mzero(), Jpg = mzero(), Jpa = mzero();
-  double dv[3] = {0, 0, 0}, dp[3] = {0, 0, 0};
-  M3 C[3][3];   // cov9 as 3x3 blocks (theta, p, v)
-  for (int i = 0; i < 3; ++i)
-    for (int j = 0; j < 3; ++j) C[i][j] = mzero();
-  for (int64_t k = 0; k + 1 < S; ++k) {                          // imu.py:106-150
-    const int64_t a0 = s0 + k, a1 = a0 + 1;
-    const double dt = ts[a1] - ts[a0];
-    double w[3], a[3], wf[3], wh[3];
-    for (int c = 0; c < 3; ++c) {
-      w[c] = 0.5 * ((gyro[3 * a0 + c] - bg[c]) + (gyro[3 * a1 + c] - bg[c]));
-      a[c] = 0.5 * ((accel[3 * a0 + c] - ba[c]) + (accel[3 * a1 + c] - ba[c]));
-      wf[c] = w[c] * dt;
-      wh[c] = w[c] * (0.5 * dt);
-    }
-    const M3 Ef = so3_exp(wf), Eh = so3_exp(wh), Jf = so3_jr(wf), Jh = so3_jr(wh);
-    const M3 Rm = mmul(dR, Eh);
-    double ai[3];
-    for (int r = 0; r < 3; ++r) ai[r] = Rm(r, 0) * a[0] + Rm(r, 1) * a[1] + Rm(r, 2) * a[2];
-    const M3 RA = mmul(Rm, mhat(a));
-    const M3 Jmid = madd(mTmul(Eh, Jr), Jh, -0.5 * dt);           // imu.py:120
-    const M3 RAJmid = mmul(RA, Jmid);
-    const M3 RAE = mmulT(RA, Eh);                                 // R_mid Ahat E_half^T
-    const M3 RAJh = mmul(RA, Jh);
-    const M3 X = mscale(RAE, -0.5 * dt * dt), Y = mscale(RAE, -dt);   // A[3:6,0:3], A[6:9,0:3]
-    // M = A C  (imu.py:124-128: A = I with the blocks above, E_full^T and dt I)
-    M3 Mb[3][3];
-    for (int j = 0; j < 3; ++j) {
-      Mb[0][j] = mTmul(Ef, C[0][j]);
-      Mb[1][j] = madd(madd(mmul(X, C[0][j]), C[1][j]), C[2][j], dt);
-      Mb[2][j] = madd(mmul(Y, C[0][j]), C[2][j]);
-    }
-    // C' = M A^T + B Qd B^T  (imu.py:130-138)
-    M3 Bg[3], Bav[3];
-    Bg[0] = mscale(Jf, -dt);
-    Bg[1] = mscale(RAJh, 0.25 * dt * dt * dt);
-    Bg[2] = mscale(RAJh, 0.5 * dt * dt);
-    Bav[0] = mzero();
-    Bav[1] = mscale(Rm, -0.5 * dt * dt);
-    Bav[2] = mscale(Rm, -dt);
-    const double qg = sg2 / dt, qa = sa2 / dt;
-    M3 Cn[3][3];
-    for (int i = 0; i < 3; ++i) {
-      Cn[i][0] = mmul(Mb[i][0], Ef);
-      Cn[i][1] = madd(madd(mmulT(Mb[i][0], X), Mb[i][1]), Mb[i][2], dt);
-      Cn[i][2] = madd(mmulT(Mb[i][0], Y), Mb[i][2]);
-      for (int j = 0; j < 3; ++j) {
-        Cn[i][j] = madd(Cn[i][j], mmulT(Bg[i], Bg[j]), qg);
-        if (i > 0 && j > 0) Cn[i][j] = madd(Cn[i][j], mmulT(Bav[i], Bav[j]), qa);
-      }
-    }
-    for (int i = 0; i < 3; ++i)                                   // symmetrise (imu.py:139)
-      for (int j = 0; j < 3; ++j)
-        for (int r = 0; r < 3; ++r)
-          for (int c = 0; c < 3; ++c) C[i][j](r, c) = 0.5 * (Cn[i][j](r, c) + Cn[j][i](c, r));
-    // bias Jacobians, position before velocity (imu.py:142-146)
-    Jpg = madd(madd(Jpg, Jvg, dt), RAJmid, -0.5 * dt * dt);
-    Jpa = madd(madd(Jpa, Jva, dt), Rm, -0.5 * dt * dt);
-    Jvg = madd(Jvg, RAJmid, -dt);
-    Jva = madd(Jva, Rm, -dt);
-    Jr = madd(mTmul(Ef, Jr), Jf, -dt);
-    for (int c = 0; c < 3; ++c) {                                  // imu.py:148-150
-      dp[c] = dp[c] + dv[c] * dt + 0.5 * dt * dt * ai[c];
-      dv[c] = dv[c] + dt * ai[c];
-    }
-    dR = mmul(dR, Ef);
+// Phase 1 (one thread per sample interval, fully parallel): everything of a step that
+// depends only on the samples -- dt, the bias-corrected midpoint accel, and the
+// exponentials / right Jacobians of the full and half rotation increments
+// (imu.py:107-117).  Record layout: dt, a[3], Ef[9], Eh[9], Jf[9], Jh[9].
+constexpr int kStepRec = 40;
+
+__global__ void __launch_bounds__(128) k_preint_steps(const double* __restrict__ ts, const double* __restrict__ gyro,
+                                                      const double* __restrict__ accel,
+                                                      const int64_t* __restrict__ soff, int F, int64_t S,
+                                                      const double* __restrict__ bias, double* __restrict__ steps,
+                                                      int* __restrict__ status) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s == 0 && soff[F] != S) atomicOr(status, 4);
+  if (s >= S) return;
+  int lo = 0, hi = F;   // pair f with soff[f] <= s < soff[f+1]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (soff[mid] <= s) lo = mid; else hi = mid;
   }
-  const double dtt = ts[s0 + S - 1] - ts[s0];
-  o[0] = dtt;
-  quat_from_matrix(dR, o + 1);
-  for (int c = 0; c < 3; ++c) { o[5 + c] = dp[c]; o[8 + c] = dv[c]; }
-  for (int i = 0; i < 9; ++i) o[11 + i] = Jr.m[i];
-  for (int r = 0; r < 3; ++r)
-    for (int c = 0; c < 3; ++c) {
-      o[20 + 6 * r + c] = Jpg(r, c); o[20 + 6 * r + 3 + c] = Jpa(r, c);
-      o[38 + 6 * r + c] = Jvg(r, c); o[38 + 6 * r + 3 + c] = Jva(r, c);
-    }
-  double* cv = o + 56;
-  for (int i = 0; i < 225; ++i) cv[i] = 0.0;
-  for (int bi = 0; bi < 3; ++bi)
-    for (int bj = 0; bj < 3; ++bj)
-      for (int r = 0; r < 3; ++r)
-        for (int c = 0; c < 3; ++c) cv[(3 * bi + r) * 15 + 3 * bj + c] = C[bi][bj](r, c);
-  for (int d = 0; d < 3; ++d) {                                    // imu.py:152-156
-    cv[(9 + d) * 15 + 9 + d] = noise[2] * noise[2] * dtt;
-    cv[(12 + d) * 15 + 12 + d] = noise[3] * noise[3] * dtt;
+  const int f = lo;
+  if (s + 1 >= soff[f + 1]) return;   // last sample of its pair
+  const double dt = ts[s + 1] - ts[s];
+  if (!(dt > 0.0)) { atomicOr(status, 2); return; }   // imu.py:89-91
+  double w[3], wf[3], wh[3];
+  double* r = steps + kStepRec * s;
+  r[0] = dt;
+  for (int c = 0; c < 3; ++c) {
+    const double bg = bias[6 * f + c], ba = bias[6 * f + 3 + c];
+    w[c] = 0.5 * ((gyro[3 * s + c] - bg) + (gyro[3 * s + 3 + c] - bg));
+    r[1 + c] = 0.5 * ((accel[3 * s + c] - ba) + (accel[3 * s + 3 + c] - ba));
+    wf[c] = w[c] * dt;
+    wh[c] = w[c] * (0.5 * dt);
+  }
+  const M3 Ef = so3_exp(wf), Eh = so3_exp(wh), Jf = so3_jr(wf), Jh = so3_jr(wh);
+  for (int i = 0; i < 9; ++i) {
+    r[4 + i] = Ef.m[i]; r[13 + i] = Eh.m[i]; r[22 + i] = Jf.m[i]; r[31 + i] = Jh.m[i];
   }
 }
 
-void launch_preintegrate(const double* ts, const double* gyro, const double* accel, const int64_t* soff, int F,
-                         const double* bias, const double* noise, double* out, int* status, cudaStream_t st) {
+// Phase 2: the sequential propagation, 16 lanes per keyframe pair (two pairs per warp).
+// The covariance recursion cov9 <- A cov9 A^T + B Qd B^T splits by columns: column c of
+// M = A cov9 needs only column c of cov9, row r of M A^T only row r of M.  Lane c (< 9)
+// owns column c of cov9 and row c of the product, the two exchanged through shared
+// memory; the bias Jacobians split the same way over their 3 columns (lanes 0-2).
+// dR, dp, dv and the 3x3 step matrices are replicated per lane (cheap, deterministic).
+// Step records are double-buffered in shared memory: each lane loads its part of step
+// k+1 into registers at the top of step k and stores it to shared memory at the end, so
+// the global-load latency hides behind the step's arithmetic.
+constexpr int kPairsPerBlock = 8;
+struct PairSmem {
+  double rec[2][kStepRec];
+  double M[81];    // M = A cov9, written by columns, read by rows
+  double Cp[81];   // C' rows, read by columns for the symmetrisation
+  double RJ[9];    // R_mid Ahat Jr_half of the current step
+  double Rm[9];    // R_mid of the current step
+};
+
+__device__ __forceinline__ double at3(const double* p, int i, int j) { return p[3 * i + j]; }
+
+__global__ void __launch_bounds__(16 * kPairsPerBlock) k_preint_propagate(const double* __restrict__ ts,
+                                                                         const int64_t* __restrict__ soff, int F,
+                                                                         const double* __restrict__ steps,
+                                                                         const double* __restrict__ noise,
+                                                                         double* __restrict__ out,
+                                                                         int* __restrict__ status) {
+  __shared__ PairSmem sm_all[kPairsPerBlock];
+  const int grp = threadIdx.x >> 4, c = threadIdx.x & 15;
+  const int f = blockIdx.x * kPairsPerBlock + grp;
+  if (f >= F) return;
+  const unsigned mask = 0xFFFFu << (threadIdx.x & 16);
+  PairSmem& sm = sm_all[grp];
+  const int64_t s0 = soff[f], S = soff[f + 1] - s0;
+  if (S < 2) { if (c == 0) atomicOr(status, 1); return; }   // imu.py:87-88
+  const double sg2 = noise[0] * noise[0], sa2 = noise[1] * noise[1];
+  const bool cov_lane = c < 9, jac_lane = c < 3;
+  const int br = cov_lane ? c / 3 : 0, rr = cov_lane ? c % 3 : 0;   // lane's row block / row in block
+  M3 dR = meye();
+  double dp[3] = {0, 0, 0}, dv[3] = {0, 0, 0};
+  double Cc[9];                                   // column c of cov9
+  for (int i = 0; i < 9; ++i) Cc[i] = 0.0;
+  double jr[3] = {0, 0, 0}, jpg[3] = {0, 0, 0}, jvg[3] = {0, 0, 0}, jpa[3] = {0, 0, 0}, jva[3] = {0, 0, 0};
+  const double* st = steps + kStepRec * s0;
+  for (int i = c; i < kStepRec; i += 16) sm.rec[0][i] = st[i];
+  __syncwarp(mask);
+  for (int64_t k = 0; k + 1 < S; ++k) {
+    const double* r = sm.rec[k & 1];
+    double pf[3] = {0.0, 0.0, 0.0};               // step k+1, loaded now, stored at the end of step k
+    if (k + 2 < S)
+      for (int q = 0; q < 3; ++q)
+        if (c + 16 * q < kStepRec) pf[q] = __ldg(st + kStepRec * (k + 1) + c + 16 * q);
+    const double* Ef = r + 4;
+    const double* Eh = r + 13;
+    const double* Jf = r + 22;
+    const double* Jh = r + 31;
+    const double dt = r[0];
+    const double a[3] = {r[1], r[2], r[3]};
+    M3 Rm, RA, RAE, RAJh;
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) Rm(i, j) = dR(i, 0) * at3(Eh, 0, j) + dR(i, 1) * at3(Eh, 1, j) + dR(i, 2) * at3(Eh, 2, j);
+    for (int i = 0; i < 3; ++i) {                 // R_mid Ahat
+      RA(i, 0) = Rm(i, 1) * a[2] - Rm(i, 2) * a[1];
+      RA(i, 1) = Rm(i, 2) * a[0] - Rm(i, 0) * a[2];
+      RA(i, 2) = Rm(i, 0) * a[1] - Rm(i, 1) * a[0];
+    }
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) {
+        RAE(i, j) = RA(i, 0) * at3(Eh, j, 0) + RA(i, 1) * at3(Eh, j, 1) + RA(i, 2) * at3(Eh, j, 2);
+        RAJh(i, j) = RA(i, 0) * at3(Jh, 0, j) + RA(i, 1) * at3(Jh, 1, j) + RA(i, 2) * at3(Jh, 2, j);
+      }
+    if (c == 0)
+      for (int i = 0; i < 9; ++i) { sm.RJ[i] = RAJh.m[i]; sm.Rm[i] = Rm.m[i]; }
+    const double hx = -0.5 * dt * dt, hy = -dt;   // X = hx * RAE, Y = hy * RAE
+    if (cov_lane) {                               // column c of M = A cov9 (imu.py:124-128)
+      for (int i = 0; i < 3; ++i) {
+        const double e0 = at3(Ef, 0, i) * Cc[0] + at3(Ef, 1, i) * Cc[1] + at3(Ef, 2, i) * Cc[2];
+        const double x0 = RAE(i, 0) * Cc[0] + RAE(i, 1) * Cc[1] + RAE(i, 2) * Cc[2];
+        sm.M[9 * i + c] = e0;
+        sm.M[9 * (3 + i) + c] = hx * x0 + Cc[3 + i] + dt * Cc[6 + i];
+        sm.M[9 * (6 + i) + c] = hy * x0 + Cc[6 + i];
+      }
+    }
+    __syncwarp(mask);
+    if (cov_lane) {                               // row c of C' = M A^T + B Qd B^T (imu.py:130-138)
+      double mr[9], cp[9];
+      for (int j = 0; j < 9; ++j) mr[j] = sm.M[9 * c + j];
+      for (int j = 0; j < 3; ++j) {
+        const double x0 = mr[0] * RAE(j, 0) + mr[1] * RAE(j, 1) + mr[2] * RAE(j, 2);
+        cp[j] = mr[0] * at3(Ef, 0, j) + mr[1] * at3(Ef, 1, j) + mr[2] * at3(Ef, 2, j);
+        cp[3 + j] = hx * x0 + mr[3 + j] + dt * mr[6 + j];
+        cp[6 + j] = hy * x0 + mr[6 + j];
+      }
+      // B rows: gyro part s_b * G_b (G_0 = Jr_full, G_1 = G_2 = R_mid Ahat Jr_half),
+      // accel part t_b * R_mid (t_0 = 0), b = row block
+      const double s1 = 0.25 * dt * dt * dt, s2 = 0.5 * dt * dt, t1 = -0.5 * dt * dt, t2 = -dt;
+      const double qg = sg2 / dt, qa = sa2 / dt;
+      const double sr = br == 0 ? -dt : (br == 1 ? s1 : s2), tr = br == 0 ? 0.0 : (br == 1 ? t1 : t2);
+      const double* gp = br == 0 ? Jf : sm.RJ;
+      const double g0 = sr * gp[3 * rr], g1 = sr * gp[3 * rr + 1], g2 = sr * gp[3 * rr + 2];
+      const double a0 = tr * sm.Rm[3 * rr], a1 = tr * sm.Rm[3 * rr + 1], a2 = tr * sm.Rm[3 * rr + 2];
+      for (int j = 0; j < 9; ++j) {
+        const int bj = j / 3, rj = j % 3;
+        const double sj = bj == 0 ? -dt : (bj == 1 ? s1 : s2), tj = bj == 0 ? 0.0 : (bj == 1 ? t1 : t2);
+        const double* gq = bj == 0 ? Jf : sm.RJ;
+        const double gg = g0 * (sj * gq[3 * rj]) + g1 * (sj * gq[3 * rj + 1]) + g2 * (sj * gq[3 * rj + 2]);
+        const double aa = a0 * (tj * sm.Rm[3 * rj]) + a1 * (tj * sm.Rm[3 * rj + 1]) + a2 * (tj * sm.Rm[3 * rj + 2]);
+        cp[j] = cp[j] + qg * gg + qa * aa;
+        sm.Cp[9 * c + j] = cp[j];
+      }
+      __syncwarp(mask & 0x01FF01FFu);
+      for (int i = 0; i < 9; ++i) Cc[i] = 0.5 * (sm.Cp[9 * i + c] + cp[i]);   // symmetrise (imu.py:139)
+    }
+    if (jac_lane) {                               // bias Jacobian column c (imu.py:120, 142-146)
+      double jm[3], rj[3], jn[3];
+      for (int i = 0; i < 3; ++i)
+        jm[i] = at3(Eh, 0, i) * jr[0] + at3(Eh, 1, i) * jr[1] + at3(Eh, 2, i) * jr[2] - 0.5 * dt * at3(Jh, i, c);
+      for (int i = 0; i < 3; ++i) rj[i] = RA(i, 0) * jm[0] + RA(i, 1) * jm[1] + RA(i, 2) * jm[2];
+      for (int i = 0; i < 3; ++i)
+        jn[i] = at3(Ef, 0, i) * jr[0] + at3(Ef, 1, i) * jr[1] + at3(Ef, 2, i) * jr[2] - dt * at3(Jf, i, c);
+      for (int i = 0; i < 3; ++i) {
+        const double rmc = sm.Rm[3 * i + c];
+        jpg[i] += dt * jvg[i] - 0.5 * dt * dt * rj[i];
+        jpa[i] += dt * jva[i] - 0.5 * dt * dt * rmc;
+        jvg[i] += -dt * rj[i];
+        jva[i] += -dt * rmc;
+        jr[i] = jn[i];
+      }
+    }
+    for (int i = 0; i < 3; ++i) {                 // imu.py:148-150
+      const double ai = Rm(i, 0) * a[0] + Rm(i, 1) * a[1] + Rm(i, 2) * a[2];
+      dp[i] = dp[i] + dv[i] * dt + 0.5 * dt * dt * ai;
+      dv[i] = dv[i] + dt * ai;
+    }
+    M3 dn;
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) dn(i, j) = dR(i, 0) * at3(Ef, 0, j) + dR(i, 1) * at3(Ef, 1, j) + dR(i, 2) * at3(Ef, 2, j);
+    dR = dn;
+    if (k + 2 < S)
+      for (int q = 0; q < 3; ++q)
+        if (c + 16 * q < kStepRec) sm.rec[(k + 1) & 1][c + 16 * q] = pf[q];
+    __syncwarp(mask);   // rec[k+1] landed; M, Cp, RJ, Rm free for the next step
+  }
+  double* o = out + (int64_t)kPreintRec * f;
+  double* cv = o + 56;
+  const double dtt = ts[s0 + S - 1] - ts[s0];
+  if (c == 0) {
+    o[0] = dtt;
+    quat_from_matrix(dR, o + 1);
+    for (int i = 0; i < 3; ++i) { o[5 + i] = dp[i]; o[8 + i] = dv[i]; }
+  }
+  if (jac_lane)
+    for (int i = 0; i < 3; ++i) {
+      o[11 + 3 * i + c] = jr[i];
+      o[20 + 6 * i + c] = jpg[i]; o[20 + 6 * i + 3 + c] = jpa[i];
+      o[38 + 6 * i + c] = jvg[i]; o[38 + 6 * i + 3 + c] = jva[i];
+    }
+  for (int r = 0; r < 15; ++r) {                  // lane c writes column c (cov9 or bias-walk block)
+    double v = 0.0;
+    if (c < 9) v = r < 9 ? Cc[r] : 0.0;
+    if (c < 15 && c >= 9 && r == c) v = (c < 12 ? noise[2] * noise[2] : noise[3] * noise[3]) * dtt;   // imu.py:152-156
+    if (c < 15) cv[15 * r + c] = v;
+  }
+}
+
+size_t preint_scratch_bytes(int64_t S) { return sizeof(double) * kStepRec * (size_t)(S > 0 ? S : 1); }
+
+void launch_preintegrate(const double* ts, const double* gyro, const double* accel, int64_t S, const int64_t* soff,
+                         int F, const double* bias, const double* noise, double* scratch, double* out, int* status,
+                         cudaStream_t st) {
   if (F <= 0) return;
-  k_preintegrate<<<(F + 63) / 64, 64, 0, st>>>(ts, gyro, accel, soff, F, bias, noise, out, status);
+  if (S > 0) {
+    k_preint_steps<<<(unsigned)((S + 127) / 128), 128, 0, st>>>(ts, gyro, accel, soff, F, S, bias, scratch, status);
+    launch_count();
+  }
+  k_preint_propagate<<<(F + kPairsPerBlock - 1) / kPairsPerBlock, 16 * kPairsPerBlock, 0, st>>>(
+      ts, soff, F, scratch, noise, out, status);
   launch_count();
 }
 

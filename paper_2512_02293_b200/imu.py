@@ -10,7 +10,6 @@ path: without the built extension or a CUDA device the calls fail.
 
 from __future__ import annotations
 
-import ctypes as C
 import importlib
 
 import numpy as np
@@ -32,20 +31,31 @@ def _noise_vector(noise):
     return v
 
 
-def preintegrate_device(ts, gyro, accel, soff, bias, noise, out=None, stream=None):
+def scratch_for(n_samples, device="cuda"):
+    """Reusable device workspace for preintegrate_device (vba_preint_scratch_bytes)."""
+    import torch
+
+    return torch.empty(int(_lib.load().vba_preint_scratch_bytes(int(n_samples))), dtype=torch.uint8, device=device)
+
+
+def preintegrate_device(ts, gyro, accel, soff, bias, noise, out=None, scratch=None, stream=None):
     """Device-resident form: torch CUDA fp64 tensors ts [S], gyro/accel [S,3],
     soff int64 [F+1] (pair f owns samples soff[f]..soff[f+1]-1), bias [F,6],
-    noise [4].  Returns (or fills) out [F, PREINT_REC]."""
+    noise [4].  Returns (or fills) out [F, PREINT_REC]; `scratch` (scratch_for(S))
+    may be kept across calls."""
     import torch
 
     lib = _lib.load()
     F = int(soff.shape[0]) - 1
     dev = ts.device
+    S = int(ts.shape[0])
     if out is None:
         out = torch.empty((max(F, 0), _lib.PREINT_REC), dtype=torch.float64, device=dev)
+    if scratch is None or scratch.numel() < lib.vba_preint_scratch_bytes(S):
+        scratch = scratch_for(S, dev)
     st = (stream or torch.cuda.current_stream(dev)).cuda_stream
-    rc = lib.vba_preintegrate(ts.data_ptr(), gyro.data_ptr(), accel.data_ptr(), soff.data_ptr(), F,
-                              bias.data_ptr(), noise.data_ptr(), out.data_ptr(), st)
+    rc = lib.vba_preintegrate(ts.data_ptr(), gyro.data_ptr(), accel.data_ptr(), S, soff.data_ptr(), F,
+                              bias.data_ptr(), noise.data_ptr(), scratch.data_ptr(), out.data_ptr(), st)
     if rc == _lib.VBA_E_INVALID:
         raise ValueError(lib.vba_last_error().decode())
     _lib.check(rc)
@@ -86,9 +96,6 @@ def preintegrate_batch(ts_list, gyro_list, accel_list, bias, noise, device="cuda
     cat = (lambda xs, w: np.concatenate(xs) if F else np.zeros((0,) + w))
     host = [cat(ts, ()), cat(gy, (3,)), cat(ac, (3,)), soff, bias, _noise_vector(noise)]
     dev = [torch.from_numpy(np.ascontiguousarray(h)).to(device) for h in host]
-    if dev[0].numel() == 0:   # keep valid (non-null) device pointers for empty windows
-        dev[0] = torch.zeros(1, dtype=torch.float64, device=device)
-        dev[1] = dev[2] = torch.zeros((1, 3), dtype=torch.float64, device=device)
     out = preintegrate_device(*dev)
     return unpack(out.cpu().numpy())
 

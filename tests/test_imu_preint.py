@@ -62,3 +62,22 @@ def test_device_preintegration_errors(cuda_ok):
         preintegrate_batch([np.array([0.0, 0.0])], [z3], [z3], np.zeros((1, 6)), (1, 1, 1, 1))
     with pytest.raises(ValueError):
         preintegrate_batch([np.array([0.0])], [z3[:1]], [z3[:1]], np.zeros((1, 6)), (1, 1, 1, 1))
+
+
+@pytest.mark.gpu
+def test_device_preintegration_reference_signature(cuda_ok):
+    """preintegrate(samples, bias_hat, noise) with the reference's object shapes (imu.py:18-62)."""
+    from types import SimpleNamespace
+
+    from paper_2512_02293_b200.imu import preintegrate, preintegrate_batch
+    noise, cases = _cases()
+    c = cases[3]
+    samples = [SimpleNamespace(timestamp=float(t), gyro=g, accel=a) for t, g, a in zip(c["ts"], c["gyro"], c["accel"])]
+    bias = SimpleNamespace(gyro_bias=c["bias"][:3], accel_bias=c["bias"][3:])
+    nm = SimpleNamespace(gyro_noise_density=noise[0], accel_noise_density=noise[1],
+                         gyro_bias_random_walk=noise[2], accel_bias_random_walk=noise[3])
+    d = preintegrate(samples, bias, nm)
+    for f in FIELDS:
+        assert _rel(d[f], c[f]) < 1e-12, f
+    empty = preintegrate_batch([], [], [], np.zeros((0, 6)), noise)
+    assert empty["covariance"].shape == (0, 15, 15)
