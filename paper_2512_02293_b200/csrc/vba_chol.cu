@@ -2456,7 +2456,7 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
   cudaMemsetAsync(stop, 0, sizeof(int), st);
   cudaMemsetAsync(out2, 0, sizeof(double) * 3, st);
   if (nt > sms) return 1;   // one resident CTA per row tile (n <= 148 * 128 here)
-  // passes until the correction is < 1e-12 max|x| (early-exit kernels after that), at most `iters`
+  // passes until the correction is <= kTcRefineTol max|x| (early-exit kernels after that), at most `iters`
   for (int it = 0; it < iters; ++it) {
     const double* rhs = b;
     if (it > 0) {
@@ -2483,9 +2483,8 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
                 (h[0][1][k] - t0) * 1e-3, (h[0][2][k] - t0) * 1e-3, (h[0][3][k] - t0) * 1e-3);
     }
 #endif
-    // stop once a pass corrects x by < 1e-6 max|x|: with the factor's contraction
-    // (~1e-3 per pass here) the returned x is then within ~1e-9 of the fp64 solution
-    k_tc_check<<<1, 1, 0, st>>>(out2, stop, 1e-6, it == iters - 1);
+    // stop once a pass corrects x by <= kTcRefineTol max|x| (vba_internal.cuh)
+    k_tc_check<<<1, 1, 0, st>>>(out2, stop, kTcRefineTol, it == iters - 1);
     launch_count();
     launch_count();
     launch_count();

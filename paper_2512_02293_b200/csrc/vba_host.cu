@@ -828,13 +828,13 @@ static int stage_step_any(Ctx* c, double lam, int use_schur, cudaStream_t st) {
 }
 
 // The tensor-core solve is accepted when its fp32 factor had positive pivots and
-// the last fp64 refinement pass moved x by < 1e-6 max|x| (so x is ~1e-9 accurate).
+// the last fp64 refinement pass moved x by <= kTcRefineTol max|x|.
 static bool tc_failed(Ctx* c, int use_schur) {
   if (!c->use_tc || c->force_fp64 || c->d_trace || c->nfree == 0 || !(use_schur || c->n_disp == 0)) return false;
   const Result& r = *c->h_res;
   ++c->tc_solves;
   c->tc_passes += (int64_t)r.tc[2];
-  return r.tc_bad != 0 || !(r.tc[0] <= 1e-6 * r.tc[1]);
+  return r.tc_bad != 0 || !(r.tc[0] <= kTcRefineTol * r.tc[1]);
 }
 
 static int run_trial(Ctx* c, double lam, int use_schur, vba_trial_result* out, cudaStream_t st) {
@@ -1147,7 +1147,7 @@ int vba_spd_solve(const double* H, int64_t n, const double* b, double* x, int32_
     cudaMemcpyAsync(hs, stat, sizeof(hs), cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(h2, tc2, sizeof(h2), cudaMemcpyDeviceToHost, st);
     if (cudaStreamSynchronize(st) != cudaSuccess) { cleanup(); set_err("vba_spd_solve: %s", cudaGetErrorString(cudaGetLastError())); return VBA_E_CUDA; }
-    used_tc = (mode == 2 || (hs[1] == 0 && h2[0] <= 1e-6 * h2[1])) ? 1 : 0;
+    used_tc = (mode == 2 || (hs[1] == 0 && h2[0] <= kTcRefineTol * h2[1])) ? 1 : 0;
   }
   if (!used_tc) {
     chol_dag_launch(Hp, npad, nt, bp, xp, Ld, part, flags, tasks, ntasks, stat, st);

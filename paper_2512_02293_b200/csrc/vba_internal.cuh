@@ -363,6 +363,12 @@ void launch_dense_dxd(const double* x, int nf, const int64_t* doff, const int64_
                       cudaStream_t st);
 void launch_unpad(const float* src, const int64_t* doff, const int64_t* roff, const int32_t* npix, int maxpix, int K,
                   double* dst, cudaStream_t st);
+// The tensor-core reduced solve stops refining once a pass corrects x by <= this fraction
+// of max|x|; the remaining error is then ~tol x (the factor's per-pass contraction, ~1e-3
+// measured), i.e. ~1e-8 relative, far inside the 1e-5 update parity.  A solve whose last
+// pass still moved x by more is redone on the fp64 path.
+constexpr double kTcRefineTol = 1e-5;
+
 // IMU preintegration (vba_preint.cu): record per keyframe pair, see include/vba.h.
 constexpr int kPreintRec = 281;
 size_t preint_scratch_bytes(int64_t S);
