@@ -795,13 +795,14 @@ void launch_edge_finalize(const int32_t* t0s, const int32_t* t1s, const PixTile*
 //   U = [k_{n,e} (6k columns) | g_d(n)]   and   V = k_{n,e} / Hdd_d(n)
 // (column-major [column][pixel], stride GPX = 36 ≡ 4 mod 16: conflict-free DMMA
 // fragments), then C = U^T V accumulates with mma.sync m8n8k4 f64 in registers
-// across all chunks (each warp owns up to GMAXT 8x8 output tiles of the lower
-// band).  The last row of C is b.  fp64 products of fp32 factors are exact and
+// across all chunks (each warp owns up to GT 8x8 output tiles of the lower
+// band, in 2x2 units).  The last row of C is b.  fp64 products of fp32 factors are exact and
 // all sums are fp64: no fp32 partial-sum error, fixed order (deterministic).
 // ---------------------------------------------------------------------------
 constexpr int GPX = kGramPC + 4;   // pixel stride of the U / V columns (doubles)
-constexpr int GMAXT = 22;          // 8x8 output tiles per warp (k <= 31)
 constexpr int GWARPS = 16;
+// 8x8 output tiles per warp: 2x2 units, 5 per warp up to 30 out-edges, 6 at 31
+__host__ __device__ constexpr int gram_tiles_per_warp(int kmax) { return kmax <= 30 ? 20 : 24; }
 
 __device__ __forceinline__ void gdmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -821,7 +822,7 @@ extern "C" __attribute__((visibility("default"))) void vba_gram_prof(unsigned lo
 #else
 #define GPROF(i, v)
 #endif
-template <int MODE>
+template <int MODE, int GT>
 __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
     const GramTile* __restrict__ gts, const float* __restrict__ disp, const EdgeGeo32* __restrict__ geo,
     const float* __restrict__ pix, const float* __restrict__ wts, const int64_t* __restrict__ eoff,
@@ -843,38 +844,58 @@ __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
   const int nc = 6 * k;
   const int NRt = (nc + 1 + 7) / 8, NCt = (nc + 7) / 8;   // row / column tiles of C
   // output tiles: lower band tj <= ti + 1 (6x6 blocks may straddle the 8-tile diagonal),
-  // grouped in units of two vertically adjacent tiles (ti, tj), (ti + 1, tj) that share
-  // their B fragments (3 shared-memory loads per 2 DMMAs); unit u belongs to warp
-  // u % GWARPS, tile slots 2 (u / GWARPS) and 2 (u / GWARPS) + 1 (tile_i = -1: empty)
-  __shared__ short tile_i[GWARPS * GMAXT], tile_j[GWARPS * GMAXT];
-  __shared__ int ntiles_s;
+  // grouped in 2x2 units (ti, ti + 1) x (tj, tj + 1) that share their A and B fragments
+  // (4 shared-memory loads per 4 DMMAs: shared-memory bandwidth co-limits the DMMA pipe).
+  // Every warp takes nu = U / GWARPS whole units (slots 4u + {0: (ti, tj), 1: (ti + 1, tj),
+  // 2: (ti, tj + 1), 3: (ti + 1, tj + 1)}); the U % GWARPS leftover units are split into
+  // column pairs {(ti, tj), (ti + 1, tj)} (3 loads per 2 DMMAs) dealt round-robin after
+  // them, so the per-chunk barrier waits for at most one pair more than the average.
+  // -1 = outside C (computed on clamped fragments, never stored; also the one tile of a
+  // diagonal unit above the band).
+  __shared__ short tile_i[GWARPS * GT], tile_j[GWARPS * GT];
+  __shared__ int nu_s, npw_s[GWARPS];
   __shared__ double invs[2][kGramPC];   // 1 / (Hdd (1 + lam) + ridge) per pixel, double-buffered by chunk
   __shared__ float4 geos[32 * 4];       // the source's out-edge geometry (k <= 31), EdgeGeo32 records
   // C = sum_n u_n u_n^T / h_n is formed as W^T W with W = u / sqrt(h_n) (one staged matrix)
   auto pixel_inv = [&](int n) { return n < T.n1 ? 1.0 / sqrt((double)Hdd[kbase + n] * damp + ridge) : 0.0; };
   if (tid == 0) {
-    int u = 0;
-    for (int tj = 0; tj < NCt; ++tj)
-      for (int ti = tj > 0 ? tj - 1 : 0; ti < NRt; ti += 2)
-        if (u < GWARPS * GMAXT / 2) {
-          const int w = u % GWARPS, sl = 2 * (u / GWARPS);
-          tile_i[w + GWARPS * sl] = (short)ti;
-          tile_j[w + GWARPS * sl] = (short)tj;
-          tile_i[w + GWARPS * (sl + 1)] = (short)(ti + 1 < NRt ? ti + 1 : -1);
-          tile_j[w + GWARPS * (sl + 1)] = (short)tj;
-          ++u;
+    int U = 0;
+    for (int tj = 0; tj < NCt; tj += 2)
+      for (int ti = tj > 0 ? tj - 1 : 0; ti < NRt; ti += 2) ++U;
+    const int nu = U / GWARPS;
+    int u = 0, pr = 0;
+    for (int w = 0; w < GWARPS; ++w) npw_s[w] = 0;
+    auto put = [&](int w, int sl, int ti, int tj) {
+      if (sl < GT) { tile_i[w + GWARPS * sl] = (short)ti; tile_j[w + GWARPS * sl] = (short)tj; }
+    };
+    for (int tj = 0; tj < NCt; tj += 2)
+      for (int ti = tj > 0 ? tj - 1 : 0; ti < NRt; ti += 2, ++u) {
+        const int r1 = ti + 1 < NRt ? ti + 1 : -1, c1 = tj + 1 < NCt ? tj + 1 : -1;
+        if (u < nu * GWARPS) {
+          const int w = u % GWARPS, sl = 4 * (u / GWARPS);
+          put(w, sl, ti, tj); put(w, sl + 1, r1, tj); put(w, sl + 2, ti, c1); put(w, sl + 3, r1, c1);
+        } else {
+          for (int h = 0; h < 2; ++h) {
+            const int c = h == 0 ? tj : c1;
+            if (c < 0) continue;
+            const int w = pr % GWARPS, sl = 4 * nu + 2 * npw_s[w];
+            put(w, sl, ti, c); put(w, sl + 1, r1, c);
+            ++npw_s[w];
+            ++pr;
+          }
         }
-    ntiles_s = u;   // units
+      }
+    nu_s = nu;
   }
-  double acc[GMAXT][2];
+  double acc[GT][2];
 #pragma unroll
-  for (int q = 0; q < GMAXT; ++q) acc[q][0] = acc[q][1] = 0.0;
+  for (int q = 0; q < GT; ++q) acc[q][0] = acc[q][1] = 0.0;
   for (int i = tid; i < 2 * (int)uvs; i += nth) UV[i] = 0.0;   // padding columns stay zero
   if (tid < kGramPC) invs[0][tid] = pixel_inv(T.n0 + tid);
   if (tid < 4 * k) geos[tid] = __ldg(reinterpret_cast<const float4*>(geo + T.eb) + tid);
   __syncthreads();
-  const int ntl = ntiles_s;
-  const int nmine = 2 * ((ntl - warp + GWARPS - 1) / GWARPS);   // tile slots of this warp
+  const int n4 = 4 * nu_s;                       // slots in whole 2x2 units (same for all warps)
+  const int nmine = n4 + 2 * npw_s[warp];        // + column pairs: tile slots of this warp
 
   // Phase 1 of a chunk: coupling vectors of its (pixel, edge) items (at most kGramItems
   // per thread), widened to fp64 into buffer b.  Loads of all items first (gload),
@@ -956,27 +977,44 @@ __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
     const double* Ub = UV + (size_t)cb * uvs;
     const double* Vb = Ub;   // C = W^T W
     const int am = lane >> 2, ak = lane & 3;
+    static_assert(GT % 4 == 0, "2x2 units");
 #pragma unroll
-    for (int q = 0; q < GMAXT; q += 2) {
-      if (q < nmine) {
-        const int t1 = tile_i[warp + GWARPS * (q + 1)];
-        const double* pa0 = Ub + (size_t)(tile_i[warp + GWARPS * q] * 8 + am) * GPX + ak;
-        const double* pa1 = Ub + (size_t)((t1 >= 0 ? t1 : 0) * 8 + am) * GPX + ak;
-        const double* pb = Vb + (size_t)(tile_j[warp + GWARPS * q] * 8 + am) * GPX + ak;
-        if (t1 >= 0) {
+    for (int q = 0; q < GT; q += 4) {
+      if (q >= n4 && q < nmine) {   // one or two column pairs (slots q, q + 1 and q + 2, q + 3)
+#pragma unroll
+        for (int h = 0; h < 4; h += 2) {
+          if (q + h >= nmine) break;
+          const int r1 = tile_i[warp + GWARPS * (q + h + 1)];
+          const double* pa0 = Ub + (size_t)(tile_i[warp + GWARPS * (q + h)] * 8 + am) * GPX + ak;
+          const double* pa1 = Ub + (size_t)((r1 >= 0 ? r1 : 0) * 8 + am) * GPX + ak;
+          const double* pb = Vb + (size_t)(tile_j[warp + GWARPS * (q + h)] * 8 + am) * GPX + ak;
 #pragma unroll
           for (int ks = 0; ks < kGramPC / 4; ++ks) {
             const double b = pb[4 * ks];
-            gdmma(acc[q][0], acc[q][1], pa0[4 * ks], b);
-            gdmma(acc[q + 1][0], acc[q + 1][1], pa1[4 * ks], b);
+            gdmma(acc[q + h][0], acc[q + h][1], pa0[4 * ks], b);
+            gdmma(acc[q + h + 1][0], acc[q + h + 1][1], pa1[4 * ks], b);
           }
-        } else {
+        }
+      } else if (q < n4) {
+        const int r1 = tile_i[warp + GWARPS * (q + 1)], c1 = tile_j[warp + GWARPS * (q + 2)];
+        const double* pa0 = Ub + (size_t)(tile_i[warp + GWARPS * q] * 8 + am) * GPX + ak;
+        const double* pa1 = Ub + (size_t)((r1 >= 0 ? r1 : 0) * 8 + am) * GPX + ak;
+        const double* pb0 = Vb + (size_t)(tile_j[warp + GWARPS * q] * 8 + am) * GPX + ak;
+        const double* pb1 = Vb + (size_t)((c1 >= 0 ? c1 : 0) * 8 + am) * GPX + ak;
 #pragma unroll
-          for (int ks = 0; ks < kGramPC / 4; ++ks) gdmma(acc[q][0], acc[q][1], pa0[4 * ks], pb[4 * ks]);
+        for (int ks = 0; ks < kGramPC / 4; ++ks) {
+          const double a0 = pa0[4 * ks], a1 = pa1[4 * ks], b0 = pb0[4 * ks], b1 = pb1[4 * ks];
+          gdmma(acc[q][0], acc[q][1], a0, b0);
+          gdmma(acc[q + 1][0], acc[q + 1][1], a1, b0);
+          gdmma(acc[q + 2][0], acc[q + 2][1], a0, b1);
+          gdmma(acc[q + 3][0], acc[q + 3][1], a1, b1);
         }
       }
-      if (q % 6 == 2 && q / 6 < kGramItems && more) gitem(q / 6, cn, cb ^ 1);
+      if (q % 8 == 4 && q / 8 < kGramItems && more) gitem(q / 8, cn, cb ^ 1);
     }
+#pragma unroll
+    for (int j = (GT + 3) / 8; j < kGramItems; ++j)
+      if (more) gitem(j, cn, cb ^ 1);
     // pixel inverses of chunk c + 2 (buffer cb: chunk c's items are done)
     if (tid >= nth - kGramPC) invs[cb][tid - (nth - kGramPC)] = pixel_inv(cn + kGramPC + tid - (nth - kGramPC));
 #ifdef VBA_GRAM_PROF
@@ -987,8 +1025,8 @@ __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
   // epilogue: scatter the lower 6x6 blocks (e1 >= e2) and the b row into the output layout
   double* o = out + T.out;
 #pragma unroll
-  for (int q = 0; q < GMAXT; ++q) {
-    if (q >= nmine || tile_i[warp + GWARPS * q] < 0) continue;
+  for (int q = 0; q < GT; ++q) {
+    if (q >= nmine || tile_i[warp + GWARPS * q] < 0 || tile_j[warp + GWARPS * q] < 0) continue;
     const int a = tile_i[warp + GWARPS * q] * 8 + (lane >> 2);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -1004,6 +1042,29 @@ __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
   }
 }
 
+template <int MODE, int GT>
+static void launch_gram_t(const GramTile* gt, int ngt, int block, size_t smem, int kmax, const DevState& s,
+                          const float* pix, const float* wts, const int64_t* eoff, const int64_t* doff, int grid_w,
+                          GridP gp, IntrP in, const float* Hdd, const float* gd, double lam, double ridge,
+                          double* gram_part, cudaStream_t st) {
+  cudaFuncSetAttribute(k_gram<MODE, GT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_gram<MODE, GT><<<ngt, block, smem, st>>>(gt, s.disp, s.geo32, pix, wts, eoff, doff, grid_w, gp, in, Hdd, gd,
+                                             lam, ridge, kmax, gram_part);
+}
+
+template <int MODE>
+static void launch_gram_m(const GramTile* gt, int ngt, int block, size_t smem, int kmax, const DevState& s,
+                          const float* pix, const float* wts, const int64_t* eoff, const int64_t* doff, int grid_w,
+                          GridP gp, IntrP in, const float* Hdd, const float* gd, double lam, double ridge,
+                          double* gram_part, cudaStream_t st) {
+  if (gram_tiles_per_warp(kmax) == 20)
+    launch_gram_t<MODE, 20>(gt, ngt, block, smem, kmax, s, pix, wts, eoff, doff, grid_w, gp, in, Hdd, gd, lam, ridge,
+                            gram_part, st);
+  else
+    launch_gram_t<MODE, 24>(gt, ngt, block, smem, kmax, s, pix, wts, eoff, doff, grid_w, gp, in, Hdd, gd, lam, ridge,
+                            gram_part, st);
+}
+
 void launch_gram(int mode, const GramTile* gt, int ngt, int block, size_t smem, int kmax, const DevState& s,
                  const float* pix, const float* wts, const int64_t* eoff, const int64_t* doff, int grid_w,
                  const double* grid, const double* intr, const float* Hdd, const float* gd, double lam,
@@ -1011,19 +1072,15 @@ void launch_gram(int mode, const GramTile* gt, int ngt, int block, size_t smem, 
   if (ngt <= 0) return;
   GridP gp{grid[0], grid[1], grid[2], grid[3]};
   IntrP in{intr[0], intr[1], intr[2], intr[3]};
-  if (mode == VBA_PIX_GRID) {
-    cudaFuncSetAttribute(k_gram<VBA_PIX_GRID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_gram<VBA_PIX_GRID><<<ngt, block, smem, st>>>(gt, s.disp, s.geo32, pix, wts, eoff, doff, grid_w, gp, in,
-                                                   Hdd, gd, lam, ridge, kmax, gram_part);
-  } else if (mode == VBA_PIX_KF) {
-    cudaFuncSetAttribute(k_gram<VBA_PIX_KF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_gram<VBA_PIX_KF><<<ngt, block, smem, st>>>(gt, s.disp, s.geo32, pix, wts, eoff, doff, grid_w, gp, in, Hdd,
-                                                 gd, lam, ridge, kmax, gram_part);
-  } else {
-    cudaFuncSetAttribute(k_gram<VBA_PIX_EDGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_gram<VBA_PIX_EDGE><<<ngt, block, smem, st>>>(gt, s.disp, s.geo32, pix, wts, eoff, doff, grid_w, gp, in,
-                                                   Hdd, gd, lam, ridge, kmax, gram_part);
-  }
+  if (mode == VBA_PIX_GRID)
+    launch_gram_m<VBA_PIX_GRID>(gt, ngt, block, smem, kmax, s, pix, wts, eoff, doff, grid_w, gp, in, Hdd, gd, lam,
+                                ridge, gram_part, st);
+  else if (mode == VBA_PIX_KF)
+    launch_gram_m<VBA_PIX_KF>(gt, ngt, block, smem, kmax, s, pix, wts, eoff, doff, grid_w, gp, in, Hdd, gd, lam,
+                              ridge, gram_part, st);
+  else
+    launch_gram_m<VBA_PIX_EDGE>(gt, ngt, block, smem, kmax, s, pix, wts, eoff, doff, grid_w, gp, in, Hdd, gd, lam,
+                                ridge, gram_part, st);
   launch_count();
 }
 
