@@ -207,6 +207,15 @@ VBA_API int vba_preintegrate(const double* ts, const double* gyro, const double*
                              const int64_t* soff, int32_t n_pairs, const double* bias, const double* noise,
                              void* scratch, double* out, void* stream);
 
+/* Device-resident hand-off from preintegration to the solver: converts F records of
+ * vba_preintegrate (`rec` [F, VBA_PREINT_REC]) plus their bias linearisation points
+ * (`bias` [F,6]) into IMU factor records `imu` [F, VBA_IMU_REC] (the host packing of
+ * PreintegratedDelta, residuals.py:274-354 inputs), e.g. straight into the buffer bound
+ * as vba_problem.imu before vba_bind_inputs(..., refresh_imu = 1).  Stream-ordered, no
+ * synchronisation. */
+VBA_API int vba_preint_factor_records(const double* rec, const double* bias, int32_t n_pairs, double* imu,
+                                      void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -22,7 +22,8 @@ EXPORTED = ("vba_last_error", "vba_version", "vba_create", "vba_destroy", "vba_s
             "vba_solve_step", "vba_export_step", "vba_apply_step", "vba_restore", "vba_accept",
             "vba_trial", "vba_solve", "vba_download", "vba_launch_count", "vba_stage_times",
             "vba_load_state", "vba_bind_inputs", "vba_set_profiling", "vba_stats", "vba_spd_solve", "vba_solve_times",
-            "vba_preintegrate", "vba_preint_scratch_bytes")
+            "vba_preintegrate", "vba_preint_scratch_bytes",
+            "vba_preint_factor_records")
 
 
 class VbaProblem(C.Structure):
@@ -112,6 +113,7 @@ def load(path: str | None = None):
         "vba_spd_solve": ([v, C.c_int64, v, v, C.c_int32, v, C.POINTER(C.c_int32)], C.c_int),
         "vba_preintegrate": ([v, v, v, C.c_int64, v, C.c_int32, v, v, v, v, v], C.c_int),
         "vba_preint_scratch_bytes": ([C.c_int64], C.c_int64),
+        "vba_preint_factor_records": ([v, v, C.c_int32, v, v], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

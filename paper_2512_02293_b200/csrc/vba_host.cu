@@ -1188,6 +1188,17 @@ int vba_preintegrate(const double* ts, const double* gyro, const double* accel, 
   return VBA_OK;
 }
 
+int vba_preint_factor_records(const double* rec, const double* bias, int32_t n_pairs, double* imu, void* stream) {
+  static_assert(VBA_IMU_REC == kImuRec, "IMU record size");
+  if (n_pairs < 0 || (n_pairs > 0 && (!rec || !bias || !imu))) {
+    set_err("vba_preint_factor_records: invalid arguments");
+    return VBA_E_INVALID;
+  }
+  launch_preint_pack(rec, bias, n_pairs, imu, (cudaStream_t)stream);
+  VBA_CUDA(cudaGetLastError());
+  return VBA_OK;
+}
+
 int vba_energy(void* ctx, void* stream, double* tot, double* vis, double* ine) {
   Ctx* c = (Ctx*)ctx;
   cudaStream_t st = (cudaStream_t)stream;

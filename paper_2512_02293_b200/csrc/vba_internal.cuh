@@ -372,6 +372,8 @@ constexpr double kTcRefineTol = 1e-5;
 // IMU preintegration (vba_preint.cu): record per keyframe pair, see include/vba.h.
 constexpr int kPreintRec = 281;
 size_t preint_scratch_bytes(int64_t S);
+constexpr int kImuRec = 180;   // VBA_IMU_REC
+void launch_preint_pack(const double* rec, const double* bias, int F, double* imu, cudaStream_t st);
 void launch_preintegrate(const double* ts, const double* gyro, const double* accel, int64_t S, const int64_t* soff,
                          int F, const double* bias, const double* noise, double* scratch, double* out, int* status,
                          cudaStream_t st);

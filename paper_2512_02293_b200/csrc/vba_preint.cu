@@ -313,6 +313,30 @@ __global__ void __launch_bounds__(16 * kPairsPerBlock) k_preint_propagate(const 
   }
 }
 
+// Preintegration record -> IMU factor record of the solver (include/vba.h VBA_IMU_REC):
+// the first 56 doubles are shared, then cov[0:9,0:9], cov[9:15,9:15], the bias
+// linearisation point.  One thread per output double.
+__global__ void k_preint_pack(const double* __restrict__ rec, const double* __restrict__ bias, int F,
+                              double* __restrict__ imu) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)F * kImuRec) return;
+  const int f = (int)(t / kImuRec), i = (int)(t % kImuRec);
+  const double* r = rec + (int64_t)kPreintRec * f;
+  double v = 0.0;
+  if (i < 56) v = r[i];
+  else if (i < 137) v = r[56 + ((i - 56) / 9) * 15 + (i - 56) % 9];
+  else if (i < 173) v = r[56 + (9 + (i - 137) / 6) * 15 + 9 + (i - 137) % 6];
+  else if (i < 179) v = bias[6 * f + (i - 173)];
+  imu[t] = v;
+}
+
+void launch_preint_pack(const double* rec, const double* bias, int F, double* imu, cudaStream_t st) {
+  if (F <= 0) return;
+  const int64_t n = (int64_t)F * kImuRec;
+  k_preint_pack<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(rec, bias, F, imu);
+  launch_count();
+}
+
 size_t preint_scratch_bytes(int64_t S) { return sizeof(double) * kStepRec * (size_t)(S > 0 ? S : 1); }
 
 void launch_preintegrate(const double* ts, const double* gyro, const double* accel, int64_t S, const int64_t* soff,

@@ -62,6 +62,21 @@ def preintegrate_device(ts, gyro, accel, soff, bias, noise, out=None, scratch=No
     return out
 
 
+def factor_records(rec, bias, out=None, stream=None):
+    """Device [F, PREINT_REC] records + bias linearisation points [F, 6] -> the solver's
+    IMU factor records [F, IMU_REC] (vba_preint_factor_records), on the device: feed them
+    to DeviceProblem.d_imu / a solve_windows window without a host round trip."""
+    import torch
+
+    lib = _lib.load()
+    F = int(rec.shape[0])
+    if out is None:
+        out = torch.empty((F, _lib.IMU_REC), dtype=torch.float64, device=rec.device)
+    st = (stream or torch.cuda.current_stream(rec.device)).cuda_stream
+    _lib.check(lib.vba_preint_factor_records(rec.data_ptr(), bias.data_ptr(), F, out.data_ptr(), st))
+    return out
+
+
 def unpack(rec):
     """Split [F, PREINT_REC] records into a dict of per-field arrays ([F, ...])."""
     rec = np.asarray(rec)

@@ -368,6 +368,9 @@ def make_workload(cfg: int, grid=None, seed=None, with_truth=False):
             bias_lin_point=T.BiasState(b_hat[f, 0:3].copy(), b_hat[f, 3:6].copy()))))
 
     graph = T.FrameGraph(kfs, edges, imu, T.GravityModel(), intr)
+    # the raw IMU stream the deltas were preintegrated from (pair f: samples idx[f])
+    graph.imu_stream = {"ts": ts, "gyro": gyro_m, "accel": acc_m, "idx": idx, "bias": b_hat[:-1].copy(),
+                        "noise": (gyro_nd, accel_nd, g_rw, a_rw)}
     return (graph, truth) if with_truth else graph
 
 

@@ -81,3 +81,53 @@ def test_device_preintegration_reference_signature(cuda_ok):
         assert _rel(d[f], c[f]) < 1e-12, f
     empty = preintegrate_batch([], [], [], np.zeros((0, 6)), noise)
     assert empty["covariance"].shape == (0, 15, 15)
+
+
+@pytest.mark.gpu
+def test_device_preintegration_feeds_the_solver(cuda_ok):
+    """Raw IMU stream -> vba_preintegrate -> vba_preint_factor_records -> the solver's IMU
+    buffer, all on the device: the records match the host packing of the workload's own
+    (numpy, imu.py scheme) deltas, and a solve_windows window fed with them reaches the
+    host-packed solve's cost and states."""
+    import copy
+
+    import torch
+
+    from paper_2512_02293_b200 import _lib
+    from paper_2512_02293_b200.device import DeviceProblem
+    from paper_2512_02293_b200.imu import factor_records, preintegrate_device
+    from paper_2512_02293_b200.problem import pack_graph
+    from paper_2512_02293_b200.workloads import make_workload
+
+    g = make_workload(1)
+    ims = g.imu_stream
+    idx = ims["idx"]
+    F, S1 = idx.shape
+    dev = "cuda"
+    ts = torch.from_numpy(ims["ts"][idx].reshape(-1).copy()).to(dev)
+    gy = torch.from_numpy(ims["gyro"][idx].reshape(-1, 3).copy()).to(dev)
+    ac = torch.from_numpy(ims["accel"][idx].reshape(-1, 3).copy()).to(dev)
+    soff = torch.arange(F + 1, dtype=torch.int64, device=dev) * S1
+    bias = torch.from_numpy(ims["bias"].copy()).to(dev)
+    noise = torch.tensor(ims["noise"], dtype=torch.float64, device=dev)
+    rec = preintegrate_device(ts, gy, ac, soff, bias, noise)
+    imu_dev = factor_records(rec, bias)
+    P = pack_graph(g)
+    opts = {"max_iterations": 2}
+    dp = DeviceProblem(copy.deepcopy(P), opts)
+    host = dp.H.imu
+    got = imu_dev.cpu().numpy()
+    assert got.shape == host.shape == (F, _lib.IMU_REC)
+    for lo, hi in ((0, 1), (1, 5), (5, 8), (8, 11), (11, 20), (20, 38), (38, 56), (56, 137), (137, 173), (173, 179)):
+        assert _rel(got[:, lo:hi], host[:, lo:hi]) < 1e-10, (lo, hi)
+    H = dp.H
+    win = {k: torch.from_numpy(np.ascontiguousarray(v).reshape(-1)).pin_memory()
+           for k, v in (("state", H.state), ("disp", H.disp), ("tgt", H.tgt), ("w", H.w), ("grav", H.grav))}
+    ref_rep = dp.solve_windows([dict(win, imu=torch.from_numpy(host.reshape(-1).copy()).pin_memory())])[0]
+    ref_state = dp.download()
+    rep = dp.solve_windows([dict(win, imu=imu_dev.reshape(-1))])[0]
+    st = dp.download()
+    assert abs(rep["final_cost"] - ref_rep["final_cost"]) <= 1e-9 * abs(ref_rep["final_cost"])
+    for k in ref_state:
+        a, b = np.asarray(st[k], float), np.asarray(ref_state[k], float)
+        assert np.abs(a - b).max(initial=0.0) <= 1e-8 * max(1.0, np.abs(b).max(initial=0.0)), k
