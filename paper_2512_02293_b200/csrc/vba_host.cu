@@ -1194,6 +1194,7 @@ int vba_preint_factor_records(const double* rec, const double* bias, int32_t n_p
     set_err("vba_preint_factor_records: invalid arguments");
     return VBA_E_INVALID;
   }
+  if (n_pairs == 0) return VBA_OK;
   launch_preint_pack(rec, bias, n_pairs, imu, (cudaStream_t)stream);
   VBA_CUDA(cudaGetLastError());
   return VBA_OK;

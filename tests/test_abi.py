@@ -79,3 +79,21 @@ def test_ctypes_struct_layout_matches_c(cls, struct):
     size, offs = _c_layout(struct, fields)
     assert size == ctypes.sizeof(S)
     assert offs == [getattr(S, f).offset for f in fields]
+
+
+def test_preintegration_entry_points_without_gpu(lib):
+    """vba_preint_scratch_bytes / vba_preintegrate / vba_preint_factor_records validate their
+    arguments on the host (VBA_E_INVALID) and accept empty windows without touching a GPU;
+    the header's record sizes match the Python binding."""
+    from paper_2512_02293_b200 import _lib
+    L = _lib.load()
+    hdr = open(os.path.join(REPO, "include", "vba.h")).read()
+    assert f"#define VBA_PREINT_REC {_lib.PREINT_REC}" in hdr
+    assert f"#define VBA_IMU_REC {_lib.IMU_REC}" in hdr
+    assert L.vba_preint_scratch_bytes(-1) == -1
+    assert L.vba_preint_scratch_bytes(1000) >= 1000 * 40 * 8
+    assert L.vba_preintegrate(None, None, None, 0, None, 0, None, None, None, None, None) == 0     # empty
+    assert L.vba_preintegrate(None, None, None, 0, None, -1, None, None, None, None, None) == 1    # invalid
+    assert L.vba_preintegrate(None, None, None, 10, None, 2, None, None, None, None, None) == 1    # null buffers
+    assert L.vba_preint_factor_records(None, None, 0, None, None) == 0
+    assert L.vba_preint_factor_records(None, None, 3, None, None) == 1

@@ -131,3 +131,28 @@ def test_device_preintegration_feeds_the_solver(cuda_ok):
     for k in ref_state:
         a, b = np.asarray(st[k], float), np.asarray(ref_state[k], float)
         assert np.abs(a - b).max(initial=0.0) <= 1e-8 * max(1.0, np.abs(b).max(initial=0.0)), k
+
+
+def test_record_layout_and_noise_parsing():
+    """Host side of paper_2512_02293_b200.imu (no GPU): the record layout covers
+    VBA_PREINT_REC exactly, unpack() splits it per field, noise objects / tuples parse."""
+    from types import SimpleNamespace
+
+    from paper_2512_02293_b200 import _lib
+    from paper_2512_02293_b200.imu import _LAYOUT, _noise_vector, unpack
+    end = 0
+    for _, off, shape in _LAYOUT:
+        assert off == end
+        end = off + int(np.prod(shape)) if shape else off + 1
+    assert end == _lib.PREINT_REC
+    rec = np.arange(2 * _lib.PREINT_REC, dtype=float).reshape(2, -1)
+    d = unpack(rec)
+    assert d["dt_total"].tolist() == [0.0, float(_lib.PREINT_REC)]
+    assert d["covariance"].shape == (2, 15, 15) and d["covariance"][1, 0, 0] == _lib.PREINT_REC + 56
+    assert d["J_pos"][0, 2, 5] == 20 + 17
+    nm = SimpleNamespace(gyro_noise_density=1.0, accel_noise_density=2.0, gyro_bias_random_walk=3.0,
+                         accel_bias_random_walk=4.0)
+    assert _noise_vector(nm).tolist() == [1.0, 2.0, 3.0, 4.0]
+    assert _noise_vector((1, 2, 3, 4)).tolist() == [1.0, 2.0, 3.0, 4.0]
+    with pytest.raises(ValueError):
+        _noise_vector((1, 2, 3))
