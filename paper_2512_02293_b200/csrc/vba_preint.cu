@@ -44,20 +44,9 @@ __device__ __forceinline__ M3 mmulT(const M3& a, const M3& b) {   // a b^T
     for (int k = 0; k < 3; ++k) c(r, k) = a(r, 0) * b(k, 0) + a(r, 1) * b(k, 1) + a(r, 2) * b(k, 2);
   return c;
 }
-__device__ __forceinline__ M3 mTmul(const M3& a, const M3& b) {   // a^T b
-  M3 c;
-  for (int r = 0; r < 3; ++r)
-    for (int k = 0; k < 3; ++k) c(r, k) = a(0, r) * b(0, k) + a(1, r) * b(1, k) + a(2, r) * b(2, k);
-  return c;
-}
 __device__ __forceinline__ M3 madd(const M3& a, const M3& b, double s = 1.0) {
   M3 c;
   for (int i = 0; i < 9; ++i) c.m[i] = a.m[i] + s * b.m[i];
-  return c;
-}
-__device__ __forceinline__ M3 mscale(const M3& a, double s) {
-  M3 c;
-  for (int i = 0; i < 9; ++i) c.m[i] = s * a.m[i];
   return c;
 }
 __device__ __forceinline__ M3 mhat(const double* v) {   // geometry.py:23-30
@@ -113,13 +102,17 @@ __device__ void quat_from_matrix(const M3& R, double* q) {
 // Phase 1 (one thread per sample interval, fully parallel): everything of a step that
 // depends only on the samples -- dt, the bias-corrected midpoint accel, and the
 // exponentials / right Jacobians of the full and half rotation increments
-// (imu.py:107-117).  Record layout: dt, a[3], Ef[9], Eh[9], Jf[9], Jh[9].
-constexpr int kStepRec = 40;
+// (imu.py:107-117) plus the state-free factors of R_mid Ahat E_half^T and
+// R_mid Ahat Jr_half (R_mid = dR E_half): P1 = E_half Ahat E_half^T, P2 = E_half Ahat
+// Jr_half, so both are one 3x3 product from dR in the sequential pass, and the noise
+// scalings.  Record layout: dt, a[3], Ef[9], Eh[9], Jf[9], Jh[9], P1[9], P2[9], qg, qa.
+constexpr int kStepRec = 60;
 
 __global__ void __launch_bounds__(128) k_preint_steps(const double* __restrict__ ts, const double* __restrict__ gyro,
                                                       const double* __restrict__ accel,
                                                       const int64_t* __restrict__ soff, int F, int64_t S,
-                                                      const double* __restrict__ bias, double* __restrict__ steps,
+                                                      const double* __restrict__ bias,
+                                                      const double* __restrict__ noise, double* __restrict__ steps,
                                                       int* __restrict__ status) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s == 0 && soff[F] != S) atomicOr(status, 4);
@@ -144,9 +137,15 @@ __global__ void __launch_bounds__(128) k_preint_steps(const double* __restrict__
     wh[c] = w[c] * (0.5 * dt);
   }
   const M3 Ef = so3_exp(wf), Eh = so3_exp(wh), Jf = so3_jr(wf), Jh = so3_jr(wh);
+  const double av[3] = {r[1], r[2], r[3]};
+  const M3 EA = mmul(Eh, mhat(av));
+  const M3 P1 = mmulT(EA, Eh), P2 = mmul(EA, Jh);
   for (int i = 0; i < 9; ++i) {
     r[4 + i] = Ef.m[i]; r[13 + i] = Eh.m[i]; r[22 + i] = Jf.m[i]; r[31 + i] = Jh.m[i];
+    r[40 + i] = P1.m[i]; r[49 + i] = P2.m[i];
   }
+  r[58] = noise[0] * noise[0] / dt;   // Qd diagonal (imu.py:137)
+  r[59] = noise[1] * noise[1] / dt;
 }
 
 // Phase 2: the sequential propagation, 16 lanes per keyframe pair (two pairs per warp).
@@ -183,7 +182,6 @@ __global__ void __launch_bounds__(16 * kPairsPerBlock) k_preint_propagate(const 
   PairSmem& sm = sm_all[grp];
   const int64_t s0 = soff[f], S = soff[f + 1] - s0;
   if (S < 2) { if (c == 0) atomicOr(status, 1); return; }   // imu.py:87-88
-  const double sg2 = noise[0] * noise[0], sa2 = noise[1] * noise[1];
   const bool cov_lane = c < 9, jac_lane = c < 3;
   const int br = cov_lane ? c / 3 : 0, rr = cov_lane ? c % 3 : 0;   // lane's row block / row in block
   M3 dR = meye();
@@ -196,9 +194,9 @@ __global__ void __launch_bounds__(16 * kPairsPerBlock) k_preint_propagate(const 
   __syncwarp(mask);
   for (int64_t k = 0; k + 1 < S; ++k) {
     const double* r = sm.rec[k & 1];
-    double pf[3] = {0.0, 0.0, 0.0};               // step k+1, loaded now, stored at the end of step k
+    double pf[4] = {0.0, 0.0, 0.0, 0.0};          // step k+1, loaded now, stored at the end of step k
     if (k + 2 < S)
-      for (int q = 0; q < 3; ++q)
+      for (int q = 0; q < 4; ++q)
         if (c + 16 * q < kStepRec) pf[q] = __ldg(st + kStepRec * (k + 1) + c + 16 * q);
     const double* Ef = r + 4;
     const double* Eh = r + 13;
@@ -206,18 +204,14 @@ __global__ void __launch_bounds__(16 * kPairsPerBlock) k_preint_propagate(const 
     const double* Jh = r + 31;
     const double dt = r[0];
     const double a[3] = {r[1], r[2], r[3]};
-    M3 Rm, RA, RAE, RAJh;
-    for (int i = 0; i < 3; ++i)
-      for (int j = 0; j < 3; ++j) Rm(i, j) = dR(i, 0) * at3(Eh, 0, j) + dR(i, 1) * at3(Eh, 1, j) + dR(i, 2) * at3(Eh, 2, j);
-    for (int i = 0; i < 3; ++i) {                 // R_mid Ahat
-      RA(i, 0) = Rm(i, 1) * a[2] - Rm(i, 2) * a[1];
-      RA(i, 1) = Rm(i, 2) * a[0] - Rm(i, 0) * a[2];
-      RA(i, 2) = Rm(i, 0) * a[1] - Rm(i, 1) * a[0];
-    }
+    const double* P1 = r + 40;
+    const double* P2 = r + 49;
+    M3 Rm, RAE, RAJh;   // R_mid, R_mid Ahat E_half^T = dR P1, R_mid Ahat Jr_half = dR P2
     for (int i = 0; i < 3; ++i)
       for (int j = 0; j < 3; ++j) {
-        RAE(i, j) = RA(i, 0) * at3(Eh, j, 0) + RA(i, 1) * at3(Eh, j, 1) + RA(i, 2) * at3(Eh, j, 2);
-        RAJh(i, j) = RA(i, 0) * at3(Jh, 0, j) + RA(i, 1) * at3(Jh, 1, j) + RA(i, 2) * at3(Jh, 2, j);
+        Rm(i, j) = dR(i, 0) * at3(Eh, 0, j) + dR(i, 1) * at3(Eh, 1, j) + dR(i, 2) * at3(Eh, 2, j);
+        RAE(i, j) = dR(i, 0) * at3(P1, 0, j) + dR(i, 1) * at3(P1, 1, j) + dR(i, 2) * at3(P1, 2, j);
+        RAJh(i, j) = dR(i, 0) * at3(P2, 0, j) + dR(i, 1) * at3(P2, 1, j) + dR(i, 2) * at3(P2, 2, j);
       }
     if (c == 0)
       for (int i = 0; i < 9; ++i) { sm.RJ[i] = RAJh.m[i]; sm.Rm[i] = Rm.m[i]; }
@@ -244,7 +238,7 @@ __global__ void __launch_bounds__(16 * kPairsPerBlock) k_preint_propagate(const 
       // B rows: gyro part s_b * G_b (G_0 = Jr_full, G_1 = G_2 = R_mid Ahat Jr_half),
       // accel part t_b * R_mid (t_0 = 0), b = row block
       const double s1 = 0.25 * dt * dt * dt, s2 = 0.5 * dt * dt, t1 = -0.5 * dt * dt, t2 = -dt;
-      const double qg = sg2 / dt, qa = sa2 / dt;
+      const double qg = r[58], qa = r[59];
       const double sr = br == 0 ? -dt : (br == 1 ? s1 : s2), tr = br == 0 ? 0.0 : (br == 1 ? t1 : t2);
       const double* gp = br == 0 ? Jf : sm.RJ;
       const double g0 = sr * gp[3 * rr], g1 = sr * gp[3 * rr + 1], g2 = sr * gp[3 * rr + 2];
@@ -265,7 +259,8 @@ __global__ void __launch_bounds__(16 * kPairsPerBlock) k_preint_propagate(const 
       double jm[3], rj[3], jn[3];
       for (int i = 0; i < 3; ++i)
         jm[i] = at3(Eh, 0, i) * jr[0] + at3(Eh, 1, i) * jr[1] + at3(Eh, 2, i) * jr[2] - 0.5 * dt * at3(Jh, i, c);
-      for (int i = 0; i < 3; ++i) rj[i] = RA(i, 0) * jm[0] + RA(i, 1) * jm[1] + RA(i, 2) * jm[2];
+      const double ax[3] = {a[1] * jm[2] - a[2] * jm[1], a[2] * jm[0] - a[0] * jm[2], a[0] * jm[1] - a[1] * jm[0]};
+      for (int i = 0; i < 3; ++i) rj[i] = Rm(i, 0) * ax[0] + Rm(i, 1) * ax[1] + Rm(i, 2) * ax[2];   // R_mid Ahat J_mid
       for (int i = 0; i < 3; ++i)
         jn[i] = at3(Ef, 0, i) * jr[0] + at3(Ef, 1, i) * jr[1] + at3(Ef, 2, i) * jr[2] - dt * at3(Jf, i, c);
       for (int i = 0; i < 3; ++i) {
@@ -287,7 +282,7 @@ __global__ void __launch_bounds__(16 * kPairsPerBlock) k_preint_propagate(const 
       for (int j = 0; j < 3; ++j) dn(i, j) = dR(i, 0) * at3(Ef, 0, j) + dR(i, 1) * at3(Ef, 1, j) + dR(i, 2) * at3(Ef, 2, j);
     dR = dn;
     if (k + 2 < S)
-      for (int q = 0; q < 3; ++q)
+      for (int q = 0; q < 4; ++q)
         if (c + 16 * q < kStepRec) sm.rec[(k + 1) & 1][c + 16 * q] = pf[q];
     __syncwarp(mask);   // rec[k+1] landed; M, Cp, RJ, Rm free for the next step
   }
@@ -344,7 +339,8 @@ void launch_preintegrate(const double* ts, const double* gyro, const double* acc
                          cudaStream_t st) {
   if (F <= 0) return;
   if (S > 0) {
-    k_preint_steps<<<(unsigned)((S + 127) / 128), 128, 0, st>>>(ts, gyro, accel, soff, F, S, bias, scratch, status);
+    k_preint_steps<<<(unsigned)((S + 127) / 128), 128, 0, st>>>(ts, gyro, accel, soff, F, S, bias, noise, scratch,
+                                                                status);
     launch_count();
   }
   k_preint_propagate<<<(F + kPairsPerBlock - 1) / kPairsPerBlock, 16 * kPairsPerBlock, 0, st>>>(
