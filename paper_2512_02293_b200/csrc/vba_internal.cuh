@@ -283,7 +283,7 @@ void launch_gram(int pixel_mode, const GramTile* gt, int ngt, int block, size_t 
                  const DevState& s, const float* pix, const float* wts, const int64_t* eoff,
                  const int64_t* doff, int grid_w, const double* grid, const double* intr,
                  const float* Hdd, const float* gd, double lam, double ridge, double* gram_part,
-                 cudaStream_t st);
+                 cudaStream_t st, const int32_t* order = nullptr);
 void launch_gram_reduce(const int32_t* src_list, int nsrc, const int32_t* src_gt0, const int32_t* src_gt1,
                         const GramTile* gt, const int32_t* src_eb, const int32_t* src_ee,
                         const int64_t* src_gram_off, const double* gram_part, double* gram,

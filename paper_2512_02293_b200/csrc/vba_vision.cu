@@ -827,9 +827,10 @@ __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
     const GramTile* __restrict__ gts, const float* __restrict__ disp, const EdgeGeo32* __restrict__ geo,
     const float* __restrict__ pix, const float* __restrict__ wts, const int64_t* __restrict__ eoff,
     const int64_t* __restrict__ doff, int grid_w, GridP gp, IntrP in, const float* __restrict__ Hdd,
-    const float* __restrict__ gd, double lam, double ridge, int kmax, double* __restrict__ out) {
+    const float* __restrict__ gd, double lam, double ridge, int kmax, double* __restrict__ out,
+    const int32_t* __restrict__ order) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const GramTile T = gts[blockIdx.x];
+  const GramTile T = gts[order ? order[blockIdx.x] : blockIdx.x];   // launch order: largest sources first
   const int k = T.ee - T.eb;
   const int npairs = k * (k + 1) / 2;
   const int NRmax = (6 * kmax + 1 + 7) / 8 * 8;
@@ -1046,41 +1047,41 @@ template <int MODE, int GT>
 static void launch_gram_t(const GramTile* gt, int ngt, int block, size_t smem, int kmax, const DevState& s,
                           const float* pix, const float* wts, const int64_t* eoff, const int64_t* doff, int grid_w,
                           GridP gp, IntrP in, const float* Hdd, const float* gd, double lam, double ridge,
-                          double* gram_part, cudaStream_t st) {
+                          double* gram_part, const int32_t* order, cudaStream_t st) {
   cudaFuncSetAttribute(k_gram<MODE, GT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_gram<MODE, GT><<<ngt, block, smem, st>>>(gt, s.disp, s.geo32, pix, wts, eoff, doff, grid_w, gp, in, Hdd, gd,
-                                             lam, ridge, kmax, gram_part);
+                                             lam, ridge, kmax, gram_part, order);
 }
 
 template <int MODE>
 static void launch_gram_m(const GramTile* gt, int ngt, int block, size_t smem, int kmax, const DevState& s,
                           const float* pix, const float* wts, const int64_t* eoff, const int64_t* doff, int grid_w,
                           GridP gp, IntrP in, const float* Hdd, const float* gd, double lam, double ridge,
-                          double* gram_part, cudaStream_t st) {
+                          double* gram_part, const int32_t* order, cudaStream_t st) {
   if (gram_tiles_per_warp(kmax) == 20)
     launch_gram_t<MODE, 20>(gt, ngt, block, smem, kmax, s, pix, wts, eoff, doff, grid_w, gp, in, Hdd, gd, lam, ridge,
-                            gram_part, st);
+                            gram_part, order, st);
   else
     launch_gram_t<MODE, 24>(gt, ngt, block, smem, kmax, s, pix, wts, eoff, doff, grid_w, gp, in, Hdd, gd, lam, ridge,
-                            gram_part, st);
+                            gram_part, order, st);
 }
 
 void launch_gram(int mode, const GramTile* gt, int ngt, int block, size_t smem, int kmax, const DevState& s,
                  const float* pix, const float* wts, const int64_t* eoff, const int64_t* doff, int grid_w,
                  const double* grid, const double* intr, const float* Hdd, const float* gd, double lam,
-                 double ridge, double* gram_part, cudaStream_t st) {
+                 double ridge, double* gram_part, cudaStream_t st, const int32_t* order) {
   if (ngt <= 0) return;
   GridP gp{grid[0], grid[1], grid[2], grid[3]};
   IntrP in{intr[0], intr[1], intr[2], intr[3]};
   if (mode == VBA_PIX_GRID)
     launch_gram_m<VBA_PIX_GRID>(gt, ngt, block, smem, kmax, s, pix, wts, eoff, doff, grid_w, gp, in, Hdd, gd, lam,
-                                ridge, gram_part, st);
+                                ridge, gram_part, order, st);
   else if (mode == VBA_PIX_KF)
     launch_gram_m<VBA_PIX_KF>(gt, ngt, block, smem, kmax, s, pix, wts, eoff, doff, grid_w, gp, in, Hdd, gd, lam,
-                              ridge, gram_part, st);
+                              ridge, gram_part, order, st);
   else
     launch_gram_m<VBA_PIX_EDGE>(gt, ngt, block, smem, kmax, s, pix, wts, eoff, doff, grid_w, gp, in, Hdd, gd, lam,
-                                ridge, gram_part, st);
+                                ridge, gram_part, order, st);
   launch_count();
 }
 
