@@ -79,7 +79,7 @@ struct Ctx {
   int ncta = 0;
   std::vector<int32_t> t0s, t1s, seb, see;
   std::vector<GramTile> gtiles;
-  std::vector<int32_t> gsrc, g0, g1, gorder;   // gorder: Gram launch order (largest sources first)
+  std::vector<int32_t> gsrc, g0, g1, gorder, gsrc_lpt;   // Gram tile / fill-in source launch orders (largest first)
   std::vector<int64_t> goff, foff;
   int kmax = 0;
   size_t gram_smem = 0;
@@ -100,7 +100,7 @@ struct Ctx {
   PixTile* d_chunks = nullptr;
   int32_t *d_t0s = nullptr, *d_t1s = nullptr, *d_seb = nullptr, *d_see = nullptr;
   GramTile* d_gtiles = nullptr;
-  int32_t *d_gsrc = nullptr, *d_g0 = nullptr, *d_g1 = nullptr, *d_gorder = nullptr;
+  int32_t *d_gsrc = nullptr, *d_g0 = nullptr, *d_g1 = nullptr, *d_gorder = nullptr, *d_gsrc_lpt = nullptr;
   int64_t *d_goff = nullptr, *d_foff = nullptr;
   double *d_part = nullptr, *d_tile_e = nullptr, *d_arena = nullptr, *d_gram_part = nullptr, *d_gram = nullptr;
   float *d_Hdd = nullptr, *d_gd = nullptr, *d_ustep = nullptr, *d_dxd = nullptr;
@@ -552,6 +552,10 @@ static int build_plans(Ctx* c, cudaStream_t st) {
   };
   std::stable_sort(c->gorder.begin(), c->gorder.end(),
                    [&](int32_t x, int32_t y) { return tile_work(x) > tile_work(y); });
+  c->gsrc_lpt = c->gsrc;   // k_fill_transform: one CTA per source, most out-edges first
+  std::stable_sort(c->gsrc_lpt.begin(), c->gsrc_lpt.end(), [&](int32_t x, int32_t y) {
+    return c->see[x] - c->seb[x] > c->see[y] - c->seb[y];
+  });
   c->gram_part_len = gpo;
   c->gram_len = go;
   c->fill_len = fo;
@@ -700,7 +704,7 @@ static int stage_step(Ctx* c, double lam, cudaStream_t st) {
     launch_gram(c->P.pixel_mode, c->d_gtiles, (int)c->gtiles.size(), kGramBlock, c->gram_smem, c->kmax, s,
                 c->pix, c->P.wts, c->d_eoff, c->d_doff, c->P.grid_w, c->grid, c->intr, c->d_Hdd, c->d_gd, lam,
                 c->O.ridge, c->d_gram_part, st, c->d_gorder);
-    launch_fill_transform(c->d_gsrc, (int)c->gsrc.size(), c->d_seb, c->d_see, c->d_g0, c->d_g1, c->d_gtiles,
+    launch_fill_transform(c->d_gsrc_lpt, (int)c->gsrc.size(), c->d_seb, c->d_see, c->d_g0, c->d_g1, c->d_gtiles,
                           c->d_foff, c->d_gram_part, s, c->extr, c->d_arena + c->arena_fill, c->kmax, st);
   }
   mark(c, 3, st);
@@ -975,7 +979,7 @@ int vba_create(void** out, const vba_problem* prob, const vba_options* opts, voi
       (rc = dupload(c, &c->d_t0s, c->t0s, st)) || (rc = dupload(c, &c->d_t1s, c->t1s, st)) ||
       (rc = dupload(c, &c->d_seb, c->seb, st)) || (rc = dupload(c, &c->d_see, c->see, st)) ||
       (rc = dupload(c, &c->d_gtiles, c->gtiles, st)) || (rc = dupload(c, &c->d_gsrc, c->gsrc, st)) ||
-      (rc = dupload(c, &c->d_gorder, c->gorder, st)) ||
+      (rc = dupload(c, &c->d_gorder, c->gorder, st)) || (rc = dupload(c, &c->d_gsrc_lpt, c->gsrc_lpt, st)) ||
       (rc = dupload(c, &c->d_g0, c->g0, st)) || (rc = dupload(c, &c->d_g1, c->g1, st)) ||
       (rc = dupload(c, &c->d_goff, c->goff, st)) || (rc = dupload(c, &c->d_foff, c->foff, st)) ||
       (rc = dupload(c, &c->d_fmap, c->fmap, st)))
