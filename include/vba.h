@@ -11,6 +11,7 @@
  *   vba_linearize        <- _linearize         solver.py:173-251
  *   vba_export_normal_eq <- (_linearize's dense outputs H_pp,H_pd,H_dd,g_p,g_d)
  *   vba_solve_step       <- _solve_step        solver.py:254-308
+ *   vba_export_reduced   <- (_solve_step's H_red, g_red)     solver.py:272-285
  *   vba_apply_step       <- _snapshot + _apply_step  solver.py:311-341
  *   vba_restore          <- _restore           solver.py:318-323
  *   vba_trial            <- one LM trial (solve, apply, energy) solver.py:370-383
@@ -144,6 +145,11 @@ VBA_API int vba_linearize(void* ctx, void* stream);
 VBA_API int vba_export_normal_eq(void* ctx, void* stream, double* H_pp, double* g_p, double* H_pd,
                          double* H_dd, double* g_d);
 VBA_API int vba_solve_step(void* ctx, void* stream, double lam, int32_t use_schur);
+/* Reduced (Schur) system of the last linearisation at damping lam, before the solve:
+ * H_red = Hf_d - Hfd D^-1 Hfd^T [nfree, nfree] row-major (full symmetric) and
+ * g_red = g_f - Hfd D^-1 g_d [nfree] (solver.py:272-285), device pointers;
+ * nfree = vba_reduced_dim().  Synchronises the stream. */
+VBA_API int vba_export_reduced(void* ctx, void* stream, double lam, double* H_red, double* g_red);
 /* dx_full [npv] (zeros at frozen states) and dx_d [n_disp] unpadded, device pointers */
 VBA_API int vba_export_step(void* ctx, void* stream, double* dx_full, double* dx_d);
 VBA_API int vba_apply_step(void* ctx, void* stream);

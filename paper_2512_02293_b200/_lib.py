@@ -19,7 +19,7 @@ PREINT_REC = 281
 
 EXPORTED = ("vba_last_error", "vba_version", "vba_create", "vba_destroy", "vba_set_collective",
             "vba_reduced_dim", "vba_energy", "vba_linearize", "vba_export_normal_eq",
-            "vba_solve_step", "vba_export_step", "vba_apply_step", "vba_restore", "vba_accept",
+            "vba_solve_step", "vba_export_step", "vba_export_reduced", "vba_apply_step", "vba_restore", "vba_accept",
             "vba_trial", "vba_solve", "vba_download", "vba_launch_count", "vba_stage_times",
             "vba_load_state", "vba_bind_inputs", "vba_set_profiling", "vba_stats", "vba_spd_solve", "vba_solve_times",
             "vba_preintegrate", "vba_preint_scratch_bytes",
@@ -97,6 +97,7 @@ def load(path: str | None = None):
         "vba_export_normal_eq": ([v, v, v, v, v, v, v], C.c_int),
         "vba_solve_step": ([v, v, C.c_double, C.c_int32], C.c_int),
         "vba_export_step": ([v, v, v, v], C.c_int),
+        "vba_export_reduced": ([v, v, C.c_double, v, v], C.c_int),
         "vba_apply_step": ([v, v], C.c_int),
         "vba_restore": ([v, v], C.c_int),
         "vba_accept": ([v, v], C.c_int),

@@ -2362,12 +2362,30 @@ __global__ void k_tc_resid(const double* __restrict__ b, const double* __restric
 }
 
 // after a refinement pass: stop when the correction is below tol max|x|, else
-// clear the maxima for the next pass (the last pass's values stay in out2)
-__global__ void k_tc_check(double* out2, int* stop, double tol, int last) {
+// Refinement stopping rule.  out[0] = max |correction| of this pass, out[1] = max |x|,
+// out[2] = passes run, out[3] = the previous pass's relative correction, out[4] = 1 once
+// accepted.  With the measured per-pass contraction rho = rel_k / rel_{k-1}, the error left
+// after pass k is bounded by rel_k * rho / (1 - rho) (geometric tail); the solve is accepted
+// when rel_k <= tol AND that bound is <= tol_err (both relative to max |x|).  A solve that
+// never meets both within `iters` passes is redone on the fp64 path by the caller.
+// The maxima are cleared for the next pass (the last pass's values stay in out).
+__global__ void k_tc_check(double* out, int* stop, double tol, double tol_err, int last) {
   if (*stop) return;
-  out2[2] += 1.0;   // passes run
-  if (out2[0] <= tol * out2[1]) *stop = 1;
-  else if (!last) out2[0] = out2[1] = 0.0;
+  out[2] += 1.0;   // passes run
+  const double rel = out[1] > 0.0 ? out[0] / out[1] : 0.0;
+  bool ok = false;
+  if (rel == 0.0) ok = true;
+  else if (rel <= tol && out[3] > 0.0) {
+    const double rho = rel / out[3];
+    ok = rho < 0.5 && rel * rho / (1.0 - rho) <= tol_err;
+  }
+  if (ok) {
+    out[4] = 1.0;
+    *stop = 1;
+  } else if (!last) {
+    out[3] = rel;
+    out[0] = out[1] = 0.0;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -2454,8 +2472,8 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
   launch_count();
   cudaMemsetAsync(x, 0, sizeof(double) * npad, st);
   cudaMemsetAsync(stop, 0, sizeof(int), st);
-  cudaMemsetAsync(out2, 0, sizeof(double) * 3, st);
-  if (nt > sms) return 1;   // one resident CTA per row tile (n <= 148 * 128 here)
+  cudaMemsetAsync(out2, 0, sizeof(double) * 5, st);
+  if (nt > sms) return 1;   // caller must solve on the fp64 path (out2[4] stays 0: not accepted)   // one resident CTA per row tile (n <= 148 * 128 here)
   // passes until the correction is <= kTcRefineTol max|x| (early-exit kernels after that), at most `iters`
   for (int it = 0; it < iters; ++it) {
     const double* rhs = b;
@@ -2484,7 +2502,7 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
     }
 #endif
     // stop once a pass corrects x by <= kTcRefineTol max|x| (vba_internal.cuh)
-    k_tc_check<<<1, 1, 0, st>>>(out2, stop, kTcRefineTol, it == iters - 1);
+    k_tc_check<<<1, 1, 0, st>>>(out2, stop, kTcRefineTol, kTcErrTol, it == iters - 1);
     launch_count();
     launch_count();
     launch_count();

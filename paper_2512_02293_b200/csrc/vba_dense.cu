@@ -145,6 +145,24 @@ void launch_pack_lower(double* H, int64_t ld, int n, double* buf, int unpack, cu
   launch_count();
 }
 
+// full symmetric row-major copy of the lower triangle (column-major, leading dim ld) of
+// the n x n reduced system, and g = scale * rhs (export of H_red / g_red for parity tests)
+__global__ void k_export_sym(const double* __restrict__ H, int64_t ld, int n, double* __restrict__ out,
+                             const double* __restrict__ rhs, double scale, double* __restrict__ g) {
+  const int r = blockIdx.x;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    const int lo = r > c ? c : r, hi = r > c ? r : c;
+    out[(int64_t)r * n + c] = H[(int64_t)lo * ld + hi];
+  }
+  if (threadIdx.x == 0 && g) g[r] = scale * rhs[r];
+}
+void launch_export_sym(const double* H, int64_t ld, int n, double* out, const double* rhs, double scale, double* g,
+                       cudaStream_t st) {
+  if (n <= 0) return;
+  k_export_sym<<<n, 256, 0, st>>>(H, ld, n, out, rhs, scale, g);
+  launch_count();
+}
+
 // identity padding of the tile-padded matrix (rows/cols n..npad) and zero rhs padding
 __global__ void k_pad_identity(double* H, int64_t ld, int n, int npad, double* rhs) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -52,7 +52,7 @@ struct Result {       // device -> host once per trial
   unsigned long long step_bits;
   int status;         // fp64 factorisation: non-positive pivot
   int tc_bad;         // tensor-core factorisation: non-positive pivot
-  double tc[3];       // tensor-core solve: last refinement correction, max |x|, passes
+  double tc[5];       // tensor-core solve: last correction, max |x|, passes, previous rel. correction, accepted
 };
 
 template <class T>
@@ -129,6 +129,7 @@ struct Ctx {
   int n_tctasks = 0;
   bool use_tc = false;             // VBA_CHOL=tc: tensor-core reduced solve
   bool force_fp64 = false;         // this step: fp64 DAG (tensor-core solve failed its checks)
+  bool tc_ran = false;             // the last step's reduced solve ran on the tensor cores
   int tc_gen = 1;
   int tc_iters = 8;   // refinement passes at most (early exit once converged)
   int64_t tc_fallbacks = 0;
@@ -694,10 +695,11 @@ static int stage_linearize(Ctx* c, cudaStream_t st) {
   return VBA_OK;
 }
 
-// reduced system + Cholesky + back-substitution into the NEXT buffers
-static int stage_step(Ctx* c, double lam, cudaStream_t st) {
+// Schur fill-in + freeze/damp assembly of the reduced system H_red (lower triangle of
+// d_H, column-major) and its right-hand side -g_red (d_rhs), all-reduced across ranks
+// for a sharded solve (solver.py:272-285)
+static int stage_reduce(Ctx* c, double lam, cudaStream_t st) {
   DevState& s = CUR(c);
-  DevState& n = NXT(c);
   mark(c, 2, st);
   VBA_CUDA(cudaMemsetAsync(c->d_res, 0, sizeof(Result), st));
   if (!c->gtiles.empty()) {
@@ -728,17 +730,33 @@ static int stage_step(Ctx* c, double lam, cudaStream_t st) {
       if (c->coll(c->coll_user, c->d_rhs, c->npad, 0, st)) { set_err("allreduce(g) failed"); return VBA_E_CUDA; }
       launch_add_ridge(c->d_H, c->npad, c->nfree, c->O.ridge, st);
     }
+  }
+  return VBA_OK;
+}
+
+// reduced system + Cholesky + back-substitution into the NEXT buffers
+static int stage_step(Ctx* c, double lam, cudaStream_t st) {
+  DevState& s = CUR(c);
+  DevState& n = NXT(c);
+  int rc = stage_reduce(c, lam, st);
+  if (rc) return rc;
+  if (c->nfree > 0) {
     if (getenv("VBA_CHOL_TRACE") && !c->d_trace) {
       if (dalloc(c, &c->d_trace, (size_t)4 * std::max(1, c->n_ctasks) + 16 * (size_t)std::max(1, c->nt)))
         return VBA_E_CUDA;
     }
+    bool tc_ran = false;
     if (c->use_tc && !c->force_fp64 && !c->d_trace) {
-      chol_tc_solve(c->d_H, c->npad, c->nfree, c->npad, c->d_rhs, c->d_x, c->d_tcws, c->d_tctasks, c->n_tctasks,
-                    c->tc_iters, &c->d_res->tc_bad, c->tc_gen, st, c->d_res->tc, nullptr,
-                    c->prof ? c->sev : nullptr);
-      c->sev_pending = c->prof;
+      // returns non-zero (before any refinement) when the system is too large for its
+      // co-resident triangular solves: solved on the fp64 DAG below instead
+      tc_ran = chol_tc_solve(c->d_H, c->npad, c->nfree, c->npad, c->d_rhs, c->d_x, c->d_tcws, c->d_tctasks,
+                             c->n_tctasks, c->tc_iters, &c->d_res->tc_bad, c->tc_gen, st, c->d_res->tc, nullptr,
+                             c->prof ? c->sev : nullptr) == 0;
+      c->sev_pending = c->prof && tc_ran;
       c->tc_gen += 2 * c->tc_iters;
-    } else {
+    }
+    c->tc_ran = tc_ran;
+    if (!tc_ran) {
       chol_dag_launch(c->d_H, c->npad, c->nt, c->d_rhs, c->d_x, c->d_Ld, c->d_cpart, c->d_cflags, c->d_ctasks,
                       c->n_ctasks, &c->d_res->status, st, c->d_trace);
     }
@@ -846,11 +864,11 @@ static int stage_step_any(Ctx* c, double lam, int use_schur, cudaStream_t st) {
 // The tensor-core solve is accepted when its fp32 factor had positive pivots and
 // the last fp64 refinement pass moved x by <= kTcRefineTol max|x|.
 static bool tc_failed(Ctx* c, int use_schur) {
-  if (!c->use_tc || c->force_fp64 || c->d_trace || c->nfree == 0 || !(use_schur || c->n_disp == 0)) return false;
+  if (!c->tc_ran || c->nfree == 0 || !(use_schur || c->n_disp == 0)) return false;
   const Result& r = *c->h_res;
   ++c->tc_solves;
   c->tc_passes += (int64_t)r.tc[2];
-  return r.tc_bad != 0 || !(r.tc[0] <= kTcRefineTol * r.tc[1]);
+  return r.tc_bad != 0 || r.tc[4] != 1.0;
 }
 
 static int run_trial(Ctx* c, double lam, int use_schur, vba_trial_result* out, cudaStream_t st) {
@@ -1030,6 +1048,12 @@ int vba_create(void** out, const vba_problem* prob, const vba_options* opts, voi
     if (ch && std::strcmp(ch, "tc") == 0) c->use_tc = c->nt > 0;
     else if (ch && std::strcmp(ch, "fp64") == 0) c->use_tc = false;
     else c->use_tc = c->nt >= kTcMinTiles;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // the tensor-core solve's triangular sweeps keep one CTA per 128-row tile resident:
+    // larger systems (n > 128 * SMs = 18944 on B200) are solved on the fp64 tile DAG
+    if (c->nt > sms) c->use_tc = false;
     const char* it = getenv("VBA_TC_ITERS");
     if (it) c->tc_iters = std::max(1, atoi(it));
   }
@@ -1134,7 +1158,7 @@ int vba_spd_solve(const double* H, int64_t n, const double* b, double* x, int32_
   };
   if (cudaMalloc(&Hp, sizeof(double) * (size_t)npad * npad) || cudaMalloc(&bp, sizeof(double) * npad) ||
       cudaMalloc(&xp, sizeof(double) * npad) || cudaMalloc(&Ld, sizeof(double) * (size_t)nt * NBc * NBc) ||
-      cudaMalloc(&part, sizeof(double) * (size_t)nt * nt * NBc) || cudaMalloc(&tc2, sizeof(double) * 3) ||
+      cudaMalloc(&part, sizeof(double) * (size_t)nt * nt * NBc) || cudaMalloc(&tc2, sizeof(double) * 5) ||
       cudaMalloc(&flags, sizeof(int) * ((size_t)2 * nt * nt + nt + 1)) || cudaMalloc(&stat, sizeof(int) * 2) ||
       cudaMalloc(&tasks, tb.size()) || cudaMalloc(&tasks2, tb2.size()) || (tcb && cudaMalloc(&ws, tcb))) {
     cleanup();
@@ -1144,7 +1168,7 @@ int vba_spd_solve(const double* H, int64_t n, const double* b, double* x, int32_
   cudaMemsetAsync(Hp, 0, sizeof(double) * (size_t)npad * npad, st);
   cudaMemsetAsync(bp, 0, sizeof(double) * npad, st);
   cudaMemsetAsync(stat, 0, sizeof(int) * 2, st);
-  cudaMemsetAsync(tc2, 0, sizeof(double) * 3, st);
+  cudaMemsetAsync(tc2, 0, sizeof(double) * 5, st);
   if (tcb) cudaMemsetAsync(ws, 0, tcb, st);
   cudaMemcpy2DAsync(Hp, sizeof(double) * npad, H, sizeof(double) * n, sizeof(double) * n, n,
                     cudaMemcpyDeviceToDevice, st);
@@ -1153,18 +1177,18 @@ int vba_spd_solve(const double* H, int64_t n, const double* b, double* x, int32_
   cudaMemcpyAsync(tasks2, tb2.data(), tb2.size(), cudaMemcpyHostToDevice, st);
   launch_pad_identity(Hp, npad, (int)n, npad, bp, st);
   int hs[2] = {0, 0};
-  double h2[2] = {0, 0};
+  double h2[5] = {0, 0, 0, 0, 0};
   int used_tc = 0;
   if (mode == 0 || mode == 2) {   // 2: tensor-core result without the fallback (diagnostics)
     const int iters = info && info[0] > 0 ? info[0] : 8;
     unsigned long long* tr = nullptr;
     if (getenv("VBA_CHOL_TRACE")) { cudaMalloc(&tr, sizeof(unsigned long long) * (4 * (size_t)ntasks2 + 16 * (size_t)nt)); cudaMemsetAsync(tr, 0, sizeof(unsigned long long) * (4 * (size_t)ntasks2 + 16 * (size_t)nt), st); }
-    chol_tc_solve(Hp, npad, (int)n, npad, bp, xp, ws, tasks2, ntasks2, iters, stat + 1, 1, st, tc2, tr);
+    const int tcrc = chol_tc_solve(Hp, npad, (int)n, npad, bp, xp, ws, tasks2, ntasks2, iters, stat + 1, 1, st, tc2, tr);
     if (tr) { cudaStreamSynchronize(st); chol_trace_print("tc", tr, tasks2, ntasks2, nt); cudaFree(tr); }
     cudaMemcpyAsync(hs, stat, sizeof(hs), cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(h2, tc2, sizeof(h2), cudaMemcpyDeviceToHost, st);
     if (cudaStreamSynchronize(st) != cudaSuccess) { cleanup(); set_err("vba_spd_solve: %s", cudaGetErrorString(cudaGetLastError())); return VBA_E_CUDA; }
-    used_tc = (mode == 2 || (hs[1] == 0 && h2[0] <= kTcRefineTol * h2[1])) ? 1 : 0;
+    used_tc = tcrc == 0 && (mode == 2 || (hs[1] == 0 && h2[4] == 1.0)) ? 1 : 0;
   }
   if (!used_tc) {
     chol_dag_launch(Hp, npad, nt, bp, xp, Ld, part, flags, tasks, ntasks, stat, st);
@@ -1373,6 +1397,16 @@ int vba_export_normal_eq(void* ctx, void* stream, double* H_pp, double* g_p, dou
     launch_export_hpd(c->P.pixel_mode, c->d_seb, c->d_see, c->d_doff, c->d_roff_real, c->d_npix, c->maxpix, c->d_ej,
                       c->K, s, c->extr, c->pix, c->P.wts, c->d_eoff, c->P.grid_w, c->grid, c->intr, o, st);
   }
+  VBA_CUDA(cudaStreamSynchronize(st));
+  return VBA_OK;
+}
+
+int vba_export_reduced(void* ctx, void* stream, double lam, double* H_red, double* g_red) {
+  Ctx* c = (Ctx*)ctx;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = stage_reduce(c, lam, st);
+  if (rc) return rc;
+  launch_export_sym(c->d_H, c->npad, c->nfree, H_red, c->d_rhs, -1.0, g_red, st);
   VBA_CUDA(cudaStreamSynchronize(st));
   return VBA_OK;
 }

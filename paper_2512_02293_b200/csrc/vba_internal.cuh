@@ -320,6 +320,8 @@ void launch_assemble_vec(const int32_t* seg_ptr, const Vec* vecs, int nseg, cons
 void launch_add_ridge(double* H, int64_t ld, int n, double ridge, cudaStream_t st);
 void launch_pack_lower(double* H, int64_t ld, int n, double* buf, int unpack, cudaStream_t st);
 void launch_pad_identity(double* H, int64_t ld, int n, int npad, double* rhs, cudaStream_t st);
+void launch_export_sym(const double* H, int64_t ld, int n, double* out, const double* rhs, double scale, double* g,
+                       cudaStream_t st);
 // tile-task DAG Cholesky (vba_chol.cu): plan writes up to `cap` task records into `out`
 // (opaque, chol_task_bytes() each) and returns the task count
 int chol_plan_tasks(int nt, void* out, int cap);
@@ -363,11 +365,13 @@ void launch_dense_dxd(const double* x, int nf, const int64_t* doff, const int64_
                       cudaStream_t st);
 void launch_unpad(const float* src, const int64_t* doff, const int64_t* roff, const int32_t* npix, int maxpix, int K,
                   double* dst, cudaStream_t st);
-// The tensor-core reduced solve stops refining once a pass corrects x by <= this fraction
-// of max|x|; the remaining error is then ~tol x (the factor's per-pass contraction, ~1e-3
-// measured), i.e. ~1e-8 relative, far inside the 1e-5 update parity.  A solve whose last
-// pass still moved x by more is redone on the fp64 path.
+// The tensor-core reduced solve stops refining once a pass corrects x by <= kTcRefineTol
+// max|x| AND the geometric-tail bound of the remaining error, rel * rho / (1 - rho) with the
+// measured per-pass contraction rho, is <= kTcErrTol (k_tc_check); with the factor's usual
+// contraction (~1e-3) that is 3 passes and ~1e-9 relative error, far inside the 1e-5 update
+// parity.  A solve that does not meet both within its pass budget is redone on the fp64 path.
 constexpr double kTcRefineTol = 1e-5;
+constexpr double kTcErrTol = 1e-8;
 
 // IMU preintegration (vba_preint.cu): record per keyframe pair, see include/vba.h.
 constexpr int kPreintRec = 281;

@@ -259,8 +259,10 @@ class DeviceProblem:
     def linearize(self):
         L.check(self.lib.vba_linearize(self.ctx, self._sptr()))
 
-    def export_normal_eq(self, with_hpd=True):
-        """Reference-layout (H_pp, H_pd, H_dd, g_p, g_d) as numpy fp64 (solver.py:173-251)."""
+    def export_normal_eq(self, with_hpd=True, hpd_cols=None):
+        """Reference-layout (H_pp, H_pd, H_dd, g_p, g_d) as numpy fp64 (solver.py:173-251).
+
+        ``hpd_cols``: return only these disparity columns of H_pd (gathered on the device)."""
         dev = self.device
         npv, nd = self.npv, self.n_disp
         Hpp = torch.empty((npv, npv), dtype=torch.float64, device=dev)
@@ -271,9 +273,19 @@ class DeviceProblem:
         L.check(self.lib.vba_export_normal_eq(self.ctx, self._sptr(), Hpp.data_ptr(), gp.data_ptr(),
                                               Hpd.data_ptr() if Hpd is not None else None,
                                               Hdd.data_ptr(), gd.data_ptr()))
-        out = [Hpp.cpu().numpy(), Hpd[:, :nd].cpu().numpy() if Hpd is not None else None,
+        if Hpd is not None:
+            Hpd = Hpd[:, :nd] if hpd_cols is None else Hpd[:, torch.as_tensor(hpd_cols, device=dev)]
+        out = [Hpp.cpu().numpy(), Hpd.cpu().numpy() if Hpd is not None else None,
                Hdd[:nd].cpu().numpy(), gp.cpu().numpy(), gd[:nd].cpu().numpy()]
         return tuple(out)
+
+    def export_reduced(self, lam):
+        """Reduced system (H_red, g_red) at damping ``lam`` (solver.py:272-285), numpy fp64."""
+        n = int(self.lib.vba_reduced_dim(self.ctx))
+        Hr = torch.empty((max(n, 1), max(n, 1)), dtype=torch.float64, device=self.device)
+        gr = torch.empty(max(n, 1), dtype=torch.float64, device=self.device)
+        L.check(self.lib.vba_export_reduced(self.ctx, self._sptr(), float(lam), Hr.data_ptr(), gr.data_ptr()))
+        return Hr[:n, :n].cpu().numpy(), gr[:n].cpu().numpy()
 
     def solve_step(self, lam, use_schur=True):
         """_solve_step (solver.py:265-308): returns (dx_full, dx_d) numpy fp64."""

@@ -17,8 +17,48 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA B200 (sm_100a) device and the built libvba")
 
 
+# --- BASELINE-config goldens (tests/golden/make_config_golden.py) -----------------
+GOLD_FULL_VEC = 65536      # per-pixel vectors stored whole up to this length, else sampled
+GOLD_VEC_SAMPLES = 32768   # seeded sample size of longer per-pixel vectors
+GOLD_FULL_MAT = 256        # pose-space matrices stored whole up to this order, else by blocks
+GOLD_OTHER_BLOCKS = 1500   # off-band non-zero blocks stored (seeded sample) for large matrices
+
+
+def golden_vec_indices(n, seed):
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.choice(n, GOLD_VEC_SAMPLES, replace=False)).astype(np.int64)
+
+
+def golden_proj_vector(n, seed):
+    return np.random.default_rng(seed).standard_normal(n)
+
+
+def packed_hash(P):
+    """sha256 of a packed problem (pack_graph output): identifies the generated inputs."""
+    import hashlib
+    h = hashlib.sha256()
+    for k in sorted(P):
+        a = np.ascontiguousarray(np.asarray(P[k]))
+        h.update(k.encode())
+        h.update(str(a.dtype).encode() + str(a.shape).encode())
+        h.update(a.tobytes())
+    return h.hexdigest()
+
+
+def load_config_golden(cfg):
+    z = np.load(os.path.join(GOLDEN_DIR, f"bcfg{cfg}.npz"), allow_pickle=False)
+    out = {k: z[k] for k in z.files}
+    out["meta"] = json.loads(str(out["meta"]))
+    return out
+
+
+def config_golden_names():
+    return sorted(int(os.path.basename(p)[4:-4]) for p in glob.glob(os.path.join(GOLDEN_DIR, "bcfg*.npz")))
+
+
 def golden_names():
-    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz")))
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz"))
+                  if not os.path.basename(p).startswith("bcfg"))
 
 
 def load_golden(name):
