@@ -18,6 +18,7 @@ PyTorch provides device memory and the CUDA stream only.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 import torch
@@ -85,79 +86,333 @@ def imu_records(P):
     return R
 
 
-class HostLayout:
-    """Padded, source-sorted host arrays (numpy) ready for upload."""
+def _f64(a):
+    return a if (type(a) is np.ndarray and a.dtype == np.float64) else np.asarray(a, dtype=np.float64)
 
-    def __init__(self, P, opts, edge_subset=None, imu_subset=None):
-        K = len(P["kid"])
+
+class _PackedSource:
+    """Layout source over a packed problem dict (``problem.pack_graph``; already validated)."""
+
+    def __init__(self, P):
+        self.P = P
+        self.K = len(P["kid"])
+        self.kid = np.asarray(P["kid"], np.int64)
+        self.doff = np.asarray(P["doff"], np.int64)
+        self.npix = (self.doff[1:] - self.doff[:-1]).astype(np.int64)
+        self.ei = np.asarray(P["ei"], np.int64)
+        self.ej = np.asarray(P["ej"], np.int64)
+        self.eoff = np.asarray(P["eoff"], np.int64)
+        self.state = np.concatenate([P["q"], P["p"], P["v"], P["bg"], P["ba"]], axis=1).astype(np.float64)
+        self.ts = np.asarray(P["ts"], np.float64)
+        self.grav = np.concatenate([P["grav_q"], [P["grav_G"]]]).astype(np.float64)
+        self.intr = np.asarray(P["intr"], np.float64)
+        self.has_Tcb = bool(P.get("has_Tcb", False))
+        self.Tcb = np.asarray(P["Tcb"], np.float64)
+        self.fi = np.asarray(P["fi"], np.int64)
+        self.fj = np.asarray(P["fj"], np.int64)
+        self._imu = None
+        self.kpix = [P["pix"][self.doff[k]:self.doff[k + 1]] for k in range(self.K)]
+        self.kdisp = [P["disp"][self.doff[k]:self.doff[k + 1]] for k in range(self.K)]
+
+    def imu(self, idx):
+        if self._imu is None:
+            self._imu = imu_records(self.P)
+        return self._imu[idx]
+
+    def edge(self, e):
+        r0, r1 = self.eoff[e], self.eoff[e + 1]
+        P = self.P
+        return P["epix"][r0:r1], P["tgt"][r0:r1], P["w"][r0:r1]
+
+
+class _GraphSource:
+    """Layout source read straight from a reference-style FrameGraph (duck-typed), with the
+    validation of ``problem.pack_graph`` (residuals.py:181-185, 281-284)."""
+
+    def __init__(self, graph):
+        kfs = list(graph.keyframes)
+        K = len(kfs)
         self.K = K
-        doff = np.asarray(P["doff"], np.int64)
-        npix = (doff[1:] - doff[:-1]).astype(np.int64)
+        self.kid = np.array([kf.kid for kf in kfs], dtype=np.int64)
+        index = {int(k): n for n, k in enumerate(self.kid)}
+        st = np.empty((K, 16))
+        ts = np.empty(K)
+        self.kpix, self.kdisp = [], []
+        for n, kf in enumerate(kfs):
+            s = kf.state
+            st[n, 0:4] = s.pose.rotation.q
+            st[n, 4:7] = s.pose.translation
+            st[n, 7:10] = s.velocity
+            st[n, 10:13] = s.bias.gyro_bias
+            st[n, 13:16] = s.bias.accel_bias
+            ts[n] = s.timestamp
+            d = _f64(kf.disparities).reshape(-1)
+            if len(d) and d.min() <= 0.0:
+                raise ValueError("disparities must be strictly positive")
+            self.kdisp.append(d)
+            self.kpix.append(_f64(kf.pixels).reshape(-1, 2))
+        self.state, self.ts = st, ts
+        self.npix = np.array([len(d) for d in self.kdisp], dtype=np.int64)
+        self.doff = np.concatenate([[0], np.cumsum(self.npix)]).astype(np.int64)
+        edges = list(graph.vision_edges)
+        self.edges = edges
+        self.ei = np.array([index[e.i] for e in edges], dtype=np.int64)
+        self.ej = np.array([index[e.j] for e in edges], dtype=np.int64)
+        rows = np.array([len(e.pixels) for e in edges], dtype=np.int64)
+        if len(edges) and np.any(rows != self.npix[self.ei]):
+            raise ValueError("disparity length must match edge pixel list")
+        self.eoff = np.concatenate([[0], np.cumsum(rows)]).astype(np.int64)
+        ies = list(graph.inertial_edges)
+        F = len(ies)
+        self.fi = np.array([index[i] for i, _, _ in ies], dtype=np.int64)
+        self.fj = np.array([index[j] for _, j, _ in ies], dtype=np.int64)
+        R = np.zeros((F, L.IMU_REC))
+        for f, (_, _, d) in enumerate(ies):
+            r = R[f]
+            r[0] = d.dt_total
+            r[1:5] = d.delta_R.q
+            r[5:8] = d.delta_p
+            r[8:11] = d.delta_v
+            r[11:20] = np.asarray(d.J_rot, float).reshape(9)
+            r[20:38] = np.asarray(d.J_pos, float).reshape(18)
+            r[38:56] = np.asarray(d.J_vel, float).reshape(18)
+            cov = np.asarray(d.covariance, float).reshape(15, 15)
+            r[56:137] = cov[:9, :9].reshape(81)
+            r[137:173] = cov[9:15, 9:15].reshape(36)
+            r[173:176] = d.bias_lin_point.gyro_bias
+            r[176:179] = d.bias_lin_point.accel_bias
+        if F:
+            dts = ts[self.fj] - ts[self.fi]
+            bad = np.nonzero(np.abs(dts - R[:, 0]) > 1e-6)[0]
+            if len(bad):
+                f = int(bad[0])
+                raise ValueError(f"delta spans {R[f, 0]:.6f}s but states are {dts[f]:.6f}s apart")
+        self._imu = R
+        g = graph.gravity
+        self.grav = np.concatenate([np.asarray(g.R_wg.q, float), [float(g.magnitude)]])
+        k = graph.intrinsics
+        self.intr = np.array([k.fx, k.fy, k.cx, k.cy], dtype=float)
+        T = getattr(graph, "T_cb", None)
+        self.has_Tcb = T is not None
+        self.Tcb = (np.concatenate([np.asarray(T.rotation.q, float), np.asarray(T.translation, float)])
+                    if T is not None else np.array([1.0, 0, 0, 0, 0, 0, 0]))
+
+    def imu(self, idx):
+        return self._imu[idx]
+
+    def edge(self, e):
+        x = self.edges[e]
+        return _f64(x.pixels), _f64(x.targets), _f64(x.weights)
+
+
+def _same_buffer(a, b):
+    """a and b view the same memory with the same layout (e.g. an edge sharing its source
+    keyframe's pixel array), so their contents are equal without reading them."""
+    if a is b:
+        return True
+    ia, ib = a.__array_interface__, b.__array_interface__
+    return ia["data"][0] == ib["data"][0] and a.shape == b.shape and a.strides == b.strides and a.dtype == b.dtype
+
+
+def _host_buffer(shape, dtype, pinned):
+    """Zero-free host buffer; page-locked (torch's caching host allocator) when ``pinned``."""
+    if pinned:
+        tdt = {np.float32: torch.float32, np.float64: torch.float64}[dtype]
+        t = torch.empty(shape, dtype=tdt, pin_memory=True)
+        return t.numpy(), t
+    return np.empty(shape, dtype), None
+
+
+_POOL = None
+
+
+def _pack_threads(total_rows):
+    n = int(os.environ.get("VBA_PACK_THREADS", "0")) or min(32, os.cpu_count() or 1)
+    return 1 if total_rows < (1 << 16) else n
+
+
+def _pool():
+    global _POOL
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _POOL = ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1), thread_name_prefix="vba-pack")
+    return _POOL
+
+
+class HostLayout:
+    """Padded, source-sorted host arrays (numpy) ready for upload.
+
+    Built from a packed problem dict (``HostLayout(P, opts)``) or straight from a
+    FrameGraph (``HostLayout.from_graph``); both run the same fill, so the arrays are
+    bitwise identical.  Flow targets are stored relative to the source pixel,
+    u* - u, computed in fp64 and rounded once to fp32 (the kernels predict the
+    displacement, which keeps fp32 error proportional to the flow).  The per-edge
+    fill runs on a thread pool (numpy releases the GIL in its loops) into page-locked
+    buffers when ``pinned``, so the upload is one asynchronous DMA per array.
+    """
+
+    def __init__(self, P, opts, edge_subset=None, imu_subset=None, pinned=False, _src=None):
+        self._build(_src if _src is not None else _PackedSource(P), opts, edge_subset, imu_subset, pinned)
+
+    @classmethod
+    def from_graph(cls, graph, opts, pinned=None):
+        if pinned is None:
+            pinned = torch.cuda.is_available()
+        return cls(None, opts, pinned=pinned, _src=_GraphSource(graph))
+
+    def _build(self, S, opts, edge_subset, imu_subset, pinned):
+        K = S.K
+        self.K = K
+        npix = S.npix
         npad = (npix + 3) // 4 * 4
         self.npix = npix.astype(np.int32)
+        self.doff = S.doff
         self.doff_pad = np.concatenate([[0], np.cumsum(npad)]).astype(np.int64)
-        self.doff = doff
-        ei_all = np.asarray(P["ei"], np.int64)
-        eidx = np.arange(len(ei_all)) if edge_subset is None else np.asarray(edge_subset, np.int64)
-        order = eidx[np.argsort(ei_all[eidx], kind="stable")]
+        eidx = np.arange(len(S.ei)) if edge_subset is None else np.asarray(edge_subset, np.int64)
+        order = eidx[np.argsort(S.ei[eidx], kind="stable")]
         self.edge_order = order
-        ei = ei_all[order]
-        ej = np.asarray(P["ej"], np.int64)[order]
+        ei, ej = S.ei[order], S.ej[order]
         E = len(order)
         self.E = E
+        rows = (S.eoff[order + 1] - S.eoff[order]) if E else np.zeros(0, np.int64)
         rows_pad = npad[ei] if E else np.zeros(0, np.int64)
         self.eoff_pad = (np.concatenate([[0], np.cumsum(rows_pad)])[:-1] if E else np.zeros(0)).astype(np.int64)
         n_rows_pad = int(rows_pad.sum()) if E else 0
-        src = np.full(n_rows_pad, -1, np.int64)
-        eoff = np.asarray(P["eoff"], np.int64)
-        for k, e in enumerate(order):
-            n = int(eoff[e + 1] - eoff[e])
-            src[self.eoff_pad[k]:self.eoff_pad[k] + n] = np.arange(eoff[e], eoff[e] + n)
-        valid = src >= 0
-        self.tgt = np.zeros((n_rows_pad, 2), np.float32)
-        self.w = np.zeros((n_rows_pad, 2), np.float32)
-        # flow targets relative to the source pixel, u* - u (fp64 difference, then fp32):
-        # the kernels predict the displacement, keeping fp32 error proportional to the flow
-        self.tgt[valid] = P["tgt"][src[valid]] - P["epix"][src[valid]]
-        self.w[valid] = P["w"][src[valid]]
         self.n_rows_pad = n_rows_pad
+        self.tgt, self._tgt_t = _host_buffer((n_rows_pad, 2), np.float32, pinned)
+        self.w, self._w_t = _host_buffer((n_rows_pad, 2), np.float32, pinned)
+
+        kpix = S.kpix
+        # weight signs are checked here for host-only layouts, else on the device after the
+        # upload (DeviceProblem), which reads the fp32 copy at HBM speed instead of the fp64 source
+        self.weights_checked = not pinned
+        neg = self._fill_edges(S, order, ei, rows, rows_pad, kpix, check_neg=not pinned)
+        if neg:
+            raise ValueError("weights must be non-negative")
+
         n_disp_pad = int(self.doff_pad[-1])
         self.n_disp_pad = n_disp_pad
+        n_real = int(S.doff[-1])
+        kk = np.repeat(np.arange(K), npix)
+        pos = np.arange(n_real) - S.doff[kk] + self.doff_pad[kk]      # padded slot of every real pixel
         dsrc = np.full(n_disp_pad, -1, np.int64)
-        for k in range(K):
-            dsrc[self.doff_pad[k]:self.doff_pad[k] + npix[k]] = np.arange(doff[k], doff[k + 1])
+        dsrc[pos] = np.arange(n_real)
         self.dsrc = dsrc
-        self.disp = np.ones(n_disp_pad, np.float32)
-        self.disp[dsrc >= 0] = P["disp"][dsrc[dsrc >= 0]]
-        self.mode, self.grid = detect_pixel_mode(P)
+        self.disp, self._disp_t = _host_buffer(n_disp_pad, np.float32, pinned)
+        self.disp.fill(1.0)
+        for k in range(K):
+            if npix[k]:
+                self.disp[self.doff_pad[k]:self.doff_pad[k] + npix[k]] = S.kdisp[k]
+        self.mode, self.grid = self._pixel_mode(kpix, self._edge_mismatch)
         if self.mode == L.PIX_KF:
             self.pix = np.zeros((n_disp_pad, 2), np.float32)
-            self.pix[dsrc >= 0] = P["pix"][dsrc[dsrc >= 0]]
+            for k in range(K):
+                self.pix[self.doff_pad[k]:self.doff_pad[k] + npix[k]] = kpix[k]
         elif self.mode == L.PIX_EDGE:
             self.pix = np.zeros((n_rows_pad, 2), np.float32)
-            self.pix[valid] = P["epix"][src[valid]]
+            for k, e in enumerate(order):
+                self.pix[self.eoff_pad[k]:self.eoff_pad[k] + rows[k]] = S.edge(e)[0]
         else:
             self.pix = None
         self.ei = ei.astype(np.int32)
         self.ej = ej.astype(np.int32)
-        fi = np.asarray(P["fi"], np.int64)
-        fidx = np.arange(len(fi)) if imu_subset is None else np.asarray(imu_subset, np.int64)
-        self.fi = fi[fidx].astype(np.int32)
-        self.fj = np.asarray(P["fj"], np.int64)[fidx].astype(np.int32)
-        self.imu = imu_records(P)[fidx] if len(fidx) else np.zeros((0, L.IMU_REC))
+        fidx = np.arange(len(S.fi)) if imu_subset is None else np.asarray(imu_subset, np.int64)
+        self.fi = S.fi[fidx].astype(np.int32)
+        self.fj = S.fj[fidx].astype(np.int32)
+        self.imu = S.imu(fidx) if len(fidx) else np.zeros((0, L.IMU_REC))
         self.F = len(fidx)
-        self.state = np.concatenate([P["q"], P["p"], P["v"], P["bg"], P["ba"]], axis=1).astype(np.float64)
-        self.ts = np.asarray(P["ts"], np.float64)
-        self.grav = np.concatenate([P["grav_q"], [P["grav_G"]]]).astype(np.float64)
+        self.state = S.state
+        self.ts = S.ts
+        self.grav = S.grav
         frozen = set(int(k) for k in opts.get("frozen_keyframes", (0,)))
-        self.frozen = np.array([int(k) in frozen for k in P["kid"]], np.int32)
-        self.intr = np.asarray(P["intr"], np.float64)
-        self.has_Tcb = bool(P.get("has_Tcb", False))
-        self.Tcb = np.asarray(P["Tcb"], np.float64)
+        self.frozen = np.array([int(k) in frozen for k in S.kid], np.int32)
+        self.intr = S.intr
+        self.has_Tcb = S.has_Tcb
+        self.Tcb = S.Tcb
+
+    def _fill_edges(self, S, order, ei, rows, rows_pad, kpix, check_neg=True):
+        """flow (u* - u, fp64 difference rounded to fp32) and weights of every edge into the
+        padded rows; records whether any edge's pixels differ from its source keyframe's.
+
+        Graph sources go through the native packer (csrc/vba_pack.cpp: buffer protocol,
+        GIL released, one thread per row range); packed dicts through numpy slices."""
+        T, W, eoff_pad = self.tgt, self.w, self.eoff_pad
+        if isinstance(S, _GraphSource):
+            from . import _vbapack
+            mism, neg = _vbapack.pack_edges(
+                S.edges, np.ascontiguousarray(order, np.int64), np.ascontiguousarray(ei, np.int64),
+                np.ascontiguousarray(rows, np.int64), np.ascontiguousarray(eoff_pad, np.int64),
+                np.ascontiguousarray(rows_pad, np.int64), kpix, T.reshape(-1), W.reshape(-1),
+                _pack_threads(int(rows.sum()) if len(rows) else 0), int(check_neg))
+            self._edge_mismatch = bool(mism)
+            return bool(neg)
+
+        def run(k0, k1):
+            mism = neg = False
+            for k in range(k0, k1):
+                pix, tgt, w = S.edge(order[k])
+                r0 = eoff_pad[k]
+                r1 = r0 + rows[k]
+                rp = r0 + rows_pad[k]
+                np.subtract(tgt, pix, out=T[r0:r1], casting="unsafe")
+                np.copyto(W[r0:r1], w, casting="unsafe")
+                if rp > r1:
+                    T[r1:rp] = 0.0
+                    W[r1:rp] = 0.0
+                if check_neg and rows[k] and w.min() < 0.0:
+                    neg = True
+                if not mism:
+                    kp = kpix[ei[k]]
+                    mism = not (_same_buffer(pix, kp) or (pix.shape == kp.shape and np.array_equal(pix, kp)))
+            return mism, neg
+
+        E = len(order)
+        total = int(rows.sum()) if E else 0
+        if total < (1 << 18) or E < 16:
+            res = [run(0, E)]
+        else:
+            nch = min(8 * min(16, os.cpu_count() or 1), E)
+            cuts = np.linspace(0, E, nch + 1).astype(int)
+            res = list(_pool().map(lambda ab: run(*ab), zip(cuts[:-1], cuts[1:])))
+        self._edge_mismatch = any(m for m, _ in res)
+        return any(n for _, n in res)
+
+    @staticmethod
+    def _pixel_mode(kpix, edge_mismatch):
+        """VBA_PIX_GRID when every keyframe uses the same exact regular grid and every edge
+        the pixels of its source keyframe; VBA_PIX_KF / VBA_PIX_EDGE otherwise."""
+        if edge_mismatch:
+            return L.PIX_EDGE, None
+        gp = None
+        first = None
+        seen = {}
+        for X in kpix:
+            if len(X) == 0:
+                continue
+            g = seen.get(id(X))
+            if g is None:
+                if first is not None and X.shape == first[0].shape and np.array_equal(X, first[0]):
+                    g = first[1]
+                else:
+                    g = _grid_params(X) or False
+                seen[id(X)] = g
+                if first is None:
+                    first = (X, g)
+            if g is False or (gp is not None and g != gp):
+                return L.PIX_KF, None
+            gp = g
+        if gp is None:
+            return L.PIX_KF, None
+        return L.PIX_GRID, gp
+
+    def pinned_tensors(self):
+        """(tgt, w, disp) page-locked torch views, or None when built unpinned."""
+        if self._tgt_t is None:
+            return None
+        return self._tgt_t, self._w_t, self._disp_t
 
 
-_TERM = {0: "max_iterations", 1: "converged", 2: "no_decrease_at_max_damping",
-         3: "singular: singular reduced pose system"}
+_TERM = {0: "max_iterations", 1: "converged", 2: "no_decrease_at_max_damping"}
 
 
 class DeviceProblem:
@@ -173,18 +428,53 @@ class DeviceProblem:
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         dev = self.device
 
-        def t(a, dt):
-            return torch.from_numpy(np.ascontiguousarray(a)).to(dev, dtype=dt, non_blocking=False)
-
-        self.d_state = t(H.state, torch.float64)
-        self.d_ts = t(H.ts, torch.float64)
-        self.d_disp = t(H.disp, torch.float32)
-        self.d_tgt = t(H.tgt.reshape(-1), torch.float32)
-        self.d_w = t(H.w.reshape(-1), torch.float32)
-        self.d_pix = t(H.pix.reshape(-1), torch.float32) if H.pix is not None else None
-        self.d_imu = t(H.imu.reshape(-1), torch.float64)
-        self.d_grav = t(H.grav, torch.float64)
+        with torch.cuda.stream(self.stream):
+            self.d_state = torch.empty((H.K, 16), dtype=torch.float64, device=dev)
+            self.d_ts = torch.empty(H.K, dtype=torch.float64, device=dev)
+            self.d_disp = torch.empty(H.n_disp_pad, dtype=torch.float32, device=dev)
+            self.d_tgt = torch.empty(2 * H.n_rows_pad, dtype=torch.float32, device=dev)
+            self.d_w = torch.empty(2 * H.n_rows_pad, dtype=torch.float32, device=dev)
+            self.d_pix = (torch.empty(H.pix.size, dtype=torch.float32, device=dev) if H.pix is not None else None)
+            self.d_imu = torch.empty(H.F * L.IMU_REC, dtype=torch.float64, device=dev)
+            self.d_grav = torch.empty(5, dtype=torch.float64, device=dev)
+        self._upload(H)
         self._create()
+
+    def _upload(self, H):
+        """Host layout -> this problem's device arrays, on the solve stream.  The bulk arrays
+        (flow, weights, disparities) go as asynchronous DMAs from page-locked buffers when the
+        layout was built pinned; weight signs are then checked on the device (ValueError, as
+        residuals.py:112-113)."""
+        pin = H.pinned_tensors()
+        with torch.cuda.stream(self.stream):
+            def put(dst, a, pinned=None):
+                if dst is None or dst.numel() == 0:
+                    return
+                if pinned is not None:
+                    dst.copy_(pinned.reshape(-1), non_blocking=True)
+                else:
+                    dst.copy_(torch.from_numpy(np.ascontiguousarray(a).reshape(-1)).to(dst.dtype), non_blocking=False)
+            put(self.d_state.view(-1), H.state)
+            put(self.d_ts, H.ts)
+            put(self.d_disp, H.disp, pin[2] if pin else None)
+            put(self.d_tgt, H.tgt, pin[0] if pin else None)
+            put(self.d_w, H.w, pin[1] if pin else None)
+            put(self.d_pix, H.pix)
+            put(self.d_imu, H.imu)
+            put(self.d_grav, H.grav)
+            if not H.weights_checked and self.d_w.numel() and bool((self.d_w < 0).any()):
+                raise ValueError("weights must be non-negative")
+
+    def rebind(self, H):
+        """Solve another window of the same topology in this context (no re-planning):
+        upload its arrays, re-derive the IMU whitening factors, reset the LM state."""
+        self.H = H
+        self._upload(H)
+        rc = self.lib.vba_bind_inputs(self.ctx, self._sptr(), self.d_tgt.data_ptr(), self.d_w.data_ptr(), 1)
+        if rc == L.VBA_E_COV:
+            raise ValueError("non-PSD preintegration covariance")
+        L.check(rc)
+        self.load_state()
 
     def _create(self):
         H = self.H
@@ -291,7 +581,8 @@ class DeviceProblem:
         """_solve_step (solver.py:265-308): returns (dx_full, dx_d) numpy fp64."""
         rc = self.lib.vba_solve_step(self.ctx, self._sptr(), float(lam), int(bool(use_schur)))
         if rc == L.VBA_E_NOT_SPD:
-            raise RuntimeError("singular reduced pose system")
+            dense = not use_schur and self.n_disp > 0
+            raise RuntimeError("singular full system" if dense else "singular reduced pose system")
         L.check(rc)
         dx = torch.empty(self.npv, dtype=torch.float64, device=self.device)
         dxd = torch.empty(max(self.n_disp, 1), dtype=torch.float64, device=self.device)
@@ -306,6 +597,15 @@ class DeviceProblem:
     def accept(self):
         L.check(self.lib.vba_accept(self.ctx, self._sptr()))
 
+    def _singular_msg(self):
+        """The reference's RuntimeError text for a singular step (solver.py:287-289, 300-303):
+        the dense path is taken when use_schur is off and there are disparities."""
+        dense = not bool(self.opts.get("use_schur", True)) and self.n_disp > 0
+        return "singular full system" if dense else "singular reduced pose system"
+
+    def _term(self, code):
+        return _TERM[code] if code in _TERM else "singular: " + self._singular_msg()
+
     def solve(self):
         """Native LM loop (solver.py:344-411).  Returns a report dict."""
         cap = 4 * int(self._o.max_iterations) + 8
@@ -314,8 +614,8 @@ class DeviceProblem:
         L.check(self.lib.vba_solve(self.ctx, self._sptr(), C.byref(rep), traj, cap))
         return dict(iterations=rep.iterations, initial_cost=rep.initial_cost, final_cost=rep.final_cost,
                     cost_trajectory=[traj[i] for i in range(min(rep.n_costs, cap))],
-                    termination=_TERM[rep.termination],
-                    condition_warnings=["singular reduced pose system"] * rep.n_warnings,
+                    termination=self._term(rep.termination),
+                    condition_warnings=[self._singular_msg()] * rep.n_warnings,
                     trials=rep.trials)
 
     def solve_windows(self, windows, outputs=None, copy_stream=None):

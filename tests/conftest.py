@@ -52,6 +52,18 @@ def load_config_golden(cfg):
     return out
 
 
+def load_contract(name):
+    """tests/golden/contract/<name>.npz (make_contract_golden.py): packed inputs, meta, outputs."""
+    z = np.load(os.path.join(GOLDEN_DIR, "contract", name + ".npz"), allow_pickle=False)
+    P = {k[3:]: z[k] for k in z.files if k.startswith("in_")}
+    P["grav_G"] = float(P["grav_G"])
+    P["has_Tcb"] = bool(P["has_Tcb"])
+    out = {k: z[k] for k in z.files if not k.startswith("in_")}
+    meta = json.loads(str(out.pop("meta")))
+    meta["opts"]["frozen_keyframes"] = tuple(meta["opts"]["frozen_keyframes"])
+    return P, out, meta
+
+
 def config_golden_names():
     return sorted(int(os.path.basename(p)[4:-4]) for p in glob.glob(os.path.join(GOLDEN_DIR, "bcfg*.npz")))
 

@@ -26,7 +26,7 @@ stored sampled (conftest.golden_* helpers document the scheme):
   diagonal and sub-diagonal sdof×sdof block plus up to 1500 other non-zero
   lower blocks (their pose 6×6 part: everything else in them is exactly zero,
   asserted here), plus the product with a seeded vector;
-* the coupling H_pd: 256 seeded disparity columns per keyframe (cfg 0-2).
+* the coupling H_pd: 256 seeded disparity columns per keyframe (cfg 0-2; 4 of them at cfg 3).
 
 Run:  python tests/golden/make_config_golden.py 0 1 2 3 4
 """
@@ -207,6 +207,8 @@ def main(cfgs):
             rng = np.random.default_rng(31)
             cols = np.concatenate([np.sort(rng.choice(np.arange(doff[k], doff[k + 1]), 256, replace=False))
                                    for k in range(K)])
+            if K * 15 > GOLD_FULL_MAT:     # large windows: 4 of those columns per keyframe (size)
+                cols = cols.reshape(K, 256)[:, ::64].ravel()
             out["H_pd_cols"] = cols.astype(np.int64)
             out["H_pd"] = np.asarray(res["H_pd"][:, cols])
             out["H_pd_maxabs"] = np.array(np.abs(res["H_pd"]).max())

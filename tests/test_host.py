@@ -115,3 +115,55 @@ def test_bench_bounded_sample():
     assert epx >= 300_000 and M < len(P["kid"])
     assert np.all(Q["ei"] < M) and np.all(Q["ej"] < M)
     assert Q["eoff"][-1] == len(Q["tgt"]) == epx
+
+
+_LAYOUT_FIELDS = ("npix", "doff_pad", "edge_order", "eoff_pad", "tgt", "w", "dsrc", "disp", "ei", "ej", "fi", "fj",
+                  "imu", "state", "ts", "grav", "frozen", "intr", "Tcb")
+
+
+@pytest.mark.parametrize("name", ["win6_frozen2", "win4_tcb", "win5_gravity", "cfg0_grid12x16", "edge_pixels",
+                                  "workload1"])
+def test_graph_layout_equals_packed_layout(name):
+    """HostLayout.from_graph (native packer, csrc/vba_pack.cpp) is bitwise the packed-dict layout."""
+    if name == "workload1":
+        g = make_workload(1)
+        opts = {"frozen_keyframes": (0,)}
+    else:
+        P, _, opts = load_golden("win8_px30" if name == "edge_pixels" else name)
+        g = graph_from_packed(P)
+        if name == "edge_pixels":          # an edge whose pixels differ from its keyframe's: VBA_PIX_EDGE
+            e = g.vision_edges[3]
+            g.vision_edges[3] = T.VisionEdge(e.i, e.j, e.pixels + 0.5, e.targets, e.weights)
+    H1 = HostLayout(pack_graph(g), opts)
+    H2 = HostLayout.from_graph(g, opts, pinned=False)
+    for k in _LAYOUT_FIELDS:
+        assert np.array_equal(getattr(H1, k), getattr(H2, k)), k
+    assert H1.mode == H2.mode and H1.grid == H2.grid
+    assert (H1.pix is None) == (H2.pix is None) and (H1.pix is None or np.array_equal(H1.pix, H2.pix))
+    if name == "edge_pixels":
+        assert H2.mode == L.PIX_EDGE
+    if name == "workload1":
+        assert H2.mode == L.PIX_GRID
+
+
+def test_graph_layout_validation():
+    """from_graph raises the reference's ValueErrors (residuals.py:181-185, 112-113, 281-284)."""
+    P, _, opts = load_golden("win4_tcb")
+    g = graph_from_packed(P)
+    bad = copy.deepcopy(g)
+    e = bad.vision_edges[0]
+    bad.vision_edges[0] = T.VisionEdge(e.i, e.j, e.pixels[:-1], e.targets[:-1], e.weights[:-1])
+    with pytest.raises(ValueError):
+        HostLayout.from_graph(bad, opts, pinned=False)
+    bad = copy.deepcopy(g)
+    bad.vision_edges[1].weights = -bad.vision_edges[1].weights - 1.0      # mutated after construction
+    with pytest.raises(ValueError):
+        HostLayout.from_graph(bad, opts, pinned=False)
+    bad = copy.deepcopy(g)
+    bad.keyframes[1].state.timestamp += 0.5
+    with pytest.raises(ValueError):
+        HostLayout.from_graph(bad, opts, pinned=False)
+    bad = copy.deepcopy(g)
+    bad.keyframes[2].disparities = bad.keyframes[2].disparities * 0.0
+    with pytest.raises(ValueError):
+        HostLayout.from_graph(bad, opts, pinned=False)
