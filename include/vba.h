@@ -92,6 +92,12 @@ typedef struct vba_problem {
   const int32_t* h_imu_i;  /* [F] */
   const int32_t* h_imu_j;  /* [F] */
   const int32_t* h_frozen; /* [K] 1 = frozen (gauge) keyframe */
+  /* optional device array (may be NULL): fp64 master disparities [n_disp_pad].  The solver
+   * keeps the disparity state in fp64 and updates it as max(d + dx_d, 1e-4) in fp64
+   * (solver.py:336-338); the per-pixel kernels read its fp32 copy.  When given it seeds the
+   * state at create / vba_load_state (disp is then ignored) and vba_download writes it;
+   * when NULL the state is seeded from the fp32 disp. */
+  double* disp64;
 } vba_problem;
 
 typedef struct vba_options {       /* SolveOptions, solver.py:82-105 */

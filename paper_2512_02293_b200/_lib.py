@@ -38,6 +38,7 @@ class VbaProblem(C.Structure):
         ("tgt", C.c_void_p), ("wts", C.c_void_p), ("imu", C.c_void_p), ("grav", C.c_void_p),
         ("h_doff", C.c_void_p), ("h_npix", C.c_void_p), ("h_edge_i", C.c_void_p), ("h_edge_j", C.c_void_p),
         ("h_eoff", C.c_void_p), ("h_imu_i", C.c_void_p), ("h_imu_j", C.c_void_p), ("h_frozen", C.c_void_p),
+        ("disp64", C.c_void_p),
     ]
 
 

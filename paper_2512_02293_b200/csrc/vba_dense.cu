@@ -95,25 +95,46 @@ void launch_assemble_vec(const int32_t* sptr, const Vec* vs, int nseg, const int
 // dense (use_schur=False) path: disparity update from the full solution x[nf + real index]
 __global__ void k_dense_dxd(const double* __restrict__ x, int nf, const int64_t* __restrict__ doff,
                             const int64_t* __restrict__ roff, const int32_t* __restrict__ npix, int K,
-                            const float* __restrict__ dcur, float* __restrict__ dnxt, float* __restrict__ dxd,
-                            unsigned long long* __restrict__ step_bits) {
+                            const double* __restrict__ dcur, float* __restrict__ dnxt, double* __restrict__ dnxt64,
+                            double* __restrict__ dxd, unsigned long long* __restrict__ step_bits) {
   const int k = blockIdx.y;
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= K || n >= npix[k]) return;
   const double dx = x[nf + roff[k] + n];
   const int64_t p = doff[k] + n;
-  dnxt[p] = fmaxf((float)((double)dcur[p] + dx), 1e-4f);
-  dxd[p] = (float)dx;
+  const double v = fmax(dcur[p] + dx, kDispFloor64);   // solver.py:336-338, fp64 master
+  dnxt64[p] = v;
+  dnxt[p] = (float)v;
+  dxd[p] = dx;
   const double m = fabs(dx);
   if (m > 0.0) atomicMax(step_bits, (unsigned long long)__double_as_longlong(m));
 }
 
 void launch_dense_dxd(const double* x, int nf, const int64_t* doff, const int64_t* roff, const int32_t* npix,
-                      int maxpix, int K, const float* dcur, float* dnxt, float* dxd, unsigned long long* step_bits,
-                      cudaStream_t st) {
+                      int maxpix, int K, const DevState& cur, const DevState& nxt, double* dxd,
+                      unsigned long long* step_bits, cudaStream_t st) {
   if (K <= 0 || maxpix <= 0) return;
   dim3 g((maxpix + 255) / 256, K);
-  k_dense_dxd<<<g, 256, 0, st>>>(x, nf, doff, roff, npix, K, dcur, dnxt, dxd, step_bits);
+  k_dense_dxd<<<g, 256, 0, st>>>(x, nf, doff, roff, npix, K, cur.disp64, nxt.disp, nxt.disp64, dxd, step_bits);
+  launch_count();
+}
+
+__global__ void k_widen(const float* __restrict__ a, double* __restrict__ b, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = (double)a[i];
+}
+__global__ void k_narrow(const double* __restrict__ a, float* __restrict__ b, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = (float)a[i];
+}
+void launch_widen(const float* src, double* dst, int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  k_widen<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, dst, n);
+  launch_count();
+}
+void launch_narrow(const double* src, float* dst, int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  k_narrow<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, dst, n);
   launch_count();
 }
 

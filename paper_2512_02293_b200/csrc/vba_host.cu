@@ -103,7 +103,8 @@ struct Ctx {
   int32_t *d_gsrc = nullptr, *d_g0 = nullptr, *d_g1 = nullptr, *d_gorder = nullptr, *d_gsrc_lpt = nullptr;
   int64_t *d_goff = nullptr, *d_foff = nullptr;
   double *d_part = nullptr, *d_tile_e = nullptr, *d_arena = nullptr, *d_gram_part = nullptr, *d_gram = nullptr;
-  float *d_Hdd = nullptr, *d_gd = nullptr, *d_ustep = nullptr, *d_dxd = nullptr;
+  float *d_Hdd = nullptr, *d_gd = nullptr, *d_ustep = nullptr;
+  double* d_dxd = nullptr;
   double *d_L = nullptr;
   int* d_imu_status = nullptr;
   // reduced system
@@ -662,6 +663,20 @@ static void prof_collect(Ctx* c, bool with_lin) {
   }
 }
 
+// seed a state buffer's disparities from the caller: the fp64 master from vba_problem.disp64
+// when given (its fp32 copy derived), else from the fp32 vba_problem.disp (widened)
+static int load_disparities(Ctx* c, DevState& s, cudaStream_t st) {
+  if (!c->n_disp) return 0;
+  if (c->P.disp64) {
+    if (cudaMemcpyAsync(s.disp64, c->P.disp64, sizeof(double) * c->n_disp, cudaMemcpyDeviceToDevice, st)) return 1;
+    launch_narrow(s.disp64, s.disp, c->n_disp, st);
+  } else {
+    if (cudaMemcpyAsync(s.disp, c->P.disp, sizeof(float) * c->n_disp, cudaMemcpyDeviceToDevice, st)) return 1;
+    launch_widen(s.disp, s.disp64, c->n_disp, st);
+  }
+  return cudaGetLastError() != cudaSuccess;
+}
+
 static int stage_energy(Ctx* c, DevState& s, cudaStream_t st) {
   launch_edge_prep(s, c->d_ei, c->d_ej, c->E, c->extr, st);
   launch_vision_energy(c->P.pixel_mode, c->d_chunks, c->d_soff, c->d_sids, c->d_sitems, c->d_ioff, c->ncta, s, c->pix, c->P.tgt, c->P.wts,
@@ -846,9 +861,12 @@ static int stage_step_dense(Ctx* c, double lam, cudaStream_t st) {
                   c->d_dtasks, c->n_dtasks, &c->d_res->status, st);
   mark(c, 4, st);
   launch_scatter_dx(c->d_dx2, c->d_fmap, c->npv, c->d_dx, st);
-  if (c->n_disp) VBA_CUDA(cudaMemcpyAsync(n.disp, s.disp, sizeof(float) * c->n_disp, cudaMemcpyDeviceToDevice, st));
-  launch_dense_dxd(c->d_dx2, c->nfree, c->d_doff, c->d_roff_real, c->d_npix, c->maxpix, c->K, s.disp, n.disp,
-                   c->d_dxd, &c->d_res->step_bits, st);
+  if (c->n_disp) {   // padding slots keep their values; real pixels are rewritten below
+    VBA_CUDA(cudaMemcpyAsync(n.disp, s.disp, sizeof(float) * c->n_disp, cudaMemcpyDeviceToDevice, st));
+    VBA_CUDA(cudaMemcpyAsync(n.disp64, s.disp64, sizeof(double) * c->n_disp, cudaMemcpyDeviceToDevice, st));
+  }
+  launch_dense_dxd(c->d_dx2, c->nfree, c->d_doff, c->d_roff_real, c->d_npix, c->maxpix, c->K, s, n, c->d_dxd,
+                   &c->d_res->step_bits, st);
   launch_retract(s, n, c->d_dx, c->d_frozen, c->K, c->sdof, c->ngrav, c->n_state, &c->d_res->step_bits, c->npv, st);
   c->have_step = true;
   c->last_lam = lam;
@@ -1006,13 +1024,14 @@ int vba_create(void** out, const vba_problem* prob, const vba_options* opts, voi
   for (int b = 0; b < 2; ++b) {
     DevState& s = c->S[b];
     if ((rc = dalloc(c, &s.state, (size_t)16 * c->K)) || (rc = dalloc(c, &s.disp, (size_t)c->n_disp)) ||
+        (rc = dalloc(c, &s.disp64, (size_t)c->n_disp)) ||
         (rc = dalloc(c, &s.grav, 5)) || (rc = dalloc(c, &s.geo32, (size_t)c->E)) ||
         (rc = dalloc(c, &s.geo64, (size_t)kGeo64 * c->E)))
       return fail(rc);
   }
   if (cudaMemcpyAsync(c->S[0].state, prob->state, sizeof(double) * 16 * c->K, cudaMemcpyDeviceToDevice, st) ||
-      (c->n_disp && cudaMemcpyAsync(c->S[0].disp, prob->disp, sizeof(float) * c->n_disp, cudaMemcpyDeviceToDevice, st)) ||
-      cudaMemcpyAsync(c->S[0].grav, prob->grav, sizeof(double) * 5, cudaMemcpyDeviceToDevice, st)) {
+      cudaMemcpyAsync(c->S[0].grav, prob->grav, sizeof(double) * 5, cudaMemcpyDeviceToDevice, st) ||
+      load_disparities(c, c->S[0], st)) {
     set_err("state upload failed");
     return fail(VBA_E_CUDA);
   }
@@ -1370,7 +1389,11 @@ int vba_download(void* ctx, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   DevState& s = CUR(c);
   VBA_CUDA(cudaMemcpyAsync(c->P.state, s.state, sizeof(double) * 16 * c->K, cudaMemcpyDeviceToDevice, st));
-  if (c->n_disp) VBA_CUDA(cudaMemcpyAsync(c->P.disp, s.disp, sizeof(float) * c->n_disp, cudaMemcpyDeviceToDevice, st));
+  if (c->n_disp) {
+    VBA_CUDA(cudaMemcpyAsync(c->P.disp, s.disp, sizeof(float) * c->n_disp, cudaMemcpyDeviceToDevice, st));
+    if (c->P.disp64)
+      VBA_CUDA(cudaMemcpyAsync(c->P.disp64, s.disp64, sizeof(double) * c->n_disp, cudaMemcpyDeviceToDevice, st));
+  }
   VBA_CUDA(cudaMemcpyAsync(c->P.grav, s.grav, sizeof(double) * 5, cudaMemcpyDeviceToDevice, st));
   return VBA_OK;
 }
@@ -1476,7 +1499,7 @@ int vba_load_state(void* ctx, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   DevState& s = CUR(c);
   VBA_CUDA(cudaMemcpyAsync(s.state, c->P.state, sizeof(double) * 16 * c->K, cudaMemcpyDeviceToDevice, st));
-  if (c->n_disp) VBA_CUDA(cudaMemcpyAsync(s.disp, c->P.disp, sizeof(float) * c->n_disp, cudaMemcpyDeviceToDevice, st));
+  if (load_disparities(c, s, st)) { set_err("load_state: %s", cudaGetErrorString(cudaGetLastError())); return VBA_E_CUDA; }
   VBA_CUDA(cudaMemcpyAsync(s.grav, c->P.grav, sizeof(double) * 5, cudaMemcpyDeviceToDevice, st));
   c->have_step = false;
   return VBA_OK;

@@ -19,6 +19,7 @@ namespace vba {
 constexpr int kTilePx = 2 * VBA_TP * 128;   // pixels per per-pixel work tile (128-thread CTAs)
 constexpr double kSmallAngle = 1e-8;
 constexpr float kDispFloor = 1e-4f;      // solver.py:32
+constexpr double kDispFloor64 = 1e-4;    // solver.py:32 (the fp64 master update)
 constexpr int kPartWarps = 4;            // warps of the K1 CTA, one fp32 32-vector each
 constexpr int kPartStride = 32 * kPartWarps;   // floats per K1 (tile, edge) partial record
 constexpr int kVisBlock = 120;           // doubles per edge pose-space block record
@@ -254,7 +255,8 @@ namespace vba {
 
 struct DevState {      // one side of the double-buffered solver state
   double* state;       // [K,16]
-  float* disp;         // [n_disp_pad]
+  float* disp;         // [n_disp_pad] fp32 copy read by the per-pixel kernels
+  double* disp64;      // [n_disp_pad] master disparities: updated in fp64 (solver.py:336-338)
   double* grav;        // [5]
   EdgeGeo32* geo32;    // [E]
   double* geo64;       // [E, kGeo64]
@@ -298,7 +300,7 @@ size_t gram_smem_bytes(int kmax, int nsplit, int npairs, int k);
 void launch_backsub(int pixel_mode, const PixTile* tiles, int ntiles, const DevState& cur, const DevState& nxt,
                     const float* pix, const float* wts, const int64_t* eoff, const int64_t* doff, int grid_w,
                     const double* grid, const double* intr, const float* Hdd, const float* gd,
-                    const float* ustep, double lam, double ridge, float* dxd_out,
+                    const float* ustep, double lam, double ridge, double* dxd_out,
                     unsigned long long* step_max_bits, cudaStream_t st);
 void launch_retract(const DevState& cur, const DevState& nxt, const double* dx_full, const int32_t* frozen,
                     int K, int sdof, int ngrav, int n_state, unsigned long long* step_max_bits,
@@ -361,10 +363,15 @@ void launch_export_hpd(int mode, const int32_t* seb, const int32_t* see, const i
                        const float* pix, const float* wts, const int64_t* eoff, int grid_w, const double* grid,
                        const double* intr, const HpdOut& out, cudaStream_t st);
 void launch_dense_dxd(const double* x, int nf, const int64_t* doff, const int64_t* roff, const int32_t* npix,
-                      int maxpix, int K, const float* dcur, float* dnxt, float* dxd, unsigned long long* step_bits,
-                      cudaStream_t st);
+                      int maxpix, int K, const DevState& cur, const DevState& nxt, double* dxd,
+                      unsigned long long* step_bits, cudaStream_t st);
 void launch_unpad(const float* src, const int64_t* doff, const int64_t* roff, const int32_t* npix, int maxpix, int K,
                   double* dst, cudaStream_t st);
+void launch_unpad(const double* src, const int64_t* doff, const int64_t* roff, const int32_t* npix, int maxpix, int K,
+                  double* dst, cudaStream_t st);
+// fp32 <-> fp64 disparity copies (master state <-> kernel copy / caller arrays)
+void launch_widen(const float* src, double* dst, int64_t n, cudaStream_t st);
+void launch_narrow(const double* src, float* dst, int64_t n, cudaStream_t st);
 // The tensor-core reduced solve stops refining once a pass corrects x by <= kTcRefineTol
 // max|x| AND the geometric-tail bound of the remaining error, rel * rho / (1 - rho) with the
 // measured per-pass contraction rho, is <= kTcErrTol (k_tc_check); with the factor's usual

@@ -1284,7 +1284,8 @@ __global__ void __launch_bounds__(kPixBlock) k_backsub(
     const float* __restrict__ pix, const float* __restrict__ wts, const int64_t* __restrict__ eoff,
     const int64_t* __restrict__ doff, int grid_w, GridP gp, IntrP in, const float* __restrict__ Hdd,
     const float* __restrict__ gd, const float* __restrict__ ustep, double lam, double ridge,
-    float* __restrict__ disp_out, float* __restrict__ dxd_out, unsigned long long* __restrict__ step_bits) {
+    const double* __restrict__ disp64, float* __restrict__ disp_out, double* __restrict__ disp64_out,
+    double* __restrict__ dxd_out, unsigned long long* __restrict__ step_bits) {
   const PixTile T = tiles[blockIdx.x];
   const int tid = threadIdx.x;
   const int64_t kbase = doff[T.src];
@@ -1367,10 +1368,12 @@ __global__ void __launch_bounds__(kPixBlock) k_backsub(
     const float2 g2 = *reinterpret_cast<const float2*>(gd + n);
     const double dx0 = (-(double)g2.x - (double)acc[2 * m]) / ((double)h2.x * damp + ridge);
     const double dx1 = (-(double)g2.y - (double)acc[2 * m + 1]) / ((double)h2.y * damp + ridge);
-    const float n0v = fmaxf((float)((double)dd[2 * m] + dx0), kDispFloor);
-    const float n1v = fmaxf((float)((double)dd[2 * m + 1] + dx1), kDispFloor);
-    *reinterpret_cast<float2*>(disp_out + n) = make_float2(n0v, n1v);
-    if (dxd_out) *reinterpret_cast<float2*>(dxd_out + n) = make_float2((float)dx0, (float)dx1);
+    // fp64 master update d' = max(d + dx_d, 1e-4) (solver.py:336-338); the kernels read its fp32 copy
+    const double2 d64 = *reinterpret_cast<const double2*>(disp64 + n);
+    const double n0v = fmax(d64.x + dx0, kDispFloor64), n1v = fmax(d64.y + dx1, kDispFloor64);
+    *reinterpret_cast<double2*>(disp64_out + n) = make_double2(n0v, n1v);
+    *reinterpret_cast<float2*>(disp_out + n) = make_float2((float)n0v, (float)n1v);
+    if (dxd_out) *reinterpret_cast<double2*>(dxd_out + n) = make_double2(dx0, dx1);
     mx = fmax(mx, fmax(fabs(dx0), fabs(dx1)));
   }
 #pragma unroll
@@ -1382,21 +1385,21 @@ __global__ void __launch_bounds__(kPixBlock) k_backsub(
 void launch_backsub(int mode, const PixTile* tiles, int ntiles, const DevState& cur, const DevState& nxt,
                     const float* pix, const float* wts, const int64_t* eoff, const int64_t* doff, int grid_w,
                     const double* grid, const double* intr, const float* Hdd, const float* gd, const float* ustep,
-                    double lam, double ridge, float* dxd_out, unsigned long long* step_bits, cudaStream_t st) {
+                    double lam, double ridge, double* dxd_out, unsigned long long* step_bits, cudaStream_t st) {
   if (ntiles <= 0) return;
   GridP gp{grid[0], grid[1], grid[2], grid[3]};
   IntrP in{intr[0], intr[1], intr[2], intr[3]};
   if (mode == VBA_PIX_GRID)
     k_backsub<VBA_PIX_GRID><<<ntiles, kPixBlock, 0, st>>>(tiles, cur.disp, cur.geo32, pix, wts, eoff, doff, grid_w,
-                                                          gp, in, Hdd, gd, ustep, lam, ridge, nxt.disp, dxd_out,
+                                                          gp, in, Hdd, gd, ustep, lam, ridge, cur.disp64, nxt.disp, nxt.disp64, dxd_out,
                                                           step_bits);
   else if (mode == VBA_PIX_KF)
     k_backsub<VBA_PIX_KF><<<ntiles, kPixBlock, 0, st>>>(tiles, cur.disp, cur.geo32, pix, wts, eoff, doff, grid_w,
-                                                        gp, in, Hdd, gd, ustep, lam, ridge, nxt.disp, dxd_out,
+                                                        gp, in, Hdd, gd, ustep, lam, ridge, cur.disp64, nxt.disp, nxt.disp64, dxd_out,
                                                         step_bits);
   else
     k_backsub<VBA_PIX_EDGE><<<ntiles, kPixBlock, 0, st>>>(tiles, cur.disp, cur.geo32, pix, wts, eoff, doff, grid_w,
-                                                          gp, in, Hdd, gd, ustep, lam, ridge, nxt.disp, dxd_out,
+                                                          gp, in, Hdd, gd, ustep, lam, ridge, cur.disp64, nxt.disp, nxt.disp64, dxd_out,
                                                           step_bits);
   launch_count();
 }
@@ -1558,8 +1561,9 @@ void launch_export_hpd(int mode, const int32_t* seb, const int32_t* see, const i
   launch_count();
 }
 
-// padded per-keyframe fp32 array -> reference-order fp64 array
-__global__ void k_unpad(const float* __restrict__ src, const int64_t* __restrict__ doff,
+// padded per-keyframe fp32 / fp64 array -> reference-order fp64 array
+template <class T>
+__global__ void k_unpad(const T* __restrict__ src, const int64_t* __restrict__ doff,
                         const int64_t* __restrict__ roff, const int32_t* __restrict__ npix, int K,
                         double* __restrict__ dst) {
   const int k = blockIdx.y;
@@ -1572,7 +1576,15 @@ void launch_unpad(const float* src, const int64_t* doff, const int64_t* roff, co
                   double* dst, cudaStream_t st) {
   if (K <= 0 || maxpix <= 0) return;
   dim3 grd((maxpix + 255) / 256, K);
-  k_unpad<<<grd, 256, 0, st>>>(src, doff, roff, npix, K, dst);
+  k_unpad<float><<<grd, 256, 0, st>>>(src, doff, roff, npix, K, dst);
+  launch_count();
+}
+
+void launch_unpad(const double* src, const int64_t* doff, const int64_t* roff, const int32_t* npix, int maxpix,
+                  int K, double* dst, cudaStream_t st) {
+  if (K <= 0 || maxpix <= 0) return;
+  dim3 grd((maxpix + 255) / 256, K);
+  k_unpad<double><<<grd, 256, 0, st>>>(src, doff, roff, npix, K, dst);
   launch_count();
 }
 

@@ -10,7 +10,9 @@ the device layout of include/vba.h:
   padding pixels carry weight 0 and disparity 1 and never reach the caller;
 * pixel coordinates implicit (regular grid, exact) when every keyframe and
   edge uses the same grid, else explicit per keyframe, else per edge;
-* flow targets, weights, disparities in fp32; states, IMU factors, gravity fp64.
+* flow targets, weights in fp32; disparities as an fp64 master copy (the solver state,
+  updated in fp64 like solver.py:336-338) plus its fp32 rounding (what the per-pixel
+  kernels read); states, IMU factors, gravity fp64.
 
 PyTorch provides device memory and the CUDA stream only.
 """
@@ -298,11 +300,12 @@ class HostLayout:
         dsrc = np.full(n_disp_pad, -1, np.int64)
         dsrc[pos] = np.arange(n_real)
         self.dsrc = dsrc
-        self.disp, self._disp_t = _host_buffer(n_disp_pad, np.float32, pinned)
-        self.disp.fill(1.0)
+        self.disp64, self._disp_t = _host_buffer(n_disp_pad, np.float64, pinned)
+        self.disp64.fill(1.0)
         for k in range(K):
             if npix[k]:
-                self.disp[self.doff_pad[k]:self.doff_pad[k] + npix[k]] = S.kdisp[k]
+                self.disp64[self.doff_pad[k]:self.doff_pad[k] + npix[k]] = S.kdisp[k]
+        self.disp = self.disp64.astype(np.float32)
         self.mode, self.grid = self._pixel_mode(kpix, self._edge_mismatch)
         if self.mode == L.PIX_KF:
             self.pix = np.zeros((n_disp_pad, 2), np.float32)
@@ -406,7 +409,7 @@ class HostLayout:
         return L.PIX_GRID, gp
 
     def pinned_tensors(self):
-        """(tgt, w, disp) page-locked torch views, or None when built unpinned."""
+        """(tgt, w, disp64) page-locked torch views, or None when built unpinned."""
         if self._tgt_t is None:
             return None
         return self._tgt_t, self._w_t, self._disp_t
@@ -432,6 +435,7 @@ class DeviceProblem:
             self.d_state = torch.empty((H.K, 16), dtype=torch.float64, device=dev)
             self.d_ts = torch.empty(H.K, dtype=torch.float64, device=dev)
             self.d_disp = torch.empty(H.n_disp_pad, dtype=torch.float32, device=dev)
+            self.d_disp64 = torch.empty(H.n_disp_pad, dtype=torch.float64, device=dev)
             self.d_tgt = torch.empty(2 * H.n_rows_pad, dtype=torch.float32, device=dev)
             self.d_w = torch.empty(2 * H.n_rows_pad, dtype=torch.float32, device=dev)
             self.d_pix = (torch.empty(H.pix.size, dtype=torch.float32, device=dev) if H.pix is not None else None)
@@ -456,7 +460,8 @@ class DeviceProblem:
                     dst.copy_(torch.from_numpy(np.ascontiguousarray(a).reshape(-1)).to(dst.dtype), non_blocking=False)
             put(self.d_state.view(-1), H.state)
             put(self.d_ts, H.ts)
-            put(self.d_disp, H.disp, pin[2] if pin else None)
+            put(self.d_disp64, H.disp64, pin[2] if pin else None)
+            put(self.d_disp, H.disp)
             put(self.d_tgt, H.tgt, pin[0] if pin else None)
             put(self.d_w, H.w, pin[1] if pin else None)
             put(self.d_pix, H.pix)
@@ -495,6 +500,7 @@ class DeviceProblem:
         p.state = self.d_state.data_ptr()
         p.ts = self.d_ts.data_ptr()
         p.disp = self.d_disp.data_ptr()
+        p.disp64 = self.d_disp64.data_ptr()
         p.pix = self.d_pix.data_ptr() if self.d_pix is not None else None
         p.tgt = self.d_tgt.data_ptr()
         p.wts = self.d_w.data_ptr()
@@ -661,6 +667,7 @@ class DeviceProblem:
             with torch.cuda.stream(st):
                 self.d_state.copy_(win["state"].reshape(self.d_state.shape), non_blocking=True)
                 self.d_disp.copy_(win["disp"].reshape(self.d_disp.shape), non_blocking=True)
+                self.d_disp64.copy_(self.d_disp)        # fp32 window disparities seed the fp64 master
                 self.d_imu.copy_(win["imu"].reshape(-1), non_blocking=True)
                 self.d_grav.copy_(win["grav"].reshape(-1), non_blocking=True)
             rc = self.lib.vba_bind_inputs(self.ctx, self._sptr(), sets[b][0].data_ptr(), sets[b][1].data_ptr(), 1)
@@ -685,7 +692,7 @@ class DeviceProblem:
         L.check(self.lib.vba_download(self.ctx, self._sptr()))
         self.stream.synchronize()
         s = self.d_state.cpu().numpy()
-        d = self.d_disp.cpu().numpy().astype(np.float64)
+        d = self.d_disp64.cpu().numpy()
         g = self.d_grav.cpu().numpy()
         disp = d[self.H.dsrc >= 0]
         return dict(q=s[:, 0:4], p=s[:, 4:7], v=s[:, 7:10], bg=s[:, 10:13], ba=s[:, 13:16], disp=disp,
@@ -723,6 +730,7 @@ class DeviceProblem:
         """Re-upload the per-step inputs (host -> device copies of flow, weights,
         disparities, states, IMU records, gravity) from the host layout."""
         H = H or self.H
-        for dst, src in ((self.d_state, H.state), (self.d_disp, H.disp), (self.d_tgt, H.tgt.reshape(-1)),
+        for dst, src in ((self.d_state, H.state), (self.d_disp, H.disp), (self.d_disp64, H.disp64),
+                         (self.d_tgt, H.tgt.reshape(-1)),
                          (self.d_w, H.w.reshape(-1)), (self.d_imu, H.imu.reshape(-1)), (self.d_grav, H.grav)):
             dst.copy_(torch.from_numpy(np.ascontiguousarray(src)), non_blocking=True)

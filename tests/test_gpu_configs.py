@@ -94,7 +94,7 @@ def _dp(P, opts):
     return DeviceProblem(P, opts)
 
 
-@pytest.mark.parametrize("cfg", CFGS)
+@pytest.mark.parametrize("cfg", CFGS, ids=lambda c: f"cfg{c}")
 def test_energy(cfg, cuda_ok):
     P, G = problem(cfg)
     dp = _dp(P, opts_of(G))
@@ -105,7 +105,7 @@ def test_energy(cfg, cuda_ok):
     assert abs(e - ref) <= TOL_COST * ref
 
 
-@pytest.mark.parametrize("cfg", CFGS)
+@pytest.mark.parametrize("cfg", CFGS, ids=lambda c: f"cfg{c}")
 def test_linearize(cfg, cuda_ok):
     P, G = problem(cfg)
     opts = opts_of(G)
@@ -146,7 +146,7 @@ def test_linearize(cfg, cuda_ok):
         assert v < TOL_H, (k, v)
 
 
-@pytest.mark.parametrize("cfg", CFGS)
+@pytest.mark.parametrize("cfg", CFGS, ids=lambda c: f"cfg{c}")
 def test_reduced_system(cfg, cuda_ok):
     P, G = problem(cfg)
     opts = opts_of(G)
@@ -162,7 +162,7 @@ def test_reduced_system(cfg, cuda_ok):
     assert st["fallbacks"] == 0
 
 
-@pytest.mark.parametrize("cfg", CFGS)
+@pytest.mark.parametrize("cfg", CFGS, ids=lambda c: f"cfg{c}")
 def test_step(cfg, cuda_ok):
     P, G = problem(cfg)
     opts = opts_of(G)
@@ -178,7 +178,7 @@ def test_step(cfg, cuda_ok):
     assert st["fallbacks"] == 0
 
 
-@pytest.mark.parametrize("cfg", CFGS)
+@pytest.mark.parametrize("cfg", CFGS, ids=lambda c: f"cfg{c}")
 def test_solve(cfg, cuda_ok):
     P, G = problem(cfg)
     opts = opts_of(G)

@@ -12,11 +12,14 @@ SolveReport out, graph written back in place):
   windows (configs 0 and 1, goldens by the reference) and the small goldens.
 
 Those contract windows are noise-free: the reference drives their energy to the
-fp64 floor (1e-8 ... 1e-21).  The GPU evaluates residuals in fp32 (north_star), so
-its attainable energy floor on them is set by fp32 rounding of the per-pixel
-residual; costs are compared with the reference's while they are above
-``FP32_FLOOR`` x the initial cost (printed), and the contract properties are
-asserted as the reference states them.
+fp64 floor (1e-8 ... 1e-21).  The GPU evaluates per-pixel residuals in fp32
+(north_star), which resolves a residual to ~1e-7 of the flow, so near the optimum
+its energies and steps follow the reference only down to an absolute floor:
+costs are compared entrywise to 1e-6 relative plus ``FP32_FLOOR`` x the initial
+cost (measured worst case on these windows: 2e-10 x), and iteration counts /
+terminations are compared only on the noisy BASELINE windows, where the costs stay
+far above that floor.  The contract properties themselves are asserted as the
+reference states them.
 """
 import copy
 
@@ -44,15 +47,15 @@ def _opts(meta, **kw):
 
 
 def _costs_agree(rep, ref):
+    """Accepted costs agree entrywise to 1e-6 relative plus an absolute fp32 floor of
+    FP32_FLOOR x the initial cost; returns how many entries were compared."""
     c, cr = list(rep.cost_trajectory), list(ref["cost_trajectory"])
-    floor = FP32_FLOOR * cr[0]
     print(f"  ours {['%.6e' % v for v in c]} {rep.iterations} it {rep.termination}\n"
           f"  ref  {['%.6e' % v for v in cr]} {ref['iterations']} it {ref['termination']}")
+    floor = FP32_FLOOR * cr[0]
     n = 0
     for a, b in zip(c, cr):
-        if b < floor:
-            break
-        assert abs(a - b) <= TOL_COST * b, (a, b)
+        assert abs(a - b) <= TOL_COST * b + floor, (a, b)
         n += 1
     return n
 
