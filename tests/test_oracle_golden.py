@@ -68,3 +68,27 @@ def test_solve_vi_ba_matches_reference(name):
     assert np.all(np.abs(c0 - c1) <= 1e-6 * np.maximum(c1, 1e-3))
     for k in ("p", "v", "disp"):
         assert np.abs(P[k] - out["final_" + k]).max() < 1e-8, k
+
+
+@pytest.mark.parametrize("cfg", [0, 1])
+def test_sparse_oracle_matches_reference_at_baseline_config(cfg):
+    """Pins the per-keyframe sparse restatement -- the oracle behind the config-4 golden, where
+    the reference cannot run -- to the reference's own outputs at BASELINE shapes (full 48x64
+    grids, out-degree 3 / 6): linearisation, Schur system, step (tests/golden/bcfg<cfg>.npz)."""
+    from conftest import load_config_golden, packed_hash
+    from oracle import vi_ba as V
+    from paper_2512_02293_b200.problem import pack_graph
+    from paper_2512_02293_b200.workloads import make_workload
+    G = load_config_golden(cfg)
+    P = pack_graph(make_workload(cfg))
+    assert packed_hash(P) == G["meta"]["input_hash"]
+    opts = dict(G["meta"]["opts"], frozen_keyframes=(0,))
+    L = oracle.Layout(P, opts)
+    H_pp, Hpd, H_dd, g_p, g_d = oracle.linearize_sparse(P, L)
+    assert rel(H_pp, G["H_pp"]) < 1e-12 and rel(g_p, G["g_p"]) < 1e-10
+    assert rel(H_dd, G["H_dd"]) < 1e-12 and rel(g_d, G["g_d"]) < 1e-10
+    H, g, _ = V.reduced_system_sparse(L, opts, H_pp, Hpd, H_dd, g_p, g_d, opts["damping"])
+    free = L.free_mask()
+    assert rel(H[np.ix_(free, free)], G["Hred"]) < 1e-12 and rel(g[free], G["gred"]) < 1e-10
+    dx, dxd = oracle.solve_step_sparse(L, opts, H_pp, Hpd, H_dd, g_p, g_d, opts["damping"])
+    assert rel(dx, G["dx"]) < 1e-8 and rel(dxd, G["dxd"]) < 1e-8
