@@ -98,6 +98,17 @@ typedef struct vba_problem {
    * state at create / vba_load_state (disp is then ignored) and vba_download writes it;
    * when NULL the state is seeded from the fp32 disp. */
   double* disp64;
+  /* edge sharding across ranks (one process per GPU).  shard_world <= 1:
+   * a single-GPU solve.  Otherwise every rank passes the FULL problem and the same keyframe
+   * bounds h_shard_kbounds[shard_world + 1] (host, read in vba_create): rank r owns the
+   * source keyframes [kb[r], kb[r+1]) -- their out-edges, pixel tiles, Schur fill-in and
+   * disparities -- and the IMU factors (i, j) with i in that range (factors must be sorted
+   * by i).  Ranks exchange their per-edge / per-factor / per-source blocks with the gather
+   * hook (vba_set_gather) and every rank assembles and solves the identical reduced system,
+   * so an N-rank solve is bitwise the 1-rank solve. */
+  int32_t shard_world;
+  int32_t shard_rank;
+  const int32_t* h_shard_kbounds;
 } vba_problem;
 
 typedef struct vba_options {       /* SolveOptions, solver.py:82-105 */
@@ -131,6 +142,10 @@ typedef struct vba_trial_result {
  * Supplied by the host (torch.distributed / NCCL); NULL for one GPU. */
 typedef int (*vba_allreduce_fn)(void* user, double* buf, int64_t count, int32_t op,
                                 void* stream);
+/* Gather hook of a sharded solve: rank r holds buf[offsets[r] .. offsets[r+1]) (doubles,
+ * device memory); on return every rank holds all of buf[offsets[0] .. offsets[world]).
+ * Stream-ordered on `stream`.  Returns 0 on success. */
+typedef int (*vba_allgather_fn)(void* user, double* buf, const int64_t* offsets, int32_t world, void* stream);
 
 VBA_API const char* vba_last_error(void);
 VBA_API int vba_version(void);
@@ -138,6 +153,7 @@ VBA_API int vba_version(void);
 VBA_API int vba_create(void** ctx, const vba_problem* prob, const vba_options* opts, void* stream);
 VBA_API int vba_destroy(void* ctx);
 VBA_API int vba_set_collective(void* ctx, vba_allreduce_fn fn, void* user);
+VBA_API int vba_set_gather(void* ctx, vba_allgather_fn fn, void* user);
 /* free-variable count of the reduced system (solver.py:254-257) */
 VBA_API int64_t vba_reduced_dim(void* ctx);
 

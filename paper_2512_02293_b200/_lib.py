@@ -17,7 +17,7 @@ PIX_GRID, PIX_KF, PIX_EDGE = 0, 1, 2
 IMU_REC = 180
 PREINT_REC = 281
 
-EXPORTED = ("vba_last_error", "vba_version", "vba_create", "vba_destroy", "vba_set_collective",
+EXPORTED = ("vba_last_error", "vba_version", "vba_create", "vba_destroy", "vba_set_collective", "vba_set_gather",
             "vba_reduced_dim", "vba_energy", "vba_linearize", "vba_export_normal_eq",
             "vba_solve_step", "vba_export_step", "vba_export_reduced", "vba_apply_step", "vba_restore", "vba_accept",
             "vba_trial", "vba_solve", "vba_download", "vba_launch_count", "vba_stage_times",
@@ -39,6 +39,7 @@ class VbaProblem(C.Structure):
         ("h_doff", C.c_void_p), ("h_npix", C.c_void_p), ("h_edge_i", C.c_void_p), ("h_edge_j", C.c_void_p),
         ("h_eoff", C.c_void_p), ("h_imu_i", C.c_void_p), ("h_imu_j", C.c_void_p), ("h_frozen", C.c_void_p),
         ("disp64", C.c_void_p),
+        ("shard_world", C.c_int32), ("shard_rank", C.c_int32), ("h_shard_kbounds", C.c_void_p),
     ]
 
 
@@ -65,6 +66,7 @@ class VbaTrialResult(C.Structure):
 
 
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.c_int32, C.c_void_p)
 
 
 class VbaError(RuntimeError):
@@ -92,6 +94,7 @@ def load(path: str | None = None):
         "vba_create": ([C.POINTER(C.c_void_p), C.POINTER(VbaProblem), C.POINTER(VbaOptions), v], C.c_int),
         "vba_destroy": ([v], C.c_int),
         "vba_set_collective": ([v, ALLREDUCE_FN, v], C.c_int),
+        "vba_set_gather": ([v, ALLGATHER_FN, v], C.c_int),
         "vba_reduced_dim": ([v], C.c_int64),
         "vba_energy": ([v, v, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)], C.c_int),
         "vba_linearize": ([v, v], C.c_int),

@@ -138,34 +138,6 @@ void launch_narrow(const double* src, float* dst, int64_t n, cudaStream_t st) {
   launch_count();
 }
 
-__global__ void k_add_ridge(double* H, int64_t ld, int n, double ridge) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) H[(int64_t)i * ld + i] += ridge;
-}
-void launch_add_ridge(double* H, int64_t ld, int n, double ridge, cudaStream_t st) {
-  if (n <= 0) return;
-  k_add_ridge<<<(n + 255) / 256, 256, 0, st>>>(H, ld, n, ridge);
-  launch_count();
-}
-
-// Lower triangle of the leading n x n block of a column-major matrix <-> a packed
-// buffer (column c at c n - c (c - 1) / 2, rows c .. n-1): the multi-GPU all-reduce
-// moves n (n + 1) / 2 doubles instead of npad^2.  One CTA per column, coalesced.
-__global__ void k_pack_lower(double* H, int64_t ld, int n, double* buf, int unpack) {
-  const int c = blockIdx.x;
-  const int64_t off = (int64_t)c * n - (int64_t)c * (c - 1) / 2;
-  double* col = H + (int64_t)c * ld;
-  for (int r = c + threadIdx.x; r < n; r += blockDim.x) {
-    if (unpack) col[r] = buf[off + (r - c)];
-    else buf[off + (r - c)] = col[r];
-  }
-}
-void launch_pack_lower(double* H, int64_t ld, int n, double* buf, int unpack, cudaStream_t st) {
-  if (n <= 0) return;
-  k_pack_lower<<<n, 256, 0, st>>>(H, ld, n, buf, unpack);
-  launch_count();
-}
-
 // full symmetric row-major copy of the lower triangle (column-major, leading dim ld) of
 // the n x n reduced system, and g = scale * rhs (export of H_red / g_red for parity tests)
 __global__ void k_export_sym(const double* __restrict__ H, int64_t ld, int n, double* __restrict__ out,

@@ -139,8 +139,16 @@ struct Ctx {
   Result* d_res = nullptr;
   Result* h_res = nullptr;
   vba_allreduce_fn coll = nullptr;
-  double* d_hpack = nullptr;   // packed lower triangle of H_red for the multi-GPU all-reduce
   void* coll_user = nullptr;
+  // edge sharding (vba_problem.shard_*): this rank owns source keyframes [own_k0, own_k1)
+  int world = 1, rank = 0, own_k0 = 0, own_k1 = 0;
+  std::vector<int32_t> kb;                          // [world+1] keyframe bounds
+  int oe0 = 0, oe1 = 0, of0 = 0, of1 = 0, ot0 = 0, ot1 = 0, oc0 = 0, oc1 = 0;   // owned edges/factors/tiles/chunks
+  std::vector<int64_t> g_vis, g_imu, g_fill, g_te, g_disp;   // [world+1] gather offsets (doubles)
+  std::vector<int32_t> gorder_own, gsrc_own;        // owned Gram tiles (launch order) / fill sources
+  int32_t *d_gorder_own = nullptr, *d_gsrc_own = nullptr;
+  vba_allgather_fn gat = nullptr;
+  void* gat_user = nullptr;
   bool have_step = false;
   double last_lam = 0.0;
   // reference (unpadded) disparity layout, built on first export
@@ -467,6 +475,11 @@ static int build_plans(Ctx* c, cudaStream_t st) {
       return w;
     };
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return work(a) > work(b); });
+    // a sharded rank streams only the chunks of its own source keyframes (the chunk list,
+    // and with it every partial's slot, is the global one on every rank)
+    order.erase(std::remove_if(order.begin(), order.end(),
+                               [&](int t) { return c->chunks[t].src < c->own_k0 || c->chunks[t].src >= c->own_k1; }),
+                order.end());
     c->ncta = std::min<int>(G, (int)order.size());
     std::vector<std::vector<int32_t>> bins(c->ncta);
     std::vector<std::pair<int64_t, int>> heap;
@@ -561,6 +574,10 @@ static int build_plans(Ctx* c, cudaStream_t st) {
   c->gram_part_len = gpo;
   c->gram_len = go;
   c->fill_len = fo;
+  for (int32_t t : c->gorder)
+    if (c->gtiles[t].src >= c->own_k0 && c->gtiles[t].src < c->own_k1) c->gorder_own.push_back(t);
+  for (int32_t n : c->gsrc_lpt)
+    if (n >= c->own_k0 && n < c->own_k1) c->gsrc_own.push_back(n);
   // --- arena layout
   const int s = c->sdof;
   c->ibs = ((3 * s * s + 6 * s + 7) + 7) / 8 * 8;
@@ -568,6 +585,46 @@ static int build_plans(Ctx* c, cudaStream_t st) {
   c->arena_imu = (int64_t)kVisBlock * E;
   c->arena_fill = c->arena_imu + (int64_t)c->ibs * c->F;
   c->arena_len = c->arena_fill + c->fill_len;
+  {  // sharding: owned ranges and the per-rank slices every gather moves
+    auto edge_at = [&](int n) { return n < K ? c->seb[n] : E; };
+    auto tile_at = [&](int n) { return n < K ? c->t0s[n] : (int)c->tiles.size(); };
+    std::vector<int32_t> chunk_at(K + 1, 0), fac_at(K + 1, 0);
+    std::vector<int64_t> fill_at(K + 1, 0);
+    {
+      size_t q = 0;
+      for (int n = 0; n <= K; ++n) {
+        while (q < c->chunks.size() && c->chunks[q].ee > c->chunks[q].eb && c->chunks[q].src < n) ++q;
+        chunk_at[n] = (int32_t)q;
+      }
+      int f = 0;
+      for (int n = 0; n <= K; ++n) {
+        while (f < c->F && P.h_imu_i[f] < n) ++f;
+        fac_at[n] = f;
+      }
+    }
+    // fill offsets per source are cumulative in source order (foff[n] for sources with a Gram)
+    {
+      int64_t acc = 0;
+      for (int n = 0; n < K; ++n) {
+        fill_at[n] = acc;
+        const int k = c->see[n] - c->seb[n];
+        if (k > 0 && P.h_npix[n] > 0) acc += (int64_t)(1 + k + k * (k + 1) / 2) * 36 + 6 * (1 + k);
+      }
+      fill_at[K] = acc;
+    }
+    c->oe0 = edge_at(c->own_k0); c->oe1 = edge_at(c->own_k1);
+    c->ot0 = tile_at(c->own_k0); c->ot1 = tile_at(c->own_k1);
+    c->oc0 = chunk_at[c->own_k0]; c->oc1 = chunk_at[c->own_k1];
+    c->of0 = fac_at[c->own_k0]; c->of1 = fac_at[c->own_k1];
+    for (int r = 0; r <= c->world; ++r) {
+      const int n = c->kb[r];
+      c->g_vis.push_back(c->arena_vis + (int64_t)kVisBlock * edge_at(n));
+      c->g_imu.push_back(c->arena_imu + (int64_t)c->ibs * fac_at[n]);
+      c->g_fill.push_back(c->arena_fill + fill_at[n]);
+      c->g_te.push_back((int64_t)kPartWarps * chunk_at[n]);
+      c->g_disp.push_back(P.h_doff[n]);
+    }
+  }
   // --- reduced-system layout (free keyframes, then gravity)
   std::vector<int> bidx(K, -1);
   std::vector<int32_t> roff, rdim;
@@ -663,6 +720,14 @@ static void prof_collect(Ctx* c, bool with_lin) {
   }
 }
 
+// sharded solve: every rank receives the other ranks' slices of buf (offsets per rank)
+static int gather(Ctx* c, double* buf, const std::vector<int64_t>& off, cudaStream_t st, const char* what) {
+  if (c->world <= 1) return VBA_OK;
+  if (!c->gat) { set_err("sharded solve without a gather hook (vba_set_gather)"); return VBA_E_INVALID; }
+  if (c->gat(c->gat_user, buf, off.data(), c->world, st)) { set_err("gather(%s) failed", what); return VBA_E_CUDA; }
+  return VBA_OK;
+}
+
 // seed a state buffer's disparities from the caller: the fp64 master from vba_problem.disp64
 // when given (its fp32 copy derived), else from the fp32 vba_problem.disp (widened)
 static int load_disparities(Ctx* c, DevState& s, cudaStream_t st) {
@@ -681,8 +746,12 @@ static int stage_energy(Ctx* c, DevState& s, cudaStream_t st) {
   launch_edge_prep(s, c->d_ei, c->d_ej, c->E, c->extr, st);
   launch_vision_energy(c->P.pixel_mode, c->d_chunks, c->d_soff, c->d_sids, c->d_sitems, c->d_ioff, c->ncta, s, c->pix, c->P.tgt, c->P.wts,
                        c->d_eoff, c->d_doff, c->P.grid_w, c->grid, c->intr, c->d_tile_e, st);
-  launch_imu_factor(c->P.imu, c->d_L, c->d_fi, c->d_fj, c->F, s, c->P.ts, c->sdof, c->ibs, 1,
+  launch_imu_factor(c->P.imu, c->d_L, c->d_fi, c->d_fj, c->of0, c->of1 - c->of0, s, c->P.ts, c->sdof, c->ibs, 1,
                     c->d_arena + c->arena_imu, st);
+  int rc;
+  if ((rc = gather(c, c->d_tile_e, c->g_te, st, "energy partials")) ||
+      (rc = gather(c, c->d_arena, c->g_imu, st, "IMU factors")))
+    return rc;
   const int oE = 3 * c->sdof * c->sdof + 6 * c->sdof + 6;
   launch_energy_reduce(c->d_tile_e, (int)c->chunks.size() * kPartWarps, c->d_arena + c->arena_imu, c->F, c->ibs, oE,
                        c->d_res->energy, st);
@@ -702,10 +771,14 @@ static int stage_linearize(Ctx* c, cudaStream_t st) {
   launch_vision_linearize(c->P.pixel_mode, c->d_chunks, c->d_soff, c->d_sids, c->d_sitems, c->d_ioff, c->ncta, s, c->pix, c->P.tgt, c->P.wts,
                           c->d_eoff, c->d_doff, c->P.grid_w, c->grid, c->intr, c->d_part, c->d_Hdd, c->d_gd, st);
   mark(c, 9, st);
-  launch_edge_finalize(c->d_t0s, c->d_t1s, c->d_tiles, c->d_ei, c->E, c->d_part, s, c->extr,
+  launch_edge_finalize(c->d_t0s, c->d_t1s, c->d_tiles, c->d_ei, c->oe0, c->oe1 - c->oe0, c->d_part, s, c->extr,
                        c->d_arena + c->arena_vis, nullptr, st);
-  launch_imu_factor(c->P.imu, c->d_L, c->d_fi, c->d_fj, c->F, s, c->P.ts, c->sdof, c->ibs, 0,
+  launch_imu_factor(c->P.imu, c->d_L, c->d_fi, c->d_fj, c->of0, c->of1 - c->of0, s, c->P.ts, c->sdof, c->ibs, 0,
                     c->d_arena + c->arena_imu, st);
+  int rc;
+  if ((rc = gather(c, c->d_arena, c->g_vis, st, "vision blocks")) ||
+      (rc = gather(c, c->d_arena, c->g_imu, st, "IMU blocks")))
+    return rc;
   mark(c, 1, st);
   return VBA_OK;
 }
@@ -717,34 +790,24 @@ static int stage_reduce(Ctx* c, double lam, cudaStream_t st) {
   DevState& s = CUR(c);
   mark(c, 2, st);
   VBA_CUDA(cudaMemsetAsync(c->d_res, 0, sizeof(Result), st));
-  if (!c->gtiles.empty()) {
-    launch_gram(c->P.pixel_mode, c->d_gtiles, (int)c->gtiles.size(), kGramBlock, c->gram_smem, c->kmax, s,
+  if (!c->gorder_own.empty()) {
+    launch_gram(c->P.pixel_mode, c->d_gtiles, (int)c->gorder_own.size(), kGramBlock, c->gram_smem, c->kmax, s,
                 c->pix, c->P.wts, c->d_eoff, c->d_doff, c->P.grid_w, c->grid, c->intr, c->d_Hdd, c->d_gd, lam,
-                c->O.ridge, c->d_gram_part, st, c->d_gorder);
-    launch_fill_transform(c->d_gsrc_lpt, (int)c->gsrc.size(), c->d_seb, c->d_see, c->d_g0, c->d_g1, c->d_gtiles,
-                          c->d_foff, c->d_gram_part, s, c->extr, c->d_arena + c->arena_fill, c->kmax, st);
+                c->O.ridge, c->d_gram_part, st, c->d_gorder_own);
+    launch_fill_transform(c->d_gsrc_own, (int)c->gsrc_own.size(), c->d_seb, c->d_see, c->d_g0, c->d_g1,
+                          c->d_gtiles, c->d_foff, c->d_gram_part, s, c->extr, c->d_arena + c->arena_fill, c->kmax,
+                          st);
   }
+  int rc = gather(c, c->d_arena, c->g_fill, st, "fill-in blocks");
+  if (rc) return rc;
   mark(c, 3, st);
   if (c->nfree > 0) {
-    const bool multi = c->coll != nullptr;
-    // single GPU: only the blocks with contributions are written (the others stay at the
-    // zeros of vba_create); ranks of a sharded solve rewrite every block (the in-place
-    // all-reduce leaves sums in their buffers).  Both solves read the lower triangle only.
+    // every rank now holds the whole arena: the identical assembly (blocks with contributions
+    // only; the others stay at the zeros of vba_create), lower triangle read by the solves
     launch_assemble(c->red.bptr, c->red.bnff, c->red.cs, c->red.nbr, c->red.roff, c->red.rdim, c->d_arena, lam,
-                    c->O.ridge, multi ? 0 : 1, c->d_H, c->npad, 0, st, multi ? nullptr : c->red.blist,
-                    c->red.nblist);
+                    c->O.ridge, 1, c->d_H, c->npad, 0, st, c->red.blist, c->red.nblist);
     // right-hand side -g_red: the step solves H_red dx = -g_red (solver.py:287)
     launch_assemble_vec(c->red.sptr, c->red.vs, c->red.nseg, c->red.soff, c->d_arena, -1.0, c->d_rhs, st);
-    if (multi) {
-      // only the lower triangle of the nfree x nfree block is read by the solves: it is
-      // packed for the all-reduce (half the bytes of the square matrix)
-      if (!c->d_hpack && dalloc(c, &c->d_hpack, (size_t)c->nfree * (c->nfree + 1) / 2)) return VBA_E_CUDA;
-      launch_pack_lower(c->d_H, c->npad, c->nfree, c->d_hpack, 0, st);
-      if (c->coll(c->coll_user, c->d_hpack, (int64_t)c->nfree * (c->nfree + 1) / 2, 0, st)) { set_err("allreduce(H) failed"); return VBA_E_CUDA; }
-      launch_pack_lower(c->d_H, c->npad, c->nfree, c->d_hpack, 1, st);
-      if (c->coll(c->coll_user, c->d_rhs, c->npad, 0, st)) { set_err("allreduce(g) failed"); return VBA_E_CUDA; }
-      launch_add_ridge(c->d_H, c->npad, c->nfree, c->O.ridge, st);
-    }
   }
   return VBA_OK;
 }
@@ -779,7 +842,7 @@ static int stage_step(Ctx* c, double lam, cudaStream_t st) {
   mark(c, 4, st);
   launch_scatter_dx(c->d_x, c->d_fmap, c->npv, c->d_dx, st);
   launch_step_edges(c->d_ei, c->d_ej, c->E, s, c->extr, c->d_dx, c->sdof, c->d_ustep, st);
-  launch_backsub(c->P.pixel_mode, c->d_tiles, (int)c->tiles.size(), s, n, c->pix, c->P.wts, c->d_eoff,
+  launch_backsub(c->P.pixel_mode, c->d_tiles + c->ot0, c->ot1 - c->ot0, s, n, c->pix, c->P.wts, c->d_eoff,
                  c->d_doff, c->P.grid_w, c->grid, c->intr, c->d_Hdd, c->d_gd, c->d_ustep, lam, c->O.ridge,
                  c->d_dxd, &c->d_res->step_bits, st);
   launch_retract(s, n, c->d_dx, c->d_frozen, c->K, c->sdof, c->ngrav, c->n_state, &c->d_res->step_bits, c->npv, st);
@@ -838,7 +901,7 @@ static int ensure_dense(Ctx* c, cudaStream_t st) {
 }
 
 static int stage_step_dense(Ctx* c, double lam, cudaStream_t st) {
-  if (c->coll) { set_err("use_schur=False is single-GPU only"); return VBA_E_UNSUPPORTED; }
+  if (c->world > 1) { set_err("use_schur=False is single-GPU only"); return VBA_E_UNSUPPORTED; }
   int rc = ensure_dense(c, st);
   if (rc) return rc;
   DevState& s = CUR(c);
@@ -896,8 +959,8 @@ static int run_trial(Ctx* c, double lam, int use_schur, vba_trial_result* out, c
   rc = stage_energy(c, NXT(c), st);
   if (rc) return rc;
   mark(c, 6, st);
-  if (c->coll) {
-    if (c->coll(c->coll_user, c->d_res->energy, 3, 0, st)) { set_err("allreduce(energy) failed"); return VBA_E_CUDA; }
+  if (c->world > 1) {   // each rank saw only its own pixels' dx_d: max of the step norm
+    if (!c->coll) { set_err("sharded solve without a collective hook (vba_set_collective)"); return VBA_E_INVALID; }
     if (c->coll(c->coll_user, (double*)&c->d_res->step_bits, 1, 1, st)) { set_err("allreduce(step) failed"); return VBA_E_CUDA; }
   }
   VBA_CUDA(cudaMemcpyAsync(c->h_res, c->d_res, sizeof(Result), cudaMemcpyDeviceToHost, st));
@@ -998,6 +1061,28 @@ int vba_create(void** out, const vba_problem* prob, const vba_options* opts, voi
   }
   if (!(opts->ridge > 0) || !(opts->damping > 0)) { set_err("invalid options"); return fail(VBA_E_INVALID); }
   make_extr(*prob, c->extr);
+  c->own_k1 = c->K;
+  if (prob->shard_world > 1) {
+    c->world = prob->shard_world;
+    c->rank = prob->shard_rank;
+    if (c->rank < 0 || c->rank >= c->world || !prob->h_shard_kbounds) {
+      set_err("invalid shard spec");
+      return fail(VBA_E_INVALID);
+    }
+    c->kb.assign(prob->h_shard_kbounds, prob->h_shard_kbounds + c->world + 1);
+    for (int r = 0; r < c->world; ++r)
+      if (c->kb[r] > c->kb[r + 1]) { set_err("shard bounds must be nondecreasing"); return fail(VBA_E_INVALID); }
+    if (c->kb[0] != 0 || c->kb[c->world] != c->K) { set_err("shard bounds must cover [0, K)"); return fail(VBA_E_INVALID); }
+    for (int f = 1; f < c->F; ++f)
+      if (prob->h_imu_i[f] < prob->h_imu_i[f - 1]) {
+        set_err("a sharded solve needs IMU factors sorted by their first keyframe");
+        return fail(VBA_E_UNSUPPORTED);
+      }
+    c->own_k0 = c->kb[c->rank];
+    c->own_k1 = c->kb[c->rank + 1];
+  } else {
+    c->kb = {0, c->K};
+  }
   int rc = build_plans(c, st);
   if (rc) return fail(rc);
   // topology to device
@@ -1018,7 +1103,8 @@ int vba_create(void** out, const vba_problem* prob, const vba_options* opts, voi
       (rc = dupload(c, &c->d_gorder, c->gorder, st)) || (rc = dupload(c, &c->d_gsrc_lpt, c->gsrc_lpt, st)) ||
       (rc = dupload(c, &c->d_g0, c->g0, st)) || (rc = dupload(c, &c->d_g1, c->g1, st)) ||
       (rc = dupload(c, &c->d_goff, c->goff, st)) || (rc = dupload(c, &c->d_foff, c->foff, st)) ||
-      (rc = dupload(c, &c->d_fmap, c->fmap, st)))
+      (rc = dupload(c, &c->d_fmap, c->fmap, st)) || (rc = dupload(c, &c->d_gorder_own, c->gorder_own, st)) ||
+      (rc = dupload(c, &c->d_gsrc_own, c->gsrc_own, st)))
     return fail(rc);
   // state double buffers
   for (int b = 0; b < 2; ++b) {
@@ -1140,6 +1226,13 @@ int vba_set_collective(void* ctx, vba_allreduce_fn fn, void* user) {
   Ctx* c = (Ctx*)ctx;
   c->coll = fn;
   c->coll_user = user;
+  return VBA_OK;
+}
+
+int vba_set_gather(void* ctx, vba_allgather_fn fn, void* user) {
+  Ctx* c = (Ctx*)ctx;
+  c->gat = fn;
+  c->gat_user = user;
   return VBA_OK;
 }
 
@@ -1265,7 +1358,6 @@ int vba_energy(void* ctx, void* stream, double* tot, double* vis, double* ine) {
   cudaStream_t st = (cudaStream_t)stream;
   int rc = stage_energy(c, CUR(c), st);
   if (rc) return rc;
-  if (c->coll && c->coll(c->coll_user, c->d_res->energy, 3, 0, st)) { set_err("allreduce failed"); return VBA_E_CUDA; }
   VBA_CUDA(cudaMemcpyAsync(c->h_res, c->d_res, sizeof(Result), cudaMemcpyDeviceToHost, st));
   VBA_CUDA(cudaStreamSynchronize(st));
   if (tot) *tot = c->h_res->energy[0];
@@ -1389,6 +1481,11 @@ int vba_download(void* ctx, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   DevState& s = CUR(c);
   VBA_CUDA(cudaMemcpyAsync(c->P.state, s.state, sizeof(double) * 16 * c->K, cudaMemcpyDeviceToDevice, st));
+  if (c->n_disp && c->world > 1) {   // each rank updated only its own keyframes' disparities
+    int rc = gather(c, s.disp64, c->g_disp, st, "disparities");
+    if (rc) return rc;
+    launch_narrow(s.disp64, s.disp, c->n_disp, st);
+  }
   if (c->n_disp) {
     VBA_CUDA(cudaMemcpyAsync(c->P.disp, s.disp, sizeof(float) * c->n_disp, cudaMemcpyDeviceToDevice, st));
     if (c->P.disp64)
@@ -1401,6 +1498,7 @@ int vba_download(void* ctx, void* stream) {
 int vba_export_normal_eq(void* ctx, void* stream, double* H_pp, double* g_p, double* H_pd, double* H_dd,
                          double* g_d) {
   Ctx* c = (Ctx*)ctx;
+  if (c->world > 1) { set_err("vba_export_normal_eq: not available on a sharded context"); return VBA_E_UNSUPPORTED; }
   cudaStream_t st = (cudaStream_t)stream;
   int rc = build_export_plan(c, st);
   if (rc) return rc;
@@ -1436,6 +1534,7 @@ int vba_export_reduced(void* ctx, void* stream, double lam, double* H_red, doubl
 
 int vba_export_step(void* ctx, void* stream, double* dx_full, double* dx_d) {
   Ctx* c = (Ctx*)ctx;
+  if (c->world > 1 && dx_d) { set_err("vba_export_step: dx_d is rank-local on a sharded context"); return VBA_E_UNSUPPORTED; }
   cudaStream_t st = (cudaStream_t)stream;
   if (!c->have_step) { set_err("no step computed"); return VBA_E_INVALID; }
   int rc = ensure_real_layout(c, st);

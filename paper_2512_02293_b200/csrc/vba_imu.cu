@@ -61,12 +61,12 @@ void launch_imu_prep(const double* imu, int F, double* Lbuf, int* status, cudaSt
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(64) k_imu_factor(const double* __restrict__ imu, const double* __restrict__ Lbuf,
                                                    const int32_t* __restrict__ fi, const int32_t* __restrict__ fj,
-                                                   const double* __restrict__ state, const double* __restrict__ grav,
-                                                   int sdof, int ibs, int energy_only,
+                                                   int f0, const double* __restrict__ state,
+                                                   const double* __restrict__ grav, int sdof, int ibs, int energy_only,
                                                    double* __restrict__ out) {
   __shared__ double J[15][kCols + 1];
   __shared__ double L[kImuL];
-  const int f = blockIdx.x, tid = threadIdx.x;
+  const int f = f0 + blockIdx.x, tid = threadIdx.x;
   const double* rec = imu + (int64_t)f * VBA_IMU_REC;
   for (int i = tid; i < 117; i += blockDim.x) L[i] = Lbuf[(int64_t)f * kImuL + i];
   for (int i = tid; i < 15 * (kCols + 1); i += blockDim.x) (&J[0][0])[i] = 0.0;
@@ -209,11 +209,11 @@ __global__ void __launch_bounds__(64) k_imu_factor(const double* __restrict__ im
   }
 }
 
-void launch_imu_factor(const double* imu, const double* Lbuf, const int32_t* fi, const int32_t* fj, int F,
+void launch_imu_factor(const double* imu, const double* Lbuf, const int32_t* fi, const int32_t* fj, int f0, int F,
                        const DevState& s, const double* /*ts*/, int sdof, int ibs, int energy_only,
                        double* imu_blocks, cudaStream_t st) {
   if (F <= 0) return;
-  k_imu_factor<<<F, 64, 0, st>>>(imu, Lbuf, fi, fj, s.state, s.grav, sdof, ibs, energy_only, imu_blocks);
+  k_imu_factor<<<F, 64, 0, st>>>(imu, Lbuf, fi, fj, f0, s.state, s.grav, sdof, ibs, energy_only, imu_blocks);
   launch_count();
 }
 

@@ -278,8 +278,9 @@ void launch_vision_energy(int pixel_mode, const PixTile* tiles, const int32_t* s
                           const StreamItem* items, const int32_t* ioff, int ncta, const DevState& s, const float* pix, const float* tgt, const float* wts,
                           const int64_t* eoff, const int64_t* doff, int grid_w, const double* grid,
                           const double* intr, double* tile_energy, cudaStream_t st);
+// edges [e0, e0 + n)
 void launch_edge_finalize(const int32_t* esrc_tile0, const int32_t* esrc_tile1, const PixTile* tiles,
-                          const int32_t* edge_i, int E, const double* partials, const DevState& s,
+                          const int32_t* edge_i, int e0, int n, const double* partials, const DevState& s,
                           const Extr& x, double* visblocks, double* edge_energy, cudaStream_t st);
 void launch_gram(int pixel_mode, const GramTile* gt, int ngt, int block, size_t smem, int kmax,
                  const DevState& s, const float* pix, const float* wts, const int64_t* eoff,
@@ -309,7 +310,8 @@ void launch_energy_reduce(const double* tile_energy, int ntiles, const double* i
                           int energy_off, double* out3, cudaStream_t st);
 // IMU
 void launch_imu_prep(const double* imu, int F, double* Lbuf, int* status, cudaStream_t st);
-void launch_imu_factor(const double* imu, const double* Lbuf, const int32_t* fi, const int32_t* fj, int F,
+// factors [f0, f0 + F)
+void launch_imu_factor(const double* imu, const double* Lbuf, const int32_t* fi, const int32_t* fj, int f0, int F,
                        const DevState& s, const double* ts, int sdof, int ibs, int energy_only,
                        double* imu_blocks, cudaStream_t st);
 // dense
@@ -319,8 +321,6 @@ void launch_assemble(const int32_t* blk_ptr, const int32_t* blk_nff, const Contr
                      int nblist = 0);
 void launch_assemble_vec(const int32_t* seg_ptr, const Vec* vecs, int nseg, const int32_t* seg_off,
                          const double* arena, double scale, double* g, cudaStream_t st, int skip_fill = 0);
-void launch_add_ridge(double* H, int64_t ld, int n, double ridge, cudaStream_t st);
-void launch_pack_lower(double* H, int64_t ld, int n, double* buf, int unpack, cudaStream_t st);
 void launch_pad_identity(double* H, int64_t ld, int n, int npad, double* rhs, cudaStream_t st);
 void launch_export_sym(const double* H, int64_t ld, int n, double* out, const double* rhs, double scale, double* g,
                        cudaStream_t st);

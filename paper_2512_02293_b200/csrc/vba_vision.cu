@@ -707,12 +707,12 @@ void launch_vision_energy(int mode, const PixTile* tiles, const int32_t* soff, c
 __global__ void __launch_bounds__(64) k_edge_finalize(const int32_t* __restrict__ t0s,
                                                       const int32_t* __restrict__ t1s,
                                                       const PixTile* __restrict__ tiles,
-                                                      const int32_t* __restrict__ edge_i,
+                                                      const int32_t* __restrict__ edge_i, int e0,
                                                       const double* __restrict__ partials,
                                                       const double* __restrict__ geo64, Extr x,
                                                       double* __restrict__ vis, double* __restrict__ eng) {
   __shared__ double v[32], S[36], Gi[36], Gj[36], T1[36], T2[36];
-  const int e = blockIdx.x, tid = threadIdx.x;
+  const int e = e0 + blockIdx.x, tid = threadIdx.x;
   const int src = edge_i[e];
   if (tid < 32) {   // K1 records: per (tile, edge) one fp32 32-vector per warp, summed in fp64, fixed order
     const float* fp = reinterpret_cast<const float*>(partials);
@@ -779,10 +779,10 @@ __global__ void __launch_bounds__(64) k_edge_finalize(const int32_t* __restrict_
 }
 
 void launch_edge_finalize(const int32_t* t0s, const int32_t* t1s, const PixTile* tiles, const int32_t* edge_i,
-                          int E, const double* partials, const DevState& s, const Extr& x, double* vis,
+                          int e0, int n, const double* partials, const DevState& s, const Extr& x, double* vis,
                           double* eng, cudaStream_t st) {
-  if (E <= 0) return;
-  k_edge_finalize<<<E, 64, 0, st>>>(t0s, t1s, tiles, edge_i, partials, s.geo64, x, vis, eng);
+  if (n <= 0) return;
+  k_edge_finalize<<<n, 64, 0, st>>>(t0s, t1s, tiles, edge_i, e0, partials, s.geo64, x, vis, eng);
   launch_count();
 }
 

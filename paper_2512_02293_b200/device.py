@@ -421,10 +421,13 @@ _TERM = {0: "max_iterations", 1: "converged", 2: "no_decrease_at_max_damping"}
 class DeviceProblem:
     """One VI-BA problem resident on the current CUDA device."""
 
-    def __init__(self, P, opts: dict, layout: HostLayout | None = None, device=None, stream=None):
+    def __init__(self, P, opts: dict, layout: HostLayout | None = None, device=None, stream=None, shard=None):
+        """``shard = (rank, world, kbounds)``: an edge-sharded rank of a multi-GPU solve
+        (paper_2512_02293_b200.distributed); the layout is the whole problem."""
         _require_cuda()
         self.lib = L.load()
         self.opts = dict(opts)
+        self.shard = shard
         self.H = layout if layout is not None else HostLayout(P, self.opts)
         H = self.H
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
@@ -508,6 +511,10 @@ class DeviceProblem:
         p.grav = self.d_grav.data_ptr()
         p.h_doff, p.h_npix, p.h_edge_i, p.h_edge_j, p.h_eoff, p.h_imu_i, p.h_imu_j, p.h_frozen = (
             a.ctypes.data for a in hk)
+        if self.shard is not None and self.shard[1] > 1:
+            rank, world, kb = self.shard
+            self._kb = np.ascontiguousarray(kb, np.int32)
+            p.shard_world, p.shard_rank, p.h_shard_kbounds = int(world), int(rank), self._kb.ctypes.data
         o = self.opts
         op = L.VbaOptions()
         op.max_iterations = int(o.get("max_iterations", 10))

@@ -4,13 +4,23 @@ Partition: every out-edge of source keyframe i lives on the
 rank that owns i, so per-pixel disparity elimination, the Schur fill-in and the
 back-substitution are rank-local.  Ranks own contiguous keyframe ranges balanced
 by edge rows; IMU factor (i, i+1) belongs to the owner of i.  States are
-replicated.  Per LM trial the native driver calls the collective hook for
+replicated.
 
-  * all_reduce(SUM) of the partial reduced system H_red, g_red (fp64), then the
-    ridge is added once and every rank runs the identical Cholesky;
-  * all_reduce(SUM) of the energy partials and all_reduce(MAX) of the step norm,
+Exchange (include/vba.h, vba_problem.shard_* and vba_set_gather): every rank
+holds the whole problem and plans the whole solve, but computes only its own
+slices of the per-edge vision blocks, per-factor IMU blocks, per-source fill-in
+blocks and per-tile energy partials.  The native LM loop all-gathers those slices
+(once per linearisation for the vision/IMU blocks, once per trial for the fill-in
+and energies) and every rank then assembles, in the single-GPU order, the
+identical reduced system and runs the identical Cholesky: an N-rank solve is
+bitwise the 1-rank solve (deterministic, rank-count invariant), and it moves the
+compact blocks (≈ 50 MB per trial at config 4) instead of all-reducing the dense
+reduced system (235 MB).  The step norm is max-reduced; the disparities each rank
+updated are gathered on download.
 
-so every rank takes the same accept/reject decision (solver.py:383-398).
+The hooks run their collectives on the solve's own CUDA stream
+(``torch.cuda.ExternalStream``), so they are ordered after the kernels that wrote
+the slices whatever torch's current stream is.
 """
 
 from __future__ import annotations
@@ -38,6 +48,12 @@ def partition_sources(P, world: int):
     return [(int(bounds[r]), int(bounds[r + 1])) for r in range(world)]
 
 
+def shard_bounds(P, world: int):
+    """Keyframe bounds kb[world + 1] of partition_sources (vba_problem.h_shard_kbounds)."""
+    parts = partition_sources(P, world)
+    return np.array([p[0] for p in parts] + [parts[-1][1]], dtype=np.int32)
+
+
 def shard(P, rank: int, world: int):
     """(edge indices, IMU factor indices) owned by ``rank``."""
     k0, k1 = partition_sources(P, world)[rank]
@@ -57,21 +73,33 @@ class _CudaView:
 
 
 class TorchCollective:
-    """vba_allreduce_fn backed by torch.distributed (NCCL on GPUs, gloo on CPU tests)."""
+    """vba_allreduce_fn / vba_allgather_fn backed by torch.distributed.
+
+    NCCL: collectives on the solve stream; variable-size gathers through one padded
+    all_gather_into_tensor.  gloo (ranks sharing a GPU in tools/dist_check.py, or CPU
+    process groups): host-staged, so no kernel ever waits on another rank's kernel."""
 
     def __init__(self, group=None, device=None):
         import torch
         import torch.distributed as dist
         self.torch, self.dist, self.group = torch, dist, group
         self.device = device
+        self.rank = dist.get_rank(group)
+        self.nccl = dist.get_backend(group) == "nccl"
         self.calls = 0
         self.bytes = 0
 
-        def _fn(user, buf, count, op, stream):
+        def _reduce(user, buf, count, op, stream):
             try:
-                t = self.torch.as_tensor(_CudaView(buf, count), device=self.device)
-                red = self.dist.ReduceOp.SUM if op == 0 else self.dist.ReduceOp.MAX
-                self.dist.all_reduce(t, op=red, group=self.group)
+                with self._on(stream):
+                    t = self.torch.as_tensor(_CudaView(buf, count), device=self.device)
+                    red = self.dist.ReduceOp.SUM if op == 0 else self.dist.ReduceOp.MAX
+                    if self.nccl:
+                        self.dist.all_reduce(t, op=red, group=self.group)
+                    else:
+                        h = t.cpu()
+                        self.dist.all_reduce(h, op=red, group=self.group)
+                        t.copy_(h)
                 self.calls += 1
                 self.bytes += 8 * int(count)
                 return 0
@@ -79,20 +107,71 @@ class TorchCollective:
                 print(f"[vba] allreduce failed: {exc}")
                 return 1
 
-        self._cfn = L.ALLREDUCE_FN(_fn)
+        def _gather(user, buf, offs, world, stream):
+            try:
+                o = [int(offs[r]) for r in range(world + 1)]
+                self._gather(buf, o, world, stream)
+                self.calls += 1
+                return 0
+            except Exception as exc:
+                print(f"[vba] gather failed: {exc}")
+                return 1
+
+        self._cfn = L.ALLREDUCE_FN(_reduce)
+        self._gfn = L.ALLGATHER_FN(_gather)
+
+    def _on(self, stream):
+        torch = self.torch
+        if stream:
+            return torch.cuda.stream(torch.cuda.ExternalStream(int(stream), device=self.device))
+        import contextlib
+        return contextlib.nullcontext()
+
+    def _gather(self, buf, o, world, stream):
+        torch, dist = self.torch, self.dist
+        sizes = [o[r + 1] - o[r] for r in range(world)]
+        m = max(sizes)
+        if m == 0:
+            return
+        base = o[0]
+        with self._on(stream):
+            full = torch.as_tensor(_CudaView(buf + 8 * base, o[-1] - base), device=self.device)
+            mine = full[o[self.rank] - base:o[self.rank + 1] - base]
+            if self.nccl:
+                if all(s == m for s in sizes):
+                    dist.all_gather_into_tensor(full, mine.clone(), group=self.group)
+                else:
+                    tmp = torch.empty(world * m, dtype=full.dtype, device=full.device)
+                    tmp[self.rank * m:self.rank * m + sizes[self.rank]].copy_(mine)
+                    dist.all_gather_into_tensor(tmp, tmp[self.rank * m:(self.rank + 1) * m].clone(),
+                                                group=self.group)
+                    for r in range(world):
+                        if r != self.rank and sizes[r]:
+                            full[o[r] - base:o[r + 1] - base].copy_(tmp[r * m:r * m + sizes[r]])
+            else:
+                h = torch.zeros(m, dtype=torch.float64)
+                h[:sizes[self.rank]].copy_(mine)
+                parts = [torch.empty(m, dtype=torch.float64) for _ in range(world)]
+                dist.all_gather(parts, h, group=self.group)
+                for r in range(world):
+                    if r != self.rank and sizes[r]:
+                        full[o[r] - base:o[r + 1] - base].copy_(parts[r][:sizes[r]])
+        self.bytes += 8 * int(o[-1] - base)
 
     def attach(self, dp):
         L.check(dp.lib.vba_set_collective(dp.ctx, self._cfn, None))
+        L.check(dp.lib.vba_set_gather(dp.ctx, self._gfn, None))
 
 
 def make_sharded_problem(P, opts, rank, world, group=None):
-    """DeviceProblem holding this rank's edge shard, with the NCCL hook attached."""
+    """DeviceProblem of the whole problem owning the source keyframes of ``rank``, with the
+    torch.distributed hooks attached (a plain single-GPU problem when world == 1)."""
     from .device import DeviceProblem, HostLayout
-    edges, imu = shard(P, rank, world)
-    H = HostLayout(P, opts, edge_subset=edges, imu_subset=imu)
-    dp = DeviceProblem(P, opts, layout=H)
-    if world > 1:
-        coll = TorchCollective(group=group, device=dp.device)
-        coll.attach(dp)
-        dp._collective = coll
+    H = HostLayout(P, opts)
+    if world <= 1:
+        return DeviceProblem(P, opts, layout=H)
+    dp = DeviceProblem(P, opts, layout=H, shard=(rank, world, shard_bounds(P, world)))
+    coll = TorchCollective(group=group, device=dp.device)
+    coll.attach(dp)
+    dp._collective = coll
     return dp
