@@ -969,9 +969,6 @@ __device__ void tc_task_gemm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
   proxy_fence_shared();   // generic staging writes before later bulk copies into the ring
 }
 
-#ifdef VBA_TRSM_PROF
-__device__ unsigned long long g_trsm_prof[8];
-#endif
 // TRSM(i,k):  L_ik = W_ik Linv_kk^T   (A = W_ik split by the threads, B = Linv images)
 __device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_t& nacc, uint32_t tmem, int i,
                              int k, bool keep_smem = false) {
@@ -979,9 +976,6 @@ __device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
   const float* Wik = a.W + tlin(i, k) * TILE_F;
   const float* ib = a.img + tlin(k, k) * TILE_F;
   if (tid == 0) proxy_fence_global();
-#ifdef VBA_TRSM_PROF
-  long long tp0 = clock64();
-#endif
   // the thread's share of A: 16-B unit u = tid % 8 of rows tid / 8 + 32 q of each chunk
   // (a warp reads four full 128-B chunk rows per instruction); all loads first
   const int u0 = tid & 7, m0 = tid >> 3;
@@ -1030,15 +1024,9 @@ __device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
     }
   }
   if (tid == 0) tc_commit(accf);
-#ifdef VBA_TRSM_PROF
-  long long tp1 = clock64();
-#endif
   tc_mbar_wait(accf, nacc & 1);
   ++nacc;
   tc_fence_after();
-#ifdef VBA_TRSM_PROF
-  long long tp2 = clock64();
-#endif
   // epilogue: L_ik (fp32) staged row-padded at TC_EPI_OFF and its hi/lo chunk images
   // (the global image layout) at 2 ch TCHUNK (hi), + TCHUNK (lo) of the idle ring;
   // then the images leave by bulk copies and the fp32 rows by coalesced stores.
@@ -1067,9 +1055,6 @@ __device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
     tc_fence_before();
     proxy_fence_shared();   // generic writes -> bulk-copy / tcgen05 reads of the images
     __syncthreads();
-#ifdef VBA_TRSM_PROF
-    if (tid == 0) atomicAdd(&g_trsm_prof[5], (unsigned long long)(clock64() - tp2));
-#endif
     float* ihi = a.img + tlin(i, k) * TILE_F;
     if (tid == 0) {
 #pragma unroll
@@ -1083,25 +1068,8 @@ __device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
     for (int q = 0; q < 16; ++q)
       __stcg(reinterpret_cast<float4*>(Lg) + (16 * w + q) * (CT / 4) + lane,
              *reinterpret_cast<const float4*>(S + (16 * w + q) * EPS + 4 * lane));
-#ifdef VBA_TRSM_PROF
-    if (tid == 0) atomicAdd(&g_trsm_prof[6], (unsigned long long)(clock64() - tp2));
-#endif
     if (tid == 0) tc_bulk_commit_wait();   // image writes complete before the caller's fences
   }
-#ifdef VBA_TRSM_PROF
-  __syncthreads();
-  long long tp3 = clock64();
-  __threadfence();
-  __syncthreads();
-  long long tp4 = clock64();
-  if (tid == 0) {
-    atomicAdd(&g_trsm_prof[0], (unsigned long long)(tp1 - tp0));
-    atomicAdd(&g_trsm_prof[1], (unsigned long long)(tp2 - tp1));
-    atomicAdd(&g_trsm_prof[2], (unsigned long long)(tp3 - tp2));
-    atomicAdd(&g_trsm_prof[3], (unsigned long long)(tp4 - tp3));
-    atomicAdd(&g_trsm_prof[4], 1ull);
-  }
-#endif
 }
 
 // Diagonal SYRK of DIAG(k): W_{k+1,k+1} -= L L^T with L = L_{k+1,k} already in shared
@@ -1504,9 +1472,6 @@ __device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d, bool defer
   __syncthreads();
   for (int sp = 0; sp < CT / 8; ++sp) {
     const int c0 = 8 * sp, r0 = c0 + 8, nr = CT - r0;
-#ifdef VBA_POTRF_PROF
-    long long q0 = clock64();
-#endif
     if (tid < nr) {   // panel TRSM: L[r][c0+c] = sum_{m<=c} A[r][c0+m] X[c][m]
       const int r = r0 + tid;
       float av[8];
@@ -1533,9 +1498,6 @@ __device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d, bool defer
       }
     }
     __syncthreads();
-#ifdef VBA_POTRF_PROF
-    long long q1 = clock64();
-#endif
     if (nr == 0) break;
     // Look-ahead: warp 0 updates the next panel's 8x8 diagonal block (three 4x4
     // blocks) and one of its threads factors it (diag8) while warps 1..7 do the rest
@@ -1562,13 +1524,7 @@ __device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d, bool defer
         }
       }
     }
-#ifdef VBA_POTRF_PROF
-    if ((tid & 31) == 0 && ph) atomicAdd(&ph[tid == 0 ? 2 : 3], (unsigned long long)(clock64() - q1));
-#endif
     __syncthreads();
-#ifdef VBA_POTRF_PROF
-    if (tid == 0 && ph) { ph[13] += 0; ph[14] += q1 - q0; ph[15] += clock64() - q1; }
-#endif
   }
   if (tid == 0 && bad) atomicExch(a.status, 1);
   if (ph && tid == 0) ph[9] = gtimer();
@@ -1859,12 +1815,7 @@ __global__ void __launch_bounds__(256) k_tc_convert(const double* __restrict__ H
 // inverse of its diagonal tile (M = Linv_kk L_{k,k-1}, resp. T = L_{k+1,k} Linv_kk),
 // so that one 128x128 matvec per step remains on the chain.
 constexpr size_t TRI_SMEM = 3 * (size_t)TILE_F * sizeof(float) + 64;
-#ifdef VBA_TRI_PROF
-__device__ unsigned long long g_tri_ts[2][4][256];   // [fwd/bwd][start, ready(prep done), offchain done, publish][k]
-#define TRI_STAMP(dir, what, k) if (threadIdx.x == 0) g_tri_ts[dir][what][k] = gtimer();
-#else
 #define TRI_STAMP(dir, what, k)
-#endif
 
 __device__ __forceinline__ void put_tagged(unsigned long long* p, float v, int gen) {
   const unsigned long long w = ((unsigned long long)(unsigned)gen << 32) | __float_as_uint(v);
@@ -2490,17 +2441,6 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
     k_tc_fwd<<<nt * (1 + hlp), 256, TRI_SMEM, st>>>(W, Fm, nt, rhs, D, y, Vs, gen + 2 * it, stop, hlp);
     k_tc_bwd<<<nt * (1 + hlp), 256, TRI_SMEM, st>>>(W, Fm, nt, y, z, Us, D, x, out2, out2 + 1, gen + 2 * it,
                                                     stop, hlp);
-#ifdef VBA_TRI_PROF
-    if (it == 0) {
-      unsigned long long h[2][4][256];
-      cudaStreamSynchronize(st);
-      cudaMemcpyFromSymbol(h, g_tri_ts, sizeof(h));
-      const unsigned long long t0 = h[0][0][0];
-      for (int k = 0; k < nt; k += (nt > 20 ? 6 : 1))
-        fprintf(stderr, "fwd k=%2d start %7.1f offchain-done %7.1f tiles-in %7.1f publish %7.1f us\n", k, (h[0][0][k] - t0) * 1e-3,
-                (h[0][1][k] - t0) * 1e-3, (h[0][2][k] - t0) * 1e-3, (h[0][3][k] - t0) * 1e-3);
-    }
-#endif
     // stop once a pass corrects x by <= kTcRefineTol max|x| (vba_internal.cuh)
     k_tc_check<<<1, 1, 0, st>>>(out2, stop, kTcRefineTol, kTcErrTol, it == iters - 1);
     launch_count();

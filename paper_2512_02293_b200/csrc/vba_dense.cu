@@ -16,8 +16,6 @@
 
 namespace vba {
 
-constexpr int NB = 64;
-
 // ---------------------------------------------------------------------------
 // assembly: one CTA per lower block (a >= b) of the block matrix
 // ---------------------------------------------------------------------------
@@ -176,219 +174,6 @@ void launch_pad_identity(double* H, int64_t ld, int n, int npad, double* rhs, cu
 
 // ---------------------------------------------------------------------------
 // Cholesky
-// ---------------------------------------------------------------------------
-// Factor the 64x64 diagonal tile in shared memory (right-looking, lower).
-__device__ void tile_potrf(double (*L)[NB + 1], int* status, bool report) {
-  const int tid = threadIdx.x, nth = blockDim.x;
-  for (int j = 0; j < NB; ++j) {
-    if (tid == 0) {
-      double d = L[j][j];
-      if (!(d > 0.0)) {
-        if (report) atomicExch(status, 1);
-        d = 1.0;
-      }
-      L[j][j] = sqrt(d);
-    }
-    __syncthreads();
-    const double inv = 1.0 / L[j][j];
-    for (int r = j + 1 + tid; r < NB; r += nth) L[r][j] *= inv;
-    __syncthreads();
-    const int m = NB - j - 1;
-    for (int t = tid; t < m * m; t += nth) {
-      const int r = j + 1 + t % m, c = j + 1 + t / m;
-      if (c <= r) L[r][c] -= L[r][j] * L[c][j];
-    }
-    __syncthreads();
-  }
-}
-
-// Panel k: every CTA factors the diagonal tile redundantly; CTA 0 writes L_kk and
-// forward-solves the rhs block, CTA b >= 1 solves X L_kk^T = A_{k+b,k}.
-__global__ void __launch_bounds__(256) k_chol_panel(double* __restrict__ A, int64_t ld, int k,
-                                                    double* __restrict__ rhs, double* __restrict__ Ldiag,
-                                                    int* __restrict__ status) {
-  extern __shared__ double dsm[];
-  double(*L)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm);
-  double(*X)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm + NB * (NB + 1));
-  const int tid = threadIdx.x, nth = blockDim.x;
-  const int64_t o = (int64_t)k * NB;
-  for (int t = tid; t < NB * NB; t += nth) {
-    const int r = t % NB, c = t / NB;
-    L[r][c] = (c <= r) ? A[(o + c) * ld + o + r] : 0.0;
-  }
-  __syncthreads();
-  tile_potrf(L, status, blockIdx.x == 0);
-  if (blockIdx.x == 0) {
-    // L_kk goes to a side buffer: the other CTAs of this launch still read A_kk
-    double* Ld = Ldiag + (int64_t)k * NB * NB;
-    for (int t = tid; t < NB * NB; t += nth) {
-      const int r = t % NB, c = t / NB;
-      Ld[c * NB + r] = L[r][c];
-    }
-    if (tid < 32) {  // forward substitution y_k = L_kk^-1 rhs_k (one warp)
-      __shared__ double y[NB];
-      for (int r = tid; r < NB; r += 32) y[r] = rhs[o + r];
-      __syncwarp();
-      for (int r = 0; r < NB; ++r) {
-        double s = 0.0;
-        for (int m = tid; m < r; m += 32) s += L[r][m] * y[m];
-#pragma unroll
-        for (int q = 16; q >= 1; q >>= 1) s += __shfl_xor_sync(0xffffffffu, s, q);
-        if (tid == 0) y[r] = (y[r] - s) / L[r][r];
-        __syncwarp();
-      }
-      for (int r = tid; r < NB; r += 32) rhs[o + r] = y[r];
-    }
-    return;
-  }
-  const int64_t ro = o + (int64_t)blockIdx.x * NB;   // tile row k + b
-  for (int t = tid; t < NB * NB; t += nth) {
-    const int r = t % NB, c = t / NB;
-    X[r][c] = A[(o + c) * ld + ro + r];
-  }
-  __syncthreads();
-  // X L^T = A  -> column sweep
-  for (int c = 0; c < NB; ++c) {
-    const double inv = 1.0 / L[c][c];
-    for (int r = tid; r < NB; r += nth) X[r][c] *= inv;
-    __syncthreads();
-    const int m = NB - c - 1;
-    for (int t = tid; t < NB * m; t += nth) {
-      const int r = t % NB, cc = c + 1 + t / NB;
-      X[r][cc] -= X[r][c] * L[cc][c];
-    }
-    __syncthreads();
-  }
-  for (int t = tid; t < NB * NB; t += nth) {
-    const int r = t % NB, c = t / NB;
-    A[(o + c) * ld + ro + r] = X[r][c];
-  }
-}
-
-// Trailing update for panel k: A_ij -= L_ik L_jk^T for k < j <= i, and rhs_i -= L_ik y_k.
-// Blocks [0, npairs) handle tile pairs, blocks [npairs, npairs + nrow) the rhs.
-__global__ void __launch_bounds__(256) k_chol_update(double* __restrict__ A, int64_t ld, int k, int nt,
-                                                     double* __restrict__ rhs) {
-  extern __shared__ double dsm[];
-  double(*Li)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm);
-  double(*Lj)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm + NB * (NB + 1));
-  const int tid = threadIdx.x;
-  const int m = nt - k - 1;
-  const int64_t npairs = (int64_t)m * (m + 1) / 2;
-  const int64_t o = (int64_t)k * NB;
-  if ((int64_t)blockIdx.x >= npairs) {
-    const int i = k + 1 + (int)(blockIdx.x - npairs);
-    const int64_t ri = (int64_t)i * NB;
-    if (tid < NB) {
-      double s = 0.0;
-      for (int c = 0; c < NB; ++c) s += A[(o + c) * ld + ri + tid] * rhs[o + c];
-      rhs[ri + tid] -= s;
-    }
-    return;
-  }
-  const int64_t id = blockIdx.x;
-  int ii = (int)((sqrt(8.0 * (double)id + 1.0) - 1.0) * 0.5);
-  while ((int64_t)(ii + 1) * (ii + 2) / 2 <= id) ++ii;
-  while ((int64_t)ii * (ii + 1) / 2 > id) --ii;
-  const int jj = (int)(id - (int64_t)ii * (ii + 1) / 2);
-  const int64_t ri = (int64_t)(k + 1 + ii) * NB, rj = (int64_t)(k + 1 + jj) * NB;
-  for (int t = tid; t < NB * NB; t += blockDim.x) {
-    const int r = t % NB, c = t / NB;
-    Li[r][c] = A[(o + c) * ld + ri + r];
-    Lj[r][c] = A[(o + c) * ld + rj + r];
-  }
-  __syncthreads();
-  const int tr = tid % 16, tc = tid / 16;
-  double acc[4][4];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-#pragma unroll 4
-  for (int q = 0; q < NB; ++q) {
-    double x[4], y[4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a) { x[a] = Li[tr + 16 * a][q]; y[a] = Lj[tc + 16 * a][q]; }
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b] = fma(x[a], y[b], acc[a][b]);
-  }
-#pragma unroll
-  for (int b = 0; b < 4; ++b)
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int64_t idx = (rj + tc + 16 * b) * ld + ri + tr + 16 * a;
-      A[idx] -= acc[a][b];
-    }
-}
-
-// Backward substitution step k: x_k = L_kk^-T y'_k where y'_k = y_k - sum_{i>k} L_ik^T x_i has
-// already been accumulated into rhs_k; CTA j < k then updates rhs_j -= L_kj^T x_k.
-__global__ void __launch_bounds__(256) k_chol_back(const double* __restrict__ A, int64_t ld, int k,
-                                                   const double* __restrict__ Ldiag, double* __restrict__ rhs,
-                                                   double* __restrict__ x) {
-  __shared__ double xs[NB];
-  __shared__ double Lkk[NB][NB + 1];
-  const int tid = threadIdx.x;
-  const int64_t o = (int64_t)k * NB;
-  const double* Ld = Ldiag + (int64_t)k * NB * NB;
-  for (int t = tid; t < NB * NB; t += blockDim.x) {
-    const int r = t % NB, c = t / NB;
-    Lkk[r][c] = (c <= r) ? Ld[c * NB + r] : 0.0;
-  }
-  if (tid < NB) xs[tid] = rhs[o + tid];
-  __syncthreads();
-  if (tid < 32) {  // L^T x = y  (upper triangular), one warp
-    for (int r = NB - 1; r >= 0; --r) {
-      double s = 0.0;
-      for (int m = r + 1 + tid; m < NB; m += 32) s += Lkk[m][r] * xs[m];
-#pragma unroll
-      for (int q = 16; q >= 1; q >>= 1) s += __shfl_xor_sync(0xffffffffu, s, q);
-      if (tid == 0) xs[r] = (xs[r] - s) / Lkk[r][r];
-      __syncwarp();
-    }
-  }
-  __syncthreads();
-  if (blockIdx.x == 0) {
-    if (tid < NB) x[o + tid] = xs[tid];
-    return;
-  }
-  const int j = blockIdx.x - 1;   // 0 .. k-1
-  const int64_t cj = (int64_t)j * NB;
-  if (tid < NB) {  // rhs_j[c] -= sum_r L_kj[r][c] x_k[r],  L_kj[r][c] = A[(cj + c)*ld + o + r]
-    double s = 0.0;
-    for (int r = 0; r < NB; ++r) s += A[(cj + tid) * ld + o + r] * xs[r];
-    rhs[cj + tid] -= s;
-  }
-}
-
-int chol_solve(double* A, int64_t ld, int npad, double* rhs, double* x, double* Ldiag, int* status,
-               cudaStream_t st) {
-  const int nt = npad / NB;
-  const int smem = 2 * NB * (NB + 1) * (int)sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_chol_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(k_chol_update, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
-  for (int k = 0; k < nt; ++k) {
-    k_chol_panel<<<nt - k, 256, smem, st>>>(A, ld, k, rhs, Ldiag, status);
-    launch_count();
-    const int m = nt - k - 1;
-    if (m > 0) {
-      const int64_t nb = (int64_t)m * (m + 1) / 2 + m;
-      k_chol_update<<<(unsigned)nb, 256, smem, st>>>(A, ld, k, nt, rhs);
-      launch_count();
-    }
-  }
-  for (int k = nt - 1; k >= 0; --k) {
-    k_chol_back<<<k + 1, 256, 0, st>>>(A, ld, k, Ldiag, rhs, x);
-    launch_count();
-  }
-  return 0;
-}
 
 // dx_full[n*sdof + r] from the free-layout solution (zeros at frozen keyframes)
 __global__ void k_scatter_dx(const double* __restrict__ x, const int32_t* __restrict__ fmap, int npv,

@@ -287,10 +287,6 @@ void launch_gram(int pixel_mode, const GramTile* gt, int ngt, int block, size_t 
                  const int64_t* doff, int grid_w, const double* grid, const double* intr,
                  const float* Hdd, const float* gd, double lam, double ridge, double* gram_part,
                  cudaStream_t st, const int32_t* order = nullptr);
-void launch_gram_reduce(const int32_t* src_list, int nsrc, const int32_t* src_gt0, const int32_t* src_gt1,
-                        const GramTile* gt, const int32_t* src_eb, const int32_t* src_ee,
-                        const int64_t* src_gram_off, const double* gram_part, double* gram,
-                        cudaStream_t st);
 void launch_fill_transform(const int32_t* src_list, int nsrc, const int32_t* src_eb, const int32_t* src_ee,
                            const int32_t* src_gt0, const int32_t* src_gt1, const GramTile* gt, const int64_t* foff,
                            const double* part, const DevState& s, const Extr& x, double* fill, int kmax,
@@ -342,8 +338,6 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
 void chol_trace_print(const char* tag, const unsigned long long* d_trace, const void* d_tasks, int ntasks, int nt);
 // copy the task list back (for trace decoding): type,i,j,k per task
 void chol_task_fields(const void* tasks, int n, int* out4);
-int chol_solve(double* H, int64_t ld, int npad, double* rhs, double* x, double* Ldiag, int* status,
-               cudaStream_t st);
 void launch_scatter_dx(const double* x, const int32_t* free_map, int npv, double* dx_full, cudaStream_t st);
 // pose-disparity coupling writer: reference-layout export (colmap == NULL, rows k*sdof+a) or the
 // free-layout full dense system of the use_schur=False path (rows colmap[k]+a, plus the damped

@@ -199,19 +199,7 @@ void launch_edge_prep(const DevState& s, const int32_t* ei, const int32_t* ej, i
 // of S = sum w K^T K and 6 of s = sum w K^T r (slots 27..31 zero), and per
 // pixel H_dd, g_d (sum over out-edges).  K2 writes one fp64 energy per tile.
 // ---------------------------------------------------------------------------
-#ifndef VBA_K1_STAGES
-#define VBA_K1_STAGES 3
-#endif
-#ifndef VBA_K1_FENCE
-#define VBA_K1_FENCE 0
-#endif
-#ifndef VBA_K1_SKIP
-#define VBA_K1_SKIP 1
-#endif
-#ifndef VBA_K1_MINB
-#define VBA_K1_MINB 3
-#endif
-constexpr int kStages = VBA_K1_STAGES;
+constexpr int kStages = 3;
 constexpr int kPairs = kTile / 2;   // float4 (= 2 pixels) per row of a stage
 static_assert(kPixBlock / 32 == kPartWarps, "K1 partial records hold one vector per warp");
 constexpr int kSchedCap = 24;       // tile records of one CTA staged in shared memory
@@ -281,22 +269,8 @@ __device__ __forceinline__ float2 operator-(float2 a) { return make_float2(-a.x,
 // Static LPT schedule: CTA b owns tiles sched_ids[sched_off[b] .. sched_off[b+1])
 // (host-balanced by edge-pixels, vba_host.cu build_plans), so the producer knows
 // every upcoming tile without a global atomic on the critical path.
-#ifdef VBA_K1_TRACE   // tuning builds: cycles spent waiting for stages vs total, per warp
-__device__ unsigned long long g_k1_trace[4];
-__device__ unsigned long long g_k1_end[1024];   // per-CTA finish time (globaltimer)
-extern "C" __attribute__((visibility("default"))) void vba_k1_ends(unsigned long long* out) {
-  cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out, g_k1_end, sizeof(g_k1_end));
-}
-extern "C" __attribute__((visibility("default"))) void vba_k1_trace(unsigned long long* out) {
-  cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out, g_k1_trace, sizeof(g_k1_trace));
-  unsigned long long z[4] = {0, 0, 0, 0};
-  cudaMemcpyToSymbol(g_k1_trace, z, sizeof(z));
-}
-#endif
 template <int MODE, bool LIN>
-__global__ void __launch_bounds__(kPixBlock, VBA_K1_MINB) k_vision_stream(
+__global__ void __launch_bounds__(kPixBlock, 3) k_vision_stream(
     const PixTile* __restrict__ tiles, const int32_t* __restrict__ sched_off, const int32_t* __restrict__ sched_ids,
     const StreamItem* __restrict__ items, const int32_t* __restrict__ item_off, const float* __restrict__ disp,
     const EdgeGeo32* __restrict__ geo, const float* __restrict__ pix, const float* __restrict__ tgt,
@@ -348,21 +322,11 @@ __global__ void __launch_bounds__(kPixBlock, VBA_K1_MINB) k_vision_stream(
   auto release = [&](int j) {   // whole warp; call after its last read of item j's stage
     __syncwarp();
     if (lane == 0) {
-#if VBA_K1_FENCE
-      __threadfence_block();
-#endif
       // the warp's reads of the stage have returned (their values were consumed);
       // the acq_rel counter orders them before the refill issued by the last warp
       unsigned int r;
-#if VBA_K1_RELAXED
-      asm volatile("atom.relaxed.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(r) : "r"(smem_u32(&S.rel[j % kStages])) : "memory");
-#else
       asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(r) : "r"(smem_u32(&S.rel[j % kStages])) : "memory");
-#endif
       if (r % (kPixBlock / 32) == (kPixBlock / 32) - 1 && j + kStages < nitems) {
-#if VBA_K1_FENCE
-        __threadfence_block();
-#endif
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // others' generic reads before the refill
         issue(j + kStages);
       }
@@ -377,9 +341,6 @@ __global__ void __launch_bounds__(kPixBlock, VBA_K1_MINB) k_vision_stream(
   __syncthreads();
 
   int item = 0;
-#ifdef VBA_K1_TRACE
-  const long long tk0 = clock64();
-#endif
 #pragma unroll 1
   for (int ord = 0; ord < nmine; ++ord) {
     const PixTile T = tile_at(ord);
@@ -416,45 +377,19 @@ __global__ void __launch_bounds__(kPixBlock, VBA_K1_MINB) k_vision_stream(
             load_rays<VBA_PIX_KF>(pix, eoff[e], T.n0 + 2 * QP[m], grid_w, gp, in, RX[m].x,
                                   RY[m].x, RX[m].y, RY[m].y);
       }
-#ifdef VBA_K1_TRACE
-      const long long tw0 = clock64();
-#endif
       mbar_wait(&S.full[s], (item / kStages) & 1);
-#ifdef VBA_K1_TRACE
-      if (LIN && lane == 0) atomicAdd(&g_k1_trace[0], (unsigned long long)(clock64() - tw0));
-#endif
       const EdgeGeo32 g = S.geo[s];
       float2 acc[LIN ? 27 : 1];
 #pragma unroll
       for (int k = 0; k < (LIN ? 27 : 1); ++k) acc[k] = make_float2(0.f, 0.f);
-#if VBA_K1_SKIP == 2
-      bool anyw = false;   // whole warp-item skip: all 64 x kTP pixels of this warp have w = 0
-#pragma unroll
-      for (int m = 0; m < kTP; ++m) {
-        const float4 wl = S.wts[s][QP[m]];
-        anyw |= ((act >> m) & 1u) && (wl.x != 0.f || wl.y != 0.f || wl.z != 0.f || wl.w != 0.f);
-      }
-      if (__any_sync(0xffffffffu, anyw))
-#endif
 #pragma unroll
       for (int m = 0; m < kTP; ++m) {
         const float4 wl = S.wts[s][QP[m]];
         // zero-weight skip: a pixel with w = 0 adds exact zeros to every sum
         // (residuals.py:254-263), so a warp whose 64 pixels all have w = 0 skips
         // the arithmetic (bitwise identical result; the rows are still streamed)
-#if VBA_K1_SKIP == 1
         const bool nz = ((act >> m) & 1u) && (wl.x != 0.f || wl.y != 0.f || wl.z != 0.f || wl.w != 0.f);
-#ifdef VBA_K1_TRACE
-        if (LIN && lane == 0) atomicAdd(&g_k1_trace[3], __any_sync(0xffffffffu, nz) ? 0ull : 1ull);
-#endif
         if (!__any_sync(0xffffffffu, nz)) continue;
-#endif
-#ifdef VBA_K1_NOMATH   // tuning builds only: pipeline + reductions without the per-pixel arithmetic
-        if (LIN) continue;
-#endif
-#ifdef VBA_K1_QUARTER  // tuning builds only: arithmetic of one pixel pair in four
-        if (LIN && m > 0) continue;
-#endif
         const float4 fl = S.flow[s][QP[m]];
         const float2 rx = RX[m], ry = RY[m], d = DD[m];
         // project(): D = (M - I) ray + d t,  x - rx = (Dx - rx Dz) / (1 + Dz)
@@ -580,17 +515,6 @@ __global__ void __launch_bounds__(kPixBlock, VBA_K1_MINB) k_vision_stream(
       if (lane == 0) tile_energy[(int64_t)tile_id(ord) * (kPixBlock / 32) + warp] = etile;
     }
   }
-#ifdef VBA_K1_TRACE
-  if (LIN && lane == 0) {
-    atomicAdd(&g_k1_trace[1], (unsigned long long)(clock64() - tk0));
-    atomicAdd(&g_k1_trace[2], (unsigned long long)item);
-  }
-  if (LIN && tid == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    g_k1_end[blockIdx.x] = t;
-  }
-#endif
 }
 
 // Planner helper: number of 64-pixel blocks with any non-zero weight per (tile, edge)
@@ -810,18 +734,7 @@ __device__ __forceinline__ void gdmma(double& c0, double& c1, double a, double b
                : "d"(a), "d"(b));
 }
 
-#ifdef VBA_GRAM_PROF   // tuning builds: per-warp cycles in phase 1 / barrier / phase 2 / barrier
-__device__ unsigned long long g_gram_prof[5];
-extern "C" __attribute__((visibility("default"))) void vba_gram_prof(unsigned long long* out) {
-  cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out, g_gram_prof, sizeof(g_gram_prof));
-  unsigned long long z[5] = {0, 0, 0, 0, 0};
-  cudaMemcpyToSymbol(g_gram_prof, z, sizeof(z));
-}
-#define GPROF(i, v) if ((threadIdx.x & 31) == 0) atomicAdd(&g_gram_prof[i], (unsigned long long)(v))
-#else
 #define GPROF(i, v)
-#endif
 template <int MODE, int GT>
 __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
     const GramTile* __restrict__ gts, const float* __restrict__ disp, const EdgeGeo32* __restrict__ geo,
@@ -960,16 +873,8 @@ __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
 #pragma unroll
   for (int j = 0; j < kGramItems; ++j) gitem(j, T.n0, 0);
   if (tid >= nth - kGramPC) invs[1][tid - (nth - kGramPC)] = pixel_inv(T.n0 + kGramPC + tid - (nth - kGramPC));
-#ifdef VBA_GRAM_PROF
-  long long gt_d = clock64();
-#endif
   for (int c0 = T.n0, cb = 0; c0 < T.n1; c0 += kGramPC, cb ^= 1) {
     __syncthreads();
-#ifdef VBA_GRAM_PROF
-    long long gt_a = clock64();
-    GPROF(3, gt_a - gt_d);
-    GPROF(4, 1);
-#endif
     // C += U^T V (buffer cb) on the fp64 tensor cores, 8 pixel-steps of 4, with the
     // phase-1 items of chunk c + 1 (buffer cb ^ 1) interleaved between the tiles
     const int cn = c0 + kGramPC;
@@ -1018,10 +923,6 @@ __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
       if (more) gitem(j, cn, cb ^ 1);
     // pixel inverses of chunk c + 2 (buffer cb: chunk c's items are done)
     if (tid >= nth - kGramPC) invs[cb][tid - (nth - kGramPC)] = pixel_inv(cn + kGramPC + tid - (nth - kGramPC));
-#ifdef VBA_GRAM_PROF
-    gt_d = clock64();
-    GPROF(2, gt_d - gt_a);
-#endif
   }
   // epilogue: scatter the lower 6x6 blocks (e1 >= e2) and the b row into the output layout
   double* o = out + T.out;
@@ -1085,31 +986,6 @@ void launch_gram(int mode, const GramTile* gt, int ngt, int block, size_t smem, 
   launch_count();
 }
 
-// sum the per-range Gram partials of each source (fixed order)
-__global__ void k_gram_reduce(const int32_t* __restrict__ srcs, const int32_t* __restrict__ g0,
-                              const int32_t* __restrict__ g1, const GramTile* __restrict__ gt,
-                              const int32_t* __restrict__ seb, const int32_t* __restrict__ see,
-                              const int64_t* __restrict__ goff, const double* __restrict__ part,
-                              double* __restrict__ gram) {
-  const int si = blockIdx.x;
-  const int s = srcs[si];
-  const int k = see[s] - seb[s];
-  const int len = k * (k + 1) / 2 * 36 + k * 6;
-  double* o = gram + goff[s];
-  for (int i = threadIdx.x; i < len; i += blockDim.x) {
-    double acc = 0.0;
-    for (int t = g0[s]; t < g1[s]; ++t) acc += part[gt[t].out + i];
-    o[i] = acc;
-  }
-}
-
-void launch_gram_reduce(const int32_t* srcs, int nsrc, const int32_t* g0, const int32_t* g1, const GramTile* gt,
-                        const int32_t* seb, const int32_t* see, const int64_t* goff, const double* part,
-                        double* gram, cudaStream_t st) {
-  if (nsrc <= 0) return;
-  k_gram_reduce<<<nsrc, 256, 0, st>>>(srcs, g0, g1, gt, seb, see, goff, part, gram);
-  launch_count();
-}
 
 // ---------------------------------------------------------------------------
 // fill-in transform (fp64, one CTA per source): K-space Gram -> pose-space blocks
