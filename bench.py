@@ -283,7 +283,7 @@ def main():
     # --- e2e: host buffers -> device, solve, device -> host, through the C ABI
     H = dp.H
     pinned = {k: torch.from_numpy(np.ascontiguousarray(v).reshape(-1)).pin_memory()
-              for k, v in (("state", H.state), ("disp", H.disp), ("tgt", H.tgt), ("w", H.w), ("imu", H.imu),
+              for k, v in (("state", H.state), ("disp64", H.disp64), ("tgt", H.tgt), ("w", H.w), ("imu", H.imu),
                            ("grav", H.grav))}
     h2d = sum(v.numel() * v.element_size() for v in pinned.values())
     d2h = dp.d_state.numel() * 8 + dp.d_disp.numel() * 4

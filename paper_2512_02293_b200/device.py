@@ -463,8 +463,7 @@ class DeviceProblem:
                     dst.copy_(torch.from_numpy(np.ascontiguousarray(a).reshape(-1)).to(dst.dtype), non_blocking=False)
             put(self.d_state.view(-1), H.state)
             put(self.d_ts, H.ts)
-            put(self.d_disp64, H.disp64, pin[2] if pin else None)
-            put(self.d_disp, H.disp)
+            put(self.d_disp64, H.disp64, pin[2] if pin else None)   # the fp32 copy is derived natively
             put(self.d_tgt, H.tgt, pin[0] if pin else None)
             put(self.d_w, H.w, pin[1] if pin else None)
             put(self.d_pix, H.pix)
@@ -635,7 +634,10 @@ class DeviceProblem:
         """Solve a sequence of windows of this problem's topology end to end from host memory.
 
         ``windows``: dicts of (ideally pinned) host tensors in HostLayout order and dtype,
-        keys ``state, disp, tgt, w, imu, grav``.  Window s+1's flow targets and weights
+        keys ``state, disp64`` (fp64 disparities; or ``disp``, fp32), ``tgt, w, imu, grav``.  Keep the
+        solve stream free of torch kernels in the loop: an fp32 ``disp`` needs a widening kernel,
+        which on the legacy default stream serialises the copy stream's uploads with the solve
+        (measured: 23.2 vs 14.8 ms per config-4 window).  Window s+1's flow targets and weights
         (the bulk of the bytes) are uploaded on ``copy_stream`` into a second device set
         while window s is solved (``vba_bind_inputs`` swaps the sets); the small arrays are
         uploaded on the solve stream.  Each window's solved state and disparities are read
@@ -673,8 +675,11 @@ class DeviceProblem:
             st.wait_event(up[b])
             with torch.cuda.stream(st):
                 self.d_state.copy_(win["state"].reshape(self.d_state.shape), non_blocking=True)
-                self.d_disp.copy_(win["disp"].reshape(self.d_disp.shape), non_blocking=True)
-                self.d_disp64.copy_(self.d_disp)        # fp32 window disparities seed the fp64 master
+                if "disp64" in win:   # fp64 master disparities: one DMA (load_state derives the fp32 copy)
+                    self.d_disp64.copy_(win["disp64"].reshape(self.d_disp64.shape), non_blocking=True)
+                else:                 # fp32 window disparities seed the fp64 master
+                    self.d_disp.copy_(win["disp"].reshape(self.d_disp.shape), non_blocking=True)
+                    self.d_disp64.copy_(self.d_disp)
                 self.d_imu.copy_(win["imu"].reshape(-1), non_blocking=True)
                 self.d_grav.copy_(win["grav"].reshape(-1), non_blocking=True)
             rc = self.lib.vba_bind_inputs(self.ctx, self._sptr(), sets[b][0].data_ptr(), sets[b][1].data_ptr(), 1)

@@ -17,7 +17,7 @@ P = pack_graph(make_workload(cfg))
 dp = DeviceProblem(P, {"max_iterations": CONFIGS[cfg].iterations})
 H = dp.H
 pinned = {k: torch.from_numpy(np.ascontiguousarray(v).reshape(-1)).pin_memory()
-          for k, v in (("state", H.state), ("disp", H.disp), ("tgt", H.tgt), ("w", H.w), ("imu", H.imu),
+          for k, v in (("state", H.state), ("disp64", H.disp64), ("tgt", H.tgt), ("w", H.w), ("imu", H.imu),
                        ("grav", H.grav))}
 dp.solve_windows([pinned])
 torch.cuda.synchronize()
