@@ -310,3 +310,159 @@ class SolveReport:
     cost_trajectory: list
     termination: str
     condition_warnings: list = field(default_factory=list)
+
+
+# ---------------------------------------------------------------------------
+# Pose-graph (PGBA) containers: geometry.py:266-341 (SimTransform),
+# residuals.py:144-156 (RelativePoseEdge), loopclosure.py:94-207 (LoopEdge,
+# PoseGraphNode, PoseGraph, CorrectionEntry, LoopCorrection).  Containers only:
+# SimTransform carries the host-side maps the drop-in needs for write-back and
+# the correction message (compose / inverse / pose); the solve itself is on the GPU.
+# ---------------------------------------------------------------------------
+
+@dataclass
+class SimTransform:
+    """Similarity transform x_out = scale * R @ x + t, scale > 0."""
+
+    rotation: Rotation
+    translation: np.ndarray
+    scale: float = 1.0
+
+    def __post_init__(self):
+        self.translation = np.asarray(self.translation, dtype=float).reshape(3)
+        self.scale = float(self.scale)
+        if not self.scale > 0.0:
+            raise ValueError(f"scale must be positive, got {self.scale}")
+
+    @staticmethod
+    def identity():
+        return SimTransform(Rotation.identity(), np.zeros(3), 1.0)
+
+    @staticmethod
+    def from_pose(pose, scale=1.0):
+        return SimTransform(Rotation(pose.rotation.q.copy()), pose.translation.copy(), scale)
+
+    def pose(self):
+        return Pose(Rotation(self.rotation.q.copy()), self.translation.copy())
+
+    def apply(self, x):
+        return self.scale * self.rotation.apply(x) + self.translation
+
+    def compose(self, other):
+        return SimTransform(self.rotation * other.rotation,
+                            self.scale * self.rotation.apply(other.translation) + self.translation,
+                            self.scale * other.scale)
+
+    __mul__ = compose
+
+    def inverse(self):
+        Rinv = self.rotation.inverse()
+        inv_s = 1.0 / self.scale
+        return SimTransform(Rinv, -inv_s * Rinv.apply(self.translation), inv_s)
+
+    def copy(self):
+        return SimTransform(Rotation(self.rotation.q.copy()), self.translation.copy(), self.scale)
+
+
+@dataclass
+class RelativePoseEdge:
+    i: int
+    j: int
+    measurement: SimTransform
+    information: np.ndarray
+
+    def __post_init__(self):
+        self.information = np.asarray(self.information, dtype=float).reshape(7, 7)
+        if np.max(np.abs(self.information - self.information.T)) > 1e-9:
+            raise ValueError("information must be symmetric")
+        if np.linalg.eigvalsh(self.information).min() < -1e-9:
+            raise ValueError("information must be PSD")
+
+
+@dataclass
+class LoopEdge:
+    i: int
+    j: int
+    relative: RelativePoseEdge
+    vision: VisionEdge | None = None
+
+    def __post_init__(self):
+        if not self.i < self.j:
+            raise ValueError("loop endpoints must satisfy i < j")
+        if (self.relative.i, self.relative.j) != (self.i, self.j):
+            raise ValueError("relative edge endpoints must match the loop pair")
+        if self.vision is not None and (self.vision.i, self.vision.j) != (self.i, self.j):
+            raise ValueError("vision edge endpoints must match the loop pair")
+
+
+@dataclass
+class PoseGraphNode:
+    kid: int
+    state: SimTransform
+    pixels: np.ndarray | None = None
+    disparities: np.ndarray | None = None
+    timestamp: float = 0.0
+
+
+@dataclass
+class PoseGraph:
+    nodes: list
+    chain: list
+    loops: list
+    intrinsics: Intrinsics | None = None
+    T_cb: Pose | None = None
+    min_loop_gap: int = 55
+
+    def __post_init__(self):
+        self.nodes = sorted(self.nodes, key=lambda n: n.kid)
+        kids = [n.kid for n in self.nodes]
+        if len(set(kids)) != len(kids):
+            raise ValueError("duplicate pose graph node ids")
+        self._index = {kid: n for n, kid in enumerate(kids)}
+        consecutive = {(kids[n], kids[n + 1]) for n in range(len(kids) - 1)}
+        covered = {(e.i, e.j) for e in self.chain}
+        if self.chain and covered != consecutive:
+            raise ValueError("chain must cover exactly the consecutive keyframe pairs")
+        for loop in self.loops:
+            if loop.i not in self._index or loop.j not in self._index:
+                raise ValueError(f"loop edge ({loop.i},{loop.j}) references unknown keyframe")
+            if loop.j - loop.i < self.min_loop_gap:
+                raise ValueError(f"loop edge ({loop.i},{loop.j}) violates the keyframe gap gate")
+            if loop.vision is not None:
+                if self.intrinsics is None:
+                    raise ValueError("vision loop edges need intrinsics")
+                src = self.node(loop.i)
+                if src.pixels is None or src.disparities is None:
+                    raise ValueError(f"keyframe {loop.i} has no pixel snapshot for its loop edge")
+                if len(src.disparities) != len(loop.vision.pixels):
+                    raise ValueError("loop vision rows must align with the source pixel snapshot")
+
+    def node(self, kid):
+        return self.nodes[self._index[kid]]
+
+    def index_of(self, kid):
+        return self._index[kid]
+
+
+@dataclass
+class CorrectionEntry:
+    kid: int
+    old_pose: Pose
+    new_pose: Pose
+    scale_change: float = 1.0
+
+    def __post_init__(self):
+        self.scale_change = float(self.scale_change)
+        if not self.scale_change > 0.0:
+            raise ValueError("scale change must be positive")
+
+    def delta(self):
+        new = SimTransform(Rotation(self.new_pose.rotation.q.copy()), self.new_pose.translation.copy(),
+                           self.scale_change)
+        return new * SimTransform.from_pose(self.old_pose).inverse()
+
+
+@dataclass
+class LoopCorrection:
+    entries: dict
+    timestamp: float = 0.0

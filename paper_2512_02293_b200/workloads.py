@@ -383,3 +383,76 @@ def workload_stats(graph) -> dict:
     N = len(graph.keyframes[0].disparities) if graph.keyframes else 0
     rows = sum(len(e.pixels) for e in graph.vision_edges)
     return {"n_kf": len(graph.keyframes), "n_edges": E, "px_per_kf": N, "edge_px": rows}
+
+
+# --------------------------------------------------------------------------
+# Pose-graph (PGBA) stress window: SURVEY.md §8(f)#1.  Not a BASELINE config (the
+# reference publishes none for PGBA); shaped like the paper's loop closure over a
+# long drifting trajectory: K keyframes on 1.25 laps of a 2 m circle (revisits after
+# one lap), Sim(3) odometry with a creeping scale drift as the chain, and loop edges
+# between revisiting keyframes carrying dense 48x64 correspondences (BASELINE
+# intrinsics) plus the exact relative pose.
+# --------------------------------------------------------------------------
+
+CHAIN_INFO = np.diag([4e4] * 3 + [1e4] * 3 + [100.0])   # test_loopclosure.py:38
+
+
+def _sim3(R, t, s=1.0):
+    return T.SimTransform(T.Rotation.from_matrix(R), np.asarray(t, float), s)
+
+
+def make_pgba_workload(n_nodes=256, n_loops=8, grid=(48, 64), seed=2024, drift=1.05, sigma_px=0.5):
+    """Seeded PoseGraph (paper_2512_02293_b200.types) + the true node states."""
+    rng = np.random.default_rng(seed)
+    rows, cols = grid
+    lap = int(round(n_nodes / 1.25))
+    ang = 2.0 * np.pi * np.arange(n_nodes) / lap
+    gt = []
+    for a in ang:
+        p = np.array([2.0 * np.cos(a), 2.0 * np.sin(a), 0.1 * np.sin(3.0 * a)])
+        # camera looks outward from the circle (z axis radial), yaw follows the angle
+        Rz = _rz(a)
+        R = Rz @ np.array([[0.0, 0.0, 1.0], [1.0, 0.0, 0.0], [0.0, 1.0, 0.0]])
+        gt.append(_sim3(R, p))
+    sig = drift ** (1.0 / (n_nodes - 1))
+    odo = [gt[0].copy()]
+    chain = []
+    for k in range(n_nodes - 1):
+        rel = gt[k + 1] * gt[k].inverse()
+        noise = T.Rotation.exp(rng.normal(0.0, 2e-4, 3))
+        meas = T.SimTransform(rel.rotation * noise, rel.translation + rng.normal(0.0, 5e-4, 3), sig)
+        odo.append(meas * odo[k])
+        chain.append(T.RelativePoseEdge(k, k + 1, meas, CHAIN_INFO))
+    fx = fy = FX_FULL / 8.0
+    cx, cy = 32.0, 24.0
+    intr = T.Intrinsics(fx, fy, cx, cy, max(cols, 33), max(rows, 25))
+    vv, uu = np.meshgrid(np.arange(rows, dtype=float), np.arange(cols, dtype=float), indexing="ij")
+    pix = np.stack([uu.ravel(), vv.ravel()], 1)
+    N = len(pix)
+    ray = np.stack([(pix[:, 0] - cx) / fx, (pix[:, 1] - cy) / fy, np.ones(N)], 1)
+    # loop pairs: j revisits i one lap later
+    cand = np.arange(0, n_nodes - lap)
+    srcs = np.sort(rng.choice(cand, size=min(n_loops, len(cand)), replace=False))
+    nodes = [T.PoseGraphNode(k, odo[k].copy(), timestamp=float(k) * KF_DT) for k in range(n_nodes)]
+    loops = []
+    for i in srcs:
+        j = int(i + lap)
+        depth = rng.uniform(0.5, 5.0, N).astype(np.float32).astype(float)
+        d_true = (1.0 / depth).astype(np.float32).astype(float)
+        Xw = gt[i].apply(ray / d_true[:, None])
+        Xj = gt[j].inverse().apply(Xw)
+        z = Xj[:, 2]
+        zs = np.where(z > 0.05, z, 1.0)
+        uv = np.stack([fx * Xj[:, 0] / zs + cx, fy * Xj[:, 1] / zs + cy], 1)
+        ok = (z > 0.05) & (uv[:, 0] >= 0) & (uv[:, 0] <= cols - 1) & (uv[:, 1] >= 0) & (uv[:, 1] <= rows - 1)
+        tgt = np.where(ok[:, None], uv + sigma_px * rng.standard_normal((N, 2)), pix)
+        w = rng.uniform(0.0, 1.0, (N, 2))
+        w[~ok] = 0.0
+        nodes[i].pixels = pix.copy()
+        nodes[i].disparities = (d_true * rng.uniform(0.97, 1.03, N)).astype(np.float32).astype(float)
+        rel = T.RelativePoseEdge(int(i), j, gt[j] * gt[i].inverse(), np.eye(7) * 1e6)
+        vis = T.VisionEdge(int(i), j, pix.copy(), tgt.astype(np.float32).astype(float),
+                           w.astype(np.float32).astype(float))
+        loops.append(T.LoopEdge(int(i), j, rel, vis))
+    graph = T.PoseGraph(nodes, chain, loops, intr, None, min_loop_gap=55)
+    return graph, gt

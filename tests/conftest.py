@@ -122,3 +122,26 @@ def cuda_ok():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return True
+
+
+def pgba_golden_names():
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN_DIR, "pgba", "*.npz")))
+
+
+def load_pgba_golden(name):
+    """tests/golden/pgba/<name>.npz (make_pgba_golden.py): packed inputs (or the stress
+    generator's, regenerated and hash-checked), meta and the reference's outputs."""
+    z = np.load(os.path.join(GOLDEN_DIR, "pgba", name + ".npz"), allow_pickle=False)
+    out = {k: z[k] for k in z.files}
+    meta = json.loads(str(out.pop("meta")))
+    meta["opts"]["frozen_keyframes"] = tuple(meta["opts"]["frozen_keyframes"])
+    P = {k[3:]: v for k, v in out.items() if k.startswith("in_")}
+    if P:
+        P["has_Tcb"] = bool(P["has_Tcb"])
+        P["n_loops"] = int(P["n_loops"])
+    else:
+        from paper_2512_02293_b200.pgba import pack_pose_graph
+        from paper_2512_02293_b200.workloads import make_pgba_workload
+        P = pack_pose_graph(make_pgba_workload()[0])
+        assert packed_hash(P) == meta["input_hash"], "PGBA stress generator drifted from the golden's inputs"
+    return P, {k: v for k, v in out.items() if not k.startswith("in_")}, meta
