@@ -244,6 +244,58 @@ VBA_API int vba_preintegrate(const double* ts, const double* gyro, const double*
 VBA_API int vba_preint_factor_records(const double* rec, const double* bias, int32_t n_pairs, double* imu,
                                       void* stream);
 
+/* ------------------------------------------------------------------------
+ * Sim(3) pose-graph BA (PGBA), replacing vislam.loopclosure.solve_pgba
+ * (loopclosure.py:502-574) and its callees: total_pg_energy (:378-390),
+ * _linearize_pg (:425-475), sim3_vision_residual (:225-307),
+ * relative_pose_residual (residuals.py:364-380), _pg_apply (:489-499), with the
+ * shared damped Schur step solver._solve_step (loopclosure.py:27,534).
+ * Nodes are sorted by kid; node 0 is the gauge.  fp64 throughout.
+ * ------------------------------------------------------------------------ */
+#define VBA_E_NONFINITE 6  /* non-finite initial energy -> RuntimeError (loopclosure.py:520-521) */
+#define VBA_PG_REL_REC 64  /* relative edge record: measurement q wxyz (4), t (3), scale (1),
+                              information 7x7 row-major (49), padding */
+
+typedef struct vba_pg_problem {
+  int32_t n_nodes;        /* K */
+  int32_t n_vis;          /* V loop edges with dense correspondences (sorted by source node) */
+  int32_t n_rel;          /* R relative edges: loops without vision, then the chain */
+  int32_t has_Tcb;
+  int64_t n_disp;         /* disparity variables: the pixels of vision-loop source nodes */
+  int64_t n_rows;         /* loop-edge rows (= the source's pixels, per edge) */
+  double fx, fy, cx, cy;
+  double Tcb[7];
+  /* device arrays (caller-owned) */
+  double* state;          /* [K,8]: q wxyz, t, scale -- read at create, written by vba_pg_download */
+  double* disp;           /* [n_disp] -- read at create, written by vba_pg_download */
+  const double* pix;      /* [n_disp,2] source pixel coordinates */
+  const double* tgt;      /* [n_rows,2] loop correspondences u* (in the target frame) */
+  const double* wts;      /* [n_rows,2] confidence weights */
+  const double* rel;      /* [R, VBA_PG_REL_REC] */
+  /* host topology (read in vba_pg_create only) */
+  const int64_t* h_doff;  /* [K+1] disparity offsets (0 pixels for non-source nodes) */
+  const int32_t* h_npix;  /* [K] */
+  const int32_t* h_vis_i; /* [V] source node */
+  const int32_t* h_vis_j; /* [V] target node */
+  const int64_t* h_voff;  /* [V+1] row offsets */
+  const int32_t* h_rel_i; /* [R] */
+  const int32_t* h_rel_j; /* [R] */
+} vba_pg_problem;
+
+VBA_API int vba_pg_create(void** ctx, const vba_pg_problem* prob, const vba_options* opts, void* stream);
+VBA_API int vba_pg_destroy(void* ctx);
+VBA_API int vba_pg_energy(void* ctx, void* stream, double* out_total);                 /* total_pg_energy */
+VBA_API int vba_pg_linearize(void* ctx, void* stream);                                 /* _linearize_pg */
+/* reference-layout normal equations (H_pp [7K,7K], g_p [7K], H_pd [7K, n_disp] row-major,
+ * H_dd/g_d [n_disp]) of the last linearisation; device pointers, any may be NULL */
+VBA_API int vba_pg_export_normal_eq(void* ctx, void* stream, double* H_pp, double* g_p, double* H_pd,
+                                    double* H_dd, double* g_d);
+VBA_API int vba_pg_solve_step(void* ctx, void* stream, double lam, int32_t use_schur);  /* _solve_step */
+VBA_API int vba_pg_export_step(void* ctx, void* stream, double* dx_full, double* dx_d);
+VBA_API int vba_pg_solve(void* ctx, void* stream, vba_report* report, double* cost_trajectory,
+                         int32_t traj_capacity);                                         /* solve_pgba */
+VBA_API int vba_pg_download(void* ctx, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

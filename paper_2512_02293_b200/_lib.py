@@ -12,7 +12,8 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("VBA_LIB") or os.path.join(HERE, "_vba.so")   # VBA_LIB: tuning builds (tools/)
 
-VBA_OK, VBA_E_INVALID, VBA_E_CUDA, VBA_E_NOT_SPD, VBA_E_COV, VBA_E_UNSUPPORTED = range(6)
+VBA_OK, VBA_E_INVALID, VBA_E_CUDA, VBA_E_NOT_SPD, VBA_E_COV, VBA_E_UNSUPPORTED, VBA_E_NONFINITE = range(7)
+PG_REL_REC = 64
 PIX_GRID, PIX_KF, PIX_EDGE = 0, 1, 2
 IMU_REC = 180
 PREINT_REC = 281
@@ -23,7 +24,9 @@ EXPORTED = ("vba_last_error", "vba_version", "vba_create", "vba_destroy", "vba_s
             "vba_trial", "vba_solve", "vba_download", "vba_launch_count", "vba_stage_times",
             "vba_load_state", "vba_bind_inputs", "vba_set_profiling", "vba_stats", "vba_spd_solve", "vba_solve_times",
             "vba_preintegrate", "vba_preint_scratch_bytes",
-            "vba_preint_factor_records")
+            "vba_preint_factor_records",
+            "vba_pg_create", "vba_pg_destroy", "vba_pg_energy", "vba_pg_linearize", "vba_pg_export_normal_eq",
+            "vba_pg_solve_step", "vba_pg_export_step", "vba_pg_solve", "vba_pg_download")
 
 
 class VbaProblem(C.Structure):
@@ -40,6 +43,19 @@ class VbaProblem(C.Structure):
         ("h_eoff", C.c_void_p), ("h_imu_i", C.c_void_p), ("h_imu_j", C.c_void_p), ("h_frozen", C.c_void_p),
         ("disp64", C.c_void_p),
         ("shard_world", C.c_int32), ("shard_rank", C.c_int32), ("h_shard_kbounds", C.c_void_p),
+    ]
+
+
+class VbaPgProblem(C.Structure):
+    _fields_ = [
+        ("n_nodes", C.c_int32), ("n_vis", C.c_int32), ("n_rel", C.c_int32), ("has_Tcb", C.c_int32),
+        ("n_disp", C.c_int64), ("n_rows", C.c_int64),
+        ("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+        ("Tcb", C.c_double * 7),
+        ("state", C.c_void_p), ("disp", C.c_void_p), ("pix", C.c_void_p), ("tgt", C.c_void_p),
+        ("wts", C.c_void_p), ("rel", C.c_void_p),
+        ("h_doff", C.c_void_p), ("h_npix", C.c_void_p), ("h_vis_i", C.c_void_p), ("h_vis_j", C.c_void_p),
+        ("h_voff", C.c_void_p), ("h_rel_i", C.c_void_p), ("h_rel_j", C.c_void_p),
     ]
 
 
@@ -119,6 +135,15 @@ def load(path: str | None = None):
         "vba_preintegrate": ([v, v, v, C.c_int64, v, C.c_int32, v, v, v, v, v], C.c_int),
         "vba_preint_scratch_bytes": ([C.c_int64], C.c_int64),
         "vba_preint_factor_records": ([v, v, C.c_int32, v, v], C.c_int),
+        "vba_pg_create": ([C.POINTER(C.c_void_p), C.POINTER(VbaPgProblem), C.POINTER(VbaOptions), v], C.c_int),
+        "vba_pg_destroy": ([v], C.c_int),
+        "vba_pg_energy": ([v, v, C.POINTER(C.c_double)], C.c_int),
+        "vba_pg_linearize": ([v, v], C.c_int),
+        "vba_pg_export_normal_eq": ([v, v, v, v, v, v, v], C.c_int),
+        "vba_pg_solve_step": ([v, v, C.c_double, C.c_int32], C.c_int),
+        "vba_pg_export_step": ([v, v, v, v], C.c_int),
+        "vba_pg_solve": ([v, v, C.POINTER(VbaReport), C.POINTER(C.c_double), C.c_int32], C.c_int),
+        "vba_pg_download": ([v, v], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

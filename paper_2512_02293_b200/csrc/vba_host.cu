@@ -19,10 +19,12 @@
 #include <vector>
 
 #include "vba_internal.cuh"
+#include "vba_plan.h"
 
 namespace vba {
 
 static thread_local std::string g_err;
+void vba_set_error_string(const char* msg) { g_err = msg; }
 static void set_err(const char* fmt, ...) {
   char buf[512];
   va_list ap;
@@ -108,15 +110,8 @@ struct Ctx {
   double *d_L = nullptr;
   int* d_imu_status = nullptr;
   // reduced system
-  struct Plan {
-    int nbr = 0, nseg = 0;
-    int32_t *bptr = nullptr, *bnff = nullptr, *roff = nullptr, *rdim = nullptr;
-    Contrib* cs = nullptr;
-    int32_t *sptr = nullptr, *soff = nullptr;   // soff: [nseg offsets][nseg dims]
-    Vec* vs = nullptr;
-    int32_t* blist = nullptr;                    // lower blocks with contributions (+ diagonal)
-    int nblist = 0;
-  } red, exp;
+  using Plan = BlkPlan;
+  Plan red, exp;
   bool exp_built = false;
   double *d_H = nullptr, *d_rhs = nullptr, *d_x = nullptr, *d_Ld = nullptr, *d_dx = nullptr;
   double* d_cpart = nullptr;       // Cholesky backward-substitution partials
@@ -218,84 +213,10 @@ static void make_extr(const vba_problem& P, Extr& x) {
     x.c2[a] = x.RbcT[a * 3 + 0] * x.pbc[0] + x.RbcT[a * 3 + 1] * x.pbc[1] + x.RbcT[a * 3 + 2] * x.pbc[2];
 }
 
-// ---------------------------------------------------------------------------
-// contribution-list planner for the block matrix (reduced or export layout)
-// ---------------------------------------------------------------------------
-struct BlkBuilder {
-  int nbr;
-  std::vector<std::vector<Contrib>> ff, fl;   // per lower block: H_ff-type, fill-type
-  std::vector<std::vector<Vec>> seg;
-  explicit BlkBuilder(int n) : nbr(n), ff((size_t)n * (n + 1) / 2), fl((size_t)n * (n + 1) / 2), seg(n) {}
-  static size_t id(int a, int b) { return (size_t)a * (a + 1) / 2 + b; }
-  // add matrix M (rows x cols, row-major ld) as block (a,b) of the symmetric matrix
-  void add(int a, int b, int64_t off, int ld, int rows, int cols, int sign, bool fill) {
-    if (a < 0 || b < 0) return;
-    auto& L = [&]() -> std::vector<std::vector<Contrib>>& { return fill ? fl : ff; }();
-    Contrib c{};
-    c.ld = ld;
-    c.sign = (int8_t)sign;
-    if (a > b) {
-      c.off = off; c.rows = (int16_t)rows; c.cols = (int16_t)cols; c.trans = 0;
-      L[id(a, b)].push_back(c);
-    } else if (a < b) {
-      c.off = off; c.rows = (int16_t)cols; c.cols = (int16_t)rows; c.trans = 1;
-      L[id(b, a)].push_back(c);
-    } else {
-      c.off = off; c.rows = (int16_t)rows; c.cols = (int16_t)cols; c.trans = 0;
-      L[id(a, a)].push_back(c);
-    }
-  }
-  // off-diagonal pair block that maps onto a diagonal block: add M and M^T
-  void add_both(int a, int b, int64_t off, int ld, int rows, int cols, int sign, bool fill) {
-    add(a, b, off, ld, rows, cols, sign, fill);
-    if (a == b && a >= 0) {
-      auto& L = fill ? fl : ff;
-      Contrib c{};
-      c.off = off; c.ld = ld; c.rows = (int16_t)cols; c.cols = (int16_t)rows; c.trans = 1; c.sign = (int8_t)sign;
-      L[id(a, a)].push_back(c);
-    }
-  }
-  void addv(int a, int64_t off, int len, int sign) {
-    if (a < 0) return;
-    seg[a].push_back(Vec{off, len, sign});
-  }
-};
-
 static int upload_plan(Ctx* c, BlkBuilder& B, const std::vector<int32_t>& roff, const std::vector<int32_t>& rdim,
                        Ctx::Plan& pl, cudaStream_t st) {
-  pl.nbr = B.nbr;
-  pl.nseg = B.nbr;
-  std::vector<int32_t> bptr(1, 0), bnff;
-  std::vector<Contrib> cs;
-  for (size_t i = 0; i < B.ff.size(); ++i) {
-    for (auto& x : B.ff[i]) cs.push_back(x);
-    bnff.push_back((int32_t)B.ff[i].size());
-    for (auto& x : B.fl[i]) cs.push_back(x);
-    bptr.push_back((int32_t)cs.size());
-  }
-  std::vector<int32_t> sptr(1, 0), soff;
-  std::vector<Vec> vs;
-  for (int a = 0; a < B.nbr; ++a) {
-    for (auto& v : B.seg[a]) vs.push_back(v);
-    sptr.push_back((int32_t)vs.size());
-  }
-  soff = roff;
-  soff.insert(soff.end(), rdim.begin(), rdim.end());
-  std::vector<int32_t> blist;
-  {
-    int64_t id = 0;
-    for (int a = 0; a < B.nbr; ++a)
-      for (int b = 0; b <= a; ++b, ++id)
-        if (a == b || bptr[id + 1] > bptr[id]) blist.push_back((int32_t)id);
-  }
-  pl.nblist = (int)blist.size();
-  int rc;
-  if ((rc = dupload(c, &pl.blist, blist, st))) return rc;
-  if ((rc = dupload(c, &pl.bptr, bptr, st)) || (rc = dupload(c, &pl.bnff, bnff, st)) ||
-      (rc = dupload(c, &pl.cs, cs, st)) || (rc = dupload(c, &pl.roff, roff, st)) ||
-      (rc = dupload(c, &pl.rdim, rdim, st)) || (rc = dupload(c, &pl.sptr, sptr, st)) ||
-      (rc = dupload(c, &pl.vs, vs, st)) || (rc = dupload(c, &pl.soff, soff, st)))
-    return rc;
+  const cudaError_t e = upload_blk_plan(c->allocs, B, roff, rdim, pl, st);
+  if (e != cudaSuccess) { set_err("plan upload: %s", cudaGetErrorString(e)); return VBA_E_CUDA; }
   return VBA_OK;
 }
 

@@ -383,6 +383,7 @@ void launch_preintegrate(const double* ts, const double* gyro, const double* acc
                          int F, const double* bias, const double* noise, double* scratch, double* out, int* status,
                          cudaStream_t st);
 void launch_count();   // instrumentation hook
+void vba_set_error_string(const char* msg);   // vba_last_error() of every C entry point
 int64_t launch_total();
 
 }  // namespace vba

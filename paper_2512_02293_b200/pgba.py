@@ -25,7 +25,7 @@ from . import _lib as L
 from .types import SolveOptions, SolveReport
 
 SIM3_DOF = 7
-PG_REL_REC = 64      # doubles per relative edge record (VBA_PG_REL_REC)
+PG_REL_REC = L.PG_REL_REC   # doubles per relative edge record (VBA_PG_REL_REC)
 
 
 def pack_pose_graph(graph) -> dict:
@@ -87,6 +87,22 @@ def pack_pose_graph(graph) -> dict:
     return P
 
 
+def _sorted_by_source(P):
+    """Loop vision edges stably sorted by source node (the device plans per source)."""
+    vi = np.asarray(P["vi"], np.int64)
+    order = np.argsort(vi, kind="stable")
+    if np.array_equal(order, np.arange(len(vi))):
+        return P
+    Q = dict(P)
+    eo = np.asarray(P["veoff"], np.int64)
+    segs = [(eo[v], eo[v + 1]) for v in order]
+    Q["vi"], Q["vj"] = vi[order], np.asarray(P["vj"])[order]
+    Q["veoff"] = np.concatenate([[0], np.cumsum([b - a for a, b in segs])]).astype(np.int64)
+    for k in ("vpix", "vtgt", "vw"):
+        Q[k] = np.concatenate([P[k][a:b] for a, b in segs])
+    return Q
+
+
 class DevicePoseGraph:
     """One pose graph resident on the current CUDA device (vba_pg_* C ABI)."""
 
@@ -100,36 +116,20 @@ class DevicePoseGraph:
         dev = torch.device("cuda", torch.cuda.current_device())
         self.device = dev
         self.stream = stream if stream is not None else torch.cuda.current_stream(dev)
+        P = _sorted_by_source(P)
+        self.P = P
         K, V, R = len(P["kid"]), len(P["vi"]), len(P["ri"])
         nd = int(P["doff"][-1])
+        nr = int(P["veoff"][-1])
         self.K, self.V, self.R, self.n_disp = K, V, R, nd
-        # per-vision-edge rows padded to 4 pixels (aligned pixel pairs), weight 0 in the padding
-        rows = np.diff(np.asarray(P["veoff"], np.int64))
-        rpad = (rows + 3) // 4 * 4
-        self.voff = np.concatenate([[0], np.cumsum(rpad)]).astype(np.int64)
-        nrp = int(self.voff[-1])
         doff = np.asarray(P["doff"], np.int64)
-        npix = np.diff(doff)
-        dpad = (npix + 3) // 4 * 4
-        self.doff_pad = np.concatenate([[0], np.cumsum(dpad)]).astype(np.int64)
-        ndp = int(self.doff_pad[-1])
-        kk = np.repeat(np.arange(K), npix)
-        self.dpos = (np.arange(nd) - doff[kk] + self.doff_pad[kk]).astype(np.int64)
-        disp = np.ones(ndp)
-        disp[self.dpos] = P["disp"]
-        pix = np.zeros((ndp, 2), np.float32)
-        pix[self.dpos] = P["pix"]
-        flow = np.zeros((nrp, 2), np.float32)
-        w = np.zeros((nrp, 2), np.float32)
+        npix = np.diff(doff).astype(np.int32)
         for v in range(V):
             r0, r1 = int(P["veoff"][v]), int(P["veoff"][v + 1])
-            o = int(self.voff[v])
-            # targets relative to the source pixel (fp64 difference, one fp32 rounding), as VI-BA
-            flow[o:o + r1 - r0] = P["vtgt"][r0:r1] - P["vpix"][r0:r1]
-            w[o:o + r1 - r0] = P["vw"][r0:r1]
-            if not np.array_equal(P["vpix"][r0:r1], P["pix"][doff[P["vi"][v]]:doff[P["vi"][v] + 1]]):
+            i = int(P["vi"][v])
+            if not np.array_equal(P["vpix"][r0:r1], P["pix"][doff[i]:doff[i + 1]]):
                 raise ValueError("loop vision rows must align with the source pixel snapshot")
-        if len(w) and w.min() < 0:
+        if len(P["vw"]) and np.min(P["vw"]) < 0:
             raise ValueError("weights must be non-negative")
         state = np.concatenate([P["sq"], P["st"], np.asarray(P["ss"])[:, None]], axis=1).reshape(K, 8)
         rel = np.zeros((R, PG_REL_REC))
@@ -138,26 +138,26 @@ class DevicePoseGraph:
             rel[:, 4:7] = P["rt"]
             rel[:, 7] = P["rs"]
             rel[:, 8:57] = np.asarray(P["rinfo"]).reshape(R, 49)
-        t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to(dev, dtype=dt)  # noqa: E731
-        self.d_state = t(state, torch.float64)
-        self.d_disp = t(disp, torch.float64)
-        self.d_pix = t(pix.reshape(-1), torch.float32)
-        self.d_flow = t(flow.reshape(-1), torch.float32)
-        self.d_w = t(w.reshape(-1), torch.float32)
-        self.d_rel = t(rel.reshape(-1), torch.float64)
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64).reshape(-1)).to(dev)  # noqa: E731
+        self.d_state = t(state)
+        self.d_disp = t(P["disp"]) if nd else torch.zeros(1, dtype=torch.float64, device=dev)
+        self.d_pix = t(P["pix"]) if nd else torch.zeros(2, dtype=torch.float64, device=dev)
+        self.d_tgt = t(P["vtgt"]) if nr else torch.zeros(2, dtype=torch.float64, device=dev)
+        self.d_w = t(P["vw"]) if nr else torch.zeros(2, dtype=torch.float64, device=dev)
+        self.d_rel = t(rel) if R else torch.zeros(PG_REL_REC, dtype=torch.float64, device=dev)
         self._h = [np.ascontiguousarray(a) for a in (
-            self.doff_pad, np.asarray(P["vi"], np.int32), np.asarray(P["vj"], np.int32), self.voff[:-1].copy(),
-            np.asarray(P["ri"], np.int32), np.asarray(P["rj"], np.int32), npix.astype(np.int32))]
+            doff, npix, np.asarray(P["vi"], np.int32), np.asarray(P["vj"], np.int32),
+            np.asarray(P["veoff"], np.int64), np.asarray(P["ri"], np.int32), np.asarray(P["rj"], np.int32))]
         p = L.VbaPgProblem()
         p.n_nodes, p.n_vis, p.n_rel = K, V, R
-        p.n_disp_pad, p.n_rows_pad = ndp, nrp
+        p.n_disp, p.n_rows = nd, nr
         p.fx, p.fy, p.cx, p.cy = (float(x) for x in P["intr"])
         p.has_Tcb = int(bool(P["has_Tcb"]))
         for k in range(7):
             p.Tcb[k] = float(P["Tcb"][k])
-        p.state, p.disp, p.pix, p.flow, p.wts, p.rel = (x.data_ptr() for x in (
-            self.d_state, self.d_disp, self.d_pix, self.d_flow, self.d_w, self.d_rel))
-        (p.h_doff, p.h_vis_i, p.h_vis_j, p.h_voff, p.h_rel_i, p.h_rel_j, p.h_npix) = (a.ctypes.data for a in self._h)
+        p.state, p.disp, p.pix, p.tgt, p.wts, p.rel = (x.data_ptr() for x in (
+            self.d_state, self.d_disp, self.d_pix, self.d_tgt, self.d_w, self.d_rel))
+        (p.h_doff, p.h_npix, p.h_vis_i, p.h_vis_j, p.h_voff, p.h_rel_i, p.h_rel_j) = (a.ctypes.data for a in self._h)
         o = L.VbaOptions()
         o.max_iterations = int(self.opts.get("max_iterations", 10))
         o.damping = float(self.opts.get("damping", 1e-4))
@@ -244,7 +244,7 @@ class DevicePoseGraph:
         L.check(self.lib.vba_pg_download(self.ctx, self._sptr()))
         self.stream.synchronize()
         s = self.d_state.cpu().numpy().reshape(self.K, 8)
-        d = self.d_disp.cpu().numpy()[self.dpos]
+        d = self.d_disp.cpu().numpy()[:self.n_disp]
         return s, d
 
 

@@ -145,3 +145,33 @@ def load_pgba_golden(name):
         P = pack_pose_graph(make_pgba_workload()[0])
         assert packed_hash(P) == meta["input_hash"], "PGBA stress generator drifted from the golden's inputs"
     return P, {k: v for k, v in out.items() if not k.startswith("in_")}, meta
+
+
+def pose_graph_from_packed(P):
+    """paper_2512_02293_b200.types PoseGraph from a packed pose graph (pack_pose_graph order:
+    relative edges = loops without vision, then the chain)."""
+    from paper_2512_02293_b200 import types as T
+    K = len(P["kid"])
+    kid = [int(k) for k in P["kid"]]
+    S = lambda q, t, s: T.SimTransform(T.Rotation(np.array(q)), np.array(t), float(s))  # noqa: E731
+    nodes = []
+    for n in range(K):
+        d0, d1 = int(P["doff"][n]), int(P["doff"][n + 1])
+        nodes.append(T.PoseGraphNode(kid[n], S(P["sq"][n], P["st"][n], P["ss"][n]),
+                                     P["pix"][d0:d1].copy() if d1 > d0 else None,
+                                     P["disp"][d0:d1].copy() if d1 > d0 else None, float(P["ts"][n])))
+    rel = [T.RelativePoseEdge(kid[P["ri"][r]], kid[P["rj"][r]], S(P["rq"][r], P["rt"][r], P["rs"][r]), P["rinfo"][r])
+           for r in range(len(P["ri"]))]
+    V = len(P["vi"])
+    n_rel_loops = int(P["n_loops"]) - V
+    loops = [T.LoopEdge(e.i, e.j, e) for e in rel[:n_rel_loops]]
+    for v in range(V):
+        i, j = kid[P["vi"][v]], kid[P["vj"][v]]
+        r0, r1 = int(P["veoff"][v]), int(P["veoff"][v + 1])
+        vis = T.VisionEdge(i, j, P["vpix"][r0:r1], P["vtgt"][r0:r1], P["vw"][r0:r1])
+        loops.append(T.LoopEdge(i, j, T.RelativePoseEdge(i, j, T.SimTransform.identity(), np.eye(7)), vis))
+    fx, fy, cx, cy = P["intr"]
+    intr = T.Intrinsics(fx, fy, cx, cy, int(max(640, 2 * cx + 1)), int(max(480, 2 * cy + 1))) if V else None
+    Tcb = T.Pose(T.Rotation(P["Tcb"][:4]), P["Tcb"][4:7]) if bool(P["has_Tcb"]) else None
+    gap = min([lp.j - lp.i for lp in loops] + [55])
+    return T.PoseGraph(nodes, rel[n_rel_loops:], loops, intr, Tcb, min_loop_gap=gap)

@@ -1,0 +1,113 @@
+"""GPU parity of the Sim(3) pose-graph BA (csrc/vba_pgba.cu) against the reference's
+vislam.loopclosure outputs (tests/golden/pgba, make_pgba_golden.py).
+
+The pose-graph path is fp64 end to end (its factors are few: a handful of dense loop edges
+and one relative factor per chain link), so it is graded at fp64 tolerances: energies and
+normal equations 1e-10 relative, the Schur step 1e-8, full solves with identical
+iterations / termination and costs within 1e-9.  The reference's own PGBA contract
+(test_loopclosure.py:407-540) runs through the drop-in ``paper_2512_02293_b200.pgba.solve_pgba``.
+"""
+import copy
+
+import numpy as np
+import pytest
+
+from conftest import load_pgba_golden, pgba_golden_names, pose_graph_from_packed
+
+pytestmark = pytest.mark.gpu
+NAMES = pgba_golden_names()
+
+
+def rel(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    s = max(np.abs(b).max(initial=0.0), 1e-300)
+    return float(np.abs(a - b).max(initial=0.0) / s)
+
+
+def _dp(P, meta):
+    from paper_2512_02293_b200.pgba import DevicePoseGraph
+    return DevicePoseGraph(P, meta["opts"])
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_energy_and_linearize(name, cuda_ok):
+    P, out, meta = load_pgba_golden(name)
+    dp = _dp(P, meta)
+    e = dp.energy()
+    ref = float(out["energy"])
+    assert abs(e - ref) <= 1e-10 * max(ref, 1.0), (e, ref)
+    dp.linearize()
+    H_pp, H_pd, H_dd, g_p, g_d = dp.export_normal_eq(hpd_cols=out.get("H_pd_cols"))
+    errs = {"H_pp": rel(H_pp, out["H_pp"]), "g_p": rel(g_p, out["g_p"])}
+    if "H_pd" in out:
+        errs.update(H_pd=rel(H_pd, out["H_pd"]), H_dd=rel(H_dd, out["H_dd"]), g_d=rel(g_d, out["g_d"]))
+    print(name, {k: f"{v:.1e}" for k, v in errs.items()})
+    for k, v in errs.items():
+        assert v < 1e-10, (k, v)
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_step(name, cuda_ok):
+    P, out, meta = load_pgba_golden(name)
+    dp = _dp(P, meta)
+    dp.linearize()
+    dx, dxd = dp.solve_step(meta["opts"]["damping"])
+    ex, ed = rel(dx, out["dx"]), (rel(dxd, out["dxd"]) if len(dxd) else 0.0)
+    print(f"{name}: dx {ex:.1e} dx_d {ed:.1e}")
+    assert ex < 1e-8 and ed < 1e-8
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_solve(name, cuda_ok):
+    P, out, meta = load_pgba_golden(name)
+    dp = _dp(copy.deepcopy(P), meta)
+    rep = dp.solve()
+    ref = meta["report"]
+    c, cr = np.array(rep["cost_trajectory"]), np.array(ref["cost_trajectory"])
+    print(f"{name}: {rep['iterations']} it {rep['termination']} / ref {ref['iterations']} {ref['termination']}; "
+          f"costs {c} / {cr}")
+    assert rep["iterations"] == ref["iterations"] and rep["termination"] == ref["termination"]
+    assert len(c) == len(cr) and np.all(np.abs(c - cr) <= 1e-9 * np.maximum(cr, 1e-6))
+    s, d = dp.download()
+    assert np.abs(s[:, 4:7] - out["final_st"]).max() < 1e-8
+    assert np.abs(s[:, 7] - out["final_ss"]).max() < 1e-8
+    if len(d):
+        assert np.abs(d - out["final_disp"]).max() < 1e-8 * np.abs(out["final_disp"]).max()
+
+
+def test_dropin_contract(cuda_ok):
+    """test_loopclosure.py:458-508 through the drop-in: the scale drift is closed, the gauge
+    state is bit-identical, the correction reproduces the new poses."""
+    from paper_2512_02293_b200.pgba import solve_pgba
+    from paper_2512_02293_b200.types import SimTransform, SolveOptions
+    P, out, meta = load_pgba_golden("circle_rel")
+    g = pose_graph_from_packed(P)
+    q0 = g.nodes[0].state.rotation.q.copy()
+    t0 = g.nodes[0].state.translation.copy()
+    report, corr = solve_pgba(g, SolveOptions(max_iterations=30))
+    assert abs(g.nodes[60].state.scale - 1.0) <= 0.005
+    assert all(b < a for a, b in zip(report.cost_trajectory, report.cost_trajectory[1:]))
+    assert np.array_equal(g.nodes[0].state.rotation.q, q0) and np.array_equal(g.nodes[0].state.translation, t0)
+    assert set(corr.entries) == {n.kid for n in g.nodes}
+    for e in corr.entries.values():
+        redone = e.delta() * SimTransform.from_pose(e.old_pose)
+        assert np.max(np.abs(redone.translation - e.new_pose.translation)) < 1e-12
+        assert abs(redone.scale - e.scale_change) < 1e-12
+    assert np.abs(np.array([n.state.translation for n in g.nodes]) - out["final_st"]).max() < 1e-8
+
+
+def test_dropin_errors(cuda_ok):
+    """loopclosure.py:510-521: no loops / disconnected chain raise ValueError; a non-finite
+    initial energy raises RuntimeError."""
+    from paper_2512_02293_b200.pgba import solve_pgba
+    from paper_2512_02293_b200.types import SimTransform, Rotation, RelativePoseEdge, LoopEdge, PoseGraph
+    P, _, _ = load_pgba_golden("exact")
+    g = pose_graph_from_packed(P)
+    with pytest.raises(ValueError, match="no loop edges"):
+        solve_pgba(PoseGraph(g.nodes, g.chain, []))
+    with pytest.raises(ValueError, match="disconnected"):
+        solve_pgba(PoseGraph([g.nodes[0], g.nodes[60]], [], g.loops))
+    bad = SimTransform(Rotation.identity(), np.array([np.nan, 0.0, 0.0]), 1.0)
+    g2 = PoseGraph(g.nodes, g.chain, [LoopEdge(0, 60, RelativePoseEdge(0, 60, bad, np.eye(7)))])
+    with pytest.raises(RuntimeError, match="finite"):
+        solve_pgba(g2)
