@@ -452,13 +452,15 @@ class DeviceProblem:
         (flow, weights, disparities) go as asynchronous DMAs from page-locked buffers when the
         layout was built pinned; weight signs are then checked on the device (ValueError, as
         residuals.py:112-113)."""
-        pin = H.pinned_tensors()
+        pin = H.pinned_tensors() if hasattr(H, "pinned_tensors") else None
         with torch.cuda.stream(self.stream):
             def put(dst, a, pinned=None):
                 if dst is None or dst.numel() == 0:
                     return
                 if pinned is not None:
                     dst.copy_(pinned.reshape(-1), non_blocking=True)
+                elif isinstance(a, torch.Tensor):   # device-resident source (window.DeviceWindow)
+                    dst.copy_(a.reshape(-1), non_blocking=True)
                 else:
                     dst.copy_(torch.from_numpy(np.ascontiguousarray(a).reshape(-1)).to(dst.dtype), non_blocking=False)
             put(self.d_state.view(-1), H.state)

@@ -275,7 +275,7 @@ def solve_pgba(graph, opts=None):
         opts = SolveOptions()
     P = pack_pose_graph(graph)
     before = {n.kid: n.state.copy() for n in graph.nodes}
-    from .problem import options_dict
+    from .problem import _rotation_exact, options_dict
     dp = DevicePoseGraph(P, options_dict(opts))
     try:
         rep = dp.solve()
@@ -285,7 +285,8 @@ def solve_pgba(graph, opts=None):
             for k, node in enumerate(graph.nodes):
                 if k > 0:    # the earliest keyframe is the gauge (loopclosure.py:403, 491)
                     st = node.state
-                    node.state = type(st)(type(st.rotation)(s[k, 0:4].copy()), s[k, 4:7].copy(), float(s[k, 7]))
+                    node.state = type(st)(_rotation_exact(type(st.rotation), s[k, 0:4]), s[k, 4:7].copy(),
+                                          float(s[k, 7]))
                 if doff[k + 1] > doff[k]:
                     node.disparities = d[doff[k]:doff[k + 1]].copy()
     finally:

@@ -104,6 +104,15 @@ def options_dict(opts) -> dict:
     return {n: getattr(opts, n) for n in names}
 
 
+def _rotation_exact(cls, q):
+    """A ``cls`` rotation holding exactly the solver's canonical quaternion.  The device already
+    normalised it (qcanon, as Rotation.__init__ does, geometry.py:94-98); constructing through
+    __init__ would renormalise and can move the last ulp (cf. frontend.py:565-573)."""
+    r = cls.identity()
+    r.q = np.asarray(q, dtype=float).reshape(4).copy()
+    return r
+
+
 def write_back(graph, q, p, v, bg, ba, disp, grav_q, opts) -> None:
     """Assign new state objects like solver.py:326-341 (_apply_step) does.
 
@@ -121,7 +130,7 @@ def write_back(graph, q, p, v, bg, ba, disp, grav_q, opts) -> None:
         if kf.kid in frozen:
             continue
         st = kf.state
-        rot = type(st.pose.rotation)(np.asarray(q[n], float).copy())
+        rot = _rotation_exact(type(st.pose.rotation), q[n])
         pose = type(st.pose)(rot, np.asarray(p[n], float).copy())
         if opts.optimize_velocity_bias:
             bias = type(st.bias)(np.asarray(bg[n], float).copy(), np.asarray(ba[n], float).copy())
@@ -131,4 +140,4 @@ def write_back(graph, q, p, v, bg, ba, disp, grav_q, opts) -> None:
         kf.state = type(st)(pose, vel, bias, st.timestamp)
     if opts.optimize_gravity:
         g = graph.gravity
-        graph.gravity = type(g)(type(g.R_wg)(np.asarray(grav_q, float).copy()), g.magnitude)
+        graph.gravity = type(g)(_rotation_exact(type(g.R_wg), grav_q), g.magnitude)

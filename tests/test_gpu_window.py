@@ -1,0 +1,102 @@
+"""Device-resident tracking window (paper_2512_02293_b200.window.DeviceWindow).
+
+* A window serialised by the REFERENCE's tracker (TrackerState.to_dict, frontend.py:209-294;
+  tests/golden/make_tracker_golden.py) replays into the device window, and its per-keyframe
+  solve (frontend.py:435-450) matches the reference's solve_vi_ba on that window.
+* A streamed tracker (insert keyframe + covisibility edges + inertial factor, solve, evict;
+  frontend.py:341-482) on the device window is bitwise the drop-in solve_vi_ba on the
+  equivalent host FrameGraph at every keyframe, while uploading only each new keyframe's
+  data and re-planning only when the window's topology changes.
+"""
+import copy
+import gzip
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN_DIR
+
+pytestmark = pytest.mark.gpu
+
+
+def test_reference_tracker_window_replay(cuda_ok):
+    from paper_2512_02293_b200.types import SolveOptions
+    from paper_2512_02293_b200.window import DeviceWindow
+    with gzip.open(os.path.join(GOLDEN_DIR, "tracker", "window.json.gz"), "rt") as fh:
+        data = json.load(fh)
+    z = np.load(os.path.join(GOLDEN_DIR, "tracker", "window_solve.npz"))
+    ref = json.loads(str(z["report"]))
+    w = DeviceWindow.from_tracker_dict(data)
+    assert w.phase == "full" and len(w.kfs) == 8
+    rep = w.solve(SolveOptions(max_iterations=4, frozen_keyframes=tuple(int(k) for k in z["frozen"])))
+    c, cr = np.array(rep.cost_trajectory), np.array(ref["cost_trajectory"])
+    print(f"replay: {rep.iterations} it {rep.termination} costs {c} / ref {cr}")
+    assert rep.iterations == ref["iterations"] and rep.termination == ref["termination"]
+    assert np.all(np.abs(c - cr) <= 1e-6 * cr)
+    p = np.array([w.state(k)[4:7] for k in w.kfs])
+    d = np.concatenate([w.disparities(k) for k in w.kfs])
+    moved = np.abs(z["final_p"] - np.array([data["graph"]["keyframes"][n]["state"]["pose"]["t"]
+                                          for n in range(8)])).max()
+    ep = np.abs(p - z["final_p"]).max()
+    ed = np.abs(d - z["final_disp"]).max() / np.abs(z["final_disp"]).max()
+    print(f"  final p err {ep:.2e} (motion {moved:.2e}), disparities {ed:.2e}")
+    assert ep <= 1e-5 * moved and ed < 1e-5
+    w.close()
+
+
+def test_streaming_window_is_bitwise_the_dropin(cuda_ok):
+    from paper_2512_02293_b200 import solver as S
+    from paper_2512_02293_b200 import types as T
+    from paper_2512_02293_b200.types import SolveOptions
+    from paper_2512_02293_b200.window import DeviceWindow
+    from paper_2512_02293_b200.workloads import make_workload
+    g = make_workload(1)
+    W, R = 8, 3
+    by_pair = {(e.i, e.j): e for e in g.vision_edges}
+    win = DeviceWindow(g.intrinsics, g.gravity, None, window_size=W)
+    h_kfs, h_edges, h_imu = [], [], []
+    per_insert = []
+    for k in range(len(g.keyframes)):
+        kf = g.keyframes[k]
+        b0 = win.h2d_bytes
+        win.add_keyframe(k, kf.state, kf.pixels, kf.disparities)
+        h_kfs.append(T.Keyframe(k, kf.state.copy(), kf.pixels.copy(), kf.disparities.copy()))
+        live = [x.kid for x in h_kfs]
+        for n in live[-(R + 1):-1]:
+            for (i, j) in ((k, n), (n, k)):
+                e = by_pair.get((i, j))
+                if e is not None:
+                    win.add_vision_edge(i, j, e.pixels, e.targets, e.weights)
+                    h_edges.append(T.VisionEdge(i, j, e.pixels.copy(), e.targets.copy(), e.weights.copy()))
+        if k > 0:
+            i, j, d = g.inertial_edges[k - 1]
+            win.add_inertial_edge(i, j, d)
+            h_imu.append((i, j, d))
+        per_insert.append(win.h2d_bytes - b0)
+        if len(h_kfs) >= 2:
+            opts = SolveOptions(max_iterations=4, frozen_keyframes=(h_kfs[0].kid,))
+            hg = T.FrameGraph(h_kfs, h_edges, h_imu, g.gravity, g.intrinsics)
+            r_host = S.solve_vi_ba(hg, opts)
+            r_win = win.solve(opts)
+            assert r_win.cost_trajectory == r_host.cost_trajectory and r_win.termination == r_host.termination
+            for x in hg.keyframes:
+                s = win.state(x.kid)
+                assert np.array_equal(s[0:4], x.state.pose.rotation.q) and np.array_equal(s[4:7], x.state.pose.translation)
+                assert np.array_equal(s[7:10], x.state.velocity)
+                assert np.array_equal(win.disparities(x.kid), x.disparities)
+        # eviction (frontend.py:453-482): both sides drop the oldest keyframe beyond the window
+        while len(h_kfs) > W:
+            old = h_kfs.pop(0).kid
+            h_edges = [e for e in h_edges if e.i != old and e.j != old]
+            h_imu = [t for t in h_imu if t[0] != old]
+            win.evict(old)
+        assert list(win.kfs) == [x.kid for x in h_kfs]
+    N = len(g.keyframes[0].disparities)
+    print(f"bytes uploaded per insertion {per_insert[-1]} (one keyframe: {8 * N} B disparities + its edges); "
+          f"{win.solves} solves, {win.replans} plans")
+    assert max(per_insert) <= 8 * N + 2 * R * 16 * N
+    assert win.replans < win.solves
+    S.clear_cache()
+    win.close()
