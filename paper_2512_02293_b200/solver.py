@@ -54,7 +54,9 @@ def _topology_key(H: HostLayout, o: dict, dev: int):
         h.update(b"|")
     if H.pix is not None:                 # explicit coordinates: part of the static schedule's input
         h.update(np.ascontiguousarray(H.pix).tobytes())
-    opts = tuple(sorted((k, tuple(v) if isinstance(v, (list, tuple)) else v) for k, v in o.items()))
+    # the frozen set enters as the per-keyframe flags hashed above (kids change as a window slides)
+    opts = tuple(sorted((k, tuple(v) if isinstance(v, (list, tuple)) else v) for k, v in o.items()
+                        if k != "frozen_keyframes"))
     return (dev, H.K, H.E, H.F, H.mode, H.grid, H.has_Tcb, opts, h.hexdigest())
 
 

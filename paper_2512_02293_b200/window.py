@@ -239,7 +239,9 @@ class DeviceWindow:
             h.update(b"|")
         if Ly.pix is not None:
             h.update(Ly.pix.tobytes())
-        opts = tuple(sorted((k, tuple(v) if isinstance(v, (list, tuple)) else v) for k, v in o.items()))
+        # the frozen set enters as the per-keyframe flags hashed above (kids change as a window slides)
+        opts = tuple(sorted((k, tuple(v) if isinstance(v, (list, tuple)) else v) for k, v in o.items()
+                            if k != "frozen_keyframes"))
         return (Ly.K, Ly.E, Ly.F, Ly.mode, Ly.grid, Ly.has_Tcb, opts, h.hexdigest())
 
     def _pack_into(self, Ly, tgt, w, disp64):

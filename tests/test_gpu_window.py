@@ -42,7 +42,9 @@ def test_reference_tracker_window_replay(cuda_ok):
     ep = np.abs(p - z["final_p"]).max()
     ed = np.abs(d - z["final_disp"]).max() / np.abs(z["final_disp"]).max()
     print(f"  final p err {ep:.2e} (motion {moved:.2e}), disparities {ed:.2e}")
-    assert ep <= 1e-5 * moved and ed < 1e-5
+    # the JSON window's targets are fp64 values the GPU stores as fp32 flow (u* - u): ~1e-7 px of
+    # input rounding the reference does not see, i.e. an absolute floor of ~1e-10 m here
+    assert ep <= max(1e-5 * moved, 1e-9) and ed < 1e-5
     w.close()
 
 
