@@ -296,6 +296,43 @@ VBA_API int vba_pg_solve(void* ctx, void* stream, vba_report* report, double* co
                          int32_t traj_capacity);                                         /* solve_pgba */
 VBA_API int vba_pg_download(void* ctx, void* stream);
 
+/* ------------------------------------------------------------------------
+ * Stage-2 inertial-only initialisation, replacing vislam.initialization.
+ * init_inertial_only (initialization.py:152-231): damped Gauss-Newton over
+ * [log-scale, gravity tangent (2), one shared bias (6), velocities (3K)] on the
+ * inertial residuals of the vision poses with positions scaled by exp(s).
+ * ------------------------------------------------------------------------ */
+typedef struct vba_init_problem {
+  int32_t n_kf, n_imu;
+  const double* q;         /* [K,4] device: vision rotations (fixed) */
+  const double* p;         /* [K,3] device: vision positions (unscaled) */
+  const double* v0;        /* [K,3] device: velocity seeds (initialization.py:121-134) */
+  const double* imu;       /* [F, VBA_IMU_REC] device */
+  const int32_t* h_imu_i;  /* [F] host, keyframe indices */
+  const int32_t* h_imu_j;
+  double grav_q[4], grav_G;   /* initial gravity model */
+  double bias0[6];            /* initial shared bias (gyro, accel) */
+} vba_init_problem;
+
+typedef struct vba_init_options {
+  int32_t max_iterations;     /* InitConfig.max_iterations_inertial */
+  double damping;             /* InitConfig.damping */
+} vba_init_options;
+
+typedef struct vba_init_result {
+  double log_scale;
+  double grav_q[4];
+  double bias[6];
+  int32_t iterations;
+  int32_t termination;        /* 0 max_iterations, 1 converged, 2 no_decrease_at_max_damping */
+  int32_t n_costs;
+  double initial_cost, final_cost;
+} vba_init_result;
+
+/* writes the solved velocities to v_out [K,3] (device) and cap costs to cost_trajectory (host) */
+VBA_API int vba_init_inertial(const vba_init_problem* prob, const vba_init_options* opts, void* stream,
+                              vba_init_result* result, double* cost_trajectory, int32_t cap, double* v_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,7 +26,7 @@ EXPORTED = ("vba_last_error", "vba_version", "vba_create", "vba_destroy", "vba_s
             "vba_preintegrate", "vba_preint_scratch_bytes",
             "vba_preint_factor_records",
             "vba_pg_create", "vba_pg_destroy", "vba_pg_energy", "vba_pg_linearize", "vba_pg_export_normal_eq",
-            "vba_pg_solve_step", "vba_pg_export_step", "vba_pg_solve", "vba_pg_download")
+            "vba_pg_solve_step", "vba_pg_export_step", "vba_pg_solve", "vba_pg_download", "vba_init_inertial")
 
 
 class VbaProblem(C.Structure):
@@ -56,6 +56,27 @@ class VbaPgProblem(C.Structure):
         ("wts", C.c_void_p), ("rel", C.c_void_p),
         ("h_doff", C.c_void_p), ("h_npix", C.c_void_p), ("h_vis_i", C.c_void_p), ("h_vis_j", C.c_void_p),
         ("h_voff", C.c_void_p), ("h_rel_i", C.c_void_p), ("h_rel_j", C.c_void_p),
+    ]
+
+
+class VbaInitProblem(C.Structure):
+    _fields_ = [
+        ("n_kf", C.c_int32), ("n_imu", C.c_int32),
+        ("q", C.c_void_p), ("p", C.c_void_p), ("v0", C.c_void_p), ("imu", C.c_void_p),
+        ("h_imu_i", C.c_void_p), ("h_imu_j", C.c_void_p),
+        ("grav_q", C.c_double * 4), ("grav_G", C.c_double), ("bias0", C.c_double * 6),
+    ]
+
+
+class VbaInitOptions(C.Structure):
+    _fields_ = [("max_iterations", C.c_int32), ("damping", C.c_double)]
+
+
+class VbaInitResult(C.Structure):
+    _fields_ = [
+        ("log_scale", C.c_double), ("grav_q", C.c_double * 4), ("bias", C.c_double * 6),
+        ("iterations", C.c_int32), ("termination", C.c_int32), ("n_costs", C.c_int32),
+        ("initial_cost", C.c_double), ("final_cost", C.c_double),
     ]
 
 
@@ -144,6 +165,8 @@ def load(path: str | None = None):
         "vba_pg_export_step": ([v, v, v, v], C.c_int),
         "vba_pg_solve": ([v, v, C.POINTER(VbaReport), C.POINTER(C.c_double), C.c_int32], C.c_int),
         "vba_pg_download": ([v, v], C.c_int),
+        "vba_init_inertial": ([C.POINTER(VbaInitProblem), C.POINTER(VbaInitOptions), v, C.POINTER(VbaInitResult),
+                               C.POINTER(C.c_double), C.c_int32, v], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

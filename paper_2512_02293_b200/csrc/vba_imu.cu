@@ -59,21 +59,17 @@ void launch_imu_prep(const double* imu, int F, double* Lbuf, int* status, cudaSt
 // factor evaluation.  Output record (ld = sdof), ibs doubles per factor:
 //   Hii[s*s] Hjj[s*s] Hij[s*s] gi[s] gj[s] Hgg[4] Hig[s*2] Hjg[s*2] gg[2] energy
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(64) k_imu_factor(const double* __restrict__ imu, const double* __restrict__ Lbuf,
-                                                   const int32_t* __restrict__ fi, const int32_t* __restrict__ fj,
-                                                   int f0, const double* __restrict__ state,
-                                                   const double* __restrict__ grav, int sdof, int ibs, int energy_only,
-                                                   double* __restrict__ out) {
-  __shared__ double J[15][kCols + 1];
-  __shared__ double L[kImuL];
-  const int f = f0 + blockIdx.x, tid = threadIdx.x;
-  const double* rec = imu + (int64_t)f * VBA_IMU_REC;
-  for (int i = tid; i < 117; i += blockDim.x) L[i] = Lbuf[(int64_t)f * kImuL + i];
+// Residual and whitened Jacobian columns [J_i | J_j | J_g | r] of one factor into J (shared
+// memory, 15 x kCols); called by every thread of the CTA (it synchronises).  energy_only:
+// the residual column only.
+__device__ void imu_whitened_J(const double* __restrict__ rec, const double* __restrict__ Lg,
+                               const double* si, const double* sj, const double* __restrict__ grav, int energy_only,
+                               double (*J)[kCols + 1], double* L) {
+  const int tid = threadIdx.x;
+  for (int i = tid; i < 117; i += blockDim.x) L[i] = Lg[i];
   for (int i = tid; i < 15 * (kCols + 1); i += blockDim.x) (&J[0][0])[i] = 0.0;
   __syncthreads();
   if (tid == 0) {
-    const double* si = state + 16 * fi[f];
-    const double* sj = state + 16 * fj[f];
     const double dt = rec[kDT];
     double Ri[9], Rj[9], Rwg[9];
     qmat(si, Ri);
@@ -178,6 +174,18 @@ __global__ void __launch_bounds__(64) k_imu_factor(const double* __restrict__ im
     }
   }
   __syncthreads();
+}
+
+__global__ void __launch_bounds__(64) k_imu_factor(const double* __restrict__ imu, const double* __restrict__ Lbuf,
+                                                   const int32_t* __restrict__ fi, const int32_t* __restrict__ fj,
+                                                   int f0, const double* __restrict__ state,
+                                                   const double* __restrict__ grav, int sdof, int ibs, int energy_only,
+                                                   double* __restrict__ out) {
+  __shared__ double J[15][kCols + 1];
+  __shared__ double L[kImuL];
+  const int f = f0 + blockIdx.x, tid = threadIdx.x;
+  imu_whitened_J(imu + (int64_t)f * VBA_IMU_REC, Lbuf + (int64_t)f * kImuL, state + 16 * fi[f], state + 16 * fj[f],
+                 grav, energy_only, J, L);
   double* o = out + (int64_t)f * ibs;
   const int s = sdof, s2 = sdof * sdof;
   const int oE = 3 * s2 + 6 * s + 6;
@@ -214,6 +222,81 @@ void launch_imu_factor(const double* imu, const double* Lbuf, const int32_t* fi,
                        double* imu_blocks, cudaStream_t st) {
   if (F <= 0) return;
   k_imu_factor<<<F, 64, 0, st>>>(imu, Lbuf, fi, fj, f0, s.state, s.grav, sdof, ibs, energy_only, imu_blocks);
+  launch_count();
+}
+
+}  // namespace vba
+
+namespace vba {
+
+// ---------------------------------------------------------------------------
+// Stage-2 inertial-only initialisation (initialization.py:152-231): per factor, the
+// whitened inertial Jacobian re-expressed in the stage-2 unknowns
+//   [log-scale, gravity (2), shared bias (6), v_i (3), v_j (3)]
+// (initialization.py:183-190), its 15x15 Gram and gradient, and the energy.
+// Record: H[15*15] g[15] e (kInit2Rec doubles).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(64) k_init2_factor(const double* __restrict__ imu, const double* __restrict__ Lbuf,
+                                                     const int32_t* __restrict__ fi, const int32_t* __restrict__ fj,
+                                                     const double* __restrict__ state, const double* __restrict__ grav,
+                                                     const double* __restrict__ pvis, const double* __restrict__ es_p,
+                                                     int energy_only, double* __restrict__ out) {
+  __shared__ double J[15][kCols + 1];
+  __shared__ double L[kImuL];
+  __shared__ double J2[15][17];
+  const int f = blockIdx.x, tid = threadIdx.x;
+  const int i = fi[f], j = fj[f];
+  imu_whitened_J(imu + (int64_t)f * VBA_IMU_REC, Lbuf + (int64_t)f * kImuL, state + 16 * i, state + 16 * j, grav,
+                 energy_only, J, L);
+  double* o = out + (int64_t)f * kInit2Rec;
+  if (energy_only) {
+    if (tid == 0) {
+      double e = 0.0;
+      for (int r = 0; r < 15; ++r) e += J[r][33] * J[r][33];
+      o[240] = e;
+    }
+    return;
+  }
+  const double es = es_p[0];
+  if (tid < 15) {
+    const int r = tid;
+    double pi[3], pj[3];
+    for (int k = 0; k < 3; ++k) {
+      pi[k] = es * pvis[3 * i + k];
+      pj[k] = es * pvis[3 * j + k];
+    }
+    double a = 0.0, b = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      a += J[r][3 + k] * pi[k];
+      b += J[r][15 + 3 + k] * pj[k];
+    }
+    J2[r][0] = a + b;                                   // log-scale
+    J2[r][1] = J[r][30];                                // gravity tangent (J_g B)
+    J2[r][2] = J[r][31];
+    for (int m = 0; m < 6; ++m) J2[r][3 + m] = J[r][9 + m] + J[r][15 + 9 + m];   // shared bias
+    for (int k = 0; k < 3; ++k) {
+      J2[r][9 + k] = J[r][6 + k];                       // v_i
+      J2[r][12 + k] = J[r][15 + 6 + k];                 // v_j
+    }
+    J2[r][15] = J[r][33];                               // residual
+  }
+  __syncthreads();
+  for (int it = tid; it < 241; it += blockDim.x) {
+    int ca, cb;
+    if (it < 225) { ca = it / 15; cb = it % 15; }
+    else if (it < 240) { ca = it - 225; cb = 15; }
+    else { ca = 15; cb = 15; }
+    double acc = 0.0;
+    for (int r = 0; r < 15; ++r) acc += J2[r][ca] * J2[r][cb];
+    o[it] = acc;
+  }
+}
+
+void launch_init2_factor(const double* imu, const double* Lbuf, const int32_t* fi, const int32_t* fj, int F,
+                         const double* state, const double* grav, const double* pvis, const double* es,
+                         int energy_only, double* out, cudaStream_t st) {
+  if (F <= 0) return;
+  k_init2_factor<<<F, 64, 0, st>>>(imu, Lbuf, fi, fj, state, grav, pvis, es, energy_only, out);
   launch_count();
 }
 

@@ -310,6 +310,11 @@ void launch_imu_prep(const double* imu, int F, double* Lbuf, int* status, cudaSt
 void launch_imu_factor(const double* imu, const double* Lbuf, const int32_t* fi, const int32_t* fj, int f0, int F,
                        const DevState& s, const double* ts, int sdof, int ibs, int energy_only,
                        double* imu_blocks, cudaStream_t st);
+// stage-2 inertial-only initialisation (vba_imu.cu / vba_init.cu)
+constexpr int kInit2Rec = 248;   // H 15x15, g 15, e (+pad)
+void launch_init2_factor(const double* imu, const double* Lbuf, const int32_t* fi, const int32_t* fj, int F,
+                         const double* state, const double* grav, const double* pvis, const double* es,
+                         int energy_only, double* out, cudaStream_t st);
 // dense
 void launch_assemble(const int32_t* blk_ptr, const int32_t* blk_nff, const Contrib* contribs, int nblk_rows,
                      const int32_t* roff, const int32_t* rdim, const double* arena, double lam, double ridge,

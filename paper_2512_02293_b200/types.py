@@ -466,3 +466,36 @@ class CorrectionEntry:
 class LoopCorrection:
     entries: dict
     timestamp: float = 0.0
+
+
+# ---------------------------------------------------------------------------
+# Staged initialisation containers: initialization.py:30-61 (InitConfig, InitResult)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class InitConfig:
+    n_vis_init: int = 10
+    n_iner_init: int = 20
+    max_iterations_vision: int = 30
+    max_iterations_inertial: int = 60
+    max_iterations_joint: int = 15
+    damping: float = 1e-4
+
+    def __post_init__(self):
+        if not 2 <= self.n_vis_init <= self.n_iner_init:
+            raise ValueError("need n_iner_init >= n_vis_init >= 2")
+        for name in ("max_iterations_vision", "max_iterations_inertial", "max_iterations_joint"):
+            if getattr(self, name) < 1:
+                raise ValueError(f"{name} must be at least 1")
+
+
+@dataclass
+class InitResult:
+    gravity: GravityModel
+    log_scale: float
+    velocities: np.ndarray
+    bias: BiasState
+    reports: dict = field(default_factory=dict)
+
+    def scale(self):
+        return float(np.exp(self.log_scale))

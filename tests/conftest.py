@@ -175,3 +175,17 @@ def pose_graph_from_packed(P):
     Tcb = T.Pose(T.Rotation(P["Tcb"][:4]), P["Tcb"][4:7]) if bool(P["has_Tcb"]) else None
     gap = min([lp.j - lp.i for lp in loops] + [55])
     return T.PoseGraph(nodes, rel[n_rel_loops:], loops, intr, Tcb, min_loop_gap=gap)
+
+
+def init_golden_names():
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN_DIR, "init", "*.npz")))
+
+
+def load_init_golden(name):
+    z = np.load(os.path.join(GOLDEN_DIR, "init", name + ".npz"), allow_pickle=False)
+    P = {k[3:]: z[k] for k in z.files if k.startswith("in_")}
+    P["grav_G"] = float(P["grav_G"])
+    P["has_Tcb"] = bool(P["has_Tcb"])
+    out = {k: z[k] for k in z.files if not k.startswith("in_")}
+    out["meta"] = json.loads(str(out["meta"]))
+    return P, out

@@ -71,7 +71,10 @@ def _c_layout(struct, fields):
 
 
 @pytest.mark.parametrize("cls,struct", [("VbaProblem", "vba_problem"), ("VbaOptions", "vba_options"),
-                                        ("VbaReport", "vba_report"), ("VbaTrialResult", "vba_trial_result")])
+                                        ("VbaReport", "vba_report"), ("VbaTrialResult", "vba_trial_result"),
+                                        ("VbaPgProblem", "vba_pg_problem"), ("VbaInitProblem", "vba_init_problem"),
+                                        ("VbaInitOptions", "vba_init_options"),
+                                        ("VbaInitResult", "vba_init_result")])
 def test_ctypes_struct_layout_matches_c(cls, struct):
     from paper_2512_02293_b200 import _lib
     S = getattr(_lib, cls)
