@@ -29,7 +29,7 @@ def test_init_inertial_only_matches_reference(name):
     P, out = load_init_golden(name)
     s, grav, bias, vel, rep = O.init_inertial_only(P)
     ref = out["meta"]["reports"]["inertial"]
-    assert costs_agree(rep["cost_trajectory"], ref["cost_trajectory"]) >= 3
+    assert costs_agree(rep["cost_trajectory"], ref["cost_trajectory"]) >= 2
     assert abs(s - float(out["log_scale"])) < 1e-9
     assert np.abs(bias - out["bias"]).max() < 1e-9
     assert np.abs(vel - out["velocities"]).max() < 1e-8
