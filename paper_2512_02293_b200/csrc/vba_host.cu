@@ -18,6 +18,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX ranges (profilers pick them up; no-ops otherwise)
+
 #include "vba_internal.cuh"
 #include "vba_plan.h"
 
@@ -1258,7 +1260,7 @@ int vba_preintegrate(const double* ts, const double* gyro, const double* accel, 
   VBA_CUDA(cudaStreamSynchronize(st));
   if (hs & 1) { set_err("Need at least two IMU samples to preintegrate"); return VBA_E_INVALID; }
   if (hs & 2) { set_err("IMU timestamps must be strictly increasing"); return VBA_E_INVALID; }
-  if (hs & 4) { set_err("vba_preintegrate: soff[n_pairs] != n_samples"); return VBA_E_INVALID; }
+  if (hs & 4) { set_err("vba_preintegrate: malformed soff (soff[n_pairs] != n_samples or out of range)"); return VBA_E_INVALID; }
   return VBA_OK;
 }
 
@@ -1362,11 +1364,17 @@ int vba_solve(void* ctx, void* stream, vba_report* rep, double* traj, int32_t ca
   int term = 0, iters = 0, warns = 0, trials = 0;
   bool broke = false;
   for (int it = 0; it < o.max_iterations; ++it) {
-    if ((rc = stage_linearize(c, st))) return rc;
+    nvtxRangePushA("vba.linearize");
+    rc = stage_linearize(c, st);
+    nvtxRangePop();
+    if (rc) return rc;
     bool accepted = false;
     while (true) {
       vba_trial_result r;
-      if ((rc = run_trial(c, lam, o.use_schur, &r, st))) return rc;
+      nvtxRangePushA("vba.trial");
+      rc = run_trial(c, lam, o.use_schur, &r, st);
+      nvtxRangePop();
+      if (rc) return rc;
       ++trials;
       if (r.status == VBA_E_NOT_SPD) {   // solver.py:373-379
         ++warns;

@@ -33,6 +33,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "vba_internal.cuh"
 #include "vba_plan.h"
 
@@ -1203,12 +1205,18 @@ int vba_pg_solve(void* ctx, void* stream, vba_report* rep, double* traj, int32_t
   int term = 0, iters = 0, warns = 0, trials = 0;
   bool broke = false;
   for (int it = 0; it < o.max_iterations; ++it) {
-    if ((rc = pg_linearize(c, st))) return rc;
+    nvtxRangePushA("vba.pg.linearize");
+    rc = pg_linearize(c, st);
+    nvtxRangePop();
+    if (rc) return rc;
     bool accepted = false;
     while (true) {
       int status;
       double nc, step;
-      if ((rc = pg_trial(c, lam, &status, &nc, &step, st))) return rc;
+      nvtxRangePushA("vba.pg.trial");
+      rc = pg_trial(c, lam, &status, &nc, &step, st);
+      nvtxRangePop();
+      if (rc) return rc;
       ++trials;
       if (status == VBA_E_NOT_SPD) {
         ++warns;

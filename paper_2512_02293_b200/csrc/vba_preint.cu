@@ -170,6 +170,7 @@ __device__ __forceinline__ double at3(const double* p, int i, int j) { return p[
 
 __global__ void __launch_bounds__(16 * kPairsPerBlock) k_preint_propagate(const double* __restrict__ ts,
                                                                          const int64_t* __restrict__ soff, int F,
+                                                                         int64_t n_samples,
                                                                          const double* __restrict__ steps,
                                                                          const double* __restrict__ noise,
                                                                          double* __restrict__ out,
@@ -181,6 +182,9 @@ __global__ void __launch_bounds__(16 * kPairsPerBlock) k_preint_propagate(const 
   const unsigned mask = 0xFFFFu << (threadIdx.x & 16);
   PairSmem& sm = sm_all[grp];
   const int64_t s0 = soff[f], S = soff[f + 1] - s0;
+  // a malformed soff must not send this pass outside the step records (the step pass, which
+  // checks soff[F] == n_samples, is skipped when there are no samples at all)
+  if (s0 < 0 || soff[f + 1] > n_samples || soff[f + 1] < s0) { if (c == 0) atomicOr(status, 4); return; }
   if (S < 2) { if (c == 0) atomicOr(status, 1); return; }   // imu.py:87-88
   const bool cov_lane = c < 9, jac_lane = c < 3;
   const int br = cov_lane ? c / 3 : 0, rr = cov_lane ? c % 3 : 0;   // lane's row block / row in block
@@ -344,7 +348,7 @@ void launch_preintegrate(const double* ts, const double* gyro, const double* acc
     launch_count();
   }
   k_preint_propagate<<<(F + kPairsPerBlock - 1) / kPairsPerBlock, 16 * kPairsPerBlock, 0, st>>>(
-      ts, soff, F, scratch, noise, out, status);
+      ts, soff, F, S, scratch, noise, out, status);
   launch_count();
 }
 
