@@ -757,10 +757,10 @@ static int stage_step(Ctx* c, double lam, cudaStream_t st) {
       c->tc_gen += 2 * c->tc_iters;
     }
     c->tc_ran = tc_ran;
-    // small systems: one-CTA shared-memory Cholesky (vba_small.cu); else the fp64 tile DAG
-    if (!tc_ran && (c->d_trace || chol_small_solve(c->d_H, c->npad, c->nfree, c->d_rhs, c->d_x, &c->d_res->status, st)))
+    if (!tc_ran) {
       chol_dag_launch(c->d_H, c->npad, c->nt, c->d_rhs, c->d_x, c->d_Ld, c->d_cpart, c->d_cflags, c->d_ctasks,
                       c->n_ctasks, &c->d_res->status, st, c->d_trace);
+    }
   }
   mark(c, 4, st);
   launch_scatter_dx(c->d_x, c->d_fmap, c->npv, c->d_dx, st);
@@ -843,9 +843,8 @@ static int stage_step_dense(Ctx* c, double lam, cudaStream_t st) {
   HpdOut o{c->d_D, c->dn_npad, c->nfree, c->sdof, c->d_kfcol, c->d_Hdd, c->d_gd, c->d_drhs, lam, c->O.ridge};
   launch_export_hpd(c->P.pixel_mode, c->d_seb, c->d_see, c->d_doff, c->d_roff_real, c->d_npix, c->maxpix, c->d_ej,
                     c->K, s, c->extr, c->pix, c->P.wts, c->d_eoff, c->P.grid_w, c->grid, c->intr, o, st);
-  if (chol_small_solve(c->d_D, c->dn_npad, c->dn_N, c->d_drhs, c->d_dx2, &c->d_res->status, st))
-    chol_dag_launch(c->d_D, c->dn_npad, c->dn_nt, c->d_drhs, c->d_dx2, c->d_dLinv, c->d_dpart, c->d_dflags,
-                    c->d_dtasks, c->n_dtasks, &c->d_res->status, st);
+  chol_dag_launch(c->d_D, c->dn_npad, c->dn_nt, c->d_drhs, c->d_dx2, c->d_dLinv, c->d_dpart, c->d_dflags,
+                  c->d_dtasks, c->n_dtasks, &c->d_res->status, st);
   mark(c, 4, st);
   launch_scatter_dx(c->d_dx2, c->d_fmap, c->npv, c->d_dx, st);
   if (c->n_disp) {   // padding slots keep their values; real pixels are rewritten below
@@ -1227,8 +1226,7 @@ int vba_spd_solve(const double* H, int64_t n, const double* b, double* x, int32_
     used_tc = tcrc == 0 && (mode == 2 || (hs[1] == 0 && h2[4] == 1.0)) ? 1 : 0;
   }
   if (!used_tc) {
-    if (chol_small_solve(Hp, npad, (int)n, bp, xp, stat, st))
-      chol_dag_launch(Hp, npad, nt, bp, xp, Ld, part, flags, tasks, ntasks, stat, st);
+    chol_dag_launch(Hp, npad, nt, bp, xp, Ld, part, flags, tasks, ntasks, stat, st);
     cudaMemcpyAsync(hs, stat, sizeof(hs), cudaMemcpyDeviceToHost, st);
   }
   cudaMemcpyAsync(x, xp, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);

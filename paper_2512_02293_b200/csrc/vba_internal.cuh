@@ -310,9 +310,6 @@ void launch_imu_prep(const double* imu, int F, double* Lbuf, int* status, cudaSt
 void launch_imu_factor(const double* imu, const double* Lbuf, const int32_t* fi, const int32_t* fj, int f0, int F,
                        const DevState& s, const double* ts, int sdof, int ibs, int energy_only,
                        double* imu_blocks, cudaStream_t st);
-// small fp64 SPD solve in one CTA (vba_small.cu): n <= kSmallN (packed lower + rhs in 227 KB)
-constexpr int kSmallN = 236;
-int chol_small_solve(const double* H, int64_t ld, int n, const double* b, double* x, int* status, cudaStream_t st);
 // stage-2 inertial-only initialisation (vba_imu.cu / vba_init.cu)
 constexpr int kInit2Rec = 248;   // H 15x15, g 15, e (+pad)
 void launch_init2_factor(const double* imu, const double* Lbuf, const int32_t* fi, const int32_t* fj, int F,
