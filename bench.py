@@ -379,7 +379,7 @@ def main():
             "config": {"workload": desc, "edges": E, "px_per_keyframe": N, "edge_px": total_edge_px,
                        "reduced_dim": int(dp.lib.vba_reduced_dim(dp.ctx)),
                        "precision": "fp32 per-pixel math, fp64 reductions / IMU / Schur assembly / Cholesky",
-                       "parallelism": f"edge-sharded by source keyframe x{world}, NCCL all_reduce of H_red",
+                       "parallelism": f"edge-sharded by source keyframe x{world}, NCCL all-gather of per-rank edge, factor and fill-in blocks",
                        "l2": ("flushed (320 MB write) between steps" if flush is not None
                               else f"inputs {footprint / 2**20:.0f} MB > 126 MB L2"),
                        "partition": partition_sources(P, world) if world > 1 else None},
