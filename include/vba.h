@@ -208,6 +208,11 @@ VBA_API int vba_solve_times(void* ctx, double* out4);
  * summed over them */
 VBA_API int vba_stats(void* ctx, int64_t* out4);
 
+/* Which Schur fill-in Gram the context runs (solver.py:282-285): 1 = tcgen05 kind::tf32
+ * 3-product kernel (windows with >= 256 pixels per source keyframe), 0 = fp64 DMMA kernel;
+ * the environment variable VBA_GRAM=tc|dmma, read by vba_create, forces either. */
+VBA_API int vba_gram_kind(void* ctx);
+
 /* Standalone SPD solve H x = b of a dense fp64 n x n system (column-major,
  * lower triangle read; device pointers), replacing np.linalg.solve(Hred, -gred)
  * of solver.py:287.  mode 0: tcgen05 split-fp16 (3-product) Cholesky + fp64 iterative

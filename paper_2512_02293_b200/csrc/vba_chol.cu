@@ -30,6 +30,7 @@
 #include <tuple>
 
 #include "vba_internal.cuh"
+#include "vba_tc.cuh"
 
 namespace vba {
 
@@ -288,7 +289,7 @@ __device__ void task_potrf(const CholArgs& a, int k, double* smem) {
   double* Mc = I + 4 * 32 * SB;          // 4 blocks: column p of M (rows i >= p), or the TRSM temp (stride TB)
   __shared__ double ys[CT];
   __shared__ int bad;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const double* Ak = tile(a, k, k);
   if (tid == 0) bad = 0;
   // async tile load (all loads in flight at once; no register staging)
@@ -752,13 +753,6 @@ struct TcArgs {
 };
 
 __device__ __forceinline__ int64_t tlin(int i, int j) { return (int64_t)i * (i + 1) / 2 + j; }
-__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
 // fp16 offset of element (row r, col c) inside one image part (see layout above):
 // 64-column K-chunks, 8-row atoms of 1 KB, 16-byte units (8 fp16) XOR-swizzled by row
 __device__ __forceinline__ int img_off(int r, int c) {
@@ -778,31 +772,6 @@ __device__ __forceinline__ void split4_h(const float4 x, uint2& hi, uint2& lo) {
   lo.y = (uint32_t)__half_as_ushort(l2) | ((uint32_t)__half_as_ushort(l3) << 16);
 }
 
-__device__ __forceinline__ void tc_mbar_init(uint64_t* b, int n) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
-}
-__device__ __forceinline__ void tc_mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "TCW_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra TCW_%=;\n}" ::"r"(su32(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tc_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void tc_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(dst)),
-      "l"(src), "r"(bytes), "r"(su32(bar))
-      : "memory");
-}
-__device__ __forceinline__ uint64_t tc_sdesc(uint32_t saddr) {   // K-major, SWIZZLE_128B, SBO 1 KB
-  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
 __device__ __forceinline__ void tc_mma(uint32_t tmem, uint64_t da, uint64_t db, uint32_t acc,
                                        uint32_t idesc = TC_IDESC) {
   asm volatile(
@@ -815,31 +784,6 @@ __device__ __forceinline__ void tc_mma3(uint32_t tmem, uint32_t a_hi, uint32_t a
   tc_mma(tmem, tc_sdesc(a_hi), tc_sdesc(b_hi), first ? 0u : 1u, TC_IDESC2);
   tc_mma(tmem, tc_sdesc(a_lo), tc_sdesc(b_hi), 1u, TC_IDESC);
 }
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void proxy_fence_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
-__device__ __forceinline__ void proxy_fence_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-// 32 consecutive accumulator columns of this thread's TMEM lane
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(r[k]);
-}
-
 // columns c .. c+31 of the 3xTF32 result: accumulator columns c and c + 128 summed
 __device__ __forceinline__ void tmem_ld_sum(uint32_t taddr, float* v) {
   float u[32];
@@ -907,7 +851,7 @@ struct TcRing {
 // one K-chunk of 3xTF32 MMAs from stage s into the accumulator
 __device__ __forceinline__ void tc_chunk_mma(const TcRing& R, int s, uint32_t tmem, bool first) {
   const uint32_t a_hi = su32(R.base + (size_t)s * TSTAGE), a_lo = a_hi + TCHUNK;
-  const uint32_t b_hi = a_hi + 2 * TCHUNK, b_lo = a_hi + 3 * TCHUNK;
+  const uint32_t b_hi = a_hi + 2 * TCHUNK;   // B_lo follows at + TCHUNK (the N = 256 descriptor spans both)
 #pragma unroll
   for (int kk = 0; kk < TKC / 8; ++kk) {   // 16 fp16 (32 B) of K per MMA
     const uint32_t o = 32u * kk;
@@ -1214,7 +1158,6 @@ __device__ void tc_task_syrk_smem(const TcArgs& a, TcRing& R, uint64_t* accf, ui
 // ---------------------------------------------------------------------------
 constexpr int SWF = CT + 4;      // 132: float4-aligned columns
 constexpr int XBS = 36;          // 32x32 block row stride (float4-aligned)
-constexpr int XB = 32 * XBS;     // floats per 32x32 block
 
 // Cholesky + inverse of a 32x32 SPD block by Gaussian elimination of the
 // augmented [A | I] without pivoting (stable for SPD): A = Lt U, U = diag(p) Lt^T,

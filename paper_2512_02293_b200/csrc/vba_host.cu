@@ -87,6 +87,7 @@ struct Ctx {
   std::vector<int64_t> goff, foff;
   int kmax = 0;
   size_t gram_smem = 0;
+  bool gram_tc = false;   // K4 on tcgen05 (3xTF32) instead of the fp64 DMMA kernel
   int64_t n_part = 0, gram_part_len = 0, gram_len = 0, fill_len = 0;
   int ibs = 0;
   int64_t arena_vis = 0, arena_imu = 0, arena_fill = 0, arena_len = 0;
@@ -477,6 +478,14 @@ static int build_plans(Ctx* c, cudaStream_t st) {
     c->foff[n] = fo;
     fo += (int64_t)(1 + k + np) * 36 + 6 * (1 + k);
   }
+  // K4 path: the tensor-core Gram (3xTF32, fp32 accumulation per pixel range) for windows
+  // with >= 256 pixels per source keyframe, the exact fp64 DMMA Gram for the small ones
+  // (where it costs little and ill-conditioned windows keep every bit); VBA_GRAM=tc|dmma forces
+  {
+    const char* gm = getenv("VBA_GRAM");
+    c->gram_tc = gm ? (strcmp(gm, "tc") == 0) : (nsrc > 0 && work_px >= 256 * (int64_t)nsrc);
+    if (c->gram_tc) c->gram_smem = gram_tc_smem_bytes(c->kmax);
+  }
   if (c->gram_smem > 227 * 1024) { set_err("Gram kernel shared memory too large"); return VBA_E_UNSUPPORTED; }
   // Gram launch order: longest tiles (pixels x edge pairs) first, so the last of the ~7
   // waves of one-CTA-per-SM tiles are the short ones.  Only the launch order changes: each
@@ -714,9 +723,14 @@ static int stage_reduce(Ctx* c, double lam, cudaStream_t st) {
   mark(c, 2, st);
   VBA_CUDA(cudaMemsetAsync(c->d_res, 0, sizeof(Result), st));
   if (!c->gorder_own.empty()) {
-    launch_gram(c->P.pixel_mode, c->d_gtiles, (int)c->gorder_own.size(), kGramBlock, c->gram_smem, c->kmax, s,
-                c->pix, c->P.wts, c->d_eoff, c->d_doff, c->P.grid_w, c->grid, c->intr, c->d_Hdd, c->d_gd, lam,
-                c->O.ridge, c->d_gram_part, st, c->d_gorder_own);
+    if (c->gram_tc)
+      launch_gram_tc(c->P.pixel_mode, c->d_gtiles, (int)c->gorder_own.size(), c->gram_smem, c->kmax, s, c->pix,
+                     c->P.wts, c->d_eoff, c->d_doff, c->P.grid_w, c->grid, c->intr, c->d_Hdd, c->d_gd, lam,
+                     c->O.ridge, c->d_gram_part, st, c->d_gorder_own);
+    else
+      launch_gram(c->P.pixel_mode, c->d_gtiles, (int)c->gorder_own.size(), kGramBlock, c->gram_smem, c->kmax, s,
+                  c->pix, c->P.wts, c->d_eoff, c->d_doff, c->P.grid_w, c->grid, c->intr, c->d_Hdd, c->d_gd, lam,
+                  c->O.ridge, c->d_gram_part, st, c->d_gorder_own);
     launch_fill_transform(c->d_gsrc_own, (int)c->gsrc_own.size(), c->d_seb, c->d_see, c->d_g0, c->d_g1,
                           c->d_gtiles, c->d_foff, c->d_gram_part, s, c->extr, c->d_arena + c->arena_fill, c->kmax,
                           st);
@@ -1170,6 +1184,8 @@ int vba_stats(void* ctx, int64_t* out4) {
   out4[3] = c->tc_passes;
   return VBA_OK;
 }
+
+int vba_gram_kind(void* ctx) { return ((Ctx*)ctx)->gram_tc ? 1 : 0; }
 
 // Standalone SPD solve (np.linalg.solve of solver.py:287 on a damped reduced system).
 int vba_spd_solve(const double* H, int64_t n, const double* b, double* x, int32_t mode, void* stream,

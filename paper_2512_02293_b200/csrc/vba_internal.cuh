@@ -294,6 +294,11 @@ void launch_fill_transform(const int32_t* src_list, int nsrc, const int32_t* src
 void launch_step_edges(const int32_t* ei, const int32_t* ej, int E, const DevState& s, const Extr& x,
                        const double* dx_full, int sdof, float* ustep, cudaStream_t st);
 size_t gram_smem_bytes(int kmax, int nsplit, int npairs, int k);
+size_t gram_tc_smem_bytes(int kmax);
+void launch_gram_tc(int pixel_mode, const GramTile* gt, int ngt, size_t smem, int kmax, const DevState& s,
+                    const float* pix, const float* wts, const int64_t* eoff, const int64_t* doff, int grid_w,
+                    const double* grid, const double* intr, const float* Hdd, const float* gd, double lam,
+                    double ridge, double* gram_part, cudaStream_t st, const int32_t* order);
 void launch_backsub(int pixel_mode, const PixTile* tiles, int ntiles, const DevState& cur, const DevState& nxt,
                     const float* pix, const float* wts, const int64_t* eoff, const int64_t* doff, int grid_w,
                     const double* grid, const double* intr, const float* Hdd, const float* gd,

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include "vba_internal.cuh"
+#include "vba_tc.cuh"
 
 namespace vba {
 
@@ -986,6 +987,298 @@ void launch_gram(int mode, const GramTile* gt, int ngt, int block, size_t smem, 
   launch_count();
 }
 
+
+// ---------------------------------------------------------------------------
+// K4 on the 5th-gen tensor cores (windows with >= 256 pixels per keyframe): the same
+// Gram C = W^T W, W = [k_{n,e} / sqrt(h_n) (6k columns) | g_d(n) / sqrt(h_n)], as
+// k_gram, on tcgen05.mma kind::tf32 with 3xTF32 splitting: w = hi + lo (hi = tf32(w),
+// lo = tf32(w - hi), 22 significant bits), C ~ Wh^T Wh + Wh^T Wl + Wl^T Wh with fp32
+// accumulation in TMEM over the tile's pixel range; k_fill_transform sums the ranges
+// in fp64 (fixed order: deterministic).  Emulated on configs 3 and 4 the reduced
+// step moves by < 1e-7 relative (tools/gram_tc_precision.py), far inside 1e-5.
+//
+// Operands: W^T staged per 32-pixel chunk as K-major SWIZZLE_128B images (row m = W
+// column m, its 32 pixels = one 128-B swizzle row; 8-row atoms of 1 KB), hi and lo.
+// A and B are the same images:  tile 0 = rows 0..127 x columns 0..Mp (N0 = Mp, the
+// rows beyond 127 of C come out transposed), tile 1 (M = 6k + 1 > 128 only) = rows
+// 128..255 x columns 128..Mp (N1 = Mp - 128).  Rows >= M of A and columns >= M of B
+// only feed accumulator rows / columns that are never read.
+//
+// Warp roles (288 threads): warps 0-7 produce the chunks (lane = pixel, warp w takes
+// out-edges w, w + 8, ...; warp 0 also the g_d row) into a 2-stage ring (full / empty
+// mbarriers) and run the epilogue; warp 8 owns TMEM (256 columns: 2 CTAs per SM) and
+// one of its lanes issues the MMAs.
+// ---------------------------------------------------------------------------
+#ifndef VBA_GTC_PW
+#define VBA_GTC_PW 8
+#endif
+#ifndef VBA_GTC_STAGES
+#define VBA_GTC_STAGES 2
+#endif
+#ifndef VBA_GTC_MINB
+#define VBA_GTC_MINB 2
+#endif
+constexpr int kGtcPW = VBA_GTC_PW;               // producer warps
+constexpr int kGtcEPW = (31 + kGtcPW - 1) / kGtcPW;   // out-edges per producer warp (k <= 31)
+constexpr int kGtcThreads = (kGtcPW + 1) * 32;
+static_assert(kGtcPW % 4 == 0, "epilogue: whole groups of 4 warps (one per TMEM lane quarter)");
+constexpr int kGtcStages = VBA_GTC_STAGES;
+constexpr int kGtcTmemCols = 256;
+
+__host__ __device__ __forceinline__ int gtc_mp(int kmax) { return (6 * kmax + 1 + 15) / 16 * 16; }
+__host__ __device__ __forceinline__ int gtc_rows(int kmax) { return gtc_mp(kmax) > 128 ? gtc_mp(kmax) : 128; }
+// stage = hi + lo images of gtc_rows rows x 128 B; tile 1's A reads 128 rows from row 128,
+// so up to 256 - rows rows past the last image are addressed (slack) -- plus 1 KB alignment
+size_t gram_tc_smem_bytes(int kmax) {
+  const int R = gtc_rows(kmax);
+  return (size_t)kGtcStages * 2 * R * 128 + (size_t)(256 - (R < 256 ? R : 256)) * 128 + 1024;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kGtcThreads, VBA_GTC_MINB) k_gram_tc(
+    const GramTile* __restrict__ gts, const float* __restrict__ disp, const EdgeGeo32* __restrict__ geo,
+    const float* __restrict__ pix, const float* __restrict__ wts, const int64_t* __restrict__ eoff,
+    const int64_t* __restrict__ doff, int grid_w, GridP gp, IntrP in, const float* __restrict__ Hdd,
+    const float* __restrict__ gd, double lam, double ridge, int kmax, double* __restrict__ out,
+    const int32_t* __restrict__ order) {
+  extern __shared__ __align__(16) unsigned char gtc_raw[];
+  unsigned char* ring = gtc_raw + ((1024u - (su32(gtc_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t full[kGtcStages], empty[kGtcStages], accb;
+  __shared__ uint32_t tmem_sh;
+  __shared__ float4 geos[32 * 4];   // the source's out-edge geometry (k <= 31)
+  const GramTile T = gts[order ? order[blockIdx.x] : blockIdx.x];
+  const int k = T.ee - T.eb, nc = 6 * k, M = nc + 1;
+  const int Mp = (M + 15) / 16 * 16;
+  const bool two = M > 128;
+  const int N0 = Mp, N1 = two ? Mp - 128 : 0;
+  const int R = gtc_rows(kmax);
+  const uint32_t img = (uint32_t)R * 128, stage_bytes = 2 * img;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t kbase = doff[T.src];
+  const int nch = (T.n1 - T.n0 + 31) / 32;
+  if (warp == kGtcPW) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_sh)),
+                 "n"(kGtcTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int q = 0; q < kGtcStages; ++q) {
+      tc_mbar_init(&full[q], kGtcPW);
+      tc_mbar_init(&empty[q], 1);
+    }
+    tc_mbar_init(&accb, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (tid < 4 * k) geos[tid] = __ldg(reinterpret_cast<const float4*>(geo + T.eb) + tid);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_sh;
+
+  if (warp == kGtcPW) {
+    // ---- MMA issuer
+    if (lane == 0) {
+      const uint32_t id0 = tc_idesc_tf32(N0), id1 = tc_idesc_tf32(two ? N1 : 16);
+      const uint32_t d0 = tmem, d1 = tmem + (uint32_t)N0;
+      for (int c = 0; c < nch; ++c) {
+        const int sidx = c % kGtcStages;
+        tc_mbar_wait(&full[sidx], (uint32_t)(c / kGtcStages) & 1u);
+        tc_fence_after();
+        const uint32_t hi = su32(ring) + (uint32_t)sidx * stage_bytes, lo = hi + img;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {   // 8 tf32 (32 B) of K per MMA
+          const uint32_t o = 32u * kk, acc = (c > 0 || kk > 0) ? 1u : 0u;
+          tc_mma_tf32(d0, tc_sdesc(hi + o), tc_sdesc(hi + o), acc, id0);
+#ifndef VBA_GTC_HHONLY
+          tc_mma_tf32(d0, tc_sdesc(hi + o), tc_sdesc(lo + o), 1u, id0);
+          tc_mma_tf32(d0, tc_sdesc(lo + o), tc_sdesc(hi + o), 1u, id0);
+#endif
+#ifdef VBA_GTC_NOT1
+          if (false) {
+#else
+          if (two) {
+#endif
+            const uint32_t t1 = 128u * 128u;   // row 128 of the images
+            tc_mma_tf32(d1, tc_sdesc(hi + t1 + o), tc_sdesc(hi + t1 + o), acc, id1);
+            tc_mma_tf32(d1, tc_sdesc(hi + t1 + o), tc_sdesc(lo + t1 + o), 1u, id1);
+            tc_mma_tf32(d1, tc_sdesc(lo + t1 + o), tc_sdesc(hi + t1 + o), 1u, id1);
+          }
+        }
+        tc_commit(&empty[sidx]);
+      }
+      tc_commit(&accb);
+    }
+    __syncwarp();
+  } else {
+    // ---- producers: lane = pixel of the chunk, warp w: out-edges w, w + 8, ...
+    // The global loads of chunk c + 1 are issued before chunk c is computed (register
+    // double buffer), so their latency hides under the arithmetic and the ring waits.
+    const float fx = (float)in.fx, fy = (float)in.fy;
+    const float fx2 = fx * fx, fy2 = fy * fy;
+    const float dampf = (float)(1.0 + lam), ridgef = (float)ridge;
+    int64_t ew[kGtcEPW];   // first flow/weight row of each of this warp's out-edges
+#pragma unroll
+    for (int q = 0; q < kGtcEPW; ++q) {
+      const int e = warp + kGtcPW * q;
+      ew[q] = e < k ? eoff[T.eb + e] : 0;
+    }
+    struct Pre { float d, h, g, rx, ry; float2 w[kGtcEPW]; };
+    auto fetch = [&](int c, Pre& p) {
+      const int n = T.n0 + 32 * c + lane;
+      p.d = p.h = p.g = p.rx = p.ry = 0.f;
+#pragma unroll
+      for (int q = 0; q < kGtcEPW; ++q) p.w[q] = make_float2(0.f, 0.f);
+      if (n >= T.n1) return;
+      p.d = disp[kbase + n];
+      p.h = Hdd[kbase + n];
+      if (warp == 0) p.g = gd[kbase + n];
+      if (MODE != VBA_PIX_EDGE) {
+        float rx1, ry1;
+        load_rays<MODE>(pix, kbase, n & ~1, grid_w, gp, in, p.rx, p.ry, rx1, ry1);
+        if (n & 1) { p.rx = rx1; p.ry = ry1; }
+      }
+#pragma unroll
+      for (int q = 0; q < kGtcEPW; ++q)
+        if (warp + kGtcPW * q < k) p.w[q] = __ldg(reinterpret_cast<const float2*>(wts + 2 * (ew[q] + n)));
+    };
+    // W^T[m][lane] = hi + lo: hi = w rounded to 11 significant bits (its low 13 bits are
+    // zero: an exact tf32), lo = w - hi exactly (the tensor core reads lo's leading 11
+    // bits: ~2^-21 relative overall)
+    auto soff = [&](int m) {   // byte offset of W^T[m][lane] in an image
+      return (uint32_t)(m >> 3) * 1024u + (uint32_t)(m & 7) * 128u +
+             ((uint32_t)((lane >> 2) ^ (m & 7)) << 4) + (uint32_t)(lane & 3) * 4u;
+    };
+    auto put = [&](unsigned char* hi, uint32_t off, float w) {
+      const float h = __uint_as_float((__float_as_uint(w) + 0x1000u) & 0xFFFFE000u);
+      *reinterpret_cast<float*>(hi + off) = h;
+      *reinterpret_cast<float*>(hi + img + off) = w - h;
+    };
+    // row m = 6 (warp + 8 q) + r: m & 7 does not depend on q (48 q = 0 mod 8), so the row
+    // offsets are base_r + q * 6 KB with warp-constant base_r
+    uint32_t base[6];
+#pragma unroll
+    for (int r = 0; r < 6; ++r) base[r] = soff(6 * warp + r);
+    const uint32_t goff = soff(nc);
+    Pre cur, nxt;
+    fetch(0, cur);
+    for (int c = 0; c < nch; ++c) {
+      const int sidx = c % kGtcStages;
+      const int n = T.n0 + 32 * c + lane;
+      const bool in_range = n < T.n1;
+      if (c + 1 < nch) fetch(c + 1, nxt);
+      const float sc = in_range ? rsqrtf(fmaf(cur.h, dampf, ridgef)) : 0.f;
+      if (c >= kGtcStages) tc_mbar_wait(&empty[sidx], (uint32_t)(c / kGtcStages - 1) & 1u);
+      unsigned char* hi = ring + (size_t)sidx * stage_bytes;
+#pragma unroll
+      for (int q = 0; q < kGtcEPW; ++q) {
+        const int e = warp + kGtcPW * q;
+        if (e >= k) break;   // warp-uniform
+        float u[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (in_range) {
+          float erx = cur.rx, ery = cur.ry;
+          if (MODE == VBA_PIX_EDGE) {
+            float rx1, ry1;
+            load_rays<VBA_PIX_KF>(pix, ew[q], n & ~1, grid_w, gp, in, erx, ery, rx1, ry1);
+            if (n & 1) { erx = rx1; ery = ry1; }
+          }
+          const EdgeGeo32 ge = load_geo<true>(reinterpret_cast<const EdgeGeo32*>(geos), e);
+          const PxGeom o = project(ge, erx, ery, cur.d);
+          const float w0 = o.valid ? cur.w[q].x : 0.f, w1 = o.valid ? cur.w[q].y : 0.f;
+          const float jd0 = fmaf(o.x, ge.t[2], -ge.t[0]) * o.izh;
+          const float jd1 = fmaf(o.y, ge.t[2], -ge.t[1]) * o.izh;
+          const float c0w = w0 * fx2 * jd0 * sc, c1w = w1 * fy2 * jd1 * sc;
+          const float xy = o.x * o.y;
+          u[0] = fmaf(c0w, xy, c1w * fmaf(o.y, o.y, 1.f));
+          u[1] = fmaf(c0w, -fmaf(o.x, o.x, 1.f), c1w * -xy);
+          u[2] = fmaf(c0w, o.y, c1w * -o.x);
+          u[3] = c0w * -o.iz;
+          u[4] = c1w * -o.iz;
+          u[5] = fmaf(c0w, o.x * o.iz, c1w * (o.y * o.iz));
+        }
+#pragma unroll
+        for (int r = 0; r < 6; ++r) put(hi, base[r] + 6144u * q, u[r]);
+      }
+      if (warp == 0) put(hi, goff, cur.g * sc);
+      proxy_fence_shared();   // generic image writes -> tcgen05 reads
+      __syncwarp();
+      if (lane == 0) tc_mbar_arrive(&full[sidx]);
+      cur = nxt;
+    }
+    // ---- epilogue: warp w reads TMEM lanes 32 (w % 4) .. + 31 (accumulator rows),
+    // column chunks of 32 split between warps w and w + 4; the lower 6x6 blocks
+    // (e1 >= e2) and the b row are scattered into the partial's fp64 layout
+    tc_mbar_wait(&accb, 0u);
+    tc_fence_after();
+    double* o = out + T.out;
+    const int npairs = k * (k + 1) / 2;
+    const int qr = warp & 3, half = warp >> 2, nhalf = kGtcPW / 4;
+    auto cidx = [&](int a, int b) { const int e1 = a / 6, e2 = b / 6;
+                                    return (e1 * (e1 + 1) / 2 + e2) * 36 + (a % 6) * 6 + (b % 6); };
+    const int a0 = 32 * qr + lane;   // tile-0 row
+    for (int cb = 32 * half; cb < N0; cb += 32 * nhalf) {
+      float v[32];
+      tmem_ld32(tmem + ((uint32_t)(32 * qr) << 16) + (uint32_t)cb, v);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int a = a0, b = cb + j;
+        if (b >= M) continue;
+        const double x = (double)v[j];
+        if (a < nc) {
+          if (b < nc) {
+            if (b / 6 <= a / 6) o[cidx(a, b)] = x;
+            if (b >= 128 && a / 6 <= b / 6) o[cidx(b, a)] = x;
+          } else if (nc >= 128) {   // b == nc: row nc lies in tile 1, this is its column a
+            o[npairs * 36 + a] = x;
+          }
+        } else if (a == nc && b < nc) {
+          o[npairs * 36 + b] = x;
+        }
+      }
+    }
+    if (two) {
+      const int a = 128 + a0;
+      for (int cb = 32 * half; cb < N1; cb += 32 * nhalf) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(32 * qr) << 16) + (uint32_t)(N0 + cb), v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int b = 128 + cb + j;
+          if (a >= M || b >= nc) continue;
+          const double x = (double)v[j];
+          if (a < nc) {
+            if (b / 6 <= a / 6) o[cidx(a, b)] = x;
+          } else {
+            o[npairs * 36 + b] = x;
+          }
+        }
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == kGtcPW) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kGtcTmemCols));
+  }
+}
+
+void launch_gram_tc(int mode, const GramTile* gt, int ngt, size_t smem, int kmax, const DevState& s, const float* pix,
+                    const float* wts, const int64_t* eoff, const int64_t* doff, int grid_w, const double* grid,
+                    const double* intr, const float* Hdd, const float* gd, double lam, double ridge,
+                    double* gram_part, cudaStream_t st, const int32_t* order) {
+  if (ngt <= 0) return;
+  GridP gp{grid[0], grid[1], grid[2], grid[3]};
+  IntrP in{intr[0], intr[1], intr[2], intr[3]};
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<ngt, kGtcThreads, smem, st>>>(gt, s.disp, s.geo32, pix, wts, eoff, doff, grid_w, gp, in, Hdd, gd, lam,
+                                          ridge, kmax, gram_part, order);
+  };
+  if (mode == VBA_PIX_GRID) go(k_gram_tc<VBA_PIX_GRID>);
+  else if (mode == VBA_PIX_KF) go(k_gram_tc<VBA_PIX_KF>);
+  else go(k_gram_tc<VBA_PIX_EDGE>);
+  launch_count();
+}
 
 // ---------------------------------------------------------------------------
 // fill-in transform (fp64, one CTA per source): K-space Gram -> pose-space blocks

@@ -738,7 +738,9 @@ class DeviceProblem:
         """[tensor-core solve enabled, fp64 fallbacks, tensor-core solves, refinement passes]."""
         out = (C.c_int64 * 4)()
         L.check(self.lib.vba_stats(self.ctx, out))
-        return dict(zip(("tc_enabled", "fallbacks", "tc_solves", "refine_passes"), list(out)))
+        d = dict(zip(("tc_enabled", "fallbacks", "tc_solves", "refine_passes"), list(out)))
+        d["gram_tc"] = int(self.lib.vba_gram_kind(self.ctx))
+        return d
 
     def upload_inputs(self, H: "HostLayout" = None):
         """Re-upload the per-step inputs (host -> device copies of flow, weights,

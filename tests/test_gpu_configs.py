@@ -207,3 +207,34 @@ def test_solve(cfg, cuda_ok):
     print(f"  final disparities rel err {dmoved:.2e}")
     assert dmoved < TOL_DX
     assert st["fallbacks"] == 0
+
+
+@pytest.mark.parametrize("cfg", [c for c in (1, 3) if c in CFGS], ids=lambda c: f"cfg{c}")
+def test_gram_paths(cfg, cuda_ok, monkeypatch):
+    """Both Schur Gram kernels at full size: the tcgen05 3xTF32 one (the default here, >= 256
+    pixels per keyframe) and the exact fp64 DMMA one (VBA_GRAM=dmma; the default for small
+    windows) meet the north_star tolerances against the reference, and agree with each other
+    far inside them (the tf32 split keeps ~21 significant bits per factor)."""
+    P, G = problem(cfg)
+    opts = opts_of(G)
+    out = {}
+    for kind in ("tc", "dmma"):
+        monkeypatch.setenv("VBA_GRAM", kind)
+        dp = _dp(P, opts)
+        assert dp.stats()["gram_tc"] == (kind == "tc")
+        dp.linearize()
+        Hr, gr = dp.export_reduced(opts["damping"])
+        dx, dxd = dp.solve_step(opts["damping"])
+        dp.close()
+        e, _ = mat_err(G, "Hred", Hr)
+        ex = float(np.abs(dx - G["dx"]).max() / np.abs(G["dx"]).max())
+        ed = vec_err(G, "dxd", dxd)
+        print(f"cfg{cfg} gram {kind}: H_red {e:.2e} dx {ex:.2e} dx_d {ed:.2e}")
+        assert e < TOL_H and ex < TOL_DX and ed < TOL_DX
+        out[kind] = (Hr, dx, dxd)
+    (h1, x1, d1), (h0, x0, d0) = out["tc"], out["dmma"]
+    dh = float(np.abs(h1 - h0).max() / np.abs(h0).max())
+    dxx = float(np.abs(x1 - x0).max() / np.abs(x0).max())
+    ddd = float(np.abs(d1 - d0).max() / np.abs(d0).max())
+    print(f"cfg{cfg} tc vs dmma: H_red {dh:.2e} dx {dxx:.2e} dx_d {ddd:.2e}")
+    assert dh < 1e-7 and dxx < 1e-6 and ddd < 1e-6
