@@ -1153,127 +1153,9 @@ __device__ void tc_task_syrk_smem(const TcArgs& a, TcRing& R, uint64_t* accf, ui
 // POTRF(k) of the tensor-core DAG, fp32 (the factor is fp32-accurate anyway;
 // iterative refinement restores fp64).  Shared-memory layout (floats):
 //   Ws  128 x 128 column-major, stride SWF: the tile, then L (lower)
-//   Xs  4 x 4 blocks of 32x32 (row-major, stride XBS): X = L^-1 blocks (i >= j)
-//   Ts  32x32 temporary (stride XBS)
+//   Xf  128 x 128 row-major, stride SWF: Y = L^-1
 // ---------------------------------------------------------------------------
 constexpr int SWF = CT + 4;      // 132: float4-aligned columns
-constexpr int XBS = 36;          // 32x32 block row stride (float4-aligned)
-
-// Cholesky + inverse of a 32x32 SPD block by Gaussian elimination of the
-// augmented [A | I] without pivoting (stable for SPD): A = Lt U, U = diag(p) Lt^T,
-// so L = Lt diag(p)^1/2 and L^-1 = diag(p)^-1/2 Lt^-1 (the I half becomes Lt^-1).
-// Thread t owns row i = t / 8 and 8 columns of one half (t % 8 < 4: A columns,
-// else I columns) in registers; one barrier per step: the owners of column j+1
-// (A half) and row j+1 (I half) publish them, with the next pivot's rsqrt, into
-// double buffers.  A (column-major, stride sw) gets L; X (row-major, XBS) L^-1.
-__device__ __forceinline__ void cta_ge32(float* A, int sw, float* X, float* buf, int* bad) {
-  // warp-uniform halves: threads 0..127 own A columns, 128..255 I columns
-  const int t = threadIdx.x, i = (t & 127) >> 2, g = (t & 3) + 4 * (t >> 7);
-  const bool ahalf = t < 128;
-  const int cb = 8 * (g & 3);
-  float* pv = buf + 128;     // [2][2]: pivot, rsqrt(pivot)
-  float* rsv = buf + 132;    // [32]: rsqrt of every pivot
-  float e[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int c = cb + q;
-    e[q] = ahalf ? (c <= i ? A[c * sw + i] : 0.f) : (c == i ? 1.f : 0.f);
-  }
-  if (ahalf && g == 0) {
-    buf[i] = e[0];
-    if (i == 0) {
-      float p = e[0];
-      if (!(p > 0.f)) { *bad = 1; p = 1.f; }
-      pv[0] = p;
-      pv[1] = rsqrtf(p);
-    }
-  }
-  if (!ahalf && i == 0) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) buf[64 + cb + q] = e[q];
-  }
-  __syncthreads();
-#pragma unroll 1
-  for (int j = 0; j < 32; ++j) {
-    const int sb = j & 1, nb = sb ^ 1;
-    const float* col = buf + sb * 32;
-    const float* row = buf + 64 + sb * 32;
-    const float2 prs = *reinterpret_cast<const float2*>(pv + 2 * sb);   // pivot, rsqrt(pivot)
-    const float p = prs.x, rs = prs.y;
-    const float ci = col[i];
-    const float f = (i > j) ? ci * (rs * rs) : 0.f;   // multiplier Lt[i][j]
-    if (ahalf) {
-      // critical path first: the owners of column j+1 publish its updated entries
-      // (and the diagonal owner the next pivot) before the rest of the update
-      const int qn = (j + 1) & 7;
-      if (j + 1 < 32 && ((j + 1) >> 3) == (g & 3) && i >= j + 1) {
-        float en = e[0];
-#pragma unroll
-        for (int q = 1; q < 8; ++q) en = (q == qn) ? e[q] : en;
-        const float vn = fmaf(-f, col[j + 1], en);
-        buf[nb * 32 + i] = vn;
-        if (i == j + 1) {
-          float pn = vn;
-          if (!(pn > 0.f)) { *bad = 1; pn = 1.f; }
-          *reinterpret_cast<float2*>(pv + 2 * nb) = make_float2(pn, rsqrtf(pn));
-        }
-      }
-      const float lij = (i > j) ? ci * rs : (i == j ? p * rs : 0.f);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int c = cb + q;
-        if (c > j && c <= i) e[q] = fmaf(-f, col[c], e[q]);
-        if (c == j) e[q] = lij;   // final L[i][j]
-      }
-    } else {
-      if (i == j + 1) {   // row j+1 of the I half: final update first, then publish
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (cb + q <= j) e[q] = fmaf(-f, row[cb + q], e[q]);
-        *reinterpret_cast<float4*>(buf + 64 + nb * 32 + cb) = make_float4(e[0], e[1], e[2], e[3]);
-        *reinterpret_cast<float4*>(buf + 64 + nb * 32 + cb + 4) = make_float4(e[4], e[5], e[6], e[7]);
-      } else {
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (cb + q <= j) e[q] = fmaf(-f, row[cb + q], e[q]);
-      }
-    }
-    if (t == 0) rsv[j] = rs;
-    __syncthreads();
-  }
-  if (ahalf) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) A[(cb + q) * sw + i] = (cb + q <= i) ? e[q] : 0.f;
-  } else {
-    const float s = rsv[i];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) X[i * XBS + cb + q] = (cb + q <= i) ? e[q] * s : 0.f;
-  }
-  __syncthreads();
-}
-
-// C (32x32, row-major XBS) = alpha * A B (+ C if acc), A(r, m) = A[r * ars + m * ams],
-// B(m, c) = B[m * bms + c * bcs]; 256 threads, 2x2 outputs each.  Caller syncs.
-__device__ __forceinline__ void blk32_gemm(float* C, const float* A, int ars, int ams, const float* B, int bms,
-                                           int bcs, float alpha, bool acc) {
-  const int t = threadIdx.x, r = 2 * (t >> 4), c = 2 * (t & 15);
-  float s00 = 0.f, s01 = 0.f, s10 = 0.f, s11 = 0.f;
-#pragma unroll 8
-  for (int m = 0; m < 32; ++m) {
-    const float a0 = A[r * ars + m * ams], a1 = A[(r + 1) * ars + m * ams];
-    const float b0 = B[m * bms + c * bcs], b1 = B[m * bms + (c + 1) * bcs];
-    s00 = fmaf(a0, b0, s00);
-    s01 = fmaf(a0, b1, s01);
-    s10 = fmaf(a1, b0, s10);
-    s11 = fmaf(a1, b1, s11);
-  }
-  float* o = C + r * XBS + c;
-  if (acc) {
-    o[0] += alpha * s00; o[1] += alpha * s01; o[XBS] += alpha * s10; o[XBS + 1] += alpha * s11;
-  } else {
-    o[0] = alpha * s00; o[1] = alpha * s01; o[XBS] = alpha * s10; o[XBS + 1] = alpha * s11;
-  }
-}
 
 // 8x8 Cholesky + inverse of the diagonal block at (c0, c0) by ONE thread in
 // registers (no barriers): L overwrites the block of Ws (column-major, upper part
