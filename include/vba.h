@@ -249,6 +249,18 @@ VBA_API int vba_preintegrate(const double* ts, const double* gyro, const double*
 VBA_API int vba_preint_factor_records(const double* rec, const double* bias, int32_t n_pairs, double* imu,
                                       void* stream);
 
+/* Batched device-to-device segment copy (the device-resident tracking window's gather
+ * of per-keyframe / per-edge buffers into the solver's packed layout and the scatter of
+ * solved disparities back, frontend.py:341-482 without host round trips): `segs` is a
+ * DEVICE array of n records {src, dst, bytes}; one launch for all of them.
+ * Stream-ordered, no synchronisation. */
+typedef struct vba_copy_seg {
+  const void* src;
+  void* dst;
+  int64_t bytes;
+} vba_copy_seg;
+VBA_API int vba_copy_segments(const vba_copy_seg* segs, int32_t n, void* stream);
+
 /* ------------------------------------------------------------------------
  * Sim(3) pose-graph BA (PGBA), replacing vislam.loopclosure.solve_pgba
  * (loopclosure.py:502-574) and its callees: total_pg_energy (:378-390),

@@ -24,9 +24,13 @@ EXPORTED = ("vba_last_error", "vba_version", "vba_create", "vba_destroy", "vba_s
             "vba_trial", "vba_solve", "vba_download", "vba_launch_count", "vba_stage_times",
             "vba_load_state", "vba_bind_inputs", "vba_set_profiling", "vba_stats", "vba_gram_kind", "vba_spd_solve", "vba_solve_times",
             "vba_preintegrate", "vba_preint_scratch_bytes",
-            "vba_preint_factor_records",
+            "vba_preint_factor_records", "vba_copy_segments",
             "vba_pg_create", "vba_pg_destroy", "vba_pg_energy", "vba_pg_linearize", "vba_pg_export_normal_eq",
             "vba_pg_solve_step", "vba_pg_export_step", "vba_pg_solve", "vba_pg_download", "vba_init_inertial")
+
+
+class VbaCopySeg(C.Structure):
+    _fields_ = [("src", C.c_void_p), ("dst", C.c_void_p), ("bytes", C.c_int64)]
 
 
 class VbaProblem(C.Structure):
@@ -152,6 +156,7 @@ def load(path: str | None = None):
         "vba_set_profiling": ([v, C.c_int32], C.c_int),
         "vba_stats": ([v, C.POINTER(C.c_int64)], C.c_int),
         "vba_gram_kind": ([v], C.c_int),
+        "vba_copy_segments": ([v, C.c_int32, v], C.c_int),
         "vba_solve_times": ([v, C.POINTER(C.c_double)], C.c_int),
         "vba_spd_solve": ([v, C.c_int64, v, v, C.c_int32, v, C.POINTER(C.c_int32)], C.c_int),
         "vba_preintegrate": ([v, v, v, C.c_int64, v, C.c_int32, v, v, v, v, v], C.c_int),
@@ -175,6 +180,19 @@ def load(path: str | None = None):
         fn.restype = res
     _lib = lib
     return lib
+
+
+_CUDA_OK = None
+
+
+def cuda_available() -> bool:
+    """torch.cuda.is_available(), evaluated once per process (each call of the torch
+    function queries the driver: ~1 ms, the whole budget of a small window solve)."""
+    global _CUDA_OK
+    if _CUDA_OK is None:
+        import torch
+        _CUDA_OK = bool(torch.cuda.is_available())
+    return _CUDA_OK
 
 
 def check(rc: int):

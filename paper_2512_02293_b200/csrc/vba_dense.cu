@@ -187,4 +187,28 @@ void launch_scatter_dx(const double* x, const int32_t* fmap, int npv, double* dx
   launch_count();
 }
 
+// Batched segment copy (vba_copy_segments): one CTA per segment, 16-byte vectors when
+// source, destination and length allow, else 4-byte words, else bytes.
+__global__ void k_copy_segments(const vba_copy_seg* __restrict__ segs) {
+  const vba_copy_seg g = segs[blockIdx.x];
+  const uintptr_t a = (uintptr_t)g.src | (uintptr_t)g.dst | (uintptr_t)g.bytes;
+  if ((a & 15) == 0) {
+    const int4* s = reinterpret_cast<const int4*>(g.src);
+    int4* d = reinterpret_cast<int4*>(g.dst);
+    for (int64_t i = threadIdx.x; i < g.bytes / 16; i += blockDim.x) d[i] = s[i];
+  } else if ((a & 3) == 0) {
+    const int* s = reinterpret_cast<const int*>(g.src);
+    int* d = reinterpret_cast<int*>(g.dst);
+    for (int64_t i = threadIdx.x; i < g.bytes / 4; i += blockDim.x) d[i] = s[i];
+  } else {
+    const char* s = reinterpret_cast<const char*>(g.src);
+    char* d = reinterpret_cast<char*>(g.dst);
+    for (int64_t i = threadIdx.x; i < g.bytes; i += blockDim.x) d[i] = s[i];
+  }
+}
+void launch_copy_segments(const vba_copy_seg* segs, int n, cudaStream_t st) {
+  k_copy_segments<<<n, 256, 0, st>>>(segs);
+  launch_count();
+}
+
 }  // namespace vba

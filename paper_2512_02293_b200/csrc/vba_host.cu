@@ -1292,6 +1292,17 @@ int vba_preint_factor_records(const double* rec, const double* bias, int32_t n_p
   return VBA_OK;
 }
 
+int vba_copy_segments(const vba_copy_seg* segs, int32_t n, void* stream) {
+  if (n < 0 || (n > 0 && !segs)) {
+    set_err("vba_copy_segments: invalid arguments");
+    return VBA_E_INVALID;
+  }
+  if (n == 0) return VBA_OK;
+  launch_copy_segments(segs, n, (cudaStream_t)stream);
+  VBA_CUDA(cudaGetLastError());
+  return VBA_OK;
+}
+
 int vba_energy(void* ctx, void* stream, double* tot, double* vis, double* ine) {
   Ctx* c = (Ctx*)ctx;
   cudaStream_t st = (cudaStream_t)stream;

@@ -295,6 +295,7 @@ void launch_step_edges(const int32_t* ei, const int32_t* ej, int E, const DevSta
                        const double* dx_full, int sdof, float* ustep, cudaStream_t st);
 size_t gram_smem_bytes(int kmax, int nsplit, int npairs, int k);
 size_t gram_tc_smem_bytes(int kmax);
+void launch_copy_segments(const vba_copy_seg* segs, int n, cudaStream_t st);
 void launch_gram_tc(int pixel_mode, const GramTile* gt, int ngt, size_t smem, int kmax, const DevState& s,
                     const float* pix, const float* wts, const int64_t* eoff, const int64_t* doff, int grid_w,
                     const double* grid, const double* intr, const float* Hdd, const float* gd, double lam,

@@ -29,7 +29,7 @@ from . import _lib as L
 
 
 def _require_cuda():
-    if not torch.cuda.is_available():
+    if not L.cuda_available():
         raise RuntimeError("paper_2512_02293_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
 
 
@@ -259,7 +259,7 @@ class HostLayout:
     @classmethod
     def from_graph(cls, graph, opts, pinned=None):
         if pinned is None:
-            pinned = torch.cuda.is_available()
+            pinned = L.cuda_available()
         return cls(None, opts, pinned=pinned, _src=_GraphSource(graph))
 
     def _build(self, S, opts, edge_subset, imu_subset, pinned):

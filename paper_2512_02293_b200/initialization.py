@@ -59,7 +59,7 @@ def init_inertial_only(graph, cfg=None):
     n = len(kfs)
     if n < 2 or not graph.inertial_edges:
         raise ValueError("need at least two keyframes with inertial edges")
-    if not torch.cuda.is_available():
+    if not L.cuda_available():
         raise RuntimeError("paper_2512_02293_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
     index = {kf.kid: k for k, kf in enumerate(kfs)}
     lib = L.load()

@@ -108,7 +108,7 @@ class DevicePoseGraph:
 
     def __init__(self, P, opts: dict, stream=None):
         import torch
-        if not torch.cuda.is_available():
+        if not L.cuda_available():
             raise RuntimeError("paper_2512_02293_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
         self.lib = L.load()
         self.P = P

@@ -31,6 +31,7 @@ from collections import OrderedDict
 import numpy as np
 import torch
 
+from . import _lib as L
 from .device import DeviceProblem, HostLayout
 from .problem import options_dict, write_back
 from .types import SolveOptions, SolveReport
@@ -61,7 +62,7 @@ def _topology_key(H: HostLayout, o: dict, dev: int):
 
 
 def _problem_for(graph, o: dict) -> DeviceProblem:
-    if not torch.cuda.is_available():
+    if not L.cuda_available():
         raise RuntimeError("paper_2512_02293_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
     H = HostLayout.from_graph(graph, o)
     dev = torch.cuda.current_device()

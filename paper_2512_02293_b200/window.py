@@ -25,6 +25,7 @@ drop-in ``solver.solve_vi_ba`` on the same graph (same packed layout, same kerne
 
 from __future__ import annotations
 
+import ctypes as C
 import hashlib
 from collections import OrderedDict
 
@@ -74,6 +75,58 @@ def _imu_record(d):
     return r
 
 
+class _Staging:
+    """Page-locked host staging for the window's uploads: insertions copy into it and
+    enqueue asynchronous host->device copies on the current stream (no synchronising
+    pageable copy per array); the buffer is recycled once the stream has drained them."""
+
+    def __init__(self, device, nbytes=1 << 22):
+        self.device = device
+        self.buf = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        self.off = 0
+        self.ev = None
+
+    def put(self, a: np.ndarray, dtype) -> torch.Tensor:
+        a = np.ascontiguousarray(a)
+        n = a.nbytes
+        if n == 0:
+            return torch.empty(0, dtype=dtype, device=self.device)
+        if self.off + n > self.buf.numel():
+            self.recycle(wait=True)
+            if n > self.buf.numel():
+                self.buf = torch.empty(max(n, 2 * self.buf.numel()), dtype=torch.uint8, pin_memory=True)
+        if self.off == 0 and self.ev is not None:   # earlier copies out of this buffer must be done
+            self.ev.synchronize()
+            self.ev = None
+        o = (self.off + 255) // 256 * 256
+        host = self.buf[o:o + n]
+        host.numpy()[:] = a.view(np.uint8).reshape(-1)
+        dev = torch.empty(n // np.dtype(a.dtype).itemsize, dtype=dtype, device=self.device)
+        dev.view(torch.uint8).copy_(host, non_blocking=True)
+        self.off = o + n
+        return dev
+
+    def recycle(self, wait=False):
+        """Start over at the head of the buffer (after the copies queued so far)."""
+        if self.off:
+            self.ev = torch.cuda.Event()
+            self.ev.record(torch.cuda.current_stream(self.device))
+            if wait:
+                self.ev.synchronize()
+                self.ev = None
+        self.off = 0
+
+
+def _segments(segs, device, stage: "_Staging"):
+    """One vba_copy_segments launch for a list of (src, dst, bytes) device copies."""
+    if not segs:
+        return
+    tab = np.array(segs, dtype=np.int64).reshape(-1, 3)
+    d = stage.put(tab, torch.int64)
+    L.check(L.load().vba_copy_segments(C.c_void_p(d.data_ptr()), len(segs),
+                                       C.c_void_p(torch.cuda.current_stream(device).cuda_stream)))
+
+
 class _WinLayout:
     """The attributes DeviceProblem reads from a HostLayout, with the bulk arrays on the device."""
 
@@ -87,7 +140,7 @@ class DeviceWindow:
     """A sliding VI-BA window resident on one GPU (frontend.py:341-482 semantics)."""
 
     def __init__(self, intrinsics, gravity=None, T_cb=None, window_size=12, device=None, cache_size=4):
-        if not torch.cuda.is_available():
+        if not L.cuda_available():
             raise RuntimeError("paper_2512_02293_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         k = intrinsics
@@ -108,6 +161,7 @@ class DeviceWindow:
         self._cache: "OrderedDict[tuple, DeviceProblem]" = OrderedDict()
         self.cache_size = cache_size
         self.h2d_bytes = 0          # bulk bytes uploaded by insertions (instrumentation)
+        self._stage = _Staging(self.device)
         self.solves = 0
         self.replans = 0
 
@@ -121,7 +175,7 @@ class DeviceWindow:
             raise ValueError("disparities must be positive")
         if kid in self.kfs:
             raise ValueError(f"keyframe {kid} is already in the window")
-        t = torch.from_numpy(np.ascontiguousarray(d)).to(self.device)
+        t = self._stage.put(d, torch.float64)
         self.h2d_bytes += d.nbytes
         self.kfs[kid] = _Kf(kid, _state16(state), float(state.timestamp), pixels, t)
 
@@ -141,8 +195,8 @@ class DeviceWindow:
         flow = (targets - pixels).astype(np.float32)   # u* - u: fp64 difference, one rounding
         w = weights.astype(np.float32)
         same = np.array_equal(pixels, self.kfs[i].pixels)
-        e = _Edge(i, j, torch.from_numpy(flow.reshape(-1)).to(self.device),
-                  torch.from_numpy(w.reshape(-1)).to(self.device), None if same else pixels)
+        e = _Edge(i, j, self._stage.put(flow.reshape(-1), torch.float32),
+                  self._stage.put(w.reshape(-1), torch.float32), None if same else pixels)
         self.h2d_bytes += flow.nbytes + w.nbytes
         self.edges.append(e)
 
@@ -245,18 +299,23 @@ class DeviceWindow:
         return (Ly.K, Ly.E, Ly.F, Ly.mode, Ly.grid, Ly.has_Tcb, opts, h.hexdigest())
 
     def _pack_into(self, Ly, tgt, w, disp64):
-        """Device-to-device gather of the window into the packed solver layout."""
+        """Device-to-device gather of the window into the packed solver layout (one
+        vba_copy_segments launch; padding rows weight 0, padding disparities 1)."""
         w.zero_()
         tgt.zero_()
         disp64.fill_(1.0)
+        segs = []
+        tp, wp, dp = tgt.data_ptr(), w.data_ptr(), disp64.data_ptr()
         for slot, q in enumerate(Ly.order):
             e = self.edges[q]
-            o = 2 * int(Ly.eoff_pad[slot])
-            tgt[o:o + e.flow.numel()].copy_(e.flow)
-            w[o:o + e.w.numel()].copy_(e.w)
+            o = 8 * int(Ly.eoff_pad[slot])   # 2 floats per row
+            nb = 4 * e.flow.numel()
+            segs.append((e.flow.data_ptr(), tp + o, nb))
+            segs.append((e.w.data_ptr(), wp + o, nb))
         for n, k in enumerate(Ly.kids):
-            o = int(Ly.doff_pad[n])
-            disp64[o:o + self.kfs[k].n].copy_(self.kfs[k].disp)
+            kf = self.kfs[k]
+            segs.append((kf.disp.data_ptr(), dp + 8 * int(Ly.doff_pad[n]), 8 * kf.n))
+        _segments(segs, self.device, self._stage)
 
     def solve(self, opts=None, use_inertial=True) -> SolveReport:
         """``solve_vi_ba`` on the window (the tracker's per-keyframe solve, frontend.py:435-450:
@@ -272,6 +331,7 @@ class DeviceWindow:
         dp = self._cache.pop(key, None)
         dev = self.device
         if dp is not None:
+            dp.stream.wait_stream(torch.cuda.current_stream(dev))   # the staged insert copies
             with torch.cuda.stream(dp.stream):
                 self._pack_into(Ly, dp.d_tgt, dp.d_w, dp.d_disp64)
             Ly.tgt, Ly.w, Ly.disp64 = dp.d_tgt, dp.d_w, dp.d_disp64
@@ -290,16 +350,17 @@ class DeviceWindow:
         self.solves += 1
         if rep["iterations"] > 0:
             L.check(dp.lib.vba_download(dp.ctx, dp._sptr()))
-            with torch.cuda.stream(dp.stream):
-                for n, k in enumerate(Ly.kids):   # solved disparities stay on the device
-                    o0 = int(Ly.doff_pad[n])
-                    self.kfs[k].disp.copy_(dp.d_disp64[o0:o0 + self.kfs[k].n])
+            with torch.cuda.stream(dp.stream):   # solved disparities stay on the device
+                base = dp.d_disp64.data_ptr()
+                _segments([(base + 8 * int(Ly.doff_pad[n]), self.kfs[k].disp.data_ptr(), 8 * self.kfs[k].n)
+                           for n, k in enumerate(Ly.kids)], dev, self._stage)
             st = dp.d_state.cpu().numpy()
             for n, k in enumerate(Ly.kids):
                 if not Ly.frozen[n]:
                     self.kfs[k].state = st[n].copy()
             if opts.optimize_gravity:
                 self.grav = dp.d_grav.cpu().numpy().copy()
+        self._stage.recycle()
         return SolveReport(rep["iterations"], rep["initial_cost"], rep["final_cost"], rep["cost_trajectory"],
                            rep["termination"], rep["condition_warnings"])
 

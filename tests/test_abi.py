@@ -74,7 +74,7 @@ def _c_layout(struct, fields):
                                         ("VbaReport", "vba_report"), ("VbaTrialResult", "vba_trial_result"),
                                         ("VbaPgProblem", "vba_pg_problem"), ("VbaInitProblem", "vba_init_problem"),
                                         ("VbaInitOptions", "vba_init_options"),
-                                        ("VbaInitResult", "vba_init_result")])
+                                        ("VbaInitResult", "vba_init_result"), ("VbaCopySeg", "vba_copy_seg")])
 def test_ctypes_struct_layout_matches_c(cls, struct):
     from paper_2512_02293_b200 import _lib
     S = getattr(_lib, cls)
@@ -100,3 +100,5 @@ def test_preintegration_entry_points_without_gpu(lib):
     assert L.vba_preintegrate(None, None, None, 10, None, 2, None, None, None, None, None) == 1    # null buffers
     assert L.vba_preint_factor_records(None, None, 0, None, None) == 0
     assert L.vba_preint_factor_records(None, None, 3, None, None) == 1
+    assert L.vba_copy_segments(None, 0, None) == 0      # nothing to copy: no device touched
+    assert L.vba_copy_segments(None, 2, None) == 1      # null segment table
