@@ -26,6 +26,8 @@
 
 namespace vba {
 
+constexpr int kInit2SmemDim = 160;   // k_init2_solve keeps A (+ b) in shared memory up to this size
+
 // virtual keyframe states [K,16] of the stage-2 estimate: q (vision), exp(s) p, v, shared bias
 __global__ void k_init2_states(const double* __restrict__ q, const double* __restrict__ p, const double* __restrict__ v,
                                const double* __restrict__ x, int K, double* __restrict__ state,
@@ -80,36 +82,46 @@ __global__ void k_init2_energy(const double* __restrict__ rec, int F, double* __
 // (H + diag(H) lam + 1e-10 I) dx = -g (initialization.py:194-196), LU with partial pivoting in
 // A (dim x dim row-major scratch); status 1 on an exactly zero pivot (numpy's LinAlgError)
 __global__ void __launch_bounds__(256) k_init2_solve(const double* __restrict__ H, const double* __restrict__ g,
-                                                     int dim, double lam, double* __restrict__ A,
+                                                     int dim, double lam, double* __restrict__ Ag,
                                                      double* __restrict__ dx, int* __restrict__ status) {
-  const int tid = threadIdx.x, nth = blockDim.x;
+  // the working matrix lives in shared memory when it fits (dim <= 160), else in Ag
+  extern __shared__ double A_s[];
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  double* A = dim <= kInit2SmemDim ? A_s : Ag;
+  double* b = dim <= kInit2SmemDim ? A_s + dim * dim : dx;
   __shared__ int piv;
-  __shared__ double pval[256];
-  __shared__ int pidx[256];
+  __shared__ double wval[8];
+  __shared__ int widx[8];
   for (int t = tid; t < dim * dim; t += nth) {
     const int r = t / dim, c = t % dim;
     double v = H[t];
     if (r == c) v = v + H[t] * lam + 1e-10;
     A[t] = v;
   }
-  for (int r = tid; r < dim; r += nth) dx[r] = -g[r];
+  for (int r = tid; r < dim; r += nth) b[r] = -g[r];
   if (tid == 0) *status = 0;
   __syncthreads();
   for (int k = 0; k < dim; ++k) {
+    // pivot: first maximum of |A[r][k]|, r >= k (idamax), by a warp tree then the warp maxima
     double best = -1.0;
     int bi = dim;
     for (int r = k + tid; r < dim; r += nth) {
-      const double a = fabs(A[(int64_t)r * dim + k]);
-      if (a > best) { best = a; bi = r; }
+      const double v = fabs(A[r * dim + k]);
+      if (v > best) { best = v; bi = r; }
     }
-    pval[tid] = best;
-    pidx[tid] = bi;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    }
+    if (lane == 0) { wval[warp] = best; widx[warp] = bi; }
     __syncthreads();
-    if (tid == 0) {   // first maximum, like idamax
+    if (tid == 0) {
       double bv = -1.0;
       int br = dim;
-      for (int t = 0; t < nth; ++t)
-        if (pval[t] > bv || (pval[t] == bv && pidx[t] < br)) { bv = pval[t]; br = pidx[t]; }
+      for (int w = 0; w < nth / 32; ++w)
+        if (wval[w] > bv || (wval[w] == bv && widx[w] < br)) { bv = wval[w]; br = widx[w]; }
       piv = br;
       if (!(bv > 0.0)) *status = 1;
     }
@@ -118,32 +130,44 @@ __global__ void __launch_bounds__(256) k_init2_solve(const double* __restrict__ 
     const int p = piv;
     if (p != k) {
       for (int c = tid; c < dim; c += nth) {
-        const double t = A[(int64_t)k * dim + c];
-        A[(int64_t)k * dim + c] = A[(int64_t)p * dim + c];
-        A[(int64_t)p * dim + c] = t;
+        const double t = A[k * dim + c];
+        A[k * dim + c] = A[p * dim + c];
+        A[p * dim + c] = t;
       }
       if (tid == 0) {
-        const double t = dx[k];
-        dx[k] = dx[p];
-        dx[p] = t;
+        const double t = b[k];
+        b[k] = b[p];
+        b[p] = t;
       }
+      __syncthreads();
     }
+    // multipliers, then the rank-1 update element-parallel (each element: one fma per k,
+    // in k order -- the same arithmetic as the row-serial form)
+    const double inv = 1.0 / A[k * dim + k];
+    const int m = dim - k - 1;
+    for (int r = k + 1 + tid; r < dim; r += nth) A[r * dim + k] *= inv;
     __syncthreads();
-    const double inv = 1.0 / A[(int64_t)k * dim + k];
-    for (int r = k + 1 + tid; r < dim; r += nth) {
-      const double f = A[(int64_t)r * dim + k] * inv;
-      A[(int64_t)r * dim + k] = f;
-      for (int c = k + 1; c < dim; ++c) A[(int64_t)r * dim + c] -= f * A[(int64_t)k * dim + c];
-      dx[r] -= f * dx[k];
+    for (int t = tid; t < m * m; t += nth) {
+      const int r = k + 1 + t / m, c = k + 1 + t % m;
+      A[r * dim + c] -= A[r * dim + k] * A[k * dim + c];
     }
+    for (int r = k + 1 + tid; r < dim; r += nth) b[r] -= A[r * dim + k] * b[k];
     __syncthreads();
   }
-  if (tid == 0)
+  // back substitution: warp 0, row dot products as warp trees (fixed order)
+  if (warp == 0) {
     for (int k = dim - 1; k >= 0; --k) {
-      double v = dx[k];
-      for (int c = k + 1; c < dim; ++c) v -= A[(int64_t)k * dim + c] * dx[c];
-      dx[k] = v / A[(int64_t)k * dim + k];
+      double v = 0.0;
+      for (int c = k + 1 + lane; c < dim; c += 32) v += A[k * dim + c] * b[c];
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) b[k] = (b[k] - v) / A[k * dim + k];
+      __syncwarp();
     }
+  }
+  __syncthreads();
+  if (b != dx)
+    for (int r = tid; r < dim; r += nth) dx[r] = b[r];
 }
 
 // trial estimate from dx (initialization.py:197-201): x = [s, 0, 0, bias(6)], gravity, velocities
@@ -183,14 +207,25 @@ int vba_init_inertial(const vba_init_problem* P, const vba_init_options* O, void
     return VBA_E_INVALID;
   }
   const int dim = 9 + 3 * K;
-  std::vector<void*> al;
+  // one device allocation per call, carved into the buffers below (256-B aligned)
+  size_t need = 0;
+  const size_t sizes[] = {sizeof(double) * kImuL * F, sizeof(double) * 16 * K, sizeof(double) * kInit2Rec * F,
+                          sizeof(double) * dim * dim, sizeof(double) * dim, sizeof(double) * dim * dim,
+                          sizeof(double) * dim, sizeof(double), sizeof(double), sizeof(int) * 2,
+                          sizeof(int32_t) * F, sizeof(int32_t) * F, sizeof(double) * 9, sizeof(double) * 5,
+                          sizeof(double) * 3 * K, sizeof(double) * 9, sizeof(double) * 5, sizeof(double) * 3 * K};
+  for (size_t z : sizes) need += (z + 255) / 256 * 256;
+  char* arena = nullptr;
+  size_t used = 0;
+  if (cudaMallocAsync((void**)&arena, need, st) != cudaSuccess) arena = nullptr;
   auto alloc = [&](void** p, size_t bytes) {
-    if (cudaMalloc(p, bytes) != cudaSuccess) return false;
-    al.push_back(*p);
-    return true;
+    if (!arena) return false;
+    *p = arena + used;
+    used += (bytes + 255) / 256 * 256;
+    return used <= need;
   };
   auto cleanup = [&]() {
-    for (void* p : al) cudaFree(p);
+    if (arena) cudaFreeAsync(arena, st);
   };
   double *L, *state, *rec, *H, *g, *A, *dx, *x[2], *gr[2], *v[2], *es, *cost;
   int32_t *fi, *fj;
@@ -209,6 +244,9 @@ int vba_init_inertial(const vba_init_problem* P, const vba_init_options* O, void
     vba_set_error_string("vba_init_inertial: allocation failed");
     return VBA_E_CUDA;
   }
+  const size_t solve_smem = dim <= kInit2SmemDim ? sizeof(double) * ((size_t)dim * dim + dim) : 0;
+  if (solve_smem > 48 * 1024)
+    cudaFuncSetAttribute(k_init2_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)solve_smem);
   double hx[9] = {0, 0, 0, P->bias0[0], P->bias0[1], P->bias0[2], P->bias0[3], P->bias0[4], P->bias0[5]};
   double hg[5] = {P->grav_q[0], P->grav_q[1], P->grav_q[2], P->grav_q[3], P->grav_G};
   cudaMemcpyAsync(x[0], hx, sizeof(hx), cudaMemcpyHostToDevice, st);
@@ -253,7 +291,7 @@ int vba_init_inertial(const vba_init_problem* P, const vba_init_options* O, void
     k_init2_assemble<<<dim, 128, 0, st>>>(rec, fi, fj, F, dim, H, g);
     bool accepted = false;
     while (lam <= 1e8) {
-      k_init2_solve<<<1, 256, 0, st>>>(H, g, dim, lam, A, dx, status);
+      k_init2_solve<<<1, 256, solve_smem, st>>>(H, g, dim, lam, A, dx, status);
       cudaMemcpyAsync(hs, status, sizeof(int), cudaMemcpyDeviceToHost, st);
       if (sync_err("solve")) { cleanup(); return VBA_E_CUDA; }
       if (hs[0]) break;   // np.linalg.LinAlgError (initialization.py:195-196)
