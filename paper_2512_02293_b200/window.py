@@ -38,11 +38,12 @@ from .types import SolveOptions, SolveReport
 
 
 class _Kf:
-    __slots__ = ("kid", "state", "ts", "pixels", "disp", "n")
+    __slots__ = ("kid", "state", "ts", "pixels", "disp", "n", "grid")
 
     def __init__(self, kid, state16, ts, pixels, disp):
         self.kid, self.state, self.ts, self.pixels, self.disp = kid, state16, ts, pixels, disp
         self.n = len(pixels)
+        self.grid = _grid_params(pixels) if self.n else None   # detected once, at insertion
 
 
 class _Edge:
@@ -263,7 +264,7 @@ class DeviceWindow:
             mode = L.PIX_EDGE
         else:
             for k in kids:
-                g = _grid_params(self.kfs[k].pixels) if self.kfs[k].n else None
+                g = self.kfs[k].grid
                 if g is None or (grid is not None and g != grid):
                     mode = L.PIX_KF
                     break
