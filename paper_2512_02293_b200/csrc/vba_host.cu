@@ -127,6 +127,7 @@ struct Ctx {
   void* d_tctasks = nullptr;       // its task DAG (DIAG-fused critical chain)
   int n_tctasks = 0;
   bool use_tc = false;             // VBA_CHOL=tc: tensor-core reduced solve
+  bool use_small = false;          // one-CTA fp64 solve (n <= 232; VBA_CHOL=dag forces the tile DAG)
   bool force_fp64 = false;         // this step: fp64 DAG (tensor-core solve failed its checks)
   bool tc_ran = false;             // the last step's reduced solve ran on the tensor cores
   int tc_gen = 1;
@@ -772,8 +773,11 @@ static int stage_step(Ctx* c, double lam, cudaStream_t st) {
     }
     c->tc_ran = tc_ran;
     if (!tc_ran) {
-      chol_dag_launch(c->d_H, c->npad, c->nt, c->d_rhs, c->d_x, c->d_Ld, c->d_cpart, c->d_cflags, c->d_ctasks,
-                      c->n_ctasks, &c->d_res->status, st, c->d_trace);
+      // small systems: the one-CTA solve (vba_small.cu); else the fp64 tile DAG
+      if (!c->use_small || c->d_trace ||
+          chol_small_solve(c->d_H, c->npad, c->nfree, c->d_rhs, c->d_x, &c->d_res->status, st))
+        chol_dag_launch(c->d_H, c->npad, c->nt, c->d_rhs, c->d_x, c->d_Ld, c->d_cpart, c->d_cflags, c->d_ctasks,
+                        c->n_ctasks, &c->d_res->status, st, c->d_trace);
     }
   }
   mark(c, 4, st);
@@ -857,8 +861,9 @@ static int stage_step_dense(Ctx* c, double lam, cudaStream_t st) {
   HpdOut o{c->d_D, c->dn_npad, c->nfree, c->sdof, c->d_kfcol, c->d_Hdd, c->d_gd, c->d_drhs, lam, c->O.ridge};
   launch_export_hpd(c->P.pixel_mode, c->d_seb, c->d_see, c->d_doff, c->d_roff_real, c->d_npix, c->maxpix, c->d_ej,
                     c->K, s, c->extr, c->pix, c->P.wts, c->d_eoff, c->P.grid_w, c->grid, c->intr, o, st);
-  chol_dag_launch(c->d_D, c->dn_npad, c->dn_nt, c->d_drhs, c->d_dx2, c->d_dLinv, c->d_dpart, c->d_dflags,
-                  c->d_dtasks, c->n_dtasks, &c->d_res->status, st);
+  if (!c->use_small || chol_small_solve(c->d_D, c->dn_npad, c->dn_N, c->d_drhs, c->d_dx2, &c->d_res->status, st))
+    chol_dag_launch(c->d_D, c->dn_npad, c->dn_nt, c->d_drhs, c->d_dx2, c->d_dLinv, c->d_dpart, c->d_dflags,
+                    c->d_dtasks, c->n_dtasks, &c->d_res->status, st);
   mark(c, 4, st);
   launch_scatter_dx(c->d_dx2, c->d_fmap, c->npv, c->d_dx, st);
   if (c->n_disp) {   // padding slots keep their values; real pixels are rewritten below
@@ -1096,6 +1101,7 @@ int vba_create(void** out, const vba_problem* prob, const vba_options* opts, voi
     // the tensor-core solve's triangular sweeps keep one CTA per 128-row tile resident:
     // larger systems (n > 128 * SMs = 18944 on B200) are solved on the fp64 tile DAG
     if (c->nt > sms) c->use_tc = false;
+    c->use_small = !c->use_tc && !(ch && std::strcmp(ch, "dag") == 0);
     const char* it = getenv("VBA_TC_ITERS");
     if (it) c->tc_iters = std::max(1, atoi(it));
   }
@@ -1242,7 +1248,9 @@ int vba_spd_solve(const double* H, int64_t n, const double* b, double* x, int32_
     used_tc = tcrc == 0 && (mode == 2 || (hs[1] == 0 && h2[4] == 1.0)) ? 1 : 0;
   }
   if (!used_tc) {
-    chol_dag_launch(Hp, npad, nt, bp, xp, Ld, part, flags, tasks, ntasks, stat, st);
+    const char* ch = getenv("VBA_CHOL");
+    if ((ch && std::strcmp(ch, "dag") == 0) || chol_small_solve(Hp, npad, (int)n, bp, xp, stat, st))
+      chol_dag_launch(Hp, npad, nt, bp, xp, Ld, part, flags, tasks, ntasks, stat, st);
     cudaMemcpyAsync(hs, stat, sizeof(hs), cudaMemcpyDeviceToHost, st);
   }
   cudaMemcpyAsync(x, xp, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);

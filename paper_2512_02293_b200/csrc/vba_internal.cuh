@@ -335,6 +335,9 @@ void launch_export_sym(const double* H, int64_t ld, int n, double* out, const do
 // (opaque, chol_task_bytes() each) and returns the task count
 int chol_plan_tasks(int nt, void* out, int cap);
 size_t chol_task_bytes();
+// one-CTA fp64 Cholesky solve of the lower triangle of A (column-major, ld) for n <= 232
+// (vba_small.cu); returns non-zero (nothing launched) for larger systems
+int chol_small_solve(const double* A, int64_t ld, int n, const double* rhs, double* x, int* status, cudaStream_t st);
 int chol_dag_launch(double* A, int64_t ld, int nt, double* rhs, double* x, double* Linv, double* part, int* flags,
                     const void* tasks, int ntasks, int* status, cudaStream_t st,
                     unsigned long long* trace = nullptr);

@@ -930,9 +930,13 @@ static int pg_step(PgCtx* c, double lam, cudaStream_t st) {
       c->tc_ran = chol_tc_solve(c->d_H, c->npad, c->nf, c->npad, c->d_rhs, c->d_x, c->d_tcws, c->d_tctasks,
                                 c->n_tctasks, c->tc_iters, &c->d_res->tc_bad, c->tc_gen, st, c->d_res->tc) == 0;
     c->tc_gen += 2 * c->tc_iters;
-    if (!c->tc_ran)
-      chol_dag_launch(c->d_H, c->npad, c->nt, c->d_rhs, c->d_x, c->d_Ld, c->d_cpart, c->d_cflags, c->d_ctasks,
-                      c->n_ctasks, &c->d_res->status, st, nullptr);
+    if (!c->tc_ran) {
+      const char* ch = getenv("VBA_CHOL");
+      if ((ch && std::strcmp(ch, "dag") == 0) ||
+          chol_small_solve(c->d_H, c->npad, c->nf, c->d_rhs, c->d_x, &c->d_res->status, st))
+        chol_dag_launch(c->d_H, c->npad, c->nt, c->d_rhs, c->d_x, c->d_Ld, c->d_cpart, c->d_cflags, c->d_ctasks,
+                        c->n_ctasks, &c->d_res->status, st, nullptr);
+    }
   }
   const int npv = 7 * c->K;
   k_pg_scatter<<<(npv + 127) / 128, 128, 0, st>>>(c->d_x, npv, c->d_dx);

@@ -5,7 +5,7 @@ set -e
 name=$1; defs=$2
 cd "$(dirname "$0")/../paper_2512_02293_b200/csrc"
 mkdir -p build/var_$name
-for f in vba_vision.cu vba_imu.cu vba_dense.cu vba_chol.cu vba_preint.cu vba_host.cu vba_pgba.cu vba_init.cu; do
+for f in vba_vision.cu vba_imu.cu vba_dense.cu vba_chol.cu vba_small.cu vba_preint.cu vba_host.cu vba_pgba.cu vba_init.cu; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
     --expt-relaxed-constexpr $defs -c $f -o build/var_$name/${f%.cu}.o &
 done
