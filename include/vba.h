@@ -216,8 +216,8 @@ VBA_API int vba_gram_kind(void* ctx);
 /* Standalone SPD solve H x = b of a dense fp64 n x n system (column-major,
  * lower triangle read; device pointers), replacing np.linalg.solve(Hred, -gred)
  * of solver.py:287.  mode 0: tcgen05 split-fp16 (3-product) Cholesky + fp64 iterative
- * refinement (falls back to mode 1 when its checks fail), mode 1: fp64 DMMA
- * tile-DAG Cholesky, mode 2: tensor-core result unconditionally (diagnostics;
+ * refinement (falls back to mode 1 when its checks fail), mode 1: fp64 Cholesky (one-CTA
+ * shared-memory solve up to n = 232, else the DMMA tile DAG; VBA_CHOL=dag forces the DAG), mode 2: tensor-core result unconditionally (diagnostics;
  * info[0] on entry = refinement passes, 0 -> 4).  On return info[0] = 1 if the
  * tensor-core result was used, info[1] = tensor-core pivot failure.  Returns VBA_E_NOT_SPD on a
  * non-positive fp64 pivot.  Synchronises `stream`. */

@@ -205,7 +205,8 @@ def spd_solve(H, b, mode: int = 0, iters: int = 0):
     """Solve H x = b for a dense SPD fp64 torch CUDA matrix (lower triangle used).
 
     mode 0: tcgen05 split-fp16 (3-product) Cholesky + fp64 iterative refinement (fp64 fallback
-    on failed checks); mode 1: fp64 DMMA Cholesky.  Returns (x, used_tensor_cores).
+    on failed checks); mode 1: fp64 Cholesky (one CTA up to n = 232, else the DMMA tile DAG;
+    VBA_CHOL=dag forces the DAG).  Returns (x, used_tensor_cores).
     Replaces np.linalg.solve(Hred, -gred) of solver.py:287.
     """
     import torch

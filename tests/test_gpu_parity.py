@@ -162,6 +162,38 @@ def test_spd_solve_tensor_core_matches_fp64(cuda_ok, n, cond):
     assert e0 < 1e-8 * max(1.0, cond / 1e5), e0
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [1, 8, 105, 165, 225, 232, 233])
+def test_spd_solve_small_and_dag_fp64(cuda_ok, n, monkeypatch):
+    """The one-CTA fp64 solve (n <= 232, vba_small.cu) and the fp64 tile DAG (VBA_CHOL=dag;
+    n = 233 goes to the DAG either way) both reproduce np.linalg.solve (solver.py:287) on an
+    ill-conditioned, badly scaled SPD system like H_red, including sizes that are not a
+    multiple of the 8-column panel (identity padding)."""
+    import torch
+    from paper_2512_02293_b200 import _lib
+    g = torch.Generator().manual_seed(1000 + n)
+    Q, _ = torch.linalg.qr(torch.randn(n, n, generator=g, dtype=torch.float64))
+    ev = torch.logspace(0, 6, n, dtype=torch.float64)
+    d = torch.exp(torch.randn(n, generator=g, dtype=torch.float64) * 3.0)
+    H = (d[:, None] * (Q * ev) @ Q.T * d[None, :])
+    H = 0.5 * (H + H.T)
+    b = torch.randn(n, generator=g, dtype=torch.float64)
+    ref = torch.linalg.solve(H, b)
+    x_small, _ = _lib.spd_solve(H.cuda(), b.cuda(), mode=1)
+    monkeypatch.setenv("VBA_CHOL", "dag")
+    x_dag, _ = _lib.spd_solve(H.cuda(), b.cuda(), mode=1)
+    for x in (x_small, x_dag):
+        err = ((x.cpu() - ref).abs().max() / ref.abs().max()).item()
+        assert err < 1e-9, (n, err)
+    # not positive definite: both report it (the reference's singular-system retry path)
+    Hn = H.clone()
+    Hn[n // 2, n // 2] = -abs(Hn[n // 2, n // 2])
+    for mode_env in ("", "dag"):
+        monkeypatch.setenv("VBA_CHOL", mode_env)
+        with pytest.raises(Exception):
+            _lib.spd_solve(Hn.cuda(), b.cuda(), mode=1)
+
+
 @pytest.fixture
 def force_tc(monkeypatch):
     """Force the tensor-core reduced solve (3xTF32 factor + fp64 refinement) on the
