@@ -641,8 +641,9 @@ class DeviceProblem:
         which on the legacy default stream serialises the copy stream's uploads with the solve
         (measured: 23.2 vs 14.8 ms per config-4 window).  Window s+1's flow targets and weights
         (the bulk of the bytes) are uploaded on ``copy_stream`` into a second device set
-        while window s is solved (``vba_bind_inputs`` swaps the sets); the small arrays are
-        uploaded on the solve stream.  Each window's solved state and disparities are read
+        while window s is solved (``vba_bind_inputs`` swaps the sets); the small arrays ride
+        the same copy stream into staging buffers and are moved into place by device copies
+        on the solve stream.  Each window's solved state and disparities are read
         back into ``outputs[s] = (state, disp)`` (pinned host tensors, allocated when not
         given) before the next window starts.  Returns the per-window reports."""
         if not windows:
@@ -652,6 +653,15 @@ class DeviceProblem:
         if getattr(self, "_stage", None) is None:
             self._stage = (torch.empty_like(self.d_tgt), torch.empty_like(self.d_w))
         sets = ((self.d_tgt, self.d_w), self._stage)
+        # the small per-window arrays travel on the copy stream too, into a device staging set
+        # per buffer, and are moved into place by device copies on the solve stream: copies
+        # from two streams share the host->device engine in no fixed order, so a small copy on
+        # the solve stream could wait behind a whole 600 MB bulk upload of the next window
+        small = ("state", "disp64", "imu", "grav")
+        dst = {"state": self.d_state, "disp64": self.d_disp64, "imu": self.d_imu, "grav": self.d_grav}
+        if getattr(self, "_stage_small", None) is None:
+            self._stage_small = [{k: torch.empty(dst[k].numel(), dtype=dst[k].dtype, device=dev) for k in small}
+                                 for _ in range(2)]
         up = [torch.cuda.Event(), torch.cuda.Event()]
         free = [torch.cuda.Event(), torch.cuda.Event()]
         used = [False, False]
@@ -660,8 +670,13 @@ class DeviceProblem:
             with torch.cuda.stream(cs):
                 if used[b]:
                     cs.wait_event(free[b])
-                sets[b][0].copy_(windows[s]["tgt"].reshape(-1), non_blocking=True)
-                sets[b][1].copy_(windows[s]["w"].reshape(-1), non_blocking=True)
+                win = windows[s]
+                for k in small:
+                    if k == "disp64" and k not in win:
+                        continue
+                    self._stage_small[b][k].copy_(win[k].reshape(-1), non_blocking=True)
+                sets[b][0].copy_(win["tgt"].reshape(-1), non_blocking=True)
+                sets[b][1].copy_(win["w"].reshape(-1), non_blocking=True)
                 up[b].record(cs)
 
         if outputs is None:
@@ -675,15 +690,14 @@ class DeviceProblem:
             if s + 1 < len(windows):
                 upload(s + 1, b ^ 1)
             st.wait_event(up[b])
-            with torch.cuda.stream(st):
-                self.d_state.copy_(win["state"].reshape(self.d_state.shape), non_blocking=True)
-                if "disp64" in win:   # fp64 master disparities: one DMA (load_state derives the fp32 copy)
-                    self.d_disp64.copy_(win["disp64"].reshape(self.d_disp64.shape), non_blocking=True)
-                else:                 # fp32 window disparities seed the fp64 master
+            with torch.cuda.stream(st):   # device-to-device (kernels: no copy engine involved)
+                for k in small:
+                    if k == "disp64" and k not in win:
+                        continue
+                    dst[k].view(-1).copy_(self._stage_small[b][k])
+                if "disp64" not in win:   # fp32 window disparities seed the fp64 master
                     self.d_disp.copy_(win["disp"].reshape(self.d_disp.shape), non_blocking=True)
                     self.d_disp64.copy_(self.d_disp)
-                self.d_imu.copy_(win["imu"].reshape(-1), non_blocking=True)
-                self.d_grav.copy_(win["grav"].reshape(-1), non_blocking=True)
             rc = self.lib.vba_bind_inputs(self.ctx, self._sptr(), sets[b][0].data_ptr(), sets[b][1].data_ptr(), 1)
             if rc == L.VBA_E_COV:
                 raise ValueError("non-PSD preintegration covariance")
