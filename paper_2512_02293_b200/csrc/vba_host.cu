@@ -47,7 +47,7 @@ static void set_err(const char* fmt, ...) {
 
 constexpr int kTileRt = kTilePx;   // pixels per per-pixel work tile (vba_internal.cuh)
 constexpr int kGramBlock = 512;
-constexpr int kMaxOutDegree = 31;
+constexpr int kMaxOutDegree = 63;   // Gram: 31 in one CTA, up to 63 in unit slices (k_gram<.., 63>)
 constexpr int NBc = 128;         // Cholesky tile (vba_chol.cu)
 constexpr int kTcMinTiles = 4;   // tensor-core reduced solve from this many 128-tiles up (n >= 385; config 3: 8.2 -> 4.5 ms)
 
@@ -314,7 +314,8 @@ static int build_plans(Ctx* c, cudaStream_t st) {
     if (npad % 4 != 0) { set_err("keyframe disparity segments must be padded to 4"); return VBA_E_INVALID; }
     const int k = c->see[n] - c->seb[n];
     if (k > kMaxOutDegree) {
-      set_err("keyframe %d has out-degree %d > %d (unsupported by the Gram kernel)", n, k, kMaxOutDegree);
+      set_err("keyframe %d has out-degree %d > %d (the Schur Gram stages at most 6*%d+1 coupling columns)", n, k,
+              kMaxOutDegree, kMaxOutDegree);
       return VBA_E_UNSUPPORTED;
     }
     c->kmax = std::max(c->kmax, k);
@@ -460,18 +461,27 @@ static int build_plans(Ctx* c, cudaStream_t st) {
     c->gram_smem = std::max(c->gram_smem, gram_smem_bytes(c->kmax, nsplit, np, k));
     int R = std::max(1, (int)((target + nsrc - 1) / nsrc));
     R = std::min(R, std::max(1, npix / 256));
+    // more than 31 out-edges: one pixel range (k_fill_transform reads its record in place),
+    // its 2x2 tile units in slices of gram_slice_units() per CTA (the DMMA Gram)
+    const bool big = k > 31;
+    if (big) R = 1;
+    const int U = big ? gram_units(k) : 0, su = gram_slice_units();
     const int chunk = ((npix + R - 1) / R + 31) / 32 * 32;   // whole k_gram staging chunks (kGramPC)
     for (int a = 0; a < npix; a += chunk) {
-      GramTile g{};
-      g.src = n;
-      g.n0 = a;
-      g.n1 = std::min(npix, a + chunk);
-      g.eb = c->seb[n];
-      g.ee = c->see[n];
-      g.nsplit = nsplit;
-      g.out = gpo;
+      for (int u0 = 0; u0 < (big ? U : 1); u0 += su) {
+        GramTile g{};
+        g.src = n;
+        g.n0 = a;
+        g.n1 = std::min(npix, a + chunk);
+        g.eb = c->seb[n];
+        g.ee = c->see[n];
+        g.nsplit = nsplit;
+        g.u0 = big ? u0 : 0;
+        g.u1 = big ? std::min(U, u0 + su) : 0;
+        g.out = gpo;
+        c->gtiles.push_back(g);
+      }
       gpo += (int64_t)np * 36 + 6 * k;
-      c->gtiles.push_back(g);
     }
     c->g1[n] = (int)c->gtiles.size();
     c->goff[n] = go;
@@ -485,6 +495,7 @@ static int build_plans(Ctx* c, cudaStream_t st) {
   {
     const char* gm = getenv("VBA_GRAM");
     c->gram_tc = gm ? (strcmp(gm, "tc") == 0) : (nsrc > 0 && work_px >= 256 * (int64_t)nsrc);
+    if (c->kmax > 31) c->gram_tc = false;   // the tensor-core Gram holds 31 out-edges per CTA
     if (c->gram_tc) c->gram_smem = gram_tc_smem_bytes(c->kmax);
   }
   if (c->gram_smem > 227 * 1024) { set_err("Gram kernel shared memory too large"); return VBA_E_UNSUPPORTED; }

@@ -61,7 +61,8 @@ struct StreamItem {
 // Work tile of the Schur Gram kernel (one source keyframe, a pixel range).
 struct GramTile {
   int32_t src, n0, n1, eb, ee, nsplit;
-  int64_t out;    // offset (doubles) of this tile's partial Gram output
+  int32_t u0, u1;   // unit slice of the DMMA Gram (u1 > u0: sources with more than 31 out-edges)
+  int64_t out;      // offset (doubles) of this tile's partial Gram output (shared by a range's slices)
 };
 
 // Assembly contribution: value(r,c) = sign * buf[off + (trans ? c*ld + r : r*ld + c)]
@@ -295,6 +296,8 @@ void launch_step_edges(const int32_t* ei, const int32_t* ej, int E, const DevSta
                        const double* dx_full, int sdof, float* ustep, cudaStream_t st);
 size_t gram_smem_bytes(int kmax, int nsplit, int npairs, int k);
 size_t gram_tc_smem_bytes(int kmax);
+int gram_units(int k);
+int gram_slice_units();
 void launch_copy_segments(const vba_copy_seg* segs, int n, cudaStream_t st);
 void launch_gram_tc(int pixel_mode, const GramTile* gt, int ngt, size_t smem, int kmax, const DevState& s,
                     const float* pix, const float* wts, const int64_t* eoff, const int64_t* doff, int grid_w,

@@ -726,8 +726,17 @@ void launch_edge_finalize(const int32_t* t0s, const int32_t* t1s, const PixTile*
 // ---------------------------------------------------------------------------
 constexpr int GPX = kGramPC + 4;   // pixel stride of the U / V columns (doubles)
 constexpr int GWARPS = 16;
-// 8x8 output tiles per warp: 2x2 units, 5 per warp up to 30 out-edges, 6 at 31
+// 8x8 output tiles per warp: 2x2 units, 5 per warp up to 30 out-edges, 6 at 31 (and in slices)
 __host__ __device__ constexpr int gram_tiles_per_warp(int kmax) { return kmax <= 30 ? 20 : 24; }
+// 2x2 tile units of a source with k out-edges, and the units one CTA takes in a slice
+int gram_units(int k) {
+  const int nc = 6 * k, NRt = (nc + 1 + 7) / 8, NCt = (nc + 7) / 8;
+  int U = 0;
+  for (int tj = 0; tj < NCt; tj += 2)
+    for (int ti = tj > 0 ? tj - 1 : 0; ti < NRt; ti += 2) ++U;
+  return U;
+}
+int gram_slice_units() { return GWARPS * 24 / 4; }
 
 __device__ __forceinline__ void gdmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -736,7 +745,7 @@ __device__ __forceinline__ void gdmma(double& c0, double& c1, double a, double b
 }
 
 #define GPROF(i, v)
-template <int MODE, int GT>
+template <int MODE, int GT, int KE>
 __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
     const GramTile* __restrict__ gts, const float* __restrict__ disp, const EdgeGeo32* __restrict__ geo,
     const float* __restrict__ pix, const float* __restrict__ wts, const int64_t* __restrict__ eoff,
@@ -770,10 +779,29 @@ __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
   __shared__ short tile_i[GWARPS * GT], tile_j[GWARPS * GT];
   __shared__ int nu_s, npw_s[GWARPS];
   __shared__ double invs[2][kGramPC];   // 1 / (Hdd (1 + lam) + ridge) per pixel, double-buffered by chunk
-  __shared__ float4 geos[32 * 4];       // the source's out-edge geometry (k <= 31), EdgeGeo32 records
+  __shared__ float4 geos[(KE + 1) * 4];   // the source's out-edge geometry (k <= KE), EdgeGeo32 records
   // C = sum_n u_n u_n^T / h_n is formed as W^T W with W = u / sqrt(h_n) (one staged matrix)
   auto pixel_inv = [&](int n) { return n < T.n1 ? 1.0 / sqrt((double)Hdd[kbase + n] * damp + ridge) : 0.0; };
-  if (tid == 0) {
+  if (tid == 0 && T.u1 > T.u0) {
+    // slice [u0, u1) of the unit list (sources with more out-edges than one CTA's registers
+    // hold: several CTAs share the pixel range, each its own units, disjoint outputs of one
+    // partial record): whole units round-robin over the warps, missing slots -1
+    const int cnt = T.u1 - T.u0, nu = (cnt + GWARPS - 1) / GWARPS;
+    for (int i = 0; i < GWARPS * GT; ++i) tile_i[i] = tile_j[i] = -1;
+    for (int w = 0; w < GWARPS; ++w) npw_s[w] = 0;
+    int u = 0;
+    for (int tj = 0; tj < NCt; tj += 2)
+      for (int ti = tj > 0 ? tj - 1 : 0; ti < NRt; ti += 2, ++u) {
+        if (u < T.u0 || u >= T.u1) continue;
+        const int r1 = ti + 1 < NRt ? ti + 1 : -1, c1 = tj + 1 < NCt ? tj + 1 : -1;
+        const int w = (u - T.u0) % GWARPS, sl = 4 * ((u - T.u0) / GWARPS);
+        tile_i[w + GWARPS * sl] = (short)ti; tile_j[w + GWARPS * sl] = (short)tj;
+        tile_i[w + GWARPS * (sl + 1)] = (short)r1; tile_j[w + GWARPS * (sl + 1)] = (short)tj;
+        tile_i[w + GWARPS * (sl + 2)] = (short)ti; tile_j[w + GWARPS * (sl + 2)] = (short)c1;
+        tile_i[w + GWARPS * (sl + 3)] = (short)r1; tile_j[w + GWARPS * (sl + 3)] = (short)c1;
+      }
+    nu_s = nu;
+  } else if (tid == 0) {
     int U = 0;
     for (int tj = 0; tj < NCt; tj += 2)
       for (int ti = tj > 0 ? tj - 1 : 0; ti < NRt; ti += 2) ++U;
@@ -816,7 +844,7 @@ __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
   // per thread), widened to fp64 into buffer b.  Loads of all items first (gload),
   // arithmetic + stores per item (gitem), so the arithmetic can be interleaved with
   // the DMMAs of the previous chunk.
-  constexpr int kGramItems = (kGramPC * 31 + GWARPS * 32 - 1) / (GWARPS * 32);
+  constexpr int kGramItems = (kGramPC * KE + GWARPS * 32 - 1) / (GWARPS * 32);
   float d_[kGramItems], rx_[kGramItems], ry_[kGramItems], gd_[kGramItems];
   float2 w_[kGramItems];
   auto gload = [&](int c0) {
@@ -892,9 +920,10 @@ __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
         for (int h = 0; h < 4; h += 2) {
           if (q + h >= nmine) break;
           const int r1 = tile_i[warp + GWARPS * (q + h + 1)];
-          const double* pa0 = Ub + (size_t)(tile_i[warp + GWARPS * (q + h)] * 8 + am) * GPX + ak;
+          const int i0 = tile_i[warp + GWARPS * (q + h)], j0 = tile_j[warp + GWARPS * (q + h)];
+          const double* pa0 = Ub + (size_t)((i0 >= 0 ? i0 : 0) * 8 + am) * GPX + ak;
           const double* pa1 = Ub + (size_t)((r1 >= 0 ? r1 : 0) * 8 + am) * GPX + ak;
-          const double* pb = Vb + (size_t)(tile_j[warp + GWARPS * (q + h)] * 8 + am) * GPX + ak;
+          const double* pb = Vb + (size_t)((j0 >= 0 ? j0 : 0) * 8 + am) * GPX + ak;
 #pragma unroll
           for (int ks = 0; ks < kGramPC / 4; ++ks) {
             const double b = pb[4 * ks];
@@ -904,9 +933,10 @@ __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
         }
       } else if (q < n4) {
         const int r1 = tile_i[warp + GWARPS * (q + 1)], c1 = tile_j[warp + GWARPS * (q + 2)];
-        const double* pa0 = Ub + (size_t)(tile_i[warp + GWARPS * q] * 8 + am) * GPX + ak;
+        const int i0 = tile_i[warp + GWARPS * q], j0 = tile_j[warp + GWARPS * q];
+        const double* pa0 = Ub + (size_t)((i0 >= 0 ? i0 : 0) * 8 + am) * GPX + ak;
         const double* pa1 = Ub + (size_t)((r1 >= 0 ? r1 : 0) * 8 + am) * GPX + ak;
-        const double* pb0 = Vb + (size_t)(tile_j[warp + GWARPS * q] * 8 + am) * GPX + ak;
+        const double* pb0 = Vb + (size_t)((j0 >= 0 ? j0 : 0) * 8 + am) * GPX + ak;
         const double* pb1 = Vb + (size_t)((c1 >= 0 ? c1 : 0) * 8 + am) * GPX + ak;
 #pragma unroll
         for (int ks = 0; ks < kGramPC / 4; ++ks) {
@@ -945,14 +975,14 @@ __global__ void __launch_bounds__(GWARPS * 32, 1) k_gram(
   }
 }
 
-template <int MODE, int GT>
+template <int MODE, int GT, int KE>
 static void launch_gram_t(const GramTile* gt, int ngt, int block, size_t smem, int kmax, const DevState& s,
                           const float* pix, const float* wts, const int64_t* eoff, const int64_t* doff, int grid_w,
                           GridP gp, IntrP in, const float* Hdd, const float* gd, double lam, double ridge,
                           double* gram_part, const int32_t* order, cudaStream_t st) {
-  cudaFuncSetAttribute(k_gram<MODE, GT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_gram<MODE, GT><<<ngt, block, smem, st>>>(gt, s.disp, s.geo32, pix, wts, eoff, doff, grid_w, gp, in, Hdd, gd,
-                                             lam, ridge, kmax, gram_part, order);
+  cudaFuncSetAttribute(k_gram<MODE, GT, KE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_gram<MODE, GT, KE><<<ngt, block, smem, st>>>(gt, s.disp, s.geo32, pix, wts, eoff, doff, grid_w, gp, in, Hdd, gd,
+                                                 lam, ridge, kmax, gram_part, order);
 }
 
 template <int MODE>
@@ -960,12 +990,15 @@ static void launch_gram_m(const GramTile* gt, int ngt, int block, size_t smem, i
                           const float* pix, const float* wts, const int64_t* eoff, const int64_t* doff, int grid_w,
                           GridP gp, IntrP in, const float* Hdd, const float* gd, double lam, double ridge,
                           double* gram_part, const int32_t* order, cudaStream_t st) {
-  if (gram_tiles_per_warp(kmax) == 20)
-    launch_gram_t<MODE, 20>(gt, ngt, block, smem, kmax, s, pix, wts, eoff, doff, grid_w, gp, in, Hdd, gd, lam, ridge,
-                            gram_part, order, st);
+  if (kmax > 31)   // sliced units (gram_unit_slice), up to 63 out-edges
+    launch_gram_t<MODE, 24, 63>(gt, ngt, block, smem, kmax, s, pix, wts, eoff, doff, grid_w, gp, in, Hdd, gd, lam,
+                                ridge, gram_part, order, st);
+  else if (gram_tiles_per_warp(kmax) == 20)
+    launch_gram_t<MODE, 20, 31>(gt, ngt, block, smem, kmax, s, pix, wts, eoff, doff, grid_w, gp, in, Hdd, gd, lam,
+                                ridge, gram_part, order, st);
   else
-    launch_gram_t<MODE, 24>(gt, ngt, block, smem, kmax, s, pix, wts, eoff, doff, grid_w, gp, in, Hdd, gd, lam, ridge,
-                            gram_part, order, st);
+    launch_gram_t<MODE, 24, 31>(gt, ngt, block, smem, kmax, s, pix, wts, eoff, doff, grid_w, gp, in, Hdd, gd, lam,
+                                ridge, gram_part, order, st);
 }
 
 void launch_gram(int mode, const GramTile* gt, int ngt, int block, size_t smem, int kmax, const DevState& s,
@@ -1307,7 +1340,10 @@ __global__ void k_fill_transform(const int32_t* __restrict__ srcs, const int32_t
   double* Gj = Gi + kmax * 36;
   double* D = Gj + kmax * 36;
   double* Cs = D + kmax * 36;
-  {
+  const double* C = Cs;
+  if (k > 31) {   // one pixel range (its unit slices share the record): read it in place
+    C = part + gt[g0[s]].out;
+  } else {
     const int len = npairs * 36 + 6 * k, t0 = g0[s], t1 = g1[s];
     const double* p0 = part + gt[t0].out;
     for (int i = threadIdx.x; i < len; i += blockDim.x) {
@@ -1316,7 +1352,6 @@ __global__ void k_fill_transform(const int32_t* __restrict__ srcs, const int32_t
       Cs[i] = acc;
     }
   }
-  const double* C = Cs;
   const double* b = C + npairs * 36;
   double* o = fill + foff[s];
   const int tid = threadIdx.x, nth = blockDim.x;
@@ -1405,7 +1440,8 @@ void launch_fill_transform(const int32_t* srcs, int nsrc, const int32_t* seb, co
                            const double* part, const DevState& s, const Extr& x, double* fill, int kmax,
                            cudaStream_t st) {
   if (nsrc <= 0) return;
-  const size_t smem = ((size_t)3 * kmax * 36 + (size_t)kmax * (kmax + 1) / 2 * 36 + 6 * kmax) * sizeof(double);
+  const int ks = kmax < 31 ? kmax : 31;   // sources with more out-edges read their Gram in place
+  const size_t smem = ((size_t)3 * kmax * 36 + (size_t)ks * (ks + 1) / 2 * 36 + 6 * ks) * sizeof(double);
   cudaFuncSetAttribute(k_fill_transform, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_fill_transform<<<nsrc, 512, smem, st>>>(srcs, seb, see, g0, g1, gt, foff, part, kmax, s.geo64, x, fill);
   launch_count();

@@ -366,3 +366,64 @@ def test_spd_solve_beyond_tensor_core_residency(cuda_ok):
     err = ((x - ref).abs().max() / ref.abs().max()).item()
     print(f"n={n}: fp64 DAG solve rel err {err:.2e}")
     assert err < 1e-9
+
+
+def _high_degree_graph(degrees, seed=7):
+    """Config 1 on a 24x32 grid with the out-edges of some sources duplicated (re-weighted) up
+    to the requested out-degrees: the reference accepts repeated keyframe pairs
+    (solver.py:62-73), and global graphs reach such degrees."""
+    from paper_2512_02293_b200 import types as T
+    from paper_2512_02293_b200.workloads import make_workload
+    g = make_workload(1, grid=(24, 32))
+    rng = np.random.default_rng(seed)
+    edges = list(g.vision_edges)
+    for src, deg in degrees.items():
+        own = [e for e in edges if e.i == src]
+        for t in range(deg - len(own)):
+            e = own[t % len(own)]
+            w = (e.weights * rng.uniform(0.5, 1.5, e.weights.shape)).astype(np.float32).astype(float)
+            edges.append(T.VisionEdge(e.i, e.j, e.pixels, e.targets, w))
+    edges.sort(key=lambda e: e.i)
+    g.vision_edges = edges
+    return g
+
+
+@pytest.mark.gpu
+def test_high_out_degree_sources(cuda_ok):
+    """Sources with 40 and 63 out-edges (beyond one Gram CTA's 31: the DMMA Gram in unit slices,
+    the fill-in transform reading its record in place) against the fp64 oracle: reduced system,
+    step and a full solve; 64 out-edges are refused with VBA_E_UNSUPPORTED."""
+    from paper_2512_02293_b200.device import DeviceProblem
+    from paper_2512_02293_b200.problem import pack_graph
+    from oracle import vi_ba as O
+    g = _high_degree_graph({5: 40, 9: 63})
+    P = pack_graph(g)
+    opts = {"max_iterations": 3, "frozen_keyframes": (0,)}
+    o = dict(O.DEFAULT_OPTS)
+    o.update(opts)
+    L = O.Layout(P, o)
+    lin = O.linearize_sparse(P, L)
+    Hr_ref, gr_ref, _ = O.reduced_system_sparse(L, o, *lin, o["damping"])
+    free = L.free_mask()
+    dx_ref, dxd_ref = O.solve_step_sparse(L, o, *lin, o["damping"])
+    dp = DeviceProblem(P, opts)
+    assert dp.stats()["gram_tc"] == 0
+    dp.linearize()
+    Hr, gr = dp.export_reduced(o["damping"])
+    dx, dxd = dp.solve_step(o["damping"])
+    eh = np.abs(Hr - Hr_ref[np.ix_(free, free)]).max() / np.abs(Hr_ref).max()
+    eg = np.abs(gr - gr_ref[free]).max() / np.abs(gr_ref).max()
+    ex = np.abs(dx - dx_ref).max() / np.abs(dx_ref).max()
+    ed = np.abs(dxd - dxd_ref).max() / np.abs(dxd_ref).max()
+    print(f"out-degree 40/63: H_red {eh:.1e} g_red {eg:.1e} dx {ex:.1e} dx_d {ed:.1e}")
+    assert eh < 1e-4 and eg < 1e-4 and ex < 1e-5 and ed < 1e-5
+    rep = dp.solve()
+    ref = O.solve_vi_ba(copy.deepcopy(P), opts, sparse=True)
+    print("costs", rep["cost_trajectory"], ref["cost_trajectory"])
+    assert rep["iterations"] == ref["iterations"] and rep["termination"] == ref["termination"]
+    assert np.allclose(rep["cost_trajectory"], ref["cost_trajectory"], rtol=1e-6)
+    dp.close()
+    from paper_2512_02293_b200 import _lib
+    with pytest.raises(_lib.VbaError) as ei:
+        DeviceProblem(pack_graph(_high_degree_graph({9: 64})), opts)
+    assert ei.value.code == _lib.VBA_E_UNSUPPORTED
