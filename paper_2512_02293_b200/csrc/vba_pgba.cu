@@ -466,19 +466,67 @@ __global__ void k_pg_rel(const double* __restrict__ relrec, const int32_t* __res
   }
 }
 
-// information -> whitening W = L^T (residuals.py:370-377: scipy cholesky lower); status on failure
+// information -> whitening W = L^T (residuals.py:370-377): L = cholesky(information, lower)
+// (scipy), or -- PSD but rank-deficient information, where the Cholesky meets a non-positive
+// pivot -- the symmetric square root's factor L = V diag(sqrt(max(lambda, 0))) of the
+// eigen-decomposition (np.linalg.eigh), computed here by cyclic Jacobi rotations.  Only
+// W^T W = information (clamped) enters the energy and the normal equations, so the
+// eigenvector basis (order, signs) does not matter.
+__device__ void pg_eig_sqrt(const double* I, double* W) {
+  double A[49], V[49];
+  for (int k = 0; k < 49; ++k) { A[k] = 0.5 * (I[k] + I[(k % 7) * 7 + k / 7]); V[k] = (k % 8 == 0) ? 1.0 : 0.0; }
+  for (int sweep = 0; sweep < 50; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int p = 0; p < 7; ++p)
+      for (int q = 0; q < 7; ++q) {
+        tot += A[p * 7 + q] * A[p * 7 + q];
+        if (p != q) off += A[p * 7 + q] * A[p * 7 + q];
+      }
+    if (off <= 1e-30 * tot) break;
+    for (int p = 0; p < 6; ++p)
+      for (int q = p + 1; q < 7; ++q) {
+        const double apq = A[p * 7 + q];
+        if (apq == 0.0) continue;
+        const double theta = (A[q * 7 + q] - A[p * 7 + p]) / (2.0 * apq);
+        const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < 7; ++k) {   // A <- A J (columns p, q)
+          const double akp = A[k * 7 + p], akq = A[k * 7 + q];
+          A[k * 7 + p] = c * akp - s * akq;
+          A[k * 7 + q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < 7; ++k) {   // A <- J^T A (rows p, q)
+          const double apk = A[p * 7 + k], aqk = A[q * 7 + k];
+          A[p * 7 + k] = c * apk - s * aqk;
+          A[q * 7 + k] = s * apk + c * aqk;
+        }
+        for (int k = 0; k < 7; ++k) {   // V <- V J
+          const double vkp = V[k * 7 + p], vkq = V[k * 7 + q];
+          V[k * 7 + p] = c * vkp - s * vkq;
+          V[k * 7 + q] = s * vkp + c * vkq;
+        }
+      }
+  }
+  // L = V diag(sqrt(max(lambda, 0))),  W = L^T: W[r][c] = sqrt(lambda_r) V[c][r]
+  for (int r = 0; r < 7; ++r) {
+    const double sl = sqrt(fmax(A[r * 7 + r], 0.0));
+    for (int c = 0; c < 7; ++c) W[r * 7 + c] = sl * V[c * 7 + r];
+  }
+}
+
 __global__ void k_pg_whiten(const double* __restrict__ relrec, int R, double* __restrict__ Wt,
                             int* __restrict__ status) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= R) return;
   const double* I = relrec + (int64_t)VBA_PG_REL_REC * e + 8;
+  double* W = Wt + 49 * (int64_t)e;
   double L[49];
   for (int k = 0; k < 49; ++k) L[k] = 0.0;
   for (int c = 0; c < 7; ++c) {
     double d = I[c * 7 + c];
     for (int k = 0; k < c; ++k) d -= L[c * 7 + k] * L[c * 7 + k];
     if (!(d > 0.0)) {
-      atomicExch(status, 1);
+      pg_eig_sqrt(I, W);
       return;
     }
     const double lc = sqrt(d);
@@ -489,9 +537,9 @@ __global__ void k_pg_whiten(const double* __restrict__ relrec, int R, double* __
       L[r * 7 + c] = v / lc;
     }
   }
-  double* W = Wt + 49 * (int64_t)e;
   for (int r = 0; r < 7; ++r)
     for (int c = 0; c < 7; ++c) W[r * 7 + c] = L[c * 7 + r];
+  (void)status;
 }
 
 // total energy: vision records then relative records (loopclosure.py:378-390), fixed order
@@ -1099,7 +1147,7 @@ int vba_pg_create(void** out, const vba_pg_problem* prob, const vba_options* opt
     return fail(VBA_E_CUDA);
   }
   if (hs) {
-    pg_set_err("relative-pose information is not positive definite (rank-deficient information is not supported)");
+    pg_set_err("relative-pose whitening failed");
     return fail(VBA_E_UNSUPPORTED);
   }
   *out = c;

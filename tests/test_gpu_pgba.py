@@ -120,3 +120,29 @@ def test_dropin_errors(cuda_ok):
     g2 = PoseGraph(g.nodes, g.chain, [LoopEdge(0, 60, RelativePoseEdge(0, 60, bad, np.eye(7)))])
     with pytest.raises(RuntimeError, match="finite"):
         solve_pgba(g2)
+
+
+@pytest.mark.gpu
+def test_rank_deficient_information(cuda_ok):
+    """A relative edge with PSD but rank-deficient information (no scale information): the
+    reference's Cholesky fails and it whitens with the eigen square root
+    (residuals.py:370-377); the device does the same (Jacobi eigen-decomposition) and the solve
+    matches the oracle restatement (oracle/pgba.py, which follows the reference's fallback)."""
+    import oracle.pgba as O
+    name = NAMES[0]
+    P, out, meta = load_pgba_golden(name)
+    P = copy.deepcopy(P)
+    info = np.array(P["rinfo"][0], float)
+    info[6, :] = 0.0
+    info[:, 6] = 0.0                      # log-scale unobserved by this edge
+    P["rinfo"][0] = info
+    P["rinfo"][1] = np.zeros((7, 7))      # and one edge that constrains nothing
+    dp = _dp(copy.deepcopy(P), meta)
+    e0 = dp.energy()
+    rep = dp.solve()
+    ref = O.solve_pgba(copy.deepcopy(P), meta["opts"])
+    c, cr = np.array(rep["cost_trajectory"]), np.array(ref["cost_trajectory"])
+    print(f"rank-deficient: energy {e0} / {cr[0]}; {rep['iterations']} it / {ref['iterations']}; {c} / {cr}")
+    assert abs(e0 - cr[0]) <= 1e-10 * cr[0]
+    assert rep["iterations"] == ref["iterations"] and rep["termination"] == ref["termination"]
+    assert np.all(np.abs(c - cr) <= 1e-8 * cr + 1e-12 * cr[0])
