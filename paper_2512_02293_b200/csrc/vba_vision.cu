@@ -1484,7 +1484,10 @@ void launch_step_edges(const int32_t* ei, const int32_t* ej, int E, const DevSta
 //   dx_d = (-g_d - sum_e k_{n,e} . u_e) / Hdd_d,   d' = max(d + dx_d, 1e-4)
 // ---------------------------------------------------------------------------
 template <int MODE>
-__global__ void __launch_bounds__(kPixBlock) k_backsub(
+#ifndef VBA_BS_MINB
+#define VBA_BS_MINB 4
+#endif
+__global__ void __launch_bounds__(kPixBlock, VBA_BS_MINB) k_backsub(
     const PixTile* __restrict__ tiles, const float* __restrict__ disp, const EdgeGeo32* __restrict__ geo,
     const float* __restrict__ pix, const float* __restrict__ wts, const int64_t* __restrict__ eoff,
     const int64_t* __restrict__ doff, int grid_w, GridP gp, IntrP in, const float* __restrict__ Hdd,
@@ -1513,25 +1516,48 @@ __global__ void __launch_bounds__(kPixBlock) k_backsub(
         load_rays<MODE>(pix, kbase, n, grid_w, gp, in, rx[2 * m], ry[2 * m], rx[2 * m + 1], ry[2 * m + 1]);
     }
   }
-  // the weight rows of edge e + 1 are loaded while edge e is computed
-  float4 wn[kTP];
-  auto ldw = [&](int e) {
-    const int64_t rb = eoff[e] + T.n0;
-#pragma unroll
-    for (int m = 0; m < kTP; ++m)
-      wn[m] = act[m] ? __ldg(reinterpret_cast<const float4*>(wts + 2 * (rb + 2 * (m * kPixBlock + tid))))
-                     : make_float4(0.f, 0.f, 0.f, 0.f);
+  // the tile's out-edge geometry and K-space steps, staged once (read every edge by all threads)
+  __shared__ float4 sgeo[64 * 4];
+  __shared__ float4 sstep[64 * 2];
+  // the weight rows of each out-edge (8 B per pixel, contiguous) stream through a 3-stage ring
+  // of bulk copies issued by thread 0, kBsStages edges ahead of the arithmetic
+  constexpr int kBsStages = 3;
+  __shared__ __align__(16) float4 wring[kBsStages][kTile / 2];
+  __shared__ __align__(8) unsigned long long wfull[kBsStages];
+  const int ne = T.ee - T.eb;
+  const uint32_t wbytes = (uint32_t)T.cnt * 8u;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  auto issue = [&](int q) {   // edge T.eb + q -> stage q % kBsStages
+    const int sidx = q % kBsStages;
+    mbar_expect_tx(&wfull[sidx], wbytes);
+    bulk_g2s(wring[sidx], wts + 2 * (eoff[T.eb + q] + T.n0), wbytes, &wfull[sidx], pol);
   };
-  if (T.eb < T.ee) ldw(T.eb);
+  for (int i = tid; i < 4 * ne; i += kPixBlock) sgeo[i] = __ldg(reinterpret_cast<const float4*>(geo + T.eb) + i);
+  for (int i = tid; i < 2 * ne; i += kPixBlock) sstep[i] = __ldg(reinterpret_cast<const float4*>(ustep + 8 * T.eb) + i);
+  if (tid == 0) {
+    for (int q = 0; q < kBsStages; ++q) mbar_init(&wfull[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int q = 0; q < kBsStages && q < ne; ++q) issue(q);
+  }
+  __syncthreads();
   for (int e = T.eb; e < T.ee; ++e) {
-    const EdgeGeo32 g = load_geo(geo, e);
-    const float4 ua = __ldg(reinterpret_cast<const float4*>(ustep + 8 * e));
-    const float2 ub = __ldg(reinterpret_cast<const float2*>(ustep + 8 * e + 4));
+    const int q = e - T.eb, sidx = q % kBsStages;
+    const EdgeGeo32 g = load_geo<true>(reinterpret_cast<const EdgeGeo32*>(sgeo), q);
+    const float4 ua = sstep[2 * q];
+    const float2 ub = make_float2(sstep[2 * q + 1].x, sstep[2 * q + 1].y);
     const int64_t rbase = eoff[e] + T.n0;
+    mbar_wait(&wfull[sidx], (uint32_t)(q / kBsStages) & 1u);
     float4 wc[kTP];
 #pragma unroll
-    for (int m = 0; m < kTP; ++m) wc[m] = wn[m];
-    if (e + 1 < T.ee) ldw(e + 1);
+    for (int m = 0; m < kTP; ++m) wc[m] = act[m] ? wring[sidx][m * kPixBlock + tid] : make_float4(0.f, 0.f, 0.f, 0.f);
+    // the stage is consumed (values in registers): refill it once every thread has read it
+    // (a CTA barrier measured faster here than K1's per-warp release counter)
+    __syncthreads();
+    if (tid == 0 && q + kBsStages < ne) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(q + kBsStages);
+    }
 #pragma unroll
     for (int m = 0; m < kTP; ++m) {
       const int p = m * kPixBlock + tid;
@@ -1541,26 +1567,36 @@ __global__ void __launch_bounds__(kPixBlock) k_backsub(
           load_rays<VBA_PIX_KF>(pix, rbase - T.n0, T.n0 + 2 * p, grid_w, gp, in, rx[2 * m], ry[2 * m],
                                 rx[2 * m + 1], ry[2 * m + 1]);
       }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int q = 2 * m + h;
-        const PxGeom o = project(g, rx[q], ry[q], dd[q]);
-        float w0 = h ? ww.z : ww.x, w1 = h ? ww.w : ww.y;
-        w0 = o.valid ? w0 : 0.f;
-        w1 = o.valid ? w1 : 0.f;
-        const float jd0 = fmaf(o.x, g.t[2], -g.t[0]) * o.izh;
-        const float jd1 = fmaf(o.y, g.t[2], -g.t[1]) * o.izh;
-        const float c0w = w0 * fx2 * jd0, c1w = w1 * fy2 * jd1;
-        const float xy = o.x * o.y;
-        // k_{n,e} . u_e
-        float s = ua.x * fmaf(c0w, xy, c1w * fmaf(o.y, o.y, 1.f));
-        s = fmaf(ua.y, fmaf(c0w, -fmaf(o.x, o.x, 1.f), c1w * -xy), s);
-        s = fmaf(ua.z, fmaf(c0w, o.y, c1w * -o.x), s);
-        s = fmaf(ua.w, c0w * -o.iz, s);
-        s = fmaf(ub.x, c1w * -o.iz, s);
-        s = fmaf(ub.y, fmaf(c0w, o.x * o.iz, c1w * (o.y * o.iz)), s);
-        acc[q] += s;
-      }
+      // the pixel pair in packed fp32 (FFMA2/FMUL2), the same operations as project() and
+      // the scalar coupling per lane
+      const float2 rxp = make_float2(rx[2 * m], rx[2 * m + 1]), ryp = make_float2(ry[2 * m], ry[2 * m + 1]);
+      const float2 d = make_float2(dd[2 * m], dd[2 * m + 1]);
+      const float2 Dx = FMA2(d, S2(g.t[0]), FMA2(S2(g.M[0]), rxp, FMA2(S2(g.M[1]), ryp, S2(g.M[2]))));
+      const float2 Dy = FMA2(d, S2(g.t[1]), FMA2(S2(g.M[3]), rxp, FMA2(S2(g.M[4]), ryp, S2(g.M[5]))));
+      const float2 Dz = FMA2(d, S2(g.t[2]), FMA2(S2(g.M[6]), rxp, FMA2(S2(g.M[7]), ryp, S2(g.M[8]))));
+      const float2 Xz = ADD2(S2(1.0f), Dz);
+      const float2 th = MUL2(S2(1e-6f), d);
+      const bool va = Xz.x > th.x, vb = Xz.y > th.y;
+      float2 izh = make_float2(va ? rcp_approx(Xz.x) : 0.f, vb ? rcp_approx(Xz.y) : 0.f);
+      izh = FMA2(izh, FMA2(-Xz, izh, S2(1.0f)), izh);
+      const float2 ddx = MUL2(FMA2(-rxp, Dz, Dx), izh);
+      const float2 ddy = MUL2(FMA2(-ryp, Dz, Dy), izh);
+      const float2 x = ADD2(rxp, ddx), y = ADD2(ryp, ddy), iz = MUL2(d, izh);
+      const float2 w0 = make_float2(va ? ww.x : 0.f, vb ? ww.z : 0.f);
+      const float2 w1 = make_float2(va ? ww.y : 0.f, vb ? ww.w : 0.f);
+      const float2 jd0 = MUL2(FMA2(x, S2(g.t[2]), S2(-g.t[0])), izh);
+      const float2 jd1 = MUL2(FMA2(y, S2(g.t[2]), S2(-g.t[1])), izh);
+      const float2 c0w = MUL2(MUL2(w0, S2(fx2)), jd0), c1w = MUL2(MUL2(w1, S2(fy2)), jd1);
+      const float2 xy = MUL2(x, y);
+      // k_{n,e} . u_e
+      float2 sv = MUL2(S2(ua.x), FMA2(c0w, xy, MUL2(c1w, FMA2(y, y, S2(1.f)))));
+      sv = FMA2(S2(ua.y), FMA2(c0w, -FMA2(x, x, S2(1.f)), MUL2(c1w, -xy)), sv);
+      sv = FMA2(S2(ua.z), FMA2(c0w, y, MUL2(c1w, -x)), sv);
+      sv = FMA2(S2(ua.w), MUL2(c0w, -iz), sv);
+      sv = FMA2(S2(ub.x), MUL2(c1w, -iz), sv);
+      sv = FMA2(S2(ub.y), FMA2(c0w, MUL2(x, iz), MUL2(c1w, MUL2(y, iz))), sv);
+      acc[2 * m] += sv.x;
+      acc[2 * m + 1] += sv.y;
     }
   }
   double mx = 0.0;
