@@ -1217,7 +1217,10 @@ __device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d, bool defer
   float* Ws = reinterpret_cast<float*>(smem_d);   // tile, then L (column-major, SWF)
   float* Xf = Ws + CT * SWF;                      // Y -> Linv (row-major, SWF)
   __shared__ int bad;
+  __shared__ unsigned short tri_tab[(CT / 4) * (CT / 4 + 1) / 2];   // triangle index -> (row << 5) | col
   const int tid = threadIdx.x;
+  for (int rb = 0; rb < CT / 4; ++rb)
+    for (int cw = tid; cw <= rb; cw += CHOL_THREADS) tri_tab[rb * (rb + 1) / 2 + cw] = (unsigned short)((rb << 5) | cw);
   float* Wk = a.W + tlin(k, k) * TILE_F;
   if (tid == 0) bad = 0;
   unsigned long long* ph = a.trace ? a.trace + 4 * (size_t)a.ntasks + 16 * (size_t)k : nullptr;   // phase stamps
@@ -1337,14 +1340,13 @@ __device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d, bool defer
       for (int b = tid - 32; b < nblk; b += CHOL_THREADS - 32) {
         if (b < nsy) {
           // mirrored so that consecutive b (lanes) walk down a block column: contiguous
-          // float4 rows of the column-major tile, conflict-free
-          int rb = (int)((sqrtf(8.f * b + 1.f) - 1.f) * 0.5f);
-          while ((rb + 1) * (rb + 2) / 2 <= b) ++rb;
-          while (rb * (rb + 1) / 2 > b) --rb;
-          const int cbk = nb4 - 1 - rb, rbk = nb4 - 1 - (b - rb * (rb + 1) / 2);
+          // float4 rows of the column-major tile, conflict-free; (rb, b - rb (rb+1)/2) of
+          // the triangle index from the table
+          const int tb = tri_tab[b], rb = tb >> 5, cw = tb & 31;
+          const int cbk = nb4 - 1 - rb, rbk = nb4 - 1 - cw;
           if (rbk >= 2) ablock(c0, r0 + 4 * rbk, r0 + 4 * cbk);   // rbk < 2: warp 0's diagonal block
         } else {
-          const int bb = b - nsy, rb = bb / nyc, cbk = bb % nyc;
+          const int bb = b - nsy, rb = bb / nyc, cbk = bb - rb * nyc;
           yblock(c0, r0 + 4 * rb, 4 * cbk);
         }
       }
