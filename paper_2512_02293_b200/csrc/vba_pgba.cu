@@ -364,12 +364,16 @@ __global__ void k_pg_pixel(const int32_t* __restrict__ pix_edge, const int32_t* 
 // ---------------------------------------------------------------------------
 // P2: per loop edge, the 15x15 Gram of [J_i | J_j | r] (fixed pixel order) -> factor record
 // ---------------------------------------------------------------------------
+constexpr int kPgRange = 256;   // pixels (rows) per CTA of k_pg_gram / k_pg_fill: partials summed in order
+
+// partial Grams: CTA (range x, edge y) over rows [r0 + x kPgRange, ...): 120 upper entries
+// (energy only: 1) to part[(y * nrng + x) * 120]
 __global__ void __launch_bounds__(128) k_pg_gram(const int64_t* __restrict__ voff, const double* __restrict__ rows,
-                                                 int energy_only, double* __restrict__ rec) {
+                                                 int energy_only, int nrng, double* __restrict__ part) {
   __shared__ double S[kPgChunk][kPgRow + 1];
-  __shared__ double G[15][15];
-  const int e = blockIdx.x, tid = threadIdx.x;
-  const int64_t r0 = voff[e], r1 = voff[e + 1];
+  const int e = blockIdx.y, tid = threadIdx.x;
+  const int64_t r0 = voff[e] + (int64_t)blockIdx.x * kPgRange;
+  const int64_t r1 = min(voff[e + 1], r0 + kPgRange);
   // thread t < 120 owns upper entry (a, b) of the 15x15 Gram (energy only: entry (14, 14))
   int a = -1, b = -1;
   if (energy_only) {
@@ -393,16 +397,39 @@ __global__ void __launch_bounds__(128) k_pg_gram(const int64_t* __restrict__ vof
         acc += S[p][16 + a] * S[p][16 + b];
       }
   }
-  if (a >= 0) {
+  if (energy_only) {
+    if (tid == 0) part[((int64_t)e * nrng + blockIdx.x) * 120] = acc;
+  } else if (tid < 120) {
+    part[((int64_t)e * nrng + blockIdx.x) * 120 + tid] = acc;
+  }
+}
+
+// per loop edge: the range partials summed in range order -> factor record
+__global__ void __launch_bounds__(128) k_pg_gram_fin(const double* __restrict__ part, int nrng, int energy_only,
+                                                     double* __restrict__ rec) {
+  __shared__ double G[15][15];
+  const int e = blockIdx.x, tid = threadIdx.x;
+  double* o = rec + (int64_t)kPgRec * e;
+  if (energy_only) {
+    if (tid == 0) {
+      double acc = 0.0;
+      for (int x = 0; x < nrng; ++x) acc += part[((int64_t)e * nrng + x) * 120];
+      o[161] = acc;
+    }
+    return;
+  }
+  if (tid < 120) {
+    double acc = 0.0;
+    for (int x = 0; x < nrng; ++x) acc += part[((int64_t)e * nrng + x) * 120 + tid];
+    int t = tid, a = 0, b = 0;
+    for (a = 0; a < 15; ++a) {
+      if (t < 15 - a) { b = a + t; break; }
+      t -= 15 - a;
+    }
     G[a][b] = acc;
     G[b][a] = acc;
   }
   __syncthreads();
-  double* o = rec + (int64_t)kPgRec * e;
-  if (energy_only) {
-    if (tid == 0) o[161] = G[14][14];
-    return;
-  }
   for (int k = tid; k < 49; k += blockDim.x) {
     const int r = k / 7, c = k % 7;
     o[k] = G[r][c];               // H_ii
@@ -584,12 +611,17 @@ __device__ __forceinline__ void pg_coupling(const PgSrc& S, const int64_t* voff,
   }
 }
 
+constexpr int kPgFillPart = 7 * kPgMaxPoses * (7 * kPgMaxPoses + 1) / 2 + 7 * kPgMaxPoses;   // doubles per partial
+
+// partial fill-ins: CTA (range x, source y) over pixels [x kPgRange, ...): the D(D+1)/2 lower
+// entries of F and the D entries of b to part[(y * nrng + x) * kPgFillPart]; the per-pixel
+// H_dd / g_d of its pixels
 __global__ void __launch_bounds__(256) k_pg_fill(const PgSrc* __restrict__ srcs, const int64_t* __restrict__ voff,
                                                  const double* __restrict__ rows, double lam, double ridge,
-                                                 double* __restrict__ arena, double* __restrict__ hdd,
+                                                 int nrng, double* __restrict__ part, double* __restrict__ hdd,
                                                  double* __restrict__ gd) {
   __shared__ double U[kPgChunk][7 * kPgMaxPoses + 2];
-  const PgSrc S = srcs[blockIdx.x];
+  const PgSrc S = srcs[blockIdx.y];
   const int tid = threadIdx.x, nth = blockDim.x;
   const int D = 7 * S.m;
   const int nent = D * (D + 1) / 2;   // lower entries (a >= b), row-major
@@ -599,8 +631,9 @@ __global__ void __launch_bounds__(256) k_pg_fill(const PgSrc* __restrict__ srcs,
 #pragma unroll
   for (int q = 0; q < kEnt; ++q) acc[q] = 0.0;
   const double damp = 1.0 + lam;
-  for (int64_t c0 = 0; c0 < S.npix; c0 += kPgChunk) {
-    const int cnt = (int)(S.npix - c0 < kPgChunk ? S.npix - c0 : kPgChunk);
+  const int64_t n0 = (int64_t)blockIdx.x * kPgRange, n1 = min(S.npix, n0 + kPgRange);
+  for (int64_t c0 = n0; c0 < n1; c0 += kPgChunk) {
+    const int cnt = (int)(n1 - c0 < kPgChunk ? n1 - c0 : kPgChunk);
     __syncthreads();
     if (tid < cnt) {
       double u[7 * kPgMaxPoses], h, g;
@@ -626,21 +659,40 @@ __global__ void __launch_bounds__(256) k_pg_fill(const PgSrc* __restrict__ srcs,
     if (tid < D)
       for (int p = 0; p < cnt; ++p) accg[0] += U[p][tid] * U[p][D + 1] * U[p][D];
   }
-  // record: blocks (A, B), A >= B, full 7x7 row-major each, then b (D)
-  double* o = arena + S.out;
+  double* o = part + ((int64_t)blockIdx.y * nrng + blockIdx.x) * kPgFillPart;
 #pragma unroll
   for (int q = 0; q < kEnt; ++q) {
     const int t = tid + q * nth;
     if (t >= nent) break;
-    int a = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-    while ((a + 1) * (a + 2) / 2 <= t) ++a;
-    while (a * (a + 1) / 2 > t) --a;
-    const int b = t - a * (a + 1) / 2;
-    const int A = a / 7, B = b / 7, ra = a % 7, cb = b % 7;
-    o[(A * (A + 1) / 2 + B) * 49 + ra * 7 + cb] = acc[q];
-    if (A == B && ra != cb) o[(A * (A + 1) / 2 + B) * 49 + cb * 7 + ra] = acc[q];
+    o[t] = acc[q];
   }
-  if (tid < D) o[(int64_t)S.m * (S.m + 1) / 2 * 49 + tid] = accg[0];
+  if (tid < D) o[nent + tid] = accg[0];
+}
+
+// per loop source: the range partials summed in range order -> fill record: blocks (A, B),
+// A >= B, full 7x7 row-major each, then b (D)
+__global__ void __launch_bounds__(256) k_pg_fill_fin(const PgSrc* __restrict__ srcs, const double* __restrict__ part,
+                                                     int nrng, double* __restrict__ arena) {
+  const PgSrc S = srcs[blockIdx.x];
+  const int D = 7 * S.m, nent = D * (D + 1) / 2;
+  const double* p = part + (int64_t)blockIdx.x * nrng * kPgFillPart;
+  double* o = arena + S.out;
+  const int nr = (int)((S.npix + kPgRange - 1) / kPgRange);
+  for (int t = threadIdx.x; t < nent + D; t += blockDim.x) {
+    double acc = 0.0;
+    for (int x = 0; x < nr; ++x) acc += p[(int64_t)x * kPgFillPart + t];
+    if (t < nent) {
+      int a = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+      while ((a + 1) * (a + 2) / 2 <= t) ++a;
+      while (a * (a + 1) / 2 > t) --a;
+      const int b = t - a * (a + 1) / 2;
+      const int A = a / 7, B = b / 7, ra = a % 7, cb = b % 7;
+      o[(A * (A + 1) / 2 + B) * 49 + ra * 7 + cb] = acc;
+      if (A == B && ra != cb) o[(A * (A + 1) / 2 + B) * 49 + cb * 7 + ra] = acc;
+    } else {
+      o[(int64_t)S.m * (S.m + 1) / 2 * 49 + (t - nent)] = acc;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -770,6 +822,8 @@ struct PgCtx {
   PgSrc* d_srcs = nullptr;
   double *d_rows = nullptr, *d_rows_t = nullptr, *d_arena = nullptr, *d_Wt = nullptr;
   double *d_hdd = nullptr, *d_gd = nullptr, *d_dxd = nullptr, *d_dx = nullptr;
+  int vrng = 1, frng = 1;   // pixel ranges of the widest loop edge / loop source (k_pg_gram / k_pg_fill CTAs)
+  double *d_gpart = nullptr, *d_fpart = nullptr;
   int64_t arena_rel = 0, arena_fill = 0, arena_len = 0;
   BlkPlan red, exp;
   bool exp_built = false;
@@ -924,7 +978,9 @@ static int pg_energy_stage(PgCtx* c, const double* state, const double* disp, cu
   int rc = pg_rows(c, state, disp, c->d_rows_t, st);
   if (rc) return rc;
   if (c->V) {
-    k_pg_gram<<<c->V, 128, 0, st>>>(c->d_voff, c->d_rows_t, 1, c->d_arena);
+    k_pg_gram<<<dim3(c->vrng, c->V), 128, 0, st>>>(c->d_voff, c->d_rows_t, 1, c->vrng, c->d_gpart);
+    k_pg_gram_fin<<<c->V, 128, 0, st>>>(c->d_gpart, c->vrng, 1, c->d_arena);
+    launch_count();
     launch_count();
   }
   if (c->R) {
@@ -942,7 +998,9 @@ static int pg_linearize(PgCtx* c, cudaStream_t st) {
   int rc = pg_rows(c, s, c->dp[c->cur], c->d_rows, st);
   if (rc) return rc;
   if (c->V) {
-    k_pg_gram<<<c->V, 128, 0, st>>>(c->d_voff, c->d_rows, 0, c->d_arena);
+    k_pg_gram<<<dim3(c->vrng, c->V), 128, 0, st>>>(c->d_voff, c->d_rows, 0, c->vrng, c->d_gpart);
+    k_pg_gram_fin<<<c->V, 128, 0, st>>>(c->d_gpart, c->vrng, 0, c->d_arena);
+    launch_count();
     launch_count();
   }
   if (c->R) {
@@ -957,8 +1015,11 @@ static int pg_linearize(PgCtx* c, cudaStream_t st) {
 static int pg_reduce(PgCtx* c, double lam, cudaStream_t st) {
   PG_CUDA(cudaMemsetAsync(c->d_res, 0, sizeof(PgResult), st));
   if (!c->srcs.empty()) {
-    k_pg_fill<<<(unsigned)c->srcs.size(), 256, 0, st>>>(c->d_srcs, c->d_voff, c->d_rows, lam, c->O.ridge, c->d_arena,
-                                                         c->d_hdd, c->d_gd);
+    k_pg_fill<<<dim3(c->frng, (unsigned)c->srcs.size()), 256, 0, st>>>(c->d_srcs, c->d_voff, c->d_rows, lam,
+                                                                        c->O.ridge, c->frng, c->d_fpart, c->d_hdd,
+                                                                        c->d_gd);
+    k_pg_fill_fin<<<(unsigned)c->srcs.size(), 256, 0, st>>>(c->d_srcs, c->d_fpart, c->frng, c->d_arena);
+    launch_count();
     launch_count();
   }
   if (c->nf > 0) {
@@ -1088,6 +1149,12 @@ int vba_pg_create(void** out, const vba_pg_problem* prob, const vba_options* opt
   for (int b = 0; b < 2; ++b)
     if ((rc = pg_alloc(c, &c->st[b], (size_t)8 * c->K)) || (rc = pg_alloc(c, &c->dp[b], (size_t)c->nd)))
       return fail(rc);
+  for (int v = 0; v < c->V; ++v)
+    c->vrng = std::max(c->vrng, (int)((voff[v + 1] - voff[v] + kPgRange - 1) / kPgRange));
+  for (const PgSrc& S : c->srcs) c->frng = std::max(c->frng, (int)((S.npix + kPgRange - 1) / kPgRange));
+  if ((rc = pg_alloc(c, &c->d_gpart, (size_t)120 * std::max(1, c->V) * c->vrng)) ||
+      (rc = pg_alloc(c, &c->d_fpart, (size_t)kPgFillPart * std::max<size_t>(1, c->srcs.size()) * c->frng)))
+    return fail(rc);
   if ((rc = pg_alloc(c, &c->d_rows, (size_t)kPgRow * c->nrows)) ||
       (rc = pg_alloc(c, &c->d_rows_t, (size_t)kPgRow * c->nrows)) || (rc = pg_alloc(c, &c->d_arena, (size_t)c->arena_len)) ||
       (rc = pg_alloc(c, &c->d_Wt, (size_t)49 * c->R)) || (rc = pg_alloc(c, &c->d_hdd, (size_t)c->nd)) ||
