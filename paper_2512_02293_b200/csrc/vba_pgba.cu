@@ -770,6 +770,47 @@ __global__ void k_pg_export_hpd(const PgSrc* __restrict__ srcs, const int64_t* _
   }
 }
 
+// dense reference path (use_schur=False, solver.py:291-304 through loopclosure.py:534): the
+// disparity rows of the full [free poses | disparities] system, column-major lower triangle
+// (ld = npad): row nf + p holds the couplings to the free pose columns of its source and
+// targets (node 0, the gauge, has none), the damped diagonal h (1 + lam) + ridge, rhs -g_d
+__global__ void k_pg_dense_disp(const PgSrc* __restrict__ srcs, const int64_t* __restrict__ voff,
+                                const double* __restrict__ rows, const int32_t* __restrict__ vj, int nf, int64_t ld,
+                                double lam, double ridge, double* __restrict__ D, double* __restrict__ rhs) {
+  const PgSrc S = srcs[blockIdx.y];
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= S.npix) return;
+  double u[7 * kPgMaxPoses], h, g;
+  pg_coupling(S, voff, rows, n, u, h, g);
+  const int64_t row = nf + S.doff + n;
+  for (int sl = 0; sl < S.m; ++sl) {
+    int node = S.node;
+    if (sl > 0)
+      for (int e = S.eb; e < S.ee; ++e)
+        if (S.slot[e - S.eb] == sl) { node = vj[e]; break; }
+    if (node == 0) continue;
+    for (int k = 0; k < 7; ++k) D[(int64_t)(7 * (node - 1) + k) * ld + row] = u[7 * sl + k];
+  }
+  D[row * ld + row] = h * (1.0 + lam) + ridge;
+  rhs[row] = -g;
+}
+
+__global__ void k_pg_dense_dxd(const double* __restrict__ x, int nf, int64_t nd, const double* __restrict__ dcur,
+                               double* __restrict__ dnxt, double* __restrict__ dxd,
+                               unsigned long long* __restrict__ step_bits) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double mx = 0.0;
+  if (p < nd) {
+    const double d = x[nf + p];
+    dnxt[p] = fmax(dcur[p] + d, kDispFloor64);
+    dxd[p] = d;
+    mx = fabs(d);
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx > 0.0) atomicMax(step_bits, (unsigned long long)__double_as_longlong(mx));
+}
+
 __global__ void k_pg_scatter(const double* __restrict__ x, int npv, double* __restrict__ dx_full) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;   // free layout = nodes 1.. (node 0 frozen)
   if (k < npv) dx_full[k] = k < 7 ? 0.0 : x[k - 7];
@@ -823,6 +864,12 @@ struct PgCtx {
   double *d_rows = nullptr, *d_rows_t = nullptr, *d_arena = nullptr, *d_Wt = nullptr;
   double *d_hdd = nullptr, *d_gd = nullptr, *d_dxd = nullptr, *d_dx = nullptr;
   int vrng = 1, frng = 1;   // pixel ranges of the widest loop edge / loop source (k_pg_gram / k_pg_fill CTAs)
+  // dense reference path (use_schur=False): the full system and its tile-DAG workspace, built on first use
+  bool dn_ready = false;
+  int dn_N = 0, dn_npad = 0, dn_nt = 0, n_dtasks = 0;
+  double *d_D = nullptr, *d_drhs = nullptr, *d_dx2 = nullptr, *d_dLinv = nullptr, *d_dpart = nullptr;
+  int* d_dflags = nullptr;
+  void* d_dtasks = nullptr;
   double *d_gpart = nullptr, *d_fpart = nullptr;
   int64_t arena_rel = 0, arena_fill = 0, arena_len = 0;
   BlkPlan red, exp;
@@ -1067,11 +1114,85 @@ static int pg_step(PgCtx* c, double lam, cudaStream_t st) {
   return VBA_OK;
 }
 
+static int pg_ensure_dense(PgCtx* c, cudaStream_t st) {
+  if (c->dn_ready) return VBA_OK;
+  const int64_t N = (int64_t)c->nf + c->nd;
+  if (N > 32768) {
+    pg_set_err("use_schur=False: dense system of %lld unknowns exceeds the verification-path limit", (long long)N);
+    return VBA_E_UNSUPPORTED;
+  }
+  c->dn_N = (int)N;
+  c->dn_npad = (int)((N + 127) / 128 * 128);
+  c->dn_nt = c->dn_npad / 128;
+  const size_t np = (size_t)c->dn_npad;
+  int rc;
+  if ((rc = pg_alloc(c, &c->d_D, np * np)) || (rc = pg_alloc(c, &c->d_drhs, np)) || (rc = pg_alloc(c, &c->d_dx2, np)) ||
+      (rc = pg_alloc(c, &c->d_dLinv, (size_t)c->dn_nt * 128 * 128)) ||
+      (rc = pg_alloc(c, &c->d_dpart, (size_t)c->dn_nt * c->dn_nt * 128)) ||
+      (rc = pg_alloc(c, &c->d_dflags, (size_t)2 * c->dn_nt * c->dn_nt + c->dn_nt + 1)))
+    return rc;
+  const int cap = chol_plan_tasks(c->dn_nt, nullptr, 0);
+  std::vector<char> buf((size_t)std::max(cap, 1) * chol_task_bytes());
+  c->n_dtasks = chol_plan_tasks(c->dn_nt, buf.data(), cap);
+  if ((rc = pg_alloc(c, (char**)&c->d_dtasks, buf.size()))) return rc;
+  PG_CUDA(cudaMemcpyAsync(c->d_dtasks, buf.data(), buf.size(), cudaMemcpyHostToDevice, st));
+  c->dn_ready = true;
+  return VBA_OK;
+}
+
+// the dense reference step: [damped H_ff | H_fd; H_df | damped diag(H_dd)] [dx_f; dx_d] = -[g_f; g_d]
+static int pg_step_dense(PgCtx* c, double lam, cudaStream_t st) {
+  int rc = pg_ensure_dense(c, st);
+  if (rc) return rc;
+  PG_CUDA(cudaMemsetAsync(c->d_res, 0, sizeof(PgResult), st));
+  PG_CUDA(cudaMemsetAsync(c->d_D, 0, sizeof(double) * (size_t)c->dn_npad * c->dn_npad, st));
+  PG_CUDA(cudaMemsetAsync(c->d_drhs, 0, sizeof(double) * c->dn_npad, st));
+  launch_pad_identity(c->d_D, c->dn_npad, c->dn_N, c->dn_npad, c->d_drhs, st);
+  if (c->nf > 0) {   // damped H_ff without the fill-in, and -g_f
+    launch_assemble(c->red.bptr, c->red.bnff, c->red.cs, c->red.nbr, c->red.roff, c->red.rdim, c->d_arena, lam,
+                    c->O.ridge, 1, c->d_D, c->dn_npad, 2, st, c->red.blist, c->red.nblist);
+    launch_assemble_vec(c->red.sptr, c->red.vs, c->red.nseg, c->red.soff, c->d_arena, -1.0, c->d_drhs, st, 1);
+  }
+  int64_t maxp = 0;
+  for (const PgSrc& S : c->srcs) maxp = std::max(maxp, S.npix);
+  if (maxp > 0) {
+    dim3 g((unsigned)((maxp + 127) / 128), (unsigned)c->srcs.size());
+    k_pg_dense_disp<<<g, 128, 0, st>>>(c->d_srcs, c->d_voff, c->d_rows, c->d_vj, c->nf, c->dn_npad, lam, c->O.ridge,
+                                       c->d_D, c->d_drhs);
+    launch_count();
+  }
+  const char* ch = getenv("VBA_CHOL");
+  if ((ch && std::strcmp(ch, "dag") == 0) ||
+      chol_small_solve(c->d_D, c->dn_npad, c->dn_N, c->d_drhs, c->d_dx2, &c->d_res->status, st))
+    chol_dag_launch(c->d_D, c->dn_npad, c->dn_nt, c->d_drhs, c->d_dx2, c->d_dLinv, c->d_dpart, c->d_dflags,
+                    c->d_dtasks, c->n_dtasks, &c->d_res->status, st, nullptr);
+  c->tc_ran = false;
+  const int npv = 7 * c->K;
+  k_pg_scatter<<<(npv + 127) / 128, 128, 0, st>>>(c->d_dx2, npv, c->d_dx);
+  launch_count();
+  const int nx = c->cur ^ 1;
+  if (c->nd > 0) {
+    k_pg_dense_dxd<<<(unsigned)((c->nd + 127) / 128), 128, 0, st>>>(c->d_dx2, c->nf, c->nd, c->dp[c->cur],
+                                                                     c->dp[nx], c->d_dxd, &c->d_res->step_bits);
+    launch_count();
+  }
+  k_pg_retract<<<(c->K + 127) / 128, 128, 0, st>>>(c->st[c->cur], c->st[nx], c->d_dx, c->K, &c->d_res->step_bits);
+  launch_count();
+  c->have_step = true;
+  return VBA_OK;
+}
+
+static int pg_step_any(PgCtx* c, double lam, int use_schur, cudaStream_t st) {
+  // the reference takes the Schur path only when there are disparities (solver.py:281)
+  if (use_schur || c->nd == 0) return pg_step(c, lam, st);
+  return pg_step_dense(c, lam, st);
+}
+
 static bool pg_tc_failed(PgCtx* c) { return c->tc_ran && (c->h_res->tc_bad != 0 || c->h_res->tc[4] != 1.0); }
 
 // one LM trial: step, energy of the trial state; returns status/new cost/step norm
 static int pg_trial(PgCtx* c, double lam, int* status, double* cost, double* step, cudaStream_t st) {
-  int rc = pg_step(c, lam, st);
+  int rc = pg_step_any(c, lam, c->O.use_schur, st);
   if (rc) return rc;
   const int nx = c->cur ^ 1;
   if ((rc = pg_energy_stage(c, c->st[nx], c->dp[nx], st))) return rc;
@@ -1111,10 +1232,6 @@ int vba_pg_create(void** out, const vba_pg_problem* prob, const vba_options* opt
   c->nrows = prob->n_rows;
   if (c->K <= 0 || c->V < 0 || c->R < 0 || c->nd < 0 || c->nrows < 0) { pg_set_err("invalid sizes"); return fail(VBA_E_INVALID); }
   if (!(opts->ridge > 0) || !(opts->damping > 0)) { pg_set_err("invalid options"); return fail(VBA_E_INVALID); }
-  if (!opts->use_schur && c->nd > 0) {
-    pg_set_err("use_schur=False is not implemented for pose graphs");
-    return fail(VBA_E_UNSUPPORTED);
-  }
   {  // T_bc = T_cb^-1 (loopclosure.py:254-256)
     double qi[4] = {1, 0, 0, 0}, t[3] = {0, 0, 0};
     if (prob->has_Tcb) {
@@ -1272,8 +1389,7 @@ int vba_pg_export_normal_eq(void* ctx, void* stream, double* H_pp, double* g_p, 
 int vba_pg_solve_step(void* ctx, void* stream, double lam, int32_t use_schur) {
   PgCtx* c = (PgCtx*)ctx;
   cudaStream_t st = (cudaStream_t)stream;
-  if (!use_schur && c->nd > 0) { pg_set_err("use_schur=False is not implemented for pose graphs"); return VBA_E_UNSUPPORTED; }
-  int rc = pg_step(c, lam, st);
+  int rc = pg_step_any(c, lam, use_schur, st);
   if (rc) return rc;
   PG_CUDA(cudaMemcpyAsync(c->h_res, c->d_res, sizeof(PgResult), cudaMemcpyDeviceToHost, st));
   PG_CUDA(cudaStreamSynchronize(st));

@@ -217,8 +217,9 @@ class DevicePoseGraph:
         """_solve_step on the pose graph (loopclosure.py:534): (dx_full [7K], dx_d [n_disp])."""
         import torch
         rc = self.lib.vba_pg_solve_step(self.ctx, self._sptr(), float(lam), int(bool(use_schur)))
-        if rc == L.VBA_E_NOT_SPD:
-            raise RuntimeError("singular reduced pose system")
+        if rc == L.VBA_E_NOT_SPD:   # solver.py:287-289 / 300-303
+            dense = not use_schur and self.n_disp > 0
+            raise RuntimeError("singular full system" if dense else "singular reduced pose system")
         L.check(rc)
         dx = torch.empty(self.K * SIM3_DOF, dtype=torch.float64, device=self.device)
         dxd = torch.empty(max(self.n_disp, 1), dtype=torch.float64, device=self.device)
@@ -233,11 +234,13 @@ class DevicePoseGraph:
         if rc == L.VBA_E_NONFINITE:
             raise RuntimeError("pose-graph energy is not finite")          # loopclosure.py:520-521
         L.check(rc)
+        msg = ("singular full system" if not self._o.use_schur and self.n_disp > 0
+               else "singular reduced pose system")
         term = {0: "max_iterations", 1: "converged", 2: "no_decrease_at_max_damping"}.get(
-            rep.termination, "singular: singular reduced pose system")
+            rep.termination, "singular: " + msg)
         return dict(iterations=rep.iterations, initial_cost=rep.initial_cost, final_cost=rep.final_cost,
                     cost_trajectory=[traj[i] for i in range(min(rep.n_costs, cap))], termination=term,
-                    condition_warnings=["singular reduced pose system"] * rep.n_warnings, trials=rep.trials)
+                    condition_warnings=[msg] * rep.n_warnings, trials=rep.trials)
 
     def download(self):
         """(states [K,8] = q wxyz, t, scale; disparities [n_disp] in the packed order)."""

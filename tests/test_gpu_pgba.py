@@ -146,3 +146,29 @@ def test_rank_deficient_information(cuda_ok):
     assert abs(e0 - cr[0]) <= 1e-10 * cr[0]
     assert rep["iterations"] == ref["iterations"] and rep["termination"] == ref["termination"]
     assert np.all(np.abs(c - cr) <= 1e-8 * cr + 1e-12 * cr[0])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", [n for n in NAMES if n.startswith("vision")])
+def test_dense_path_matches_schur(name, cuda_ok):
+    """use_schur=False on pose graphs with vision loops (loopclosure.py:534 passes opts.use_schur
+    to solver._solve_step, which then solves the full [poses | disparities] system,
+    solver.py:291-304): the step equals the Schur step and the oracle's dense step, and the
+    full LM solve follows the oracle's dense trajectory."""
+    import oracle.pgba as O
+    P, out, meta = load_pgba_golden(name)
+    opts = dict(meta["opts"], use_schur=False)
+    dp = _dp(copy.deepcopy(P), dict(meta, opts=opts))
+    dp.linearize()
+    dx_s, dd_s = dp.solve_step(opts["damping"], use_schur=True)
+    dx_d, dd_d = dp.solve_step(opts["damping"], use_schur=False)
+    ex = np.abs(dx_d - dx_s).max() / np.abs(dx_s).max()
+    ed = np.abs(dd_d - dd_s).max() / max(np.abs(dd_s).max(), 1e-300)
+    print(f"{name}: dense vs Schur step dx {ex:.1e} dx_d {ed:.1e}")
+    assert ex < 1e-8 and ed < 1e-8
+    rep = dp.solve()
+    ref = O.solve_pgba(copy.deepcopy(P), opts)
+    c, cr = np.array(rep["cost_trajectory"]), np.array(ref["cost_trajectory"])
+    print(f"  dense solve {rep['iterations']} it {rep['termination']} / {ref['iterations']} {ref['termination']}")
+    assert rep["iterations"] == ref["iterations"] and rep["termination"] == ref["termination"]
+    assert np.all(np.abs(c - cr) <= 1e-8 * cr + 1e-12 * cr[0])
