@@ -26,10 +26,18 @@ __global__ void __launch_bounds__(256) k_assemble(const int32_t* __restrict__ bp
                                                   int add_ridge, double* __restrict__ H, int64_t ld, int sym,
                                                   const int32_t* __restrict__ blist) {
   const int64_t id = blist ? blist[blockIdx.x] : blockIdx.x;   // blist: blocks with contributions
-  int a = (int)((sqrt(8.0 * (double)id + 1.0) - 1.0) * 0.5);
-  while ((int64_t)(a + 1) * (a + 2) / 2 <= id) ++a;
-  while ((int64_t)a * (a + 1) / 2 > id) --a;
-  const int b = (int)(id - (int64_t)a * (a + 1) / 2);
+  // block (a, b) of the packed lower index, decoded once per CTA (an fp64 sqrt per thread
+  // was a fifth of the kernel's instructions)
+  __shared__ int ab[2];
+  if (threadIdx.x == 0) {
+    int a0 = (int)((sqrtf(8.f * (float)id + 1.f) - 1.f) * 0.5f);
+    while ((int64_t)(a0 + 1) * (a0 + 2) / 2 <= id) ++a0;
+    while ((int64_t)a0 * (a0 + 1) / 2 > id) --a0;
+    ab[0] = a0;
+    ab[1] = (int)(id - (int64_t)a0 * (a0 + 1) / 2);
+  }
+  __syncthreads();
+  const int a = ab[0], b = ab[1];
   const int ra = rdim[a], cb = rdim[b];
   // sym bit 0: also write the upper triangle; bit 1: skip the Schur fill-in contributions
   const int p0 = bptr[id], pf = p0 + bnff[id], p1 = (sym & 2) ? pf : bptr[id + 1];
