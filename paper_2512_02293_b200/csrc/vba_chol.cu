@@ -2301,6 +2301,14 @@ void chol_trace_print(const char* tag, const unsigned long long* d_trace, const 
       }
     }
     if (ns > 0) fprintf(stderr, "  POTRF SM clock %.0f MHz\n", 1e3 * clk / ns);
+    if (getenv("VBA_CHOL_TRACE_STEPS"))   // per chain step: POTRF, operand wait, TRSM, SYRK wait, SYRK (us)
+      for (int k = 0; k < nt; ++k) {
+        const unsigned long long* q = &ph[16 * (size_t)k];
+        if (!q[0] || !q[10] || !q[4] || !q[7]) continue;
+        fprintf(stderr, "   step %2d: potrf %5.1f wait %5.1f trsm %5.1f wait %4.1f syrk %4.1f\n", k,
+                (double)(q[10] - q[0]) * 1e-3, (double)(q[4] - q[10]) * 1e-3, (double)(q[5] - q[4]) * 1e-3,
+                (double)(q[6] - q[5]) * 1e-3, (double)(q[7] - q[6]) * 1e-3);
+      }
     fprintf(stderr, "  POTRF phases (avg us): load %.2f | panels %.2f | inverse+store %.2f\n", ld / nt, u / nt,
             inv / nt);
     if (nd)

@@ -1042,20 +1042,12 @@ void launch_gram(int mode, const GramTile* gt, int ngt, int block, size_t smem, 
 // mbarriers) and run the epilogue; warp 8 owns TMEM (256 columns: 2 CTAs per SM) and
 // one of its lanes issues the MMAs.
 // ---------------------------------------------------------------------------
-#ifndef VBA_GTC_PW
-#define VBA_GTC_PW 8
-#endif
-#ifndef VBA_GTC_STAGES
-#define VBA_GTC_STAGES 2
-#endif
-#ifndef VBA_GTC_MINB
-#define VBA_GTC_MINB 2
-#endif
-constexpr int kGtcPW = VBA_GTC_PW;               // producer warps
+// measured alternatives: 12 or 16 producer warps, 3-4 stages at 1 CTA per SM
+constexpr int kGtcPW = 8;                        // producer warps
 constexpr int kGtcEPW = (31 + kGtcPW - 1) / kGtcPW;   // out-edges per producer warp (k <= 31)
 constexpr int kGtcThreads = (kGtcPW + 1) * 32;
 static_assert(kGtcPW % 4 == 0, "epilogue: whole groups of 4 warps (one per TMEM lane quarter)");
-constexpr int kGtcStages = VBA_GTC_STAGES;
+constexpr int kGtcStages = 2;
 constexpr int kGtcTmemCols = 256;
 
 __host__ __device__ __forceinline__ int gtc_mp(int kmax) { return (6 * kmax + 1 + 15) / 16 * 16; }
@@ -1068,7 +1060,7 @@ size_t gram_tc_smem_bytes(int kmax) {
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kGtcThreads, VBA_GTC_MINB) k_gram_tc(
+__global__ void __launch_bounds__(kGtcThreads, 2) k_gram_tc(
     const GramTile* __restrict__ gts, const float* __restrict__ disp, const EdgeGeo32* __restrict__ geo,
     const float* __restrict__ pix, const float* __restrict__ wts, const int64_t* __restrict__ eoff,
     const int64_t* __restrict__ doff, int grid_w, GridP gp, IntrP in, const float* __restrict__ Hdd,
@@ -1122,15 +1114,9 @@ __global__ void __launch_bounds__(kGtcThreads, VBA_GTC_MINB) k_gram_tc(
         for (int kk = 0; kk < 4; ++kk) {   // 8 tf32 (32 B) of K per MMA
           const uint32_t o = 32u * kk, acc = (c > 0 || kk > 0) ? 1u : 0u;
           tc_mma_tf32(d0, tc_sdesc(hi + o), tc_sdesc(hi + o), acc, id0);
-#ifndef VBA_GTC_HHONLY
           tc_mma_tf32(d0, tc_sdesc(hi + o), tc_sdesc(lo + o), 1u, id0);
           tc_mma_tf32(d0, tc_sdesc(lo + o), tc_sdesc(hi + o), 1u, id0);
-#endif
-#ifdef VBA_GTC_NOT1
-          if (false) {
-#else
           if (two) {
-#endif
             const uint32_t t1 = 128u * 128u;   // row 128 of the images
             tc_mma_tf32(d1, tc_sdesc(hi + t1 + o), tc_sdesc(hi + t1 + o), acc, id1);
             tc_mma_tf32(d1, tc_sdesc(hi + t1 + o), tc_sdesc(lo + t1 + o), 1u, id1);
@@ -1484,10 +1470,7 @@ void launch_step_edges(const int32_t* ei, const int32_t* ej, int E, const DevSta
 //   dx_d = (-g_d - sum_e k_{n,e} . u_e) / Hdd_d,   d' = max(d + dx_d, 1e-4)
 // ---------------------------------------------------------------------------
 template <int MODE>
-#ifndef VBA_BS_MINB
-#define VBA_BS_MINB 4
-#endif
-__global__ void __launch_bounds__(kPixBlock, VBA_BS_MINB) k_backsub(
+__global__ void __launch_bounds__(kPixBlock, 4) k_backsub(
     const PixTile* __restrict__ tiles, const float* __restrict__ disp, const EdgeGeo32* __restrict__ geo,
     const float* __restrict__ pix, const float* __restrict__ wts, const int64_t* __restrict__ eoff,
     const int64_t* __restrict__ doff, int grid_w, GridP gp, IntrP in, const float* __restrict__ Hdd,
