@@ -131,7 +131,7 @@ struct Ctx {
   bool force_fp64 = false;         // this step: fp64 DAG (tensor-core solve failed its checks)
   bool tc_ran = false;             // the last step's reduced solve ran on the tensor cores
   int tc_gen = 1;
-  int tc_iters = 8;   // refinement passes at most (early exit once converged)
+  int tc_iters = 5;   // refinement passes at most (early exit once converged; fp64 fallback beyond)
   int64_t tc_fallbacks = 0;
   int64_t tc_solves = 0, tc_passes = 0;
   int32_t* d_fmap = nullptr;

@@ -882,7 +882,7 @@ struct PgCtx {
   void* d_tctasks = nullptr;
   int n_tctasks = 0;
   bool use_tc = false, force_fp64 = false, tc_ran = false;
-  int tc_gen = 1, tc_iters = 8;
+  int tc_gen = 1, tc_iters = 5;
   int* d_status = nullptr;
   PgResult* d_res = nullptr;
   PgResult* h_res = nullptr;
