@@ -41,7 +41,7 @@ constexpr int CHOL_THREADS = 256;
 constexpr int SB = 36;           // 32x32 block stride in POTRF (doubles, = 4 mod 16)
 constexpr size_t CHOL_SMEM = (size_t)2 * 2 * KC * SP * sizeof(double);   // 2 stages x (A, B)
 
-enum TaskType { T_POTRF = 0, T_TRSM = 1, T_GEMM = 2, T_BUPD = 3, T_BSOL = 4, T_DIAG = 5, T_CHAIN = 6 };
+enum TaskType { T_POTRF = 0, T_TRSM = 1, T_GEMM = 2, T_BUPD = 3, T_BSOL = 4, T_DIAG = 5, T_CHAIN = 6, T_TILE = 7 };
 
 struct CholTask {
   int32_t type, i, j, k;
@@ -610,6 +610,22 @@ int chol_plan_tasks_tc(int nt, void* outv, int cap) {
     ++n;
   };
   if (nt <= 0) return 0;
+  const char* pl = getenv("VBA_CHOL_PLAN");
+  if (!(pl && pl[0] == 'r')) {
+    // Left-looking (default): one TILE task per off-chain lower tile, in the order the chain
+    // needs them.  At "step" s: the chain's TRSM operand (s+2, s+1) and SYRK target (s+2, s+2)
+    // of step s+1, then the tiles of column s+1 (each accumulating columns 0..s and applying
+    // the TRSM once the chain publishes Linv_{s+1}), the one feeding step s+2's operand first.
+    // TILE fields: k = number of columns accumulated, expect = 1 if the TRSM follows.
+    push(T_CHAIN, 0, 0, 0, 0);
+    for (int i = 2; i < nt; ++i) push(T_TRSM, i, 0, 0, 0);
+    for (int s = 0; s + 2 < nt; ++s) {
+      push(T_TILE, s + 2, s + 1, s + 1, 0);
+      push(T_TILE, s + 2, s + 2, s + 1, 0);
+      for (int i = s + 3; i < nt; ++i) push(T_TILE, i, s + 1, s + 1, 1);
+    }
+    return n;
+  }
   // the whole POTRF -> TRSM -> SYRK chain is one task (one CTA, the diagonal tile handed
   // from each SYRK to the next POTRF in shared memory), claimed first
   push(T_CHAIN, 0, 0, 0, 0);
@@ -1013,6 +1029,101 @@ __device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
       __stcg(reinterpret_cast<float4*>(Lg) + (16 * w + q) * (CT / 4) + lane,
              *reinterpret_cast<const float4*>(S + (16 * w + q) * EPS + 4 * lane));
     if (tid == 0) tc_bulk_commit_wait();   // image writes complete before the caller's fences
+  }
+}
+
+// TILE(i,j) (left-looking): W_ij = A_ij - sum_{m < mend} L_im L_jm^T with the sum formed
+// on the tensor cores and kept on chip -- column pairs accumulate in TMEM, each pair is
+// drained (fp32, round-to-nearest) into a register tile, and W_ij is written once -- then,
+// for trsm, L_ij = W_ij Linv_jj^T as tc_task_trsm.  The operand chunks of all columns are
+// one stream through the ring (the next pair's loads are in flight while a pair drains);
+// column m's images are waited for (done flags) when its first chunk is loaded.
+__device__ void tc_task_tile(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_t& nacc, uint32_t tmem, int i,
+                             int j, int mend, bool trsm) {
+  const int tid = threadIdx.x, nt = a.nt;
+  const int w = tid >> 5, lane = tid & 31;
+  const int c0 = 64 * (w >> 2);
+  const uint32_t trow = (uint32_t)(32 * (w & 3)) << 16;
+  float acc[64];
+#pragma unroll
+  for (int q = 0; q < 64; ++q) acc[q] = 0.f;
+  constexpr int GCH = 2 * TNCH;   // chunks per column pair
+  const int nchunks = mend * TNCH;
+  constexpr int PRE = TC_STAGES - 1;
+  for (int q = 0; q < nchunks + PRE; ++q) {
+    const int qc = q - PRE;
+    if (tid == 0) {
+      if (q < nchunks) {
+        const int m = q / TNCH, ch = q % TNCH;
+        if (ch == 0) {
+          int ns = 32;
+          while (ld_acquire(&a.done[i * nt + m]) < 1 || ld_acquire(&a.done[j * nt + m]) < 1) {
+            __nanosleep(ns);
+            if (ns < 1024) ns <<= 1;
+          }
+          proxy_fence_global();   // images written by other CTAs (generic) -> our bulk reads (async)
+        }
+        const uint32_t n = R.nfill++;
+        const int s = n % TC_STAGES;
+        if (n >= TC_STAGES) tc_mbar_wait(&R.empty[s], ((n / TC_STAGES) - 1) & 1);
+        const float* ia = a.img + tlin(i, m) * TILE_F + ch * (CT * TKC);
+        const float* ib = a.img + tlin(j, m) * TILE_F + ch * (CT * TKC);
+        unsigned char* st = R.base + (size_t)s * TSTAGE;
+        tc_expect_tx(&R.full[s], TSTAGE);
+        tc_bulk(st, ia, TCHUNK, &R.full[s]);
+        tc_bulk(st + TCHUNK, ia + IMGP_F, TCHUNK, &R.full[s]);
+        tc_bulk(st + 2 * TCHUNK, ib, TCHUNK, &R.full[s]);
+        tc_bulk(st + 3 * TCHUNK, ib + IMGP_F, TCHUNK, &R.full[s]);
+      }
+      if (qc >= 0) {
+        const uint32_t n = R.ncons++;
+        const int s = n % TC_STAGES;
+        tc_mbar_wait(&R.full[s], (n / TC_STAGES) & 1);
+        tc_fence_after();
+        tc_chunk_mma(R, s, tmem, qc % GCH == 0);
+        tc_commit(&R.empty[s]);
+        if (qc % GCH == GCH - 1 || qc == nchunks - 1) tc_commit(accf);
+      }
+    }
+    if (qc >= 0 && (qc % GCH == GCH - 1 || qc == nchunks - 1)) {   // a pair is complete: drain it
+      tc_mbar_wait(accf, nacc & 1);
+      ++nacc;
+      tc_fence_after();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float v[32];
+        tmem_ld_sum(tmem + trow + (uint32_t)(c0 + 32 * h), v);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) acc[32 * h + k] += v[k];
+      }
+      tc_fence_before();
+      __syncthreads();   // every lane has read the pair before the next pair's first MMA overwrites it
+    }
+  }
+  if (tid != 0) {
+    R.nfill += nchunks;
+    R.ncons += nchunks;
+  }
+  // W_ij = A_ij - acc, staged through shared memory (the ring is idle) and written coalesced
+  float* Cg = a.W + tlin(i, j) * TILE_F;
+  float4 o[16];
+  tc_epi_prefetch(Cg, o);
+  float* S = reinterpret_cast<float*>(R.base + TC_EPI_OFF);
+  {
+    const int row = 32 * (w & 3) + lane;
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+      *reinterpret_cast<float4*>(S + row * EPS + c0 + 4 * q) =
+          make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+  }
+  __syncthreads();
+  tc_epi_sub_store(Cg, o, S);
+  proxy_fence_shared();   // generic staging writes before later bulk copies into the ring
+  __syncthreads();        // W_ij complete (the TRSM below reads it back)
+  if (trsm) {
+    wait_geq(&a.done[j * nt + j], 1);
+    __syncthreads();
+    tc_task_trsm(a, R, accf, nacc, tmem, i, j);
   }
 }
 
@@ -1543,6 +1654,17 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
         }
         break;
       }
+      case T_TILE:
+        if (a.trace && tid == 0) a.trace[4 * t + 1] = gtimer();
+        tc_task_tile(a, R, &accf, nacc, tmem, T.i, T.j, T.k, T.expect != 0);
+        if (T.expect) proxy_fence_global();
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+          if (T.expect) st_release(&a.done[T.i * nt + T.j], 1);
+          else st_release(&a.upd[T.i * nt + T.j], T.k);
+        }
+        break;
       case T_GEMM:
         wait_geq(&a.done[T.i * nt + T.k], 1);
         wait_geq(&a.done[T.j * nt + T.k], 1);
@@ -2305,7 +2427,8 @@ void chol_trace_print(const char* tag, const unsigned long long* d_trace, const 
       for (int k = 0; k < nt; ++k) {
         const unsigned long long* q = &ph[16 * (size_t)k];
         if (!q[0] || !q[10] || !q[4] || !q[7]) continue;
-        fprintf(stderr, "   step %2d: potrf %5.1f wait %5.1f trsm %5.1f wait %4.1f syrk %4.1f\n", k,
+        fprintf(stderr, "   step %2d at %7.1f: potrf %5.1f wait %5.1f trsm %5.1f wait %4.1f syrk %4.1f\n", k,
+                (double)(q[0] - ph[0]) * 1e-3,
                 (double)(q[10] - q[0]) * 1e-3, (double)(q[4] - q[10]) * 1e-3, (double)(q[5] - q[4]) * 1e-3,
                 (double)(q[6] - q[5]) * 1e-3, (double)(q[7] - q[6]) * 1e-3);
       }
@@ -2320,8 +2443,8 @@ void chol_trace_print(const char* tag, const unsigned long long* d_trace, const 
   cudaMemcpy(tr.data(), d_trace, tr.size() * 8, cudaMemcpyDeviceToHost);
   cudaMemcpy(tk.data(), d_tasks, tk.size() * sizeof(CholTask), cudaMemcpyDeviceToHost);
   unsigned long long t0 = ~0ull, t1 = 0;
-  double busy[7] = {0, 0, 0, 0, 0, 0, 0}, wait[7] = {0, 0, 0, 0, 0, 0, 0};
-  int cnt[7] = {0, 0, 0, 0, 0, 0, 0};
+  double busy[8] = {0, 0, 0, 0, 0, 0, 0, 0}, wait[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int q = 0; q < ntasks; ++q) {
     if (tr[4 * q] == 0) continue;
     t0 = std::min(t0, tr[4 * q]);
@@ -2348,6 +2471,7 @@ void chol_trace_print(const char* tag, const unsigned long long* d_trace, const 
       for (int q = 0; q < ntasks; ++q) {
         const CholTask& T = tk[q];
         const bool hit = (T.type == T_GEMM && T.j == kk && (T.i == kk || T.i == kk + 1)) ||
+                         (T.type == T_GEMM && T.j == kk - 1 && T.i == kk + 1) ||
                          (T.type == T_TRSM && (T.i == kk || T.i == kk + 1)) || (T.type == T_DIAG && T.k >= kk - 2 && T.k <= kk);
         if (hit && tr[4 * q])
           fprintf(stderr, "   task %6d type %d (i %d j %d k %d k2 %d exp %d): grab %8.1f ready %8.1f done %8.1f sm %llu\n", q,
@@ -2366,9 +2490,9 @@ void chol_trace_print(const char* tag, const unsigned long long* d_trace, const 
               ((double)tr[4 * dg[0].second + 1] - (double)t0) * 1e-3, gap, gmax, kmax,
               ((double)tr[4 * dg.back().second + 2] - (double)t0) * 1e-3);
   }
-  const char* nm[7] = {"POTRF", "TRSM", "GEMM", "BUPD", "BSOL", "DIAG", "CHAIN"};
+  const char* nm[8] = {"POTRF", "TRSM", "GEMM", "BUPD", "BSOL", "DIAG", "CHAIN", "TILE"};
   fprintf(stderr, "[%s trace] nt=%d tasks=%d span %.1f us\n", tag, nt, ntasks, (double)(t1 - t0) * 1e-3);
-  for (int ty = 0; ty < 7; ++ty)
+  for (int ty = 0; ty < 8; ++ty)
     if (cnt[ty])
       fprintf(stderr, "  %-5s n=%6d  avg busy %8.2f us  avg wait %8.2f us  total busy %.1f us\n", nm[ty], cnt[ty],
               busy[ty] / cnt[ty], wait[ty] / cnt[ty], busy[ty]);
