@@ -42,6 +42,10 @@ constexpr int SB = 36;           // 32x32 block stride in POTRF (doubles, = 4 mo
 constexpr size_t CHOL_SMEM = (size_t)2 * 2 * KC * SP * sizeof(double);   // 2 stages x (A, B)
 
 enum TaskType { T_POTRF = 0, T_TRSM = 1, T_GEMM = 2, T_BUPD = 3, T_BSOL = 4, T_DIAG = 5, T_CHAIN = 6, T_TILE = 7 };
+// TILE task modes (CholTask::expect): the chain's SYRK target (W written, upd = columns),
+// the chain's TRSM operand (W and its hi/lo images written, upd = columns + 1), or an
+// off-chain tile whose TRSM follows in the same task (done = 1)
+enum TileMode { TILE_SYRK_TARGET = 0, TILE_TRSM = 1, TILE_OPERAND = 2 };
 
 struct CholTask {
   int32_t type, i, j, k;
@@ -605,51 +609,25 @@ int chol_plan_tasks(int nt, void* outv, int cap) {
 int chol_plan_tasks_tc(int nt, void* outv, int cap) {
   CholTask* out = reinterpret_cast<CholTask*>(outv);
   int n = 0;
-  auto push = [&](int type, int i, int j, int k, int expect, int k2 = -1) {
-    if (n < cap) out[n] = CholTask{type, i, j, k, expect, k2, {0, 0}};
+  auto push = [&](int type, int i, int j, int k, int expect) {
+    if (n < cap) out[n] = CholTask{type, i, j, k, expect, -1, {0, 0}};
     ++n;
   };
   if (nt <= 0) return 0;
-  const char* pl = getenv("VBA_CHOL_PLAN");
-  if (!(pl && pl[0] == 'r')) {
-    // Left-looking (default): one TILE task per off-chain lower tile, in the order the chain
-    // needs them.  At "step" s: the chain's TRSM operand (s+2, s+1) and SYRK target (s+2, s+2)
-    // of step s+1, then the tiles of column s+1 (each accumulating columns 0..s and applying
-    // the TRSM once the chain publishes Linv_{s+1}), the one feeding step s+2's operand first.
-    // TILE fields: k = number of columns accumulated, expect = 1 if the TRSM follows.
-    push(T_CHAIN, 0, 0, 0, 0);
-    for (int i = 2; i < nt; ++i) push(T_TRSM, i, 0, 0, 0);
-    for (int s = 0; s + 2 < nt; ++s) {
-      push(T_TILE, s + 2, s + 1, s + 1, 0);
-      push(T_TILE, s + 2, s + 2, s + 1, 0);
-      for (int i = s + 3; i < nt; ++i) push(T_TILE, i, s + 1, s + 1, 1);
-    }
-    return n;
-  }
-  // the whole POTRF -> TRSM -> SYRK chain is one task (one CTA, the diagonal tile handed
-  // from each SYRK to the next POTRF in shared memory), claimed first
+  // Left-looking: the chain task, then one TILE task per off-chain lower tile in the order
+  // the chain needs them.  At "step" s: the chain's TRSM operand (s+2, s+1) and SYRK target
+  // (s+2, s+2) of step s+1, then the tiles of column s+1 (each accumulating columns 0..s and
+  // applying its TRSM once the chain publishes Linv_{s+1}), the one feeding step s+2's
+  // operand first.  TILE fields: k = number of columns accumulated, expect = TILE_* mode.
+  // (Right-looking orders with per-update GEMM tasks left the chain waiting 6-41 us per step
+  // in the first third -- each update re-read and re-wrote its fp32 tile through L2.)
   push(T_CHAIN, 0, 0, 0, 0);
+  if (nt > 1) push(T_TILE, 1, 0, 0, TILE_OPERAND);
   for (int i = 2; i < nt; ++i) push(T_TRSM, i, 0, 0, 0);
-  // trailing update of tile (i, j) from column(s) s: a pair (s-1, s) for odd s, the single
-  // column s for even s and j = s + 2 (else none)
-  auto tupd = [&](int s, int i, int j) {
-    if (s & 1) push(T_GEMM, i, j, s - 1, s - 1, s);
-    else if (s == j - 2) push(T_GEMM, i, j, s, s);
-  };
-  for (int s = 0; s + 1 < nt; ++s) {
-    // next panel column (off-diagonal); its first task GEMM(s+2, s+1, s) -- what the chain's
-    // TRSM(s+2, s+1) waits for -- was queued ahead of the previous step's trailing updates
-    for (int i = s == 0 ? 2 : s + 3; i < nt; ++i) push(T_GEMM, i, s + 1, s, s);
-    for (int i = s + 3; i < nt; ++i) push(T_TRSM, i, s + 1, s + 1, s + 1);
-    // hoisted ahead of this step's trailing updates: the next step's first next-panel update
-    // and the next step's update of the chain's SYRK target tile (s+3, s+3)
-    if (s + 3 < nt) {
-      push(T_GEMM, s + 3, s + 2, s + 1, s + 1);
-      tupd(s + 1, s + 3, s + 3);
-    }
-    for (int j = s + 2; j < nt; ++j)
-      for (int i = j; i < nt; ++i)
-        if (!(s >= 1 && i == s + 2 && j == s + 2)) tupd(s, i, j);   // (s+2, s+2) was hoisted
+  for (int s = 0; s + 2 < nt; ++s) {
+    push(T_TILE, s + 2, s + 1, s + 1, TILE_OPERAND);
+    push(T_TILE, s + 2, s + 2, s + 1, TILE_SYRK_TARGET);
+    for (int i = s + 3; i < nt; ++i) push(T_TILE, i, s + 1, s + 1, TILE_TRSM);
   }
   return n;
 }
@@ -739,7 +717,12 @@ constexpr size_t TC_RING = (size_t)TC_STAGES * TSTAGE;
 constexpr size_t TC_EPI_OFF = (size_t)8 * TCHUNK;
 constexpr size_t TC_EPI_END = TC_EPI_OFF + (size_t)CT * (CT + 4) * 4;
 constexpr size_t TC_SMEM_0 = TC_RING > POTRF_SMEM ? TC_RING : POTRF_SMEM;
-constexpr size_t TC_SMEM = (TC_SMEM_0 > TC_EPI_END ? TC_SMEM_0 : TC_EPI_END) + 1024;
+// the chain's TRSM A operand (W_{k+1,k} hi/lo images, 64 KB), prefetched while POTRF(k) runs:
+// above POTRF's two 128 x 132 fp32 tiles (Ws, Xf: 135 KB)
+constexpr size_t TC_ABUF_OFF = (size_t)136 * 1024;
+constexpr size_t TC_ABUF_END = TC_ABUF_OFF + (size_t)4 * TCHUNK;
+constexpr size_t TC_SMEM_1 = TC_SMEM_0 > TC_EPI_END ? TC_SMEM_0 : TC_EPI_END;
+constexpr size_t TC_SMEM = (TC_SMEM_1 > TC_ABUF_END ? TC_SMEM_1 : TC_ABUF_END) + 1024;
 constexpr int64_t TILE_F = (int64_t)CT * CT;  // floats per tile (= the two fp16 image parts of a tile)
 constexpr int64_t IMGP_F = TILE_F / 2;        // one fp16 image part, in 4-byte words
 // instruction descriptor: D f32, A/B tf32, both K-major, N = 128, M = 128
@@ -875,60 +858,6 @@ __device__ __forceinline__ void tc_chunk_mma(const TcRing& R, int s, uint32_t tm
   }
 }
 
-// GEMM(i,j,k[,k2]):  W_ij -= L_ik L_jk^T (+ L_ik2 L_jk2^T)   (operands: images)
-__device__ void tc_task_gemm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_t& nacc, uint32_t tmem, int i,
-                             int j, int k, int k2) {
-  const int tid = threadIdx.x;
-  const int nchunks = (k2 >= 0 ? 2 : 1) * TNCH;
-  if (tid == 0) {
-    proxy_fence_global();   // images written by other CTAs (generic) -> our bulk reads (async)
-    constexpr int PRE = TC_STAGES - 1;
-    for (int q = 0; q < nchunks + PRE; ++q) {
-      if (q < nchunks) {
-        const uint32_t n = R.nfill++;
-        const int s = n % TC_STAGES;
-        if (n >= TC_STAGES) tc_mbar_wait(&R.empty[s], ((n / TC_STAGES) - 1) & 1);
-        const int kq = q < TNCH ? k : k2, ch = q % TNCH;
-        const float* ia = a.img + tlin(i, kq) * TILE_F + ch * (CT * TKC);
-        const float* ib = a.img + tlin(j, kq) * TILE_F + ch * (CT * TKC);
-        unsigned char* st = R.base + (size_t)s * TSTAGE;
-        tc_expect_tx(&R.full[s], TSTAGE);
-        tc_bulk(st, ia, TCHUNK, &R.full[s]);
-        tc_bulk(st + TCHUNK, ia + IMGP_F, TCHUNK, &R.full[s]);
-        tc_bulk(st + 2 * TCHUNK, ib, TCHUNK, &R.full[s]);
-        tc_bulk(st + 3 * TCHUNK, ib + IMGP_F, TCHUNK, &R.full[s]);
-      }
-      const int qc = q - PRE;
-      if (qc >= 0) {
-        const uint32_t n = R.ncons++;
-        const int s = n % TC_STAGES;
-        tc_mbar_wait(&R.full[s], (n / TC_STAGES) & 1);
-        tc_fence_after();
-        tc_chunk_mma(R, s, tmem, qc == 0);
-        tc_commit(&R.empty[s]);
-      }
-    }
-    tc_commit(accf);
-  } else {
-    R.nfill += nchunks;
-    R.ncons += nchunks;
-  }
-  // epilogue (C prefetched before waiting for the accumulator); the ring is idle
-  // once the accumulator is complete, so the staging tile may overlap it
-  float* Cg = a.W + tlin(i, j) * TILE_F;
-  float4 o[16];
-  tc_epi_prefetch(Cg, o);
-  tc_mbar_wait(accf, nacc & 1);
-  ++nacc;
-  tc_fence_after();
-  float* S = reinterpret_cast<float*>(R.base + TC_EPI_OFF);
-  tc_epi_stage(tmem, S);
-  tc_fence_before();
-  __syncthreads();
-  tc_epi_sub_store(Cg, o, S);
-  proxy_fence_shared();   // generic staging writes before later bulk copies into the ring
-}
-
 // TRSM(i,k):  L_ik = W_ik Linv_kk^T   (A = W_ik split by the threads, B = Linv images)
 __device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_t& nacc, uint32_t tmem, int i,
                              int k, bool keep_smem = false) {
@@ -1039,7 +968,7 @@ __device__ void tc_task_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
 // one stream through the ring (the next pair's loads are in flight while a pair drains);
 // column m's images are waited for (done flags) when its first chunk is loaded.
 __device__ void tc_task_tile(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_t& nacc, uint32_t tmem, int i,
-                             int j, int mend, bool trsm) {
+                             int j, int mend, int mode) {
   const int tid = threadIdx.x, nt = a.nt;
   const int w = tid >> 5, lane = tid & 31;
   const int c0 = 64 * (w >> 2);
@@ -1117,10 +1046,41 @@ __device__ void tc_task_tile(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
           make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
   }
   __syncthreads();
+  if (mode == TILE_OPERAND) {
+    // W_ij (fp32) and its hi/lo chunk images (the chain's TRSM A operand), the images
+    // built in the idle ring (global layout) and copied out by bulk stores
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int r = 16 * w + q, c = 4 * lane, ch = c >> 6;
+      const float4 d = *reinterpret_cast<const float4*>(S + r * EPS + c);
+      float4 t = o[q];
+      t.x -= d.x; t.y -= d.y; t.z -= d.z; t.w -= d.w;
+      __stcg(reinterpret_cast<float4*>(Cg) + r * (CT / 4) + lane, t);
+      uint2 hh, ll;
+      split4_h(t, hh, ll);
+      const int o2 = img_off(r, c) - ch * (CT * 64);   // fp16 units within the chunk
+      unsigned char* sh = R.base + (size_t)2 * ch * TCHUNK;
+      *reinterpret_cast<uint2*>(sh + 2 * o2) = hh;
+      *reinterpret_cast<uint2*>(sh + TCHUNK + 2 * o2) = ll;
+    }
+    proxy_fence_shared();   // generic image writes -> bulk-copy reads
+    __syncthreads();
+    if (tid == 0) {
+      float* ihi = a.img + tlin(i, j) * TILE_F;
+#pragma unroll
+      for (int ch = 0; ch < TNCH; ++ch) {
+        tc_bulk_store(ihi + ch * (CT * TKC), R.base + (size_t)2 * ch * TCHUNK, TCHUNK);
+        tc_bulk_store(ihi + IMGP_F + ch * (CT * TKC), R.base + (size_t)(2 * ch + 1) * TCHUNK, TCHUNK);
+      }
+      tc_bulk_commit_wait();   // the images are complete before the caller's fences and release
+    }
+    __syncthreads();
+    return;
+  }
   tc_epi_sub_store(Cg, o, S);
   proxy_fence_shared();   // generic staging writes before later bulk copies into the ring
   __syncthreads();        // W_ij complete (the TRSM below reads it back)
-  if (trsm) {
+  if (mode == TILE_TRSM) {
     wait_geq(&a.done[j * nt + j], 1);
     __syncthreads();
     tc_task_trsm(a, R, accf, nacc, tmem, i, j);
@@ -1129,55 +1089,47 @@ __device__ void tc_task_tile(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
 
 // Diagonal SYRK of DIAG(k): W_{k+1,k+1} -= L L^T with L = L_{k+1,k} already in shared
 // memory as chunk images (tc_task_trsm keep_smem): A and B descriptors share them.
-// TRSM(i,k) of the DIAG task: B = Linv_kk images already in shared memory at
-// 2 ch TCHUNK (POTRF's output), A = W_ik split into two 32-KB chunk buffers at
-// TC_EPI_OFF (chunk ch in buffer ch & 1; chunk ch >= 2 waits for the MMAs of ch - 2 on
-// dbar).  While the MMAs run, POTRF's bulk stores are drained and done[k][k] is
-// published.  The epilogue leaves L_ik's images in shared memory for the SYRK and
-// starts (does not wait for) their bulk stores.
-__device__ void tc_diag_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_t& nacc, uint32_t tmem, int i,
-                             int k, uint64_t* dbar, uint32_t* dcnt) {
-  const int tid = threadIdx.x;
-  const float* Wik = a.W + tlin(i, k) * TILE_F;
-  const int u0 = tid & 7, m0 = tid >> 3;
-  float4 areg[TNCH][4][2];   // unit u0 (8 columns) of rows m0 + 32 q of each 64-column chunk
-#pragma unroll
-  for (int ch = 0; ch < TNCH; ++ch)
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-      for (int v = 0; v < 2; ++v)
-        areg[ch][q][v] =
-            __ldcg(reinterpret_cast<const float4*>(Wik + (int64_t)(m0 + 32 * q) * CT + 64 * ch + 8 * u0 + 4 * v));
+// TRSM(k+1,k) of the chain: B = Linv_kk images already in shared memory at 2 ch TCHUNK
+// (POTRF's output), A = W_{k+1,k}'s hi/lo images, written by its TILE_OPERAND task, bulk
+// copied to TC_ABUF_OFF -- while POTRF(k) runs when the operand is ready by then.
+// While the MMAs run, POTRF's bulk stores are drained and done[k][k] is published.  The
+// epilogue leaves L_ik's images in shared memory for the SYRK and starts (does not wait
+// for) their bulk stores.
+// A operand of the chain's TRSM(i,k): W_ik's hi/lo images -> TC_ABUF_OFF (thread 0)
+__device__ __forceinline__ void tc_chain_operand_load(const TcArgs& a, unsigned char* base, int i, int k,
+                                                      uint64_t* lbar) {
+  proxy_fence_global();   // the images were written by another CTA
+  const float* ia = a.img + tlin(i, k) * TILE_F;
+  unsigned char* abuf = base + TC_ABUF_OFF;
+  tc_expect_tx(lbar, 2 * TNCH * TCHUNK);
 #pragma unroll
   for (int ch = 0; ch < TNCH; ++ch) {
-    const int b = ch & 1;
-    if (ch >= 2) tc_mbar_wait(&dbar[b], (dcnt[b] - 1) & 1);
-    unsigned char* abuf = R.base + TC_EPI_OFF + (size_t)b * 2 * TCHUNK;
-    unsigned char* hi = abuf;
-    unsigned char* lo = abuf + TCHUNK;
+    tc_bulk(abuf + (size_t)2 * ch * TCHUNK, ia + ch * (CT * TKC), TCHUNK, lbar);
+    tc_bulk(abuf + (size_t)(2 * ch + 1) * TCHUNK, ia + IMGP_F + ch * (CT * TKC), TCHUNK, lbar);
+  }
+}
+__device__ int tc_diag_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_t& nacc, uint32_t tmem, int i,
+                            int k, uint64_t* lbar, uint32_t& lcnt, bool prefetched, const int* sflag) {
+  int sv = 0;   // (thread 0) *sflag, loaded once the MMAs are issued
+  const int tid = threadIdx.x;
+  unsigned long long* ph = a.trace ? a.trace + 4 * (size_t)a.ntasks + 16 * (size_t)k : nullptr;
+  unsigned char* abuf = R.base + TC_ABUF_OFF;
+  if (tid == 0) {
+    if (!prefetched) tc_chain_operand_load(a, R.base, i, k, lbar);
+    tc_mbar_wait(lbar, lcnt & 1);
+    tc_fence_after();
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint2 h0, l0, h1, l1;
-      split4_h(areg[ch][q][0], h0, l0);
-      split4_h(areg[ch][q][1], h1, l1);
-      const int m = m0 + 32 * q;
-      const int off = (m >> 3) * 1024 + (m & 7) * 128 + ((u0 ^ (m & 7)) << 4);   // bytes
-      *reinterpret_cast<uint4*>(hi + off) = make_uint4(h0.x, h0.y, h1.x, h1.y);
-      *reinterpret_cast<uint4*>(lo + off) = make_uint4(l0.x, l0.y, l1.x, l1.y);
-    }
-    proxy_fence_shared();
-    __syncthreads();
-    if (tid == 0) {
-      tc_fence_after();
-      const uint32_t ah = su32(abuf), al = ah + TCHUNK, bh = su32(R.base + (size_t)2 * ch * TCHUNK);
+    for (int ch = 0; ch < TNCH; ++ch) {
+      const uint32_t ah = su32(abuf + (size_t)2 * ch * TCHUNK), al = ah + TCHUNK,
+                     bh = su32(R.base + (size_t)2 * ch * TCHUNK);
 #pragma unroll
       for (int kk = 0; kk < TKC / 8; ++kk) tc_mma3(tmem, ah + 32u * kk, al + 32u * kk, bh + 32u * kk, ch == 0 && kk == 0);
-      tc_commit(&dbar[b]);
     }
-    ++dcnt[b];
+    tc_commit(accf);
+    sv = ld_acquire(sflag);
   }
-  if (tid == 0) tc_commit(accf);
+  ++lcnt;
+  if (ph && tid == 0) ph[2] = gtimer();
   // publish POTRF(k): its bulk image stores and W_kk stores complete, then done[k][k]
   if (tid == 0) {
     tc_bulk_wait_all();
@@ -1186,9 +1138,11 @@ __device__ void tc_diag_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
   __threadfence();
   __syncthreads();
   if (tid == 0) st_release(&a.done[k * a.nt + k], 1);
+  if (ph && tid == 0) ph[3] = gtimer();
   tc_mbar_wait(accf, nacc & 1);
   ++nacc;
   tc_fence_after();
+  if (ph && tid == 0) ph[8] = gtimer();
   {
     const int w = tid >> 5, lane = tid & 31;
     const int row = 32 * (w & 3) + lane, c0 = 64 * (w >> 2);
@@ -1229,6 +1183,7 @@ __device__ void tc_diag_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
              *reinterpret_cast<const float4*>(S + (16 * w + q) * EPS + 4 * lane));
   }
   __syncthreads();   // S is reused by the SYRK epilogue
+  return sv;
 }
 
 __device__ void tc_task_syrk_smem(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_t& nacc, uint32_t tmem,
@@ -1267,6 +1222,7 @@ __device__ void tc_task_syrk_smem(const TcArgs& a, TcRing& R, uint64_t* accf, ui
 //   Xf  128 x 128 row-major, stride SWF: Y = L^-1
 // ---------------------------------------------------------------------------
 constexpr int SWF = CT + 4;      // 132: float4-aligned columns
+static_assert(TC_ABUF_OFF >= (size_t)2 * CT * SWF * sizeof(float), "chain A-operand buffer overlaps POTRF's tiles");
 
 // 8x8 Cholesky + inverse of the diagonal block at (c0, c0) by ONE thread in
 // registers (no barriers): L overwrites the block of Ws (column-major, upper part
@@ -1324,7 +1280,10 @@ __device__ __forceinline__ void diag8(float* Ws, float* Xf, int c0, int* bad) {
 // the factorisation).  Linv goes to W_kk (fp32 row-major, zeros above the
 // diagonal, for the triangular solves) and to its hi/lo images (TRSM operand).
 // from_smem: the updated diagonal tile is already in Ws (handed over by the chain's SYRK)
-__device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d, bool defer = false, bool from_smem = false) {
+// pf: (chain) the flag of the next TRSM operand W_{k+1,k}; the last thread polls it between
+// panels and starts the operand's bulk load (tc_chain_operand_load) once it is set (*pre = 1)
+__device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d, bool defer = false, bool from_smem = false,
+                              const int* pf = nullptr, uint64_t* lbar = nullptr, int* pre = nullptr) {
   float* Ws = reinterpret_cast<float*>(smem_d);   // tile, then L (column-major, SWF)
   float* Xf = Ws + CT * SWF;                      // Y -> Linv (row-major, SWF)
   __shared__ int bad;
@@ -1447,6 +1406,10 @@ __device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d, bool defer
       __syncwarp();
       if (tid == 0) diag8(Ws, Xf, r0, &bad);
     } else {
+      // operand poll: a relaxed load issued here, looked at after this panel's updates
+      int fv = 0;
+      const bool poll = pf && tid == CHOL_THREADS - 1 && !*pre;
+      if (poll) asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(fv) : "l"(pf) : "memory");
       const int nb4 = nr / 4, nsy = nb4 * (nb4 + 1) / 2, nyc = r0 / 4, nblk = nsy + nb4 * nyc;
       for (int b = tid - 32; b < nblk; b += CHOL_THREADS - 32) {
         if (b < nsy) {
@@ -1460,6 +1423,11 @@ __device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d, bool defer
           const int bb = b - nsy, rb = bb / nyc, cbk = bb - rb * nyc;
           yblock(c0, r0 + 4 * rb, 4 * cbk);
         }
+      }
+      if (poll && fv >= k + 1) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");   // acquire the release that set the flag
+        tc_chain_operand_load(a, reinterpret_cast<unsigned char*>(smem_d), k + 1, k, lbar);
+        *pre = 1;
       }
     }
     __syncthreads();
@@ -1512,11 +1480,11 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
   // 1024-B aligned (SW128 operand images) by pointer arithmetic on the __shared__
   // array itself, so the compiler keeps the shared state space (LDS/STS, not generic)
   unsigned char* sm = tc_raw + ((1024u - (su32(tc_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t full[TC_STAGES], empty[TC_STAGES], accf, dbar[2];
+  __shared__ uint64_t full[TC_STAGES], empty[TC_STAGES], accf, lbar;
   __shared__ uint32_t tmem_sh;
-  __shared__ int tsk;
+  __shared__ int tsk, pre_sh;
   const int tid = threadIdx.x, nt = a.nt;
-  uint32_t dcnt[2] = {0u, 0u};   // commits issued on dbar[0..1] (identical in every thread)
+  uint32_t lcnt = 0;   // phases of lbar completed (identical in every thread)
   if (tid < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_sh)),
                  "n"(TC_TMEM_COLS));
@@ -1528,8 +1496,7 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
       tc_mbar_init(&empty[s], 1);
     }
     tc_mbar_init(&accf, 1);
-    tc_mbar_init(&dbar[0], 1);
-    tc_mbar_init(&dbar[1], 1);
+    tc_mbar_init(&lbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   tc_fence_before();
@@ -1548,16 +1515,6 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
     unsigned long long t0 = 0;
     if (a.trace && tid == 0) t0 = gtimer();
     switch (T.type) {
-      case T_POTRF:
-        wait_geq(&a.upd[T.k * nt + T.k], T.expect);
-        __syncthreads();
-        if (a.trace && tid == 0) a.trace[4 * t + 1] = gtimer();
-        tc_task_potrf(a, T.k, reinterpret_cast<double*>(sm));
-        proxy_fence_global();
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) st_release(&a.done[T.k * nt + T.k], 1);
-        break;
       case T_TRSM:
         wait_geq(&a.done[T.k * nt + T.k], 1);
         wait_geq(&a.upd[T.i * nt + T.k], T.expect);
@@ -1569,17 +1526,10 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
         __syncthreads();
         if (tid == 0) st_release(&a.done[T.i * nt + T.k], 1);
         break;
-      case T_DIAG:
-      case T_CHAIN: {   // DIAG(k) = POTRF(k) -> TRSM(k+1,k) -> SYRK(k+1); T_CHAIN: every k in one CTA
-        const bool chain = T.type == T_CHAIN;
-        const int kend = chain ? nt : T.k + 1;
-        for (int k = T.k; k < kend; ++k) {
-          const bool cont = chain && k > T.k;   // the tile is in Ws: the previous step's SYRK put it there
-          if (!cont) {
-            wait_geq(&a.upd[k * nt + k], chain ? k : T.expect);
-            __syncthreads();
-            if (a.trace && tid == 0) a.trace[4 * t + 1] = gtimer();
-          }
+      case T_CHAIN:   // POTRF(k) -> TRSM(k+1,k) -> SYRK(k+1) for every k, in one CTA
+        if (a.trace && tid == 0) a.trace[4 * t + 1] = gtimer();
+        for (int k = 0; k < nt; ++k) {
+          const bool cont = k > 0;   // the tile is in Ws: the previous step's SYRK put it there
           if (k + 1 >= nt) {
             tc_task_potrf(a, k, reinterpret_cast<double*>(sm), false, cont);
             proxy_fence_global();
@@ -1590,14 +1540,17 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
           }
           // POTRF's outputs stay in shared memory as the TRSM's B operand; done[k][k] is
           // published inside tc_diag_trsm once POTRF's stores have drained
-          tc_task_potrf(a, k, reinterpret_cast<double*>(sm), true, cont);
+          if (tid == 0) pre_sh = 0;   // set once the TRSM operand's load is under way
+          tc_task_potrf(a, k, reinterpret_cast<double*>(sm), true, cont, &a.upd[(k + 1) * nt + k], &lbar, &pre_sh);
           unsigned long long* ph = a.trace ? a.trace + 4 * (size_t)a.ntasks + 16 * (size_t)k : nullptr;
-          wait_geq(&a.upd[(k + 1) * nt + k], k);
+          wait_geq(&a.upd[(k + 1) * nt + k], k + 1);   // W_{k+1,k} and its images (TILE_OPERAND)
           __syncthreads();
           if (ph && tid == 0) ph[4] = gtimer();
-          tc_diag_trsm(a, R, &accf, nacc, tmem, k + 1, k, dbar, dcnt);
+          // the SYRK target's flag is read (acquire) by thread 0 while the TRSM's MMAs run
+          const int sv = tc_diag_trsm(a, R, &accf, nacc, tmem, k + 1, k, &lbar, lcnt, pre_sh != 0,
+                                      &a.upd[(k + 1) * nt + k + 1]);
           if (ph && tid == 0) ph[5] = gtimer();
-          wait_geq(&a.upd[(k + 1) * nt + k + 1], k);
+          if (tid == 0 && sv < k) wait_geq(&a.upd[(k + 1) * nt + k + 1], k);
           __syncthreads();
           if (ph && tid == 0) ph[6] = gtimer();
           {   // SYRK(k+1) from the images in shared memory; L_{k+1,k} is published while it runs
@@ -1628,57 +1581,32 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
             tc_epi_stage(tmem, S);
             tc_fence_before();
             __syncthreads();
-            if (chain) {
-              // next POTRF's input straight into Ws (symmetric tile: row-major = column-major)
-              float* Wn = reinterpret_cast<float*>(sm);
-              const int w = tid >> 5, lane = tid & 31;
+            // next POTRF's input straight into Ws (symmetric tile: row-major = column-major)
+            float* Wn = reinterpret_cast<float*>(sm);
+            const int w = tid >> 5, lane = tid & 31;
 #pragma unroll
-              for (int q = 0; q < 16; ++q) {
-                const float4 d = *reinterpret_cast<const float4*>(S + (16 * w + q) * EPS + 4 * lane);
-                float4 v = o[q];
-                v.x -= d.x; v.y -= d.y; v.z -= d.z; v.w -= d.w;
-                *reinterpret_cast<float4*>(Wn + (16 * w + q) * SWF + 4 * lane) = v;
-              }
-              __syncthreads();
-            } else {
-              tc_epi_sub_store(Cg, o, S);
-              proxy_fence_shared();
+            for (int q = 0; q < 16; ++q) {
+              const float4 d = *reinterpret_cast<const float4*>(S + (16 * w + q) * EPS + 4 * lane);
+              float4 v = o[q];
+              v.x -= d.x; v.y -= d.y; v.z -= d.z; v.w -= d.w;
+              *reinterpret_cast<float4*>(Wn + (16 * w + q) * SWF + 4 * lane) = v;
             }
-          }
-          if (!chain) {
-            __threadfence();
+            proxy_fence_shared();   // S (generic writes) is where the next operand prefetch lands
             __syncthreads();
-            if (tid == 0) st_release(&a.upd[(k + 1) * nt + k + 1], k + 1);
           }
           if (ph && tid == 0) ph[7] = gtimer();
         }
         break;
-      }
       case T_TILE:
         if (a.trace && tid == 0) a.trace[4 * t + 1] = gtimer();
-        tc_task_tile(a, R, &accf, nacc, tmem, T.i, T.j, T.k, T.expect != 0);
-        if (T.expect) proxy_fence_global();
+        tc_task_tile(a, R, &accf, nacc, tmem, T.i, T.j, T.k, T.expect);
+        proxy_fence_global();
         __threadfence();
         __syncthreads();
         if (tid == 0) {
-          if (T.expect) st_release(&a.done[T.i * nt + T.j], 1);
-          else st_release(&a.upd[T.i * nt + T.j], T.k);
+          if (T.expect == TILE_TRSM) st_release(&a.done[T.i * nt + T.j], 1);
+          else st_release(&a.upd[T.i * nt + T.j], T.k + (T.expect == TILE_OPERAND ? 1 : 0));
         }
-        break;
-      case T_GEMM:
-        wait_geq(&a.done[T.i * nt + T.k], 1);
-        wait_geq(&a.done[T.j * nt + T.k], 1);
-        if (T.k2 >= 0) {
-          wait_geq(&a.done[T.i * nt + T.k2], 1);
-          wait_geq(&a.done[T.j * nt + T.k2], 1);
-        }
-        wait_geq(&a.upd[T.i * nt + T.j], T.expect);
-        __syncthreads();
-        if (a.trace && tid == 0) a.trace[4 * t + 1] = gtimer();
-        tc_task_gemm(a, R, &accf, nacc, tmem, T.i, T.j, T.k, T.k2);
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) st_release(&a.upd[T.i * nt + T.j], T.expect + (T.k2 >= 0 ? 2 : 1));
         break;
       default:
         break;
@@ -2427,10 +2355,10 @@ void chol_trace_print(const char* tag, const unsigned long long* d_trace, const 
       for (int k = 0; k < nt; ++k) {
         const unsigned long long* q = &ph[16 * (size_t)k];
         if (!q[0] || !q[10] || !q[4] || !q[7]) continue;
-        fprintf(stderr, "   step %2d at %7.1f: potrf %5.1f wait %5.1f trsm %5.1f wait %4.1f syrk %4.1f\n", k,
-                (double)(q[0] - ph[0]) * 1e-3,
-                (double)(q[10] - q[0]) * 1e-3, (double)(q[4] - q[10]) * 1e-3, (double)(q[5] - q[4]) * 1e-3,
-                (double)(q[6] - q[5]) * 1e-3, (double)(q[7] - q[6]) * 1e-3);
+        fprintf(stderr, "   step %2d at %7.1f: potrf %5.1f wait %5.1f trsm %5.1f [mma-issued %4.1f published %4.1f acc %4.1f] wait %4.1f syrk %4.1f\n", k,
+                (double)(q[0] - ph[0]) * 1e-3, (double)(q[10] - q[0]) * 1e-3, (double)(q[4] - q[10]) * 1e-3,
+                (double)(q[5] - q[4]) * 1e-3, (double)(q[2] - q[4]) * 1e-3, (double)(q[3] - q[4]) * 1e-3,
+                (double)(q[8] - q[4]) * 1e-3, (double)(q[6] - q[5]) * 1e-3, (double)(q[7] - q[6]) * 1e-3);
       }
     fprintf(stderr, "  POTRF phases (avg us): load %.2f | panels %.2f | inverse+store %.2f\n", ld / nt, u / nt,
             inv / nt);
