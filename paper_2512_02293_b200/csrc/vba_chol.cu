@@ -41,7 +41,7 @@ constexpr int CHOL_THREADS = 256;
 constexpr int SB = 36;           // 32x32 block stride in POTRF (doubles, = 4 mod 16)
 constexpr size_t CHOL_SMEM = (size_t)2 * 2 * KC * SP * sizeof(double);   // 2 stages x (A, B)
 
-enum TaskType { T_POTRF = 0, T_TRSM = 1, T_GEMM = 2, T_BUPD = 3, T_BSOL = 4, T_DIAG = 5, T_CHAIN = 6, T_TILE = 7 };
+enum TaskType { T_POTRF = 0, T_TRSM = 1, T_GEMM = 2, T_BUPD = 3, T_BSOL = 4, T_DIAG = 5, T_CHAIN = 6, T_TILE = 7, T_CONV = 8 };
 // TILE task modes (CholTask::expect): the chain's SYRK target (W written, upd = columns),
 // the chain's TRSM operand (W and its hi/lo images written, upd = columns + 1), or an
 // off-chain tile whose TRSM follows in the same task (done = 1)
@@ -629,6 +629,7 @@ int chol_plan_tasks_tc(int nt, void* outv, int cap) {
     push(T_TILE, s + 2, s + 2, s + 1, TILE_SYRK_TARGET);
     for (int i = s + 3; i < nt; ++i) push(T_TILE, i, s + 1, s + 1, TILE_TRSM);
   }
+  for (int k = 0; k < nt; ++k) push(T_CONV, k, k, k, 0);   // fp32 Linv_kk, L_{k+1,k} for the solves
   return n;
 }
 
@@ -1092,9 +1093,11 @@ __device__ void tc_task_tile(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
 // TRSM(k+1,k) of the chain: B = Linv_kk images already in shared memory at 2 ch TCHUNK
 // (POTRF's output), A = W_{k+1,k}'s hi/lo images, written by its TILE_OPERAND task, bulk
 // copied to TC_ABUF_OFF -- while POTRF(k) runs when the operand is ready by then.
-// While the MMAs run, POTRF's bulk stores are drained and done[k][k] is published.  The
-// epilogue leaves L_ik's images in shared memory for the SYRK and starts (does not wait
-// for) their bulk stores.
+// The epilogue leaves L_ik's hi/lo images in shared memory (the SYRK's operands) and starts
+// (does not wait for) their bulk stores.  done[k][k] is published with done[k+1][k] (the
+// TILE tasks waiting for Linv_kk are ~20 us off the chain's critical path).  The chain
+// stores only images: one SM's store bandwidth (~0.1 TB/s) made the fp32 copies of Linv_kk
+// and L_{k+1,k} cost ~2 us per step; CONV tasks rebuild them (hi + lo) off the chain.
 // A operand of the chain's TRSM(i,k): W_ik's hi/lo images -> TC_ABUF_OFF (thread 0)
 __device__ __forceinline__ void tc_chain_operand_load(const TcArgs& a, unsigned char* base, int i, int k,
                                                       uint64_t* lbar) {
@@ -1130,15 +1133,6 @@ __device__ int tc_diag_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_t
   }
   ++lcnt;
   if (ph && tid == 0) ph[2] = gtimer();
-  // publish POTRF(k): its bulk image stores and W_kk stores complete, then done[k][k]
-  if (tid == 0) {
-    tc_bulk_wait_all();
-    proxy_fence_global();
-  }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) st_release(&a.done[k * a.nt + k], 1);
-  if (ph && tid == 0) ph[3] = gtimer();
   tc_mbar_wait(accf, nacc & 1);
   ++nacc;
   tc_fence_after();
@@ -1146,7 +1140,6 @@ __device__ int tc_diag_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_t
   {
     const int w = tid >> 5, lane = tid & 31;
     const int row = 32 * (w & 3) + lane, c0 = 64 * (w >> 2);
-    float* S = reinterpret_cast<float*>(R.base + TC_EPI_OFF);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       float v[32];
@@ -1155,7 +1148,6 @@ __device__ int tc_diag_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_t
       for (int q = 0; q < 8; ++q) {
         const int cc = c0 + 32 * h + 4 * q, ch = cc >> 6;
         const float4 x = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        *reinterpret_cast<float4*>(S + row * EPS + cc) = x;
         uint2 hh, ll;
         split4_h(x, hh, ll);
         const int o2 = img_off(row, cc) - ch * (CT * 64);   // fp16 units within the chunk
@@ -1176,43 +1168,8 @@ __device__ int tc_diag_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_t
       }
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
-    float* Lg = a.W + tlin(i, k) * TILE_F;
-#pragma unroll
-    for (int q = 0; q < 16; ++q)
-      __stcg(reinterpret_cast<float4*>(Lg) + (16 * w + q) * (CT / 4) + lane,
-             *reinterpret_cast<const float4*>(S + (16 * w + q) * EPS + 4 * lane));
   }
-  __syncthreads();   // S is reused by the SYRK epilogue
   return sv;
-}
-
-__device__ void tc_task_syrk_smem(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_t& nacc, uint32_t tmem,
-                                  int i) {
-  const int tid = threadIdx.x;
-  float* Cg = a.W + tlin(i, i) * TILE_F;
-  float4 o[16];
-  tc_epi_prefetch(Cg, o);
-  if (tid == 0) {
-    tc_fence_after();
-    for (int ch = 0; ch < TNCH; ++ch) {
-      const uint32_t hi = su32(R.base + (size_t)2 * ch * TCHUNK), lo = hi + TCHUNK;
-#pragma unroll
-      for (int kk = 0; kk < TKC / 8; ++kk) {
-        const uint32_t off = 32u * kk;
-        tc_mma3(tmem, hi + off, lo + off, hi + off, ch == 0 && kk == 0);
-      }
-    }
-    tc_commit(accf);
-  }
-  tc_mbar_wait(accf, nacc & 1);
-  ++nacc;
-  tc_fence_after();
-  float* S = reinterpret_cast<float*>(R.base + TC_EPI_OFF);
-  tc_epi_stage(tmem, S);
-  tc_fence_before();
-  __syncthreads();
-  tc_epi_sub_store(Cg, o, S);
-  proxy_fence_shared();   // the ring is refilled by bulk copies after these generic writes
 }
 
 // ---------------------------------------------------------------------------
@@ -1451,7 +1408,6 @@ __device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d, bool defer
   for (int u = 0; u < CT * CT / 4 / CHOL_THREADS; ++u) {
     const int t4 = tid + u * CHOL_THREADS, r = t4 / (CT / 4), c = 4 * (t4 % (CT / 4)), ch = c >> 6;
     const float4 x = xo[u];
-    __stcg(reinterpret_cast<float4*>(Wk + r * CT + c), x);
     uint2 hh, ll;
     split4_h(x, hh, ll);
     const int o2 = img_off(r, c) - ch * (CT * 64);   // fp16 units within the chunk
@@ -1473,6 +1429,34 @@ __device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d, bool defer
   }
   if (ph && tid == 0) { ph[10] = gtimer(); ph[12] = clock64(); }
   if (!defer) __syncthreads();
+}
+
+// CONV(k): the fp32 tiles of the chain's outputs for the triangular solves, rebuilt from
+// their hi/lo images (hi + lo: 22 significant bits, the precision the factor's products
+// carry): W_kk = Linv_kk (zeros above the diagonal) and W_{k+1,k} = L_{k+1,k}
+__device__ void tc_task_conv(const TcArgs& a, int k) {
+  const int tid = threadIdx.x, nt = a.nt;
+  for (int t = 0; t < 2 && k + t < nt; ++t) {
+    const int i = k + t;
+    wait_geq(&a.done[i * nt + k], 1);
+    __syncthreads();
+    const __half* ih = reinterpret_cast<const __half*>(a.img + tlin(i, k) * TILE_F);
+    const __half* il = ih + 2 * IMGP_F;
+    float* Wg = a.W + tlin(i, k) * TILE_F;
+#pragma unroll 4
+    for (int u = 0; u < CT * CT / 4 / CHOL_THREADS; ++u) {
+      const int t4 = tid + u * CHOL_THREADS, r = t4 / (CT / 4), c = 4 * (t4 % (CT / 4));
+      const int o = img_off(r, c);
+      const uint2 h = __ldcg(reinterpret_cast<const uint2*>(ih + o));
+      const uint2 l = __ldcg(reinterpret_cast<const uint2*>(il + o));
+      const float2 h0 = __half22float2(*reinterpret_cast<const __half2*>(&h.x));
+      const float2 h1 = __half22float2(*reinterpret_cast<const __half2*>(&h.y));
+      const float2 l0 = __half22float2(*reinterpret_cast<const __half2*>(&l.x));
+      const float2 l1 = __half22float2(*reinterpret_cast<const __half2*>(&l.y));
+      __stcg(reinterpret_cast<float4*>(Wg + r * CT + c),
+             make_float4(h0.x + l0.x, h0.y + l0.y, h1.x + l1.x, h1.y + l1.y));
+    }
+  }
 }
 
 __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
@@ -1565,25 +1549,19 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
               }
               tc_commit(&accf);
             }
+            const int w = tid >> 5, lane = tid & 31;
+            float* S = reinterpret_cast<float*>(R.base + TC_EPI_OFF);
             float4 o[16];
             tc_epi_prefetch(Cg, o);
-            if (tid == 0) {
-              tc_bulk_wait_all();   // L_{k+1,k} images out
-              proxy_fence_global();
-            }
-            __threadfence();        // L_{k+1,k} fp32 rows out
             __syncthreads();
-            if (tid == 0) st_release(&a.done[(k + 1) * nt + k], 1);
             tc_mbar_wait(&accf, nacc & 1);
             ++nacc;
             tc_fence_after();
-            float* S = reinterpret_cast<float*>(R.base + TC_EPI_OFF);
             tc_epi_stage(tmem, S);
             tc_fence_before();
             __syncthreads();
             // next POTRF's input straight into Ws (symmetric tile: row-major = column-major)
             float* Wn = reinterpret_cast<float*>(sm);
-            const int w = tid >> 5, lane = tid & 31;
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
               const float4 d = *reinterpret_cast<const float4*>(S + (16 * w + q) * EPS + 4 * lane);
@@ -1592,10 +1570,23 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
               *reinterpret_cast<float4*>(Wn + (16 * w + q) * SWF + 4 * lane) = v;
             }
             proxy_fence_shared();   // S (generic writes) is where the next operand prefetch lands
+            // publish Linv_kk and L_{k+1,k} (their image stores have had the SYRK to drain)
+            if (tid == 0) {
+              tc_bulk_wait_all();
+              proxy_fence_global();
+            }
+            __threadfence();
             __syncthreads();
+            if (tid == 0) {
+              st_release(&a.done[k * nt + k], 1);
+              st_release(&a.done[(k + 1) * nt + k], 1);
+            }
           }
           if (ph && tid == 0) ph[7] = gtimer();
         }
+        break;
+      case T_CONV:
+        tc_task_conv(a, T.k);
         break;
       case T_TILE:
         if (a.trace && tid == 0) a.trace[4 * t + 1] = gtimer();
@@ -2355,9 +2346,9 @@ void chol_trace_print(const char* tag, const unsigned long long* d_trace, const 
       for (int k = 0; k < nt; ++k) {
         const unsigned long long* q = &ph[16 * (size_t)k];
         if (!q[0] || !q[10] || !q[4] || !q[7]) continue;
-        fprintf(stderr, "   step %2d at %7.1f: potrf %5.1f wait %5.1f trsm %5.1f [mma-issued %4.1f published %4.1f acc %4.1f] wait %4.1f syrk %4.1f\n", k,
+        fprintf(stderr, "   step %2d at %7.1f: potrf %5.1f wait %5.1f trsm %5.1f [mma-issued %4.1f acc %4.1f] wait %4.1f syrk %4.1f\n", k,
                 (double)(q[0] - ph[0]) * 1e-3, (double)(q[10] - q[0]) * 1e-3, (double)(q[4] - q[10]) * 1e-3,
-                (double)(q[5] - q[4]) * 1e-3, (double)(q[2] - q[4]) * 1e-3, (double)(q[3] - q[4]) * 1e-3,
+                (double)(q[5] - q[4]) * 1e-3, (double)(q[2] - q[4]) * 1e-3,
                 (double)(q[8] - q[4]) * 1e-3, (double)(q[6] - q[5]) * 1e-3, (double)(q[7] - q[6]) * 1e-3);
       }
     fprintf(stderr, "  POTRF phases (avg us): load %.2f | panels %.2f | inverse+store %.2f\n", ld / nt, u / nt,
@@ -2371,8 +2362,8 @@ void chol_trace_print(const char* tag, const unsigned long long* d_trace, const 
   cudaMemcpy(tr.data(), d_trace, tr.size() * 8, cudaMemcpyDeviceToHost);
   cudaMemcpy(tk.data(), d_tasks, tk.size() * sizeof(CholTask), cudaMemcpyDeviceToHost);
   unsigned long long t0 = ~0ull, t1 = 0;
-  double busy[8] = {0, 0, 0, 0, 0, 0, 0, 0}, wait[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  double busy[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, wait[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  int cnt[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int q = 0; q < ntasks; ++q) {
     if (tr[4 * q] == 0) continue;
     t0 = std::min(t0, tr[4 * q]);
@@ -2418,9 +2409,9 @@ void chol_trace_print(const char* tag, const unsigned long long* d_trace, const 
               ((double)tr[4 * dg[0].second + 1] - (double)t0) * 1e-3, gap, gmax, kmax,
               ((double)tr[4 * dg.back().second + 2] - (double)t0) * 1e-3);
   }
-  const char* nm[8] = {"POTRF", "TRSM", "GEMM", "BUPD", "BSOL", "DIAG", "CHAIN", "TILE"};
+  const char* nm[9] = {"POTRF", "TRSM", "GEMM", "BUPD", "BSOL", "DIAG", "CHAIN", "TILE", "CONV"};
   fprintf(stderr, "[%s trace] nt=%d tasks=%d span %.1f us\n", tag, nt, ntasks, (double)(t1 - t0) * 1e-3);
-  for (int ty = 0; ty < 8; ++ty)
+  for (int ty = 0; ty < 9; ++ty)
     if (cnt[ty])
       fprintf(stderr, "  %-5s n=%6d  avg busy %8.2f us  avg wait %8.2f us  total busy %.1f us\n", nm[ty], cnt[ty],
               busy[ty] / cnt[ty], wait[ty] / cnt[ty], busy[ty]);
