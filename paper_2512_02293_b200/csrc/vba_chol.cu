@@ -1159,7 +1159,7 @@ __device__ int tc_diag_trsm(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_t
     tc_fence_before();
     proxy_fence_shared();
     __syncthreads();
-    if (tid == 0) {
+    if (tid == CHOL_THREADS - 1) {   // the chain's publishing thread
       float* ihi = a.img + tlin(i, k) * TILE_F;
 #pragma unroll
       for (int ch = 0; ch < TNCH; ++ch) {
@@ -1417,7 +1417,7 @@ __device__ void tc_task_potrf(const TcArgs& a, int k, double* smem_d, bool defer
   }
   proxy_fence_shared();   // generic image writes -> bulk-copy / tcgen05 reads
   __syncthreads();
-  if (tid == 0) {
+  if (tid == (defer ? CHOL_THREADS - 1 : 0)) {   // deferred: the chain's publishing thread
     float* ihi = a.img + tlin(k, k) * TILE_F;
 #pragma unroll
     for (int ch = 0; ch < TNCH; ++ch) {
@@ -1553,6 +1553,13 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
             float* S = reinterpret_cast<float*>(R.base + TC_EPI_OFF);
             float4 o[16];
             tc_epi_prefetch(Cg, o);
+            if (tid == CHOL_THREADS - 1) {   // publish Linv_kk and L_{k+1,k} (the images are all the
+              tc_bulk_wait_all();            // chain CTA writes: no CTA-wide fence needed)
+              proxy_fence_global();
+              __threadfence();
+              st_release(&a.done[k * nt + k], 1);
+              st_release(&a.done[(k + 1) * nt + k], 1);
+            }
             __syncthreads();
             tc_mbar_wait(&accf, nacc & 1);
             ++nacc;
@@ -1570,17 +1577,7 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
               *reinterpret_cast<float4*>(Wn + (16 * w + q) * SWF + 4 * lane) = v;
             }
             proxy_fence_shared();   // S (generic writes) is where the next operand prefetch lands
-            // publish Linv_kk and L_{k+1,k} (their image stores have had the SYRK to drain)
-            if (tid == 0) {
-              tc_bulk_wait_all();
-              proxy_fence_global();
-            }
-            __threadfence();
             __syncthreads();
-            if (tid == 0) {
-              st_release(&a.done[k * nt + k], 1);
-              st_release(&a.done[(k + 1) * nt + k], 1);
-            }
           }
           if (ph && tid == 0) ph[7] = gtimer();
         }
