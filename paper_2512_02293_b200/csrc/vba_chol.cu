@@ -1583,6 +1583,7 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
         }
         break;
       case T_CONV:
+        if (a.trace && tid == 0) a.trace[4 * t + 1] = gtimer();
         tc_task_conv(a, T.k);
         break;
       case T_TILE:
