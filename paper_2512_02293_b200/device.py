@@ -285,10 +285,12 @@ class HostLayout:
         self.w, self._w_t = _host_buffer((n_rows_pad, 2), np.float32, pinned)
 
         kpix = S.kpix
-        # weight signs are checked here for host-only layouts, else on the device after the
-        # upload (DeviceProblem), which reads the fp32 copy at HBM speed instead of the fp64 source
-        self.weights_checked = not pinned
-        neg = self._fill_edges(S, order, ei, rows, rows_pad, kpix, check_neg=not pinned)
+        # weight signs: checked while packing by the native packer (graph sources: the weights
+        # are read there anyway) and for host-only layouts; pinned packed-dict layouts are
+        # checked on the device after the upload (DeviceProblem), which reads the fp32 copy at
+        # HBM speed instead of the fp64 source
+        self.weights_checked = not pinned or isinstance(S, _GraphSource)
+        neg = self._fill_edges(S, order, ei, rows, rows_pad, kpix, check_neg=self.weights_checked)
         if neg:
             raise ValueError("weights must be non-negative")
 
@@ -461,8 +463,9 @@ class DeviceProblem:
                     dst.copy_(pinned.reshape(-1), non_blocking=True)
                 elif isinstance(a, torch.Tensor):   # device-resident source (window.DeviceWindow)
                     dst.copy_(a.reshape(-1), non_blocking=True)
-                else:
-                    dst.copy_(torch.from_numpy(np.ascontiguousarray(a).reshape(-1)).to(dst.dtype), non_blocking=False)
+                else:   # small host arrays: through page-locked staging (torch's caching host allocator), async
+                    src = torch.from_numpy(np.ascontiguousarray(a).reshape(-1)).to(dst.dtype)
+                    dst.copy_(src.pin_memory() if pin else src, non_blocking=pin is not None)
             put(self.d_state.view(-1), H.state)
             put(self.d_ts, H.ts)
             put(self.d_disp64, H.disp64, pin[2] if pin else None)   # the fp32 copy is derived natively
