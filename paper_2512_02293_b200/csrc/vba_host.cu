@@ -902,6 +902,9 @@ static bool tc_failed(Ctx* c, int use_schur) {
   const Result& r = *c->h_res;
   ++c->tc_solves;
   c->tc_passes += (int64_t)r.tc[2];
+  if (getenv("VBA_TC_REFINE_TRACE"))   // passes, previous pass's and last pass's relative corrections
+    fprintf(stderr, "tc refine: passes %.0f rel_prev %.3e rel_last %.3e accepted %.0f\n", r.tc[2], r.tc[3],
+            r.tc[1] > 0 ? r.tc[0] / r.tc[1] : 0.0, r.tc[4]);
   return r.tc_bad != 0 || r.tc[4] != 1.0;
 }
 
