@@ -213,6 +213,14 @@ VBA_API int vba_stats(void* ctx, int64_t* out4);
  * the environment variable VBA_GRAM=tc|dmma, read by vba_create, forces either. */
 VBA_API int vba_gram_kind(void* ctx);
 
+/* Task list of the tensor-core Cholesky DAG for nt 128-row tiles (host only, no GPU):
+ * writes min(count, cap) tasks as 5 ints each -- type (1 TRSM of column 0, 6 the chain task,
+ * 7 a left-looking tile task, 8 a CONV task), i, j, k (TILE: columns accumulated), mode
+ * (TILE: 0 SYRK target, 1 followed by its TRSM, 2 the chain's TRSM operand) -- in claim order
+ * and returns the count.  Exposed so the host tests can check the DAG's invariants (every tile
+ * produced once, every dependency earlier in claim order or on the chain). */
+VBA_API int vba_chol_plan(int32_t nt, int32_t* out5, int32_t cap);
+
 /* Standalone SPD solve H x = b of a dense fp64 n x n system (column-major,
  * lower triangle read; device pointers), replacing np.linalg.solve(Hred, -gred)
  * of solver.py:287.  mode 0: tcgen05 split-fp16 (3-product) Cholesky + fp64 iterative

@@ -22,7 +22,7 @@ EXPORTED = ("vba_last_error", "vba_version", "vba_create", "vba_destroy", "vba_s
             "vba_reduced_dim", "vba_energy", "vba_linearize", "vba_export_normal_eq",
             "vba_solve_step", "vba_export_step", "vba_export_reduced", "vba_apply_step", "vba_restore", "vba_accept",
             "vba_trial", "vba_solve", "vba_download", "vba_launch_count", "vba_stage_times",
-            "vba_load_state", "vba_bind_inputs", "vba_set_profiling", "vba_stats", "vba_gram_kind", "vba_spd_solve", "vba_solve_times",
+            "vba_load_state", "vba_bind_inputs", "vba_set_profiling", "vba_stats", "vba_gram_kind", "vba_chol_plan", "vba_spd_solve", "vba_solve_times",
             "vba_preintegrate", "vba_preint_scratch_bytes",
             "vba_preint_factor_records", "vba_copy_segments",
             "vba_pg_create", "vba_pg_destroy", "vba_pg_energy", "vba_pg_linearize", "vba_pg_export_normal_eq",
@@ -156,6 +156,7 @@ def load(path: str | None = None):
         "vba_set_profiling": ([v, C.c_int32], C.c_int),
         "vba_stats": ([v, C.POINTER(C.c_int64)], C.c_int),
         "vba_gram_kind": ([v], C.c_int),
+        "vba_chol_plan": ([C.c_int32, v, C.c_int32], C.c_int),
         "vba_copy_segments": ([v, C.c_int32, v], C.c_int),
         "vba_solve_times": ([v, C.POINTER(C.c_double)], C.c_int),
         "vba_spd_solve": ([v, C.c_int64, v, v, C.c_int32, v, C.POINTER(C.c_int32)], C.c_int),

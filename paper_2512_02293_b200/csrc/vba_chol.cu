@@ -674,6 +674,16 @@ int chol_dag_launch(double* A, int64_t ld, int nt, double* rhs, double* x, doubl
 }  // namespace vba
 
 namespace vba {
+void chol_task_fields5(const void* tasks, int n, int* out5) {
+  const CholTask* t = reinterpret_cast<const CholTask*>(tasks);
+  for (int q = 0; q < n; ++q) {
+    out5[5 * q + 0] = t[q].type;
+    out5[5 * q + 1] = t[q].i;
+    out5[5 * q + 2] = t[q].j;
+    out5[5 * q + 3] = t[q].k;
+    out5[5 * q + 4] = t[q].expect;
+  }
+}
 void chol_task_fields(const void* tasks, int n, int* out4) {
   const CholTask* t = reinterpret_cast<const CholTask*>(tasks);
   for (int q = 0; q < n; ++q) {

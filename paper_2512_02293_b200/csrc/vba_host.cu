@@ -1207,6 +1207,18 @@ int vba_stats(void* ctx, int64_t* out4) {
 
 int vba_gram_kind(void* ctx) { return ((Ctx*)ctx)->gram_tc ? 1 : 0; }
 
+int vba_chol_plan(int32_t nt, int32_t* out5, int32_t cap) {
+  if (nt < 0 || cap < 0 || (cap > 0 && !out5)) { set_err("vba_chol_plan: bad arguments"); return VBA_E_INVALID; }
+  const int n = chol_plan_tasks_tc(nt, nullptr, 0);
+  std::vector<char> tb((size_t)std::max(n, 1) * chol_task_bytes());
+  chol_plan_tasks_tc(nt, tb.data(), n);
+  std::vector<int> f((size_t)5 * std::max(n, 1));
+  chol_task_fields5(tb.data(), n, f.data());
+  for (int q = 0; q < n && q < cap; ++q)
+    for (int u = 0; u < 5; ++u) out5[5 * q + u] = f[5 * (size_t)q + u];
+  return n;
+}
+
 // Standalone SPD solve (np.linalg.solve of solver.py:287 on a damped reduced system).
 int vba_spd_solve(const double* H, int64_t n, const double* b, double* x, int32_t mode, void* stream,
                   int32_t* info) {

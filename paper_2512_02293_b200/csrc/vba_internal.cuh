@@ -355,6 +355,7 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
 void chol_trace_print(const char* tag, const unsigned long long* d_trace, const void* d_tasks, int ntasks, int nt);
 // copy the task list back (for trace decoding): type,i,j,k per task
 void chol_task_fields(const void* tasks, int n, int* out4);
+void chol_task_fields5(const void* tasks, int n, int* out5);
 void launch_scatter_dx(const double* x, const int32_t* free_map, int npv, double* dx_full, cudaStream_t st);
 // pose-disparity coupling writer: reference-layout export (colmap == NULL, rows k*sdof+a) or the
 // free-layout full dense system of the use_schur=False path (rows colmap[k]+a, plus the damped
