@@ -633,6 +633,27 @@ int chol_plan_tasks_tc(int nt, void* outv, int cap) {
   return n;
 }
 
+// Launch with every CTA guaranteed co-resident (cooperative launch).  The DAG Cholesky
+// kernels and the triangular-solve chains hand work between CTAs through flags in global
+// memory, so a CTA that never got an SM would leave the others spinning (e.g. next to other
+// work on the GPU); a grid that cannot be co-resident fails the launch (reported as
+// VBA_E_CUDA by the caller's error check) instead of hanging.
+template <class... KArgs, class... Args>
+static void launch_coresident(void (*k)(KArgs...), int grid, int block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t lc = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  lc.gridDim = dim3((unsigned)grid);
+  lc.blockDim = dim3((unsigned)block);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = st;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  cudaLaunchKernelEx(&lc, k, args...);
+}
+
 size_t chol_smem_bytes() { return CHOL_SMEM; }
 
 int chol_dag_launch(double* A, int64_t ld, int nt, double* rhs, double* x, double* Linv, double* part, int* flags,
@@ -666,7 +687,7 @@ int chol_dag_launch(double* A, int64_t ld, int nt, double* rhs, double* x, doubl
   a.status = status;
   a.trace = trace;
   const int g = ntasks < grid ? ntasks : grid;
-  k_chol_dag<<<g, CHOL_THREADS, DAG_SMEM, st>>>(a);
+  launch_coresident(k_chol_dag, g, CHOL_THREADS, DAG_SMEM, st, a);
   launch_count();
   return 0;
 }
@@ -2290,7 +2311,7 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
   a.status = status;
   a.trace = trace;
   if (ev3) cudaEventRecord(ev3[0], st);
-  k_chol_tc<<<ntasks < grid ? ntasks : grid, CHOL_THREADS, TC_SMEM, st>>>(a);
+  launch_coresident(k_chol_tc, ntasks < grid ? ntasks : grid, CHOL_THREADS, TC_SMEM, st, a);
   launch_count();
   launch_count();
   launch_count();
@@ -2314,9 +2335,11 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
     // one chain CTA per block row, plus a sweep helper per block row when 2 nt CTAs
     // fit on the GPU at once (all CTAs of these kernels must be co-resident)
     const int hlp = 2 * nt <= sms ? 1 : 0;
-    k_tc_fwd<<<nt * (1 + hlp), 256, TRI_SMEM, st>>>(W, Fm, nt, rhs, D, y, Vs, gen + 2 * it, stop, hlp);
-    k_tc_bwd<<<nt * (1 + hlp), 256, TRI_SMEM, st>>>(W, Fm, nt, y, z, Us, D, x, out2, out2 + 1, gen + 2 * it,
-                                                    stop, hlp);
+    launch_coresident(k_tc_fwd, nt * (1 + hlp), 256, TRI_SMEM, st, (const float*)W, (const float*)Fm, nt, rhs,
+                      (const double*)D, y, Vs, gen + 2 * it, (const int*)stop, hlp);
+    launch_coresident(k_tc_bwd, nt * (1 + hlp), 256, TRI_SMEM, st, (const float*)W, (const float*)Fm, nt,
+                      (const unsigned long long*)y, z, Us, (const double*)D, x, out2, out2 + 1, gen + 2 * it,
+                      (const int*)stop, hlp);
     // stop once a pass corrects x by <= kTcRefineTol max|x| (vba_internal.cuh)
     k_tc_check<<<1, 1, 0, st>>>(out2, stop, kTcRefineTol, kTcErrTol, it == iters - 1);
     launch_count();
