@@ -1330,12 +1330,34 @@ __global__ void k_fill_transform(const int32_t* __restrict__ srcs, const int32_t
   if (k > 31) {   // one pixel range (its unit slices share the record): read it in place
     C = part + gt[g0[s]].out;
   } else {
+    // four elements per thread per pass, their loads issued together (one element at a time
+    // left one dependent global load in flight per thread: the staging dominated the kernel)
     const int len = npairs * 36 + 6 * k, t0 = g0[s], t1 = g1[s];
     const double* p0 = part + gt[t0].out;
-    for (int i = threadIdx.x; i < len; i += blockDim.x) {
-      double acc = p0[i];
-      for (int t = t0 + 1; t < t1; ++t) acc += part[gt[t].out + i];
-      Cs[i] = acc;
+    const int nth4 = 4 * blockDim.x;
+    for (int i0 = threadIdx.x; i0 < len; i0 += nth4) {
+      double acc[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * blockDim.x;
+        acc[u] = i < len ? p0[i] : 0.0;
+      }
+      for (int t = t0 + 1; t < t1; ++t) {
+        const double* pt = part + gt[t].out;
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u * blockDim.x;
+          v[u] = i < len ? pt[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] += v[u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * blockDim.x;
+        if (i < len) Cs[i] = acc[u];
+      }
     }
   }
   const double* b = C + npairs * 36;
