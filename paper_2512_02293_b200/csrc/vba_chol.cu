@@ -1674,6 +1674,27 @@ __global__ void __launch_bounds__(256) k_tc_convert(const double* __restrict__ H
   const int j = (int)(id - (int64_t)i * (i + 1) / 2);
   float* Wt = W + id * TILE_F;
   const int tid = threadIdx.x;
+  if (i != j && CT * (i + 1) <= n) {
+    // interior off-diagonal tile (all of it in the stored lower triangle): 16-B loads of row
+    // pairs, a warp reads 512 contiguous bytes of a column; 16 loads in flight per thread
+    const double dr0 = D[CT * i + 2 * (tid & 63)], dr1 = D[CT * i + 2 * (tid & 63) + 1];
+#pragma unroll 1
+    for (int half = 0; half < 2; ++half) {
+      double2 v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int idx = tid + 256 * (q + 16 * half), c = idx >> 6, rp = idx & 63;
+        v[q] = __ldcs(reinterpret_cast<const double2*>(H + (int64_t)(CT * j + c) * ld + CT * i + 2 * rp));
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int idx = tid + 256 * (q + 16 * half), c = idx >> 6, rp = idx & 63;
+        const double dc = D[CT * j + c];
+        ttile[(2 * rp) * (CT + 1) + c] = (float)(dr0 * v[q].x * dc);
+        ttile[(2 * rp + 1) * (CT + 1) + c] = (float)(dr1 * v[q].y * dc);
+      }
+    }
+  } else {
 #pragma unroll 1
   for (int half = 0; half < 2; ++half) {
     float v[32];
@@ -1694,11 +1715,13 @@ __global__ void __launch_bounds__(256) k_tc_convert(const double* __restrict__ H
       ttile[r * (CT + 1) + c] = v[q];
     }
   }
+  }
   __syncthreads();
 #pragma unroll 4
-  for (int q = 0; q < 64; ++q) {
-    const int idx = tid + 256 * q, r = idx >> 7, c = idx & 127;
-    Wt[r * CT + c] = ttile[r * (CT + 1) + c];
+  for (int q = 0; q < 16; ++q) {   // 16-B stores, a warp writes one 512-B row
+    const int idx = tid + 256 * q, r = idx >> 5, c = 4 * (idx & 31);
+    const float* t = ttile + r * (CT + 1) + c;
+    *reinterpret_cast<float4*>(Wt + r * CT + c) = make_float4(t[0], t[1], t[2], t[3]);
   }
 }
 
