@@ -2161,61 +2161,61 @@ constexpr int SYB = 64;
 __global__ void __launch_bounds__(256) k_tc_symv(const double* __restrict__ H, int64_t ld, int n, int nb,
                                                  const double* __restrict__ x, double* __restrict__ P,
                                                  const int* __restrict__ stop) {
-  __shared__ double Ts[SYB][SYB + 1];   // Ts[c][r] = H(64 i + r, 64 j + c)
+  // Warp w holds columns w, w+8, .., w+56 of the block, lane l rows 2l, 2l+1 (16-B loads, a
+  // warp reads one 512-B column).  Column sums (H^T x_i) are warp reductions; row sums
+  // (H x_j) are per-lane partials over the warp's 8 columns, summed over the 8 warps through
+  // shared memory -- no transpose of the block.  Diagonal blocks (lower half stored): rows
+  // use c <= r, columns r > c, so the two sums together are the symmetric product.
   __shared__ double xi[SYB], xj[SYB];
-  __shared__ double red[2][4][SYB];
+  __shared__ double rowp[8][SYB], colv[SYB];
   if (*stop) return;
   const int64_t id = blockIdx.x;
   int i = (int)((sqrt(8.0 * (double)id + 1.0) - 1.0) * 0.5);
   while ((int64_t)(i + 1) * (i + 2) / 2 <= id) ++i;
   while ((int64_t)i * (i + 1) / 2 > id) --i;
   const int j = (int)(id - (int64_t)i * (i + 1) / 2);
-  const int tid = threadIdx.x;
-  // 16-B loads, a warp reads 512 contiguous bytes (one column); all loads before the stores
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
   double2 v[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    const int t2 = tid + 256 * q, c = t2 >> 5, r2 = t2 & 31;
-    v[q] = __ldcg(reinterpret_cast<const double2*>(H + (int64_t)(SYB * j + c) * ld + SYB * i) + r2);
+    const int c = w + 8 * q;
+    v[q] = __ldcg(reinterpret_cast<const double2*>(H + (int64_t)(SYB * j + c) * ld + SYB * i) + l);
   }
   if (tid < SYB) {
     const int R = SYB * i + tid, C = SYB * j + tid;
     xi[tid] = R < n ? x[R] : 0.0;
     xj[tid] = C < n ? x[C] : 0.0;
   }
+  __syncthreads();
+  const int r0 = 2 * l, r1 = 2 * l + 1;
+  const bool rin0 = SYB * i + r0 < n, rin1 = SYB * i + r1 < n;
+  const bool diag = i == j;
+  double rs0 = 0.0, rs1 = 0.0;
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    const int t2 = tid + 256 * q, c = t2 >> 5, r = 2 * (t2 & 31);
+    const int c = w + 8 * q;
     const bool cin = SYB * j + c < n;
-    Ts[c][r] = (cin && SYB * i + r < n) ? v[q].x : 0.0;
-    Ts[c][r + 1] = (cin && SYB * i + r + 1 < n) ? v[q].y : 0.0;
-  }
-  __syncthreads();
-  const int l = tid & (SYB - 1), qq = tid >> 6;   // 4 quarters of 16
-  {   // rows of block i: sum_c H(r, c) x_j[c], c in quarter qq
-    const int r = l;
-    double s = 0.0;
+    const double h0 = (cin && rin0) ? v[q].x : 0.0, h1 = (cin && rin1) ? v[q].y : 0.0;
+    // rows of block i: H(r, c) x_j[c] (diagonal block: c <= r)
+    rs0 = fma((!diag || c <= r0) ? h0 : 0.0, xj[c], rs0);
+    rs1 = fma((!diag || c <= r1) ? h1 : 0.0, xj[c], rs1);
+    // rows of block j (column c): sum_r H(r, c) x_i[r] (diagonal block: r > c)
+    double cs = fma((!diag || r0 > c) ? h0 : 0.0, xi[r0], ((!diag || r1 > c) ? h1 : 0.0) * xi[r1]);
 #pragma unroll
-    for (int cc = 0; cc < 16; ++cc) {
-      const int c = 16 * qq + cc;
-      const double hv = (i != j || c <= r) ? Ts[c][r] : Ts[r][c];
-      s = fma(hv, xj[c], s);
-    }
-    red[0][qq][r] = s;
+    for (int o = 16; o >= 1; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
+    if (l == 0) colv[c] = cs;
   }
-  if (i != j) {   // rows of block j: sum_r H(r, c) x_i[r], r in quarter qq
-    const int c = l;
-    double s = 0.0;
-#pragma unroll
-    for (int rr = 0; rr < 16; ++rr) s = fma(Ts[c][16 * qq + rr], xi[16 * qq + rr], s);
-    red[1][qq][c] = s;
-  }
+  rowp[w][r0] = rs0;
+  rowp[w][r1] = rs1;
   __syncthreads();
   if (tid < SYB) {
-    P[((int64_t)i * nb + j) * SYB + tid] = ((red[0][0][tid] + red[0][1][tid]) + red[0][2][tid]) + red[0][3][tid];
-  } else if (tid < 2 * SYB && i != j) {
-    const int c = tid - SYB;
-    P[((int64_t)j * nb + i) * SYB + c] = ((red[1][0][c] + red[1][1][c]) + red[1][2][c]) + red[1][3][c];
+    double s = rowp[0][tid];
+#pragma unroll
+    for (int u = 1; u < 8; ++u) s += rowp[u][tid];
+    if (diag) s += colv[tid];
+    P[((int64_t)i * nb + j) * SYB + tid] = s;
+  } else if (tid < 2 * SYB && !diag) {
+    P[((int64_t)j * nb + i) * SYB + (tid - SYB)] = colv[tid - SYB];
   }
 }
 
