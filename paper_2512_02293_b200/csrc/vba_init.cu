@@ -90,8 +90,6 @@ __global__ void __launch_bounds__(256) k_init2_solve(const double* __restrict__ 
   double* A = dim <= kInit2SmemDim ? A_s : Ag;
   double* b = dim <= kInit2SmemDim ? A_s + dim * dim : dx;
   __shared__ int piv;
-  __shared__ double wval[8];
-  __shared__ int widx[8];
   for (int t = tid; t < dim * dim; t += nth) {
     const int r = t / dim, c = t % dim;
     double v = H[t];
@@ -101,33 +99,31 @@ __global__ void __launch_bounds__(256) k_init2_solve(const double* __restrict__ 
   for (int r = tid; r < dim; r += nth) b[r] = -g[r];
   if (tid == 0) *status = 0;
   __syncthreads();
+  const int nw = nth / 32;
   for (int k = 0; k < dim; ++k) {
-    // pivot: first maximum of |A[r][k]|, r >= k (idamax), by a warp tree then the warp maxima
-    double best = -1.0;
-    int bi = dim;
-    for (int r = k + tid; r < dim; r += nth) {
-      const double v = fabs(A[r * dim + k]);
-      if (v > best) { best = v; bi = r; }
-    }
+    // pivot: first maximum of |A[r][k]|, r >= k (idamax), by warp 0 alone (dim <= a few
+    // hundred: a lane-strided scan and one warp tree, no cross-warp stage)
+    if (warp == 0) {
+      double best = -1.0;
+      int bi = dim;
+      for (int r = k + lane; r < dim; r += 32) {
+        const double v = fabs(A[r * dim + k]);
+        if (v > best) { best = v; bi = r; }
+      }
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-    }
-    if (lane == 0) { wval[warp] = best; widx[warp] = bi; }
-    __syncthreads();
-    if (tid == 0) {
-      double bv = -1.0;
-      int br = dim;
-      for (int w = 0; w < nth / 32; ++w)
-        if (wval[w] > bv || (wval[w] == bv && widx[w] < br)) { bv = wval[w]; br = widx[w]; }
-      piv = br;
-      if (!(bv > 0.0)) *status = 1;
+      for (int o = 16; o >= 1; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+      }
+      if (lane == 0) piv = best > 0.0 ? bi : -1;   // exactly zero column: numpy's LinAlgError
     }
     __syncthreads();
-    if (*status) return;
-    const int p = piv;
+    const int p = piv;   // (shared: a global status read here cost a memory round trip per column)
+    if (p < 0) {
+      if (tid == 0) *status = 1;
+      return;
+    }
     if (p != k) {
       for (int c = tid; c < dim; c += nth) {
         const double t = A[k * dim + c];
@@ -141,17 +137,18 @@ __global__ void __launch_bounds__(256) k_init2_solve(const double* __restrict__ 
       }
       __syncthreads();
     }
-    // multipliers, then the rank-1 update element-parallel (each element: one fma per k,
-    // in k order -- the same arithmetic as the row-serial form)
+    // multiplier and rank-1 update of row r by one warp (lanes over columns): each element
+    // one fma per k, in k order -- the same arithmetic as the row-serial form
     const double inv = 1.0 / A[k * dim + k];
-    const int m = dim - k - 1;
-    for (int r = k + 1 + tid; r < dim; r += nth) A[r * dim + k] *= inv;
-    __syncthreads();
-    for (int t = tid; t < m * m; t += nth) {
-      const int r = k + 1 + t / m, c = k + 1 + t % m;
-      A[r * dim + c] -= A[r * dim + k] * A[k * dim + c];
+    for (int r = k + 1 + warp; r < dim; r += nw) {
+      const double l = A[r * dim + k] * inv;
+      for (int c = k + 1 + lane; c < dim; c += 32) A[r * dim + c] -= l * A[k * dim + c];
+      __syncwarp();   // every lane has read A[r][k]
+      if (lane == 0) {
+        A[r * dim + k] = l;
+        b[r] -= l * b[k];
+      }
     }
-    for (int r = k + 1 + tid; r < dim; r += nth) b[r] -= A[r * dim + k] * b[k];
     __syncthreads();
   }
   // back substitution: warp 0, row dot products as warp trees (fixed order)
