@@ -214,6 +214,17 @@ int vba_init_inertial(const vba_init_problem* P, const vba_init_options* O, void
   for (size_t z : sizes) need += (z + 255) / 256 * 256;
   char* arena = nullptr;
   size_t used = 0;
+  {   // keep the default pool's freed blocks cached (release threshold 0 hands them back to the
+      // driver at every synchronisation, and the next call's allocation re-maps them)
+    static bool kept = false;
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (!kept && cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~(uint64_t)0;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      kept = true;
+    }
+  }
   if (cudaMallocAsync((void**)&arena, need, st) != cudaSuccess) arena = nullptr;
   auto alloc = [&](void** p, size_t bytes) {
     if (!arena) return false;
