@@ -719,22 +719,23 @@ void chol_task_fields(const void* tasks, int n, int* out4) {
 namespace vba {
 
 // ===========================================================================
-// Mixed-precision SPD solve on the 5th-gen tensor cores (tcgen05, kind::tf32).
+// Mixed-precision SPD solve on the 5th-gen tensor cores (tcgen05, kind::f16).
 //
-// Same task DAG as k_chol_dag (POTRF / TRSM / GEMM, lookahead 1, static update
-// pairing), run on a Jacobi-scaled fp32 copy of the lower triangle:
+// A tile DAG on a Jacobi-scaled fp32 copy of the lower triangle:
 //   As = D H D,  D = diag(H)^-1/2      (the scaling makes cond(As) ~1e4 here)
-// GEMM-shaped tasks use 3xTF32 splitting (a = hi + lo, hi/lo rounded to tf32,
-// A B^T ~ Ah Bh^T + Ah Bl^T + Al Bh^T, fp32 accumulation in TMEM), so the
-// factor has ~fp32 accuracy at tensor-core speed.  The fp64 answer of
-// np.linalg.solve (solver.py:287) is then recovered by iterative refinement
+// one chain task (POTRF -> TRSM -> SYRK of every step, one CTA) and left-looking tile
+// tasks (each off-chain tile accumulates all its updates in TMEM and is written once,
+// then its TRSM follows), claimed in list order by persistent co-resident CTAs.  Tile
+// products split every fp32 operand into fp16 hi + lo (A B^T ~ Ah Bh^T + Ah Bl^T + Al Bh^T,
+// fp32 accumulation in TMEM), so the factor has ~fp32 accuracy at tensor-core speed.  The
+// fp64 answer of np.linalg.solve (solver.py:287) is then recovered by iterative refinement
 // against the fp64 H:  x += D (L L^T)^-1 D (b - H x)   (fp64 residuals).
 //
 // Tile storage (nt x nt lower tiles, linear index i(i+1)/2 + j):
 //   W    fp32 row-major 128x128: working tile; after the factorisation
 //        L_ij (i > j) and L_kk^-1 (diagonal) for the triangular solves
-//   IMG  per tile two operand images (hi, lo) in the UMMA canonical K-major
-//        SWIZZLE_128B layout: 4 K-chunks of 32 fp32 x 128 rows (16 KB each),
+//   IMG  per tile two operand images (fp16 hi, lo) in the UMMA canonical K-major
+//        SWIZZLE_128B layout: 2 K-chunks of 64 fp16 x 128 rows (16 KB each),
 //        8-row atoms of 1 KB, 16-byte units XOR-swizzled by (row mod 8); a
 //        chunk is one contiguous cp.async.bulk into shared memory.
 // ===========================================================================
@@ -1119,8 +1120,6 @@ __device__ void tc_task_tile(const TcArgs& a, TcRing& R, uint64_t* accf, uint32_
   }
 }
 
-// Diagonal SYRK of DIAG(k): W_{k+1,k+1} -= L L^T with L = L_{k+1,k} already in shared
-// memory as chunk images (tc_task_trsm keep_smem): A and B descriptors share them.
 // TRSM(k+1,k) of the chain: B = Linv_kk images already in shared memory at 2 ch TCHUNK
 // (POTRF's output), A = W_{k+1,k}'s hi/lo images, written by its TILE_OPERAND task, bulk
 // copied to TC_ABUF_OFF -- while POTRF(k) runs when the operand is ready by then.
