@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 
 #include "vba_internal.cuh"
@@ -312,6 +313,284 @@ __global__ void __launch_bounds__(16 * kPairsPerBlock) k_preint_propagate(const 
   }
 }
 
+// Phase 2, log-depth variant (default): the recursion of a pair is an affine map of the
+// state (dp, dv, cov9, bias Jacobians) once the rotation before each step is known, and such
+// maps compose associatively.  One warp per pair: lane L takes a contiguous chunk of steps;
+//   1. rotation: each lane multiplies its chunk's Exp(w dt) factors, a warp scan of 3x3
+//      products (shuffles) gives every chunk its starting dR;
+//   2. each lane composes its chunk's steps into one aggregate map (below) from the true dR;
+//   3. a 5-level tree combines the 32 aggregates in chunk order; lane 0 writes the record.
+// Aggregate (per lane, in shared memory, element e of lane L at e * 32 + L):
+//   cov:  Phi = [[R,0,0],[X,I,T I],[Y,0,I]] (error-state transition), C (accumulated noise):
+//         (Phi2, C2) o (Phi1, C1) = (Phi2 Phi1, Phi2 C1 Phi2^T + C2)
+//   bias Jacobians (gyro, state [J_rot; J_vel; J_pos]): M = [[R,0,0],[JX,I,0],[JY,T I,I]] and
+//         offsets O = [OR; OV; OP]:  (M2, O2) o (M1, O1) = (M2 M1, M2 O1 + O2)
+//   dp/dv and the accel Jacobians: dv = dv0 + V, dp = dp0 + T dv0 + P (and J_vel/J_pos accel
+//         columns alike with VA, PA).
+// A step is the aggregate of one interval (R = Ef^T, X = -dt^2/2 RAE, Y = -dt RAE, C = B Qd B^T,
+// ...), combined onto the running one, so the step update and the tree share one function.
+// fp64 throughout; the reassociation moves results by ~1e-16 relative (parity tests: 1e-12).
+namespace {
+constexpr int kAR = 0, kAX = 9, kAY = 18, kAT = 27, kAC = 28, kJX = 109, kJY = 118, kOR = 127, kOV = 136,
+              kOP = 145, kAP = 154, kAV = 157, kPA = 160, kVA = 169, kAggN = 178;
+struct AggRef {   // one lane's aggregate in shared memory
+  double* b;
+  __device__ double& operator[](int e) const { return b[e * 32]; }
+};
+// 3x3 helpers on strided aggregate storage (row-major 3x3 at element offset e)
+__device__ __forceinline__ void m3_load(const AggRef& a, int e, double* m) {
+  for (int i = 0; i < 9; ++i) m[i] = a[e + i];
+}
+__device__ __forceinline__ void m3_store(const AggRef& a, int e, const double* m) {
+  for (int i = 0; i < 9; ++i) a[e + i] = m[i];
+}
+__device__ __forceinline__ void mm3(const double* A, const double* B, double* C) {   // C = A B
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) C[3 * r + c] = A[3 * r] * B[c] + A[3 * r + 1] * B[3 + c] + A[3 * r + 2] * B[6 + c];
+}
+__device__ __forceinline__ void mm3T(const double* A, const double* B, double* C) {   // C = A B^T
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c)
+      C[3 * r + c] = A[3 * r] * B[3 * c] + A[3 * r + 1] * B[3 * c + 1] + A[3 * r + 2] * B[3 * c + 2];
+}
+// e1 (earlier, in/out) := e2 (later) o e1
+__device__ void agg_combine(const AggRef& e2, const AggRef& e1) {
+  double R1[9], R2[9], X1[9], X2[9], Y1[9], Y2[9], t[9], u[9];
+  const double T1 = e1[kAT], T2 = e2[kAT];
+  m3_load(e1, kAR, R1); m3_load(e2, kAR, R2);
+  m3_load(e2, kAX, X2); m3_load(e2, kAY, Y2);
+  // covariance: C = Phi2 C1 Phi2^T + C2 by 3x3 blocks, B = Phi2 C1 first
+  double B[3][3][9];
+  {
+    double Cb[3][9];
+    for (int j = 0; j < 3; ++j) {
+      for (int bi = 0; bi < 3; ++bi)
+        for (int r = 0; r < 3; ++r)
+          for (int c = 0; c < 3; ++c) Cb[bi][3 * r + c] = e1[kAC + 9 * (3 * bi + r) + 3 * j + c];
+      // column block j of C1: Cb[bi] = C1_{bi, j}
+      mm3(R2, Cb[0], B[0][j]);
+      mm3(X2, Cb[0], t);
+      mm3(Y2, Cb[0], u);
+      for (int q = 0; q < 9; ++q) {
+        B[1][j][q] = t[q] + Cb[1][q] + T2 * Cb[2][q];
+        B[2][j][q] = u[q] + Cb[2][q];
+      }
+    }
+  }
+  for (int i = 0; i < 3; ++i) {   // row block i of B Phi2^T:  [B_i0 R2^T, B_i0 X2^T + B_i1 + T2 B_i2, B_i0 Y2^T + B_i2]
+    double D0[9], D1[9], D2[9];
+    mm3T(B[i][0], R2, D0);
+    mm3T(B[i][0], X2, D1);
+    mm3T(B[i][0], Y2, D2);
+    for (int q = 0; q < 9; ++q) {
+      D1[q] += B[i][1][q] + T2 * B[i][2][q];
+      D2[q] += B[i][2][q];
+    }
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) {
+        const int row = 9 * (3 * i + r);
+        e1[kAC + row + c] = D0[3 * r + c] + e2[kAC + row + c];
+        e1[kAC + row + 3 + c] = D1[3 * r + c] + e2[kAC + row + 3 + c];
+        e1[kAC + row + 6 + c] = D2[3 * r + c] + e2[kAC + row + 6 + c];
+      }
+  }
+  // symmetrise (imu.py:139: the sequential recursion does it every step)
+  for (int r = 0; r < 9; ++r)
+    for (int c = r + 1; c < 9; ++c) {
+      const double v = 0.5 * (e1[kAC + 9 * r + c] + e1[kAC + 9 * c + r]);
+      e1[kAC + 9 * r + c] = v;
+      e1[kAC + 9 * c + r] = v;
+    }
+  // covariance transition: X = X2 R1 + X1 + T2 Y1, Y = Y2 R1 + Y1
+  m3_load(e1, kAX, X1); m3_load(e1, kAY, Y1);
+  mm3(X2, R1, t);
+  for (int q = 0; q < 9; ++q) t[q] += X1[q] + T2 * Y1[q];
+  m3_store(e1, kAX, t);
+  mm3(Y2, R1, t);
+  for (int q = 0; q < 9; ++q) t[q] += Y1[q];
+  m3_store(e1, kAY, t);
+  // Jacobian maps: offsets first (they read the earlier JX1 .. through O1 only)
+  double OR1[9], OV1[9], OP1[9], JX2[9], JY2[9];
+  m3_load(e1, kOR, OR1); m3_load(e1, kOV, OV1); m3_load(e1, kOP, OP1);
+  m3_load(e2, kJX, JX2); m3_load(e2, kJY, JY2);
+  mm3(R2, OR1, t);
+  for (int q = 0; q < 9; ++q) t[q] += e2[kOR + q];
+  m3_store(e1, kOR, t);
+  mm3(JX2, OR1, t);
+  for (int q = 0; q < 9; ++q) t[q] += OV1[q] + e2[kOV + q];
+  m3_store(e1, kOV, t);
+  mm3(JY2, OR1, t);
+  for (int q = 0; q < 9; ++q) t[q] += T2 * OV1[q] + OP1[q] + e2[kOP + q];
+  m3_store(e1, kOP, t);
+  // M = M2 M1: JX = JX2 R1 + JX1, JY = JY2 R1 + T2 JX1 + JY1
+  double JX1[9], JY1[9];
+  m3_load(e1, kJX, JX1); m3_load(e1, kJY, JY1);
+  mm3(JX2, R1, t);
+  for (int q = 0; q < 9; ++q) t[q] += JX1[q];
+  m3_store(e1, kJX, t);
+  mm3(JY2, R1, t);
+  for (int q = 0; q < 9; ++q) t[q] += T2 * JX1[q] + JY1[q];
+  m3_store(e1, kJY, t);
+  // dp/dv and the accel Jacobians
+  for (int q = 0; q < 3; ++q) {
+    const double v1 = e1[kAV + q];
+    e1[kAP + q] = e1[kAP + q] + e2[kAP + q] + T2 * v1;
+    e1[kAV + q] = v1 + e2[kAV + q];
+  }
+  for (int q = 0; q < 9; ++q) {
+    const double v1 = e1[kVA + q];
+    e1[kPA + q] = e1[kPA + q] + e2[kPA + q] + T2 * v1;
+    e1[kVA + q] = v1 + e2[kVA + q];
+  }
+  mm3(R2, R1, t);
+  m3_store(e1, kAR, t);
+  e1[kAT] = T1 + T2;
+}
+__device__ void agg_identity(const AggRef& a) {
+  for (int e = 0; e < kAggN; ++e) a[e] = 0.0;
+  a[kAR] = a[kAR + 4] = a[kAR + 8] = 1.0;
+}
+}  // namespace
+
+constexpr int kScanWarps = 2;   // pairs per CTA
+__global__ void __launch_bounds__(32 * kScanWarps) k_preint_scan(const double* __restrict__ ts,
+                                                                 const int64_t* __restrict__ soff, int F,
+                                                                 int64_t n_samples,
+                                                                 const double* __restrict__ steps,
+                                                                 const double* __restrict__ noise,
+                                                                 double* __restrict__ out, int* __restrict__ status) {
+  extern __shared__ double scan_sm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int f = blockIdx.x * kScanWarps + w;
+  if (f >= F) return;
+  double* base = scan_sm + (size_t)w * 2 * kAggN * 32;
+  const AggRef run{base + lane}, stp{base + kAggN * 32 + lane};
+  const int64_t s0 = soff[f], S = soff[f + 1] - s0;
+  if (s0 < 0 || soff[f + 1] > n_samples || soff[f + 1] < s0) { if (lane == 0) atomicOr(status, 4); return; }
+  if (S < 2) { if (lane == 0) atomicOr(status, 1); return; }
+  const int64_t n = S - 1, ch = (n + 31) / 32, k0 = lane * ch, k1 = k0 + ch < n ? k0 + ch : n;
+  const double* st = steps + kStepRec * s0;
+  // 1. rotation prefix: Pr = product of this chunk's Ef, then an inclusive warp scan
+  double Pr[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, t[9];
+  for (int64_t k = k0; k < k1; ++k) {
+    mm3(Pr, st + kStepRec * k + 4, t);
+    for (int q = 0; q < 9; ++q) Pr[q] = t[q];
+  }
+  for (int d = 1; d < 32; d <<= 1) {
+    double o[9];
+    for (int q = 0; q < 9; ++q) o[q] = __shfl_up_sync(0xffffffffu, Pr[q], d);
+    if (lane >= d) {
+      mm3(o, Pr, t);
+      for (int q = 0; q < 9; ++q) Pr[q] = t[q];
+    }
+  }
+  double dR[9];   // rotation before this chunk (exclusive scan)
+  for (int q = 0; q < 9; ++q) {
+    const double v = __shfl_up_sync(0xffffffffu, Pr[q], 1);
+    dR[q] = lane == 0 ? (q % 4 == 0 ? 1.0 : 0.0) : v;
+  }
+  double dRtot[9];
+  for (int q = 0; q < 9; ++q) dRtot[q] = __shfl_sync(0xffffffffu, Pr[q], 31);
+  // 2. this chunk's aggregate
+  agg_identity(run);
+  for (int64_t k = k0; k < k1; ++k) {
+    const double* r = st + kStepRec * k;
+    const double dt = r[0];
+    const double* Ef = r + 4;
+    const double* Eh = r + 13;
+    const double* Jf = r + 22;
+    const double* Jh = r + 31;
+    double Rm[9], RAE[9], RJ[9], E[9];
+    mm3(dR, Eh, Rm);
+    mm3(dR, r + 40, RAE);
+    mm3(dR, r + 49, RJ);
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) E[3 * i + j] = Ef[3 * j + i];
+    m3_store(stp, kAR, E);
+    for (int q = 0; q < 9; ++q) {
+      stp[kAX + q] = -0.5 * dt * dt * RAE[q];
+      stp[kAY + q] = -dt * RAE[q];
+    }
+    stp[kAT] = dt;
+    // B Qd B^T: row c = (block br, row rr); gyro rows s_b G_b, accel rows t_b Rm (imu.py:130-138)
+    const double qg = r[58], qa = r[59];
+    const double s1 = 0.25 * dt * dt * dt, s2 = 0.5 * dt * dt, t1 = -0.5 * dt * dt, t2 = -dt;
+    for (int c = 0; c < 9; ++c) {
+      const int br = c / 3, rr = c % 3;
+      const double sr = br == 0 ? -dt : (br == 1 ? s1 : s2), tr = br == 0 ? 0.0 : (br == 1 ? t1 : t2);
+      const double* gp = br == 0 ? Jf : RJ;
+      const double g0 = sr * gp[3 * rr], g1 = sr * gp[3 * rr + 1], g2 = sr * gp[3 * rr + 2];
+      const double a0 = tr * Rm[3 * rr], a1 = tr * Rm[3 * rr + 1], a2 = tr * Rm[3 * rr + 2];
+      for (int j = 0; j < 9; ++j) {
+        const int bj = j / 3, rj = j % 3;
+        const double sj = bj == 0 ? -dt : (bj == 1 ? s1 : s2), tj = bj == 0 ? 0.0 : (bj == 1 ? t1 : t2);
+        const double* gq = bj == 0 ? Jf : RJ;
+        const double gg = g0 * (sj * gq[3 * rj]) + g1 * (sj * gq[3 * rj + 1]) + g2 * (sj * gq[3 * rj + 2]);
+        const double aa = a0 * (tj * Rm[3 * rj]) + a1 * (tj * Rm[3 * rj + 1]) + a2 * (tj * Rm[3 * rj + 2]);
+        stp[kAC + 9 * c + j] = qg * gg + qa * aa;
+      }
+    }
+    // Jacobian step map: G = Rm [a]x Eh^T, h = Rm [a]x Jh (imu.py:120, 142-146)
+    const double a[3] = {r[1], r[2], r[3]};
+    double AxEt[9], Axh[9], G[9], h[9];
+    for (int c = 0; c < 3; ++c) {   // column c of [a]x Eh^T and [a]x Jh
+      const double e0 = Eh[3 * c], e1 = Eh[3 * c + 1], e2 = Eh[3 * c + 2];   // (Eh^T)[:, c] = row c of Eh
+      AxEt[c] = a[1] * e2 - a[2] * e1; AxEt[3 + c] = a[2] * e0 - a[0] * e2; AxEt[6 + c] = a[0] * e1 - a[1] * e0;
+      const double j0 = Jh[c], j1 = Jh[3 + c], j2 = Jh[6 + c];
+      Axh[c] = a[1] * j2 - a[2] * j1; Axh[3 + c] = a[2] * j0 - a[0] * j2; Axh[6 + c] = a[0] * j1 - a[1] * j0;
+    }
+    mm3(Rm, AxEt, G);
+    mm3(Rm, Axh, h);
+    for (int q = 0; q < 9; ++q) {
+      stp[kJX + q] = -dt * G[q];
+      stp[kJY + q] = -0.5 * dt * dt * G[q];
+      stp[kOR + q] = -dt * Jf[q];
+      stp[kOV + q] = 0.5 * dt * dt * h[q];
+      stp[kOP + q] = 0.25 * dt * dt * dt * h[q];
+      stp[kPA + q] = -0.5 * dt * dt * Rm[q];
+      stp[kVA + q] = -dt * Rm[q];
+    }
+    for (int i = 0; i < 3; ++i) {
+      const double ai = Rm[3 * i] * a[0] + Rm[3 * i + 1] * a[1] + Rm[3 * i + 2] * a[2];
+      stp[kAP + i] = 0.5 * dt * dt * ai;
+      stp[kAV + i] = dt * ai;
+    }
+    agg_combine(stp, run);
+    mm3(dR, Ef, t);
+    for (int q = 0; q < 9; ++q) dR[q] = t[q];
+  }
+  // 3. ordered tree over the chunks
+  for (int d = 1; d < 32; d <<= 1) {
+    __syncwarp();
+    if ((lane & (2 * d - 1)) == 0 && lane + d < 32) agg_combine(AggRef{base + lane + d}, run);
+  }
+  __syncwarp();
+  if (lane != 0) return;
+  double* o = out + (int64_t)kPreintRec * f;
+  const double dtt = ts[s0 + S - 1] - ts[s0];
+  o[0] = dtt;
+  M3 R;
+  for (int q = 0; q < 9; ++q) R.m[q] = dRtot[q];
+  quat_from_matrix(R, o + 1);
+  for (int i = 0; i < 3; ++i) { o[5 + i] = run[kAP + i]; o[8 + i] = run[kAV + i]; }
+  for (int i = 0; i < 3; ++i)
+    for (int c = 0; c < 3; ++c) {
+      o[11 + 3 * i + c] = run[kOR + 3 * i + c];
+      o[20 + 6 * i + c] = run[kOP + 3 * i + c];
+      o[20 + 6 * i + 3 + c] = run[kPA + 3 * i + c];
+      o[38 + 6 * i + c] = run[kOV + 3 * i + c];
+      o[38 + 6 * i + 3 + c] = run[kVA + 3 * i + c];
+    }
+  double* cv = o + 56;
+  for (int r = 0; r < 15; ++r)
+    for (int c = 0; c < 15; ++c) {
+      double v = 0.0;
+      if (r < 9 && c < 9) v = run[kAC + 9 * r + c];
+      else if (r == c) v = (c < 12 ? noise[2] * noise[2] : noise[3] * noise[3]) * dtt;   // imu.py:152-156
+      cv[15 * r + c] = v;
+    }
+}
+
 // Preintegration record -> IMU factor record of the solver (include/vba.h VBA_IMU_REC):
 // the first 56 doubles are shared, then cov[0:9,0:9], cov[9:15,9:15], the bias
 // linearisation point.  One thread per output double.
@@ -347,8 +626,24 @@ void launch_preintegrate(const double* ts, const double* gyro, const double* acc
                                                                 status);
     launch_count();
   }
-  k_preint_propagate<<<(F + kPairsPerBlock - 1) / kPairsPerBlock, 16 * kPairsPerBlock, 0, st>>>(
-      ts, soff, F, S, scratch, noise, out, status);
+  // the log-depth scan wins from ~64 intervals per pair (256 x 200: 0.14 vs 0.30 ms); with
+  // short pairs the 32-chunk tree costs more than the sequential steps it replaces (1024 x 40:
+  // 0.22 vs 0.11 ms).  VBA_PREINT=seq / scan forces either.
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_preint_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(double) * 2 * kAggN * 32 * kScanWarps));
+    attr = true;
+  }
+  const char* e = getenv("VBA_PREINT");   // read per call (tests switch it)
+  const int force = !e ? -1 : (e[0] == 's' && e[1] == 'e') ? 1 : (e[0] == 's' && e[1] == 'c') ? 0 : -1;
+  const bool seq = force >= 0 ? force == 1 : S < (int64_t)64 * F;
+  if (seq)
+    k_preint_propagate<<<(F + kPairsPerBlock - 1) / kPairsPerBlock, 16 * kPairsPerBlock, 0, st>>>(
+        ts, soff, F, S, scratch, noise, out, status);
+  else
+    k_preint_scan<<<(F + kScanWarps - 1) / kScanWarps, 32 * kScanWarps,
+                    sizeof(double) * 2 * kAggN * 32 * kScanWarps, st>>>(ts, soff, F, S, scratch, noise, out, status);
   launch_count();
 }
 

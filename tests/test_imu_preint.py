@@ -43,8 +43,13 @@ def test_oracle_rejects_like_reference():
 
 
 @pytest.mark.gpu
-def test_device_preintegration_matches_reference(cuda_ok):
+@pytest.mark.parametrize("mode", ["seq", "scan"])
+def test_device_preintegration_matches_reference(cuda_ok, mode, monkeypatch):
+    """Both propagation kernels -- the sequential one (16 lanes per pair) and the log-depth scan
+    (one warp per pair, composed affine maps; the default from 64 intervals per pair) -- against
+    the reference's goldens."""
     from paper_2512_02293_b200.imu import preintegrate_batch
+    monkeypatch.setenv("VBA_PREINT", mode)
     noise, cases = _cases()
     out = preintegrate_batch([c["ts"] for c in cases], [c["gyro"] for c in cases],
                              [c["accel"] for c in cases], np.stack([c["bias"] for c in cases]), noise)
