@@ -19,7 +19,7 @@ namespace vba {
 // ---------------------------------------------------------------------------
 // assembly: one CTA per lower block (a >= b) of the block matrix
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_assemble(const int32_t* __restrict__ bptr, const int32_t* __restrict__ bnff,
+__global__ void __launch_bounds__(128) k_assemble(const int32_t* __restrict__ bptr, const int32_t* __restrict__ bnff,
                                                   const Contrib* __restrict__ cs, int nbr,
                                                   const int32_t* __restrict__ roff, const int32_t* __restrict__ rdim,
                                                   const double* __restrict__ arena, double lam, double ridge,
@@ -70,7 +70,7 @@ void launch_assemble(const int32_t* bptr, const int32_t* bnff, const Contrib* cs
                      int64_t ld, int sym, cudaStream_t st, const int32_t* blist, int nblist) {
   const int64_t nblk = blist ? (int64_t)nblist : (int64_t)nbr * (nbr + 1) / 2;
   if (nblk <= 0) return;
-  k_assemble<<<(unsigned)nblk, 256, 0, st>>>(bptr, bnff, cs, nbr, roff, rdim, arena, lam, ridge, add_ridge, H, ld,
+  k_assemble<<<(unsigned)nblk, 128, 0, st>>>(bptr, bnff, cs, nbr, roff, rdim, arena, lam, ridge, add_ridge, H, ld,
                                              sym, blist);
   launch_count();
 }
