@@ -1660,12 +1660,13 @@ __global__ void k_tc_diag(const double* __restrict__ H, int64_t ld, int n, int n
 }
 
 // W_ij = fp32(D_i H_ij D_j) from the lower triangle (identity padding); one CTA per lower tile
+constexpr int kCvS = CT / 2 + 1;   // staging row stride (one 64-column half of a tile)
 __global__ void __launch_bounds__(256) k_tc_convert(const double* __restrict__ H, int64_t ld, int n, int nt,
                                                     const double* __restrict__ D, float* __restrict__ W) {
-  // one 128x128 tile per CTA: H read column-major (a warp reads 32 consecutive rows of a
-  // column), 32 loads in flight per thread, transposed through a padded shared tile and
-  // written row-major a full row per warp instruction
-  extern __shared__ float ttile[];   // [CT][CT + 1]
+  // one 128x128 tile per CTA, in two 64-column halves: H read column-major (a warp reads
+  // contiguous rows of a column), transposed through a padded 128 x 64 shared buffer (33 KB:
+  // 6 CTAs per SM) and written row-major, 256 B of a row per warp instruction
+  extern __shared__ float ttile[];   // [CT][kCvS]
   const int64_t id = blockIdx.x;
   int i = (int)((sqrt(8.0 * (double)id + 1.0) - 1.0) * 0.5);
   while ((int64_t)(i + 1) * (i + 2) / 2 <= id) ++i;
@@ -1673,54 +1674,52 @@ __global__ void __launch_bounds__(256) k_tc_convert(const double* __restrict__ H
   const int j = (int)(id - (int64_t)i * (i + 1) / 2);
   float* Wt = W + id * TILE_F;
   const int tid = threadIdx.x;
-  if (i != j && CT * (i + 1) <= n) {
-    // interior off-diagonal tile (all of it in the stored lower triangle): 16-B loads of row
-    // pairs, a warp reads 512 contiguous bytes of a column; 16 loads in flight per thread
-    const double dr0 = D[CT * i + 2 * (tid & 63)], dr1 = D[CT * i + 2 * (tid & 63) + 1];
+  // interior off-diagonal tile (all of it in the stored lower triangle): 16-B loads of row pairs
+  const bool fast = i != j && CT * (i + 1) <= n;
+  const double dr0 = D[CT * i + 2 * (tid & 63)], dr1 = D[CT * i + 2 * (tid & 63) + 1];
 #pragma unroll 1
-    for (int half = 0; half < 2; ++half) {
+  for (int half = 0; half < 2; ++half) {
+    if (fast) {
       double2 v[16];
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
-        const int idx = tid + 256 * (q + 16 * half), c = idx >> 6, rp = idx & 63;
-        v[q] = __ldcs(reinterpret_cast<const double2*>(H + (int64_t)(CT * j + c) * ld + CT * i + 2 * rp));
+        const int idx = tid + 256 * q, c = idx >> 6, rp = idx & 63;
+        v[q] = __ldcs(reinterpret_cast<const double2*>(H + (int64_t)(CT * j + 64 * half + c) * ld + CT * i + 2 * rp));
       }
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
-        const int idx = tid + 256 * (q + 16 * half), c = idx >> 6, rp = idx & 63;
-        const double dc = D[CT * j + c];
-        ttile[(2 * rp) * (CT + 1) + c] = (float)(dr0 * v[q].x * dc);
-        ttile[(2 * rp + 1) * (CT + 1) + c] = (float)(dr1 * v[q].y * dc);
+        const int idx = tid + 256 * q, c = idx >> 6, rp = idx & 63;
+        const double dc = D[CT * j + 64 * half + c];
+        ttile[(2 * rp) * kCvS + c] = (float)(dr0 * v[q].x * dc);
+        ttile[(2 * rp + 1) * kCvS + c] = (float)(dr1 * v[q].y * dc);
+      }
+    } else {
+      float v[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const int idx = tid + 256 * q, c = idx >> 7, r = idx & 127;
+        const int R = CT * i + r, C = CT * j + 64 * half + c;
+        if (R < n && C < n) {
+          const int64_t a = (R >= C) ? (int64_t)C * ld + R : (int64_t)R * ld + C;   // lower triangle
+          v[q] = (float)(D[R] * __ldcs(H + a) * D[C]);
+        } else {
+          v[q] = (R == C) ? 1.0f : 0.0f;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const int idx = tid + 256 * q, c = idx >> 7, r = idx & 127;
+        ttile[r * kCvS + c] = v[q];
       }
     }
-  } else {
-#pragma unroll 1
-  for (int half = 0; half < 2; ++half) {
-    float v[32];
-#pragma unroll
-    for (int q = 0; q < 32; ++q) {
-      const int idx = tid + 256 * (q + 32 * half), c = idx >> 7, r = idx & 127;
-      const int R = CT * i + r, C = CT * j + c;
-      if (R < n && C < n) {
-        const int64_t a = (R >= C) ? (int64_t)C * ld + R : (int64_t)R * ld + C;   // lower triangle
-        v[q] = (float)(D[R] * __ldcs(H + a) * D[C]);
-      } else {
-        v[q] = (R == C) ? 1.0f : 0.0f;
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 32; ++q) {
-      const int idx = tid + 256 * (q + 32 * half), c = idx >> 7, r = idx & 127;
-      ttile[r * (CT + 1) + c] = v[q];
-    }
-  }
-  }
-  __syncthreads();
+    __syncthreads();
 #pragma unroll 4
-  for (int q = 0; q < 16; ++q) {   // 16-B stores, a warp writes one 512-B row
-    const int idx = tid + 256 * q, r = idx >> 5, c = 4 * (idx & 31);
-    const float* t = ttile + r * (CT + 1) + c;
-    *reinterpret_cast<float4*>(Wt + r * CT + c) = make_float4(t[0], t[1], t[2], t[3]);
+    for (int q = 0; q < 8; ++q) {   // 16-B stores, a warp writes two 256-B half rows
+      const int idx = tid + 256 * q, r = idx >> 4, c = 4 * (idx & 15);
+      const float* t = ttile + r * kCvS + c;
+      *reinterpret_cast<float4*>(Wt + r * CT + 64 * half + c) = make_float4(t[0], t[1], t[2], t[3]);
+    }
+    __syncthreads();
   }
 }
 
@@ -2311,7 +2310,7 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
     cudaFuncSetAttribute(k_tc_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRI_SMEM);
     cudaFuncSetAttribute(k_tc_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRI_SMEM);
     cudaFuncSetAttribute(k_tc_convert, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)((size_t)CT * (CT + 1) * sizeof(float)));
+                         (int)((size_t)CT * kCvS * sizeof(float)));
     int dev = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -2319,7 +2318,7 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
     grid = sms * (per > 0 ? per : 1);
   }
   k_tc_diag<<<(npad + 255) / 256, 256, 0, st>>>(H, ld, n, npad, D);
-  k_tc_convert<<<(unsigned)ntl, 256, (size_t)CT * (CT + 1) * sizeof(float), st>>>(H, ld, n, nt, D, W);
+  k_tc_convert<<<(unsigned)ntl, 256, (size_t)CT * kCvS * sizeof(float), st>>>(H, ld, n, nt, D, W);
   cudaMemsetAsync(flags, 0, sizeof(int) * ((size_t)2 * nt * nt + 1), st);
   TcArgs a;
   a.W = W;
