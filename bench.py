@@ -219,9 +219,16 @@ def main():
 
     from paper_2512_02293_b200.distributed import make_sharded_problem, partition_sources
 
+    # one rank per GPU over NCCL; more ranks than GPUs (a functional check of the N > 1 path on
+    # a smaller box) share GPUs round-robin over gloo, as tools/dist_check.py
+    ngpu = max(torch.cuda.device_count(), 1)
+    local = local % ngpu
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if world <= ngpu:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     g = make_workload(a.config)
     P = pack_graph(g)
     N = int(P["doff"][1] - P["doff"][0])
