@@ -69,92 +69,105 @@ __device__ void imu_whitened_J(const double* __restrict__ rec, const double* __r
   for (int i = tid; i < 117; i += blockDim.x) L[i] = Lg[i];
   for (int i = tid; i < 15 * (kCols + 1); i += blockDim.x) (&J[0][0])[i] = 0.0;
   __syncthreads();
-  if (tid == 0) {
+  // the residual and raw Jacobian blocks by two threads in different warps (they run in
+  // parallel): warp 0 the rotation rows (the long serial chain: Exp, Log, Jr^-1 x 2, Jr),
+  // warp 1 the position / velocity / bias rows
+  if (tid == 0 || tid == 32) {
     const double dt = rec[kDT];
-    double Ri[9], Rj[9], Rwg[9];
+    double Ri[9];
     qmat(si, Ri);
-    qmat(sj, Rj);
-    qmat(grav, Rwg);
-    const double G = grav[4];
-    const double g[3] = {Rwg[2] * G, Rwg[5] * G, Rwg[8] * G};      // R_wg (0,0,G)  residuals.py:125-130
     double db[6];
     for (int k = 0; k < 6; ++k) db[k] = si[10 + k] - rec[kBH + k];   // s_i.bias - b_hat (:291)
-    const double* Jr = rec + kJR;
-    const double* Jp = rec + kJP;
-    const double* Jv = rec + kJV;
-    double ct[3];
-    mat3_vec(Jr, db, ct);                                           // corr_rot_tangent (:294)
-    double dR[9], Ect[9], C[9], T2[9], Mrot[9];
-    qmat(rec + kDR, dR);
-    so3_exp(ct, Ect);
-    mat3_mul(dR, Ect, C);                                           // :295
-    // Mrot = C^T R_i^T R_j
-    for (int a = 0; a < 3; ++a)
-      for (int b = 0; b < 3; ++b)
-        T2[a * 3 + b] = C[0 * 3 + a] * Ri[b * 3 + 0] + C[1 * 3 + a] * Ri[b * 3 + 1] + C[2 * 3 + a] * Ri[b * 3 + 2];
-    mat3_mul(T2, Rj, Mrot);
-    double qrot[4], rrot[3];
-    q_from_mat(Mrot, qrot);
-    qlog(qrot, rrot);                                               // r_rot (:296)
-    double spos[3], svel[3], rpos[3], rvel[3];
-    for (int k = 0; k < 3; ++k) {
-      spos[k] = sj[4 + k] - si[4 + k] - si[7 + k] * dt - 0.5 * dt * dt * g[k];   // :297
-      svel[k] = sj[7 + k] - si[7 + k] - dt * g[k];                              // :299
-    }
-    double Rs[3], Rv[3];
-    mat3T_vec(Ri, spos, Rs);
-    mat3T_vec(Ri, svel, Rv);
-    for (int k = 0; k < 3; ++k) {
-      double jp = 0.0, jv = 0.0;
-      for (int m = 0; m < 6; ++m) { jp += Jp[k * 6 + m] * db[m]; jv += Jv[k * 6 + m] * db[m]; }
-      rpos[k] = Rs[k] - (rec[kDP + k] + jp);                         // :298
-      rvel[k] = Rv[k] - (rec[kDV + k] + jv);                         // :300
-    }
-    for (int k = 0; k < 3; ++k) {
-      J[k][33] = rrot[k];
-      J[3 + k][33] = rpos[k];
-      J[6 + k][33] = rvel[k];
-    }
-    for (int k = 0; k < 6; ++k) J[9 + k][33] = sj[10 + k] - si[10 + k];   // r_bias (:301)
-    if (!energy_only) {
-      double Jri[9], Jli[9], mr[3] = {-rrot[0], -rrot[1], -rrot[2]}, Jrc[9];
-      so3_jr_inv(rrot, Jri);                                        // :303
-      so3_jr_inv(mr, Jli);                                          // :304
-      so3_jr(ct, Jrc);
-      double RjtRi[9], A1[9], A2[9], A3[9];
-      mat3_Tmul(Rj, Ri, RjtRi);
-      mat3_mul(Jri, RjtRi, A1);                                     // J_i[rot,θ] = -Jr^-1 R_j^T R_i
-      mat3_mul(Jli, Jrc, A2);
-      mat3_mul(A2, Jr, A3);                                         // J_i[rot,bg] = -Jl^-1 Jr(ct) J_rot
-      double Hs[9], Hv[9], RwgH[9], hg[9], gI[3] = {0.0, 0.0, G}, RitRwgH[9];
-      hat3(Rs, Hs);
-      hat3(Rv, Hv);
-      hat3(gI, hg);
-      mat3_mul(Rwg, hg, RwgH);
-      mat3_Tmul(Ri, RwgH, RitRwgH);                                 // R_i^T R_wg [g_I]x
+    if (tid == 0) {
+      double Rj[9];
+      qmat(sj, Rj);
+      const double* Jr = rec + kJR;
+      double ct[3];
+      mat3_vec(Jr, db, ct);                                         // corr_rot_tangent (:294)
+      double dR[9], Ect[9], C[9], T2[9], Mrot[9];
+      qmat(rec + kDR, dR);
+      so3_exp(ct, Ect);
+      mat3_mul(dR, Ect, C);                                         // :295
+      // Mrot = C^T R_i^T R_j
       for (int a = 0; a < 3; ++a)
-        for (int b = 0; b < 3; ++b) {
-          J[a][b] = -A1[a * 3 + b];
-          J[a][15 + b] = Jri[a * 3 + b];                            // J_j[rot,θ]
-          J[a][9 + b] = -A3[a * 3 + b];
-          J[3 + a][b] = Hs[a * 3 + b];                              // J_i[pos,θ]
-          J[3 + a][3 + b] = -Ri[b * 3 + a];                         // -R_i^T
-          J[3 + a][15 + 3 + b] = Ri[b * 3 + a];                     // J_j[pos,p] = R_i^T
-          J[3 + a][6 + b] = -dt * Ri[b * 3 + a];
-          J[3 + a][30 + b] = 0.5 * dt * dt * RitRwgH[a * 3 + b];    // J_g[pos]
-          J[6 + a][b] = Hv[a * 3 + b];                              // J_i[vel,θ]
-          J[6 + a][6 + b] = -Ri[b * 3 + a];
-          J[6 + a][15 + 6 + b] = Ri[b * 3 + a];
-          J[6 + a][30 + b] = dt * RitRwgH[a * 3 + b];               // J_g[vel]
+        for (int b = 0; b < 3; ++b)
+          T2[a * 3 + b] = C[0 * 3 + a] * Ri[b * 3 + 0] + C[1 * 3 + a] * Ri[b * 3 + 1] + C[2 * 3 + a] * Ri[b * 3 + 2];
+      mat3_mul(T2, Rj, Mrot);
+      double qrot[4], rrot[3];
+      q_from_mat(Mrot, qrot);
+      qlog(qrot, rrot);                                             // r_rot (:296)
+      for (int k = 0; k < 3; ++k) J[k][33] = rrot[k];
+      if (!energy_only) {
+        double Jri[9], Jli[9], mr[3] = {-rrot[0], -rrot[1], -rrot[2]}, Jrc[9];
+        so3_jr_inv(rrot, Jri);                                      // :303
+        so3_jr_inv(mr, Jli);                                        // :304
+        so3_jr(ct, Jrc);
+        double RjtRi[9], A1[9], A2[9], A3[9];
+        mat3_Tmul(Rj, Ri, RjtRi);
+        mat3_mul(Jri, RjtRi, A1);                                   // J_i[rot,θ] = -Jr^-1 R_j^T R_i
+        mat3_mul(Jli, Jrc, A2);
+        mat3_mul(A2, Jr, A3);                                       // J_i[rot,bg] = -Jl^-1 Jr(ct) J_rot
+        for (int a = 0; a < 3; ++a)
+          for (int b = 0; b < 3; ++b) {
+            J[a][b] = -A1[a * 3 + b];
+            J[a][15 + b] = Jri[a * 3 + b];                          // J_j[rot,θ]
+            J[a][9 + b] = -A3[a * 3 + b];
+          }
+      }
+    } else {
+      double Rwg[9];
+      qmat(grav, Rwg);
+      const double G = grav[4];
+      const double g[3] = {Rwg[2] * G, Rwg[5] * G, Rwg[8] * G};    // R_wg (0,0,G)  residuals.py:125-130
+      const double* Jp = rec + kJP;
+      const double* Jv = rec + kJV;
+      double spos[3], svel[3], rpos[3], rvel[3];
+      for (int k = 0; k < 3; ++k) {
+        spos[k] = sj[4 + k] - si[4 + k] - si[7 + k] * dt - 0.5 * dt * dt * g[k];   // :297
+        svel[k] = sj[7 + k] - si[7 + k] - dt * g[k];                              // :299
+      }
+      double Rs[3], Rv[3];
+      mat3T_vec(Ri, spos, Rs);
+      mat3T_vec(Ri, svel, Rv);
+      for (int k = 0; k < 3; ++k) {
+        double jp = 0.0, jv = 0.0;
+        for (int m = 0; m < 6; ++m) { jp += Jp[k * 6 + m] * db[m]; jv += Jv[k * 6 + m] * db[m]; }
+        rpos[k] = Rs[k] - (rec[kDP + k] + jp);                       // :298
+        rvel[k] = Rv[k] - (rec[kDV + k] + jv);                       // :300
+      }
+      for (int k = 0; k < 3; ++k) {
+        J[3 + k][33] = rpos[k];
+        J[6 + k][33] = rvel[k];
+      }
+      for (int k = 0; k < 6; ++k) J[9 + k][33] = sj[10 + k] - si[10 + k];   // r_bias (:301)
+      if (!energy_only) {
+        double Hs[9], Hv[9], RwgH[9], hg[9], gI[3] = {0.0, 0.0, G}, RitRwgH[9];
+        hat3(Rs, Hs);
+        hat3(Rv, Hv);
+        hat3(gI, hg);
+        mat3_mul(Rwg, hg, RwgH);
+        mat3_Tmul(Ri, RwgH, RitRwgH);                               // R_i^T R_wg [g_I]x
+        for (int a = 0; a < 3; ++a)
+          for (int b = 0; b < 3; ++b) {
+            J[3 + a][b] = Hs[a * 3 + b];                            // J_i[pos,θ]
+            J[3 + a][3 + b] = -Ri[b * 3 + a];                       // -R_i^T
+            J[3 + a][15 + 3 + b] = Ri[b * 3 + a];                   // J_j[pos,p] = R_i^T
+            J[3 + a][6 + b] = -dt * Ri[b * 3 + a];
+            J[3 + a][30 + b] = 0.5 * dt * dt * RitRwgH[a * 3 + b];  // J_g[pos]
+            J[6 + a][b] = Hv[a * 3 + b];                            // J_i[vel,θ]
+            J[6 + a][6 + b] = -Ri[b * 3 + a];
+            J[6 + a][15 + 6 + b] = Ri[b * 3 + a];
+            J[6 + a][30 + b] = dt * RitRwgH[a * 3 + b];             // J_g[vel]
+          }
+        for (int a = 0; a < 3; ++a)
+          for (int m = 0; m < 6; ++m) {
+            J[3 + a][9 + m] = -Jp[a * 6 + m];
+            J[6 + a][9 + m] = -Jv[a * 6 + m];
+          }
+        for (int k = 0; k < 6; ++k) {
+          J[9 + k][9 + k] = -1.0;
+          J[9 + k][15 + 9 + k] = 1.0;
         }
-      for (int a = 0; a < 3; ++a)
-        for (int m = 0; m < 6; ++m) {
-          J[3 + a][9 + m] = -Jp[a * 6 + m];
-          J[6 + a][9 + m] = -Jv[a * 6 + m];
-        }
-      for (int k = 0; k < 6; ++k) {
-        J[9 + k][9 + k] = -1.0;
-        J[9 + k][15 + 9 + k] = 1.0;
       }
     }
   }
