@@ -41,7 +41,7 @@ constexpr int CHOL_THREADS = 256;
 constexpr int SB = 36;           // 32x32 block stride in POTRF (doubles, = 4 mod 16)
 constexpr size_t CHOL_SMEM = (size_t)2 * 2 * KC * SP * sizeof(double);   // 2 stages x (A, B)
 
-enum TaskType { T_POTRF = 0, T_TRSM = 1, T_GEMM = 2, T_BUPD = 3, T_BSOL = 4, T_DIAG = 5, T_CHAIN = 6, T_TILE = 7, T_CONV = 8 };
+enum TaskType { T_POTRF = 0, T_TRSM = 1, T_GEMM = 2, T_BUPD = 3, T_BSOL = 4, T_DIAG = 5, T_CHAIN = 6, T_TILE = 7, T_CONV = 8, T_PREP = 9 };
 // TILE task modes (CholTask::expect): the chain's SYRK target (W written, upd = columns),
 // the chain's TRSM operand (W and its hi/lo images written, upd = columns + 1), or an
 // off-chain tile whose TRSM follows in the same task (done = 1)
@@ -630,6 +630,12 @@ int chol_plan_tasks_tc(int nt, void* outv, int cap) {
     for (int i = s + 3; i < nt; ++i) push(T_TILE, i, s + 1, s + 1, TILE_TRSM);
   }
   for (int k = 0; k < nt; ++k) push(T_CONV, k, k, k, 0);   // fp32 Linv_kk, L_{k+1,k} for the solves
+  // the triangular solves' folded matrices (kinds 0-4 of tc_task_prep), each as soon as its
+  // tiles are final: overlapped with the end of the chain instead of a kernel after it
+  for (int k = 0; k < nt; ++k)
+    for (int kind = 0; kind < 5; ++kind)
+      if (!((kind == 1 && k < 1) || (kind == 2 && k < 2) || (kind == 3 && k + 1 >= nt) || (kind == 4 && k + 2 >= nt)))
+        push(T_PREP, k, kind, k, 0);
   return n;
 }
 
@@ -782,7 +788,10 @@ struct TcArgs {
   int ntasks;
   int* status;
   unsigned long long* trace;   // optional [ntasks][4]: t_grab, t_ready, t_done, smid
+  float* Fm;                   // folded solve matrices (PREP tasks)
+  int* convd;                  // [nt]: CONV(k) has written its fp32 tiles
 };
+__device__ void tc_task_prep(const TcArgs& a, int k, int kind, float* A, float* B);
 
 __device__ __forceinline__ int64_t tlin(int i, int j) { return (int64_t)i * (i + 1) / 2 + j; }
 // fp16 offset of element (row r, col c) inside one image part (see layout above):
@@ -1615,7 +1624,22 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) k_chol_tc(TcArgs a) {
       case T_CONV:
         if (a.trace && tid == 0) a.trace[4 * t + 1] = gtimer();
         tc_task_conv(a, T.k);
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) st_release(&a.convd[T.k], 1);
         break;
+      case T_PREP: {   // inputs: the fp32 tiles CONV wrote (Linv_kk, L_{k+1,k}, L_{k,k-1}) or a TILE's TRSM
+        const int k = T.i, kind = T.j;
+        wait_geq(&a.convd[k], 1);
+        if (kind == 1) wait_geq(&a.convd[k - 1], 1);
+        if (kind == 2) wait_geq(&a.done[k * nt + k - 2], 1);
+        if (kind == 4) wait_geq(&a.done[(k + 2) * nt + k], 1);
+        __syncthreads();
+        if (a.trace && tid == 0) a.trace[4 * t + 1] = gtimer();
+        float* A = reinterpret_cast<float*>(sm);
+        tc_task_prep(a, k, kind, A, A + TILE_F);
+        break;
+      }
       case T_TILE:
         if (a.trace && tid == 0) a.trace[4 * t + 1] = gtimer();
         tc_task_tile(a, R, &accf, nacc, tmem, T.i, T.j, T.k, T.expect);
@@ -1870,36 +1894,36 @@ __device__ __forceinline__ void tri_prefetch(float* d0, const float* s0, float* 
 //   kind 2: (Linv_kk L_{k,k-2})^T
 //   kind 3: L_{k+1,k} Linv_kk           (backward chain, read as column sums)
 //   kind 4: L_{k+2,k} Linv_kk
-__global__ void __launch_bounds__(256, 1) k_tc_prep(const float* __restrict__ W, int nt, float* __restrict__ F) {
-  extern __shared__ __align__(16) unsigned char tri_raw[];
-  float* A = reinterpret_cast<float*>(tri_raw);
-  float* B = A + TILE_F;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(B + 2 * TILE_F);
-  const int k = blockIdx.x, kind = blockIdx.y;
-  float* out = F + ((int64_t)kind * nt + k) * TILE_F;
-  const float* Lin = W + tlin(k, k) * TILE_F;
-  const float* other = nullptr;
-  if (kind == 1 && k >= 1) other = W + tlin(k, k - 1) * TILE_F;
-  if (kind == 2 && k >= 2) other = W + tlin(k, k - 2) * TILE_F;
-  if (kind == 3 && k + 1 < nt) other = W + tlin(k + 1, k) * TILE_F;
-  if (kind == 4 && k + 2 < nt) other = W + tlin(k + 2, k) * TILE_F;
-  if (kind != 0 && !other) return;
+__device__ void tc_task_prep(const TcArgs& a, int k, int kind, float* A, float* B) {
+  const int nt = a.nt;
+  float* out = a.Fm + ((int64_t)kind * nt + k) * TILE_F;
+  const float* Lin = a.W + tlin(k, k) * TILE_F;
+  const float* other = Lin;
+  if (kind == 1) other = a.W + tlin(k, k - 1) * TILE_F;
+  if (kind == 2) other = a.W + tlin(k, k - 2) * TILE_F;
+  if (kind == 3) other = a.W + tlin(k + 1, k) * TILE_F;
+  if (kind == 4) other = a.W + tlin(k + 2, k) * TILE_F;
   // kinds 1, 2: C = Lin X (A = Lin, B = X);  kinds 3, 4: C = X Lin (A = X, B = Lin)
-  tri_prefetch(kind >= 3 ? B : A, Lin, kind >= 3 ? A : B, other, nullptr, nullptr, bar);
-  __syncthreads();   // barrier initialised before anyone waits on it
-  tc_mbar_wait(bar, 0);
+  const float4* sa = reinterpret_cast<const float4*>(kind >= 3 ? other : Lin);
+  const float4* sb = reinterpret_cast<const float4*>(kind >= 3 ? Lin : other);
+  for (int e = threadIdx.x; e < TILE_F / 4; e += blockDim.x) {
+    reinterpret_cast<float4*>(A)[e] = __ldcg(sa + e);
+    if (kind != 0) reinterpret_cast<float4*>(B)[e] = __ldcg(sb + e);
+  }
+  __syncthreads();
   if (kind == 0) {
     smem_transpose128(A);
   } else {
     smem_gemm128(A, A, B, kind <= 2, kind >= 3, kind <= 2);   // in place; transposed output for kinds 1, 2
   }
-  for (int e = threadIdx.x; e < TILE_F / 4; e += 256)
+  for (int e = threadIdx.x; e < TILE_F / 4; e += blockDim.x)
     __stcg(reinterpret_cast<float4*>(out) + e, reinterpret_cast<const float4*>(A)[e]);
+  __syncthreads();   // shared memory is reused by the next task
 }
 
 // forward: L y = v, v = D r.  With M1 = Linv_kk L_{k,k-1}, M2 = Linv_kk L_{k,k-2}:
 //   y_k = Linv_kk (v_k - sum_{j<k-2} L_kj y_j) - M2 y_{k-2} - M1 y_{k-1}
-// LinvT, M1^T, M2^T come precomputed (k_tc_prep); the chain sees one 128x128
+// LinvT, M1^T, M2^T come precomputed (PREP tasks of the DAG, tc_task_prep); the chain sees one 128x128
 // shared-memory matvec per step.  Off-chain tiles are register-prefetched two deep.
 // one butterfly stage of a warp transpose-reduction: lanes with bit LB set keep the
 // upper ST values (adding their partner's), the others the lower ST
@@ -1916,7 +1940,7 @@ __device__ __forceinline__ void bfly_stage(float* pr, int ln) {
 
 // forward: L y = D r (row tile k; one CTA per row tile, all co-resident).
 //   acc_k = D r_k - sum_{j <= k-3} V[k][j],   V[k][j] = L_kj y_j
-//   y_k = Linv_kk acc_k - M2 y_{k-2} - M1 y_{k-1}     (M1, M2 folded by k_tc_prep)
+//   y_k = Linv_kk acc_k - M2 y_{k-2} - M1 y_{k-1}     (M1, M2 folded by tc_task_prep)
 // The off-chain products V[i][k] (i >= k+3) are computed by CTA k right after it
 // publishes y_k (a column sweep over tiles L_ik, prefetched before y_k is known) and
 // handed over as tagged words, so every row tile's off-chain sum is ready long
@@ -2028,7 +2052,7 @@ __global__ void __launch_bounds__(256, 1) k_tc_fwd(const float* __restrict__ W, 
 
 // backward: L^T z = y.  With T1 = L_{k+1,k} Linv_kk, T2 = L_{k+2,k} Linv_kk:
 //   z_k = Linv^T (y_k - sum_{i>k+2} L_ik^T z_i) - T2^T z_{k+2} - T1^T z_{k+1};
-// then x += D z (fp64) with max |dx|, max |x|.  T1, T2 precomputed (k_tc_prep).
+// then x += D z (fp64) with max |dx|, max |x|.  T1, T2 precomputed (tc_task_prep).
 __global__ void __launch_bounds__(256, 1) k_tc_bwd(const float* __restrict__ W, const float* __restrict__ F,
                                                    int nt, const unsigned long long* __restrict__ y,
                                                    unsigned long long* __restrict__ z,
@@ -2272,7 +2296,7 @@ size_t chol_tc_ws_bytes(int npad) {
          + sizeof(double) * ((size_t)npad * 4)                      // D, r, y, z
          + sizeof(unsigned long long) * (size_t)2 * nt * npad       // off-chain slots of the solves
          + sizeof(double) * (size_t)nb * nb * SYB                   // symv partials
-         + sizeof(int) * ((size_t)2 * nt * nt + 2 + 2 * (size_t)nt) + 256 * 12;
+         + sizeof(int) * ((size_t)2 * nt * nt + 2 + 3 * (size_t)nt) + 256 * 12;
 }
 
 // Solve H x = b (H: fp64 column-major, lower triangle read, npad = nt * 128,
@@ -2300,14 +2324,13 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
   unsigned long long* Vs = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * (size_t)nt * npad));
   unsigned long long* Us = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * (size_t)nt * npad));
   double* P = reinterpret_cast<double*>(take(sizeof(double) * (size_t)nb * nb * SYB));
-  int* flags = reinterpret_cast<int*>(take(sizeof(int) * ((size_t)2 * nt * nt + 1)));
+  int* flags = reinterpret_cast<int*>(take(sizeof(int) * ((size_t)2 * nt * nt + 1 + nt)));
   int* sfl = reinterpret_cast<int*>(take(sizeof(int) * 2 * (size_t)nt));
   int* stop = reinterpret_cast<int*>(take(sizeof(int)));
   static int grid = 0, sms = 0;
   if (grid == 0) {
     cudaFuncSetAttribute(k_chol_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM);
     cudaFuncSetAttribute(k_tc_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRI_SMEM);
-    cudaFuncSetAttribute(k_tc_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRI_SMEM);
     cudaFuncSetAttribute(k_tc_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRI_SMEM);
     cudaFuncSetAttribute(k_tc_convert, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)((size_t)CT * kCvS * sizeof(float)));
@@ -2319,7 +2342,7 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
   }
   k_tc_diag<<<(npad + 255) / 256, 256, 0, st>>>(H, ld, n, npad, D);
   k_tc_convert<<<(unsigned)ntl, 256, (size_t)CT * kCvS * sizeof(float), st>>>(H, ld, n, nt, D, W);
-  cudaMemsetAsync(flags, 0, sizeof(int) * ((size_t)2 * nt * nt + 1), st);
+  cudaMemsetAsync(flags, 0, sizeof(int) * ((size_t)2 * nt * nt + 1 + nt), st);
   TcArgs a;
   a.W = W;
   a.img = img;
@@ -2331,14 +2354,14 @@ int chol_tc_solve(const double* H, int64_t ld, int n, int npad, const double* b,
   a.ntasks = ntasks;
   a.status = status;
   a.trace = trace;
+  a.Fm = Fm;
+  a.convd = flags + (size_t)2 * nt * nt + 1;
   if (ev3) cudaEventRecord(ev3[0], st);
   launch_coresident(k_chol_tc, ntasks < grid ? ntasks : grid, CHOL_THREADS, TC_SMEM, st, a);
   launch_count();
   launch_count();
   launch_count();
   if (ev3) cudaEventRecord(ev3[1], st);
-  k_tc_prep<<<dim3(nt, 5), 256, TRI_SMEM, st>>>(W, nt, Fm);
-  launch_count();
   cudaMemsetAsync(x, 0, sizeof(double) * npad, st);
   cudaMemsetAsync(stop, 0, sizeof(int), st);
   cudaMemsetAsync(out2, 0, sizeof(double) * 5, st);
@@ -2414,8 +2437,8 @@ void chol_trace_print(const char* tag, const unsigned long long* d_trace, const 
   cudaMemcpy(tr.data(), d_trace, tr.size() * 8, cudaMemcpyDeviceToHost);
   cudaMemcpy(tk.data(), d_tasks, tk.size() * sizeof(CholTask), cudaMemcpyDeviceToHost);
   unsigned long long t0 = ~0ull, t1 = 0;
-  double busy[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, wait[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  int cnt[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  double busy[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, wait[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  int cnt[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int q = 0; q < ntasks; ++q) {
     if (tr[4 * q] == 0) continue;
     t0 = std::min(t0, tr[4 * q]);
@@ -2461,9 +2484,9 @@ void chol_trace_print(const char* tag, const unsigned long long* d_trace, const 
               ((double)tr[4 * dg[0].second + 1] - (double)t0) * 1e-3, gap, gmax, kmax,
               ((double)tr[4 * dg.back().second + 2] - (double)t0) * 1e-3);
   }
-  const char* nm[9] = {"POTRF", "TRSM", "GEMM", "BUPD", "BSOL", "DIAG", "CHAIN", "TILE", "CONV"};
+  const char* nm[10] = {"POTRF", "TRSM", "GEMM", "BUPD", "BSOL", "DIAG", "CHAIN", "TILE", "CONV", "PREP"};
   fprintf(stderr, "[%s trace] nt=%d tasks=%d span %.1f us\n", tag, nt, ntasks, (double)(t1 - t0) * 1e-3);
-  for (int ty = 0; ty < 9; ++ty)
+  for (int ty = 0; ty < 10; ++ty)
     if (cnt[ty])
       fprintf(stderr, "  %-5s n=%6d  avg busy %8.2f us  avg wait %8.2f us  total busy %.1f us\n", nm[ty], cnt[ty],
               busy[ty] / cnt[ty], wait[ty] / cnt[ty], busy[ty]);

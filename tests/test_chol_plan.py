@@ -12,7 +12,7 @@ import pytest
 
 from paper_2512_02293_b200 import _lib as L
 
-T_TRSM, T_CHAIN, T_TILE, T_CONV = 1, 6, 7, 8
+T_TRSM, T_CHAIN, T_TILE, T_CONV, T_PREP = 1, 6, 7, 8, 9
 SYRK_TARGET, TILE_TRSM, OPERAND = 0, 1, 2
 
 
@@ -35,7 +35,7 @@ def test_bad_arguments():
 def test_tc_cholesky_plan_invariants(nt):
     P = _plan(nt)
     assert P[0, 0] == T_CHAIN and int((P[:, 0] == T_CHAIN).sum()) == 1
-    assert set(P[:, 0].tolist()) <= {T_TRSM, T_CHAIN, T_TILE, T_CONV}
+    assert set(P[:, 0].tolist()) <= {T_TRSM, T_CHAIN, T_TILE, T_CONV, T_PREP}
 
     # producers: L_ij (i >= j+2) by a TRSM (j = 0) or a TILE in TRSM mode; the chain makes
     # L_{j+1,j} and Linv_jj at its step j
@@ -58,8 +58,14 @@ def test_tc_cholesky_plan_invariants(nt):
     assert set(operand) == {(j + 1, j) for j in range(nt - 1)}
     assert set(syrk) == {(j, j) for j in range(2, nt)}
     conv = [q for q, t in enumerate(P[:, 0].tolist()) if t == T_CONV]
+    prep = [q for q, t in enumerate(P[:, 0].tolist()) if t == T_PREP]
     assert sorted(P[conv, 1].tolist()) == list(range(nt))
-    assert conv == list(range(len(P) - nt, len(P)))        # the list ends with them
+    # the folded solve matrices: every (k, kind) whose neighbour tile exists, exactly once
+    want = {(k, kind) for k in range(nt) for kind in range(5)
+            if not ((kind == 1 and k < 1) or (kind == 2 and k < 2) or (kind == 3 and k + 1 >= nt)
+                    or (kind == 4 and k + 2 >= nt))}
+    assert sorted(map(tuple, P[prep][:, 1:3].tolist())) == sorted(want)
+    assert conv + prep == list(range(len(P) - nt - len(prep), len(P)))   # the list ends with them
 
     # every input of a task is made earlier in claim order or by the chain; need[q] = the
     # latest chain step task q waits for
@@ -83,6 +89,13 @@ def test_tc_cholesky_plan_invariants(nt):
             need[q] = w
         elif t == T_CONV:
             need[q] = k                                  # Linv_kk, L_{k+1,k}
+        elif t == T_PREP:                                # CONV(i) (+ CONV(i-1) or a TRSM tile)
+            kk, kind = i, j
+            need[q] = kk
+            if kind == 2:
+                assert prod[(kk, kk - 2)] < q
+            if kind == 4:
+                assert prod[(kk + 2, kk)] < q
     # chain step s waits for its operand (s+1, s) and SYRK target (s+1, s+1); no task claimed
     # before them may wait for a chain step beyond s (else every CTA could end up spinning)
     for s in range(nt - 1):
