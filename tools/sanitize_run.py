@@ -3,7 +3,7 @@
 Runs every kernel family of libvba at sizes the sanitizers finish in minutes:
 K1/K2/K3/K4/K6/K7 (linearise, energy, IMU, Schur Gram + fill transform, back-substitution,
 retraction) through a 2-iteration solve of BASELINE config 1; the tensor-core reduced
-solve (k_tc_diag/convert, k_chol_tc, k_tc_prep, k_tc_fwd/bwd, k_tc_symv/resid, k_tc_check)
+solve (k_tc_diag/convert, k_chol_tc (PREP tasks), k_tc_fwd/bwd, k_tc_symv/resid, k_tc_check)
 forced on that 2-tile system and on a standalone 8-tile SPD system; the fp64 tile-DAG
 Cholesky; the dense (use_schur=False) path on a small golden window; IMU preintegration.
 """
